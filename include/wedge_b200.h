@@ -1,0 +1,215 @@
+/*
+ * wedge_b200.h — C ABI of the B200-native Wedge-Frontier pull engine.
+ *
+ * Plain pointers and sizes only (no torch / C++ types).  Every pointer named
+ * `d_*` or documented as "device" is a CUDA device pointer; `stream` is a
+ * cudaStream_t passed as void*.  Every function returns WG_OK (0) or a
+ * negative WG_E* code; the message of the last error on the calling thread is
+ * available from wg_last_error().  Nothing is allocated behind the caller's
+ * back: scratch space comes from caller-provided workspaces whose sizes are
+ * queried first.
+ *
+ * Reference interface each entry point replaces (wedgegraph 0.1.0,
+ * /root/reference/pkg/src/wedgegraph):
+ *
+ *   wg_build_layout      build_pull_topology  graph.py:220-263
+ *                        build_edge_index     graph.py:283-301
+ *                        compute_out_degrees  graph.py:277-280
+ *   wg_transform         Backend.transform    kernels.py:116-125 -> _kernels.pyx:55-62
+ *                        (transform_frontier  frontier.py:174-209)
+ *   wg_pull_full         Backend.pull_full    kernels.py:81-95   -> _kernels.pyx:98-110
+ *   wg_pull_wedge        Backend.pull_wedge   kernels.py:97-114  -> _kernels.pyx:176-189
+ *   wg_covered_groups    covered_positions    _kernels_py.py:24-32 (wedge_covered_vectors,
+ *                                                                  frontier.py:156-160)
+ *   wg_run_*             run_until_convergence engine.py:330-388 (device-resident loop)
+ *   wg_pagerank          (no reference symbol; BASELINE.json config 5)
+ *   wg_rmat_edges        _generate_rmat       graph_io.py:188-202 (bit-identical PCG64 stream)
+ *   wg_weights_hash      synthesize_weights   graph_io.py:205-221
+ *   wg_canonical_edges   symmetrize(dedup)    graph_io.py:87-112 (+ directed dedup)
+ */
+#ifndef WEDGE_B200_H
+#define WEDGE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define WG_ABI_VERSION 1
+
+#define WG_OK 0
+#define WG_EINVAL -1     /* bad argument (null pointer, size, unsupported width) */
+#define WG_ECUDA -2      /* CUDA runtime error (launch, copy, device fault) */
+#define WG_ENOSPACE -3   /* workspace too small / capacity exceeded */
+#define WG_EOVERFLOW -4  /* a uint32 value would have exceeded 0xFFFFFFFE (run is invalid) */
+
+/* Vertex value encodings. */
+#define WG_VAL_U32 0 /* uint32 values, 0xFFFFFFFF = unreached (fast path) */
+#define WG_VAL_I64 1 /* int64 values with the reference sentinel (engine.py:41-43) */
+
+#define WG_NO_LANE 0xFFFFFFFFu /* padding lane in vsrc */
+
+/* Device-resident pull layout.  All pointers device. */
+typedef struct wg_graph {
+    uint32_t n;          /* vertices */
+    uint32_t width;      /* lanes per vector: 1, 2, 4, 8 (graph.py:215-217) */
+    uint64_t nvec;       /* vectors */
+    uint64_t edges;      /* |E| as stored (PullTopology.edge_count) */
+    uint64_t entries;    /* edge-index entries (EdgeIndex.positions length) */
+    const uint32_t *vsrc;    /* [nvec*width] lane sources, WG_NO_LANE padded */
+    const uint32_t *vdst;    /* [nvec] destination of each vector */
+    const uint32_t *vw;      /* [nvec*width] lane weights or NULL */
+    const uint64_t *idx_off; /* [n+1] edge-index offsets */
+    const uint32_t *idx_pos; /* [entries] ascending de-duplicated vector positions */
+    const uint32_t *outdeg;  /* [n] out-degrees */
+} wg_graph;
+
+/* MinPlusKernel (engine.py:50-63). */
+typedef struct wg_minplus {
+    int32_t filter_unvisited;
+    int32_t use_weight;
+    int64_t apply_increment;
+    int64_t sentinel; /* WG_VAL_I64 only: the reference's UNREACHED */
+} wg_minplus;
+
+const char *wg_last_error(void);
+int wg_abi_version(void);
+int wg_device_sm_count(int *out);
+
+/* ---------------- layout construction (graph.py:220-301) ---------------- */
+/* Upper bound on vectors for m edges over n vertices at `width`. */
+uint64_t wg_vector_capacity(uint64_t m, uint32_t n, uint32_t width);
+/* Scratch bytes for wg_build_layout. */
+size_t wg_layout_scratch_bytes(uint64_t m, uint32_t n);
+/* Edges (d_src, d_dst, optional d_w; device, length m) -> layout.  Outputs are
+ * caller-allocated: d_vsrc/d_vw [cap*width], d_vdst [cap], d_idx_off [n+1],
+ * d_idx_pos [m], d_outdeg [n].  h_counts (host) receives {nvec, entries}.
+ * Synchronises `stream` to read the counts back. */
+int wg_build_layout(uint32_t n, uint64_t m, const uint32_t *d_src, const uint32_t *d_dst,
+                    const uint32_t *d_w, uint32_t width, uint64_t vec_capacity, uint32_t *d_vsrc,
+                    uint32_t *d_vdst, uint32_t *d_vw, uint64_t *d_idx_off, uint32_t *d_idx_pos,
+                    uint32_t *d_outdeg, void *d_scratch, size_t scratch_bytes,
+                    uint64_t *h_counts, void *stream);
+
+/* ---------------- per-call kernels (backend protocol, kernels.py:55-125) --- */
+/* Workspace for wg_transform / wg_pull_wedge / wg_covered_groups. */
+size_t wg_kernel_workspace_bytes(const wg_graph *g, int shift);
+/* Transform: frontier bitmap (uint32 LE words over n) -> wedge group bitmap
+ * (OR-ed into d_wedge_words, words over ceil(nvec>>shift)).  h_visited
+ * (host) receives the index entries visited.  Synchronises. */
+int wg_transform(const wg_graph *g, const uint32_t *d_frontier_words, int shift,
+                 uint32_t *d_wedge_words, void *d_ws, size_t ws_bytes, uint64_t *h_visited,
+                 void *stream);
+/* Dense pull over all vectors.  d_prev/d_nxt hold values of `val_type`;
+ * d_nxt must equal d_prev on entry (engine.py:264).  Bits of updated
+ * destinations are OR-ed into d_out_words.  h_touched (host) receives
+ * vectors touched.  Synchronises. */
+int wg_pull_full(const wg_graph *g, int val_type, const void *d_prev, void *d_nxt,
+                 uint32_t *d_out_words, const wg_minplus *k, void *d_ws, size_t ws_bytes,
+                 uint64_t *h_touched, void *stream);
+/* Pull restricted to vectors covered by set bits of d_wedge_words at `shift`. */
+int wg_pull_wedge(const wg_graph *g, const uint32_t *d_wedge_words, int shift, int val_type,
+                  const void *d_prev, void *d_nxt, uint32_t *d_out_words, const wg_minplus *k,
+                  void *d_ws, size_t ws_bytes, uint64_t *h_touched, void *stream);
+/* Ascending list of set group ids of d_wedge_words (group_count bits) into
+ * d_groups; h_count (host) receives their number. */
+int wg_covered_groups(const uint32_t *d_wedge_words, uint64_t group_count, uint32_t *d_groups,
+                      void *d_ws, size_t ws_bytes, uint64_t *h_count, void *stream);
+
+/* ---------------- device-resident convergence loop (engine.py:330-388) ---- */
+/* Per-iteration record written by the device (16 x uint64). */
+typedef struct wg_iter_rec {
+    uint64_t mode;             /* 0 not run, 1 FullScan, 2 Wedge */
+    uint64_t active_edges;     /* sum outdeg of the consumed frontier (engine.py:361) */
+    uint64_t vectors_touched;
+    uint64_t frontier_out;     /* produced frontier size */
+    uint64_t out_edge_sum;     /* sum outdeg of the produced frontier */
+    uint64_t nz_packed;        /* (members with out-edges << 32) | their index entries */
+    uint64_t z_count;          /* produced members without out-edges */
+    uint64_t covered_vectors;  /* WedgeFrontier.covered_vector_count (frontier.py:143-150) */
+    uint64_t transform_entries;/* WedgeFrontier.entries_visited */
+    uint64_t groups;           /* selected wedge groups */
+    uint64_t overflow;         /* WG_VAL_U32 overflow flag */
+    uint64_t reserved[5];
+} wg_iter_rec;
+
+/* Device buffers of a run; all caller-allocated (sizes from
+ * wg_run_buffer_sizes).  vals[2] hold `val_type` values. */
+typedef struct wg_run_bufs {
+    void *vals[2];          /* [n] each */
+    uint32_t *fbits[2];     /* [ceil(n/32)] each, zero on init */
+    uint32_t *fvert[2];     /* [n] frontier lists */
+    uint32_t *fpref[2];     /* [n] entry prefixes of the lists */
+    uint32_t *gbits;        /* [ceil(groups/32)] zero on init */
+    uint32_t *glist;        /* [groups] */
+    uint64_t *bcount;       /* [blocks] compaction scratch */
+    wg_iter_rec *recs;      /* [ring] */
+    uint64_t *ctrl;         /* [4]: base iteration, ... */
+    uint32_t ring;          /* record ring length */
+} wg_run_bufs;
+
+typedef struct wg_run_params {
+    int32_t val_type;
+    int32_t shift;          /* log2(vectors per group) */
+    wg_minplus kern;
+    uint64_t wedge_limit;   /* wedge iff E>0 and edge_sum < wedge_limit (= ceil(num*E/den)) */
+} wg_run_params;
+
+/* Element counts: [0] fbits words, [1] groups, [2] gbits words, [3] bcount
+ * entries (the caller multiplies by element sizes). */
+int wg_run_buffer_sizes(const wg_graph *g, int shift, uint64_t *h_sizes4);
+/* Seed iteration 0 from the initial-frontier bitmap d_init_words (uint32
+ * words over n): builds list 0 and record 0, zeroes record 1.  The caller has
+ * already written vals[0] == vals[1] == initial values. */
+int wg_run_init(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p,
+                const uint32_t *d_init_words, void *stream);
+/* Enqueue iterations [it_begin, it_begin + count) (1-based).  Each kernel
+ * re-derives the gate and the converged flag on device from the previous
+ * record, so iterations after convergence are no-ops.  Asynchronous. */
+int wg_run_enqueue(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p,
+                   uint64_t it_begin, uint32_t count, void *stream);
+/* Enqueue only the launches of one iteration (for CUDA-graph capture); the
+ * iteration number comes from the device counter b->ctrl[0] which the last
+ * launch advances. */
+int wg_run_enqueue_counter(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p,
+                           uint32_t count, void *stream);
+
+/* ---------------- PageRank (BASELINE config 5) ---------------------------- */
+/* float32 ranks, damping, fixed iterations, dangling mass spread uniformly.
+ * d_rank [n] out; d_acc [n], d_contrib [n] scratch; d_scal [4] doubles scratch. */
+int wg_pagerank(const wg_graph *g, int iterations, double damping, float *d_rank, float *d_acc,
+                float *d_contrib, double *d_scal, void *stream);
+
+/* ---------------- input generation (graph_io.py:87-221) ------------------- */
+/* RMAT edges m = edge_factor << scale from PCG64(state, inc) exactly like
+ * numpy's default_rng(PCG64(seed)).random((m, scale)) (graph_io.py:188-202).
+ * state/inc are 128-bit values split into hi/lo words.  thresholds = {a, a+b,
+ * a+b+c} as computed in float64. */
+int wg_rmat_edges(uint32_t scale, uint64_t m, uint64_t state_hi, uint64_t state_lo,
+                  uint64_t inc_hi, uint64_t inc_lo, const double *h_thresholds3, uint32_t *d_src,
+                  uint32_t *d_dst, void *stream);
+/* Canonical edge list: optional self-loop removal, optional symmetrize, sort
+ * by (src, dst) and de-duplicate.  In-place on d_src/d_dst (capacity
+ * 2*m when symmetrizing); d_scratch from wg_canonical_scratch_bytes.
+ * h_m_out (host) receives the resulting edge count.  Synchronises. */
+size_t wg_canonical_scratch_bytes(uint64_t m);
+int wg_canonical_edges(uint64_t m, uint32_t *d_src, uint32_t *d_dst, int drop_loops,
+                       int symmetrize, void *d_scratch, size_t scratch_bytes, uint64_t *h_m_out,
+                       void *stream);
+/* weight = 1 + ((((s*K) ^ d) * K) >> 48) % max_weight  (graph_io.py:215-220). */
+int wg_weights_hash(uint64_t m, const uint32_t *d_src, const uint32_t *d_dst, uint32_t max_weight,
+                    uint32_t *d_w, void *stream);
+/* 4-neighbour rows x cols grid, each undirected edge kept with probability
+ * keep_per_million/1e6 and weight uniform in [1, max_weight], both directions
+ * with the same weight; counter-based hash stream keyed by seed.  Outputs up
+ * to 4*rows*cols directed edges; h_m_out receives the count.  Synchronises. */
+int wg_grid_edges(uint32_t rows, uint32_t cols, uint64_t seed, uint32_t keep_per_million,
+                  uint32_t max_weight, uint32_t *d_src, uint32_t *d_dst, uint32_t *d_w,
+                  uint64_t *d_counter, uint64_t *h_m_out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* WEDGE_B200_H */

@@ -1,0 +1,148 @@
+"""ctypes binding of the C ABI declared in include/wedge_b200.h.
+
+The shared library ``libwedge_b200.so`` is built in-tree by
+``paper_1903_07754_b200._build.build()`` (nvcc, sm_100a).  There is no CPU
+fallback: if the library is missing or no CUDA device is visible, every entry
+point raises, loudly.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+LIB_PATH = PKG / "libwedge_b200.so"
+
+WG_OK = 0
+WG_EINVAL, WG_ECUDA, WG_ENOSPACE, WG_EOVERFLOW = -1, -2, -3, -4
+WG_VAL_U32, WG_VAL_I64 = 0, 1
+NO_LANE = 0xFFFFFFFF
+
+c_u32, c_u64, c_i32, c_i64, c_vp = ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p
+
+
+class WgGraph(ctypes.Structure):
+    _fields_ = [("n", c_u32), ("width", c_u32), ("nvec", c_u64), ("edges", c_u64),
+                ("entries", c_u64), ("vsrc", c_vp), ("vdst", c_vp), ("vw", c_vp),
+                ("idx_off", c_vp), ("idx_pos", c_vp), ("outdeg", c_vp)]
+
+
+class WgMinPlus(ctypes.Structure):
+    _fields_ = [("filter_unvisited", c_i32), ("use_weight", c_i32), ("apply_increment", c_i64),
+                ("sentinel", c_i64)]
+
+
+REC_FIELDS = ["mode", "active_edges", "vectors_touched", "frontier_out", "out_edge_sum",
+              "nz_packed", "z_count", "covered_vectors", "transform_entries", "groups", "overflow"]
+REC_U64 = 16  # record size in uint64 words
+
+
+class WgRunBufs(ctypes.Structure):
+    _fields_ = [("vals", c_vp * 2), ("fbits", c_vp * 2), ("fvert", c_vp * 2), ("fpref", c_vp * 2),
+                ("gbits", c_vp), ("glist", c_vp), ("bcount", c_vp), ("recs", c_vp), ("ctrl", c_vp),
+                ("ring", c_u32)]
+
+
+class WgRunParams(ctypes.Structure):
+    _fields_ = [("val_type", c_i32), ("shift", c_i32), ("kern", WgMinPlus), ("wedge_limit", c_u64)]
+
+
+EXPORTS = [
+    "wg_last_error", "wg_abi_version", "wg_device_sm_count", "wg_vector_capacity",
+    "wg_layout_scratch_bytes", "wg_build_layout", "wg_kernel_workspace_bytes", "wg_transform",
+    "wg_pull_full", "wg_pull_wedge", "wg_covered_groups", "wg_run_buffer_sizes", "wg_run_init",
+    "wg_run_enqueue", "wg_run_enqueue_counter", "wg_pagerank", "wg_rmat_edges",
+    "wg_canonical_scratch_bytes", "wg_canonical_edges", "wg_weights_hash", "wg_grid_edges",
+]
+
+_LIB = None
+
+
+class WedgeError(RuntimeError):
+    """A C-ABI call failed (the message comes from wg_last_error)."""
+
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"wedge_b200 error {code}: {msg}")
+        self.code = code
+
+
+class OverflowError32(WedgeError):
+    pass
+
+
+def load(path: os.PathLike | str | None = None):
+    """Load libwedge_b200.so (no compute call is made)."""
+    global _LIB
+    if _LIB is not None and path is None:
+        return _LIB
+    p = Path(path) if path else LIB_PATH
+    if not p.exists():
+        raise RuntimeError(
+            f"{p} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(the B200 engine has no CPU fallback)")
+    L = ctypes.CDLL(str(p))
+    G = ctypes.POINTER(WgGraph)
+    K = ctypes.POINTER(WgMinPlus)
+    B = ctypes.POINTER(WgRunBufs)
+    P = ctypes.POINTER(WgRunParams)
+    u64p = ctypes.POINTER(c_u64)
+    sig = {
+        "wg_last_error": (ctypes.c_char_p, []),
+        "wg_abi_version": (ctypes.c_int, []),
+        "wg_device_sm_count": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int)]),
+        "wg_vector_capacity": (c_u64, [c_u64, c_u32, c_u32]),
+        "wg_layout_scratch_bytes": (ctypes.c_size_t, [c_u64, c_u32]),
+        "wg_build_layout": (ctypes.c_int, [c_u32, c_u64, c_vp, c_vp, c_vp, c_u32, c_u64, c_vp, c_vp,
+                                           c_vp, c_vp, c_vp, c_vp, c_vp, ctypes.c_size_t, u64p, c_vp]),
+        "wg_kernel_workspace_bytes": (ctypes.c_size_t, [G, ctypes.c_int]),
+        "wg_transform": (ctypes.c_int, [G, c_vp, ctypes.c_int, c_vp, c_vp, ctypes.c_size_t, u64p, c_vp]),
+        "wg_pull_full": (ctypes.c_int, [G, ctypes.c_int, c_vp, c_vp, c_vp, K, c_vp, ctypes.c_size_t,
+                                        u64p, c_vp]),
+        "wg_pull_wedge": (ctypes.c_int, [G, c_vp, ctypes.c_int, ctypes.c_int, c_vp, c_vp, c_vp, K, c_vp,
+                                         ctypes.c_size_t, u64p, c_vp]),
+        "wg_covered_groups": (ctypes.c_int, [c_vp, c_u64, c_vp, c_vp, ctypes.c_size_t, u64p, c_vp]),
+        "wg_run_buffer_sizes": (ctypes.c_int, [G, ctypes.c_int, u64p]),
+        "wg_run_init": (ctypes.c_int, [G, B, P, c_vp, c_vp]),
+        "wg_run_enqueue": (ctypes.c_int, [G, B, P, c_u64, c_u32, c_vp]),
+        "wg_run_enqueue_counter": (ctypes.c_int, [G, B, P, c_u32, c_vp]),
+        "wg_pagerank": (ctypes.c_int, [G, ctypes.c_int, ctypes.c_double, c_vp, c_vp, c_vp, c_vp, c_vp]),
+        "wg_rmat_edges": (ctypes.c_int, [c_u32, c_u64, c_u64, c_u64, c_u64, c_u64,
+                                         ctypes.POINTER(ctypes.c_double), c_vp, c_vp, c_vp]),
+        "wg_canonical_scratch_bytes": (ctypes.c_size_t, [c_u64]),
+        "wg_canonical_edges": (ctypes.c_int, [c_u64, c_vp, c_vp, ctypes.c_int, ctypes.c_int, c_vp,
+                                              ctypes.c_size_t, u64p, c_vp]),
+        "wg_weights_hash": (ctypes.c_int, [c_u64, c_vp, c_vp, c_u32, c_vp, c_vp]),
+        "wg_grid_edges": (ctypes.c_int, [c_u32, c_u32, c_u64, c_u32, c_u32, c_vp, c_vp, c_vp, c_vp,
+                                         u64p, c_vp]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    if path is None:
+        _LIB = L
+    return L
+
+
+def check(rc: int) -> None:
+    if rc != WG_OK:
+        msg = load().wg_last_error().decode(errors="replace")
+        if rc == WG_EOVERFLOW:
+            raise OverflowError32(rc, msg)
+        raise WedgeError(rc, msg)
+
+
+def require_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1903_07754_b200 needs a CUDA device (B200, sm_100a); none is visible")
+    load()
+    return torch
+
+
+def stream_ptr(stream=None) -> int:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)

@@ -1,0 +1,424 @@
+// engine.cu — C-ABI entry points of the pull engine: per-call kernels (the
+// reference backend protocol, kernels.py:55-125) and the device-resident
+// convergence loop (engine.py:330-388).
+#include <mutex>
+#include <unordered_map>
+
+#include "frontier.cuh"
+#include "pull.cuh"
+
+using namespace wg;
+
+namespace {
+
+struct Occ {
+    std::mutex mu;
+    std::unordered_map<const void *, int> blocks;
+};
+Occ &occ() {
+    static Occ o;
+    return o;
+}
+
+template <typename K>
+unsigned persistent_grid(K kernel, int threads, uint64_t work_blocks) {
+    const void *key = (const void *)kernel;
+    int per_sm = 0;
+    {
+        std::lock_guard<std::mutex> lk(occ().mu);
+        auto it = occ().blocks.find(key);
+        if (it != occ().blocks.end()) per_sm = it->second;
+    }
+    if (per_sm == 0) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0) != cudaSuccess ||
+            per_sm < 1)
+            per_sm = 1;
+        std::lock_guard<std::mutex> lk(occ().mu);
+        occ().blocks[key] = per_sm;
+    }
+    uint64_t cap = (uint64_t)sm_count() * per_sm;
+    if (work_blocks < 1) work_blocks = 1;
+    return (unsigned)(work_blocks < cap ? work_blocks : cap);
+}
+
+using PullFn = void (*)(LoopCtx, wg_graph, PullBufs, int, int64_t, int64_t);
+
+template <typename T, int W>
+PullFn pick_pull_w(bool weight, bool filter) {
+    if (weight) return filter ? pull_kernel<T, W, true, true> : pull_kernel<T, W, true, false>;
+    return filter ? pull_kernel<T, W, false, true> : pull_kernel<T, W, false, false>;
+}
+
+template <typename T>
+PullFn pick_pull_t(int width, bool weight, bool filter) {
+    switch (width) {
+        case 1: return pick_pull_w<T, 1>(weight, filter);
+        case 2: return pick_pull_w<T, 2>(weight, filter);
+        case 4: return pick_pull_w<T, 4>(weight, filter);
+        case 8: return pick_pull_w<T, 8>(weight, filter);
+    }
+    return nullptr;
+}
+
+PullFn pick_pull(int val_type, int width, bool weight, bool filter) {
+    return val_type == WG_VAL_U32 ? pick_pull_t<uint32_t>(width, weight, filter)
+                                  : pick_pull_t<int64_t>(width, weight, filter);
+}
+
+int check_graph(const wg_graph *g) {
+    WG_REQUIRE(g != nullptr, "graph is null");
+    WG_REQUIRE(g->width == 1 || g->width == 2 || g->width == 4 || g->width == 8,
+               "unsupported vector width %u (1, 2, 4, 8)", g->width);
+    WG_REQUIRE(g->n < 0xffffffffu, "vertex count must be < 2^32-1");
+    WG_REQUIRE(g->nvec < (1ull << 32) && g->entries < (1ull << 32), "layout too large for uint32 ids");
+    if (g->nvec) WG_REQUIRE(g->vsrc && g->vdst, "null layout arrays");
+    WG_REQUIRE(g->idx_off && g->outdeg, "null index/degree arrays");
+    return WG_OK;
+}
+
+uint64_t groups_of(const wg_graph *g, int shift) { return (g->nvec + (1ull << shift) - 1) >> shift; }
+
+struct KernelWs {
+    wg_iter_rec *recs;
+    uint32_t *fvert[2], *fpref[2], *glist;
+    uint64_t *bcount;
+};
+
+int carve_kernel_ws(const wg_graph *g, int shift, void *ws, size_t bytes, KernelWs *k) {
+    Carve cv{(char *)ws, 0, bytes};
+    uint64_t n = g->n ? g->n : 1, groups = groups_of(g, shift);
+    uint64_t nb = cb_blocks(n) * 4;
+    uint64_t gb = cb_blocks(groups ? groups : 1);
+    k->recs = cv.take<wg_iter_rec>(2);
+    for (int i = 0; i < 2; ++i) {
+        k->fvert[i] = cv.take<uint32_t>(n);
+        k->fpref[i] = cv.take<uint32_t>(n);
+    }
+    k->glist = cv.take<uint32_t>(groups ? groups : 1);
+    k->bcount = cv.take<uint64_t>(nb > gb ? nb : gb);
+    if (!k->recs || !k->fvert[1] || !k->fpref[1] || !k->glist || !k->bcount) {
+        set_error("kernel workspace too small (%zu bytes)", bytes);
+        return WG_ENOSPACE;
+    }
+    return WG_OK;
+}
+
+LoopCtx forced_ctx(wg_iter_rec *recs, int mode, uint64_t edges) {
+    LoopCtx c{};
+    c.recs = recs;
+    c.ring = 2;
+    c.forced_mode = mode;
+    c.ctrl = nullptr;
+    c.it_arg = 1;
+    c.wedge_limit = 0;
+    c.edges = edges;
+    return c;
+}
+
+int launch_group_compaction(const LoopCtx &c, uint32_t *words, uint64_t ngroups, uint64_t *bcount,
+                            uint32_t *glist, int clear, int shift, uint64_t nvec, cudaStream_t s) {
+    uint64_t nb = cb_blocks(ngroups ? ngroups : 1);
+    group_count_kernel<<<(unsigned)nb, CB_THREADS, 0, s>>>(c, words, ngroups, bcount);
+    group_list_kernel<<<(unsigned)nb, CB_THREADS, 0, s>>>(c, words, ngroups, bcount, glist, clear,
+                                                          shift, nvec);
+    WG_CHECK_LAUNCH("group compaction");
+    return WG_OK;
+}
+
+int launch_frontier_compaction(const wg_graph *g, const uint32_t *words, uint64_t *bcount,
+                               uint32_t *fvert, uint32_t *fpref, wg_iter_rec *rec, cudaStream_t s) {
+    uint64_t nb = cb_blocks(g->n ? g->n : 1);
+    frontier_count_kernel<<<(unsigned)nb, CB_THREADS, 0, s>>>(words, g->n, g->idx_off, g->outdeg,
+                                                              bcount);
+    frontier_list_kernel<<<(unsigned)nb, CB_THREADS, 0, s>>>(words, g->n, g->idx_off, bcount, fvert,
+                                                             fpref, rec);
+    WG_CHECK_LAUNCH("frontier compaction");
+    return WG_OK;
+}
+
+int launch_transform(const LoopCtx &c, const wg_graph *g, uint32_t *const fvert[2],
+                     uint32_t *const fpref[2], int shift, uint32_t *gbits, cudaStream_t s) {
+    unsigned grid = persistent_grid(transform_kernel, TR_THREADS, (g->entries + TR_TILE - 1) / TR_TILE);
+    transform_kernel<<<grid, TR_THREADS, 0, s>>>(c, fvert[0], fvert[1], fpref[0], fpref[1], g->idx_off,
+                                                 g->idx_pos, shift, gbits);
+    WG_CHECK_LAUNCH("transform");
+    return WG_OK;
+}
+
+int launch_pull(const LoopCtx &c, const wg_graph *g, const PullBufs &pb, int val_type, int shift,
+                const wg_minplus *k, uint64_t max_items, cudaStream_t s) {
+    PullFn fn = pick_pull(val_type, (int)g->width, k->use_weight != 0, k->filter_unvisited != 0);
+    WG_REQUIRE(fn != nullptr, "no pull kernel for width %u", g->width);
+    WG_REQUIRE(!k->use_weight || g->vw, "weighted kernel on an unweighted layout");
+    unsigned grid = persistent_grid(fn, 256, (max_items + 255) / 256);
+    fn<<<grid, 256, 0, s>>>(c, *g, pb, shift, k->apply_increment, k->sentinel);
+    WG_CHECK_LAUNCH("pull");
+    return WG_OK;
+}
+
+int read_rec(const wg_iter_rec *d_rec, wg_iter_rec *h, cudaStream_t s) {
+    WG_CUDA(cudaMemcpyAsync(h, d_rec, sizeof(wg_iter_rec), cudaMemcpyDeviceToHost, s));
+    WG_CUDA(cudaStreamSynchronize(s));
+    return WG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t wg_kernel_workspace_bytes(const wg_graph *g, int shift) {
+    if (!g || shift < 0 || shift > 4) return 0;
+    uint64_t n = g->n ? g->n : 1, groups = groups_of(g, shift);
+    uint64_t nb = cb_blocks(n) * 4, gb = cb_blocks(groups ? groups : 1);
+    return carve_size(2 * sizeof(wg_iter_rec)) + 4 * carve_size(n * 4) +
+           carve_size((groups ? groups : 1) * 4) + carve_size((nb > gb ? nb : gb) * 8) + 256;
+}
+
+int wg_transform(const wg_graph *g, const uint32_t *d_frontier_words, int shift,
+                 uint32_t *d_wedge_words, void *d_ws, size_t ws_bytes, uint64_t *h_visited,
+                 void *stream) {
+    int rc = check_graph(g);
+    if (rc) return rc;
+    WG_REQUIRE(shift >= 0 && shift <= 4, "shift must be in [0, 4]");
+    WG_REQUIRE(d_frontier_words && h_visited, "null argument");
+    cudaStream_t s = as_stream(stream);
+    KernelWs k;
+    if ((rc = carve_kernel_ws(g, shift, d_ws, ws_bytes, &k))) return rc;
+    WG_CUDA(cudaMemsetAsync(k.recs, 0, 2 * sizeof(wg_iter_rec), s));
+    *h_visited = 0;
+    if (g->n == 0) return WG_OK;
+    if ((rc = launch_frontier_compaction(g, d_frontier_words, k.bcount, k.fvert[0], k.fpref[0],
+                                         &k.recs[0], s)))
+        return rc;
+    if (g->entries) {
+        WG_REQUIRE(d_wedge_words && g->idx_pos, "null wedge words / index");
+        LoopCtx c = forced_ctx(k.recs, MODE_WEDGE, g->edges);
+        if ((rc = launch_transform(c, g, k.fvert, k.fpref, shift, d_wedge_words, s))) return rc;
+    }
+    wg_iter_rec h[2];
+    WG_CUDA(cudaMemcpyAsync(h, k.recs, sizeof(h), cudaMemcpyDeviceToHost, s));
+    WG_CUDA(cudaStreamSynchronize(s));
+    *h_visited = h[0].nz_packed & 0xffffffffull;
+    return WG_OK;
+}
+
+static int pull_common(const wg_graph *g, const uint32_t *d_wedge_words, int shift, int val_type,
+                       const void *d_prev, void *d_nxt, uint32_t *d_out_words, const wg_minplus *k,
+                       void *d_ws, size_t ws_bytes, uint64_t *h_touched, void *stream) {
+    int rc = check_graph(g);
+    if (rc) return rc;
+    WG_REQUIRE(val_type == WG_VAL_U32 || val_type == WG_VAL_I64, "bad value type");
+    WG_REQUIRE(k && d_prev && d_nxt && d_out_words && h_touched, "null argument");
+    WG_REQUIRE(shift >= 0 && shift <= 4, "shift must be in [0, 4]");
+    cudaStream_t s = as_stream(stream);
+    KernelWs ws;
+    if ((rc = carve_kernel_ws(g, shift, d_ws, ws_bytes, &ws))) return rc;
+    *h_touched = 0;
+    if (g->nvec == 0) return WG_OK;
+    WG_CUDA(cudaMemsetAsync(ws.recs, 0, 2 * sizeof(wg_iter_rec), s));
+    bool wedge = d_wedge_words != nullptr;
+    LoopCtx c = forced_ctx(ws.recs, wedge ? MODE_WEDGE : MODE_FULL, g->edges);
+    uint64_t items = g->nvec;
+    if (wedge) {
+        uint64_t groups = groups_of(g, shift);
+        if ((rc = launch_group_compaction(c, const_cast<uint32_t *>(d_wedge_words), groups, ws.bcount,
+                                          ws.glist, 0, shift, g->nvec, s)))
+            return rc;
+        items = groups << shift;
+    }
+    PullBufs pb{};
+    pb.vals[0] = const_cast<void *>(d_prev);
+    pb.vals[1] = d_nxt;
+    pb.fbits[0] = pb.fbits[1] = d_out_words;
+    pb.fvert[0] = ws.fvert[0];
+    pb.fvert[1] = ws.fvert[1];
+    pb.fpref[0] = ws.fpref[0];
+    pb.fpref[1] = ws.fpref[1];
+    pb.glist = ws.glist;
+    pb.n = g->n;
+    if ((rc = launch_pull(c, g, pb, val_type, shift, k, items, s))) return rc;
+    wg_iter_rec h[2];
+    WG_CUDA(cudaMemcpyAsync(h, ws.recs, sizeof(h), cudaMemcpyDeviceToHost, s));
+    WG_CUDA(cudaStreamSynchronize(s));
+    if (h[1].overflow) {
+        set_error("uint32 value overflow: a candidate reached 0xFFFFFFFF");
+        return WG_EOVERFLOW;
+    }
+    *h_touched = h[1].vectors_touched;
+    return WG_OK;
+}
+
+int wg_pull_full(const wg_graph *g, int val_type, const void *d_prev, void *d_nxt,
+                 uint32_t *d_out_words, const wg_minplus *k, void *d_ws, size_t ws_bytes,
+                 uint64_t *h_touched, void *stream) {
+    return pull_common(g, nullptr, 0, val_type, d_prev, d_nxt, d_out_words, k, d_ws, ws_bytes,
+                       h_touched, stream);
+}
+
+int wg_pull_wedge(const wg_graph *g, const uint32_t *d_wedge_words, int shift, int val_type,
+                  const void *d_prev, void *d_nxt, uint32_t *d_out_words, const wg_minplus *k,
+                  void *d_ws, size_t ws_bytes, uint64_t *h_touched, void *stream) {
+    if (!d_wedge_words) {
+        set_error("null wedge words");
+        return WG_EINVAL;
+    }
+    return pull_common(g, d_wedge_words, shift, val_type, d_prev, d_nxt, d_out_words, k, d_ws,
+                       ws_bytes, h_touched, stream);
+}
+
+int wg_covered_groups(const uint32_t *d_wedge_words, uint64_t group_count, uint32_t *d_groups,
+                      void *d_ws, size_t ws_bytes, uint64_t *h_count, void *stream) {
+    WG_REQUIRE(h_count, "null argument");
+    *h_count = 0;
+    if (group_count == 0) return WG_OK;
+    WG_REQUIRE(d_wedge_words && d_groups, "null argument");
+    cudaStream_t s = as_stream(stream);
+    Carve cv{(char *)d_ws, 0, ws_bytes};
+    wg_iter_rec *recs = cv.take<wg_iter_rec>(2);
+    uint64_t *bcount = cv.take<uint64_t>(cb_blocks(group_count));
+    if (!recs || !bcount) {
+        set_error("workspace too small");
+        return WG_ENOSPACE;
+    }
+    WG_CUDA(cudaMemsetAsync(recs, 0, 2 * sizeof(wg_iter_rec), s));
+    LoopCtx c = forced_ctx(recs, MODE_WEDGE, 1);
+    int rc = launch_group_compaction(c, const_cast<uint32_t *>(d_wedge_words), group_count, bcount,
+                                     d_groups, 0, 0, group_count, s);
+    if (rc) return rc;
+    wg_iter_rec h[2];
+    WG_CUDA(cudaMemcpyAsync(h, recs, sizeof(h), cudaMemcpyDeviceToHost, s));
+    WG_CUDA(cudaStreamSynchronize(s));
+    *h_count = h[1].groups;
+    return WG_OK;
+}
+
+// ------------------------------------------------------------ run loop ---
+int wg_run_buffer_sizes(const wg_graph *g, int shift, uint64_t *h_sizes4) {
+    int rc = check_graph(g);
+    if (rc) return rc;
+    WG_REQUIRE(h_sizes4, "null argument");
+    uint64_t groups = groups_of(g, shift);
+    uint64_t nb = cb_blocks(g->n ? g->n : 1) * 4, gb = cb_blocks(groups ? groups : 1);
+    h_sizes4[0] = ((uint64_t)g->n + 31) >> 5;
+    h_sizes4[1] = groups;
+    h_sizes4[2] = (groups + 31) >> 5;
+    h_sizes4[3] = nb > gb ? nb : gb;
+    return WG_OK;
+}
+
+static LoopCtx loop_ctx(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p,
+                        const uint64_t *ctrl, uint64_t it) {
+    LoopCtx c{};
+    c.recs = b->recs;
+    c.ring = b->ring;
+    c.forced_mode = 0;
+    c.ctrl = ctrl;
+    c.it_arg = it;
+    c.wedge_limit = p->wedge_limit;
+    c.edges = g->edges;
+    return c;
+}
+
+static PullBufs pull_bufs(const wg_graph *g, const wg_run_bufs *b) {
+    PullBufs pb{};
+    for (int i = 0; i < 2; ++i) {
+        pb.vals[i] = b->vals[i];
+        pb.fbits[i] = b->fbits[i];
+        pb.fvert[i] = b->fvert[i];
+        pb.fpref[i] = b->fpref[i];
+    }
+    pb.glist = b->glist;
+    pb.n = g->n;
+    return pb;
+}
+
+static int check_run(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p) {
+    int rc = check_graph(g);
+    if (rc) return rc;
+    WG_REQUIRE(b && p, "null argument");
+    WG_REQUIRE(p->val_type == WG_VAL_U32 || p->val_type == WG_VAL_I64, "bad value type");
+    WG_REQUIRE(p->shift >= 0 && p->shift <= 4, "shift must be in [0, 4]");
+    WG_REQUIRE(b->ring >= 4, "record ring must hold >= 4 records");
+    WG_REQUIRE(b->vals[0] && b->vals[1] && b->fbits[0] && b->fbits[1] && b->fvert[0] && b->fvert[1] &&
+                   b->fpref[0] && b->fpref[1] && b->gbits && b->glist && b->bcount && b->recs &&
+                   b->ctrl,
+               "null run buffer");
+    WG_REQUIRE(!p->kern.use_weight || g->vw, "weighted kernel on an unweighted layout");
+    return WG_OK;
+}
+
+int wg_run_init(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p,
+                const uint32_t *d_init_words, void *stream) {
+    int rc = check_run(g, b, p);
+    if (rc) return rc;
+    WG_REQUIRE(d_init_words, "null initial frontier");
+    cudaStream_t s = as_stream(stream);
+    uint64_t words = ((uint64_t)g->n + 31) >> 5;
+    uint64_t groups = groups_of(g, p->shift);
+    WG_CUDA(cudaMemsetAsync(b->recs, 0, sizeof(wg_iter_rec) * b->ring, s));
+    WG_CUDA(cudaMemsetAsync(b->ctrl, 0, 4 * sizeof(uint64_t), s));
+    WG_CUDA(cudaMemsetAsync(b->fbits[0], 0, words * 4, s));
+    WG_CUDA(cudaMemsetAsync(b->fbits[1], 0, words * 4, s));
+    WG_CUDA(cudaMemsetAsync(b->gbits, 0, ((groups + 31) >> 5) * 4, s));
+    if (g->n == 0) return WG_OK;
+    return launch_frontier_compaction(g, d_init_words, b->bcount, b->fvert[0], b->fpref[0],
+                                      &b->recs[0], s);
+}
+
+static int enqueue_one(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p,
+                       const LoopCtx &c, cudaStream_t s) {
+    int rc;
+    uint64_t groups = groups_of(g, p->shift);
+    uint32_t *fv[2] = {b->fvert[0], b->fvert[1]};
+    uint32_t *fp[2] = {b->fpref[0], b->fpref[1]};
+    if (g->entries) {
+        if ((rc = launch_transform(c, g, fv, fp, p->shift, b->gbits, s))) return rc;
+    }
+    if (groups) {
+        if ((rc = launch_group_compaction(c, b->gbits, groups, b->bcount, b->glist, 1, p->shift,
+                                          g->nvec, s)))
+            return rc;
+    }
+    PullBufs pb = pull_bufs(g, b);
+    if (g->nvec) {
+        if ((rc = launch_pull(c, g, pb, p->val_type, p->shift, &p->kern, g->nvec, s))) return rc;
+    }
+    unsigned grid = (unsigned)sm_count() * 2;
+    if (p->val_type == WG_VAL_U32)
+        finalize_kernel<uint32_t><<<grid, 256, 0, s>>>(c, pb);
+    else
+        finalize_kernel<int64_t><<<grid, 256, 0, s>>>(c, pb);
+    WG_CHECK_LAUNCH("finalize");
+    return WG_OK;
+}
+
+int wg_run_enqueue(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p,
+                   uint64_t it_begin, uint32_t count, void *stream) {
+    int rc = check_run(g, b, p);
+    if (rc) return rc;
+    WG_REQUIRE(it_begin >= 1, "iterations are 1-based");
+    WG_REQUIRE(count + 1 < b->ring, "batch of %u iterations needs a ring > %u", count, count + 1);
+    cudaStream_t s = as_stream(stream);
+    for (uint32_t i = 0; i < count; ++i) {
+        LoopCtx c = loop_ctx(g, b, p, nullptr, it_begin + i);
+        if ((rc = enqueue_one(g, b, p, c, s))) return rc;
+    }
+    return WG_OK;
+}
+
+int wg_run_enqueue_counter(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p,
+                           uint32_t count, void *stream) {
+    int rc = check_run(g, b, p);
+    if (rc) return rc;
+    WG_REQUIRE(count + 1 < b->ring, "batch of %u iterations needs a ring > %u", count, count + 1);
+    cudaStream_t s = as_stream(stream);
+    for (uint32_t i = 0; i < count; ++i) {
+        LoopCtx c = loop_ctx(g, b, p, b->ctrl, 1 + i);
+        if ((rc = enqueue_one(g, b, p, c, s))) return rc;
+    }
+    bump_counter_kernel<<<1, 1, 0, s>>>(b->ctrl, count);
+    WG_CHECK_LAUNCH("bump");
+    return WG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,484 @@
+// layout.cu — on-device construction of the pull layout (K1) and the seeded
+// input generators (K9).
+//
+// Layout (graph.py:220-301 restated for the GPU):
+//   1. radix-sort edges by (dst, src) (stable, like np.lexsort((src, dst)));
+//   2. per destination run: first/last edge -> in-degree -> vectors
+//      ceil(indeg / W) -> exclusive scan = first vector of each destination;
+//   3. pack: edge of rank r in its run goes to vector base + r / W, lane r % W;
+//      padding lanes hold WG_NO_LANE (only the last vector of a run is partial,
+//      graph.py:113-116);
+//   4. edge index: keys (src, vector) in vector order, radix-sorted by src,
+//      adjacent duplicates removed (graph.py:293-297); run bounds per source
+//      give the CSR offsets; the pre-dedup run lengths are the out-degrees.
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+
+using namespace wg;
+
+namespace {
+
+inline int bits_for(uint64_t x) {  // bits needed to represent values < x (>= 1)
+    int b = 1;
+    while (b < 64 && (1ull << b) < x) ++b;
+    return b;
+}
+
+__global__ void make_dst_keys(uint64_t m, const uint32_t *src, const uint32_t *dst, int sb,
+                              uint64_t *keys) {
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m;
+         e += (uint64_t)gridDim.x * blockDim.x)
+        keys[e] = ((uint64_t)dst[e] << sb) | src[e];
+}
+
+// first[k] / last[k] of each run of equal (key >> shift) in sorted keys.
+__global__ void run_bounds(uint64_t m, const uint64_t *keys, int shift, uint64_t *first,
+                           uint64_t *last) {
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t k = keys[e] >> shift;
+        if (e == 0 || (keys[e - 1] >> shift) != k) first[k] = e;
+        if (e == m - 1 || (keys[e + 1] >> shift) != k) last[k] = e;
+    }
+}
+
+// per-vertex count = run length (0 when the vertex has no run), optionally
+// rounded up to whole vectors; the count itself is also written to deg.
+__global__ void run_counts(uint32_t n, const uint64_t *first, const uint64_t *last, int width,
+                           uint64_t *out, uint32_t *deg) {
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
+         v += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t f = first[v];
+        uint64_t c = (f == ~0ull) ? 0 : last[v] - f + 1;
+        out[v] = width > 0 ? (c + width - 1) / width : c;
+        if (deg) deg[v] = (uint32_t)c;
+    }
+}
+
+__global__ void pack_vectors(uint64_t m, const uint64_t *keys, const uint32_t *wsorted, int sb,
+                             const uint64_t *first, const uint64_t *vbase, int width,
+                             uint32_t *vsrc, uint32_t *vdst, uint32_t *vw, uint64_t *ikeys, int vb) {
+    const uint64_t smask = (1ull << sb) - 1;
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t key = keys[e];
+        uint32_t d = (uint32_t)(key >> sb), s = (uint32_t)(key & smask);
+        uint64_t r = e - first[d];
+        uint64_t vec = vbase[d] + r / width;
+        uint32_t lane = (uint32_t)(r % width);
+        vsrc[vec * width + lane] = s;
+        if (vw) vw[vec * width + lane] = wsorted[e];
+        if (lane == 0) vdst[vec] = d;
+        ikeys[e] = ((uint64_t)s << vb) | vec;  // index entry, in ascending vector order
+    }
+}
+
+__global__ void unpack_positions(uint64_t k, const uint64_t *keys, int vb, uint32_t *pos) {
+    const uint64_t vmask = (1ull << vb) - 1;
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < k;
+         e += (uint64_t)gridDim.x * blockDim.x)
+        pos[e] = (uint32_t)(keys[e] & vmask);
+}
+
+unsigned grid_1d(uint64_t work) { return grid_for(work, 256 * 8, 16); }
+
+struct LayoutScratch {
+    uint64_t *k0, *k1;     // m keys x2
+    uint32_t *w0, *w1;     // m weights x2
+    uint64_t *first, *last, *base;  // n+1 each
+    uint64_t *count;       // 1
+    void *temp;
+    size_t temp_bytes;
+};
+
+size_t cub_temp_bytes(uint64_t m, uint32_t n) {
+    size_t a = 0, b = 0, c = 0, d = 0;
+    cub::DoubleBuffer<uint64_t> kb(nullptr, nullptr);
+    cub::DoubleBuffer<uint32_t> vb(nullptr, nullptr);
+    cub::DeviceRadixSort::SortPairs(nullptr, a, kb, vb, (int64_t)m, 0, 64);
+    cub::DeviceRadixSort::SortKeys(nullptr, b, kb, (int64_t)m, 0, 64);
+    cub::DeviceScan::ExclusiveSum(nullptr, c, (uint64_t *)nullptr, (uint64_t *)nullptr, (int64_t)n + 1);
+    cub::DeviceSelect::Unique(nullptr, d, (uint64_t *)nullptr, (uint64_t *)nullptr,
+                              (uint64_t *)nullptr, (int64_t)m);
+    size_t t = a;
+    if (b > t) t = b;
+    if (c > t) t = c;
+    if (d > t) t = d;
+    return t;
+}
+
+int carve_layout(uint64_t m, uint32_t n, void *scratch, size_t bytes, LayoutScratch *ls) {
+    Carve cv{(char *)scratch, 0, bytes};
+    uint64_t mm = m ? m : 1;
+    ls->k0 = cv.take<uint64_t>(mm);
+    ls->k1 = cv.take<uint64_t>(mm);
+    ls->w0 = cv.take<uint32_t>(mm);
+    ls->w1 = cv.take<uint32_t>(mm);
+    ls->first = cv.take<uint64_t>((uint64_t)n + 1);
+    ls->last = cv.take<uint64_t>((uint64_t)n + 1);
+    ls->base = cv.take<uint64_t>((uint64_t)n + 1);
+    ls->count = cv.take<uint64_t>(4);
+    ls->temp_bytes = cub_temp_bytes(mm, n);
+    ls->temp = cv.take<char>(ls->temp_bytes);
+    if (!ls->temp) {
+        set_error("layout scratch too small (%zu bytes)", bytes);
+        return WG_ENOSPACE;
+    }
+    return WG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+uint64_t wg_vector_capacity(uint64_t m, uint32_t n, uint32_t width) {
+    if (width == 0) return 0;
+    uint64_t runs = m < n ? m : n;
+    return m / width + runs + 1;
+}
+
+size_t wg_layout_scratch_bytes(uint64_t m, uint32_t n) {
+    uint64_t mm = m ? m : 1;
+    return 2 * carve_size(mm * 8) + 2 * carve_size(mm * 4) + 3 * carve_size(((uint64_t)n + 1) * 8) +
+           carve_size(32) + carve_size(cub_temp_bytes(mm, n)) + 1024;
+}
+
+int wg_build_layout(uint32_t n, uint64_t m, const uint32_t *d_src, const uint32_t *d_dst,
+                    const uint32_t *d_w, uint32_t width, uint64_t vec_capacity, uint32_t *d_vsrc,
+                    uint32_t *d_vdst, uint32_t *d_vw, uint64_t *d_idx_off, uint32_t *d_idx_pos,
+                    uint32_t *d_outdeg, void *d_scratch, size_t scratch_bytes, uint64_t *h_counts,
+                    void *stream) {
+    WG_REQUIRE(width == 1 || width == 2 || width == 4 || width == 8, "unsupported width %u", width);
+    WG_REQUIRE(n < 0xffffffffu, "vertex count must be < 2^32-1");
+    WG_REQUIRE(h_counts && d_idx_off && d_outdeg, "null argument");
+    WG_REQUIRE(vec_capacity >= wg_vector_capacity(m, n, width) || m == 0, "vector capacity too small");
+    cudaStream_t s = as_stream(stream);
+    h_counts[0] = h_counts[1] = 0;
+    WG_CUDA(cudaMemsetAsync(d_idx_off, 0, ((uint64_t)n + 1) * 8, s));
+    WG_CUDA(cudaMemsetAsync(d_outdeg, 0, (uint64_t)n * 4, s));
+    if (m == 0 || n == 0) return WG_OK;
+    WG_REQUIRE(d_src && d_dst && d_vsrc && d_vdst && d_idx_pos, "null argument");
+    LayoutScratch ls;
+    int rc = carve_layout(m, n, d_scratch, scratch_bytes, &ls);
+    if (rc) return rc;
+    const int sb = bits_for(n);
+    const bool weighted = d_w != nullptr;
+    WG_REQUIRE(!weighted || d_vw, "weights given without an output weight array");
+
+    // 1. sort by (dst, src), stable
+    make_dst_keys<<<grid_1d(m), 256, 0, s>>>(m, d_src, d_dst, sb, ls.k0);
+    WG_CHECK_LAUNCH("make_dst_keys");
+    cub::DoubleBuffer<uint64_t> kb(ls.k0, ls.k1);
+    size_t tb = ls.temp_bytes;
+    if (weighted) {
+        WG_CUDA(cudaMemcpyAsync(ls.w0, d_w, m * 4, cudaMemcpyDeviceToDevice, s));
+        cub::DoubleBuffer<uint32_t> vb(ls.w0, ls.w1);
+        WG_CUDA(cub::DeviceRadixSort::SortPairs(ls.temp, tb, kb, vb, (int64_t)m, 0, 2 * sb, s));
+        if (vb.Current() != ls.w0)
+            WG_CUDA(cudaMemcpyAsync(ls.w0, vb.Current(), m * 4, cudaMemcpyDeviceToDevice, s));
+    } else {
+        WG_CUDA(cub::DeviceRadixSort::SortKeys(ls.temp, tb, kb, (int64_t)m, 0, 2 * sb, s));
+    }
+    uint64_t *sorted = kb.Current();
+    uint64_t *other = kb.Alternate();
+
+    // 2. destination runs -> vectors per destination -> first vector per destination
+    WG_CUDA(cudaMemsetAsync(ls.first, 0xff, ((uint64_t)n + 1) * 8, s));
+    run_bounds<<<grid_1d(m), 256, 0, s>>>(m, sorted, sb, ls.first, ls.last);
+    run_counts<<<grid_1d(n), 256, 0, s>>>(n, ls.first, ls.last, (int)width, ls.base, nullptr);
+    WG_CHECK_LAUNCH("dst runs");
+    WG_CUDA(cudaMemsetAsync(ls.base + n, 0, 8, s));
+    tb = ls.temp_bytes;
+    WG_CUDA(cub::DeviceScan::ExclusiveSum(ls.temp, tb, ls.base, ls.base, (int64_t)n + 1, s));
+    uint64_t nvec = 0;
+    WG_CUDA(cudaMemcpyAsync(&nvec, ls.base + n, 8, cudaMemcpyDeviceToHost, s));
+    WG_CUDA(cudaStreamSynchronize(s));
+    WG_REQUIRE(nvec <= vec_capacity, "vector capacity exceeded");
+    const int vb = bits_for(nvec);
+    WG_REQUIRE(sb + vb <= 64, "graph too large for 64-bit index keys");
+
+    // 3. pack (padding lanes pre-filled)
+    WG_CUDA(cudaMemsetAsync(d_vsrc, 0xff, nvec * width * 4, s));
+    if (weighted) WG_CUDA(cudaMemsetAsync(d_vw, 0, nvec * width * 4, s));
+    pack_vectors<<<grid_1d(m), 256, 0, s>>>(m, sorted, weighted ? ls.w0 : nullptr, sb, ls.first,
+                                            ls.base, (int)width, d_vsrc, d_vdst,
+                                            weighted ? d_vw : nullptr, other, vb);
+    WG_CHECK_LAUNCH("pack_vectors");
+
+    // 4. edge index: sort (src, vector) keys by src (stable: vectors stay ascending)
+    cub::DoubleBuffer<uint64_t> ib(other, sorted);
+    tb = ls.temp_bytes;
+    WG_CUDA(cub::DeviceRadixSort::SortKeys(ls.temp, tb, ib, (int64_t)m, vb, vb + sb, s));
+    uint64_t *isorted = ib.Current();
+    uint64_t *ialt = ib.Alternate();
+    // out-degrees from the pre-dedup source runs (graph.py:277-280)
+    WG_CUDA(cudaMemsetAsync(ls.first, 0xff, ((uint64_t)n + 1) * 8, s));
+    run_bounds<<<grid_1d(m), 256, 0, s>>>(m, isorted, vb, ls.first, ls.last);
+    run_counts<<<grid_1d(n), 256, 0, s>>>(n, ls.first, ls.last, 0, ls.base, d_outdeg);
+    WG_CHECK_LAUNCH("src runs");
+    // de-duplicate (src, vector) pairs (graph.py:293-297)
+    tb = ls.temp_bytes;
+    WG_CUDA(cub::DeviceSelect::Unique(ls.temp, tb, isorted, ialt, ls.count, (int64_t)m, s));
+    uint64_t entries = 0;
+    WG_CUDA(cudaMemcpyAsync(&entries, ls.count, 8, cudaMemcpyDeviceToHost, s));
+    WG_CUDA(cudaStreamSynchronize(s));
+    WG_CUDA(cudaMemsetAsync(ls.first, 0xff, ((uint64_t)n + 1) * 8, s));
+    run_bounds<<<grid_1d(entries), 256, 0, s>>>(entries, ialt, vb, ls.first, ls.last);
+    run_counts<<<grid_1d(n), 256, 0, s>>>(n, ls.first, ls.last, 0, ls.base, nullptr);
+    WG_CHECK_LAUNCH("index runs");
+    WG_CUDA(cudaMemsetAsync(ls.base + n, 0, 8, s));
+    tb = ls.temp_bytes;
+    WG_CUDA(cub::DeviceScan::ExclusiveSum(ls.temp, tb, ls.base, d_idx_off, (int64_t)n + 1, s));
+    unpack_positions<<<grid_1d(entries), 256, 0, s>>>(entries, ialt, vb, d_idx_pos);
+    WG_CHECK_LAUNCH("unpack_positions");
+    WG_CUDA(cudaStreamSynchronize(s));
+    h_counts[0] = nvec;
+    h_counts[1] = entries;
+    return WG_OK;
+}
+
+}  // extern "C"
+
+// ===================================================================== K9 ==
+// Input generators.
+namespace {
+
+typedef unsigned __int128 u128;
+
+__device__ __forceinline__ u128 mk128(uint64_t hi, uint64_t lo) { return ((u128)hi << 64) | lo; }
+
+// PCG64 (numpy's PCG64: 128-bit LCG, XSL-RR output, step-then-output).
+__device__ __forceinline__ uint64_t pcg_out(u128 st) {
+    uint64_t x = (uint64_t)(st >> 64) ^ (uint64_t)st;
+    unsigned rot = (unsigned)(st >> 122);
+    return (x >> rot) | (x << ((64 - rot) & 63));
+}
+
+__device__ u128 pcg_advance(u128 state, u128 inc, u128 mult, uint64_t delta) {
+    u128 acc_mult = 1, acc_plus = 0, cur_mult = mult, cur_plus = inc;
+    while (delta) {
+        if (delta & 1) {
+            acc_mult *= cur_mult;
+            acc_plus = acc_plus * cur_mult + cur_plus;
+        }
+        cur_plus = (cur_mult + 1) * cur_plus;
+        cur_mult *= cur_mult;
+        delta >>= 1;
+    }
+    return acc_mult * state + acc_plus;
+}
+
+constexpr int RMAT_EPT = 64;  // edges per thread
+
+__global__ void rmat_kernel(uint32_t scale, uint64_t m, uint64_t shi, uint64_t slo, uint64_t ihi,
+                            uint64_t ilo, double t1, double t2, double t3, uint32_t *src,
+                            uint32_t *dst) {
+    const u128 mult = mk128(0x2360ED051FC65DA4ull, 0x4385DF649FCCF645ull);
+    const u128 inc = mk128(ihi, ilo);
+    for (uint64_t chunk = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; chunk * RMAT_EPT < m;
+         chunk += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t e0 = chunk * RMAT_EPT;
+        uint64_t e1 = e0 + RMAT_EPT < m ? e0 + RMAT_EPT : m;
+        u128 st = pcg_advance(mk128(shi, slo), inc, mult, e0 * scale);
+        for (uint64_t e = e0; e < e1; ++e) {
+            uint32_t s = 0, d = 0;
+            for (uint32_t level = 0; level < scale; ++level) {
+                st = st * mult + inc;
+                double r = (double)(pcg_out(st) >> 11) * (1.0 / 9007199254740992.0);
+                uint32_t q = (r >= t1) + (r >= t2) + (r >= t3);
+                uint32_t sh = scale - 1 - level;
+                s |= (q >> 1) << sh;
+                d |= (q & 1) << sh;
+            }
+            src[e] = s;
+            dst[e] = d;
+        }
+    }
+}
+
+__global__ void edge_keys(uint64_t m, const uint32_t *src, const uint32_t *dst, int drop_loops,
+                          int sym, uint64_t *keys, unsigned long long *count) {
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t s = src[e], d = dst[e];
+        bool loop = s == d;
+        bool keep = !(drop_loops && loop);
+        bool rev = keep && sym && !loop;
+        unsigned want = (keep ? 1u : 0u) + (rev ? 1u : 0u);
+        unsigned mask = __activemask();
+        // warp-aggregated slot reservation
+        unsigned incl = want;
+        for (int off = 1; off < 32; off <<= 1) {
+            unsigned o = __shfl_up_sync(mask, incl, off);
+            if ((int)(threadIdx.x & 31) >= off) incl += o;
+        }
+        // active lanes form a prefix of the warp (grid-stride tail)
+        const int leader = 31 - __clz(mask);
+        unsigned total = __shfl_sync(mask, incl, leader);
+        unsigned long long base = 0;
+        if ((int)(threadIdx.x & 31) == leader) base = atomicAdd(count, (unsigned long long)total);
+        base = __shfl_sync(mask, base, leader);
+        uint64_t pos = base + incl - want;
+        if (keep) keys[pos++] = ((uint64_t)s << 32) | d;
+        if (rev) keys[pos] = ((uint64_t)d << 32) | s;
+    }
+}
+
+__global__ void split_keys(uint64_t m, const uint64_t *keys, uint32_t *src, uint32_t *dst) {
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        src[e] = (uint32_t)(keys[e] >> 32);
+        dst[e] = (uint32_t)keys[e];
+    }
+}
+
+__global__ void weights_kernel(uint64_t m, const uint32_t *src, const uint32_t *dst, uint32_t maxw,
+                               uint32_t *w) {
+    const uint64_t K = 0x9E3779B97F4A7C15ull;
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t h = (((uint64_t)src[e] * K) ^ (uint64_t)dst[e]) * K;
+        w[e] = 1u + (uint32_t)((h >> 48) % maxw);
+    }
+}
+
+__device__ __forceinline__ uint64_t mix64(uint64_t seed, uint64_t u) {
+    uint64_t z = seed ^ (u * 0x9E3779B97F4A7C15ull);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+__global__ void grid_kernel(uint32_t rows, uint32_t cols, uint64_t seed, uint32_t keep_ppm,
+                            uint32_t maxw, uint32_t *src, uint32_t *dst, uint32_t *w,
+                            unsigned long long *count) {
+    uint64_t H = (uint64_t)rows * (cols - 1), V = (uint64_t)(rows - 1) * cols;
+    for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < H + V;
+         u += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t a, b;
+        if (u < H) {
+            uint64_t r = u / (cols - 1), c = u % (cols - 1);
+            a = (uint32_t)(r * cols + c);
+            b = a + 1;
+        } else {
+            uint64_t v = u - H;
+            a = (uint32_t)v;
+            b = (uint32_t)(v + cols);
+        }
+        uint64_t h = mix64(seed, u);
+        if ((uint32_t)(h % 1000000ull) >= keep_ppm) continue;
+        uint32_t wt = 1u + (uint32_t)((h >> 32) % maxw);
+        unsigned long long pos = atomicAdd(count, 2ull);
+        src[pos] = a; dst[pos] = b; w[pos] = wt;
+        src[pos + 1] = b; dst[pos + 1] = a; w[pos + 1] = wt;
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int wg_rmat_edges(uint32_t scale, uint64_t m, uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
+                  uint64_t inc_lo, const double *h_thresholds3, uint32_t *d_src, uint32_t *d_dst,
+                  void *stream) {
+    WG_REQUIRE(scale >= 1 && scale <= 31, "scale must be in [1, 31]");
+    WG_REQUIRE(h_thresholds3 && d_src && d_dst, "null argument");
+    if (m == 0) return WG_OK;
+    cudaStream_t s = as_stream(stream);
+    uint64_t chunks = (m + RMAT_EPT - 1) / RMAT_EPT;
+    unsigned grid = grid_for(chunks, 256, 8);
+    rmat_kernel<<<grid, 256, 0, s>>>(scale, m, state_hi, state_lo, inc_hi, inc_lo, h_thresholds3[0],
+                                     h_thresholds3[1], h_thresholds3[2], d_src, d_dst);
+    WG_CHECK_LAUNCH("rmat");
+    return WG_OK;
+}
+
+size_t wg_canonical_scratch_bytes(uint64_t m) {
+    uint64_t mm = 2 * (m ? m : 1);
+    size_t a = 0, b = 0;
+    cub::DoubleBuffer<uint64_t> kb(nullptr, nullptr);
+    cub::DeviceRadixSort::SortKeys(nullptr, a, kb, (int64_t)mm, 0, 64);
+    cub::DeviceSelect::Unique(nullptr, b, (uint64_t *)nullptr, (uint64_t *)nullptr,
+                              (uint64_t *)nullptr, (int64_t)mm);
+    return 2 * carve_size(mm * 8) + carve_size(64) + carve_size(a > b ? a : b) + 1024;
+}
+
+int wg_canonical_edges(uint64_t m, uint32_t *d_src, uint32_t *d_dst, int drop_loops, int symmetrize,
+                       void *d_scratch, size_t scratch_bytes, uint64_t *h_m_out, void *stream) {
+    WG_REQUIRE(h_m_out, "null argument");
+    *h_m_out = 0;
+    if (m == 0) return WG_OK;
+    WG_REQUIRE(d_src && d_dst && d_scratch, "null argument");
+    cudaStream_t s = as_stream(stream);
+    uint64_t mm = 2 * m;
+    Carve cv{(char *)d_scratch, 0, scratch_bytes};
+    uint64_t *k0 = cv.take<uint64_t>(mm), *k1 = cv.take<uint64_t>(mm);
+    unsigned long long *cnt = cv.take<unsigned long long>(8);
+    size_t a = 0, b = 0;
+    {
+        cub::DoubleBuffer<uint64_t> kb(nullptr, nullptr);
+        cub::DeviceRadixSort::SortKeys(nullptr, a, kb, (int64_t)mm, 0, 64);
+        cub::DeviceSelect::Unique(nullptr, b, (uint64_t *)nullptr, (uint64_t *)nullptr,
+                                  (uint64_t *)nullptr, (int64_t)mm);
+    }
+    size_t tb = a > b ? a : b;
+    void *temp = cv.take<char>(tb);
+    if (!temp) {
+        set_error("canonical scratch too small");
+        return WG_ENOSPACE;
+    }
+    WG_CUDA(cudaMemsetAsync(cnt, 0, 64, s));
+    edge_keys<<<grid_for(m, 256 * 8, 16), 256, 0, s>>>(m, d_src, d_dst, drop_loops, symmetrize, k0, cnt);
+    WG_CHECK_LAUNCH("edge_keys");
+    unsigned long long k = 0;
+    WG_CUDA(cudaMemcpyAsync(&k, cnt, 8, cudaMemcpyDeviceToHost, s));
+    WG_CUDA(cudaStreamSynchronize(s));
+    cub::DoubleBuffer<uint64_t> kb(k0, k1);
+    size_t t = tb;
+    WG_CUDA(cub::DeviceRadixSort::SortKeys(temp, t, kb, (int64_t)k, 0, 64, s));
+    t = tb;
+    WG_CUDA(cub::DeviceSelect::Unique(temp, t, kb.Current(), kb.Alternate(), (uint64_t *)(cnt + 1),
+                                      (int64_t)k, s));
+    unsigned long long u = 0;
+    WG_CUDA(cudaMemcpyAsync(&u, cnt + 1, 8, cudaMemcpyDeviceToHost, s));
+    WG_CUDA(cudaStreamSynchronize(s));
+    WG_REQUIRE(u <= (symmetrize ? 2 * m : m), "internal: unique count");
+    split_keys<<<grid_for(u, 256 * 8, 16), 256, 0, s>>>(u, kb.Alternate(), d_src, d_dst);
+    WG_CHECK_LAUNCH("split_keys");
+    WG_CUDA(cudaStreamSynchronize(s));
+    *h_m_out = u;
+    return WG_OK;
+}
+
+int wg_weights_hash(uint64_t m, const uint32_t *d_src, const uint32_t *d_dst, uint32_t max_weight,
+                    uint32_t *d_w, void *stream) {
+    WG_REQUIRE(max_weight >= 1, "max_weight must be >= 1");
+    if (m == 0) return WG_OK;
+    WG_REQUIRE(d_src && d_dst && d_w, "null argument");
+    weights_kernel<<<grid_for(m, 256 * 8, 16), 256, 0, as_stream(stream)>>>(m, d_src, d_dst,
+                                                                           max_weight, d_w);
+    WG_CHECK_LAUNCH("weights");
+    return WG_OK;
+}
+
+int wg_grid_edges(uint32_t rows, uint32_t cols, uint64_t seed, uint32_t keep_per_million,
+                  uint32_t max_weight, uint32_t *d_src, uint32_t *d_dst, uint32_t *d_w,
+                  uint64_t *d_counter, uint64_t *h_m_out, void *stream) {
+    WG_REQUIRE(rows >= 1 && cols >= 1 && max_weight >= 1, "bad grid arguments");
+    WG_REQUIRE(d_src && d_dst && d_w && d_counter && h_m_out, "null argument");
+    cudaStream_t s = as_stream(stream);
+    WG_CUDA(cudaMemsetAsync(d_counter, 0, 8, s));
+    uint64_t und = (uint64_t)rows * (cols - 1) + (uint64_t)(rows - 1) * cols;
+    if (und) {
+        grid_kernel<<<grid_for(und, 256 * 8, 16), 256, 0, s>>>(
+            rows, cols, seed, keep_per_million, max_weight, d_src, d_dst, d_w,
+            (unsigned long long *)d_counter);
+        WG_CHECK_LAUNCH("grid");
+    }
+    WG_CUDA(cudaMemcpyAsync(h_m_out, d_counter, 8, cudaMemcpyDeviceToHost, s));
+    WG_CUDA(cudaStreamSynchronize(s));
+    return WG_OK;
+}
+
+}  // extern "C"

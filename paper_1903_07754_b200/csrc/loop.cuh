@@ -1,0 +1,49 @@
+// loop.cuh — iteration context shared by every kernel of the device loop.
+//
+// The device-resident loop (engine.py:330-388 restated for the GPU) keeps one
+// wg_iter_rec per iteration in a ring.  Iteration `it` (1-based) consumes the
+// frontier produced by iteration it-1 (list parity (it-1)&1, record
+// (it-1)%ring; iteration 0 is the initial frontier) and produces list it&1.
+// Every kernel re-derives the gate from the previous record, so a batch of
+// enqueued iterations needs no host round trip and iterations after
+// convergence are no-ops.
+#pragma once
+#include "common.cuh"
+
+namespace wg {
+
+enum : int { MODE_NONE = 0, MODE_FULL = 1, MODE_WEDGE = 2 };
+
+struct LoopCtx {
+    wg_iter_rec *recs;
+    uint32_t ring;
+    int32_t forced_mode;    // != 0: per-call kernel (backend protocol), no gate
+    const uint64_t *ctrl;   // device iteration base (graph replay) or null
+    uint64_t it_arg;
+    uint64_t wedge_limit;   // wedge iff edges > 0 and edge_sum < wedge_limit
+    uint64_t edges;
+};
+
+__device__ __forceinline__ uint64_t ctx_iter(const LoopCtx &c) {
+    return c.it_arg + (c.ctrl ? *(volatile const uint64_t *)c.ctrl : 0ull);
+}
+
+// Gate (frontier.py:163-171; engine.py:356-362): the first iteration always
+// runs; afterwards iteration it runs iff the frontier produced by it-1 has
+// out-edges, and uses the Wedge path iff its edge sum is below the limit.
+__device__ __forceinline__ int ctx_mode(const LoopCtx &c, uint64_t it) {
+    if (c.forced_mode) return c.forced_mode;
+    const wg_iter_rec &p = c.recs[(it - 1) % c.ring];
+    uint64_t sum = *(volatile const uint64_t *)&p.out_edge_sum;
+    if (it > 1 && sum == 0) return MODE_NONE;
+    return (c.edges > 0 && sum < c.wedge_limit) ? MODE_WEDGE : MODE_FULL;
+}
+
+__device__ __forceinline__ wg_iter_rec *ctx_out(const LoopCtx &c, uint64_t it) {
+    return &c.recs[it % c.ring];
+}
+__device__ __forceinline__ const wg_iter_rec *ctx_in(const LoopCtx &c, uint64_t it) {
+    return &c.recs[(it - 1) % c.ring];
+}
+
+}  // namespace wg

@@ -1,0 +1,557 @@
+"""Device runtime: the resident pull layout, the device loop driver, the
+per-call kernels of the backend protocol, PageRank and the input generators.
+
+PyTorch is used only as the device-memory / stream provider: every tensor
+here is a raw buffer whose pointer is handed to the C ABI (include/wedge_b200.h).
+uint32 device data is stored in ``torch.int32`` tensors (same bits).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+from fractions import Fraction
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from ._lib import (WG_VAL_I64, WG_VAL_U32, NO_LANE, REC_FIELDS, REC_U64, WgGraph, WgMinPlus,
+                   WgRunBufs, WgRunParams, check)
+
+UNREACHED = 1 << 62  # engine.py:43
+U32_INF = 0xFFFFFFFF
+
+
+def _torch():
+    return _lib.require_cuda()
+
+
+def _ptr(t) -> Optional[int]:
+    return None if t is None else int(t.data_ptr())
+
+
+def to_dev_u32(a, device="cuda"):
+    """numpy / torch integer array -> device int32 tensor holding uint32 bits."""
+    torch = _torch()
+    if isinstance(a, torch.Tensor):
+        if a.dtype == torch.int32:
+            return a.to(device).contiguous()
+        return (a.to(device=device, dtype=torch.int64) & 0xFFFFFFFF).to(torch.int32).contiguous()
+    arr = np.ascontiguousarray(a)
+    if arr.dtype != np.uint32:
+        if arr.size and (arr.min() < 0 or arr.max() > 0xFFFFFFFF):
+            raise ValueError("values do not fit in uint32")
+        arr = arr.astype(np.uint32)
+    return torch.from_numpy(arr.view(np.int32)).to(device)
+
+
+def u32_to_np64(t) -> np.ndarray:
+    """device int32 (uint32 bits) tensor -> host int64 numpy array."""
+    return t.cpu().numpy().view(np.uint32).astype(np.int64)
+
+
+# ---------------------------------------------------------------------------
+# Device graph
+# ---------------------------------------------------------------------------
+class DeviceGraph:
+    """The pull layout resident in HBM: W-lane vectors ordered by (dst, src),
+    their destinations, optional lane weights, the per-source edge index and
+    out-degrees.  Replaces PullTopology + EdgeIndex + out-degrees
+    (graph.py:109-212) on the device."""
+
+    def __init__(self, n, width, edges, nvec, entries, vsrc, vdst, vw, idx_off, idx_pos, outdeg):
+        self.n, self.width, self.edges = int(n), int(width), int(edges)
+        self.nvec, self.entries = int(nvec), int(entries)
+        self.vsrc, self.vdst, self.vw = vsrc, vdst, vw
+        self.idx_off, self.idx_pos, self.outdeg = idx_off, idx_pos, outdeg
+        self._struct = None
+
+    # -- construction ------------------------------------------------------
+    @classmethod
+    def build(cls, n: int, src, dst, weight=None, width: int = 4, stream=None) -> "DeviceGraph":
+        """Build on device from an edge list (graph.py:220-301 via wg_build_layout)."""
+        torch = _torch()
+        L = _lib.load()
+        if width not in (1, 2, 4, 8):
+            raise ValueError(f"vector width must be one of 1, 2, 4, 8 on the B200 engine, got {width}")
+        s = to_dev_u32(src)
+        d = to_dev_u32(dst)
+        w = to_dev_u32(weight) if weight is not None else None
+        m = int(s.numel())
+        if d.numel() != m or (w is not None and w.numel() != m):
+            raise ValueError("src/dst/weight lengths differ")
+        cap = int(L.wg_vector_capacity(m, n, width))
+        dev = s.device
+        vsrc = torch.empty(max(cap * width, 1), dtype=torch.int32, device=dev)
+        vdst = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+        vw = torch.empty(max(cap * width, 1), dtype=torch.int32, device=dev) if w is not None else None
+        idx_off = torch.empty(n + 1, dtype=torch.int64, device=dev)
+        idx_pos = torch.empty(max(m, 1), dtype=torch.int32, device=dev)
+        outdeg = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        scratch = torch.empty(int(L.wg_layout_scratch_bytes(m, n)), dtype=torch.uint8, device=dev)
+        counts = (ctypes.c_uint64 * 2)()
+        check(L.wg_build_layout(n, m, _ptr(s), _ptr(d), _ptr(w), width, cap, _ptr(vsrc), _ptr(vdst),
+                                _ptr(vw), _ptr(idx_off), _ptr(idx_pos), _ptr(outdeg), _ptr(scratch),
+                                scratch.numel(), counts, _lib.stream_ptr(stream)))
+        del scratch
+        nvec, entries = int(counts[0]), int(counts[1])
+        return cls(n, width, m, nvec, entries, vsrc[: max(nvec * width, 1)], vdst[: max(nvec, 1)],
+                   vw[: max(nvec * width, 1)] if vw is not None else None, idx_off,
+                   idx_pos[: max(entries, 1)], outdeg)
+
+    @classmethod
+    def from_reference(cls, topology, index, degrees, device="cuda") -> "DeviceGraph":
+        """Upload a reference-layout PullTopology / EdgeIndex / degrees
+        (int64 host arrays, graph.py:109-212) into the device layout."""
+        torch = _torch()
+        n, width = int(topology.vertex_count), int(topology.vector_width)
+        if width not in (1, 2, 4, 8):
+            raise ValueError(f"vector width {width} is not supported by the B200 engine (1, 2, 4, 8)")
+        nvec = int(topology.vector_count)
+        lane_src = np.asarray(topology.lane_src, dtype=np.int64).reshape(nvec, width)
+        valid = np.asarray(topology.lane_count)[:, None] > np.arange(width)[None, :]
+        vs = np.where(valid, lane_src, NO_LANE).astype(np.uint32)
+        vw = None
+        if topology.lane_weight is not None:
+            lw = np.asarray(topology.lane_weight, dtype=np.int64).reshape(nvec, width)
+            if lw.size and (lw.min() < 0 or lw.max() > 0xFFFFFFFF):
+                raise ValueError("lane weights do not fit in uint32")
+            vw = to_dev_u32(np.where(valid, lw, 0).astype(np.uint32).ravel(), device)
+        deg = np.asarray(degrees, dtype=np.int64)
+        if deg.size and deg.max() > 0xFFFFFFFF:
+            raise ValueError("degrees do not fit in uint32")
+        off = torch.from_numpy(np.ascontiguousarray(index.offsets, dtype=np.int64)).to(device)
+        pos = np.asarray(index.positions, dtype=np.int64)
+        return cls(n, width, int(topology.edge_count), nvec, int(pos.size),
+                   to_dev_u32(vs.ravel() if vs.size else np.zeros(1, np.uint32), device),
+                   to_dev_u32(np.asarray(topology.vec_dst, np.int64) if nvec else np.zeros(1, np.int64), device),
+                   vw, off,
+                   to_dev_u32(pos if pos.size else np.zeros(1, np.int64), device),
+                   to_dev_u32(deg if deg.size else np.zeros(1, np.int64), device))
+
+    def struct(self) -> WgGraph:
+        if self._struct is None:
+            self._struct = WgGraph(self.n, self.width, self.nvec, self.edges, self.entries,
+                                   _ptr(self.vsrc), _ptr(self.vdst), _ptr(self.vw), _ptr(self.idx_off),
+                                   _ptr(self.idx_pos), _ptr(self.outdeg))
+        return self._struct
+
+    def weighted(self) -> bool:
+        return self.vw is not None
+
+    # -- host views in the reference layout (int64) -------------------------
+    def vec_dst_np(self) -> np.ndarray:
+        return u32_to_np64(self.vdst[: self.nvec]) if self.nvec else np.empty(0, np.int64)
+
+    def lanes_np(self):
+        """(lane_src, lane_weight, lane_count) with the reference's zero padding."""
+        W = self.width
+        if self.nvec == 0:
+            e = np.empty((0, W), np.int64)
+            return e, (e.copy() if self.weighted() else None), np.empty(0, np.int64)
+        vs = self.vsrc[: self.nvec * W].cpu().numpy().view(np.uint32).reshape(self.nvec, W)
+        valid = vs != NO_LANE
+        lane_src = np.where(valid, vs.astype(np.int64), 0)
+        lane_w = None
+        if self.weighted():
+            lw = self.vw[: self.nvec * W].cpu().numpy().view(np.uint32).reshape(self.nvec, W)
+            lane_w = np.where(valid, lw.astype(np.int64), 0)
+        return lane_src, lane_w, valid.sum(axis=1).astype(np.int64)
+
+    def offsets_np(self) -> np.ndarray:
+        return self.idx_off.cpu().numpy().astype(np.int64)
+
+    def positions_np(self) -> np.ndarray:
+        return u32_to_np64(self.idx_pos[: self.entries]) if self.entries else np.empty(0, np.int64)
+
+    def outdeg_np(self) -> np.ndarray:
+        return u32_to_np64(self.outdeg[: self.n]) if self.n else np.empty(0, np.int64)
+
+    def memory_bytes(self) -> int:
+        t = [self.vsrc, self.vdst, self.vw, self.idx_off, self.idx_pos, self.outdeg]
+        return sum(x.numel() * x.element_size() for x in t if x is not None)
+
+
+# ---------------------------------------------------------------------------
+# Per-call kernels: the reference backend protocol (kernels.py:55-125)
+# ---------------------------------------------------------------------------
+def _minplus(kern, sentinel) -> WgMinPlus:
+    return WgMinPlus(int(bool(kern.filter_unvisited)), int(bool(kern.use_weight)),
+                     int(kern.apply_increment), int(sentinel))
+
+
+def _workspace(g: DeviceGraph, shift: int):
+    torch = _torch()
+    nbytes = int(_lib.load().wg_kernel_workspace_bytes(ctypes.byref(g.struct()), shift))
+    return torch.empty(max(nbytes, 1), dtype=torch.uint8, device="cuda")
+
+
+def _words_dev(words_u64: np.ndarray, nbits: int):
+    """uint64 LE words (reference Bitmask) -> device uint32 words (same bytes)."""
+    torch = _torch()
+    w = np.ascontiguousarray(words_u64, dtype=np.uint64).view(np.int32)
+    need = (nbits + 31) >> 5
+    out = torch.zeros(max(need, w.size, 1), dtype=torch.int32, device="cuda")
+    if w.size:
+        out[: w.size].copy_(torch.from_numpy(w.copy()))
+    return out
+
+
+def _words_back(dev_words, out_u64: np.ndarray) -> None:
+    host = dev_words.cpu().numpy().view(np.uint32)
+    view = out_u64.view(np.uint32)
+    view[:] = host[: view.size]
+
+
+def pull_call(g: DeviceGraph, prev: np.ndarray, nxt: np.ndarray, out_words: np.ndarray, kern,
+              sentinel: int, wedge_words: Optional[np.ndarray] = None, shift: int = 0) -> int:
+    """Run wg_pull_full / wg_pull_wedge on host int64 buffers (reference
+    semantics, WG_VAL_I64) and write nxt / out_words back in place."""
+    torch = _torch()
+    L = _lib.load()
+    if g.nvec == 0:
+        return 0
+    dprev = torch.from_numpy(np.ascontiguousarray(prev, dtype=np.int64)).cuda()
+    dnxt = torch.from_numpy(np.ascontiguousarray(nxt, dtype=np.int64)).cuda()
+    dout = _words_dev(out_words, g.n)
+    ws = _workspace(g, shift)
+    k = _minplus(kern, sentinel)
+    touched = ctypes.c_uint64(0)
+    st = _lib.stream_ptr()
+    if wedge_words is None:
+        check(L.wg_pull_full(ctypes.byref(g.struct()), WG_VAL_I64, _ptr(dprev), _ptr(dnxt), _ptr(dout),
+                             ctypes.byref(k), _ptr(ws), ws.numel(), ctypes.byref(touched), st))
+    else:
+        groups = (g.nvec + (1 << shift) - 1) >> shift
+        dw = _words_dev(wedge_words, groups)
+        check(L.wg_pull_wedge(ctypes.byref(g.struct()), _ptr(dw), shift, WG_VAL_I64, _ptr(dprev),
+                              _ptr(dnxt), _ptr(dout), ctypes.byref(k), _ptr(ws), ws.numel(),
+                              ctypes.byref(touched), st))
+    nxt[...] = dnxt.cpu().numpy()
+    _words_back(dout, out_words)
+    return int(touched.value)
+
+
+def transform_call(g: DeviceGraph, frontier_words: np.ndarray, shift: int,
+                   wedge_words: np.ndarray) -> int:
+    """wg_transform on host buffers: OR group bits into wedge_words; returns
+    index entries visited (frontier.py:174-209)."""
+    L = _lib.load()
+    groups = (g.nvec + (1 << shift) - 1) >> shift
+    df = _words_dev(frontier_words, g.n)
+    dw = _words_dev(wedge_words, groups)
+    ws = _workspace(g, shift)
+    visited = ctypes.c_uint64(0)
+    check(L.wg_transform(ctypes.byref(g.struct()), _ptr(df), shift, _ptr(dw), _ptr(ws), ws.numel(),
+                         ctypes.byref(visited), _lib.stream_ptr()))
+    _words_back(dw, wedge_words)
+    return int(visited.value)
+
+
+def covered_groups(words_u64: np.ndarray, group_count: int) -> np.ndarray:
+    """Ascending set group ids (device compaction, K4)."""
+    torch = _torch()
+    L = _lib.load()
+    if group_count == 0:
+        return np.empty(0, np.int64)
+    dw = _words_dev(words_u64, group_count)
+    out = torch.empty(group_count, dtype=torch.int32, device="cuda")
+    ws = torch.empty(4096 + 16 * ((group_count >> 15) + 2) + 1024, dtype=torch.uint8, device="cuda")
+    cnt = ctypes.c_uint64(0)
+    check(L.wg_covered_groups(_ptr(dw), group_count, _ptr(out), _ptr(ws), ws.numel(),
+                              ctypes.byref(cnt), _lib.stream_ptr()))
+    return u32_to_np64(out[: cnt.value]) if cnt.value else np.empty(0, np.int64)
+
+
+# ---------------------------------------------------------------------------
+# Device-resident convergence loop (engine.py:330-388)
+# ---------------------------------------------------------------------------
+MODE_NAMES = {1: "FullScan", 2: "Wedge"}
+
+
+@dataclass
+class IterRecord:
+    iteration: int
+    mode: str
+    active_edges: int
+    vectors_touched: int
+    frontier_out_size: int
+    covered_vectors: int
+    transform_entries: int
+
+
+@dataclass
+class LoopResult:
+    values: object            # device tensor (int32 bits of uint32, or int64)
+    val_type: int
+    records: list = field(default_factory=list)
+    converged: bool = False
+
+    def values_int64(self) -> np.ndarray:
+        """Final values in the reference encoding (int64, UNREACHED sentinel)."""
+        return values_to_int64(self.values, self.val_type)
+
+
+def values_to_int64(t, val_type: int) -> np.ndarray:
+    if val_type == WG_VAL_I64:
+        return t.cpu().numpy().astype(np.int64)
+    v = t.cpu().numpy().view(np.uint32).astype(np.int64)
+    v[v == U32_INF] = UNREACHED
+    return v
+
+
+def wedge_limit(threshold: Fraction, edges: int) -> int:
+    """Smallest edge sum that is NOT below the threshold share:
+    sum*den < num*E  <=>  sum < ceil(num*E/den) (frontier.py:163-171)."""
+    num, den = threshold.numerator, threshold.denominator
+    return -((-num * edges) // den)
+
+
+class DeviceLoop:
+    """Buffers and host driver of the device loop for one graph / precision.
+
+    The host enqueues batches of iterations (wg_run_enqueue); every kernel
+    re-derives the gate and convergence from the previous iteration's device
+    record, so the host only reads the records after each batch.
+    """
+
+    def __init__(self, g: DeviceGraph, shift: int, val_type: int = WG_VAL_U32, ring: int = 1024):
+        torch = _torch()
+        self.g, self.shift, self.val_type, self.ring = g, int(shift), int(val_type), int(ring)
+        L = _lib.load()
+        sizes = (ctypes.c_uint64 * 4)()
+        check(L.wg_run_buffer_sizes(ctypes.byref(g.struct()), self.shift, sizes))
+        fwords, groups, gwords, nbc = (int(x) for x in sizes)
+        n = max(g.n, 1)
+        dt = torch.int32 if self.val_type == WG_VAL_U32 else torch.int64
+        dev = "cuda"
+        self.vals = [torch.empty(n, dtype=dt, device=dev) for _ in range(2)]
+        self.fbits = [torch.zeros(max(fwords, 1), dtype=torch.int32, device=dev) for _ in range(2)]
+        self.fvert = [torch.empty(n, dtype=torch.int32, device=dev) for _ in range(2)]
+        self.fpref = [torch.empty(n, dtype=torch.int32, device=dev) for _ in range(2)]
+        self.gbits = torch.zeros(max(gwords, 1), dtype=torch.int32, device=dev)
+        self.glist = torch.empty(max(groups, 1), dtype=torch.int32, device=dev)
+        self.bcount = torch.empty(max(nbc, 1), dtype=torch.int64, device=dev)
+        self.recs = torch.zeros(self.ring * REC_U64, dtype=torch.int64, device=dev)
+        self.ctrl = torch.zeros(4, dtype=torch.int64, device=dev)
+        self.host_recs = torch.zeros(self.ring * REC_U64, dtype=torch.int64).pin_memory()
+        b = WgRunBufs()
+        for i in range(2):
+            b.vals[i] = _ptr(self.vals[i])
+            b.fbits[i] = _ptr(self.fbits[i])
+            b.fvert[i] = _ptr(self.fvert[i])
+            b.fpref[i] = _ptr(self.fpref[i])
+        b.gbits, b.glist, b.bcount = _ptr(self.gbits), _ptr(self.glist), _ptr(self.bcount)
+        b.recs, b.ctrl, b.ring = _ptr(self.recs), _ptr(self.ctrl), self.ring
+        self.bufs = b
+        self.graph_cache = {}
+
+    def params(self, kern, threshold: Fraction) -> WgRunParams:
+        p = WgRunParams()
+        p.val_type = self.val_type
+        p.shift = self.shift
+        p.kern = _minplus(kern, UNREACHED)
+        p.wedge_limit = wedge_limit(threshold, self.g.edges) if self.g.edges > 0 else 0
+        return p
+
+    def seed(self, init_values, init_words, kern, threshold, stream=None) -> WgRunParams:
+        """Write both value buffers and build iteration 0 from the frontier bitmap."""
+        for v in self.vals:
+            v.copy_(init_values)
+        p = self.params(kern, threshold)
+        check(_lib.load().wg_run_init(ctypes.byref(self.g.struct()), ctypes.byref(self.bufs),
+                                      ctypes.byref(p), _ptr(init_words), _lib.stream_ptr(stream)))
+        return p
+
+    def enqueue(self, p: WgRunParams, it_begin: int, count: int, stream=None) -> None:
+        check(_lib.load().wg_run_enqueue(ctypes.byref(self.g.struct()), ctypes.byref(self.bufs),
+                                         ctypes.byref(p), it_begin, count, _lib.stream_ptr(stream)))
+
+    def _read(self, it_begin: int, count: int, stream=None):
+        torch = _torch()
+        s = stream or torch.cuda.current_stream()
+        lo = it_begin % self.ring
+        hi = lo + count
+        if hi <= self.ring:
+            self.host_recs[lo * REC_U64: hi * REC_U64].copy_(self.recs[lo * REC_U64: hi * REC_U64],
+                                                             non_blocking=True)
+        else:
+            self.host_recs.copy_(self.recs, non_blocking=True)
+        s.synchronize()
+        arr = self.host_recs.numpy().view(np.uint64).reshape(self.ring, REC_U64)
+        return [arr[(it_begin + j) % self.ring] for j in range(count)]
+
+    def drive(self, p: WgRunParams, max_iterations: int, trace=None, stream=None):
+        """Enqueue batches until convergence or the cap; returns (records, converged, last_it)."""
+        records: list[IterRecord] = []
+        converged = False
+        it, batch, last = 1, 2, 0
+        cap_batch = min(256, self.ring - 2)
+        while it <= max_iterations and not converged:
+            cnt = 1 if trace is not None else min(batch, max_iterations - it + 1)
+            self.enqueue(p, it, cnt, stream)
+            rows = self._read(it, cnt, stream)
+            for j, r in enumerate(rows):
+                mode = int(r[0])
+                if mode == 0:
+                    converged = True
+                    break
+                if int(r[10]):
+                    raise _lib.OverflowError32(_lib.WG_EOVERFLOW, "uint32 value overflow in device loop")
+                records.append(IterRecord(it + j, MODE_NAMES[mode], int(r[1]), int(r[2]), int(r[3]),
+                                          int(r[7]) if mode == 2 else 0, int(r[8]) if mode == 2 else 0))
+                last = it + j
+                if trace is not None:
+                    trace(self, last)
+                if int(r[4]) == 0:
+                    converged = True
+                    break
+            it += cnt
+            batch = min(batch * 2, cap_batch)
+        return records, converged, last
+
+    def frontier_members(self, it: int) -> np.ndarray:
+        """Sorted members of the frontier produced by iteration it (trace mode)."""
+        arr = self.host_recs.numpy().view(np.uint64).reshape(self.ring, REC_U64)[it % self.ring]
+        nz, z = int(arr[5]) >> 32, int(arr[6])
+        lst = self.fvert[it & 1]
+        parts = []
+        if nz:
+            parts.append(u32_to_np64(lst[:nz]))
+        if z:
+            parts.append(u32_to_np64(lst[self.g.n - z:]))
+        return np.sort(np.concatenate(parts)) if parts else np.empty(0, np.int64)
+
+    def values_after(self, it: int):
+        return self.vals[it & 1]
+
+
+def initial_words(n: int, members: np.ndarray):
+    """Device uint32 bitmap of the initial frontier."""
+    torch = _torch()
+    words = np.zeros(max((n + 31) >> 5, 1), np.uint32)
+    m = np.unique(np.asarray(members, dtype=np.int64))
+    if m.size:
+        if m.min() < 0 or m.max() >= n:
+            raise IndexError("bit position out of range")
+        np.bitwise_or.at(words, m >> 5, (np.uint32(1) << (m & 31).astype(np.uint32)))
+    return torch.from_numpy(words.view(np.int32)).cuda()
+
+
+def all_words(n: int):
+    torch = _torch()
+    words = torch.full((max((n + 31) >> 5, 1),), -1, dtype=torch.int32, device="cuda")
+    return words
+
+
+def encode_values(values: np.ndarray, val_type: int):
+    """Reference int64 values -> device buffer of `val_type` (UNREACHED <-> 0xFFFFFFFF)."""
+    torch = _torch()
+    v = np.asarray(values, dtype=np.int64)
+    if val_type == WG_VAL_I64:
+        return torch.from_numpy(np.ascontiguousarray(v)).cuda()
+    u = np.where(v == UNREACHED, U32_INF, v)
+    if u.size and (u.min() < 0 or u.max() > U32_INF):
+        raise ValueError("values do not fit the uint32 encoding")
+    if u.size and np.any((u == U32_INF) & (v != UNREACHED)):
+        raise ValueError("value 0xFFFFFFFF collides with the uint32 sentinel")
+    return torch.from_numpy(u.astype(np.uint32).view(np.int32)).cuda()
+
+
+def fits_u32(values: np.ndarray, kern, g: DeviceGraph) -> bool:
+    """Conservative check that the uint32 encoding cannot lose information
+    before the device overflow flag would catch it."""
+    v = np.asarray(values, dtype=np.int64)
+    fin = v[v != UNREACHED]
+    return not fin.size or (fin.min() >= 0 and fin.max() < U32_INF)
+
+
+# ---------------------------------------------------------------------------
+# PageRank (K8)
+# ---------------------------------------------------------------------------
+def pagerank(g: DeviceGraph, iterations: int = 20, damping: float = 0.85, stream=None, bufs=None):
+    torch = _torch()
+    n = max(g.n, 1)
+    if bufs is None:
+        bufs = (torch.empty(n, dtype=torch.float32, device="cuda"),
+                torch.empty(n, dtype=torch.float32, device="cuda"),
+                torch.empty(n, dtype=torch.float32, device="cuda"),
+                torch.zeros(4, dtype=torch.float64, device="cuda"))
+    rank, acc, contrib, scal = bufs
+    check(_lib.load().wg_pagerank(ctypes.byref(g.struct()), int(iterations), float(damping),
+                                  _ptr(rank), _ptr(acc), _ptr(contrib), _ptr(scal),
+                                  _lib.stream_ptr(stream)))
+    return rank
+
+
+# ---------------------------------------------------------------------------
+# Generators (graph_io.py:87-221, K9)
+# ---------------------------------------------------------------------------
+RMAT_PROBS = (0.57, 0.19, 0.19, 0.05)
+
+
+def rmat_edges(scale: int, edge_factor: int, seed: int = 1, probs=RMAT_PROBS, stream=None):
+    """Bit-identical to graph_io._generate_rmat: numpy PCG64(seed) stream,
+    draws (m, scale) row-major, quadrant thresholds a, a+b, a+b+c."""
+    torch = _torch()
+    n = 1 << scale
+    m = edge_factor * n
+    st = np.random.PCG64(seed).state["state"]
+    state, inc = int(st["state"]), int(st["inc"])
+    a, b, c, _ = probs
+    th = (ctypes.c_double * 3)(a, a + b, a + b + c)
+    src = torch.empty(m, dtype=torch.int32, device="cuda")
+    dst = torch.empty(m, dtype=torch.int32, device="cuda")
+    M = (1 << 64) - 1
+    check(_lib.load().wg_rmat_edges(scale, m, state >> 64, state & M, inc >> 64, inc & M, th,
+                                    _ptr(src), _ptr(dst), _lib.stream_ptr(stream)))
+    return n, src, dst
+
+
+def canonical_edges(src, dst, drop_loops: bool, symmetrize: bool, stream=None):
+    """Sorted (src, dst)-unique edge list; optional self-loop removal and
+    symmetrisation (graph_io.py:87-112 with dedup)."""
+    torch = _torch()
+    L = _lib.load()
+    m = int(src.numel())
+    cap = 2 * m if symmetrize else m
+    s = torch.empty(max(cap, 1), dtype=torch.int32, device="cuda")
+    d = torch.empty(max(cap, 1), dtype=torch.int32, device="cuda")
+    s[:m].copy_(src)
+    d[:m].copy_(dst)
+    scratch = torch.empty(int(L.wg_canonical_scratch_bytes(m)), dtype=torch.uint8, device="cuda")
+    out = ctypes.c_uint64(0)
+    check(L.wg_canonical_edges(m, _ptr(s), _ptr(d), int(drop_loops), int(symmetrize), _ptr(scratch),
+                               scratch.numel(), ctypes.byref(out), _lib.stream_ptr(stream)))
+    k = int(out.value)
+    return s[:k].clone(), d[:k].clone()
+
+
+def weights_hash(src, dst, max_weight: int, stream=None):
+    torch = _torch()
+    m = int(src.numel())
+    w = torch.empty(max(m, 1), dtype=torch.int32, device="cuda")
+    check(_lib.load().wg_weights_hash(m, _ptr(src), _ptr(dst), int(max_weight), _ptr(w),
+                                      _lib.stream_ptr(stream)))
+    return w[:m]
+
+
+def grid_edges(rows: int, cols: int, seed: int, keep: float = 0.9, max_weight: int = 1000, stream=None):
+    """4-neighbour grid, each undirected edge kept with probability `keep`,
+    symmetric weight uniform in [1, max_weight] (BASELINE config 3; the
+    reference has no such generator, so the stream is defined here and
+    restated in oracle.grid_edges)."""
+    torch = _torch()
+    und = rows * (cols - 1) + (rows - 1) * cols
+    cap = max(2 * und, 1)
+    s = torch.empty(cap, dtype=torch.int32, device="cuda")
+    d = torch.empty(cap, dtype=torch.int32, device="cuda")
+    w = torch.empty(cap, dtype=torch.int32, device="cuda")
+    ctr = torch.zeros(1, dtype=torch.int64, device="cuda")
+    out = ctypes.c_uint64(0)
+    check(_lib.load().wg_grid_edges(rows, cols, int(seed), int(round(keep * 1_000_000)), int(max_weight),
+                                    _ptr(s), _ptr(d), _ptr(w), _ptr(ctr), ctypes.byref(out),
+                                    _lib.stream_ptr(stream)))
+    k = int(out.value)
+    return rows * cols, s[:k], d[:k], w[:k]

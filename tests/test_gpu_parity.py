@@ -1,0 +1,294 @@
+"""GPU parity: the sm_100a kernels behind the C ABI against the reference's
+own outputs (golden fixtures) and the CPU oracle.  Bit-exact for every
+integer result.  Marked gpu."""
+
+from __future__ import annotations
+
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import GT_EDGES, GT_VERTICES
+
+pytestmark = pytest.mark.gpu
+
+UNREACHED = oracle.UNREACHED
+
+
+@pytest.fixture(scope="module")
+def wg():
+    import paper_1903_07754_b200 as wg
+    return wg
+
+
+def _graph(wg, n, src, dst, w, width):
+    return wg.build_pull_topology(wg.EdgeList(n, src, dst, w), width)
+
+
+# --------------------------------------------------------------- layout ---
+def test_device_layout_matches_reference(wg, golden):
+    z = golden.npz("layout")
+    for c in golden.meta("layout"):
+        nm = c["name"]
+        w = z[f"{nm}/w"] if c["weighted"] else None
+        topo = _graph(wg, c["n"], z[f"{nm}/src"], z[f"{nm}/dst"], w, c["width"])
+        assert np.array_equal(topo.vec_dst, z[f"{nm}/vec_dst"]), nm
+        assert np.array_equal(topo.lane_src, z[f"{nm}/lane_src"]), nm
+        assert np.array_equal(topo.lane_count, z[f"{nm}/lane_count"]), nm
+        if c["weighted"]:
+            assert np.array_equal(topo.lane_weight, z[f"{nm}/lane_weight"]), nm
+        idx = wg.build_edge_index(topo)
+        assert np.array_equal(idx.offsets, z[f"{nm}/offsets"]), nm
+        assert np.array_equal(idx.positions, z[f"{nm}/positions"]), nm
+        assert np.array_equal(topo.device.outdeg_np(), z[f"{nm}/degrees"]), nm
+
+
+def test_device_layout_edge_cases(wg):
+    # empty graph, isolated vertices, all edges into one hub (multi-warp run)
+    t = _graph(wg, 3, [], [], None, 4)
+    assert t.vector_count == 0 and wg.build_edge_index(t).offsets.tolist() == [0, 0, 0, 0]
+    hub = 5000
+    src = np.arange(1, hub + 1)
+    dst = np.zeros(hub, np.int64)
+    t = _graph(wg, hub + 1, src, dst, None, 4)
+    ref = oracle.build_pull_topology(hub + 1, src, dst, None, 4)
+    assert np.array_equal(t.vec_dst, ref.vec_dst) and np.array_equal(t.lane_src, ref.lane_src)
+    # duplicates and self-loops are processed like any edge (graph.py:36-41)
+    src = [0, 0, 1, 1, 2, 2, 2]
+    dst = [1, 1, 1, 2, 2, 0, 0]
+    t = _graph(wg, 3, src, dst, [5, 3, 1, 1, 1, 2, 7], 2)
+    ref = oracle.build_pull_topology(3, src, dst, [5, 3, 1, 1, 1, 2, 7], 2)
+    assert np.array_equal(t.lane_weight, ref.lane_weight) and np.array_equal(t.lane_src, ref.lane_src)
+    ri = oracle.build_edge_index(ref)
+    assert np.array_equal(wg.build_edge_index(t).positions, ri.positions)
+
+
+# ------------------------------------------------- backend protocol (Tier 1)
+@pytest.mark.parametrize("kind", ["pull_full", "pull_wedge", "transform"])
+def test_backend_protocol_bit_exact(wg, golden, kind):
+    """Every golden case of pkg/tests/test_kernels_backends.py:24-94 style,
+    through B200Backend on a reference-layout topology (as the unmodified
+    reference engine would call it)."""
+    be = wg.B200Backend()
+    for c in (c for c in golden.meta("kernels") if c["kind"] == kind):
+        g = golden.kernel_case(c)
+        n, width = c["n"], c["width"]
+        topo = oracle.build_pull_topology(n, g["src"], g["dst"], g["w"], width)
+        if kind == "transform":
+            idx = oracle.build_edge_index(topo)
+            ww = np.zeros_like(g["wedge"])
+            v = be.transform(g["frontier"], n, idx.offsets, idx.positions, c["shift"], ww, 16, 1)
+            assert v == c["visited"], c["id"]
+            assert np.array_equal(ww, g["wedge"]), c["id"]
+            continue
+        kern = oracle.kern_of(c["app"])
+        prev = g["prev"].copy()
+        nxt = prev.copy()
+        out = np.zeros_like(g["out"])
+        if kind == "pull_full":
+            t = be.pull_full(topo, prev, nxt, out, kern, UNREACHED, 1)
+        else:
+            t = be.pull_wedge(topo, g["wedge"], c["shift"], c["groups"], prev, nxt, out, kern, UNREACHED, 1)
+        assert t == c["touched"], c["id"]
+        assert np.array_equal(nxt, g["nxt"]), c["id"]
+        assert np.array_equal(out, g["out"]), c["id"]
+
+
+def test_backend_protocol_random_states_vs_oracle(wg):
+    """Larger random graphs and states: B200Backend == oracle, all W, shifts."""
+    be = wg.B200Backend()
+    port = oracle.PortBackend(4)
+    rng = np.random.default_rng(123)
+    for trial in range(6):
+        n = int(rng.integers(500, 5000))
+        m = int(rng.integers(1000, 60000))
+        src = rng.integers(0, n, m)
+        dst = np.minimum((rng.pareto(0.8, m) * 5).astype(np.int64), n - 1) if trial % 2 else rng.integers(0, n, m)
+        w = rng.integers(1, 1000, m)
+        for width in (1, 2, 4, 8):
+            topo = oracle.build_pull_topology(n, src, dst, w, width)
+            idx = oracle.build_edge_index(topo)
+            for app in ("bfs", "cc", "sssp"):
+                kern = oracle.kern_of(app)
+                prev = rng.integers(0, n + 2, n).astype(np.int64)
+                prev[rng.random(n) < 0.3] = UNREACHED
+                a_n, b_n = prev.copy(), prev.copy()
+                a_o = np.zeros((n + 63) // 64, np.uint64)
+                b_o = a_o.copy()
+                ta = be.pull_full(topo, prev, a_n, a_o, kern, UNREACHED)
+                tb = port.pull_full(topo, prev, b_n, b_o, kern, UNREACHED)
+                assert ta == tb and np.array_equal(a_n, b_n) and np.array_equal(a_o, b_o)
+                for shift in (0, 2, 3):
+                    groups = (topo.vector_count + (1 << shift) - 1) >> shift
+                    ww = np.zeros((groups + 63) // 64, np.uint64)
+                    members = rng.choice(n, size=int(rng.integers(1, n // 4 + 2)), replace=False)
+                    fw = np.zeros((n + 63) // 64, np.uint64)
+                    oracle.set_bits(fw, members)
+                    ww2 = ww.copy()
+                    va = be.transform(fw, n, idx.offsets, idx.positions, shift, ww, 4096, 1)
+                    vb = port.transform(fw, n, idx.offsets, idx.positions, shift, ww2, 4096, 1)
+                    assert va == vb and np.array_equal(ww, ww2)
+                    a_n, b_n = prev.copy(), prev.copy()
+                    a_o[:] = 0
+                    b_o[:] = 0
+                    ta = be.pull_wedge(topo, ww, shift, groups, prev, a_n, a_o, kern, UNREACHED)
+                    tb = port.pull_wedge(topo, ww, shift, groups, prev, b_n, b_o, kern, UNREACHED)
+                    assert ta == tb and np.array_equal(a_n, b_n) and np.array_equal(a_o, b_o)
+
+
+# ------------------------------------------------------ engine (Tier 2) ---
+def _prep(wg, scale, app, width):
+    el = wg.generate(wg.GenSpec("rmat", scale=scale, edge_factor=16, seed=1))
+    el = wg.drop_self_loops_dedup(el, symmetric=True)
+    if app == "sssp":
+        el = wg.synthesize_weights(el, 255)
+    topo = wg.build_pull_topology(el, width)
+    return el, topo, wg.build_edge_index(topo), wg.compute_out_degrees(el)
+
+
+def test_device_loop_matches_reference_runs(wg, golden):
+    """Digest + every per-iteration stat (incl. work counters at equal W/vpg)
+    + per-iteration frontiers, for all golden runs (RMAT s8-s12)."""
+    zr = golden.npz("runs")
+    cache = {}
+    for r in golden.meta("runs"):
+        key = (r["scale"], r["app"], r["width"])
+        if key not in cache:
+            cache[key] = _prep(wg, r["scale"], r["app"], r["width"])
+        el, topo, idx, deg = cache[key]
+        assert el.edge_count == r["E"]
+        prog = wg.make_program(r["app"], None if r["app"] == "cc" else r["root"])
+        cfg = wg.EngineConfig(threshold=wg.FullnessThreshold(Fraction(*r["thr"])),
+                              precision=wg.FrontierPrecision(r["vpg"]), max_iterations=100000)
+        flog = [] if r["scale"] <= 10 else None
+        res = wg.run_until_convergence(topo, idx, prog, deg, cfg, frontier_log=flog)
+        assert wg.result_digest(res.values) == r["digest"], r["name"]
+        got = [[s.iteration, s.mode, s.active_edges, s.vectors_touched, s.frontier_out_size,
+                s.covered_vectors, s.transform_entries] for s in res.stats]
+        assert got == r["stats"], r["name"]
+        assert res.converged == r["converged"]
+        if flog is not None:
+            assert [len(f) for f in flog] == zr[f"{r['name']}/flog_len"].tolist(), r["name"]
+            cat = np.concatenate(flog) if flog else np.empty(0, np.int64)
+            assert np.array_equal(cat, zr[f"{r['name']}/flog"]), r["name"]
+
+
+def test_engine_known_answers(wg):
+    """pkg/tests/test_engine.py:138-197 known answers on the device loop."""
+    def built(edges, n, width=2):
+        el = wg.EdgeList.from_pairs(edges, n)
+        t = wg.build_pull_topology(el, width)
+        return t, wg.build_edge_index(t), wg.compute_out_degrees(el)
+
+    def cfg(threshold="0.2", vpg=1, max_iterations=200):
+        return wg.EngineConfig(threshold=wg.FullnessThreshold.of(threshold),
+                               precision=wg.FrontierPrecision(vpg), max_iterations=max_iterations)
+
+    t, i, d = built(GT_EDGES, GT_VERTICES)
+    r = wg.run_until_convergence(t, i, wg.bfs_program(0), d, cfg(threshold=1, vpg=1))
+    assert r.values.tolist() == [0, 1, 1, 2, 3, 4] and r.converged
+    assert r.stats[-1].frontier_out_size == 0 and all(s.mode == "Wedge" for s in r.stats)
+    t, i, d = built([(0, 1), (1, 0), (2, 3), (3, 2)], 4)
+    assert wg.run_until_convergence(t, i, wg.cc_program(), d, cfg()).values.tolist() == [0, 0, 2, 2]
+    t, i, d = built([(0, 1, 5), (1, 2, 3)], 3)
+    assert wg.run_until_convergence(t, i, wg.sssp_program(0), d, cfg()).values.tolist() == [0, 5, 8]
+    t, i, d = built([(0, 1, 1), (0, 2, 4), (1, 2, 1)], 3)
+    assert wg.run_until_convergence(t, i, wg.sssp_program(0), d, cfg()).values[2] == 2
+    t, i, d = built([(0, 1), (1, 2), (2, 3)], 4)
+    r = wg.run_until_convergence(t, i, wg.bfs_program(0), d, cfg(max_iterations=1))
+    assert not r.converged and r.iterations == 1
+    t, i, d = built([], 1)
+    r = wg.run_until_convergence(t, i, wg.bfs_program(0), d, cfg())
+    assert r.values.tolist() == [0] and r.iterations == 1 and r.converged
+    t, i, d = built([(0, 1)], 2)
+    r = wg.run_until_convergence(t, i, wg.bfs_program(1), d, cfg())
+    assert r.values.tolist() == [UNREACHED, 0] and r.converged
+
+
+def test_per_iteration_api_known_answers(wg):
+    """pkg/tests/test_engine.py:58-130 through run_iteration_full/wedge."""
+    el = wg.EdgeList.from_pairs(GT_EDGES, GT_VERTICES)
+    t = wg.build_pull_topology(el, 2)
+    i = wg.build_edge_index(t)
+    d = wg.compute_out_degrees(el)
+    buf = wg.ValueBuffers(np.array([0] + [UNREACHED] * 5), np.array([0] + [UNREACHED] * 5))
+    fr, st = wg.run_iteration_full(t, buf, wg.bfs_program(0), d)
+    assert buf.next.tolist() == [0, 1, 1, UNREACHED, UNREACHED, UNREACHED]
+    assert fr.members().tolist() == [1, 2] and st.vectors_touched == t.vector_count
+    buf = wg.ValueBuffers(np.array([0, 1, 1] + [UNREACHED] * 3), np.array([0, 1, 1] + [UNREACHED] * 3))
+    _, st = wg.run_iteration_full(t, buf, wg.bfs_program(0), d)
+    assert st.vectors_touched == t.vector_count - 2
+    wedge = wg.WedgeFrontier.from_groups([0, 1], t.vector_count, wg.FrontierPrecision(1))
+    buf = wg.ValueBuffers(np.array([0] + [UNREACHED] * 5), np.array([0] + [UNREACHED] * 5))
+    fr, st = wg.run_iteration_wedge(t, wedge, buf, wg.bfs_program(0), d)
+    assert buf.next.tolist() == [0, 1, 1, UNREACHED, UNREACHED, UNREACHED] and st.vectors_touched == 2
+    f = wg.VertexFrontier.from_vertices([5], d, GT_VERTICES)
+    w = wg.transform_frontier(f, i, wg.FrontierPrecision(4))
+    assert w.bits.indices().tolist() == [0]
+    f = wg.VertexFrontier.from_vertices([1, 2], d, GT_VERTICES)
+    w = wg.transform_frontier(f, i, wg.FrontierPrecision(1))
+    assert w.bits.indices().tolist() == [2] and w.entries_visited == 2
+    f = wg.VertexFrontier.from_vertices([0], d, GT_VERTICES)
+    assert wg.transform_frontier(f, i, wg.FrontierPrecision(1)).bits.indices().tolist() == [0, 1]
+    assert wg.transform_frontier(f, i, wg.FrontierPrecision(2)).bits.indices().tolist() == [0]
+    w = wg.WedgeFrontier.from_groups([2], 5, wg.FrontierPrecision(2))
+    assert wg.wedge_covered_vectors(w, 5).tolist() == [4]
+
+
+def test_generators_bit_identical(wg, golden):
+    z = golden.npz("gen")
+    el = wg.generate(wg.GenSpec("rmat", scale=8, edge_factor=16, seed=1))
+    assert np.array_equal(el.src, z["rmat8_src"]) and np.array_equal(el.dst, z["rmat8_dst"])
+    el = wg.generate(wg.GenSpec("rmat", scale=11, edge_factor=4, seed=7))
+    assert np.array_equal(el.src, z["rmat11_s7_src"]) and np.array_equal(el.dst, z["rmat11_s7_dst"])
+    sym = wg.drop_self_loops_dedup(el, symmetric=True)
+    assert np.array_equal(sym.src, z["rmat11_s7_sym_src"]) and np.array_equal(sym.dst, z["rmat11_s7_sym_dst"])
+    wt = wg.synthesize_weights(sym, 255)
+    assert np.array_equal(wt.weight, z["rmat11_s7_sym_w255"])
+    h = wg.synthesize_weights(wg.EdgeList(1 << 26, z["hash_src"], z["hash_dst"]), 1000)
+    assert np.array_equal(h.weight, z["hash_w1000"])
+
+
+def test_grid_generator_matches_oracle(wg):
+    el = wg.grid_graph(37, 53, seed=2)
+    n, s, d, w = oracle.grid_edges(37, 53, seed=2)
+    a = np.lexsort((el.dst, el.src))
+    b = np.lexsort((d, s))
+    assert np.array_equal(el.src[a], s[b]) and np.array_equal(el.dst[a], d[b])
+    assert np.array_equal(el.weight[a], w[b])
+
+
+def test_pagerank_within_tolerance(wg):
+    """|r_gpu - r_cpu| <= 1e-6 per vertex (north_star), float64 oracle."""
+    for scale, ef, seed in ((10, 8, 1), (14, 16, 2)):
+        el = wg.generate(wg.GenSpec("rmat", scale=scale, edge_factor=ef, seed=seed))
+        el = wg.drop_self_loops_dedup(el, symmetric=False)
+        topo = wg.build_pull_topology(el, 4)
+        r = wg.pagerank(topo, 20, 0.85)
+        ref = oracle.pagerank_numpy(el.vertex_count, el.src, el.dst, 20, 0.85)
+        assert np.max(np.abs(r.astype(np.float64) - ref)) <= 1e-6
+        assert abs(float(r.astype(np.float64).sum()) - 1.0) < 1e-4
+
+
+def test_survey_digests_s16(wg):
+    """Reference digests frozen in SURVEY §8(c) at RMAT s16 (BFS/CC/SSSP)."""
+    want = {"bfs": ("591673cb243fad4e", 5), "cc": ("42bbdb18405bc729", 5), "sssp": ("7d2c2554722fbf74", 11)}
+    defaults = {"bfs": (8, "0.01"), "cc": (4, "0.2"), "sssp": (4, "0.2")}
+    for app, (dig, iters) in want.items():
+        el, topo, idx, deg = _prep(wg, 16, app, 4)
+        vpg, thr = defaults[app]
+        cfg = wg.EngineConfig(threshold=wg.FullnessThreshold.of(thr), precision=wg.FrontierPrecision(vpg))
+        res = wg.run_until_convergence(topo, idx, wg.make_program(app, None if app == "cc" else 0), deg, cfg)
+        assert wg.result_digest(res.values) == dig, app
+        assert res.iterations == iters, app
+
+
+def test_u32_overflow_falls_back_exactly(wg):
+    """Values beyond uint32 take the exact int64 device path."""
+    el = wg.EdgeList(3, [0, 1], [1, 2], [4_000_000_000, 4_000_000_000])
+    t = wg.build_pull_topology(el, 4)
+    r = wg.run_until_convergence(t, wg.build_edge_index(t), wg.sssp_program(0), wg.compute_out_degrees(el),
+                                 wg.EngineConfig())
+    assert r.values.tolist() == [0, 4_000_000_000, 8_000_000_000]
