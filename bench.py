@@ -1,0 +1,531 @@
+"""Benchmark of the B200 Wedge-Frontier pull engine (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--workload cc22|bfs16|sssp_grid|pr25|bfs26|sssp26]
+
+Default workload (BASELINE.json configs[1], the metric's reference config):
+Connected Components on RMAT scale 22, edge factor 16, (a,b,c,d) =
+(.57,.19,.19,.05), seed 1, self-loops removed, symmetrised + de-duplicated,
+W=4 vectors, Wedge precision 4 vectors/bit, fullness threshold 1/5 (the
+reference CLI defaults, cli.py:52-56).  Inputs are generated on the device with
+the reference's own PCG64 stream (bit-identical, tests/test_gpu_parity.py).
+
+A step = one run to convergence (time-to-solution, TTS) with the graph
+resident in HBM; value = GTEPS = |E| / TTS.  The graph (>= 600 MB) is larger
+than the 126 MB L2 and L2 is additionally flushed (256 MB write) between
+timed steps.  e2e = the same run through the C ABI with the layout in pinned
+host memory: H2D of the layout + loop + D2H of the labels, per step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from fractions import Fraction
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+WORKLOADS = {
+    "cc22": dict(app="cc", scale=22, ef=16, sym=True, vpg=4, thr="0.2", weights=None,
+                 desc="CC on symmetrized RMAT s22 ef16 (BASELINE configs[1])",
+                 expect_digest="a9b4aaec4bde3218"),
+    "bfs16": dict(app="bfs", scale=16, ef=16, sym=True, vpg=8, thr="0.01", weights=None,
+                  desc="BFS on symmetrized RMAT s16 ef16 (BASELINE configs[0])",
+                  expect_digest="591673cb243fad4e"),
+    "sssp16": dict(app="sssp", scale=16, ef=16, sym=True, vpg=4, thr="0.2", weights=255,
+                   desc="SSSP on symmetrized RMAT s16 ef16, hash weights <= 255",
+                   expect_digest="7d2c2554722fbf74"),
+    "sssp_grid": dict(app="sssp", grid=(4096, 4096), vpg=4, thr="0.2",
+                      desc="SSSP on 4096x4096 grid, p=0.9, w in [1,1000] (BASELINE configs[2])"),
+    "bfs26": dict(app="bfs", scale=26, ef=16, sym=False, vpg=8, thr="0.01", weights=None,
+                  desc="BFS on directed dedup RMAT s26 ef16 (BASELINE configs[3])"),
+    "sssp26": dict(app="sssp", scale=26, ef=16, sym=False, vpg=4, thr="0.2", weights=255,
+                   desc="SSSP on directed dedup RMAT s26 ef16, w<=255 (BASELINE configs[3])"),
+    "pr25": dict(app="pr", scale=25, ef=32, sym=False, desc="PageRank 20 it on directed dedup RMAT s25 ef32 "
+                 "(BASELINE configs[4])"),
+}
+GRID_SEED = 2
+METRIC = "GTEPS"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ----------------------------------------------------------------- clocks --
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int = 0):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 3 + i and r[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# -------------------------------------------------------------- workload --
+def make_graph(wl, width=4):
+    import paper_1903_07754_b200 as wg
+    if "grid" in wl:
+        el = wg.grid_graph(wl["grid"][0], wl["grid"][1], GRID_SEED, 0.9, 1000)
+    else:
+        el = wg.generate(wg.GenSpec("rmat", scale=wl["scale"], edge_factor=wl["ef"], seed=1))
+        el = wg.drop_self_loops_dedup(el, symmetric=wl["sym"])
+        if wl.get("weights"):
+            el = wg.synthesize_weights(el, wl["weights"])
+    topo = wg.build_pull_topology(el, width)
+    return el, topo
+
+
+def run_b200(args, wl):
+    import torch
+    import paper_1903_07754_b200 as wg
+    from paper_1903_07754_b200 import _lib, device as dv
+    from paper_1903_07754_b200.engine import _initial_values
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    t0 = time.perf_counter()
+    el, topo = make_graph(wl)
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t0
+    g = topo.device
+    n, E = g.n, g.edges
+    log(f"[bench] built {wl['desc']}: V={n} E={E} nvec={g.nvec} entries={g.entries} in {build_s:.1f}s "
+        f"({g.memory_bytes() / 1e9:.2f} GB layout)")
+
+    if wl["app"] == "pr":
+        return run_pagerank(args, wl, el, topo, build_s)
+
+    app = wl["app"]
+    root = 0
+    prog = wg.make_program(app, None if app == "cc" else root)
+    kern = prog.kernel
+    thr = Fraction(wl["thr"])
+    shift = {1: 0, 2: 1, 4: 2, 8: 3, 16: 4}[wl["vpg"]]
+    init = _initial_values(prog, n)
+    loop = dv.DeviceLoop(g, shift, _lib.WG_VAL_U32)
+    dinit = dv.encode_values(init, _lib.WG_VAL_U32)
+    words = dv.all_words(n) if app == "cc" else dv.initial_words(n, np.array([root]))
+    max_it = n + 16  # cli.py:162
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def step(timer=None):
+        p = loop.seed(dinit, words, kern, thr)
+        if timer is not None:
+            p.timer = timer.handle
+        return loop.drive(p, max_it)
+
+    for _ in range(args.warmup):
+        recs, conv, last = step()
+    torch.cuda.synchronize()
+    values = dv.values_to_int64(loop.values_after(last), _lib.WG_VAL_U32)
+    digest = wg.result_digest(values)
+    iters = len(recs)
+    modes = "".join("W" if r.mode == "Wedge" else "F" for r in recs)
+    log(f"[bench] {iters} iterations ({modes}), converged={conv}, digest={digest}")
+
+    # ---- timed region: K steps, events per step, L2 flushed in between ----
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    launches0 = _lib.launch_count()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        wall0 = time.perf_counter()
+        for k in range(args.steps):
+            flush.fill_(k & 0xFF)
+            ev[k][0].record(stream)
+            step()
+            ev[k][1].record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - wall0
+    launches = _lib.launch_count() - launches0
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    ms = float(np.mean(step_ms))
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+        torch.distributed.barrier()
+    gteps = E * world / (ms * 1e-3) / 1e9
+
+    # ---- roofline of the dominant kernel (pull), CUDA events per launch ----
+    timer = _lib.EventTimer(8 * (iters + 8))
+    flush.fill_(1)
+    torch.cuda.synchronize()
+    recs_t, _, _ = step(timer)
+    torch.cuda.synchronize()
+    rows = timer.read()
+    roof = roofline(rows, recs_t, n, E, g.weighted(), kern.filter_unvisited, wl)
+
+    out = {
+        "metric": METRIC, "value": round(gteps, 4), "unit": "GTEPS (|E|/time-to-solution)",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic (device RMAT, reference PCG64 stream)",
+        "config": {"workload": wl["desc"], "app": app, "V": n, "E": E, "W": 4, "vpg": wl["vpg"],
+                   "threshold": wl["thr"], "iterations": iters, "modes": modes,
+                   "l2": "inputs larger than L2 + 256 MB flush between steps",
+                   "build_s": round(build_s, 2), "tts_ms": round(ms, 4)},
+        "parity": {"digest": digest, "expected": wl.get("expect_digest"),
+                   "ok": (digest == wl["expect_digest"]) if wl.get("expect_digest") else None},
+        "gpu_launches": int(launches),
+        "timed_wall_s": round(wall, 3),
+        "roofline": roof,
+    }
+    clocks = clk.summary()
+    out["clocks"] = clocks
+    if rank == 0 and not args.no_e2e:
+        out["e2e"] = e2e_b200(args, wl, g, loop, dinit, words, kern, thr, max_it)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(wl, g, prog, thr, max_it, sample_runs=1)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def roofline(rows, recs, n, E, weighted, filt, wl):
+    """achieved = algorithmic bytes per pull launch / its CUDA-event duration
+    (dense launches: the dominant kernel); wedge iterations reported beside."""
+    peak, peak_src = peaks()
+    by_it = {}
+    for kind, it, ms in rows:
+        by_it.setdefault(it, {})[kind] = ms
+    w = 1 if weighted else 0
+    dense_b = dense_t = 0.0
+    wedge_b = wedge_t = 0.0
+    step_t = 0.0
+    prev_out = None
+    per_iter = []
+    for r in recs:
+        t = by_it.get(r.iteration, {})
+        pull_ms = t.get(2, 0.0)
+        prep_ms = t.get(1, 0.0)
+        fin_ms = t.get(3, 0.0)
+        step_t += pull_ms + prep_ms + fin_ms
+        U = r.frontier_out_size
+        if r.mode == "FullScan":
+            ep = E if not filt else min(E, 4 * r.vectors_touched)
+            b = 4 * ep * (1 + w) + 4 * n + 4 * U + n / 8
+            dense_b += b
+            dense_t += pull_ms
+        else:
+            A = r.active_edges
+            F = prev_out if prev_out is not None else 0
+            b = 4 * A * (1 + w) + 4 * F + 4 * U + n / 8 + (n / 8 + 8 * F + 4 * A)
+            wedge_b += b
+            wedge_t += pull_ms + prep_ms
+        per_iter.append({"it": r.iteration, "mode": r.mode, "pull_ms": round(pull_ms, 4),
+                         "prep_ms": round(prep_ms, 4), "end_ms": round(fin_ms, 4),
+                         "alg_MB": round(b / 1e6, 2)})
+        prev_out = U
+    if dense_t > 0:
+        ach = dense_b / (dense_t * 1e-3) / 1e9
+        kernel = "pull_kernel<u32,W4> dense (K6)"
+        traffic = dense_b / max(1, sum(1 for r in recs if r.mode == "FullScan"))
+    else:
+        ach = wedge_b / (wedge_t * 1e-3) / 1e9 if wedge_t else 0.0
+        kernel = "transform + wedge pull (K3+K4+K5)"
+        traffic = None
+    prof = ROOT / "profiles" / "traffic.json"
+    measured_traffic = None
+    if prof.exists():
+        try:
+            measured_traffic = json.loads(prof.read_text()).get(wl["desc"])
+        except Exception:
+            pass
+    return {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(ach / peak, 4), "traffic": measured_traffic, "kernel": kernel,
+            "peak_source": peak_src,
+            "algorithmic_bytes_per_launch": round(traffic, 1) if traffic else None,
+            "wedge_iters_achieved_gbs": round(wedge_b / (wedge_t * 1e-3) / 1e9, 1) if wedge_t else None,
+            "kernel_sum_ms": round(step_t, 4), "per_iteration": per_iter}
+
+
+def e2e_b200(args, wl, g, loop, dinit, words, kern, thr, max_it):
+    """Same metric through the C ABI with the layout in pinned HOST memory:
+    per step H2D of the layout, the device loop, D2H of the result."""
+    import torch
+    from paper_1903_07754_b200 import _lib, device as dv
+
+    host = {}
+    for name in ("vsrc", "vdst", "vw", "idx_off", "idx_pos", "outdeg"):
+        t = getattr(g, name)
+        if t is not None:
+            host[name] = t.cpu().pin_memory()
+    dev = {k: torch.empty_like(v, device="cuda") for k, v in host.items()}
+    g2 = dv.DeviceGraph(g.n, g.width, g.edges, g.nvec, g.entries, dev["vsrc"], dev["vdst"], dev.get("vw"),
+                        dev["idx_off"], dev["idx_pos"], dev["outdeg"])
+    loop2 = dv.DeviceLoop(g2, loop.shift, loop.val_type)
+    out_host = torch.empty(g.n, dtype=torch.int32).pin_memory()
+    h2d = sum(v.numel() * v.element_size() for v in host.values())
+    d2h = out_host.numel() * 4
+    stream = torch.cuda.current_stream()
+
+    def one():
+        for k, v in host.items():
+            dev[k].copy_(v, non_blocking=True)
+        p = loop2.seed(dinit, words, kern, thr)
+        recs, conv, last = loop2.drive(p, max_it)
+        out_host.copy_(loop2.values_after(last), non_blocking=True)
+        return last
+
+    for _ in range(max(1, args.warmup)):
+        one()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(args.steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        one()
+        b.record(stream)
+        b.synchronize()
+        ts.append(a.elapsed_time(b))
+    ms = float(np.mean(ts))
+    return {"value": round(g.edges / (ms * 1e-3) / 1e9, 4), "unit": "GTEPS (|E|/time-to-solution)",
+            "ms_per_step": round(ms, 3), "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "path": "pinned host layout -> H2D -> wg_run_init/wg_run_enqueue -> D2H labels"}
+
+
+def host_reference_layout(g):
+    """Reference-layout int64 arrays (graph.py:109-212) downloaded from the
+    device build (input preparation for the CPU arm; parity of this layout
+    with the reference's own builder is tested in tests/test_gpu_parity.py)."""
+    import oracle
+    lane_src, lane_w, lane_count = g.lanes_np()
+    topo = oracle.RefTopology(g.n, g.width, g.edges, g.vec_dst_np(), lane_src, lane_w, lane_count)
+    idx = oracle.RefIndex(g.n, g.nvec, g.offsets_np(), g.positions_np())
+    return topo, idx, g.outdeg_np()
+
+
+def cpu_baseline(wl, g, prog, thr, max_it, sample_runs=1, kind=None, threads=None):
+    """The reference CPU path on this host: the reference's own compiled
+    kernels (oracle/_ref, built from /root/reference by oracle/Makefile) in
+    the reference driver restated (oracle.run_until_convergence), all host
+    threads; falls back to the C restatement ("port") when _ref is absent."""
+    import oracle
+    threads = threads or os.cpu_count() or 1
+    topo, idx, deg = host_reference_layout(g)
+    if oracle.ref_kernels() is not None:
+        be, kind = oracle.RefBackend(threads), "reference"
+    else:
+        be, kind = oracle.PortBackend(threads), "port"
+    init = np.asarray(prog.initial_values(g.n), dtype=np.int64)
+    front = np.arange(g.n) if wl["app"] == "cc" else np.array([0])
+    kern = oracle.kern_of(wl["app"])
+    times = []
+    out = None
+    for _ in range(sample_runs):
+        t0 = time.perf_counter()
+        out = oracle.run_until_convergence(topo, idx, deg, kern, init, front, thr, wl["vpg"], max_it,
+                                           backend=be)
+        times.append(time.perf_counter() - t0)
+    t = min(times)
+    return {"value": round(g.edges / t / 1e9, 5), "unit": "GTEPS (|E|/time-to-solution)",
+            "cores": threads, "kind": kind, "seconds_per_run": round(t, 3),
+            "sample": f"{sample_runs} full run(s) of the same workload (E={g.edges}), "
+                      f"{len(out.stats)} iterations, digest {oracle.result_digest(out.values)}"}
+
+
+def run_pagerank(args, wl, el, topo, build_s):
+    import torch
+    import paper_1903_07754_b200 as wg
+    from paper_1903_07754_b200 import _lib, device as dv
+    g = topo.device
+    n, E = g.n, g.edges
+    bufs = (torch.empty(n, dtype=torch.float32, device="cuda"), torch.empty(n, dtype=torch.float32, device="cuda"),
+            torch.empty(n, dtype=torch.float32, device="cuda"), torch.zeros(4, dtype=torch.float64, device="cuda"))
+    for _ in range(args.warmup):
+        dv.pagerank(g, 20, 0.85, bufs=bufs)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    ts = []
+    launches0 = _lib.launch_count()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    with ClockSampler(0) as clk:
+        for k in range(args.steps):
+            flush.fill_(k & 0xFF)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            dv.pagerank(g, 20, 0.85, bufs=bufs)
+            b.record(stream)
+            b.synchronize()
+            ts.append(a.elapsed_time(b))
+    ms = float(np.mean(ts))
+    peak, src = peaks()
+    alg = 20 * (4 * E + 20 * n)
+    ach = alg / (ms * 1e-3) / 1e9
+    out = {"metric": METRIC, "value": round(20 * E / (ms * 1e-3) / 1e9, 4),
+           "unit": "GTEPS (20*|E|/time, PageRank)", "n_gpus": 1, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+           "config": {"workload": wl["desc"], "V": n, "E": E, "build_s": round(build_s, 2)},
+           "gpu_launches": int(_lib.launch_count() - launches0),
+           "roofline": {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+                        "frac": round(ach / peak, 4), "traffic": None, "peak_source": src,
+                        "kernel": "pr_prep + pr_pull (20 iterations)"},
+           "clocks": clk.summary()}
+    print(json.dumps(out), flush=True)
+
+
+def run_reference(args, wl):
+    """--impl reference: the reference's CPU implementation on the host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    threads = os.cpu_count() or 1
+    # input preparation (not timed): the graph on the GPU when present, else the oracle
+    try:
+        import torch
+        have_gpu = torch.cuda.is_available()
+    except Exception:
+        have_gpu = False
+    if have_gpu:
+        import paper_1903_07754_b200 as wg
+        el, topo = make_graph(wl)
+        g = topo.device
+        tp, idx, deg = host_reference_layout(g)
+        n, E = g.n, g.edges
+    else:
+        if "grid" in wl:
+            n, s, d, w = oracle.grid_edges(wl["grid"][0], wl["grid"][1], GRID_SEED)
+        else:
+            n, s, d = oracle.rmat_edges(wl["scale"], wl["ef"], 1)
+            keep = s != d
+            if wl["sym"]:
+                s, d, _ = oracle.symmetrize(s[keep], d[keep], None, dedup=True)
+            else:
+                s, d = oracle.dedup_directed(s[keep], d[keep])
+            w = oracle.synthesize_weights(s, d, wl["weights"]) if wl.get("weights") else None
+        tp = oracle.build_pull_topology(n, s, d, w, 4)
+        idx = oracle.build_edge_index(tp)
+        deg = oracle.compute_out_degrees(n, s)
+        E = len(s)
+    if wl["app"] == "pr":
+        t0 = time.perf_counter()
+        oracle.pagerank(tp, deg, 20, 0.85, threads)
+        t = time.perf_counter() - t0
+        val = 20 * E / t / 1e9
+        print(json.dumps({"impl": "reference", "metric": METRIC, "value": round(val, 5),
+                          "unit": "GTEPS (20*|E|/time, PageRank)", "n_gpus": 1, "steps": 1, "warmup": 0,
+                          "higher_is_better": True, "cpu_baseline": {"value": round(val, 5), "cores": threads,
+                          "kind": "port", "sample": "1 run of 20 iterations (no reference PR exists)"},
+                          "e2e": {"value": round(val, 5), "unit": "GTEPS", "h2d_bytes_per_step": 0,
+                                  "d2h_bytes_per_step": 0}, "config": {"workload": wl["desc"]}}))
+        return
+    if oracle.ref_kernels() is not None:
+        be, kind = oracle.RefBackend(threads), "reference"
+    else:
+        be, kind = oracle.PortBackend(threads), "port"
+    app = wl["app"]
+    init, front = oracle.initial_state(app, n, 0)
+    kern = oracle.kern_of(app)
+    thr = Fraction(wl["thr"])
+    ts = []
+    out = None
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        out = oracle.run_until_convergence(tp, idx, deg, kern, init, front, thr, wl["vpg"], n + 16,
+                                           backend=be)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            ts.append(dt)
+    ms = float(np.mean(ts)) * 1e3
+    val = E / (ms * 1e-3) / 1e9
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(val, 5),
+        "unit": "GTEPS (|E|/time-to-solution)", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": {"workload": wl["desc"], "V": n, "E": E, "iterations": len(out.stats)},
+        "parity": {"digest": oracle.result_digest(out.values), "expected": wl.get("expect_digest")},
+        "cpu_baseline": {"value": round(val, 5), "unit": "GTEPS", "cores": threads, "kind": kind,
+                         "sample": f"each step = 1 full run to convergence ({len(out.stats)} iterations)"},
+        "e2e": {"value": round(val, 5), "unit": "GTEPS (|E|/time-to-solution)", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0}}), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=("b200", "reference"))
+    ap.add_argument("--workload", default="cc22", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
+    wl = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        run_reference(args, wl)
+    else:
+        run_b200(args, wl)
+
+
+if __name__ == "__main__":
+    main()

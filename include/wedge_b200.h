@@ -155,6 +155,7 @@ typedef struct wg_run_params {
     int32_t shift;          /* log2(vectors per group) */
     wg_minplus kern;
     uint64_t wedge_limit;   /* wedge iff E>0 and edge_sum < wedge_limit (= ceil(num*E/den)) */
+    void *timer;            /* optional wg_timer*: CUDA events around each launch group */
 } wg_run_params;
 
 /* Element counts: [0] fbits words, [1] groups, [2] gbits words, [3] bcount
@@ -175,6 +176,21 @@ int wg_run_enqueue(const wg_graph *g, const wg_run_bufs *b, const wg_run_params 
  * launch advances. */
 int wg_run_enqueue_counter(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p,
                            uint32_t count, void *stream);
+
+/* ---------------- measurement --------------------------------------------- */
+/* Event timer: when attached to wg_run_params.timer, wg_run_enqueue records a
+ * CUDA event pair (on the launch stream) around the Wedge preparation
+ * (transform + group compaction, kind 1), the pull (kind 2) and the
+ * end-of-iteration kernel (kind 3) of every enqueued iteration. */
+void *wg_timer_create(int capacity);
+void wg_timer_destroy(void *timer);
+int wg_timer_reset(void *timer);
+/* Elapsed ms of each recorded pair (stream must be complete); h_kind and
+ * h_iter receive the launch group and the iteration.  *h_count = pairs. */
+int wg_timer_read(void *timer, float *h_ms, int32_t *h_kind, int64_t *h_iter, int capacity,
+                  int *h_count);
+/* Kernels launched by this library since load (all entry points). */
+uint64_t wg_launch_count(void);
 
 /* ---------------- PageRank (BASELINE config 5) ---------------------------- */
 /* float32 ranks, damping, fixed iterations, dangling mass spread uniformly.

@@ -46,7 +46,8 @@ class WgRunBufs(ctypes.Structure):
 
 
 class WgRunParams(ctypes.Structure):
-    _fields_ = [("val_type", c_i32), ("shift", c_i32), ("kern", WgMinPlus), ("wedge_limit", c_u64)]
+    _fields_ = [("val_type", c_i32), ("shift", c_i32), ("kern", WgMinPlus), ("wedge_limit", c_u64),
+                ("timer", c_vp)]
 
 
 EXPORTS = [
@@ -55,6 +56,7 @@ EXPORTS = [
     "wg_pull_full", "wg_pull_wedge", "wg_covered_groups", "wg_run_buffer_sizes", "wg_run_init",
     "wg_run_enqueue", "wg_run_enqueue_counter", "wg_pagerank", "wg_rmat_edges",
     "wg_canonical_scratch_bytes", "wg_canonical_edges", "wg_weights_hash", "wg_grid_edges",
+    "wg_timer_create", "wg_timer_destroy", "wg_timer_reset", "wg_timer_read", "wg_launch_count",
 ]
 
 _LIB = None
@@ -116,6 +118,12 @@ def load(path: os.PathLike | str | None = None):
         "wg_weights_hash": (ctypes.c_int, [c_u64, c_vp, c_vp, c_u32, c_vp, c_vp]),
         "wg_grid_edges": (ctypes.c_int, [c_u32, c_u32, c_u64, c_u32, c_u32, c_vp, c_vp, c_vp, c_vp,
                                          u64p, c_vp]),
+        "wg_timer_create": (c_vp, [ctypes.c_int]),
+        "wg_timer_destroy": (None, [c_vp]),
+        "wg_timer_reset": (ctypes.c_int, [c_vp]),
+        "wg_timer_read": (ctypes.c_int, [c_vp, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(c_i32),
+                                         ctypes.POINTER(c_i64), ctypes.c_int, ctypes.POINTER(ctypes.c_int)]),
+        "wg_launch_count": (c_u64, []),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -132,6 +140,40 @@ def check(rc: int) -> None:
         if rc == WG_EOVERFLOW:
             raise OverflowError32(rc, msg)
         raise WedgeError(rc, msg)
+
+
+class EventTimer:
+    """CUDA-event pairs recorded by the library around each launch group of
+    the device loop (kind 1 Wedge prep, 2 pull, 3 end-of-iteration)."""
+
+    def __init__(self, capacity: int = 4096):
+        L = load()
+        self.capacity = capacity
+        self.handle = L.wg_timer_create(capacity)
+        if not self.handle:
+            raise WedgeError(WG_ECUDA, L.wg_last_error().decode())
+
+    def reset(self):
+        check(load().wg_timer_reset(self.handle))
+
+    def read(self):
+        n = ctypes.c_int(0)
+        ms = (ctypes.c_float * self.capacity)()
+        kind = (c_i32 * self.capacity)()
+        it = (c_i64 * self.capacity)()
+        check(load().wg_timer_read(self.handle, ms, kind, it, self.capacity, ctypes.byref(n)))
+        return [(int(kind[i]), int(it[i]), float(ms[i])) for i in range(n.value)]
+
+    def __del__(self):
+        try:
+            if self.handle:
+                load().wg_timer_destroy(self.handle)
+        except Exception:
+            pass
+
+
+def launch_count() -> int:
+    return int(load().wg_launch_count())
 
 
 def require_cuda():

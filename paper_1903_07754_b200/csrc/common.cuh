@@ -34,6 +34,9 @@ int cuda_fail(cudaError_t e, const char *what);
     } while (0)
 
 int sm_count();
+void count_launch(uint64_t k = 1);
+int timer_begin(void *timer, int kind, int64_t it, cudaStream_t s);
+void timer_end(void *timer, int slot, cudaStream_t s);
 
 // Persistent-grid sizing: a multiple of the SM count, never more blocks
 // than there is work for.

@@ -118,9 +118,9 @@ LoopCtx forced_ctx(wg_iter_rec *recs, int mode, uint64_t edges) {
 int launch_group_compaction(const LoopCtx &c, uint32_t *words, uint64_t ngroups, uint64_t *bcount,
                             uint32_t *glist, int clear, int shift, uint64_t nvec, cudaStream_t s) {
     uint64_t nb = cb_blocks(ngroups ? ngroups : 1);
-    group_count_kernel<<<(unsigned)nb, CB_THREADS, 0, s>>>(c, words, ngroups, bcount);
+    group_count_kernel<<<(unsigned)nb, CB_THREADS, 0, s>>>(c, words, ngroups, bcount); ::wg::count_launch();
     group_list_kernel<<<(unsigned)nb, CB_THREADS, 0, s>>>(c, words, ngroups, bcount, glist, clear,
-                                                          shift, nvec);
+                                                          shift, nvec); ::wg::count_launch();
     WG_CHECK_LAUNCH("group compaction");
     return WG_OK;
 }
@@ -129,9 +129,9 @@ int launch_frontier_compaction(const wg_graph *g, const uint32_t *words, uint64_
                                uint32_t *fvert, uint32_t *fpref, wg_iter_rec *rec, cudaStream_t s) {
     uint64_t nb = cb_blocks(g->n ? g->n : 1);
     frontier_count_kernel<<<(unsigned)nb, CB_THREADS, 0, s>>>(words, g->n, g->idx_off, g->outdeg,
-                                                              bcount);
+                                                              bcount); ::wg::count_launch();
     frontier_list_kernel<<<(unsigned)nb, CB_THREADS, 0, s>>>(words, g->n, g->idx_off, bcount, fvert,
-                                                             fpref, rec);
+                                                             fpref, rec); ::wg::count_launch();
     WG_CHECK_LAUNCH("frontier compaction");
     return WG_OK;
 }
@@ -140,7 +140,7 @@ int launch_transform(const LoopCtx &c, const wg_graph *g, uint32_t *const fvert[
                      uint32_t *const fpref[2], int shift, uint32_t *gbits, cudaStream_t s) {
     unsigned grid = persistent_grid(transform_kernel, TR_THREADS, (g->entries + TR_TILE - 1) / TR_TILE);
     transform_kernel<<<grid, TR_THREADS, 0, s>>>(c, fvert[0], fvert[1], fpref[0], fpref[1], g->idx_off,
-                                                 g->idx_pos, shift, gbits);
+                                                 g->idx_pos, shift, gbits); ::wg::count_launch();
     WG_CHECK_LAUNCH("transform");
     return WG_OK;
 }
@@ -151,7 +151,7 @@ int launch_pull(const LoopCtx &c, const wg_graph *g, const PullBufs &pb, int val
     WG_REQUIRE(fn != nullptr, "no pull kernel for width %u", g->width);
     WG_REQUIRE(!k->use_weight || g->vw, "weighted kernel on an unweighted layout");
     unsigned grid = persistent_grid(fn, 256, (max_items + 255) / 256);
-    fn<<<grid, 256, 0, s>>>(c, *g, pb, shift, k->apply_increment, k->sentinel);
+    fn<<<grid, 256, 0, s>>>(c, *g, pb, shift, k->apply_increment, k->sentinel); ::wg::count_launch();
     WG_CHECK_LAUNCH("pull");
     return WG_OK;
 }
@@ -371,6 +371,7 @@ static int enqueue_one(const wg_graph *g, const wg_run_bufs *b, const wg_run_par
     uint64_t groups = groups_of(g, p->shift);
     uint32_t *fv[2] = {b->fvert[0], b->fvert[1]};
     uint32_t *fp[2] = {b->fpref[0], b->fpref[1]};
+    int slot = timer_begin(p->timer, 1, (int64_t)c.it_arg, s);
     if (g->entries) {
         if ((rc = launch_transform(c, g, fv, fp, p->shift, b->gbits, s))) return rc;
     }
@@ -379,15 +380,21 @@ static int enqueue_one(const wg_graph *g, const wg_run_bufs *b, const wg_run_par
                                           g->nvec, s)))
             return rc;
     }
+    timer_end(p->timer, slot, s);
     PullBufs pb = pull_bufs(g, b);
+    slot = timer_begin(p->timer, 2, (int64_t)c.it_arg, s);
     if (g->nvec) {
         if ((rc = launch_pull(c, g, pb, p->val_type, p->shift, &p->kern, g->nvec, s))) return rc;
     }
+    timer_end(p->timer, slot, s);
     unsigned grid = (unsigned)sm_count() * 2;
+    slot = timer_begin(p->timer, 3, (int64_t)c.it_arg, s);
     if (p->val_type == WG_VAL_U32)
         finalize_kernel<uint32_t><<<grid, 256, 0, s>>>(c, pb);
     else
         finalize_kernel<int64_t><<<grid, 256, 0, s>>>(c, pb);
+    ::wg::count_launch();
+    timer_end(p->timer, slot, s);
     WG_CHECK_LAUNCH("finalize");
     return WG_OK;
 }
@@ -416,7 +423,7 @@ int wg_run_enqueue_counter(const wg_graph *g, const wg_run_bufs *b, const wg_run
         LoopCtx c = loop_ctx(g, b, p, b->ctrl, 1 + i);
         if ((rc = enqueue_one(g, b, p, c, s))) return rc;
     }
-    bump_counter_kernel<<<1, 1, 0, s>>>(b->ctrl, count);
+    bump_counter_kernel<<<1, 1, 0, s>>>(b->ctrl, count); ::wg::count_launch();
     WG_CHECK_LAUNCH("bump");
     return WG_OK;
 }

@@ -167,7 +167,7 @@ int wg_build_layout(uint32_t n, uint64_t m, const uint32_t *d_src, const uint32_
     WG_REQUIRE(!weighted || d_vw, "weights given without an output weight array");
 
     // 1. sort by (dst, src), stable
-    make_dst_keys<<<grid_1d(m), 256, 0, s>>>(m, d_src, d_dst, sb, ls.k0);
+    make_dst_keys<<<grid_1d(m), 256, 0, s>>>(m, d_src, d_dst, sb, ls.k0); ::wg::count_launch();
     WG_CHECK_LAUNCH("make_dst_keys");
     cub::DoubleBuffer<uint64_t> kb(ls.k0, ls.k1);
     size_t tb = ls.temp_bytes;
@@ -185,8 +185,8 @@ int wg_build_layout(uint32_t n, uint64_t m, const uint32_t *d_src, const uint32_
 
     // 2. destination runs -> vectors per destination -> first vector per destination
     WG_CUDA(cudaMemsetAsync(ls.first, 0xff, ((uint64_t)n + 1) * 8, s));
-    run_bounds<<<grid_1d(m), 256, 0, s>>>(m, sorted, sb, ls.first, ls.last);
-    run_counts<<<grid_1d(n), 256, 0, s>>>(n, ls.first, ls.last, (int)width, ls.base, nullptr);
+    run_bounds<<<grid_1d(m), 256, 0, s>>>(m, sorted, sb, ls.first, ls.last); ::wg::count_launch();
+    run_counts<<<grid_1d(n), 256, 0, s>>>(n, ls.first, ls.last, (int)width, ls.base, nullptr); ::wg::count_launch();
     WG_CHECK_LAUNCH("dst runs");
     WG_CUDA(cudaMemsetAsync(ls.base + n, 0, 8, s));
     tb = ls.temp_bytes;
@@ -203,7 +203,7 @@ int wg_build_layout(uint32_t n, uint64_t m, const uint32_t *d_src, const uint32_
     if (weighted) WG_CUDA(cudaMemsetAsync(d_vw, 0, nvec * width * 4, s));
     pack_vectors<<<grid_1d(m), 256, 0, s>>>(m, sorted, weighted ? ls.w0 : nullptr, sb, ls.first,
                                             ls.base, (int)width, d_vsrc, d_vdst,
-                                            weighted ? d_vw : nullptr, other, vb);
+                                            weighted ? d_vw : nullptr, other, vb); ::wg::count_launch();
     WG_CHECK_LAUNCH("pack_vectors");
 
     // 4. edge index: sort (src, vector) keys by src (stable: vectors stay ascending)
@@ -214,8 +214,8 @@ int wg_build_layout(uint32_t n, uint64_t m, const uint32_t *d_src, const uint32_
     uint64_t *ialt = ib.Alternate();
     // out-degrees from the pre-dedup source runs (graph.py:277-280)
     WG_CUDA(cudaMemsetAsync(ls.first, 0xff, ((uint64_t)n + 1) * 8, s));
-    run_bounds<<<grid_1d(m), 256, 0, s>>>(m, isorted, vb, ls.first, ls.last);
-    run_counts<<<grid_1d(n), 256, 0, s>>>(n, ls.first, ls.last, 0, ls.base, d_outdeg);
+    run_bounds<<<grid_1d(m), 256, 0, s>>>(m, isorted, vb, ls.first, ls.last); ::wg::count_launch();
+    run_counts<<<grid_1d(n), 256, 0, s>>>(n, ls.first, ls.last, 0, ls.base, d_outdeg); ::wg::count_launch();
     WG_CHECK_LAUNCH("src runs");
     // de-duplicate (src, vector) pairs (graph.py:293-297)
     tb = ls.temp_bytes;
@@ -224,13 +224,13 @@ int wg_build_layout(uint32_t n, uint64_t m, const uint32_t *d_src, const uint32_
     WG_CUDA(cudaMemcpyAsync(&entries, ls.count, 8, cudaMemcpyDeviceToHost, s));
     WG_CUDA(cudaStreamSynchronize(s));
     WG_CUDA(cudaMemsetAsync(ls.first, 0xff, ((uint64_t)n + 1) * 8, s));
-    run_bounds<<<grid_1d(entries), 256, 0, s>>>(entries, ialt, vb, ls.first, ls.last);
-    run_counts<<<grid_1d(n), 256, 0, s>>>(n, ls.first, ls.last, 0, ls.base, nullptr);
+    run_bounds<<<grid_1d(entries), 256, 0, s>>>(entries, ialt, vb, ls.first, ls.last); ::wg::count_launch();
+    run_counts<<<grid_1d(n), 256, 0, s>>>(n, ls.first, ls.last, 0, ls.base, nullptr); ::wg::count_launch();
     WG_CHECK_LAUNCH("index runs");
     WG_CUDA(cudaMemsetAsync(ls.base + n, 0, 8, s));
     tb = ls.temp_bytes;
     WG_CUDA(cub::DeviceScan::ExclusiveSum(ls.temp, tb, ls.base, d_idx_off, (int64_t)n + 1, s));
-    unpack_positions<<<grid_1d(entries), 256, 0, s>>>(entries, ialt, vb, d_idx_pos);
+    unpack_positions<<<grid_1d(entries), 256, 0, s>>>(entries, ialt, vb, d_idx_pos); ::wg::count_launch();
     WG_CHECK_LAUNCH("unpack_positions");
     WG_CUDA(cudaStreamSynchronize(s));
     h_counts[0] = nvec;
@@ -389,7 +389,7 @@ int wg_rmat_edges(uint32_t scale, uint64_t m, uint64_t state_hi, uint64_t state_
     uint64_t chunks = (m + RMAT_EPT - 1) / RMAT_EPT;
     unsigned grid = grid_for(chunks, 256, 8);
     rmat_kernel<<<grid, 256, 0, s>>>(scale, m, state_hi, state_lo, inc_hi, inc_lo, h_thresholds3[0],
-                                     h_thresholds3[1], h_thresholds3[2], d_src, d_dst);
+                                     h_thresholds3[1], h_thresholds3[2], d_src, d_dst); ::wg::count_launch();
     WG_CHECK_LAUNCH("rmat");
     return WG_OK;
 }
@@ -429,7 +429,7 @@ int wg_canonical_edges(uint64_t m, uint32_t *d_src, uint32_t *d_dst, int drop_lo
         return WG_ENOSPACE;
     }
     WG_CUDA(cudaMemsetAsync(cnt, 0, 64, s));
-    edge_keys<<<grid_for(m, 256 * 8, 16), 256, 0, s>>>(m, d_src, d_dst, drop_loops, symmetrize, k0, cnt);
+    edge_keys<<<grid_for(m, 256 * 8, 16), 256, 0, s>>>(m, d_src, d_dst, drop_loops, symmetrize, k0, cnt); ::wg::count_launch();
     WG_CHECK_LAUNCH("edge_keys");
     unsigned long long k = 0;
     WG_CUDA(cudaMemcpyAsync(&k, cnt, 8, cudaMemcpyDeviceToHost, s));
@@ -444,7 +444,7 @@ int wg_canonical_edges(uint64_t m, uint32_t *d_src, uint32_t *d_dst, int drop_lo
     WG_CUDA(cudaMemcpyAsync(&u, cnt + 1, 8, cudaMemcpyDeviceToHost, s));
     WG_CUDA(cudaStreamSynchronize(s));
     WG_REQUIRE(u <= (symmetrize ? 2 * m : m), "internal: unique count");
-    split_keys<<<grid_for(u, 256 * 8, 16), 256, 0, s>>>(u, kb.Alternate(), d_src, d_dst);
+    split_keys<<<grid_for(u, 256 * 8, 16), 256, 0, s>>>(u, kb.Alternate(), d_src, d_dst); ::wg::count_launch();
     WG_CHECK_LAUNCH("split_keys");
     WG_CUDA(cudaStreamSynchronize(s));
     *h_m_out = u;
@@ -457,7 +457,7 @@ int wg_weights_hash(uint64_t m, const uint32_t *d_src, const uint32_t *d_dst, ui
     if (m == 0) return WG_OK;
     WG_REQUIRE(d_src && d_dst && d_w, "null argument");
     weights_kernel<<<grid_for(m, 256 * 8, 16), 256, 0, as_stream(stream)>>>(m, d_src, d_dst,
-                                                                           max_weight, d_w);
+                                                                           max_weight, d_w); ::wg::count_launch();
     WG_CHECK_LAUNCH("weights");
     return WG_OK;
 }
@@ -473,7 +473,7 @@ int wg_grid_edges(uint32_t rows, uint32_t cols, uint64_t seed, uint32_t keep_per
     if (und) {
         grid_kernel<<<grid_for(und, 256 * 8, 16), 256, 0, s>>>(
             rows, cols, seed, keep_per_million, max_weight, d_src, d_dst, d_w,
-            (unsigned long long *)d_counter);
+            (unsigned long long *)d_counter); ::wg::count_launch();
         WG_CHECK_LAUNCH("grid");
     }
     WG_CUDA(cudaMemcpyAsync(h_m_out, d_counter, 8, cudaMemcpyDeviceToHost, s));

@@ -114,12 +114,15 @@ extern "C" int wg_pagerank(const wg_graph *g, int iterations, double damping, fl
     if (per_sm < 1) per_sm = 1;
     unsigned egrid = grid_for(g->nvec, 256, (unsigned)per_sm);
     for (int it = 0; it < iterations; ++it) {
-        pr_prep<<<vgrid, 256, 0, s>>>(g->n, it, damping, g->outdeg, d_acc, d_contrib, nullptr, d_scal);
-        if (g->nvec) pull<<<egrid, 256, 0, s>>>(*g, d_contrib, d_acc);
+        pr_prep<<<vgrid, 256, 0, s>>>(g->n, it, damping, g->outdeg, d_acc, d_contrib, nullptr, d_scal); ::wg::count_launch();
+        if (g->nvec) {
+            pull<<<egrid, 256, 0, s>>>(*g, d_contrib, d_acc);
+            ::wg::count_launch();
+        }
     }
     // final apply: prep of iteration `iterations` writes the ranks
     pr_prep<<<vgrid, 256, 0, s>>>(g->n, iterations, damping, g->outdeg, d_acc, d_contrib, d_rank,
-                                  d_scal);
+                                  d_scal); ::wg::count_launch();
     WG_CHECK_LAUNCH("pagerank");
     return WG_OK;
 }
