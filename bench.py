@@ -316,7 +316,8 @@ def e2e_b200(args, wl, g, loop, dinit, words, kern, thr, max_it):
         t = getattr(g, name)
         if t is not None:
             host[name] = t.cpu().pin_memory()
-    dev = {k: torch.empty_like(v, device="cuda") for k, v in host.items()}
+    # device buffers with readable slack past the end (TMA tail rounding, wedge_b200.h)
+    dev = {k: torch.empty(v.numel() + 64, dtype=v.dtype, device="cuda")[: v.numel()] for k, v in host.items()}
     g2 = dv.DeviceGraph(g.n, g.width, g.edges, g.nvec, g.entries, dev["vsrc"], dev["vdst"], dev.get("vw"),
                         dev["idx_off"], dev["idx_pos"], dev["outdeg"])
     loop2 = dv.DeviceLoop(g2, loop.shift, loop.val_type)

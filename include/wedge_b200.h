@@ -51,7 +51,9 @@ extern "C" {
 
 #define WG_NO_LANE 0xFFFFFFFFu /* padding lane in vsrc */
 
-/* Device-resident pull layout.  All pointers device. */
+/* Device-resident pull layout.  All pointers device.
+ * vsrc / vdst / vw must stay readable for 16 vectors past nvec (the dense
+ * pull streams them with TMA bulk copies rounded up to 16 bytes). */
 typedef struct wg_graph {
     uint32_t n;          /* vertices */
     uint32_t width;      /* lanes per vector: 1, 2, 4, 8 (graph.py:215-217) */

@@ -1,6 +1,8 @@
 // engine.cu — C-ABI entry points of the pull engine: per-call kernels (the
 // reference backend protocol, kernels.py:55-125) and the device-resident
 // convergence loop (engine.py:330-388).
+#include <stdlib.h>
+
 #include <mutex>
 #include <unordered_map>
 
@@ -10,6 +12,12 @@
 using namespace wg;
 
 namespace {
+
+// TMA-fed dense pull on/off (WG_DENSE_TMA=0 selects the direct-load kernel).
+bool g_dense_tma = [] {
+    const char *e = getenv("WG_DENSE_TMA");
+    return !(e && e[0] == '0');
+}();
 
 struct Occ {
     std::mutex mu;
@@ -21,7 +29,7 @@ Occ &occ() {
 }
 
 template <typename K>
-unsigned persistent_grid(K kernel, int threads, uint64_t work_blocks) {
+unsigned persistent_grid(K kernel, int threads, uint64_t work_blocks, size_t dyn_smem = 0) {
     const void *key = (const void *)kernel;
     int per_sm = 0;
     {
@@ -30,7 +38,9 @@ unsigned persistent_grid(K kernel, int threads, uint64_t work_blocks) {
         if (it != occ().blocks.end()) per_sm = it->second;
     }
     if (per_sm == 0) {
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0) != cudaSuccess ||
+        if (dyn_smem > 48 * 1024)
+            cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_smem);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, dyn_smem) != cudaSuccess ||
             per_sm < 1)
             per_sm = 1;
         std::lock_guard<std::mutex> lk(occ().mu);
@@ -41,12 +51,14 @@ unsigned persistent_grid(K kernel, int threads, uint64_t work_blocks) {
     return (unsigned)(work_blocks < cap ? work_blocks : cap);
 }
 
-using PullFn = void (*)(LoopCtx, wg_graph, PullBufs, int, int64_t, int64_t);
+using PullFn = void (*)(LoopCtx, wg_graph, PullBufs, int, int64_t, int64_t, int);
+using DenseFn = void (*)(LoopCtx, wg_graph, PullBufs, int, int64_t, int64_t);
 
 template <typename T, int W>
 PullFn pick_pull_w(bool weight, bool filter) {
-    if (weight) return filter ? pull_kernel<T, W, true, true> : pull_kernel<T, W, true, false>;
-    return filter ? pull_kernel<T, W, false, true> : pull_kernel<T, W, false, false>;
+    constexpr int U = W >= 8 ? 1 : 2;
+    if (weight) return filter ? pull_kernel<T, W, true, true, U> : pull_kernel<T, W, true, false, U>;
+    return filter ? pull_kernel<T, W, false, true, U> : pull_kernel<T, W, false, false, U>;
 }
 
 template <typename T>
@@ -63,6 +75,24 @@ PullFn pick_pull_t(int width, bool weight, bool filter) {
 PullFn pick_pull(int val_type, int width, bool weight, bool filter) {
     return val_type == WG_VAL_U32 ? pick_pull_t<uint32_t>(width, weight, filter)
                                   : pick_pull_t<int64_t>(width, weight, filter);
+}
+
+template <typename T, int W>
+DenseFn pick_dense_w(bool weight, size_t *smem) {
+    *smem = weight ? TmaSmem<W, true>::BLOCK_BYTES : TmaSmem<W, false>::BLOCK_BYTES;
+    return weight ? pull_dense_tma_kernel<T, W, true> : pull_dense_tma_kernel<T, W, false>;
+}
+
+// TMA-streamed dense pull (unfiltered programs only).
+DenseFn pick_dense(int val_type, int width, bool weight, size_t *smem) {
+    bool u32 = val_type == WG_VAL_U32;
+    switch (width) {
+        case 1: return u32 ? pick_dense_w<uint32_t, 1>(weight, smem) : pick_dense_w<int64_t, 1>(weight, smem);
+        case 2: return u32 ? pick_dense_w<uint32_t, 2>(weight, smem) : pick_dense_w<int64_t, 2>(weight, smem);
+        case 4: return u32 ? pick_dense_w<uint32_t, 4>(weight, smem) : pick_dense_w<int64_t, 4>(weight, smem);
+        case 8: return u32 ? pick_dense_w<uint32_t, 8>(weight, smem) : pick_dense_w<int64_t, 8>(weight, smem);
+    }
+    return nullptr;
 }
 
 int check_graph(const wg_graph *g) {
@@ -147,11 +177,24 @@ int launch_transform(const LoopCtx &c, const wg_graph *g, uint32_t *const fvert[
 
 int launch_pull(const LoopCtx &c, const wg_graph *g, const PullBufs &pb, int val_type, int shift,
                 const wg_minplus *k, uint64_t max_items, cudaStream_t s) {
-    PullFn fn = pick_pull(val_type, (int)g->width, k->use_weight != 0, k->filter_unvisited != 0);
+    const bool weight = k->use_weight != 0, filter = k->filter_unvisited != 0;
+    WG_REQUIRE(!weight || g->vw, "weighted kernel on an unweighted layout");
+    PullFn fn = pick_pull(val_type, (int)g->width, weight, filter);
     WG_REQUIRE(fn != nullptr, "no pull kernel for width %u", g->width);
-    WG_REQUIRE(!k->use_weight || g->vw, "weighted kernel on an unweighted layout");
-    unsigned grid = persistent_grid(fn, 256, (max_items + 255) / 256);
-    fn<<<grid, 256, 0, s>>>(c, *g, pb, shift, k->apply_increment, k->sentinel); ::wg::count_launch();
+    int handles = (1 << MODE_FULL) | (1 << MODE_WEDGE);
+    if (!filter && g_dense_tma && (c.forced_mode == 0 || c.forced_mode == MODE_FULL)) {
+        size_t smem = 0;
+        DenseFn dn = pick_dense(val_type, (int)g->width, weight, &smem);
+        unsigned grid = persistent_grid(dn, PULL_THREADS, (g->nvec + 255) / 256, smem);
+        dn<<<grid, PULL_THREADS, smem, s>>>(c, *g, pb, shift, k->apply_increment, k->sentinel);
+        ::wg::count_launch();
+        WG_CHECK_LAUNCH("pull (dense, TMA)");
+        handles = 1 << MODE_WEDGE;
+        if (c.forced_mode == MODE_FULL) return WG_OK;
+    }
+    unsigned grid = persistent_grid(fn, PULL_THREADS, (max_items + 255) / 256);
+    fn<<<grid, PULL_THREADS, 0, s>>>(c, *g, pb, shift, k->apply_increment, k->sentinel, handles);
+    ::wg::count_launch();
     WG_CHECK_LAUNCH("pull");
     return WG_OK;
 }

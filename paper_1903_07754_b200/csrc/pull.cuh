@@ -1,4 +1,4 @@
-// pull.cuh — the atomic-free, warp-segmented min-plus pull (K5 wedge / K6 dense).
+// pull.cuh — the warp-segmented min-plus pull (K5 wedge / K6 dense).
 //
 // Reference semantics (engine.py:251-327; _kernels.pyx:65-95, 113-173):
 // per destination d, agg = min over processed in-lanes of prev[src] (+ weight);
@@ -6,17 +6,23 @@
 // bit) iff cand < prev[d].  BFS skips destinations already visited and does
 // not count their vectors as touched.
 //
-// B200 mapping: a warp consumes a tile of 32 work items, one vector per lane
-// (dense mode: consecutive vectors; wedge mode: vectors of the selected groups,
-// ascending).  Each lane streams its vector's W lanes with one vector load,
-// gathers prev[src], and reduces locally; a 5-step segmented min-scan keyed by
-// destination combines the lanes of equal destinations.  The tail lane of each
-// segment applies.  Only a segment that touches the tile's first or last lane
-// AND continues in the neighbouring work item can be shared with another warp;
-// those (at most two per tile) use atomicMin, every other destination is a
-// plain store.  The next-frontier bitmap, the produced member list (with the
-// edge-index prefix the next transform balances on), the out-degree sum (next
-// gate input) and the work counters are all emitted in the same kernel.
+// B200 mapping.  Every warp owns a contiguous range of 32-item tiles (dense:
+// consecutive vectors; wedge: the vectors of the selected groups, ascending)
+// and walks it in order, one vector per lane.  Lanes gather prev[src] for
+// their W lanes and fold them; equal destinations are combined with a single
+// REDUX min over the segment's lane mask (uint32) or a 5-step shuffle scan
+// (int64).  The segment touching lane 31 is CARRIED into the next tile, so a
+// destination is applied once, by one lane, with a plain store -- atomicMin is
+// only needed for the (at most two) segments that cross the ends of a warp's
+// range.  The next-frontier bitmap (one atomicOr per bitmap-word run), the
+// produced member list (staged per warp in shared memory, flushed with one
+// atomic per 32 members), the out-degree sum (the next gate's input) and the
+// work counter are all produced in the same kernel.
+//
+// Dense, unfiltered pulls stream the edge layout with TMA bulk copies
+// (cp.async.bulk + mbarrier, a per-warp S-stage ring in shared memory), so the
+// HBM stream runs ahead of the dependent gathers independently of register
+// pressure; wedge / filtered pulls load their vectors directly.
 #pragma once
 #include "loop.cuh"
 
@@ -44,15 +50,35 @@ struct PullBufs {
     uint32_t n;
 };
 
-__device__ __forceinline__ uint64_t min_u64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+constexpr int PULL_THREADS = 256;
+constexpr int PULL_WARPS = PULL_THREADS / 32;
+constexpr int STAGE = 96;  // per-warp staged frontier entries
+constexpr uint32_t NONE = 0xffffffffu;
 
 template <typename T>
+__device__ __forceinline__ T shfl_t(T v, int src) {
+    if constexpr (sizeof(T) == 8) return (T)__shfl_sync(FULL, (unsigned long long)v, src);
+    else return (T)__shfl_sync(FULL, (unsigned)v, src);
+}
+template <typename T>
 __device__ __forceinline__ T shfl_up_t(T v, int off) {
-    if constexpr (sizeof(T) == 8) {
-        return (T)__shfl_up_sync(FULL, (unsigned long long)v, off);
-    } else {
-        return (T)__shfl_up_sync(FULL, (unsigned)v, off);
+    if constexpr (sizeof(T) == 8) return (T)__shfl_up_sync(FULL, (unsigned long long)v, off);
+    else return (T)__shfl_up_sync(FULL, (unsigned)v, off);
+}
+
+// Segmented inclusive min-scan keyed by destination (equal destinations are
+// contiguous in a tile): the tail lane of each segment ends with its minimum.
+// (A REDUX with per-segment lane masks serialises per mask, so shuffles win.)
+template <typename T>
+__device__ __forceinline__ T segment_min(T v, uint32_t d) {
+    const unsigned lane = lane_id();
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        T o = shfl_up_t(v, off);
+        uint32_t od = __shfl_up_sync(FULL, d, off);
+        if ((int)lane >= off && od == d && o < v) v = o;
     }
+    return v;
 }
 
 // Map work item k to a vector position (or ~0 when out of range).
@@ -64,157 +90,447 @@ __device__ __forceinline__ uint64_t item_pos(uint64_t k, uint64_t nitems, bool w
     return p < nvec ? p : ~0ull;
 }
 
-template <typename T, int W, bool WEIGHT, bool FILTER>
-__global__ void __launch_bounds__(256) pull_kernel(LoopCtx c, wg_graph g, PullBufs b, int shift,
-                                                   int64_t inc, int64_t sentinel) {
+// ---------------------------------------------------------------------------
+// Per-warp output: counters in registers, frontier list staged in smem.
+struct PullOut {
+    uint32_t *stage;
+    uint32_t staged;    // warp-uniform
+    uint64_t edge_sum;  // per lane
+    uint64_t touched;   // lane 0
+    uint32_t ovf;
+};
+
+__device__ __forceinline__ void flush_stage(PullOut &o, const wg_graph &g, wg_iter_rec *out,
+                                            uint32_t *overt, uint32_t *opref, uint32_t n) {
+    const unsigned lane = lane_id();
+    for (uint32_t base = 0; base < o.staged; base += 32) {
+        const bool have = base + lane < o.staged;
+        const uint32_t d = have ? o.stage[base + lane] : 0u;
+        uint32_t len = 0;
+        if (have) {
+            len = (uint32_t)(g.idx_off[d + 1] - g.idx_off[d]);
+            o.edge_sum += g.outdeg[d];
+        }
+        const bool nz = have && len > 0;
+        const unsigned nzm = __ballot_sync(FULL, nz);
+        const unsigned zm = __ballot_sync(FULL, have) & ~nzm;
+        const uint32_t incl = warp_inclusive_sum(nz ? len : 0u);
+        const uint32_t tot = __shfl_sync(FULL, incl, 31);
+        unsigned long long nzb = 0, zb = 0;
+        if (lane == 0) {
+            if (nzm)
+                nzb = atomicAdd((unsigned long long *)&out->nz_packed,
+                                ((unsigned long long)__popc(nzm) << 32) | tot);
+            if (zm) zb = atomicAdd((unsigned long long *)&out->z_count, (unsigned long long)__popc(zm));
+        }
+        nzb = __shfl_sync(FULL, nzb, 0);
+        zb = __shfl_sync(FULL, zb, 0);
+        if (nz) {
+            uint64_t pos = (nzb >> 32) + __popc(nzm & lanemask_lt());
+            overt[pos] = d;
+            opref[pos] = (uint32_t)(nzb & 0xffffffffull) + (incl - len);
+        } else if (have) {
+            overt[n - 1 - (zb + __popc(zm & lanemask_lt()))] = d;
+        }
+    }
+    __syncwarp();
+    o.staged = 0;
+}
+
+// Collective apply, one segment per flagged lane (the min-plus update rule,
+// _kernels.pyx:91-94): plain store when the segment is complete, atomicMin
+// when another warp may hold part of it; one atomicOr per run of updating
+// lanes sharing a bitmap word; newly set destinations are staged.
+template <typename T>
+__device__ __forceinline__ void apply_segments(bool app, uint32_t d, T agg, T pd, bool complete,
+                                               T INF, int64_t inc, T *nxt, uint32_t *obits,
+                                               PullOut &o) {
     using VT = ValTraits<T>;
+    const unsigned lane = lane_id();
+    bool upd = false;
+    T cand = agg;
+    if (app) {
+        if constexpr (VT::U32) {
+            if (agg != INF) {
+                uint64_t cc = (uint64_t)agg + (uint64_t)inc;
+                if (cc >= 0xffffffffull) o.ovf = 1;
+                else {
+                    cand = (T)cc;
+                    upd = cand < pd;
+                }
+            }
+        } else {
+            cand = agg + (T)inc;
+            upd = cand < pd;
+        }
+    }
+    if (__ballot_sync(FULL, upd) == 0) return;
+    bool newly = false;
+    if (upd) {
+        const uint32_t bit = 1u << (d & 31);
+        if (complete) {
+            // the only writer of d this iteration: the bit is new (the bitmap
+            // was cleared by the previous end-of-iteration kernel)
+            nxt[d] = cand;
+            atomicOr(&obits[d >> 5], bit);
+            newly = true;
+        } else {
+            if constexpr (VT::U32) atomicMin((unsigned *)&nxt[d], (unsigned)cand);
+            else atomicMin((long long *)&nxt[d], (long long)cand);
+            newly = !(atomicOr(&obits[d >> 5], bit) & bit);
+        }
+    }
+    const unsigned nm = __ballot_sync(FULL, newly);
+    if (newly) o.stage[o.staged + __popc(nm & lanemask_lt())] = d;
+    __syncwarp();
+    o.staged += __popc(nm);
+}
+
+// Fold one vector's lanes into a minimum (messages prev[src] (+ weight)).
+template <typename T, int W, bool WEIGHT>
+__device__ __forceinline__ T fold_lanes(const uint32_t (&src)[W], const uint32_t (&wt)[W],
+                                        const T *__restrict__ prev, T INF, uint32_t &ovf) {
+    using VT = ValTraits<T>;
+    T ps[W];
+#pragma unroll
+    for (int l = 0; l < W; ++l) ps[l] = src[l] != WG_NO_LANE ? prev[src[l]] : INF;
+    T agg = INF;
+#pragma unroll
+    for (int l = 0; l < W; ++l) {
+        if constexpr (VT::U32) {
+            if (WEIGHT) {
+                if (ps[l] != INF) {
+                    uint64_t m = (uint64_t)ps[l] + wt[l];
+                    if (m >= 0xffffffffull) ovf = 1;
+                    else agg = (T)m < agg ? (T)m : agg;
+                }
+            } else {
+                agg = ps[l] < agg ? ps[l] : agg;  // INF never wins; no overflow without weights
+            }
+        } else {
+            if (src[l] != WG_NO_LANE) {
+                T m = ps[l] + (WEIGHT ? (T)wt[l] : (T)0);
+                agg = m < agg ? m : agg;
+            }
+        }
+    }
+    return agg;
+}
+
+// Warp-uniform carry of the open segment across tiles of a warp's range.
+template <typename T>
+struct Carry {
+    uint32_t d = NONE;
+    T agg, pd;
+    bool act = false, left = true;
+};
+
+// Reduce + apply one tile (32 lanes, lane order = item order).  The segment
+// min is a shuffle scan limited to each lane's distance from its segment head
+// (one SHFL + one predicated min per step, and only as many steps as the
+// longest segment in the tile needs).
+template <typename T>
+__device__ __forceinline__ void finish_tile(uint32_t d, T agg, T pd, bool act, bool first_tile,
+                                            bool last_tile, uint32_t dleft, uint32_t dright,
+                                            Carry<T> &cy, T INF, int64_t inc, T *nxt,
+                                            uint32_t *obits, PullOut &o, const wg_graph &g,
+                                            wg_iter_rec *out, uint32_t *overt, uint32_t *opref,
+                                            uint32_t n) {
+    const unsigned lane = lane_id();
+    const unsigned am = __ballot_sync(FULL, act);
+    o.touched += __popc(am);
+    const uint32_t d0 = __shfl_sync(FULL, d, 0);
+    bool left0;
+    if (cy.d == NONE) {
+        left0 = first_tile ? (dleft != d0) : true;
+    } else if (d0 == cy.d) {
+        if (lane == 0 && cy.act) agg = cy.agg < agg ? cy.agg : agg;
+        left0 = cy.left;
+    } else {
+        // the carried segment ended exactly at the previous tile's end
+        apply_segments<T>(lane == 0 && cy.act, cy.d, cy.agg, cy.pd, cy.left, INF, inc, nxt, obits, o);
+        left0 = true;
+    }
+    const uint32_t dp = __shfl_up_sync(FULL, d, 1);
+    const unsigned heads = __ballot_sync(FULL, lane == 0 || dp != d);
+    const unsigned h = 31u - __clz(heads & (0xffffffffu >> (31 - lane)));
+    const unsigned dist = lane - h;
+    const unsigned maxdist = __reduce_max_sync(FULL, dist);
+    for (unsigned off = 1; off <= maxdist; off <<= 1) {
+        const T ov = shfl_up_t(agg, (int)off);
+        if (off <= dist && ov < agg) agg = ov;
+    }
+    const bool tail = ((heads >> 1) | 0x80000000u) >> lane & 1u;
+    const bool left = h > 0 || left0;
+    const uint32_t d31 = __shfl_sync(FULL, d, 31);
+    const bool carry = !last_tile && d31 != NONE;
+    if (carry) {
+        cy.d = d31;
+        cy.agg = shfl_t(agg, 31);
+        cy.pd = shfl_t(pd, 31);
+        cy.act = (am >> 31) & 1u;
+        cy.left = (31u - __clz(heads)) > 0 || left0;
+    } else {
+        cy.d = NONE;
+    }
+    const bool right = !(lane == 31 && last_tile && dright == d);
+    const bool app = tail && act && !(carry && lane == 31);
+    apply_segments<T>(app, d, agg, pd, left && right, INF, inc, nxt, obits, o);
+    if (o.staged > STAGE - 34) flush_stage(o, g, out, overt, opref, n);
+}
+
+// ---------------------------------------------------------------------------
+// TMA helpers (cp.async.bulk + mbarrier; per-warp pipeline)
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_1d(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    uint32_t ok = 0;
+    const uint32_t a = smem_u32(bar);
+    while (true) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(ok)
+            : "r"(a), "r"(parity)
+            : "memory");
+        if (ok) break;
+    }
+}
+
+// Range of tiles owned by this warp (contiguous; balanced).
+__device__ __forceinline__ void warp_range(uint64_t ntiles, uint64_t gwarp, uint64_t nwarps,
+                                           uint64_t &t0, uint64_t &t1) {
+    const uint64_t per = ntiles / nwarps, extra = ntiles % nwarps;
+    t0 = gwarp * per + (gwarp < extra ? gwarp : extra);
+    t1 = t0 + per + (gwarp < extra ? 1 : 0);
+}
+
+template <typename T>
+__device__ __forceinline__ void end_of_pull(PullOut &o, wg_iter_rec *out) {
+    const uint64_t es = warp_sum(o.edge_sum);
+    const uint32_t ovf = __any_sync(FULL, o.ovf);
+    if (lane_id() == 0) {
+        if (o.touched) atomicAdd((unsigned long long *)&out->vectors_touched, (unsigned long long)o.touched);
+        if (es) atomicAdd((unsigned long long *)&out->out_edge_sum, (unsigned long long)es);
+        if (ovf) out->overflow = 1;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Direct-load pull: wedge mode, filtered (BFS) dense mode, and any width.
+template <typename T, int W, bool WEIGHT, bool FILTER, int U>
+__global__ void __launch_bounds__(PULL_THREADS) pull_kernel(LoopCtx c, wg_graph g, PullBufs b,
+                                                            int shift, int64_t inc, int64_t sentinel,
+                                                            int handles) {
+    using VT = ValTraits<T>;
+    __shared__ uint32_t s_stage[PULL_WARPS][STAGE];
     const uint64_t it = ctx_iter(c);
     const int mode = ctx_mode(c, it);
-    if (mode == MODE_NONE) return;
+    if (mode == MODE_NONE || !((handles >> mode) & 1)) return;
     const bool wedge = (mode == MODE_WEDGE);
     wg_iter_rec *out = ctx_out(c, it);
-    const T *__restrict__ prev = (const T *)b.vals[(it - 1) & 1];
-    T *__restrict__ nxt = (T *)b.vals[it & 1];
-    uint32_t *__restrict__ obits = b.fbits[it & 1];
-    uint32_t *__restrict__ overt = b.fvert[it & 1];
-    uint32_t *__restrict__ opref = b.fpref[it & 1];
+    const T *__restrict__ prev = (const T *)(((it - 1) & 1) ? b.vals[1] : b.vals[0]);
+    T *__restrict__ nxt = (T *)((it & 1) ? b.vals[1] : b.vals[0]);
+    uint32_t *__restrict__ obits = ((it & 1) ? b.fbits[1] : b.fbits[0]);
+    uint32_t *__restrict__ overt = ((it & 1) ? b.fvert[1] : b.fvert[0]);
+    uint32_t *__restrict__ opref = ((it & 1) ? b.fpref[1] : b.fpref[0]);
     const uint64_t nitems = wedge ? (out->groups << shift) : g.nvec;
     const T INF = VT::inf(sentinel);
     const unsigned lane = lane_id();
     const uint64_t gwarp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    const uint64_t ntiles = (nitems + 31) >> 5;
-    uint64_t touched = 0;
-    uint32_t ovf = 0;
+    PullOut o{s_stage[threadIdx.x >> 5], 0u, 0ull, 0ull, 0u};
 
-    for (uint64_t tile = gwarp; tile < ntiles; tile += nwarps) {
-        const uint64_t k = (tile << 5) + lane;
-        const uint64_t p = item_pos(k, nitems, wedge, b.glist, shift, g.nvec);
-        const bool valid = p != ~0ull;
-        const uint32_t d = valid ? g.vdst[p] : 0xffffffffu;
-        T pd = INF;
-        if (FILTER && valid) pd = prev[d];
-        const bool active = valid && !(FILTER && pd != INF);
-        T agg = INF;
-        if (active) {
-            uint32_t src[W];
-            load_lanes<W>(g.vsrc, p, src);
-            uint32_t wt[W];
-            if (WEIGHT) load_lanes<W>(g.vw, p, wt);
+    uint64_t t0, t1;
+    warp_range((nitems + 31) >> 5, gwarp, nwarps, t0, t1);
+    if (t0 < t1) {
+        uint32_t dleft = NONE, dright = NONE;
+        if (lane == 0 && t0 > 0) {
+            uint64_t q = item_pos((t0 << 5) - 1, nitems, wedge, b.glist, shift, g.nvec);
+            if (q != ~0ull) dleft = g.vdst[q];
+        }
+        if (lane == 1) {
+            uint64_t q = item_pos(t1 << 5, nitems, wedge, b.glist, shift, g.nvec);
+            if (q != ~0ull) dright = g.vdst[q];
+        }
+        dleft = __shfl_sync(FULL, dleft, 0);
+        dright = __shfl_sync(FULL, dright, 1);
+        Carry<T> cy;
+        for (uint64_t tile = t0; tile < t1; tile += U) {
+            uint32_t d[U];
+            T pd[U], agg[U];
+            bool act[U];
 #pragma unroll
-            for (int l = 0; l < W; ++l) {
-                if (src[l] == WG_NO_LANE) continue;
-                T ps = prev[src[l]];
-                if constexpr (VT::U32) {
-                    if (ps == INF) continue;
-                    uint64_t m = (uint64_t)ps + (WEIGHT ? wt[l] : 0u);
-                    if (m >= 0xffffffffull) { ovf = 1; continue; }
-                    agg = (T)min_u64(agg, m);
-                } else {
-                    T m = ps + (WEIGHT ? (T)wt[l] : (T)0);
-                    agg = m < agg ? m : agg;
+            for (int u = 0; u < U; ++u) {
+                const uint64_t p = (tile + u < t1)
+                                       ? item_pos(((tile + u) << 5) + lane, nitems, wedge, b.glist, shift, g.nvec)
+                                       : ~0ull;
+                d[u] = p != ~0ull ? g.vdst[p] : NONE;
+                pd[u] = INF;
+                agg[u] = INF;
+                if (FILTER && d[u] != NONE) pd[u] = prev[d[u]];
+                act[u] = d[u] != NONE && !(FILTER && pd[u] != INF);
+                if (act[u]) {
+                    uint32_t src[W], wt[W];
+                    load_lanes<W>(g.vsrc, p, src);
+                    if (WEIGHT) load_lanes<W>(g.vw, p, wt);
+                    if (!FILTER) pd[u] = prev[d[u]];
+                    agg[u] = fold_lanes<T, W, WEIGHT>(src, wt, prev, INF, o.ovf);
                 }
             }
-        }
-        touched += __popc(__ballot_sync(FULL, active));
-
-        // segmented inclusive min-scan keyed by destination
 #pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            T o = shfl_up_t(agg, off);
-            uint32_t od = __shfl_up_sync(FULL, d, off);
-            if ((int)lane >= off && od == d && o < agg) agg = o;
+            for (int u = 0; u < U; ++u) {
+                if (tile + u < t1)
+                    finish_tile<T>(d[u], agg[u], pd[u], act[u], tile + u == t0, tile + u == t1 - 1, dleft,
+                               dright, cy, INF, inc, nxt, obits, o, g, out, overt, opref, b.n);
+            }
         }
-        const uint32_t dn = __shfl_down_sync(FULL, d, 1);
-        const uint32_t dp = __shfl_up_sync(FULL, d, 1);
-        const bool head = lane == 0 || dp != d;
-        const bool tail = lane == 31 || dn != d;
-        const unsigned heads = __ballot_sync(FULL, head);
-        const unsigned head_lane = 31 - __clz(heads & (0xffffffffu >> (31 - lane)));
+        if (o.staged) flush_stage(o, g, out, overt, opref, b.n);
+    }
+    end_of_pull<T>(o, out);
+}
 
-        bool newly = false;
-        if (tail && active) {
-            // complete iff no neighbouring work item (outside the tile) has d
-            bool complete = true;
-            if (head_lane == 0 && (tile << 5) > 0) {
-                uint64_t q = item_pos((tile << 5) - 1, nitems, wedge, b.glist, shift, g.nvec);
-                if (q != ~0ull && g.vdst[q] == d) complete = false;
-            }
-            if (lane == 31) {
-                uint64_t q = item_pos((tile << 5) + 32, nitems, wedge, b.glist, shift, g.nvec);
-                if (q != ~0ull && g.vdst[q] == d) complete = false;
-            }
-            if (!FILTER) pd = prev[d];
-            bool upd;
-            T cand;
-            if constexpr (VT::U32) {
-                upd = false;
-                if (agg != INF) {
-                    uint64_t cc = (uint64_t)agg + (uint64_t)inc;
-                    if (cc >= 0xffffffffull) {
-                        ovf = 1;
-                    } else {
-                        cand = (T)cc;
-                        upd = cand < pd;
-                    }
-                }
-            } else {
-                cand = agg + (T)inc;
-                upd = cand < pd;
-            }
-            if (upd) {
-                if (complete) {
-                    nxt[d] = cand;
+// ---------------------------------------------------------------------------
+// Dense unfiltered pull fed by TMA: each warp streams its range through an
+// S-stage ring of CH-tile chunks (vsrc, vdst, vw) in shared memory.
+constexpr int TMA_CH = 2;  // tiles per stage
+constexpr int TMA_S = 4;   // stages per warp
+
+template <int W, bool WEIGHT>
+struct TmaSmem {
+    static constexpr int VEC = TMA_CH * 32;
+    static constexpr int SRC_WORDS = VEC * W;
+    static constexpr int STAGE_WORDS = SRC_WORDS + VEC + (WEIGHT ? SRC_WORDS : 0);
+    static constexpr size_t WARP_BYTES = (size_t)TMA_S * STAGE_WORDS * 4 + TMA_S * 8 + STAGE * 4;
+    static constexpr size_t BLOCK_BYTES = PULL_WARPS * WARP_BYTES;
+};
+
+__device__ __forceinline__ uint32_t pad16(uint32_t b) { return (b + 15u) & ~15u; }
+
+template <typename T, int W, bool WEIGHT>
+__global__ void __launch_bounds__(PULL_THREADS) pull_dense_tma_kernel(LoopCtx c, wg_graph g, PullBufs b,
+                                                                      int shift, int64_t inc,
+                                                                      int64_t sentinel) {
+    using VT = ValTraits<T>;
+    using SM = TmaSmem<W, WEIGHT>;
+    extern __shared__ __align__(128) unsigned char s_raw[];
+    const uint64_t it = ctx_iter(c);
+    const int mode = ctx_mode(c, it);
+    if (mode != MODE_FULL) return;  // wedge iterations use pull_kernel
+    wg_iter_rec *out = ctx_out(c, it);
+    const T *__restrict__ prev = (const T *)(((it - 1) & 1) ? b.vals[1] : b.vals[0]);
+    T *__restrict__ nxt = (T *)((it & 1) ? b.vals[1] : b.vals[0]);
+    uint32_t *__restrict__ obits = ((it & 1) ? b.fbits[1] : b.fbits[0]);
+    uint32_t *__restrict__ overt = ((it & 1) ? b.fvert[1] : b.fvert[0]);
+    uint32_t *__restrict__ opref = ((it & 1) ? b.fpref[1] : b.fpref[0]);
+    const uint64_t nvec = g.nvec;
+    const T INF = VT::inf(sentinel);
+    const unsigned lane = lane_id();
+    const unsigned wib = threadIdx.x >> 5;
+    const uint64_t gwarp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+
+    unsigned char *wbase = s_raw + (size_t)wib * SM::WARP_BYTES;
+    uint32_t *ring = reinterpret_cast<uint32_t *>(wbase);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(wbase + (size_t)TMA_S * SM::STAGE_WORDS * 4);
+    uint32_t *stage_buf = reinterpret_cast<uint32_t *>(bars + TMA_S);
+    PullOut o{stage_buf, 0u, 0ull, 0ull, 0u};
+
+    uint64_t t0, t1;
+    warp_range((nvec + 31) >> 5, gwarp, nwarps, t0, t1);
+    if (t0 < t1) {
+        const uint64_t nchunks = (t1 - t0 + TMA_CH - 1) / TMA_CH;
+        if (lane == 0) {
+            for (int s = 0; s < TMA_S; ++s) mbar_init(&bars[s], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncwarp();
+        auto issue = [&](uint64_t ch) {
+            const int s = (int)(ch % TMA_S);
+            const uint64_t v0 = (t0 + ch * TMA_CH) << 5;
+            uint64_t v1 = (t0 + (ch + 1) * TMA_CH) << 5;
+            const uint64_t vend = t1 << 5 < nvec ? t1 << 5 : nvec;
+            if (v1 > vend) v1 = vend;
+            const uint32_t nv = (uint32_t)(v1 - v0);
+            uint32_t *st = ring + (size_t)s * SM::STAGE_WORDS;
+            const uint32_t b_src = pad16(nv * W * 4), b_dst = pad16(nv * 4);
+            const uint32_t total = b_src + b_dst + (WEIGHT ? b_src : 0);
+            mbar_expect_tx(&bars[s], total);
+            tma_1d(st, g.vsrc + v0 * W, b_src, &bars[s]);
+            tma_1d(st + SM::SRC_WORDS, g.vdst + v0, b_dst, &bars[s]);
+            if (WEIGHT) tma_1d(st + SM::SRC_WORDS + SM::VEC, g.vw + v0 * W, b_src, &bars[s]);
+        };
+        if (lane == 0)
+            for (uint64_t ch = 0; ch < nchunks && ch < TMA_S; ++ch) issue(ch);
+        uint32_t dleft = NONE, dright = NONE;
+        if (lane == 0 && t0 > 0) dleft = g.vdst[(t0 << 5) - 1];
+        if (lane == 1 && (t1 << 5) < nvec) dright = g.vdst[t1 << 5];
+        dleft = __shfl_sync(FULL, dleft, 0);
+        dright = __shfl_sync(FULL, dright, 1);
+        Carry<T> cy;
+        const uint32_t tfirst = (uint32_t)t0, tlast = (uint32_t)t1 - 1, nv32 = (uint32_t)nvec;
+        for (uint32_t ch = 0; ch < (uint32_t)nchunks; ++ch) {
+            const int s = (int)(ch % TMA_S);
+            mbar_wait(&bars[s], (ch / TMA_S) & 1u);
+            const uint32_t *st = ring + (size_t)s * SM::STAGE_WORDS;
+            const uint32_t tbase = tfirst + ch * TMA_CH;
+            uint32_t d[TMA_CH];
+            uint32_t src[TMA_CH][W], wt[TMA_CH][W];
+            bool act[TMA_CH];
+#pragma unroll
+            for (int u = 0; u < TMA_CH; ++u) {
+                const uint32_t tile = tbase + u;
+                const bool valid = tile <= tlast && (tile << 5) + lane < nv32;
+                const int j = u * 32 + lane;
+                act[u] = valid;
+                d[u] = valid ? st[SM::SRC_WORDS + j] : NONE;
+                if constexpr (W == 4) {
+                    const uint4 v = *reinterpret_cast<const uint4 *>(st + j * 4);
+                    src[u][0] = v.x; src[u][1] = v.y; src[u][2] = v.z; src[u][3] = v.w;
                 } else {
-                    if constexpr (VT::U32) atomicMin((unsigned *)&nxt[d], (unsigned)cand);
-                    else atomicMin((long long *)&nxt[d], (long long)cand);
+#pragma unroll
+                    for (int l = 0; l < W; ++l) src[u][l] = st[j * W + l];
                 }
-                const uint32_t bit = 1u << (d & 31);
-                newly = !(atomicOr(&obits[d >> 5], bit) & bit);
+#pragma unroll
+                for (int l = 0; l < W; ++l) {
+                    if (!valid) src[u][l] = WG_NO_LANE;
+                    wt[u][l] = WEIGHT ? st[SM::SRC_WORDS + SM::VEC + j * W + l] : 0u;
+                }
+            }
+            __syncwarp();
+            // the stage is consumed (values in registers): refill it
+            if (lane == 0 && ch + TMA_S < nchunks) issue(ch + TMA_S);
+            T pd[TMA_CH], agg[TMA_CH];
+#pragma unroll
+            for (int u = 0; u < TMA_CH; ++u) {
+                pd[u] = act[u] ? prev[d[u]] : INF;
+                agg[u] = fold_lanes<T, W, WEIGHT>(src[u], wt[u], prev, INF, o.ovf);
+            }
+#pragma unroll
+            for (int u = 0; u < TMA_CH; ++u) {
+                const uint32_t tile = tbase + u;
+                if (tile <= tlast)
+                    finish_tile<T>(d[u], agg[u], pd[u], act[u], tile == tfirst, tile == tlast, dleft, dright,
+                               cy, INF, inc, nxt, obits, o, g, out, overt, opref, b.n);
             }
         }
-
-        // warp-aggregated append of newly activated destinations
-        const unsigned nm = __ballot_sync(FULL, newly);
-        if (nm) {
-            uint32_t len = 0, od = 0;
-            if (newly) {
-                len = (uint32_t)(g.idx_off[d + 1] - g.idx_off[d]);
-                od = g.outdeg[d];
-            }
-            const bool nz = newly && len > 0;
-            const unsigned nzm = __ballot_sync(FULL, nz);
-            const unsigned zm = nm & ~nzm;
-            const uint32_t incl = warp_inclusive_sum(nz ? len : 0u);
-            const uint32_t tot = __shfl_sync(FULL, incl, 31);
-            const uint64_t osum = warp_sum((uint64_t)od);
-            unsigned long long base = 0, zbase = 0;
-            if (lane == 0) {
-                if (nzm)
-                    base = atomicAdd((unsigned long long *)&out->nz_packed,
-                                     ((unsigned long long)__popc(nzm) << 32) | tot);
-                if (zm) zbase = atomicAdd((unsigned long long *)&out->z_count,
-                                          (unsigned long long)__popc(zm));
-                atomicAdd((unsigned long long *)&out->out_edge_sum, (unsigned long long)osum);
-            }
-            base = __shfl_sync(FULL, base, 0);
-            zbase = __shfl_sync(FULL, zbase, 0);
-            if (nz) {
-                uint64_t pos = (base >> 32) + __popc(nzm & lanemask_lt());
-                overt[pos] = d;
-                opref[pos] = (uint32_t)(base & 0xffffffffull) + (incl - len);
-            } else if (newly) {
-                uint64_t zpos = zbase + __popc(zm & lanemask_lt());
-                overt[b.n - 1 - zpos] = d;
-            }
-        }
+        if (o.staged) flush_stage(o, g, out, overt, opref, b.n);
     }
-    touched = warp_sum(touched) / 32;  // every lane counted the same ballots
-    ovf = __any_sync(FULL, ovf);
-    if (lane == 0) {
-        if (touched) atomicAdd((unsigned long long *)&out->vectors_touched, (unsigned long long)touched);
-        if (ovf) out->overflow = 1;
-    }
+    end_of_pull<T>(o, out);
 }
 
 // ---------------- K7: end of iteration -------------------------------------
@@ -233,17 +549,17 @@ __global__ void __launch_bounds__(256) finalize_kernel(LoopCtx c, PullBufs b) {
     if (mode != MODE_NONE) {
         const wg_iter_rec *out = ctx_out(c, it);
         const wg_iter_rec *in = ctx_in(c, it);
-        const T *src = (const T *)b.vals[it & 1];
-        T *dst = (T *)b.vals[(it - 1) & 1];
-        const uint32_t *list = b.fvert[it & 1];
+        const T *src = (const T *)((it & 1) ? b.vals[1] : b.vals[0]);
+        T *dst = (T *)(((it - 1) & 1) ? b.vals[1] : b.vals[0]);
+        const uint32_t *list = ((it & 1) ? b.fvert[1] : b.fvert[0]);
         uint64_t nz = out->nz_packed >> 32, z = out->z_count;
         for (uint64_t i = tid; i < nz + z; i += nthreads) {
             uint32_t v = i < nz ? list[i] : list[b.n - 1 - (i - nz)];
             dst[v] = src[v];
         }
         // clear bits of the frontier produced by it-1 (its bitmap is reused by it+1)
-        uint32_t *obits = b.fbits[(it - 1) & 1];
-        const uint32_t *plist = b.fvert[(it - 1) & 1];
+        uint32_t *obits = (((it - 1) & 1) ? b.fbits[1] : b.fbits[0]);
+        const uint32_t *plist = (((it - 1) & 1) ? b.fvert[1] : b.fvert[0]);
         uint64_t pnz = in->nz_packed >> 32, pz = in->z_count;
         uint64_t words = ((uint64_t)b.n + 31) >> 5;
         if (pnz + pz > words) {

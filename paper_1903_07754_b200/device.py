@@ -20,6 +20,7 @@ from ._lib import (WG_VAL_I64, WG_VAL_U32, NO_LANE, REC_FIELDS, REC_U64, WgGraph
                    WgRunBufs, WgRunParams, check)
 
 UNREACHED = 1 << 62  # engine.py:43
+SLACK = 16  # vectors of readable slack after vsrc / vdst / vw (TMA tail rounding)
 U32_INF = 0xFFFFFFFF
 
 
@@ -29,6 +30,13 @@ def _torch():
 
 def _ptr(t) -> Optional[int]:
     return None if t is None else int(t.data_ptr())
+
+
+def _padded(t, extra: int):
+    import torch
+    out = torch.zeros(t.numel() + extra, dtype=t.dtype, device=t.device)
+    out[: t.numel()].copy_(t)
+    return out[: t.numel()]
 
 
 def to_dev_u32(a, device="cuda"):
@@ -83,9 +91,10 @@ class DeviceGraph:
             raise ValueError("src/dst/weight lengths differ")
         cap = int(L.wg_vector_capacity(m, n, width))
         dev = s.device
-        vsrc = torch.empty(max(cap * width, 1), dtype=torch.int32, device=dev)
-        vdst = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
-        vw = torch.empty(max(cap * width, 1), dtype=torch.int32, device=dev) if w is not None else None
+        # +SLACK vectors: TMA bulk copies of the last chunk round up to 16 bytes
+        vsrc = torch.empty((cap + SLACK) * width, dtype=torch.int32, device=dev)
+        vdst = torch.empty(cap + SLACK, dtype=torch.int32, device=dev)
+        vw = torch.empty((cap + SLACK) * width, dtype=torch.int32, device=dev) if w is not None else None
         idx_off = torch.empty(n + 1, dtype=torch.int64, device=dev)
         idx_pos = torch.empty(max(m, 1), dtype=torch.int32, device=dev)
         outdeg = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
@@ -123,9 +132,12 @@ class DeviceGraph:
             raise ValueError("degrees do not fit in uint32")
         off = torch.from_numpy(np.ascontiguousarray(index.offsets, dtype=np.int64)).to(device)
         pos = np.asarray(index.positions, dtype=np.int64)
+        if vw is not None:
+            vw = _padded(vw, SLACK * width)
         return cls(n, width, int(topology.edge_count), nvec, int(pos.size),
-                   to_dev_u32(vs.ravel() if vs.size else np.zeros(1, np.uint32), device),
-                   to_dev_u32(np.asarray(topology.vec_dst, np.int64) if nvec else np.zeros(1, np.int64), device),
+                   _padded(to_dev_u32(vs.ravel() if vs.size else np.zeros(1, np.uint32), device), SLACK * width),
+                   _padded(to_dev_u32(np.asarray(topology.vec_dst, np.int64) if nvec else np.zeros(1, np.int64),
+                                      device), SLACK),
                    vw, off,
                    to_dev_u32(pos if pos.size else np.zeros(1, np.int64), device),
                    to_dev_u32(deg if deg.size else np.zeros(1, np.int64), device))
