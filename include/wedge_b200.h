@@ -179,6 +179,23 @@ int wg_run_enqueue(const wg_graph *g, const wg_run_bufs *b, const wg_run_params 
 int wg_run_enqueue_counter(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p,
                            uint32_t count, void *stream);
 
+/* ---------------- multi-GPU exchange ----------------------- */
+/* Destination-range sharding: each rank's layout holds the vectors of its
+ * destination range (global ids) and a local edge index; values and the
+ * frontier are replicated.  After wg_run_enqueue(it, 1):
+ *   wg_exchange_pack   copies the members produced by iteration `it` on this
+ *                      rank and their new values into d_verts / d_vals
+ *                      (capacity entries); h_count receives the count;
+ *   wg_exchange_apply  writes every rank's (vertex, value) pairs into both
+ *                      value buffers, marks them in the frontier bitmap and
+ *                      rebuilds the frontier list and record of `it` for the
+ *                      GLOBAL frontier (so every rank's next gate agrees). */
+int wg_exchange_pack(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p, uint64_t it,
+                     uint32_t *d_verts, void *d_vals, uint64_t capacity, uint64_t *h_count,
+                     void *stream);
+int wg_exchange_apply(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p, uint64_t it,
+                      const uint32_t *d_verts, const void *d_vals, uint64_t count, void *stream);
+
 /* ---------------- measurement --------------------------------------------- */
 /* Event timer: when attached to wg_run_params.timer, wg_run_enqueue records a
  * CUDA event pair (on the launch stream) around the Wedge preparation

@@ -57,6 +57,7 @@ EXPORTS = [
     "wg_run_enqueue", "wg_run_enqueue_counter", "wg_pagerank", "wg_rmat_edges",
     "wg_canonical_scratch_bytes", "wg_canonical_edges", "wg_weights_hash", "wg_grid_edges",
     "wg_timer_create", "wg_timer_destroy", "wg_timer_reset", "wg_timer_read", "wg_launch_count",
+    "wg_exchange_pack", "wg_exchange_apply",
 ]
 
 _LIB = None
@@ -124,6 +125,8 @@ def load(path: os.PathLike | str | None = None):
         "wg_timer_read": (ctypes.c_int, [c_vp, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(c_i32),
                                          ctypes.POINTER(c_i64), ctypes.c_int, ctypes.POINTER(ctypes.c_int)]),
         "wg_launch_count": (c_u64, []),
+        "wg_exchange_pack": (ctypes.c_int, [G, B, P, c_u64, c_vp, c_vp, c_u64, u64p, c_vp]),
+        "wg_exchange_apply": (ctypes.c_int, [G, B, P, c_u64, c_vp, c_vp, c_u64, c_vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -471,4 +471,94 @@ int wg_run_enqueue_counter(const wg_graph *g, const wg_run_bufs *b, const wg_run
     return WG_OK;
 }
 
+// ------------------------------------------------------- exchange (K10) --
+}  // extern "C"
+
+namespace {
+
+template <typename T>
+__global__ void exchange_pack_kernel(const uint32_t *list, uint64_t nz, uint64_t z, uint32_t n,
+                                     const T *vals, uint32_t *verts, T *out) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nz + z;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t v = i < nz ? list[i] : list[n - 1 - (i - nz)];
+        verts[i] = v;
+        out[i] = vals[v];
+    }
+}
+
+template <typename T>
+__global__ void exchange_apply_kernel(const uint32_t *verts, const T *in, uint64_t count, T *v0, T *v1,
+                                      uint32_t *bits) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t v = verts[i];
+        T x = in[i];
+        v0[v] = x;
+        v1[v] = x;
+        atomicOr(&bits[v >> 5], 1u << (v & 31));
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int wg_exchange_pack(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p, uint64_t it,
+                     uint32_t *d_verts, void *d_vals, uint64_t capacity, uint64_t *h_count,
+                     void *stream) {
+    int rc = check_run(g, b, p);
+    if (rc) return rc;
+    WG_REQUIRE(d_verts && d_vals && h_count, "null argument");
+    cudaStream_t s = as_stream(stream);
+    wg_iter_rec h;
+    WG_CUDA(cudaMemcpyAsync(&h, &b->recs[it % b->ring], sizeof(h), cudaMemcpyDeviceToHost, s));
+    WG_CUDA(cudaStreamSynchronize(s));
+    uint64_t nz = h.nz_packed >> 32, z = h.z_count;
+    *h_count = nz + z;
+    if (nz + z > capacity) {
+        set_error("exchange capacity %llu < %llu", (unsigned long long)capacity,
+                  (unsigned long long)(nz + z));
+        return WG_ENOSPACE;
+    }
+    if (nz + z == 0) return WG_OK;
+    unsigned grid = grid_for(nz + z, 256 * 4, 8);
+    const uint32_t *list = b->fvert[it & 1];
+    if (p->val_type == WG_VAL_U32)
+        exchange_pack_kernel<uint32_t><<<grid, 256, 0, s>>>(list, nz, z, g->n,
+                                                            (const uint32_t *)b->vals[it & 1], d_verts,
+                                                            (uint32_t *)d_vals);
+    else
+        exchange_pack_kernel<int64_t><<<grid, 256, 0, s>>>(list, nz, z, g->n,
+                                                           (const int64_t *)b->vals[it & 1], d_verts,
+                                                           (int64_t *)d_vals);
+    ::wg::count_launch();
+    WG_CHECK_LAUNCH("exchange_pack");
+    return WG_OK;
+}
+
+int wg_exchange_apply(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p, uint64_t it,
+                      const uint32_t *d_verts, const void *d_vals, uint64_t count, void *stream) {
+    int rc = check_run(g, b, p);
+    if (rc) return rc;
+    cudaStream_t s = as_stream(stream);
+    uint32_t *bits = b->fbits[it & 1];
+    if (count) {
+        WG_REQUIRE(d_verts && d_vals, "null argument");
+        unsigned grid = grid_for(count, 256 * 4, 8);
+        if (p->val_type == WG_VAL_U32)
+            exchange_apply_kernel<uint32_t><<<grid, 256, 0, s>>>(
+                d_verts, (const uint32_t *)d_vals, count, (uint32_t *)b->vals[0], (uint32_t *)b->vals[1], bits);
+        else
+            exchange_apply_kernel<int64_t><<<grid, 256, 0, s>>>(
+                d_verts, (const int64_t *)d_vals, count, (int64_t *)b->vals[0], (int64_t *)b->vals[1], bits);
+        ::wg::count_launch();
+        WG_CHECK_LAUNCH("exchange_apply");
+    }
+    // the global frontier of `it`: ordered list, index prefixes, counts and
+    // the global out-degree sum (the next gate's input) from the bitmap
+    return launch_frontier_compaction(g, bits, b->bcount, b->fvert[it & 1], b->fpref[it & 1],
+                                      &b->recs[it % b->ring], s);
+}
+
 }  // extern "C"

@@ -1,0 +1,210 @@
+"""Destination-range sharding across GPUs (the paper's
+multi-socket design, which the reference does not implement).
+
+Rank r owns a contiguous destination range chosen on destination boundaries
+so that every rank holds about the same number of vectors (balanced by edges,
+not vertices: RMAT puts the hubs at low ids and ~half the vertices have no
+in-edges).  Each rank keeps its own vectors, a local edge index over ALL
+sources (positions local to its slice), the global out-degrees, and full
+replicas of the values and of the frontier.  Per iteration:
+
+  1. every rank runs the gate on the same global frontier edge sum, so the
+     mode (Wedge / FullScan) is a global decision;
+  2. local Wedge transform + local pull (wg_run_enqueue, one iteration);
+  3. exchange: each rank packs the destinations it updated and their new
+     values (wg_exchange_pack) and all ranks all-gather them (NCCL over
+     NVLink on GPUs; the same code runs on gloo in the CPU tests); counts
+     first, then a padded all-gather (NCCL has no all-gatherv);
+  4. wg_exchange_apply writes the union into both value buffers and rebuilds
+     the global frontier list / edge sum for the next gate.
+
+The driver (``run_sharded``) is written against a small shard interface so
+that the exchange protocol is tested on CPU with world_size 2 (gloo) while
+the device shard (``DeviceShard``) runs the sm_100a kernels.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+from fractions import Fraction
+from typing import Optional
+
+import numpy as np
+
+
+# ---------------------------------------------------------------------------
+# Partitioning
+# ---------------------------------------------------------------------------
+def destination_bounds(indeg, width: int, world: int) -> list[int]:
+    """Split [0, n) into `world` destination ranges holding ~equal numbers of
+    W-lane vectors (vectors of d = ceil(indeg(d)/W), graph.py:240-243).
+    Ranges never split a destination (the kernels.py:39-52 invariant)."""
+    deg = np.asarray(indeg, dtype=np.int64)
+    n = int(deg.shape[0])
+    vec = (deg + width - 1) // width
+    cum = np.cumsum(vec)
+    total = int(cum[-1]) if n else 0
+    bounds = [0]
+    for k in range(1, world):
+        target = (k * total) // world
+        d = int(np.searchsorted(cum, target, side="left")) + 1 if total else 0
+        d = min(max(d, bounds[-1]), n)
+        bounds.append(d)
+    bounds.append(n)
+    return bounds
+
+
+# ---------------------------------------------------------------------------
+# Exchange
+# ---------------------------------------------------------------------------
+def all_gather_var(t, group=None):
+    """All-gather tensors of different lengths: counts first, then a padded
+    all-gather of equal-size buffers (works on nccl and gloo)."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    cnt = torch.tensor([t.numel()], dtype=torch.int64, device=t.device)
+    counts = [torch.zeros_like(cnt) for _ in range(world)]
+    dist.all_gather(counts, cnt, group=group)
+    counts = [int(c.item()) for c in counts]
+    maxc = max(counts)
+    if maxc == 0:
+        return t[:0]
+    buf = torch.zeros(maxc, dtype=t.dtype, device=t.device)
+    buf[: t.numel()].copy_(t)
+    parts = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(parts, buf, group=group)
+    return torch.cat([p[:c] for p, c in zip(parts, counts)])
+
+
+@dataclass
+class ShardRecord:
+    iteration: int
+    mode: str
+    active_edges: int
+    vectors_touched: int
+    frontier_out_size: int
+    out_edge_sum: int
+    covered_vectors: int = 0
+    transform_entries: int = 0
+
+
+def run_sharded(shard, max_iterations: int, group=None):
+    """The reference loop (engine.py:330-388) over destination shards:
+    local step, exchange of updated values, global frontier for the gate."""
+    import torch
+    import torch.distributed as dist
+    shard.seed()
+    recs: list[ShardRecord] = []
+    converged = False
+    it = 0
+    while it < max_iterations:
+        it += 1
+        verts, vals = shard.step(it)
+        all_v = all_gather_var(verts, group)
+        all_x = all_gather_var(vals, group)
+        rec = shard.apply(it, all_v, all_x)
+        recs.append(rec)
+        if rec.out_edge_sum == 0:
+            converged = True
+            break
+    # work counters are per shard: sum them across ranks (traces are global already)
+    if recs:
+        dev = shard.device if hasattr(shard, "device") else "cpu"
+        w = torch.tensor([[r.vectors_touched, r.covered_vectors, r.transform_entries] for r in recs],
+                         dtype=torch.int64, device=dev)
+        dist.all_reduce(w, group=group)
+        for r, row in zip(recs, w.cpu().tolist()):
+            r.vectors_touched, r.covered_vectors, r.transform_entries = row
+    return shard.values_int64(), recs, converged
+
+
+# ---------------------------------------------------------------------------
+# Device shard
+# ---------------------------------------------------------------------------
+class DeviceShard:
+    """One rank's destination shard on its GPU (uses the device loop for the
+    local iteration and the C-ABI exchange kernels)."""
+
+    device = "cuda"
+
+    def __init__(self, n: int, src, dst, weight, width: int, bounds: list[int], rank: int, kern,
+                 init_values: np.ndarray, init_members: Optional[np.ndarray], threshold: Fraction,
+                 shift: int, val_type: int):
+        import torch
+        from . import _lib
+        from . import device as dv
+        self.dv, self._lib = dv, _lib
+        lo, hi = bounds[rank], bounds[rank + 1]
+        s = dv.to_dev_u32(src)
+        d = dv.to_dev_u32(dst)
+        w = dv.to_dev_u32(weight) if weight is not None else None
+        d64 = d.to(torch.int64) & 0xFFFFFFFF
+        mask = (d64 >= lo) & (d64 < hi)
+        E = int(s.numel())
+        gdeg = torch.bincount(s.to(torch.int64) & 0xFFFFFFFF, minlength=n).to(torch.int32)
+        g = dv.DeviceGraph.build(n, s[mask], d[mask], w[mask] if w is not None else None, width)
+        # global out-degrees and |E| drive the (global) gate
+        self.g = dv.DeviceGraph(n, width, E, g.nvec, g.entries, g.vsrc, g.vdst, g.vw, g.idx_off,
+                                g.idx_pos, gdeg)
+        self.lo, self.hi, self.n = lo, hi, n
+        self.kern, self.threshold, self.shift, self.val_type = kern, threshold, shift, val_type
+        self.loop = dv.DeviceLoop(self.g, shift, val_type)
+        self.init = dv.encode_values(init_values, val_type)
+        self.words = dv.all_words(n) if init_members is None else dv.initial_words(n, init_members)
+        cap = max(hi - lo, 1)
+        self.out_v = torch.empty(cap, dtype=torch.int32, device="cuda")
+        self.out_x = torch.empty(cap, dtype=torch.int32 if val_type == _lib.WG_VAL_U32 else torch.int64,
+                                 device="cuda")
+        self.p = None
+
+    def seed(self):
+        self.p = self.loop.seed(self.init, self.words, self.kern, self.threshold)
+
+    def step(self, it: int):
+        L = self._lib.load()
+        self.loop.enqueue(self.p, it, 1)
+        cnt = ctypes.c_uint64(0)
+        self._lib.check(L.wg_exchange_pack(ctypes.byref(self.g.struct()), ctypes.byref(self.loop.bufs),
+                                           ctypes.byref(self.p), it, self.out_v.data_ptr(),
+                                           self.out_x.data_ptr(), self.out_v.numel(), ctypes.byref(cnt),
+                                           self._lib.stream_ptr()))
+        k = int(cnt.value)
+        return self.out_v[:k], self.out_x[:k]
+
+    def apply(self, it: int, verts, vals) -> ShardRecord:
+        L = self._lib.load()
+        self._lib.check(L.wg_exchange_apply(ctypes.byref(self.g.struct()), ctypes.byref(self.loop.bufs),
+                                            ctypes.byref(self.p), it, verts.data_ptr() if verts.numel() else None,
+                                            vals.data_ptr() if vals.numel() else None, int(verts.numel()),
+                                            self._lib.stream_ptr()))
+        r = self.loop._read(it, 1)[0]
+        if int(r[10]):
+            raise self._lib.OverflowError32(self._lib.WG_EOVERFLOW, "uint32 overflow in sharded loop")
+        mode = {1: "FullScan", 2: "Wedge"}.get(int(r[0]), "None")
+        return ShardRecord(it, mode, int(r[1]), int(r[2]), int(r[3]), int(r[4]),
+                           int(r[7]) if mode == "Wedge" else 0, int(r[8]) if mode == "Wedge" else 0)
+
+    def values_int64(self) -> np.ndarray:
+        # after wg_exchange_apply both value buffers hold the global state
+        return self.dv.values_to_int64(self.loop.vals[0], self.val_type)
+
+
+def run_sharded_device(n: int, src, dst, weight, width: int, program, config, group=None):
+    """Device entry point: run a MinPlusKernel program over destination
+    shards (one rank per GPU, torch.distributed initialised by the caller)."""
+    import torch
+    import torch.distributed as dist
+    from . import _lib
+    from .engine import _initial_members, _initial_values
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    d = torch.as_tensor(np.asarray(dst) if not isinstance(dst, torch.Tensor) else dst)
+    indeg = torch.bincount(d.to(torch.int64).cuda() & 0xFFFFFFFF, minlength=n).cpu().numpy()
+    bounds = destination_bounds(indeg, width, world)
+    init = _initial_values(program, n)
+    members = _initial_members(program, n)
+    shard = DeviceShard(n, src, dst, weight, width, bounds, rank, program.kernel, init, members,
+                        config.threshold.fraction, config.precision.shift, _lib.WG_VAL_U32)
+    return run_sharded(shard, config.max_iterations, group)

@@ -1,0 +1,202 @@
+"""CPU tests of the drop-in boundary and the host-side logic (no GPU).
+
+* the C-ABI library builds for sm_100a, loads, and exports every symbol
+  include/wedge_b200.h declares (no compute call is made without a GPU);
+* the product package never imports the oracle;
+* gate arithmetic, thresholds, precisions, bitmaps and the API's validation
+  behave like the reference (frontier.py, engine.py, apps.py).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import re
+from fractions import Fraction
+from pathlib import Path
+
+import numpy as np
+import pytest
+from hypothesis import given, settings
+from hypothesis import strategies as st
+
+ROOT = Path(__file__).resolve().parent.parent
+HEADER = ROOT / "include" / "wedge_b200.h"
+PKG = ROOT / "paper_1903_07754_b200"
+
+
+def declared_symbols():
+    text = HEADER.read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(wg_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_1903_07754_b200 import _build, _lib
+    _build.build()
+    lib = ctypes.CDLL(str(_lib.LIB_PATH))
+    syms = declared_symbols()
+    assert len(syms) >= 20
+    missing = [s for s in syms if not hasattr(lib, s)]
+    assert not missing, missing
+    assert set(syms) == set(_lib.EXPORTS)
+    L = _lib.load()
+    assert L.wg_abi_version() == 1
+    assert L.wg_vector_capacity(100, 10, 4) >= 25 + 10
+
+
+def test_library_is_sm100a():
+    import subprocess
+    from paper_1903_07754_b200 import _lib
+    out = subprocess.run(["cuobjdump", "--list-elf", str(_lib.LIB_PATH)], capture_output=True, text=True)
+    assert "sm_100a" in out.stdout, out.stdout[:500]
+    sass = subprocess.run(["cuobjdump", "-sass", str(_lib.LIB_PATH)], capture_output=True, text=True).stdout
+    assert "UBLKCP" in sass  # TMA bulk copies in the dense pull
+    assert "SYNCS.ARRIVE.TRANS64" in sass  # mbarrier pipeline
+
+
+def test_product_never_imports_oracle():
+    for f in PKG.rglob("*.py"):
+        src = f.read_text()
+        assert not re.search(r"^\s*(import|from)\s+oracle\b", src, flags=re.M), f
+    for f in (PKG / "csrc").glob("*"):
+        assert "wedge_oracle" not in f.read_text(), f
+
+
+def test_error_codes_and_message_without_gpu():
+    from paper_1903_07754_b200 import _lib
+    L = _lib.load()
+    # invalid arguments are rejected before touching the device
+    assert L.wg_build_layout(10, 5, None, None, None, 3, 0, None, None, None, None, None, None, None, 0,
+                             (ctypes.c_uint64 * 2)(), None) == _lib.WG_EINVAL
+    assert b"width" in L.wg_last_error()
+    assert L.wg_run_buffer_sizes(None, 0, (ctypes.c_uint64 * 4)()) == _lib.WG_EINVAL
+    assert L.wg_timer_create(0) is None
+
+
+def test_no_gpu_fails_loudly():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    import paper_1903_07754_b200 as wg
+    el = wg.EdgeList(3, [0, 1], [1, 2])
+    with pytest.raises(RuntimeError, match="CUDA device"):
+        wg.build_pull_topology(el, 4)
+
+
+# ---------------------------------------------------------------- gate ---
+@given(st.integers(0, 10**12), st.integers(1, 10**12), st.integers(0, 1000), st.integers(1, 1000))
+@settings(max_examples=300, deadline=None)
+def test_device_gate_limit_equals_rational_compare(edge_sum, edges, num, den):
+    """wedge iff sum*den < num*E (frontier.py:163-171) <=> sum < wedge_limit."""
+    from paper_1903_07754_b200.device import wedge_limit
+    if num > den:
+        num = den
+    thr = Fraction(num, den)
+    want = edge_sum * thr.denominator < thr.numerator * edges
+    assert (edge_sum < wedge_limit(thr, edges)) == want
+
+
+def test_gate_known_answers():
+    """pkg/tests/test_frontier.py:63-90."""
+    import paper_1903_07754_b200 as wg
+    deg = np.array([2, 1, 1, 1, 1, 1])
+    f = wg.VertexFrontier.from_vertices([3], deg, 6)
+    assert wg.should_transform(f, 7, wg.FullnessThreshold.of("0.20"))
+    f = wg.VertexFrontier.from_vertices([0], deg, 6)
+    assert not wg.should_transform(f, 7, wg.FullnessThreshold.of("0.20"))
+    assert wg.should_transform(wg.VertexFrontier.empty(6), 7, wg.FullnessThreshold.of("0.01"))
+    assert not wg.should_transform(f, 7, wg.FullnessThreshold(Fraction(2, 7)))  # tie -> full
+    with pytest.raises(ValueError):
+        wg.should_transform(wg.VertexFrontier.empty(6), 0, wg.FullnessThreshold.of(1))
+    with pytest.raises(ValueError):
+        wg.FullnessThreshold(Fraction(3, 2))
+    with pytest.raises(ValueError):
+        wg.FrontierPrecision(3)
+    assert wg.FullnessThreshold.of(0.01).fraction == Fraction(1, 100)
+    assert [wg.FrontierPrecision(v).shift for v in (1, 2, 4, 8, 16)] == [0, 1, 2, 3, 4]
+
+
+def test_vertex_frontier_semantics():
+    import paper_1903_07754_b200 as wg
+    deg = np.array([2, 1, 1, 1, 1, 1])
+    f = wg.VertexFrontier.empty(6)
+    f.insert(0, deg)
+    f.insert(0, deg)
+    f.insert(3, deg)
+    assert f.member_edge_sum == 3 and f.member_count() == 2
+    with pytest.raises(IndexError):
+        f.insert(6, deg)
+    assert f.recount_edge_sum(deg) == 3
+
+
+@given(st.lists(st.integers(0, 199), max_size=80))
+@settings(max_examples=100, deadline=None)
+def test_bitmask_matches_set_semantics(ids):
+    """Bitmask memory image: bit i in uint64 word i>>6 at i&63 (bitmask.py:15-32)."""
+    import oracle
+    from paper_1903_07754_b200 import Bitmask
+    bm = Bitmask.from_indices(200, ids)
+    ref = np.zeros(4, np.uint64)
+    oracle.set_bits(ref, ids)
+    assert np.array_equal(bm.words, ref)
+    assert bm.indices().tolist() == sorted(set(ids))
+    assert bm.count() == len(set(ids))
+    b2 = Bitmask(200)
+    fresh = [b2.set(i) for i in ids]
+    assert sum(fresh) == len(set(ids)) and b2 == bm
+
+
+def test_wedge_frontier_covered_count():
+    import paper_1903_07754_b200 as wg
+    w = wg.WedgeFrontier.from_groups([0, 2], 5, wg.FrontierPrecision(2))
+    assert w.group_count == 3 and w.covered_vector_count() == 3  # group 2 clipped to 1 vector
+    assert wg.WedgeFrontier(6, wg.FrontierPrecision(2)).is_empty()
+
+
+def test_programs_and_config_validation():
+    import paper_1903_07754_b200 as wg
+    with pytest.raises(ValueError):
+        wg.make_program("pagerank")  # pkg/tests/test_apps.py:167-169
+    with pytest.raises(ValueError):
+        wg.make_program("bfs")
+    with pytest.raises(ValueError):
+        wg.bfs_program(-1)
+    assert wg.make_program("cc").kernel == wg.MinPlusKernel(False, False, 0)
+    assert wg.make_program("bfs", 3).kernel == wg.MinPlusKernel(True, False, 1)
+    assert wg.make_program("sssp", 0).needs_weights
+    for bad in (dict(workers=0), dict(max_iterations=0), dict(slice_size=0)):
+        with pytest.raises(ValueError):
+            wg.EngineConfig(**bad)
+    # apply algebra (apps.py:17-25)
+    assert wg.bfs_program(0).apply(5, None) == (5, False)
+    assert wg.bfs_program(0).apply(5, 2) == (3, True)
+    assert wg.cc_program().apply(2, 2) == (2, False)
+
+
+def test_edge_list_validation():
+    import paper_1903_07754_b200 as wg
+    with pytest.raises(ValueError):
+        wg.EdgeList(3, [0, 3], [1, 1])
+    with pytest.raises(ValueError):
+        wg.EdgeList(3, [0, 1], [1, 1], [1, 0])
+    with pytest.raises(ValueError):
+        wg.EdgeList(3, [0], [1, 2])
+    el = wg.EdgeList.from_pairs([(0, 1, 5), (1, 2, 3)])
+    assert el.vertex_count == 3 and el.is_weighted() and list(el.edges()) == [(0, 1, 5), (1, 2, 3)]
+
+
+def test_digest_is_reference_digest():
+    import oracle
+    import paper_1903_07754_b200 as wg
+    v = np.array([0, 1, 1, wg.UNREACHED])
+    assert wg.result_digest(v) == oracle.result_digest(v)
+
+
+def test_genspec_parsing():
+    import paper_1903_07754_b200 as wg
+    assert wg.GenSpec.parse("rmat:14:16").scale == 14
+    assert wg.GenSpec.parse("grid:3:4").cols == 4
+    with pytest.raises(ValueError):
+        wg.GenSpec.parse("rmat:14")
+    with pytest.raises(ValueError):
+        wg.GenSpec("rmat", scale=4, edge_factor=2, probs=(0.5, 0.5, 0.5, 0.5))

@@ -1,0 +1,154 @@
+"""Multi-rank destination sharding on CPU: world_size 2 over gloo.
+
+The product's sharded driver (paper_1903_07754_b200.distributed.run_sharded,
+its partitioning and its all-gather exchange) runs unchanged; each rank's
+local compute is a CPU stand-in built from the oracle (test infrastructure)
+over that rank's destination shard.  The union must reproduce the
+single-process reference run: identical values and per-iteration traces
+(mode, active edges, produced frontier size)."""
+
+from __future__ import annotations
+
+import os
+import socket
+from fractions import Fraction
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+from paper_1903_07754_b200.distributed import ShardRecord, destination_bounds, run_sharded
+
+
+class OracleShard:
+    """CPU stand-in for DeviceShard: the shard's vectors and local index in
+    the reference layout, driven through the same step / apply protocol."""
+
+    device = "cpu"
+
+    def __init__(self, n, src, dst, w, width, bounds, rank, app, root, threshold, vpg):
+        lo, hi = bounds[rank], bounds[rank + 1]
+        m = (dst >= lo) & (dst < hi)
+        self.topo = oracle.build_pull_topology(n, src[m], dst[m], None if w is None else w[m], width)
+        self.idx = oracle.build_edge_index(self.topo)
+        self.deg = oracle.compute_out_degrees(n, src)  # global out-degrees
+        self.E = len(src)
+        self.n, self.app, self.root, self.thr, self.vpg = n, app, root, threshold, vpg
+        self.kern = oracle.kern_of(app)
+
+    def seed(self):
+        vals, front = oracle.initial_state(self.app, self.n, self.root)
+        self.prev, self.nxt = vals.copy(), vals.copy()
+        self.fwords = np.zeros(oracle.word_count(self.n), np.uint64)
+        oracle.set_bits(self.fwords, front)
+        self.edge_sum = int(self.deg[np.unique(front)].sum())
+
+    def step(self, it):
+        be = oracle.PortBackend(1)
+        np.copyto(self.nxt, self.prev)
+        out = np.zeros(oracle.word_count(self.n), np.uint64)
+        self.active = self.edge_sum
+        num, den = self.thr.numerator, self.thr.denominator
+        shift = self.vpg.bit_length() - 1
+        if self.E > 0 and self.edge_sum * den < num * self.E:
+            groups = (self.topo.vector_count + self.vpg - 1) // self.vpg
+            ww = np.zeros(oracle.word_count(groups), np.uint64)
+            be.transform(self.fwords, self.n, self.idx.offsets, self.idx.positions, shift, ww)
+            self.touched = be.pull_wedge(self.topo, ww, shift, groups, self.prev, self.nxt, out, self.kern,
+                                         oracle.UNREACHED)
+            self.mode = "Wedge"
+        else:
+            self.touched = be.pull_full(self.topo, self.prev, self.nxt, out, self.kern, oracle.UNREACHED)
+            self.mode = "FullScan"
+        ch = oracle.bit_indices(out, self.n)
+        return torch.from_numpy(ch.astype(np.int64)), torch.from_numpy(self.nxt[ch].copy())
+
+    def apply(self, it, verts, vals):
+        v = verts.numpy()
+        self.nxt[v] = vals.numpy()
+        self.prev, self.nxt = self.nxt, self.prev
+        self.fwords = np.zeros(oracle.word_count(self.n), np.uint64)
+        oracle.set_bits(self.fwords, v)
+        self.edge_sum = int(self.deg[v].sum()) if v.size else 0
+        return ShardRecord(it, self.mode, self.active, self.touched, int(v.size), self.edge_sum)
+
+    def values_int64(self):
+        return self.prev
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, case, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n, src, dst, w, app, thr, vpg = case
+        bounds = destination_bounds(np.bincount(dst, minlength=n), 4, world)
+        shard = OracleShard(n, src, dst, w, 4, bounds, rank, app, 0, thr, vpg)
+        vals, recs, conv = run_sharded(shard, 10_000)
+        if rank == 0:
+            q.put((vals, [(r.iteration, r.mode, r.active_edges, r.frontier_out_size) for r in recs], conv,
+                   bounds))
+    finally:
+        dist.destroy_process_group()
+
+
+def _single(case):
+    n, src, dst, w, app, thr, vpg = case
+    topo = oracle.build_pull_topology(n, src, dst, w, 4)
+    idx = oracle.build_edge_index(topo)
+    deg = oracle.compute_out_degrees(n, src)
+    vals, front = oracle.initial_state(app, n, 0)
+    out = oracle.run_until_convergence(topo, idx, deg, oracle.kern_of(app), vals, front, thr, vpg)
+    return out.values, list(oracle.trace(out.stats)), out.converged
+
+
+def _case(app, scale=10):
+    n, s, d = oracle.rmat_edges(scale, 8, 5)
+    keep = s != d
+    s, d, _ = oracle.symmetrize(s[keep], d[keep], None, dedup=True)
+    w = oracle.synthesize_weights(s, d, 255) if app == "sssp" else None
+    thr = {"bfs": Fraction(1, 100), "cc": Fraction(1, 5), "sssp": Fraction(1, 5)}[app]
+    vpg = 8 if app == "bfs" else 4
+    return n, s, d, w, app, thr, vpg
+
+
+@pytest.mark.parametrize("app", ["bfs", "cc", "sssp"])
+def test_two_rank_sharded_run_matches_single(app):
+    case = _case(app)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, case, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    vals, trace, conv, bounds = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want_vals, want_trace, want_conv = _single(case)
+    assert 0 < bounds[1] < case[0]
+    assert np.array_equal(vals, want_vals)
+    assert [tuple(t) for t in trace] == [tuple(t) for t in want_trace]
+    assert conv == want_conv
+
+
+def test_destination_bounds_balance_and_alignment():
+    rng = np.random.default_rng(0)
+    deg = (rng.pareto(0.7, 5000) * 4).astype(np.int64)
+    for world in (1, 2, 4, 8):
+        b = destination_bounds(deg, 4, world)
+        assert b[0] == 0 and b[-1] == len(deg) and all(x <= y for x, y in zip(b, b[1:]))
+        vec = (deg + 3) // 4
+        parts = [vec[b[i]:b[i + 1]].sum() for i in range(world)]
+        assert sum(parts) == vec.sum()
+        assert max(parts) - min(parts) <= 2 * vec.max() + 1
