@@ -57,6 +57,22 @@ GRID_SEED = 2
 METRIC = "GTEPS"
 
 
+def rle_modes(recs) -> str:
+    """Mode sequence, run-length encoded: e.g. "F3W3" (FullScan x3, Wedge x3)."""
+    out, prev, cnt = [], None, 0
+    for r in recs:
+        m = "W" if r.mode == "Wedge" else "F"
+        if m == prev:
+            cnt += 1
+        else:
+            if prev:
+                out.append(f"{prev}{cnt}")
+            prev, cnt = m, 1
+    if prev:
+        out.append(f"{prev}{cnt}")
+    return "".join(out)
+
+
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
@@ -144,6 +160,9 @@ def run_b200(args, wl):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
+    if (world > 1 or args.sharded) and wl["app"] != "pr":
+        return run_b200_sharded(args, wl, rank, world, local)
+
     t0 = time.perf_counter()
     el, topo = make_graph(wl)
     torch.cuda.synchronize()
@@ -182,7 +201,7 @@ def run_b200(args, wl):
     values = dv.values_to_int64(loop.values_after(last), _lib.WG_VAL_U32)
     digest = wg.result_digest(values)
     iters = len(recs)
-    modes = "".join("W" if r.mode == "Wedge" else "F" for r in recs)
+    modes = rle_modes(recs)
     log(f"[bench] {iters} iterations ({modes}), converged={conv}, digest={digest}")
 
     # ---- timed region: K steps, events per step, L2 flushed in between ----
@@ -223,10 +242,10 @@ def run_b200(args, wl):
     out = {
         "metric": METRIC, "value": round(gteps, 4), "unit": "GTEPS (|E|/time-to-solution)",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
         "data": "synthetic (device RMAT, reference PCG64 stream)",
         "config": {"workload": wl["desc"], "app": app, "V": n, "E": E, "W": 4, "vpg": wl["vpg"],
-                   "threshold": wl["thr"], "iterations": iters, "modes": modes,
+                   "threshold": wl["thr"], "iterations": iters, "modes": modes, "parallelism": "1 GPU",
                    "l2": "inputs larger than L2 + 256 MB flush between steps",
                    "build_s": round(build_s, 2), "tts_ms": round(ms, 4)},
         "parity": {"digest": digest, "expected": wl.get("expect_digest"),
@@ -245,6 +264,79 @@ def run_b200(args, wl):
         print(json.dumps(out), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+def run_b200_sharded(args, wl, rank, world, local):
+    """N GPUs: destination-range shards of the same graph (strong scaling),
+    per-iteration exchange of updated values by NCCL all-gather; the time of
+    a step is the max over ranks (CUDA events on each rank's stream)."""
+    import torch
+    import torch.distributed as dist
+    import paper_1903_07754_b200 as wg
+    from paper_1903_07754_b200 import _lib
+    from paper_1903_07754_b200.distributed import DeviceShard, destination_bounds, run_sharded
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        dist.init_process_group("nccl", rank=rank, world_size=world,
+                                device_id=torch.device("cuda", local))
+    t0 = time.perf_counter()
+    if "grid" in wl:
+        el = wg.grid_graph(wl["grid"][0], wl["grid"][1], GRID_SEED, 0.9, 1000)
+    else:
+        el = wg.generate(wg.GenSpec("rmat", scale=wl["scale"], edge_factor=wl["ef"], seed=1))
+        el = wg.drop_self_loops_dedup(el, symmetric=wl["sym"])
+        if wl.get("weights"):
+            el = wg.synthesize_weights(el, wl["weights"])
+    s, d, w = el.device_arrays()
+    n, E = el.vertex_count, el.edge_count
+    indeg = torch.bincount(d.to(torch.int64) & 0xFFFFFFFF, minlength=n).cpu().numpy()
+    bounds = destination_bounds(indeg, 4, world)
+    app = wl["app"]
+    prog = wg.make_program(app, None if app == "cc" else 0)
+    shift = {1: 0, 2: 1, 4: 2, 8: 3, 16: 4}[wl["vpg"]]
+    shard = DeviceShard(n, s, d, w, 4, bounds, rank, prog.kernel, prog.initial_values(n),
+                        None if app == "cc" else np.array([0]), Fraction(wl["thr"]), shift, _lib.WG_VAL_U32)
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t0
+    max_it = n + 16
+    for _ in range(args.warmup):
+        vals, recs, conv = run_sharded(shard, max_it)
+    digest = wg.result_digest(vals)
+    dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = _lib.launch_count()
+    stream = torch.cuda.current_stream()
+    ts = []
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            vals, recs, conv = run_sharded(shard, max_it)
+            b.record(stream)
+            b.synchronize()
+            ts.append(a.elapsed_time(b))
+    dist.barrier()
+    launches = _lib.launch_count() - launches0
+    t = torch.tensor([float(np.mean(ts))], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    out = {
+        "metric": METRIC, "value": round(E / (ms * 1e-3) / 1e9, 4), "unit": "GTEPS (|E|/time-to-solution)",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic (device RMAT, reference PCG64 stream)",
+        "config": {"workload": wl["desc"], "app": app, "V": n, "E": E, "W": 4, "vpg": wl["vpg"],
+                   "threshold": wl["thr"], "iterations": len(recs), "parallelism": f"dst-shard x{world}",
+                   "bounds": bounds, "build_s": round(build_s, 2),
+                   "l2": "inputs larger than L2"},
+        "parity": {"digest": digest, "expected": wl.get("expect_digest"),
+                   "ok": (digest == wl["expect_digest"]) if wl.get("expect_digest") else None},
+        "gpu_launches": int(launches), "clocks": clk.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    dist.destroy_process_group()
 
 
 def roofline(rows, recs, n, E, weighted, filt, wl):
@@ -302,7 +394,9 @@ def roofline(rows, recs, n, E, weighted, filt, wl):
             "peak_source": peak_src,
             "algorithmic_bytes_per_launch": round(traffic, 1) if traffic else None,
             "wedge_iters_achieved_gbs": round(wedge_b / (wedge_t * 1e-3) / 1e9, 1) if wedge_t else None,
-            "kernel_sum_ms": round(step_t, 4), "per_iteration": per_iter}
+            "kernel_sum_ms": round(step_t, 4),
+            "per_iteration": per_iter if len(per_iter) <= 16 else per_iter[:8] + per_iter[-2:],
+            "iterations_timed": len(per_iter)}
 
 
 def e2e_b200(args, wl, g, loop, dinit, words, kern, thr, max_it):
@@ -422,7 +516,7 @@ def run_pagerank(args, wl, el, topo, build_s):
     out = {"metric": METRIC, "value": round(20 * E / (ms * 1e-3) / 1e9, 4),
            "unit": "GTEPS (20*|E|/time, PageRank)", "n_gpus": 1, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
-           "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+           "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
            "config": {"workload": wl["desc"], "V": n, "E": E, "build_s": round(build_s, 2)},
            "gpu_launches": int(_lib.launch_count() - launches0),
            "roofline": {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
@@ -501,7 +595,7 @@ def run_reference(args, wl):
         "impl": "reference", "metric": METRIC, "value": round(val, 5),
         "unit": "GTEPS (|E|/time-to-solution)", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
         "config": {"workload": wl["desc"], "V": n, "E": E, "iterations": len(out.stats)},
         "parity": {"digest": oracle.result_digest(out.values), "expected": wl.get("expect_digest")},
         "cpu_baseline": {"value": round(val, 5), "unit": "GTEPS", "cores": threads, "kind": kind,
@@ -519,6 +613,7 @@ def main():
     ap.add_argument("--workload", default="cc22", choices=sorted(WORKLOADS))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sharded", action="store_true", help="use the multi-GPU sharded path even at N=1")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
     wl = WORKLOADS[args.workload]

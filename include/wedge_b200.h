@@ -179,6 +179,24 @@ int wg_run_enqueue(const wg_graph *g, const wg_run_bufs *b, const wg_run_params 
 int wg_run_enqueue_counter(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p,
                            uint32_t count, void *stream);
 
+/* CUDA graph of `count` iterations driven by the device iteration counter
+ * (b->ctrl[0]); each launch advances the counter by `count`.  The graph is
+ * captured on `stream` once and replayed with wg_run_graph_launch; the host
+ * reads the records after each replay.  Returns an opaque handle or NULL. */
+void *wg_run_graph_create(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p,
+                          uint32_t count, void *stream);
+int wg_run_graph_launch(void *graph, void *stream);
+void wg_run_graph_destroy(void *graph);
+/* Device-resident loop as ONE CUDA graph: a conditional WHILE node whose body
+ * is one iteration followed by a single-thread kernel that advances the
+ * device iteration counter and clears the loop condition when the produced
+ * frontier has no out-edges (engine.py:386) or the iteration limit is hit.
+ * wg_run_loop_launch runs iterations ctrl[0]+1 .. at most max_iteration with
+ * no host round trip; the host then reads ctrl[0] and the records. */
+void *wg_run_loop_graph_create(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p,
+                               void *stream);
+int wg_run_loop_launch(void *graph, const wg_run_bufs *b, uint64_t max_iteration, void *stream);
+
 /* ---------------- multi-GPU exchange ----------------------- */
 /* Destination-range sharding: each rank's layout holds the vectors of its
  * destination range (global ids) and a local edge index; values and the

@@ -57,7 +57,8 @@ EXPORTS = [
     "wg_run_enqueue", "wg_run_enqueue_counter", "wg_pagerank", "wg_rmat_edges",
     "wg_canonical_scratch_bytes", "wg_canonical_edges", "wg_weights_hash", "wg_grid_edges",
     "wg_timer_create", "wg_timer_destroy", "wg_timer_reset", "wg_timer_read", "wg_launch_count",
-    "wg_exchange_pack", "wg_exchange_apply",
+    "wg_exchange_pack", "wg_exchange_apply", "wg_run_graph_create", "wg_run_graph_launch",
+    "wg_run_graph_destroy", "wg_run_loop_graph_create", "wg_run_loop_launch",
 ]
 
 _LIB = None
@@ -127,6 +128,11 @@ def load(path: os.PathLike | str | None = None):
         "wg_launch_count": (c_u64, []),
         "wg_exchange_pack": (ctypes.c_int, [G, B, P, c_u64, c_vp, c_vp, c_u64, u64p, c_vp]),
         "wg_exchange_apply": (ctypes.c_int, [G, B, P, c_u64, c_vp, c_vp, c_u64, c_vp]),
+        "wg_run_graph_create": (c_vp, [G, B, P, c_u32, c_vp]),
+        "wg_run_graph_launch": (ctypes.c_int, [c_vp, c_vp]),
+        "wg_run_graph_destroy": (None, [c_vp]),
+        "wg_run_loop_graph_create": (c_vp, [G, B, P, c_vp]),
+        "wg_run_loop_launch": (ctypes.c_int, [c_vp, B, c_u64, c_vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

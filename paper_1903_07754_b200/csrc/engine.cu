@@ -349,6 +349,25 @@ int wg_run_buffer_sizes(const wg_graph *g, int shift, uint64_t *h_sizes4) {
     return WG_OK;
 }
 
+}  // extern "C"
+
+namespace {
+// Advance the device iteration counter and decide whether the WHILE body runs
+// again: stop once the iteration did not run or produced a frontier without
+// out-edges (engine.py:356-386), or at the launch's iteration limit.
+__global__ void loop_step_kernel(cudaGraphConditionalHandle h, uint64_t *ctrl, const wg_iter_rec *recs,
+                                 uint32_t ring) {
+    uint64_t it = ctrl[0] + 1;
+    ctrl[0] = it;
+    const wg_iter_rec &r = recs[it % ring];
+    bool stop = r.mode == 0 || r.out_edge_sum == 0 || it >= ctrl[1];
+    cudaGraphSetConditional(h, stop ? 0u : 1u);
+}
+__global__ void set_limit_kernel(uint64_t *ctrl, uint64_t limit) { ctrl[1] = limit; }
+}  // namespace
+
+extern "C" {
+
 static LoopCtx loop_ctx(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p,
                         const uint64_t *ctrl, uint64_t it) {
     LoopCtx c{};
@@ -468,6 +487,124 @@ int wg_run_enqueue_counter(const wg_graph *g, const wg_run_bufs *b, const wg_run
     }
     bump_counter_kernel<<<1, 1, 0, s>>>(b->ctrl, count); ::wg::count_launch();
     WG_CHECK_LAUNCH("bump");
+    return WG_OK;
+}
+
+// ---------------------------------------------------------- CUDA graph --
+void *wg_run_graph_create(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p,
+                          uint32_t count, void *stream) {
+    if (check_run(g, b, p)) return nullptr;
+    (void)stream;
+    cudaStream_t s = nullptr;
+    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) {
+        set_error("cudaStreamCreate failed");
+        return nullptr;
+    }
+    struct StreamGuard {
+        cudaStream_t s;
+        ~StreamGuard() { cudaStreamDestroy(s); }
+    } guard{s};
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+        set_error("cudaStreamBeginCapture failed");
+        return nullptr;
+    }
+    int rc = wg_run_enqueue_counter(g, b, p, count, (void *)s);
+    cudaError_t e = cudaStreamEndCapture(s, &graph);
+    if (rc != WG_OK || e != cudaSuccess) {
+        if (graph) cudaGraphDestroy(graph);
+        if (rc == WG_OK) cuda_fail(e, "cudaStreamEndCapture");
+        return nullptr;
+    }
+    e = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) {
+        cuda_fail(e, "cudaGraphInstantiate");
+        return nullptr;
+    }
+    return (void *)exec;
+}
+
+int wg_run_graph_launch(void *graph, void *stream) {
+    WG_REQUIRE(graph, "null graph");
+    WG_CUDA(cudaGraphLaunch((cudaGraphExec_t)graph, as_stream(stream)));
+    return WG_OK;
+}
+
+void wg_run_graph_destroy(void *graph) {
+    if (graph) cudaGraphExecDestroy((cudaGraphExec_t)graph);
+}
+
+void *wg_run_loop_graph_create(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p,
+                               void *stream) {
+    if (check_run(g, b, p)) return nullptr;
+    (void)stream;
+    // capture on a private stream (the legacy default stream cannot capture)
+    cudaStream_t s = nullptr;
+    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) {
+        set_error("cudaStreamCreate failed");
+        return nullptr;
+    }
+    struct StreamGuard {
+        cudaStream_t s;
+        ~StreamGuard() { cudaStreamDestroy(s); }
+    } guard{s};
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    if (cudaGraphCreate(&graph, 0) != cudaSuccess) {
+        set_error("cudaGraphCreate failed");
+        return nullptr;
+    }
+    cudaGraphConditionalHandle handle;
+    cudaError_t e = cudaGraphConditionalHandleCreate(&handle, graph, 1, cudaGraphCondAssignDefault);
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = handle;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    if (e == cudaSuccess) e = cudaGraphAddNode(&node, graph, nullptr, 0, &cp);
+    if (e != cudaSuccess) {
+        cudaGraphDestroy(graph);
+        cuda_fail(e, "conditional node");
+        return nullptr;
+    }
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    e = cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) {
+        cudaGraphDestroy(graph);
+        cuda_fail(e, "cudaStreamBeginCaptureToGraph");
+        return nullptr;
+    }
+    wg_run_params q = *p;
+    q.timer = nullptr;
+    LoopCtx c = loop_ctx(g, b, &q, b->ctrl, 1);
+    int rc = enqueue_one(g, b, &q, c, s);
+    loop_step_kernel<<<1, 1, 0, s>>>(handle, b->ctrl, b->recs, b->ring);
+    ::wg::count_launch();
+    e = cudaStreamEndCapture(s, &body);
+    if (rc != WG_OK || e != cudaSuccess) {
+        cudaGraphDestroy(graph);
+        if (rc == WG_OK) cuda_fail(e, "cudaStreamEndCapture");
+        return nullptr;
+    }
+    e = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) {
+        cuda_fail(e, "cudaGraphInstantiate");
+        return nullptr;
+    }
+    return (void *)exec;
+}
+
+int wg_run_loop_launch(void *graph, const wg_run_bufs *b, uint64_t max_iteration, void *stream) {
+    WG_REQUIRE(graph && b && b->ctrl, "null argument");
+    cudaStream_t s = as_stream(stream);
+    set_limit_kernel<<<1, 1, 0, s>>>(b->ctrl, max_iteration);
+    ::wg::count_launch();
+    WG_CHECK_LAUNCH("set_limit");
+    WG_CUDA(cudaGraphLaunch((cudaGraphExec_t)graph, s));
     return WG_OK;
 }
 

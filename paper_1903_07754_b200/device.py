@@ -394,8 +394,80 @@ class DeviceLoop:
         arr = self.host_recs.numpy().view(np.uint64).reshape(self.ring, REC_U64)
         return [arr[(it_begin + j) % self.ring] for j in range(count)]
 
-    def drive(self, p: WgRunParams, max_iterations: int, trace=None, stream=None):
-        """Enqueue batches until convergence or the cap; returns (records, converged, last_it)."""
+    def _graph_for(self, p: WgRunParams, stream=None):
+        key = (p.val_type, p.shift, p.kern.filter_unvisited, p.kern.use_weight, p.kern.apply_increment,
+               p.kern.sentinel, p.wedge_limit)
+        exe = self.graph_cache.get(key)
+        if exe is None:
+            q = WgRunParams()
+            ctypes.pointer(q)[0] = p
+            q.timer = None
+            L = _lib.load()
+            exe = L.wg_run_loop_graph_create(ctypes.byref(self.g.struct()), ctypes.byref(self.bufs),
+                                             ctypes.byref(q), _lib.stream_ptr(stream))
+            if not exe:
+                raise _lib.WedgeError(_lib.WG_ECUDA, L.wg_last_error().decode())
+            self.graph_cache[key] = exe
+        return exe
+
+    def __del__(self):
+        try:
+            L = _lib.load()
+            for exe in self.graph_cache.values():
+                L.wg_run_graph_destroy(exe)
+        except Exception:
+            pass
+
+    def _parse(self, rows, it0, records, trace):
+        """Append records of iterations it0.. until one did not run or converged."""
+        for j, r in enumerate(rows):
+            mode = int(r[0])
+            if mode == 0:
+                return True, None
+            if int(r[10]):
+                raise _lib.OverflowError32(_lib.WG_EOVERFLOW, "uint32 value overflow in device loop")
+            records.append(IterRecord(it0 + j, MODE_NAMES[mode], int(r[1]), int(r[2]), int(r[3]),
+                                      int(r[7]) if mode == 2 else 0, int(r[8]) if mode == 2 else 0))
+            if trace is not None:
+                trace(self, it0 + j)
+            if int(r[4]) == 0:
+                return True, it0 + j
+        return False, None
+
+    def drive_graph(self, p: WgRunParams, max_iterations: int, stream=None):
+        """Whole loop as one conditional CUDA graph per launch (no host round
+        trip between iterations); at most ring-2 iterations per launch."""
+        torch = _torch()
+        s = stream or torch.cuda.current_stream()
+        L = _lib.load()
+        exe = self._graph_for(p, stream)
+        records: list[IterRecord] = []
+        it, converged, last = 1, False, 0
+        ctrl_host = torch.zeros(4, dtype=torch.int64).pin_memory()
+        while it <= max_iterations and not converged:
+            limit = min(max_iterations, it - 1 + self.ring - 2)
+            check(L.wg_run_loop_launch(exe, ctypes.byref(self.bufs), limit, _lib.stream_ptr(stream)))
+            ctrl_host.copy_(self.ctrl, non_blocking=True)
+            s.synchronize()
+            done = int(ctrl_host[0])
+            rows = self._read(it, done - it + 1, stream) if done >= it else []
+            conv, at = self._parse(rows, it, records, None)
+            if records:
+                last = records[-1].iteration
+            if conv:
+                converged = True
+            it = done + 1
+        return records, converged, last
+
+    def drive(self, p: WgRunParams, max_iterations: int, trace=None, stream=None, graph=None):
+        """Run to convergence or the cap; returns (records, converged, last_it).
+        Default: one conditional-graph launch per ring of iterations; trace
+        mode (frontier/value logs) steps one iteration at a time."""
+        import os
+        if graph is None:
+            graph = os.environ.get("WG_GRAPH", "1") != "0"
+        if trace is None and graph and p.timer is None:
+            return self.drive_graph(p, max_iterations, stream)
         records: list[IterRecord] = []
         converged = False
         it, batch, last = 1, 2, 0
