@@ -77,10 +77,40 @@ PullFn pick_pull(int val_type, int width, bool weight, bool filter) {
                                   : pick_pull_t<int64_t>(width, weight, filter);
 }
 
+// TMA dense-pull configuration (tiles per stage, stages, min blocks/SM);
+// WG_TMA_CFG=0|1|2 selects among the compiled variants for experiments.
+// Persistent sparse loop on/off (WG_SPARSE_LOOP=0 disables it).
+bool g_sparse_loop = [] {
+    const char *e = getenv("WG_SPARSE_LOOP");
+    return !(e && e[0] == '0');
+}();
+
+int g_tma_cfg = [] {
+    const char *e = getenv("WG_TMA_CFG");
+    return e ? atoi(e) : 0;
+}();
+
+template <typename T, int W, bool WEIGHT>
+DenseFn pick_dense_wt(size_t *smem) {
+    switch (g_tma_cfg) {
+        case 1:
+            *smem = TmaSmem<W, WEIGHT, 4, 2>::BLOCK_BYTES;
+            return pull_dense_tma_kernel<T, W, WEIGHT, 4, 2, 1>;
+        case 2:
+            *smem = TmaSmem<W, WEIGHT, 4, 2>::BLOCK_BYTES;
+            return pull_dense_tma_kernel<T, W, WEIGHT, 4, 2, 2>;
+        case 3:
+            *smem = TmaSmem<W, WEIGHT, 2, 3>::BLOCK_BYTES;
+            return pull_dense_tma_kernel<T, W, WEIGHT, 2, 3, 3>;
+        default:
+            *smem = TmaSmem<W, WEIGHT, 2, 4>::BLOCK_BYTES;
+            return pull_dense_tma_kernel<T, W, WEIGHT, 2, 4, 1>;
+    }
+}
+
 template <typename T, int W>
 DenseFn pick_dense_w(bool weight, size_t *smem) {
-    *smem = weight ? TmaSmem<W, true>::BLOCK_BYTES : TmaSmem<W, false>::BLOCK_BYTES;
-    return weight ? pull_dense_tma_kernel<T, W, true> : pull_dense_tma_kernel<T, W, false>;
+    return weight ? pick_dense_wt<T, W, true>(smem) : pick_dense_wt<T, W, false>(smem);
 }
 
 // TMA-streamed dense pull (unfiltered programs only).
@@ -167,30 +197,110 @@ int launch_frontier_compaction(const wg_graph *g, const uint32_t *words, uint64_
 }
 
 int launch_transform(const LoopCtx &c, const wg_graph *g, uint32_t *const fvert[2],
-                     uint32_t *const fpref[2], int shift, uint32_t *gbits, cudaStream_t s) {
+                     uint32_t *const fpref[2], int shift, uint32_t *gbits, cudaStream_t s,
+                     int append = 0, uint32_t *glist = nullptr, uint64_t ngroups = 0) {
     unsigned grid = persistent_grid(transform_kernel, TR_THREADS, (g->entries + TR_TILE - 1) / TR_TILE);
     transform_kernel<<<grid, TR_THREADS, 0, s>>>(c, fvert[0], fvert[1], fpref[0], fpref[1], g->idx_off,
-                                                 g->idx_pos, shift, gbits); ::wg::count_launch();
+                                                 g->idx_pos, shift, gbits, append, glist, ngroups);
+    ::wg::count_launch();
     WG_CHECK_LAUNCH("transform");
     return WG_OK;
 }
 
+using SparseFn = void (*)(LoopCtx, wg_graph, PullBufs, int, int64_t, int64_t, uint32_t *, uint64_t);
+
+template <typename T, int W>
+SparseFn pick_sparse_w(bool weight, bool filter) {
+    if (weight) return filter ? pull_sparse_kernel<T, W, true, true> : pull_sparse_kernel<T, W, true, false>;
+    return filter ? pull_sparse_kernel<T, W, false, true> : pull_sparse_kernel<T, W, false, false>;
+}
+
+SparseFn pick_sparse(int val_type, int width, bool weight, bool filter) {
+    bool u32 = val_type == WG_VAL_U32;
+    switch (width) {
+        case 1: return u32 ? pick_sparse_w<uint32_t, 1>(weight, filter) : pick_sparse_w<int64_t, 1>(weight, filter);
+        case 2: return u32 ? pick_sparse_w<uint32_t, 2>(weight, filter) : pick_sparse_w<int64_t, 2>(weight, filter);
+        case 4: return u32 ? pick_sparse_w<uint32_t, 4>(weight, filter) : pick_sparse_w<int64_t, 4>(weight, filter);
+        case 8: return u32 ? pick_sparse_w<uint32_t, 8>(weight, filter) : pick_sparse_w<int64_t, 8>(weight, filter);
+    }
+    return nullptr;
+}
+
+using LoopFn = void (*)(LoopCtx, wg_graph, PullBufs, int, int64_t, int64_t, uint32_t *, uint64_t);
+
+template <typename T, int W>
+LoopFn pick_loop_w(bool weight, bool filter) {
+    if (weight) return filter ? sparse_loop_kernel<T, W, true, true> : sparse_loop_kernel<T, W, true, false>;
+    return filter ? sparse_loop_kernel<T, W, false, true> : sparse_loop_kernel<T, W, false, false>;
+}
+
+LoopFn pick_loop(int val_type, int width, bool weight, bool filter) {
+    bool u32 = val_type == WG_VAL_U32;
+    switch (width) {
+        case 1: return u32 ? pick_loop_w<uint32_t, 1>(weight, filter) : pick_loop_w<int64_t, 1>(weight, filter);
+        case 2: return u32 ? pick_loop_w<uint32_t, 2>(weight, filter) : pick_loop_w<int64_t, 2>(weight, filter);
+        case 4: return u32 ? pick_loop_w<uint32_t, 4>(weight, filter) : pick_loop_w<int64_t, 4>(weight, filter);
+        case 8: return u32 ? pick_loop_w<uint32_t, 8>(weight, filter) : pick_loop_w<int64_t, 8>(weight, filter);
+    }
+    return nullptr;
+}
+
+// Cooperative launch of the persistent sparse loop (all blocks co-resident).
+int launch_sparse_loop(const LoopCtx &c, const wg_graph *g, const PullBufs &pb, int val_type, int shift,
+                       const wg_minplus *k, uint32_t *gbits, uint64_t ngroups, cudaStream_t s) {
+    LoopFn fn = pick_loop(val_type, (int)g->width, k->use_weight != 0, k->filter_unvisited != 0);
+    WG_REQUIRE(fn != nullptr, "no sparse loop kernel for width %u", g->width);
+    int per_sm = 0;
+    WG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, PULL_THREADS, 0));
+    WG_REQUIRE(per_sm >= 1, "sparse loop kernel does not fit on an SM");
+    if (per_sm > 2) per_sm = 2;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(sm_count() * per_sm));
+    cfg.blockDim = dim3(PULL_THREADS);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    WG_CUDA(cudaLaunchKernelEx(&cfg, fn, c, *g, pb, shift, (int64_t)k->apply_increment, (int64_t)k->sentinel,
+                               gbits, ngroups));
+    ::wg::count_launch();
+    return WG_OK;
+}
+
+int launch_pull_sparse(const LoopCtx &c, const wg_graph *g, const PullBufs &pb, int val_type, int shift,
+                       const wg_minplus *k, uint32_t *gbits, uint64_t ngroups, cudaStream_t s) {
+    SparseFn fn = pick_sparse(val_type, (int)g->width, k->use_weight != 0, k->filter_unvisited != 0);
+    WG_REQUIRE(fn != nullptr, "no sparse pull kernel for width %u", g->width);
+    unsigned grid = persistent_grid(fn, PULL_THREADS, (g->nvec + 255) / 256);
+    fn<<<grid, PULL_THREADS, 0, s>>>(c, *g, pb, shift, k->apply_increment, k->sentinel, gbits, ngroups);
+    ::wg::count_launch();
+    WG_CHECK_LAUNCH("pull (sparse)");
+    return WG_OK;
+}
+
+// only: 0 = everything the gate may need (non-graph path); MODE_FULL / MODE_WEDGE
+// = just that mode's kernels (conditional graph bodies).
 int launch_pull(const LoopCtx &c, const wg_graph *g, const PullBufs &pb, int val_type, int shift,
-                const wg_minplus *k, uint64_t max_items, cudaStream_t s) {
+                const wg_minplus *k, uint64_t max_items, cudaStream_t s, int only = 0) {
     const bool weight = k->use_weight != 0, filter = k->filter_unvisited != 0;
     WG_REQUIRE(!weight || g->vw, "weighted kernel on an unweighted layout");
     PullFn fn = pick_pull(val_type, (int)g->width, weight, filter);
     WG_REQUIRE(fn != nullptr, "no pull kernel for width %u", g->width);
     int handles = (1 << MODE_FULL) | (1 << MODE_WEDGE);
-    if (!filter && g_dense_tma && (c.forced_mode == 0 || c.forced_mode == MODE_FULL)) {
+    if (only) handles = 1 << only;
+    const bool want_full = only == 0 || only == MODE_FULL;
+    if (!filter && g_dense_tma && want_full && (c.forced_mode == 0 || c.forced_mode == MODE_FULL)) {
         size_t smem = 0;
         DenseFn dn = pick_dense(val_type, (int)g->width, weight, &smem);
         unsigned grid = persistent_grid(dn, PULL_THREADS, (g->nvec + 255) / 256, smem);
         dn<<<grid, PULL_THREADS, smem, s>>>(c, *g, pb, shift, k->apply_increment, k->sentinel);
         ::wg::count_launch();
         WG_CHECK_LAUNCH("pull (dense, TMA)");
-        handles = 1 << MODE_WEDGE;
-        if (c.forced_mode == MODE_FULL) return WG_OK;
+        handles &= ~(1 << MODE_FULL);
+        if (c.forced_mode == MODE_FULL || handles == 0) return WG_OK;
     }
     unsigned grid = persistent_grid(fn, PULL_THREADS, (max_items + 255) / 256);
     fn<<<grid, PULL_THREADS, 0, s>>>(c, *g, pb, shift, k->apply_increment, k->sentinel, handles);
@@ -357,13 +467,37 @@ namespace {
 // out-edges (engine.py:356-386), or at the launch's iteration limit.
 __global__ void loop_step_kernel(cudaGraphConditionalHandle h, uint64_t *ctrl, const wg_iter_rec *recs,
                                  uint32_t ring) {
-    uint64_t it = ctrl[0] + 1;
+    const uint64_t it = ctrl[0] + 1;
+    if (it > ctrl[1]) {  // the persistent sparse loop already reached the launch limit
+        cudaGraphSetConditional(h, 0u);
+        return;
+    }
     ctrl[0] = it;
     const wg_iter_rec &r = recs[it % ring];
-    bool stop = r.mode == 0 || r.out_edge_sum == 0 || it >= ctrl[1];
+    const bool stop = r.mode == 0 || r.out_edge_sum == 0 || it >= ctrl[1];
     cudaGraphSetConditional(h, stop ? 0u : 1u);
 }
 __global__ void set_limit_kernel(uint64_t *ctrl, uint64_t limit) { ctrl[1] = limit; }
+
+// Device-side gate of the graph body: FullScan, Wedge through the ordered
+// group list, or Wedge through the sparse (append) path when the transform
+// work is small against the group bitmap (no bitmap scans are worth it).
+__global__ void decide_kernel(LoopCtx c, cudaGraphConditionalHandle hf, cudaGraphConditionalHandle hs,
+                              cudaGraphConditionalHandle hp, uint64_t ngroups, int has_entries) {
+    const uint64_t it = ctx_iter(c);
+    const int mode = ctx_mode(c, it);
+    int variant = 0;
+    if (mode == MODE_FULL) {
+        variant = 1;
+    } else if (mode == MODE_WEDGE) {
+        const uint64_t entries = ctx_in(c, it)->nz_packed & 0xffffffffull;
+        variant = (has_entries && entries * 8 < ngroups) ? 3 : 2;
+    }
+    ctx_out(c, it)->reserved[0] = (uint64_t)variant;
+    cudaGraphSetConditional(hf, variant == 1 ? 1u : 0u);
+    cudaGraphSetConditional(hs, variant == 2 ? 1u : 0u);
+    cudaGraphSetConditional(hp, variant == 3 ? 1u : 0u);
+}
 }  // namespace
 
 extern "C" {
@@ -419,6 +553,7 @@ int wg_run_init(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p,
     uint64_t groups = groups_of(g, p->shift);
     WG_CUDA(cudaMemsetAsync(b->recs, 0, sizeof(wg_iter_rec) * b->ring, s));
     WG_CUDA(cudaMemsetAsync(b->ctrl, 0, 4 * sizeof(uint64_t), s));
+    WG_CUDA(cudaMemsetAsync(b->ctrl + 1, 0xff, sizeof(uint64_t), s));  // no iteration limit
     WG_CUDA(cudaMemsetAsync(b->fbits[0], 0, words * 4, s));
     WG_CUDA(cudaMemsetAsync(b->fbits[1], 0, words * 4, s));
     WG_CUDA(cudaMemsetAsync(b->gbits, 0, ((groups + 31) >> 5) * 4, s));
@@ -536,31 +671,57 @@ void wg_run_graph_destroy(void *graph) {
     if (graph) cudaGraphExecDestroy((cudaGraphExec_t)graph);
 }
 
+// Append a conditional IF node to the graph being captured on `s` (after
+// everything captured so far) and return its body graph.
+static cudaError_t capture_if_node(cudaStream_t s, cudaGraphConditionalHandle h, cudaGraph_t *inner) {
+    cudaStreamCaptureStatus st;
+    cudaGraph_t g = nullptr;
+    const cudaGraphNode_t *deps = nullptr;
+    size_t ndeps = 0;
+    cudaError_t e = cudaStreamGetCaptureInfo(s, &st, nullptr, &g, &deps, &ndeps);
+    if (e != cudaSuccess) return e;
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeIf;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    e = cudaGraphAddNode(&node, g, deps, ndeps, &cp);
+    if (e != cudaSuccess) return e;
+    e = cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies);
+    *inner = cp.conditional.phGraph_out[0];
+    return e;
+}
+
 void *wg_run_loop_graph_create(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p,
                                void *stream) {
     if (check_run(g, b, p)) return nullptr;
     (void)stream;
-    // capture on a private stream (the legacy default stream cannot capture)
-    cudaStream_t s = nullptr;
-    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) {
+    // capture on private streams (the legacy default stream cannot capture)
+    cudaStream_t s = nullptr, s2 = nullptr;
+    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking) != cudaSuccess) {
         set_error("cudaStreamCreate failed");
         return nullptr;
     }
     struct StreamGuard {
-        cudaStream_t s;
-        ~StreamGuard() { cudaStreamDestroy(s); }
-    } guard{s};
+        cudaStream_t a, b;
+        ~StreamGuard() {
+            if (a) cudaStreamDestroy(a);
+            if (b) cudaStreamDestroy(b);
+        }
+    } guard{s, s2};
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     if (cudaGraphCreate(&graph, 0) != cudaSuccess) {
         set_error("cudaGraphCreate failed");
         return nullptr;
     }
-    cudaGraphConditionalHandle handle;
-    cudaError_t e = cudaGraphConditionalHandleCreate(&handle, graph, 1, cudaGraphCondAssignDefault);
+    cudaGraphConditionalHandle hw;
+    cudaError_t e = cudaGraphConditionalHandleCreate(&hw, graph, 1, cudaGraphCondAssignDefault);
     cudaGraphNodeParams cp = {};
     cp.type = cudaGraphNodeTypeConditional;
-    cp.conditional.handle = handle;
+    cp.conditional.handle = hw;
     cp.conditional.type = cudaGraphCondTypeWhile;
     cp.conditional.size = 1;
     cudaGraphNode_t node;
@@ -571,22 +732,72 @@ void *wg_run_loop_graph_create(const wg_graph *g, const wg_run_bufs *b, const wg
         return nullptr;
     }
     cudaGraph_t body = cp.conditional.phGraph_out[0];
-    e = cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+    cudaGraphConditionalHandle hf, hs, hp;
+    e = cudaGraphConditionalHandleCreate(&hf, body, 0, cudaGraphCondAssignDefault);
+    if (e == cudaSuccess) e = cudaGraphConditionalHandleCreate(&hs, body, 0, cudaGraphCondAssignDefault);
+    if (e == cudaSuccess) e = cudaGraphConditionalHandleCreate(&hp, body, 0, cudaGraphCondAssignDefault);
+    if (e == cudaSuccess)
+        e = cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
     if (e != cudaSuccess) {
         cudaGraphDestroy(graph);
-        cuda_fail(e, "cudaStreamBeginCaptureToGraph");
+        cuda_fail(e, "loop body capture");
         return nullptr;
     }
     wg_run_params q = *p;
     q.timer = nullptr;
     LoopCtx c = loop_ctx(g, b, &q, b->ctrl, 1);
-    int rc = enqueue_one(g, b, &q, c, s);
-    loop_step_kernel<<<1, 1, 0, s>>>(handle, b->ctrl, b->recs, b->ring);
+    const uint64_t groups = groups_of(g, q.shift);
+    uint32_t *fv[2] = {b->fvert[0], b->fvert[1]};
+    uint32_t *fp[2] = {b->fpref[0], b->fpref[1]};
+    PullBufs pb = pull_bufs(g, b);
+    int rc = WG_OK;
+    // 0. as many consecutive sparse Wedge iterations as possible, persistently
+    if (g_sparse_loop && g->entries && g->nvec)
+        rc = launch_sparse_loop(c, g, pb, q.val_type, q.shift, &q.kern, b->gbits, groups, s);
+    // 1. device-side gate: which of the three bodies runs this iteration
+    decide_kernel<<<1, 1, 0, s>>>(c, hf, hs, hp, groups, g->entries > 0 ? 1 : 0);
     ::wg::count_launch();
-    e = cudaStreamEndCapture(s, &body);
-    if (rc != WG_OK || e != cudaSuccess) {
+    // 2. IF FullScan: dense pull
+    cudaGraph_t inner;
+    if ((e = capture_if_node(s, hf, &inner)) == cudaSuccess &&
+        (e = cudaStreamBeginCaptureToGraph(s2, inner, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal)) ==
+            cudaSuccess) {
+        if (g->nvec) rc = launch_pull(c, g, pb, q.val_type, q.shift, &q.kern, g->nvec, s2, MODE_FULL);
+        e = cudaStreamEndCapture(s2, &inner);
+    }
+    // 3. IF Wedge (large frontier): transform -> ordered group list -> pull
+    if (rc == WG_OK && e == cudaSuccess && (e = capture_if_node(s, hs, &inner)) == cudaSuccess &&
+        (e = cudaStreamBeginCaptureToGraph(s2, inner, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal)) ==
+            cudaSuccess) {
+        if (g->entries) rc = launch_transform(c, g, fv, fp, q.shift, b->gbits, s2);
+        if (rc == WG_OK && groups)
+            rc = launch_group_compaction(c, b->gbits, groups, b->bcount, b->glist, 1, q.shift, g->nvec, s2);
+        if (rc == WG_OK && g->nvec) rc = launch_pull(c, g, pb, q.val_type, q.shift, &q.kern, g->nvec, s2, MODE_WEDGE);
+        e = cudaStreamEndCapture(s2, &inner);
+    }
+    // 4. IF Wedge (sparse frontier): transform appends groups -> unsorted pull
+    if (rc == WG_OK && e == cudaSuccess && (e = capture_if_node(s, hp, &inner)) == cudaSuccess &&
+        (e = cudaStreamBeginCaptureToGraph(s2, inner, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal)) ==
+            cudaSuccess) {
+        if (g->entries) rc = launch_transform(c, g, fv, fp, q.shift, b->gbits, s2, 1, b->glist, groups);
+        if (rc == WG_OK && g->nvec) rc = launch_pull_sparse(c, g, pb, q.val_type, q.shift, &q.kern, b->gbits, groups, s2);
+        e = cudaStreamEndCapture(s2, &inner);
+    }
+    // 5. end of iteration + loop control
+    if (rc == WG_OK && e == cudaSuccess) {
+        unsigned grid = (unsigned)sm_count() * 2;
+        if (q.val_type == WG_VAL_U32)
+            finalize_kernel<uint32_t><<<grid, 256, 0, s>>>(c, pb);
+        else
+            finalize_kernel<int64_t><<<grid, 256, 0, s>>>(c, pb);
+        ::wg::count_launch();
+        loop_step_kernel<<<1, 1, 0, s>>>(hw, b->ctrl, b->recs, b->ring);
+        ::wg::count_launch();
+    }
+    cudaError_t e2 = cudaStreamEndCapture(s, &body);
+    if (rc != WG_OK || e != cudaSuccess || e2 != cudaSuccess) {
         cudaGraphDestroy(graph);
-        if (rc == WG_OK) cuda_fail(e, "cudaStreamEndCapture");
+        if (rc == WG_OK) cuda_fail(e != cudaSuccess ? e : e2, "loop body capture");
         return nullptr;
     }
     e = cudaGraphInstantiate(&exec, graph, 0);

@@ -233,68 +233,127 @@ __device__ __forceinline__ uint64_t block_search(const uint32_t *pref, uint64_t 
     return lo;
 }
 
-__global__ void __launch_bounds__(TR_THREADS) transform_kernel(
-    LoopCtx c, const uint32_t *fvert0, const uint32_t *fvert1, const uint32_t *fpref0,
-    const uint32_t *fpref1, const uint64_t *idx_off, const uint32_t *idx_pos, int shift,
-    uint32_t *gbits) {
-    uint64_t it = ctx_iter(c);
-    if (ctx_mode(c, it) != MODE_WEDGE) return;
+struct TransformSmem {
+    uint32_t pref[TR_TILE + 1];
+    uint64_t base[TR_TILE + 1];
+    uint64_t tmp[2];
+    uint32_t app[TR_TILE];  // groups newly selected by this block in this tile (append mode)
+    uint32_t napp;
+};
+
+// Set the group bits of one bitmap word; in append mode (unsorted Wedge path)
+// newly set groups are staged in shared memory and appended to the group list
+// with one global atomic per block tile.
+__device__ __forceinline__ void or_group_bits(uint32_t *gbits, uint32_t word, uint32_t bits, int append,
+                                              TransformSmem &sm) {
+    if (!append) {
+        atomicOr(&gbits[word], bits);
+        return;
+    }
+    uint32_t fresh = bits & ~atomicOr(&gbits[word], bits);
+    if (!fresh) return;
+    uint32_t pos = atomicAdd(&sm.napp, (uint32_t)__popc(fresh));
+    while (fresh) {
+        const int b = __ffs(fresh) - 1;
+        fresh &= fresh - 1;
+        sm.app[pos++] = (word << 5) + b;
+    }
+}
+
+__device__ __forceinline__ void flush_appended(TransformSmem &sm, uint32_t *glist, wg_iter_rec *out,
+                                               uint64_t ngroups) {
+    __syncthreads();
+    const uint32_t k = sm.napp;
+    if (k) {
+        if (threadIdx.x == 0)
+            sm.tmp[1] = atomicAdd((unsigned long long *)&out->groups, (unsigned long long)k);
+        __syncthreads();
+        const uint64_t base = sm.tmp[1];
+        for (uint32_t i = threadIdx.x; i < k; i += blockDim.x) {
+            const uint32_t gid = sm.app[i];
+            glist[base + i] = gid;
+            if (gid == ngroups - 1) out->reserved[1] = 1;  // the clipped last group is selected
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) sm.napp = 0;
+    __syncthreads();
+}
+
+// Transform of iteration `it` by `nblocks` cooperating blocks (block index
+// `block`).  Also used inside the persistent sparse-loop kernel, hence no
+// read-only-cache loads of the (rewritten) frontier lists.
+__device__ __forceinline__ void transform_phase(const LoopCtx &c, uint64_t it, const uint32_t *fvert0,
+                                                const uint32_t *fvert1, const uint32_t *fpref0,
+                                                const uint32_t *fpref1, const uint64_t *idx_off,
+                                                const uint32_t *idx_pos, int shift, uint32_t *gbits,
+                                                int append, uint32_t *glist, uint64_t ngroups,
+                                                TransformSmem &sm, uint64_t block, uint64_t nblocks) {
     const wg_iter_rec *in = ctx_in(c, it);
-    uint64_t packed = in->nz_packed;
-    uint64_t count = packed >> 32, total = packed & 0xffffffffull;
-    if (blockIdx.x == 0 && threadIdx.x == 0) ctx_out(c, it)->transform_entries = total;
+    const uint64_t packed = *(volatile const uint64_t *)&in->nz_packed;
+    const uint64_t count = packed >> 32, total = packed & 0xffffffffull;
+    if (block == 0 && threadIdx.x == 0) ctx_out(c, it)->transform_entries = total;
     if (total == 0) return;
     const uint32_t *fvert = ((it - 1) & 1) ? fvert1 : fvert0;
     const uint32_t *fpref = ((it - 1) & 1) ? fpref1 : fpref0;
-
-    __shared__ uint32_t s_pref[TR_TILE + 1];
-    __shared__ uint64_t s_base[TR_TILE + 1];
-    __shared__ uint64_t s_tmp[2];
-    uint64_t ntiles = (total + TR_TILE - 1) / TR_TILE;
-    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        uint64_t e0 = tile * TR_TILE;
-        uint64_t e1 = e0 + TR_TILE < total ? e0 + TR_TILE : total;
-        uint64_t i0 = block_search(fpref, 0, count, e0, s_tmp);
-        uint64_t nitems = count - i0 < (uint64_t)TR_TILE + 1 ? count - i0 : (uint64_t)TR_TILE + 1;
+    const uint64_t ntiles = (total + TR_TILE - 1) / TR_TILE;
+    if (threadIdx.x == 0) sm.napp = 0;
+    __syncthreads();
+    for (uint64_t tile = block; tile < ntiles; tile += nblocks) {
+        const uint64_t e0 = tile * TR_TILE;
+        const uint64_t e1 = e0 + TR_TILE < total ? e0 + TR_TILE : total;
+        const uint64_t i0 = block_search(fpref, 0, count, e0, sm.tmp);
+        const uint64_t nitems = count - i0 < (uint64_t)TR_TILE + 1 ? count - i0 : (uint64_t)TR_TILE + 1;
         for (uint64_t k = threadIdx.x; k < nitems; k += blockDim.x) {
-            uint32_t v = fvert[i0 + k];
-            uint32_t p = fpref[i0 + k];
-            s_pref[k] = p;
-            s_base[k] = idx_off[v] - p;
+            const uint32_t v = fvert[i0 + k];
+            const uint32_t p = fpref[i0 + k];
+            sm.pref[k] = p;
+            sm.base[k] = idx_off[v] - p;
         }
         __syncthreads();
         uint64_t e = e0 + (uint64_t)threadIdx.x * TR_EPT;
         if (e < e1) {
-            // last k with s_pref[k] <= e
-            uint32_t lo = 0, hi = (uint32_t)nitems;
+            uint32_t lo = 0, hi = (uint32_t)nitems;  // last k with pref[k] <= e
             while (hi - lo > 1) {
-                uint32_t mid = (lo + hi) >> 1;
-                if (s_pref[mid] <= e) lo = mid; else hi = mid;
+                const uint32_t mid = (lo + hi) >> 1;
+                if (sm.pref[mid] <= e) lo = mid; else hi = mid;
             }
             uint32_t k = lo;
-            uint64_t next = (k + 1 < nitems) ? s_pref[k + 1] : ~0ull;
+            uint64_t next = (k + 1 < nitems) ? sm.pref[k + 1] : ~0ull;
             uint32_t last_g = 0xffffffffu, acc_word = 0xffffffffu, acc_bits = 0;
-            uint64_t eend = e + TR_EPT < e1 ? e + TR_EPT : e1;
+            const uint64_t eend = e + TR_EPT < e1 ? e + TR_EPT : e1;
             for (; e < eend; ++e) {
                 while (e >= next) {
                     ++k;
-                    next = (k + 1 < nitems) ? s_pref[k + 1] : ~0ull;
+                    next = (k + 1 < nitems) ? sm.pref[k + 1] : ~0ull;
                 }
-                uint32_t g = idx_pos[s_base[k] + e] >> shift;
-                if (g == last_g) continue;
-                last_g = g;
-                uint32_t wd = g >> 5;
+                const uint32_t gid = idx_pos[sm.base[k] + e] >> shift;
+                if (gid == last_g) continue;
+                last_g = gid;
+                const uint32_t wd = gid >> 5;
                 if (wd != acc_word) {
-                    if (acc_bits) atomicOr(&gbits[acc_word], acc_bits);
+                    if (acc_bits) or_group_bits(gbits, acc_word, acc_bits, append, sm);
                     acc_word = wd;
                     acc_bits = 0;
                 }
-                acc_bits |= 1u << (g & 31);
+                acc_bits |= 1u << (gid & 31);
             }
-            if (acc_bits) atomicOr(&gbits[acc_word], acc_bits);
+            if (acc_bits) or_group_bits(gbits, acc_word, acc_bits, append, sm);
         }
-        __syncthreads();
+        if (append) flush_appended(sm, glist, ctx_out(c, it), ngroups);
+        else __syncthreads();
     }
+}
+
+__global__ void __launch_bounds__(TR_THREADS) transform_kernel(
+    LoopCtx c, const uint32_t *fvert0, const uint32_t *fvert1, const uint32_t *fpref0,
+    const uint32_t *fpref1, const uint64_t *idx_off, const uint32_t *idx_pos, int shift,
+    uint32_t *gbits, int append, uint32_t *glist, uint64_t ngroups) {
+    const uint64_t it = ctx_iter(c);
+    if (ctx_mode(c, it) != MODE_WEDGE) return;
+    __shared__ TransformSmem sm;
+    transform_phase(c, it, fvert0, fvert1, fpref0, fpref1, idx_off, idx_pos, shift, gbits, append, glist,
+                    ngroups, sm, blockIdx.x, gridDim.x);
 }
 
 }  // namespace wg

@@ -33,6 +33,8 @@ __device__ __forceinline__ uint64_t ctx_iter(const LoopCtx &c) {
 // out-edges, and uses the Wedge path iff its edge sum is below the limit.
 __device__ __forceinline__ int ctx_mode(const LoopCtx &c, uint64_t it) {
     if (c.forced_mode) return c.forced_mode;
+    // graph launches carry an iteration limit in ctrl[1]
+    if (c.ctrl && it > *(volatile const uint64_t *)&c.ctrl[1]) return MODE_NONE;
     const wg_iter_rec &p = c.recs[(it - 1) % c.ring];
     uint64_t sum = *(volatile const uint64_t *)&p.out_edge_sum;
     if (it > 1 && sum == 0) return MODE_NONE;

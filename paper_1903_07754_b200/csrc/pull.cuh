@@ -24,7 +24,12 @@
 // HBM stream runs ahead of the dependent gathers independently of register
 // pressure; wedge / filtered pulls load their vectors directly.
 #pragma once
+#include <cooperative_groups.h>
+
+#include "frontier.cuh"
 #include "loop.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace wg {
 
@@ -189,7 +194,7 @@ __device__ __forceinline__ void apply_segments(bool app, uint32_t d, T agg, T pd
 // Fold one vector's lanes into a minimum (messages prev[src] (+ weight)).
 template <typename T, int W, bool WEIGHT>
 __device__ __forceinline__ T fold_lanes(const uint32_t (&src)[W], const uint32_t (&wt)[W],
-                                        const T *__restrict__ prev, T INF, uint32_t &ovf) {
+                                        const T *prev, T INF, uint32_t &ovf) {
     using VT = ValTraits<T>;
     T ps[W];
 #pragma unroll
@@ -407,26 +412,36 @@ __global__ void __launch_bounds__(PULL_THREADS) pull_kernel(LoopCtx c, wg_graph 
 // ---------------------------------------------------------------------------
 // Dense unfiltered pull fed by TMA: each warp streams its range through an
 // S-stage ring of CH-tile chunks (vsrc, vdst, vw) in shared memory.
-constexpr int TMA_CH = 2;  // tiles per stage
-constexpr int TMA_S = 4;   // stages per warp
-
-template <int W, bool WEIGHT>
+template <int W, bool WEIGHT, int TMA_CH, int TMA_S>
 struct TmaSmem {
     static constexpr int VEC = TMA_CH * 32;
     static constexpr int SRC_WORDS = VEC * W;
     static constexpr int STAGE_WORDS = SRC_WORDS + VEC + (WEIGHT ? SRC_WORDS : 0);
-    static constexpr size_t WARP_BYTES = (size_t)TMA_S * STAGE_WORDS * 4 + TMA_S * 8 + STAGE * 4;
+    // 128-byte aligned per-warp slice (TMA destinations need 16 B, mbarriers 8 B)
+    static constexpr size_t WARP_BYTES =
+        ((size_t)TMA_S * STAGE_WORDS * 4 + TMA_S * 8 + STAGE * 4 + 127) & ~(size_t)127;
     static constexpr size_t BLOCK_BYTES = PULL_WARPS * WARP_BYTES;
 };
 
 __device__ __forceinline__ uint32_t pad16(uint32_t b) { return (b + 15u) & ~15u; }
 
-template <typename T, int W, bool WEIGHT>
-__global__ void __launch_bounds__(PULL_THREADS) pull_dense_tma_kernel(LoopCtx c, wg_graph g, PullBufs b,
+// Dense pull, unfiltered programs (CC, SSSP, PageRank-like min-plus): the
+// warp streams its tile range with TMA and processes CH tiles per stage in
+// four phases so that independent work overlaps:
+//   1. destinations and lanes from shared memory; segment heads per tile
+//      (ballot) -> only segment TAILS gather prev[d];
+//   2. all gathers of the CH tiles in flight together; lane folds;
+//   3. the CH segmented min-scans, interleaved (none depends on the carry:
+//      the carried segment only ever joins a tile's HEAD segment, whose tail
+//      lane takes the carried minimum in phase 4);
+//   4. a warp-uniform carry chain across the CH tiles, then the applies.
+template <typename T, int W, bool WEIGHT, int TMA_CH, int TMA_S, int MINB>
+__global__ void __launch_bounds__(PULL_THREADS, MINB) pull_dense_tma_kernel(LoopCtx c, wg_graph g, PullBufs b,
                                                                       int shift, int64_t inc,
                                                                       int64_t sentinel) {
     using VT = ValTraits<T>;
-    using SM = TmaSmem<W, WEIGHT>;
+    using SM = TmaSmem<W, WEIGHT, TMA_CH, TMA_S>;
+    constexpr int CH = TMA_CH;
     extern __shared__ __align__(128) unsigned char s_raw[];
     const uint64_t it = ctx_iter(c);
     const int mode = ctx_mode(c, it);
@@ -437,12 +452,13 @@ __global__ void __launch_bounds__(PULL_THREADS) pull_dense_tma_kernel(LoopCtx c,
     uint32_t *__restrict__ obits = ((it & 1) ? b.fbits[1] : b.fbits[0]);
     uint32_t *__restrict__ overt = ((it & 1) ? b.fvert[1] : b.fvert[0]);
     uint32_t *__restrict__ opref = ((it & 1) ? b.fpref[1] : b.fpref[0]);
-    const uint64_t nvec = g.nvec;
+    const uint32_t nvec = (uint32_t)g.nvec;
     const T INF = VT::inf(sentinel);
     const unsigned lane = lane_id();
     const unsigned wib = threadIdx.x >> 5;
     const uint64_t gwarp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const unsigned le = 0xffffffffu >> (31 - lane);
 
     unsigned char *wbase = s_raw + (size_t)wib * SM::WARP_BYTES;
     uint32_t *ring = reinterpret_cast<uint32_t *>(wbase);
@@ -450,54 +466,55 @@ __global__ void __launch_bounds__(PULL_THREADS) pull_dense_tma_kernel(LoopCtx c,
     uint32_t *stage_buf = reinterpret_cast<uint32_t *>(bars + TMA_S);
     PullOut o{stage_buf, 0u, 0ull, 0ull, 0u};
 
-    uint64_t t0, t1;
-    warp_range((nvec + 31) >> 5, gwarp, nwarps, t0, t1);
-    if (t0 < t1) {
-        const uint64_t nchunks = (t1 - t0 + TMA_CH - 1) / TMA_CH;
+    uint64_t t0w, t1w;
+    warp_range(((uint64_t)nvec + 31) >> 5, gwarp, nwarps, t0w, t1w);
+    if (t0w < t1w) {
+        const uint32_t tfirst = (uint32_t)t0w, tend = (uint32_t)t1w;
+        const uint32_t vend = (tend << 5) < nvec ? (tend << 5) : nvec;
+        o.touched = vend - (tfirst << 5);  // every vector of the range is processed
+        const uint32_t nchunks = (tend - tfirst + CH - 1) / CH;
         if (lane == 0) {
             for (int s = 0; s < TMA_S; ++s) mbar_init(&bars[s], 1);
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
         __syncwarp();
-        auto issue = [&](uint64_t ch) {
+        auto issue = [=](uint32_t ch) {
             const int s = (int)(ch % TMA_S);
-            const uint64_t v0 = (t0 + ch * TMA_CH) << 5;
-            uint64_t v1 = (t0 + (ch + 1) * TMA_CH) << 5;
-            const uint64_t vend = t1 << 5 < nvec ? t1 << 5 : nvec;
+            const uint32_t v0 = (tfirst + ch * CH) << 5;
+            uint32_t v1 = (tfirst + (ch + 1) * CH) << 5;
             if (v1 > vend) v1 = vend;
-            const uint32_t nv = (uint32_t)(v1 - v0);
+            const uint32_t nv = v1 - v0;
             uint32_t *st = ring + (size_t)s * SM::STAGE_WORDS;
             const uint32_t b_src = pad16(nv * W * 4), b_dst = pad16(nv * 4);
-            const uint32_t total = b_src + b_dst + (WEIGHT ? b_src : 0);
-            mbar_expect_tx(&bars[s], total);
-            tma_1d(st, g.vsrc + v0 * W, b_src, &bars[s]);
+            mbar_expect_tx(&bars[s], b_src + b_dst + (WEIGHT ? b_src : 0));
+            tma_1d(st, g.vsrc + (uint64_t)v0 * W, b_src, &bars[s]);
             tma_1d(st + SM::SRC_WORDS, g.vdst + v0, b_dst, &bars[s]);
-            if (WEIGHT) tma_1d(st + SM::SRC_WORDS + SM::VEC, g.vw + v0 * W, b_src, &bars[s]);
+            if (WEIGHT) tma_1d(st + SM::SRC_WORDS + SM::VEC, g.vw + (uint64_t)v0 * W, b_src, &bars[s]);
         };
         if (lane == 0)
-            for (uint64_t ch = 0; ch < nchunks && ch < TMA_S; ++ch) issue(ch);
+            for (uint32_t ch = 0; ch < nchunks && ch < (uint32_t)TMA_S; ++ch) issue(ch);
         uint32_t dleft = NONE, dright = NONE;
-        if (lane == 0 && t0 > 0) dleft = g.vdst[(t0 << 5) - 1];
-        if (lane == 1 && (t1 << 5) < nvec) dright = g.vdst[t1 << 5];
+        if (lane == 0 && tfirst > 0) dleft = g.vdst[(tfirst << 5) - 1];
+        if (lane == 1 && (tend << 5) < nvec) dright = g.vdst[tend << 5];
         dleft = __shfl_sync(FULL, dleft, 0);
         dright = __shfl_sync(FULL, dright, 1);
         Carry<T> cy;
-        const uint32_t tfirst = (uint32_t)t0, tlast = (uint32_t)t1 - 1, nv32 = (uint32_t)nvec;
-        for (uint32_t ch = 0; ch < (uint32_t)nchunks; ++ch) {
+
+        for (uint32_t ch = 0; ch < nchunks; ++ch) {
             const int s = (int)(ch % TMA_S);
             mbar_wait(&bars[s], (ch / TMA_S) & 1u);
             const uint32_t *st = ring + (size_t)s * SM::STAGE_WORDS;
-            const uint32_t tbase = tfirst + ch * TMA_CH;
-            uint32_t d[TMA_CH];
-            uint32_t src[TMA_CH][W], wt[TMA_CH][W];
-            bool act[TMA_CH];
+            const uint32_t tbase = tfirst + ch * CH;
+            // ---- phase 1: destinations, lanes, segment heads ----
+            uint32_t d[CH], src[CH][W], wt[CH][W];
+            unsigned heads[CH];
+            bool valid[CH];
 #pragma unroll
-            for (int u = 0; u < TMA_CH; ++u) {
+            for (int u = 0; u < CH; ++u) {
                 const uint32_t tile = tbase + u;
-                const bool valid = tile <= tlast && (tile << 5) + lane < nv32;
                 const int j = u * 32 + lane;
-                act[u] = valid;
-                d[u] = valid ? st[SM::SRC_WORDS + j] : NONE;
+                valid[u] = tile < tend && (tile << 5) + lane < nvec;
+                d[u] = valid[u] ? st[SM::SRC_WORDS + j] : NONE;
                 if constexpr (W == 4) {
                     const uint4 v = *reinterpret_cast<const uint4 *>(st + j * 4);
                     src[u][0] = v.x; src[u][1] = v.y; src[u][2] = v.z; src[u][3] = v.w;
@@ -507,30 +524,182 @@ __global__ void __launch_bounds__(PULL_THREADS) pull_dense_tma_kernel(LoopCtx c,
                 }
 #pragma unroll
                 for (int l = 0; l < W; ++l) {
-                    if (!valid) src[u][l] = WG_NO_LANE;
+                    if (!valid[u]) src[u][l] = WG_NO_LANE;
                     wt[u][l] = WEIGHT ? st[SM::SRC_WORDS + SM::VEC + j * W + l] : 0u;
                 }
             }
+            // all lanes' generic-proxy reads of this stage precede the async-proxy
+            // (TMA) refill that overwrites it
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
-            // the stage is consumed (values in registers): refill it
             if (lane == 0 && ch + TMA_S < nchunks) issue(ch + TMA_S);
-            T pd[TMA_CH], agg[TMA_CH];
 #pragma unroll
-            for (int u = 0; u < TMA_CH; ++u) {
-                pd[u] = act[u] ? prev[d[u]] : INF;
+            for (int u = 0; u < CH; ++u) {
+                const uint32_t dp = __shfl_up_sync(FULL, d[u], 1);
+                heads[u] = __ballot_sync(FULL, lane == 0 || dp != d[u]);
+            }
+            // ---- phase 2: gathers (tails read prev[d]) ----
+            T pd[CH], agg[CH];
+#pragma unroll
+            for (int u = 0; u < CH; ++u) {
+                const bool tail = (((heads[u] >> 1) | 0x80000000u) >> lane) & 1u;
+                pd[u] = (valid[u] && tail) ? prev[d[u]] : INF;
                 agg[u] = fold_lanes<T, W, WEIGHT>(src[u], wt[u], prev, INF, o.ovf);
             }
+            // ---- phase 3: segmented min-scans, interleaved across tiles ----
+            unsigned dist[CH], maxd = 0;
 #pragma unroll
-            for (int u = 0; u < TMA_CH; ++u) {
+            for (int u = 0; u < CH; ++u) {
+                dist[u] = lane - (31u - __clz(heads[u] & le));
+                maxd = dist[u] > maxd ? dist[u] : maxd;
+            }
+            maxd = __reduce_max_sync(FULL, maxd);
+            for (unsigned off = 1; off <= maxd; off <<= 1) {
+#pragma unroll
+                for (int u = 0; u < CH; ++u) {
+                    const T ov = shfl_up_t(agg[u], (int)off);
+                    if (off <= dist[u] && ov < agg[u]) agg[u] = ov;
+                }
+            }
+            // ---- phase 4: carry chain (warp-uniform), then applies ----
+#pragma unroll
+            for (int u = 0; u < CH; ++u) {
                 const uint32_t tile = tbase + u;
-                if (tile <= tlast)
-                    finish_tile<T>(d[u], agg[u], pd[u], act[u], tile == tfirst, tile == tlast, dleft, dright,
-                               cy, INF, inc, nxt, obits, o, g, out, overt, opref, b.n);
+                if (tile >= tend) continue;
+                const bool last_tile = tile == tend - 1;
+                const uint32_t d0 = __shfl_sync(FULL, d[u], 0);
+                const uint32_t d31 = __shfl_sync(FULL, d[u], 31);
+                const T a31 = shfl_t(agg[u], 31);
+                const T p31 = shfl_t(pd[u], 31);
+                const unsigned first_tail = __ffs((heads[u] >> 1) | 0x80000000u) - 1;
+                bool left0;
+                bool merge = false;
+                T cin = INF;
+                if (cy.d == NONE) {
+                    left0 = tile == tfirst ? (dleft != d0) : true;
+                } else if (d0 == cy.d) {
+                    merge = true;
+                    cin = cy.agg;
+                    left0 = cy.left;
+                } else {
+                    apply_segments<T>(lane == 0, cy.d, cy.agg, cy.pd, cy.left, INF, inc, nxt, obits, o);
+                    left0 = true;
+                }
+                // the head segment's tail lane takes the carried minimum
+                if (merge && lane == first_tail && cin < agg[u]) agg[u] = cin;
+                const bool whole = heads[u] == 1u;  // one segment spans the tile
+                const bool carry = !last_tile && d31 != NONE;
+                if (carry) {
+                    cy.d = d31;
+                    cy.agg = (merge && whole && cin < a31) ? cin : a31;
+                    cy.pd = p31;
+                    cy.left = (heads[u] >> 1) ? true : left0;  // a head after lane 0 precedes lane 31
+                } else {
+                    cy.d = NONE;
+                }
+                const bool tail = (((heads[u] >> 1) | 0x80000000u) >> lane) & 1u;
+                const bool left = (heads[u] & le & ~1u) ? true : left0;
+                const bool right = !(lane == 31 && last_tile && dright == d[u]);
+                const bool app = tail && valid[u] && !(carry && lane == 31);
+                apply_segments<T>(app, d[u], agg[u], pd[u], left && right, INF, inc, nxt, obits, o);
+                if (o.staged > STAGE - 34) flush_stage(o, g, out, overt, opref, b.n);
             }
         }
         if (o.staged) flush_stage(o, g, out, overt, opref, b.n);
     }
     end_of_pull<T>(o, out);
+}
+
+// ---------------------------------------------------------------------------
+// Sparse Wedge pull: the selected groups come UNSORTED from the transform's
+// append list (no bitmap scans).  A warp tile holds 32/vpg groups, one
+// vector per lane; segments never cross a group, so a segment is complete
+// unless it touches its group's first / last vector AND the neighbouring
+// vector outside the group has the same destination (then atomicMin; the
+// minimum is order-independent, so the unsorted list gives the reference's
+// values, frontier and counters exactly).  Clears the group bits it consumed.
+template <typename T, int W, bool WEIGHT, bool FILTER>
+__device__ __forceinline__ void sparse_pull_phase(const LoopCtx &c, uint64_t it, const wg_graph &g,
+                                                  const PullBufs &b, int shift, int64_t inc,
+                                                  int64_t sentinel, uint32_t *gbits, uint64_t ngroups_all,
+                                                  uint32_t *stage, uint64_t gwarp, uint64_t nwarps) {
+    using VT = ValTraits<T>;
+    wg_iter_rec *out = ctx_out(c, it);
+    // no read-only-cache loads of values here: the persistent loop rewrites them
+    const T *prev = (const T *)(((it - 1) & 1) ? b.vals[1] : b.vals[0]);
+    T *nxt = (T *)((it & 1) ? b.vals[1] : b.vals[0]);
+    uint32_t *obits = ((it & 1) ? b.fbits[1] : b.fbits[0]);
+    uint32_t *overt = ((it & 1) ? b.fvert[1] : b.fvert[0]);
+    uint32_t *opref = ((it & 1) ? b.fpref[1] : b.fpref[0]);
+    const T INF = VT::inf(sentinel);
+    const unsigned lane = lane_id();
+    const unsigned le = 0xffffffffu >> (31 - lane);
+    const uint64_t nsel = *(volatile const uint64_t *)&out->groups;
+    const uint32_t vpg = 1u << shift, jmask = vpg - 1, gpt = 32u >> shift;
+    const uint32_t j = lane & jmask;
+    const uint64_t ntiles = (nsel + gpt - 1) / gpt;
+    PullOut o{stage, 0u, 0ull, 0ull, 0u};
+    if (gwarp == 0 && lane == 0) {
+        uint64_t cov = nsel * vpg;
+        if (*(volatile const uint64_t *)&out->reserved[1]) cov -= ngroups_all * vpg - g.nvec;
+        out->covered_vectors = cov;
+    }
+    for (uint64_t tile = gwarp; tile < ntiles; tile += nwarps) {
+        const uint64_t gi = tile * gpt + (lane >> shift);
+        const bool gvalid = gi < nsel;
+        const uint64_t grp = gvalid ? ((volatile const uint32_t *)b.glist)[gi] : 0;
+        const uint64_t p = (grp << shift) + j;
+        const bool valid = gvalid && p < g.nvec;
+        const uint32_t d = valid ? g.vdst[p] : NONE;
+        T pd = INF, agg = INF;
+        if (FILTER && valid) pd = prev[d];
+        const bool act = valid && !(FILTER && pd != INF);
+        if (act) {
+            uint32_t src[W], wt[W];
+            load_lanes<W>(g.vsrc, p, src);
+            if (WEIGHT) load_lanes<W>(g.vw, p, wt);
+            agg = fold_lanes<T, W, WEIGHT>(src, wt, prev, INF, o.ovf);
+        }
+        if (gvalid && j == 0) gbits[grp >> 5] = 0;  // every bit of this word was set this iteration
+        const unsigned am = __ballot_sync(FULL, act);
+        o.touched += __popc(am);
+        const uint32_t dp = __shfl_up_sync(FULL, d, 1);
+        const unsigned heads = __ballot_sync(FULL, j == 0 || dp != d);
+        const unsigned hl = 31u - __clz(heads & le);
+        const unsigned dist = lane - hl;
+        const unsigned maxd = __reduce_max_sync(FULL, dist);
+        for (unsigned off = 1; off <= maxd; off <<= 1) {
+            const T ov = shfl_up_t(agg, (int)off);
+            if (off <= dist && ov < agg) agg = ov;
+        }
+        const bool tail = (((heads >> 1) | 0x80000000u) >> lane) & 1u;
+        const bool app = tail && act;
+        bool complete = true;
+        if (app) {
+            if (!FILTER) pd = prev[d];
+            // left: the segment starts at the group's first vector -> look before it
+            if ((hl & jmask) == 0 && grp > 0 && g.vdst[(grp << shift) - 1] == d) complete = false;
+            // right: the segment ends at the group's last vector -> look after it
+            if (j == jmask && p + 1 < g.nvec && g.vdst[p + 1] == d) complete = false;
+        }
+        apply_segments<T>(app, d, agg, pd, complete, INF, inc, nxt, obits, o);
+        if (o.staged > STAGE - 34) flush_stage(o, g, out, overt, opref, b.n);
+    }
+    if (o.staged) flush_stage(o, g, out, overt, opref, b.n);
+    end_of_pull<T>(o, out);
+}
+
+template <typename T, int W, bool WEIGHT, bool FILTER>
+__global__ void __launch_bounds__(PULL_THREADS) pull_sparse_kernel(LoopCtx c, wg_graph g, PullBufs b,
+                                                                   int shift, int64_t inc, int64_t sentinel,
+                                                                   uint32_t *gbits, uint64_t ngroups_all) {
+    __shared__ uint32_t s_stage[PULL_WARPS][STAGE];
+    const uint64_t it = ctx_iter(c);
+    if (ctx_mode(c, it) != MODE_WEDGE) return;
+    const uint64_t gwarp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    sparse_pull_phase<T, W, WEIGHT, FILTER>(c, it, g, b, shift, inc, sentinel, gbits, ngroups_all,
+                                            s_stage[threadIdx.x >> 5], gwarp, nwarps);
 }
 
 // ---------------- K7: end of iteration -------------------------------------
@@ -541,32 +710,31 @@ __global__ void __launch_bounds__(PULL_THREADS) pull_dense_tma_kernel(LoopCtx c,
 // bitmap of iteration it-1 (reused by it+1), finalises the record and zeroes
 // the record the next iteration will fill.
 template <typename T>
-__global__ void __launch_bounds__(256) finalize_kernel(LoopCtx c, PullBufs b) {
-    const uint64_t it = ctx_iter(c);
-    const int mode = ctx_mode(c, it);
-    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
+__device__ __forceinline__ void finalize_phase(const LoopCtx &c, uint64_t it, int mode, const PullBufs &b,
+                                               uint64_t tid, uint64_t nthreads) {
     if (mode != MODE_NONE) {
         const wg_iter_rec *out = ctx_out(c, it);
         const wg_iter_rec *in = ctx_in(c, it);
         const T *src = (const T *)((it & 1) ? b.vals[1] : b.vals[0]);
         T *dst = (T *)(((it - 1) & 1) ? b.vals[1] : b.vals[0]);
         const uint32_t *list = ((it & 1) ? b.fvert[1] : b.fvert[0]);
-        uint64_t nz = out->nz_packed >> 32, z = out->z_count;
+        const uint64_t nz = *(volatile const uint64_t *)&out->nz_packed >> 32;
+        const uint64_t z = *(volatile const uint64_t *)&out->z_count;
         for (uint64_t i = tid; i < nz + z; i += nthreads) {
-            uint32_t v = i < nz ? list[i] : list[b.n - 1 - (i - nz)];
-            dst[v] = src[v];
+            const uint32_t v = i < nz ? list[i] : list[b.n - 1 - (i - nz)];
+            dst[v] = *(volatile const T *)&src[v];
         }
         // clear bits of the frontier produced by it-1 (its bitmap is reused by it+1)
         uint32_t *obits = (((it - 1) & 1) ? b.fbits[1] : b.fbits[0]);
         const uint32_t *plist = (((it - 1) & 1) ? b.fvert[1] : b.fvert[0]);
-        uint64_t pnz = in->nz_packed >> 32, pz = in->z_count;
-        uint64_t words = ((uint64_t)b.n + 31) >> 5;
+        const uint64_t pnz = *(volatile const uint64_t *)&in->nz_packed >> 32;
+        const uint64_t pz = *(volatile const uint64_t *)&in->z_count;
+        const uint64_t words = ((uint64_t)b.n + 31) >> 5;
         if (pnz + pz > words) {
             for (uint64_t w = tid; w < words; w += nthreads) obits[w] = 0;
         } else {
             for (uint64_t i = tid; i < pnz + pz; i += nthreads) {
-                uint32_t v = i < pnz ? plist[i] : plist[b.n - 1 - (i - pnz)];
+                const uint32_t v = i < pnz ? plist[i] : plist[b.n - 1 - (i - pnz)];
                 obits[v >> 5] = 0;
             }
         }
@@ -575,13 +743,59 @@ __global__ void __launch_bounds__(256) finalize_kernel(LoopCtx c, PullBufs b) {
         wg_iter_rec *out = ctx_out(c, it);
         if (mode != MODE_NONE) {
             out->mode = (uint64_t)mode;
-            out->frontier_out = (out->nz_packed >> 32) + out->z_count;
-            out->active_edges = ctx_in(c, it)->out_edge_sum;
+            out->frontier_out = (*(volatile uint64_t *)&out->nz_packed >> 32) + *(volatile uint64_t *)&out->z_count;
+            out->active_edges = *(volatile const uint64_t *)&ctx_in(c, it)->out_edge_sum;
         }
-        wg_iter_rec *nx = &c.recs[(it + 1) % c.ring];
-        uint64_t *q = (uint64_t *)nx;
+        uint64_t *q = (uint64_t *)&c.recs[(it + 1) % c.ring];
 #pragma unroll
         for (int i = 0; i < 16; ++i) q[i] = 0;
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) finalize_kernel(LoopCtx c, PullBufs b) {
+    const uint64_t it = ctx_iter(c);
+    const int mode = ctx_mode(c, it);
+    finalize_phase<T>(c, it, mode, b, (uint64_t)blockIdx.x * blockDim.x + threadIdx.x,
+                      (uint64_t)gridDim.x * blockDim.x);
+}
+
+// ---------------- persistent sparse loop ----------------------------------
+// Runs consecutive SPARSE Wedge iterations (transform with group append ->
+// unsorted-group pull -> end of iteration) inside one cooperative launch,
+// separated by grid-wide barriers, and advances the device iteration counter
+// ctrl[0].  It returns as soon as the next iteration is not a sparse Wedge
+// iteration (dense, large frontier, converged or past the launch limit
+// ctrl[1]); the regular kernels of the loop graph take it from there.  This is
+// what keeps high-diameter runs (the 4096^2 grid: ~8.6K thin wavefronts) from
+// paying several kernel launches per iteration.
+template <typename T, int W, bool WEIGHT, bool FILTER>
+__global__ void __launch_bounds__(PULL_THREADS) sparse_loop_kernel(LoopCtx c, wg_graph g, PullBufs b,
+                                                                   int shift, int64_t inc, int64_t sentinel,
+                                                                   uint32_t *gbits, uint64_t ngroups) {
+    __shared__ TransformSmem tsm;
+    __shared__ uint32_t s_stage[PULL_WARPS][STAGE];
+    cg::grid_group grid = cg::this_grid();
+    const uint64_t gwarp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
+    uint64_t *ctrl = const_cast<uint64_t *>(c.ctrl);
+    while (true) {
+        const uint64_t it = *(volatile uint64_t *)&ctrl[0] + 1;
+        const int mode = ctx_mode(c, it);  // includes the launch limit
+        if (mode != MODE_WEDGE) break;
+        if (g.entries == 0) break;
+        if (tid == 0) ctx_out(c, it)->reserved[0] = 3;
+        transform_phase(c, it, b.fvert[0], b.fvert[1], b.fpref[0], b.fpref[1], g.idx_off, g.idx_pos, shift,
+                        gbits, 1, const_cast<uint32_t *>(b.glist), ngroups, tsm, blockIdx.x, gridDim.x);
+        grid.sync();
+        sparse_pull_phase<T, W, WEIGHT, FILTER>(c, it, g, b, shift, inc, sentinel, gbits, ngroups,
+                                                s_stage[threadIdx.x >> 5], gwarp, nwarps);
+        grid.sync();
+        finalize_phase<T>(c, it, MODE_WEDGE, b, tid, nthreads);
+        if (tid == 0) *(volatile uint64_t *)&ctrl[0] = it;
+        grid.sync();
     }
 }
 

@@ -449,7 +449,7 @@ class DeviceLoop:
             check(L.wg_run_loop_launch(exe, ctypes.byref(self.bufs), limit, _lib.stream_ptr(stream)))
             ctrl_host.copy_(self.ctrl, non_blocking=True)
             s.synchronize()
-            done = int(ctrl_host[0])
+            done = min(int(ctrl_host[0]), limit)
             rows = self._read(it, done - it + 1, stream) if done >= it else []
             conv, at = self._parse(rows, it, records, None)
             if records:
