@@ -50,6 +50,7 @@ extern "C" {
 #define WG_VAL_I64 1 /* int64 values with the reference sentinel (engine.py:41-43) */
 
 #define WG_NO_LANE 0xFFFFFFFFu /* padding lane in vsrc */
+#define WG_TRANSFORM_TILE 2048u /* edge-index entries per transform tile */
 
 /* Device-resident pull layout.  All pointers device.
  * vsrc / vdst / vw must stay readable for 16 vectors past nvec (the dense
@@ -144,6 +145,8 @@ typedef struct wg_run_bufs {
     uint32_t *fbits[2];     /* [ceil(n/32)] each, zero on init */
     uint32_t *fvert[2];     /* [n] frontier lists */
     uint32_t *fpref[2];     /* [n] entry prefixes of the lists */
+    uint32_t *tstart[2];    /* [entries/WG_TRANSFORM_TILE + 2] list position of the member
+                               covering each transform tile's first entry */
     uint32_t *gbits;        /* [ceil(groups/32)] zero on init */
     uint32_t *glist;        /* [groups] */
     uint64_t *bcount;       /* [blocks] compaction scratch */
@@ -161,8 +164,8 @@ typedef struct wg_run_params {
 } wg_run_params;
 
 /* Element counts: [0] fbits words, [1] groups, [2] gbits words, [3] bcount
- * entries (the caller multiplies by element sizes). */
-int wg_run_buffer_sizes(const wg_graph *g, int shift, uint64_t *h_sizes4);
+ * entries, [4] tstart entries (the caller multiplies by element sizes). */
+int wg_run_buffer_sizes(const wg_graph *g, int shift, uint64_t *h_sizes5);
 /* Seed iteration 0 from the initial-frontier bitmap d_init_words (uint32
  * words over n): builds list 0 and record 0, zeroes record 1.  The caller has
  * already written vals[0] == vals[1] == initial values. */
@@ -196,6 +199,15 @@ void wg_run_graph_destroy(void *graph);
 void *wg_run_loop_graph_create(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p,
                                void *stream);
 int wg_run_loop_launch(void *graph, const wg_run_bufs *b, uint64_t max_iteration, void *stream);
+/* The persistent cooperative Wedge loop on its own (outside any graph): runs
+ * consecutive Wedge iterations ctrl[0]+1 .. up to max_iteration and stops at
+ * the first non-Wedge iteration; used by drivers and profilers. */
+int wg_run_persistent(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p,
+                      uint64_t max_iteration, void *stream);
+/* Profiling aid: record 4 %globaltimer stamps per persistent-loop iteration
+ * (start, after transform, after pull, after end-of-iteration) into d_buf
+ * (4*iterations uint64); pass NULL to disable. */
+int wg_debug_phase_buffer(uint64_t *d_buf, uint64_t iterations);
 
 /* ---------------- multi-GPU exchange ----------------------- */
 /* Destination-range sharding: each rank's layout holds the vectors of its

@@ -41,8 +41,8 @@ REC_U64 = 16  # record size in uint64 words
 
 class WgRunBufs(ctypes.Structure):
     _fields_ = [("vals", c_vp * 2), ("fbits", c_vp * 2), ("fvert", c_vp * 2), ("fpref", c_vp * 2),
-                ("gbits", c_vp), ("glist", c_vp), ("bcount", c_vp), ("recs", c_vp), ("ctrl", c_vp),
-                ("ring", c_u32)]
+                ("tstart", c_vp * 2), ("gbits", c_vp), ("glist", c_vp), ("bcount", c_vp), ("recs", c_vp),
+                ("ctrl", c_vp), ("ring", c_u32)]
 
 
 class WgRunParams(ctypes.Structure):
@@ -58,7 +58,8 @@ EXPORTS = [
     "wg_canonical_scratch_bytes", "wg_canonical_edges", "wg_weights_hash", "wg_grid_edges",
     "wg_timer_create", "wg_timer_destroy", "wg_timer_reset", "wg_timer_read", "wg_launch_count",
     "wg_exchange_pack", "wg_exchange_apply", "wg_run_graph_create", "wg_run_graph_launch",
-    "wg_run_graph_destroy", "wg_run_loop_graph_create", "wg_run_loop_launch",
+    "wg_run_graph_destroy", "wg_run_loop_graph_create", "wg_run_loop_launch", "wg_run_persistent",
+    "wg_debug_phase_buffer",
 ]
 
 _LIB = None
@@ -133,6 +134,8 @@ def load(path: os.PathLike | str | None = None):
         "wg_run_graph_destroy": (None, [c_vp]),
         "wg_run_loop_graph_create": (c_vp, [G, B, P, c_vp]),
         "wg_run_loop_launch": (ctypes.c_int, [c_vp, B, c_u64, c_vp]),
+        "wg_run_persistent": (ctypes.c_int, [G, B, P, c_u64, c_vp]),
+        "wg_debug_phase_buffer": (ctypes.c_int, [c_vp, c_u64]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -140,9 +140,11 @@ uint64_t groups_of(const wg_graph *g, int shift) { return (g->nvec + (1ull << sh
 
 struct KernelWs {
     wg_iter_rec *recs;
-    uint32_t *fvert[2], *fpref[2], *glist;
+    uint32_t *fvert[2], *fpref[2], *tstart[2], *glist;
     uint64_t *bcount;
 };
+
+uint64_t tstart_entries(const wg_graph *g) { return g->entries / TR_TILE + 2; }
 
 int carve_kernel_ws(const wg_graph *g, int shift, void *ws, size_t bytes, KernelWs *k) {
     Carve cv{(char *)ws, 0, bytes};
@@ -153,10 +155,11 @@ int carve_kernel_ws(const wg_graph *g, int shift, void *ws, size_t bytes, Kernel
     for (int i = 0; i < 2; ++i) {
         k->fvert[i] = cv.take<uint32_t>(n);
         k->fpref[i] = cv.take<uint32_t>(n);
+        k->tstart[i] = cv.take<uint32_t>(tstart_entries(g));
     }
     k->glist = cv.take<uint32_t>(groups ? groups : 1);
     k->bcount = cv.take<uint64_t>(nb > gb ? nb : gb);
-    if (!k->recs || !k->fvert[1] || !k->fpref[1] || !k->glist || !k->bcount) {
+    if (!k->recs || !k->fvert[1] || !k->fpref[1] || !k->tstart[1] || !k->glist || !k->bcount) {
         set_error("kernel workspace too small (%zu bytes)", bytes);
         return WG_ENOSPACE;
     }
@@ -186,22 +189,24 @@ int launch_group_compaction(const LoopCtx &c, uint32_t *words, uint64_t ngroups,
 }
 
 int launch_frontier_compaction(const wg_graph *g, const uint32_t *words, uint64_t *bcount,
-                               uint32_t *fvert, uint32_t *fpref, wg_iter_rec *rec, cudaStream_t s) {
+                               uint32_t *fvert, uint32_t *fpref, uint32_t *tstart, wg_iter_rec *rec,
+                               cudaStream_t s) {
     uint64_t nb = cb_blocks(g->n ? g->n : 1);
     frontier_count_kernel<<<(unsigned)nb, CB_THREADS, 0, s>>>(words, g->n, g->idx_off, g->outdeg,
                                                               bcount); ::wg::count_launch();
     frontier_list_kernel<<<(unsigned)nb, CB_THREADS, 0, s>>>(words, g->n, g->idx_off, bcount, fvert,
-                                                             fpref, rec); ::wg::count_launch();
+                                                             fpref, tstart, rec); ::wg::count_launch();
     WG_CHECK_LAUNCH("frontier compaction");
     return WG_OK;
 }
 
 int launch_transform(const LoopCtx &c, const wg_graph *g, uint32_t *const fvert[2],
-                     uint32_t *const fpref[2], int shift, uint32_t *gbits, cudaStream_t s,
-                     int append = 0, uint32_t *glist = nullptr, uint64_t ngroups = 0) {
+                     uint32_t *const fpref[2], uint32_t *const tstart[2], int shift, uint32_t *gbits,
+                     cudaStream_t s, int append = 0, uint32_t *glist = nullptr, uint64_t ngroups = 0) {
     unsigned grid = persistent_grid(transform_kernel, TR_THREADS, (g->entries + TR_TILE - 1) / TR_TILE);
-    transform_kernel<<<grid, TR_THREADS, 0, s>>>(c, fvert[0], fvert[1], fpref[0], fpref[1], g->idx_off,
-                                                 g->idx_pos, shift, gbits, append, glist, ngroups);
+    transform_kernel<<<grid, TR_THREADS, 0, s>>>(c, fvert[0], fvert[1], fpref[0], fpref[1], tstart[0],
+                                                 tstart[1], g->idx_off, g->idx_pos, shift, gbits, append,
+                                                 glist, ngroups);
     ::wg::count_launch();
     WG_CHECK_LAUNCH("transform");
     return WG_OK;
@@ -253,7 +258,11 @@ int launch_sparse_loop(const LoopCtx &c, const wg_graph *g, const PullBufs &pb, 
     int per_sm = 0;
     WG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, PULL_THREADS, 0));
     WG_REQUIRE(per_sm >= 1, "sparse loop kernel does not fit on an SM");
-    if (per_sm > 2) per_sm = 2;
+    static const int cap = [] {
+        const char *e = getenv("WG_PERSIST_BLOCKS");
+        return e ? atoi(e) : 4;
+    }();
+    if (cap > 0 && per_sm > cap) per_sm = cap;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(sm_count() * per_sm));
     cfg.blockDim = dim3(PULL_THREADS);
@@ -323,7 +332,7 @@ size_t wg_kernel_workspace_bytes(const wg_graph *g, int shift) {
     if (!g || shift < 0 || shift > 4) return 0;
     uint64_t n = g->n ? g->n : 1, groups = groups_of(g, shift);
     uint64_t nb = cb_blocks(n) * 4, gb = cb_blocks(groups ? groups : 1);
-    return carve_size(2 * sizeof(wg_iter_rec)) + 4 * carve_size(n * 4) +
+    return carve_size(2 * sizeof(wg_iter_rec)) + 4 * carve_size(n * 4) + 2 * carve_size(tstart_entries(g) * 4) +
            carve_size((groups ? groups : 1) * 4) + carve_size((nb > gb ? nb : gb) * 8) + 256;
 }
 
@@ -341,12 +350,12 @@ int wg_transform(const wg_graph *g, const uint32_t *d_frontier_words, int shift,
     *h_visited = 0;
     if (g->n == 0) return WG_OK;
     if ((rc = launch_frontier_compaction(g, d_frontier_words, k.bcount, k.fvert[0], k.fpref[0],
-                                         &k.recs[0], s)))
+                                         k.tstart[0], &k.recs[0], s)))
         return rc;
     if (g->entries) {
         WG_REQUIRE(d_wedge_words && g->idx_pos, "null wedge words / index");
         LoopCtx c = forced_ctx(k.recs, MODE_WEDGE, g->edges);
-        if ((rc = launch_transform(c, g, k.fvert, k.fpref, shift, d_wedge_words, s))) return rc;
+        if ((rc = launch_transform(c, g, k.fvert, k.fpref, k.tstart, shift, d_wedge_words, s))) return rc;
     }
     wg_iter_rec h[2];
     WG_CUDA(cudaMemcpyAsync(h, k.recs, sizeof(h), cudaMemcpyDeviceToHost, s));
@@ -387,6 +396,8 @@ static int pull_common(const wg_graph *g, const uint32_t *d_wedge_words, int shi
     pb.fvert[1] = ws.fvert[1];
     pb.fpref[0] = ws.fpref[0];
     pb.fpref[1] = ws.fpref[1];
+    pb.tstart[0] = ws.tstart[0];
+    pb.tstart[1] = ws.tstart[1];
     pb.glist = ws.glist;
     pb.n = g->n;
     if ((rc = launch_pull(c, g, pb, val_type, shift, k, items, s))) return rc;
@@ -446,7 +457,7 @@ int wg_covered_groups(const uint32_t *d_wedge_words, uint64_t group_count, uint3
 }
 
 // ------------------------------------------------------------ run loop ---
-int wg_run_buffer_sizes(const wg_graph *g, int shift, uint64_t *h_sizes4) {
+int wg_run_buffer_sizes(const wg_graph *g, int shift, uint64_t *h_sizes4) {  /* 5 entries */
     int rc = check_graph(g);
     if (rc) return rc;
     WG_REQUIRE(h_sizes4, "null argument");
@@ -456,6 +467,7 @@ int wg_run_buffer_sizes(const wg_graph *g, int shift, uint64_t *h_sizes4) {
     h_sizes4[1] = groups;
     h_sizes4[2] = (groups + 31) >> 5;
     h_sizes4[3] = nb > gb ? nb : gb;
+    h_sizes4[4] = tstart_entries(g);
     return WG_OK;
 }
 
@@ -522,6 +534,7 @@ static PullBufs pull_bufs(const wg_graph *g, const wg_run_bufs *b) {
         pb.fbits[i] = b->fbits[i];
         pb.fvert[i] = b->fvert[i];
         pb.fpref[i] = b->fpref[i];
+        pb.tstart[i] = b->tstart[i];
     }
     pb.glist = b->glist;
     pb.n = g->n;
@@ -536,7 +549,8 @@ static int check_run(const wg_graph *g, const wg_run_bufs *b, const wg_run_param
     WG_REQUIRE(p->shift >= 0 && p->shift <= 4, "shift must be in [0, 4]");
     WG_REQUIRE(b->ring >= 4, "record ring must hold >= 4 records");
     WG_REQUIRE(b->vals[0] && b->vals[1] && b->fbits[0] && b->fbits[1] && b->fvert[0] && b->fvert[1] &&
-                   b->fpref[0] && b->fpref[1] && b->gbits && b->glist && b->bcount && b->recs &&
+                   b->fpref[0] && b->fpref[1] && b->tstart[0] && b->tstart[1] && b->gbits && b->glist &&
+                   b->bcount && b->recs &&
                    b->ctrl,
                "null run buffer");
     WG_REQUIRE(!p->kern.use_weight || g->vw, "weighted kernel on an unweighted layout");
@@ -558,7 +572,7 @@ int wg_run_init(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p,
     WG_CUDA(cudaMemsetAsync(b->fbits[1], 0, words * 4, s));
     WG_CUDA(cudaMemsetAsync(b->gbits, 0, ((groups + 31) >> 5) * 4, s));
     if (g->n == 0) return WG_OK;
-    return launch_frontier_compaction(g, d_init_words, b->bcount, b->fvert[0], b->fpref[0],
+    return launch_frontier_compaction(g, d_init_words, b->bcount, b->fvert[0], b->fpref[0], b->tstart[0],
                                       &b->recs[0], s);
 }
 
@@ -568,9 +582,10 @@ static int enqueue_one(const wg_graph *g, const wg_run_bufs *b, const wg_run_par
     uint64_t groups = groups_of(g, p->shift);
     uint32_t *fv[2] = {b->fvert[0], b->fvert[1]};
     uint32_t *fp[2] = {b->fpref[0], b->fpref[1]};
+    uint32_t *ts[2] = {b->tstart[0], b->tstart[1]};
     int slot = timer_begin(p->timer, 1, (int64_t)c.it_arg, s);
     if (g->entries) {
-        if ((rc = launch_transform(c, g, fv, fp, p->shift, b->gbits, s))) return rc;
+        if ((rc = launch_transform(c, g, fv, fp, ts, p->shift, b->gbits, s))) return rc;
     }
     if (groups) {
         if ((rc = launch_group_compaction(c, b->gbits, groups, b->bcount, b->glist, 1, p->shift,
@@ -749,6 +764,7 @@ void *wg_run_loop_graph_create(const wg_graph *g, const wg_run_bufs *b, const wg
     const uint64_t groups = groups_of(g, q.shift);
     uint32_t *fv[2] = {b->fvert[0], b->fvert[1]};
     uint32_t *fp[2] = {b->fpref[0], b->fpref[1]};
+    uint32_t *ts[2] = {b->tstart[0], b->tstart[1]};
     PullBufs pb = pull_bufs(g, b);
     int rc = WG_OK;
     // 0. as many consecutive sparse Wedge iterations as possible, persistently
@@ -769,7 +785,7 @@ void *wg_run_loop_graph_create(const wg_graph *g, const wg_run_bufs *b, const wg
     if (rc == WG_OK && e == cudaSuccess && (e = capture_if_node(s, hs, &inner)) == cudaSuccess &&
         (e = cudaStreamBeginCaptureToGraph(s2, inner, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal)) ==
             cudaSuccess) {
-        if (g->entries) rc = launch_transform(c, g, fv, fp, q.shift, b->gbits, s2);
+        if (g->entries) rc = launch_transform(c, g, fv, fp, ts, q.shift, b->gbits, s2);
         if (rc == WG_OK && groups)
             rc = launch_group_compaction(c, b->gbits, groups, b->bcount, b->glist, 1, q.shift, g->nvec, s2);
         if (rc == WG_OK && g->nvec) rc = launch_pull(c, g, pb, q.val_type, q.shift, &q.kern, g->nvec, s2, MODE_WEDGE);
@@ -779,7 +795,7 @@ void *wg_run_loop_graph_create(const wg_graph *g, const wg_run_bufs *b, const wg
     if (rc == WG_OK && e == cudaSuccess && (e = capture_if_node(s, hp, &inner)) == cudaSuccess &&
         (e = cudaStreamBeginCaptureToGraph(s2, inner, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal)) ==
             cudaSuccess) {
-        if (g->entries) rc = launch_transform(c, g, fv, fp, q.shift, b->gbits, s2, 1, b->glist, groups);
+        if (g->entries) rc = launch_transform(c, g, fv, fp, ts, q.shift, b->gbits, s2, 1, b->glist, groups);
         if (rc == WG_OK && g->nvec) rc = launch_pull_sparse(c, g, pb, q.val_type, q.shift, &q.kern, b->gbits, groups, s2);
         e = cudaStreamEndCapture(s2, &inner);
     }
@@ -807,6 +823,26 @@ void *wg_run_loop_graph_create(const wg_graph *g, const wg_run_bufs *b, const wg
         return nullptr;
     }
     return (void *)exec;
+}
+
+// Debug: phase timestamps of the persistent loop into a device buffer.
+int wg_debug_phase_buffer(uint64_t *d_buf, uint64_t iterations) {
+    WG_CUDA(cudaMemcpyToSymbol(g_phase_ts, &d_buf, sizeof(d_buf)));
+    WG_CUDA(cudaMemcpyToSymbol(g_phase_cap, &iterations, sizeof(iterations)));
+    return WG_OK;
+}
+
+int wg_run_persistent(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p,
+                      uint64_t max_iteration, void *stream) {
+    int rc = check_run(g, b, p);
+    if (rc) return rc;
+    cudaStream_t s = as_stream(stream);
+    set_limit_kernel<<<1, 1, 0, s>>>(b->ctrl, max_iteration);
+    ::wg::count_launch();
+    LoopCtx c = loop_ctx(g, b, p, b->ctrl, 1);
+    PullBufs pb = pull_bufs(g, b);
+    if (!g->entries || !g->nvec) return WG_OK;
+    return launch_sparse_loop(c, g, pb, p->val_type, p->shift, &p->kern, b->gbits, groups_of(g, p->shift), s);
 }
 
 int wg_run_loop_launch(void *graph, const wg_run_bufs *b, uint64_t max_iteration, void *stream) {
@@ -906,7 +942,7 @@ int wg_exchange_apply(const wg_graph *g, const wg_run_bufs *b, const wg_run_para
     // the global frontier of `it`: ordered list, index prefixes, counts and
     // the global out-degree sum (the next gate's input) from the bitmap
     return launch_frontier_compaction(g, bits, b->bcount, b->fvert[it & 1], b->fpref[it & 1],
-                                      &b->recs[it % b->ring], s);
+                                      b->tstart[it & 1], &b->recs[it % b->ring], s);
 }
 
 }  // extern "C"

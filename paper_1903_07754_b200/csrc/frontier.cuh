@@ -19,6 +19,19 @@ constexpr int CB_THREADS = 256;
 constexpr int CB_WPT = 4;                       // words per thread
 constexpr int CB_WORDS = CB_THREADS * CB_WPT;   // words per block
 
+constexpr int TR_THREADS = 256;
+constexpr int TR_EPT = 8;
+constexpr int TR_TILE = TR_THREADS * TR_EPT;
+static_assert(TR_TILE == WG_TRANSFORM_TILE, "transform tile");
+
+// A list member covering entries [pref, pref+len) at list position pos owns
+// the tile starts of every transform tile whose first entry it covers.
+__device__ __forceinline__ void mark_tile_starts(uint32_t *tstart, uint64_t pref, uint64_t len,
+                                                 uint32_t pos) {
+    const uint64_t k0 = (pref + TR_TILE - 1) / TR_TILE, k1 = (pref + len - 1) / TR_TILE;
+    for (uint64_t k = k0; k <= k1; ++k) tstart[k] = pos;
+}
+
 __host__ __device__ inline uint64_t cb_blocks(uint64_t nbits) {
     uint64_t words = (nbits + 31) >> 5;
     return (words + CB_WORDS - 1) / CB_WORDS;
@@ -141,7 +154,7 @@ __global__ void __launch_bounds__(CB_THREADS) frontier_count_kernel(const uint32
 
 __global__ void __launch_bounds__(CB_THREADS) frontier_list_kernel(
     const uint32_t *words, uint64_t nbits, const uint64_t *idx_off, const uint64_t *bcount,
-    uint32_t *fvert, uint32_t *fpref, wg_iter_rec *rec) {
+    uint32_t *fvert, uint32_t *fpref, uint32_t *tstart, wg_iter_rec *rec) {
     __shared__ uint64_t sm[33];
     uint64_t nz_base = prior_blocks_sum(bcount, blockIdx.x, 4, 0, sm);
     uint64_t ent_base = prior_blocks_sum(bcount, blockIdx.x, 4, 1, sm);
@@ -176,6 +189,7 @@ __global__ void __launch_bounds__(CB_THREADS) frontier_list_kernel(
             if (len) {
                 fvert[nzp] = (uint32_t)u;
                 fpref[nzp] = (uint32_t)entp;
+                if (tstart) mark_tile_starts(tstart, entp, len, (uint32_t)nzp);
                 ++nzp;
                 entp += len;
             } else {
@@ -202,9 +216,7 @@ __global__ void __launch_bounds__(CB_THREADS) frontier_list_kernel(
 // the list items overlapping the tile are staged in shared memory; each thread
 // then walks TR_EPT consecutive entries, OR-ing group bits pos >> shift and
 // skipping repeats (a source's positions ascend, so equal groups are adjacent).
-constexpr int TR_THREADS = 256;
-constexpr int TR_EPT = 8;
-constexpr int TR_TILE = TR_THREADS * TR_EPT;
+
 
 // Last index i in [lo, hi) with pref[i] <= e (block-cooperative k-ary search;
 // pref ascending, pref[lo] <= e).  All threads return the same value.
@@ -241,25 +253,9 @@ struct TransformSmem {
     uint32_t napp;
 };
 
-// Set the group bits of one bitmap word; in append mode (unsorted Wedge path)
-// newly set groups are staged in shared memory and appended to the group list
-// with one global atomic per block tile.
-__device__ __forceinline__ void or_group_bits(uint32_t *gbits, uint32_t word, uint32_t bits, int append,
-                                              TransformSmem &sm) {
-    if (!append) {
-        atomicOr(&gbits[word], bits);
-        return;
-    }
-    uint32_t fresh = bits & ~atomicOr(&gbits[word], bits);
-    if (!fresh) return;
-    uint32_t pos = atomicAdd(&sm.napp, (uint32_t)__popc(fresh));
-    while (fresh) {
-        const int b = __ffs(fresh) - 1;
-        fresh &= fresh - 1;
-        sm.app[pos++] = (word << 5) + b;
-    }
-}
-
+// Append mode (unsorted Wedge path): newly selected groups are staged in
+// shared memory and appended to the group list with one global atomic per
+// block tile.
 __device__ __forceinline__ void flush_appended(TransformSmem &sm, uint32_t *glist, wg_iter_rec *out,
                                                uint64_t ngroups) {
     __syncthreads();
@@ -285,7 +281,8 @@ __device__ __forceinline__ void flush_appended(TransformSmem &sm, uint32_t *glis
 // read-only-cache loads of the (rewritten) frontier lists.
 __device__ __forceinline__ void transform_phase(const LoopCtx &c, uint64_t it, const uint32_t *fvert0,
                                                 const uint32_t *fvert1, const uint32_t *fpref0,
-                                                const uint32_t *fpref1, const uint64_t *idx_off,
+                                                const uint32_t *fpref1, const uint32_t *tstart0,
+                                                const uint32_t *tstart1, const uint64_t *idx_off,
                                                 const uint32_t *idx_pos, int shift, uint32_t *gbits,
                                                 int append, uint32_t *glist, uint64_t ngroups,
                                                 TransformSmem &sm, uint64_t block, uint64_t nblocks) {
@@ -296,14 +293,18 @@ __device__ __forceinline__ void transform_phase(const LoopCtx &c, uint64_t it, c
     if (total == 0) return;
     const uint32_t *fvert = ((it - 1) & 1) ? fvert1 : fvert0;
     const uint32_t *fpref = ((it - 1) & 1) ? fpref1 : fpref0;
+    const uint32_t *tstart = ((it - 1) & 1) ? tstart1 : tstart0;
     const uint64_t ntiles = (total + TR_TILE - 1) / TR_TILE;
     if (threadIdx.x == 0) sm.napp = 0;
     __syncthreads();
     for (uint64_t tile = block; tile < ntiles; tile += nblocks) {
         const uint64_t e0 = tile * TR_TILE;
         const uint64_t e1 = e0 + TR_TILE < total ? e0 + TR_TILE : total;
-        const uint64_t i0 = block_search(fpref, 0, count, e0, sm.tmp);
-        const uint64_t nitems = count - i0 < (uint64_t)TR_TILE + 1 ? count - i0 : (uint64_t)TR_TILE + 1;
+        // members covering this tile: from the one holding entry e0 to the one
+        // holding the next tile's first entry (recorded by the list producer)
+        const uint64_t i0 = tstart[tile];
+        const uint64_t ilast = tile + 1 < ntiles ? tstart[tile + 1] : count - 1;
+        const uint64_t nitems = ilast - i0 + 1;
         for (uint64_t k = threadIdx.x; k < nitems; k += blockDim.x) {
             const uint32_t v = fvert[i0 + k];
             const uint32_t p = fpref[i0 + k];
@@ -320,25 +321,40 @@ __device__ __forceinline__ void transform_phase(const LoopCtx &c, uint64_t it, c
             }
             uint32_t k = lo;
             uint64_t next = (k + 1 < nitems) ? sm.pref[k + 1] : ~0ull;
-            uint32_t last_g = 0xffffffffu, acc_word = 0xffffffffu, acc_bits = 0;
-            const uint64_t eend = e + TR_EPT < e1 ? e + TR_EPT : e1;
-            for (; e < eend; ++e) {
-                while (e >= next) {
-                    ++k;
-                    next = (k + 1 < nitems) ? sm.pref[k + 1] : ~0ull;
+            // all loads of this thread's entries first, then all atomics, so
+            // neither the index reads nor the bit sets wait on one another
+            uint32_t gid[TR_EPT];
+#pragma unroll
+            for (int i = 0; i < TR_EPT; ++i) {
+                const uint64_t ee = e + i;
+                gid[i] = 0xffffffffu;
+                if (ee < e1) {
+                    while (ee >= next) {
+                        ++k;
+                        next = (k + 1 < nitems) ? sm.pref[k + 1] : ~0ull;
+                    }
+                    gid[i] = idx_pos[sm.base[k] + ee] >> shift;
                 }
-                const uint32_t gid = idx_pos[sm.base[k] + e] >> shift;
-                if (gid == last_g) continue;
-                last_g = gid;
-                const uint32_t wd = gid >> 5;
-                if (wd != acc_word) {
-                    if (acc_bits) or_group_bits(gbits, acc_word, acc_bits, append, sm);
-                    acc_word = wd;
-                    acc_bits = 0;
-                }
-                acc_bits |= 1u << (gid & 31);
             }
-            if (acc_bits) or_group_bits(gbits, acc_word, acc_bits, append, sm);
+            uint32_t old[TR_EPT];
+#pragma unroll
+            for (int i = 0; i < TR_EPT; ++i) {
+                old[i] = 0xffffffffu;
+                // a source's positions ascend: equal groups are adjacent
+                const bool fresh_gid = gid[i] != 0xffffffffu && (i == 0 || gid[i] != gid[i - 1]);
+                if (fresh_gid) {
+                    const uint32_t bit = 1u << (gid[i] & 31);
+                    if (append) old[i] = atomicOr(&gbits[gid[i] >> 5], bit);
+                    else atomicOr(&gbits[gid[i] >> 5], bit);
+                }
+            }
+            if (append) {
+#pragma unroll
+                for (int i = 0; i < TR_EPT; ++i) {
+                    if (old[i] != 0xffffffffu && !((old[i] >> (gid[i] & 31)) & 1u))
+                        sm.app[atomicAdd(&sm.napp, 1u)] = gid[i];
+                }
+            }
         }
         if (append) flush_appended(sm, glist, ctx_out(c, it), ngroups);
         else __syncthreads();
@@ -347,13 +363,13 @@ __device__ __forceinline__ void transform_phase(const LoopCtx &c, uint64_t it, c
 
 __global__ void __launch_bounds__(TR_THREADS) transform_kernel(
     LoopCtx c, const uint32_t *fvert0, const uint32_t *fvert1, const uint32_t *fpref0,
-    const uint32_t *fpref1, const uint64_t *idx_off, const uint32_t *idx_pos, int shift,
-    uint32_t *gbits, int append, uint32_t *glist, uint64_t ngroups) {
+    const uint32_t *fpref1, const uint32_t *tstart0, const uint32_t *tstart1, const uint64_t *idx_off,
+    const uint32_t *idx_pos, int shift, uint32_t *gbits, int append, uint32_t *glist, uint64_t ngroups) {
     const uint64_t it = ctx_iter(c);
     if (ctx_mode(c, it) != MODE_WEDGE) return;
     __shared__ TransformSmem sm;
-    transform_phase(c, it, fvert0, fvert1, fpref0, fpref1, idx_off, idx_pos, shift, gbits, append, glist,
-                    ngroups, sm, blockIdx.x, gridDim.x);
+    transform_phase(c, it, fvert0, fvert1, fpref0, fpref1, tstart0, tstart1, idx_off, idx_pos, shift, gbits,
+                    append, glist, ngroups, sm, blockIdx.x, gridDim.x);
 }
 
 }  // namespace wg

@@ -51,11 +51,18 @@ struct PullBufs {
     uint32_t *fbits[2];
     uint32_t *fvert[2];
     uint32_t *fpref[2];
+    uint32_t *tstart[2];
     const uint32_t *glist;
     uint32_t n;
 };
 
 constexpr int PULL_THREADS = 256;
+#ifndef SPARSE_MINB
+#define SPARSE_MINB 3
+#endif
+#ifndef SPARSE_U
+#define SPARSE_U 2
+#endif
 constexpr int PULL_WARPS = PULL_THREADS / 32;
 constexpr int STAGE = 96;  // per-warp staged frontier entries
 constexpr uint32_t NONE = 0xffffffffu;
@@ -106,7 +113,8 @@ struct PullOut {
 };
 
 __device__ __forceinline__ void flush_stage(PullOut &o, const wg_graph &g, wg_iter_rec *out,
-                                            uint32_t *overt, uint32_t *opref, uint32_t n) {
+                                            uint32_t *overt, uint32_t *opref, uint32_t *otstart,
+                                            uint32_t n) {
     const unsigned lane = lane_id();
     for (uint32_t base = 0; base < o.staged; base += 32) {
         const bool have = base + lane < o.staged;
@@ -131,9 +139,11 @@ __device__ __forceinline__ void flush_stage(PullOut &o, const wg_graph &g, wg_it
         nzb = __shfl_sync(FULL, nzb, 0);
         zb = __shfl_sync(FULL, zb, 0);
         if (nz) {
-            uint64_t pos = (nzb >> 32) + __popc(nzm & lanemask_lt());
+            const uint64_t pos = (nzb >> 32) + __popc(nzm & lanemask_lt());
+            const uint32_t pref = (uint32_t)(nzb & 0xffffffffull) + (incl - len);
             overt[pos] = d;
-            opref[pos] = (uint32_t)(nzb & 0xffffffffull) + (incl - len);
+            opref[pos] = pref;
+            if (otstart) mark_tile_starts(otstart, pref, len, (uint32_t)pos);
         } else if (have) {
             overt[n - 1 - (zb + __popc(zm & lanemask_lt()))] = d;
         }
@@ -240,7 +250,7 @@ __device__ __forceinline__ void finish_tile(uint32_t d, T agg, T pd, bool act, b
                                             Carry<T> &cy, T INF, int64_t inc, T *nxt,
                                             uint32_t *obits, PullOut &o, const wg_graph &g,
                                             wg_iter_rec *out, uint32_t *overt, uint32_t *opref,
-                                            uint32_t n) {
+                                            uint32_t *otstart, uint32_t n) {
     const unsigned lane = lane_id();
     const unsigned am = __ballot_sync(FULL, act);
     o.touched += __popc(am);
@@ -281,7 +291,7 @@ __device__ __forceinline__ void finish_tile(uint32_t d, T agg, T pd, bool act, b
     const bool right = !(lane == 31 && last_tile && dright == d);
     const bool app = tail && act && !(carry && lane == 31);
     apply_segments<T>(app, d, agg, pd, left && right, INF, inc, nxt, obits, o);
-    if (o.staged > STAGE - 34) flush_stage(o, g, out, overt, opref, n);
+    if (o.staged > STAGE - 34) flush_stage(o, g, out, overt, opref, otstart, n);
 }
 
 // ---------------------------------------------------------------------------
@@ -353,6 +363,7 @@ __global__ void __launch_bounds__(PULL_THREADS) pull_kernel(LoopCtx c, wg_graph 
     uint32_t *__restrict__ obits = ((it & 1) ? b.fbits[1] : b.fbits[0]);
     uint32_t *__restrict__ overt = ((it & 1) ? b.fvert[1] : b.fvert[0]);
     uint32_t *__restrict__ opref = ((it & 1) ? b.fpref[1] : b.fpref[0]);
+    uint32_t *otstart = ((it & 1) ? b.tstart[1] : b.tstart[0]);
     const uint64_t nitems = wedge ? (out->groups << shift) : g.nvec;
     const T INF = VT::inf(sentinel);
     const unsigned lane = lane_id();
@@ -401,10 +412,10 @@ __global__ void __launch_bounds__(PULL_THREADS) pull_kernel(LoopCtx c, wg_graph 
             for (int u = 0; u < U; ++u) {
                 if (tile + u < t1)
                     finish_tile<T>(d[u], agg[u], pd[u], act[u], tile + u == t0, tile + u == t1 - 1, dleft,
-                               dright, cy, INF, inc, nxt, obits, o, g, out, overt, opref, b.n);
+                               dright, cy, INF, inc, nxt, obits, o, g, out, overt, opref, otstart, b.n);
             }
         }
-        if (o.staged) flush_stage(o, g, out, overt, opref, b.n);
+        if (o.staged) flush_stage(o, g, out, overt, opref, otstart, b.n);
     }
     end_of_pull<T>(o, out);
 }
@@ -452,6 +463,7 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) pull_dense_tma_kernel(Loop
     uint32_t *__restrict__ obits = ((it & 1) ? b.fbits[1] : b.fbits[0]);
     uint32_t *__restrict__ overt = ((it & 1) ? b.fvert[1] : b.fvert[0]);
     uint32_t *__restrict__ opref = ((it & 1) ? b.fpref[1] : b.fpref[0]);
+    uint32_t *otstart = ((it & 1) ? b.tstart[1] : b.tstart[0]);
     const uint32_t nvec = (uint32_t)g.nvec;
     const T INF = VT::inf(sentinel);
     const unsigned lane = lane_id();
@@ -602,10 +614,10 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) pull_dense_tma_kernel(Loop
                 const bool right = !(lane == 31 && last_tile && dright == d[u]);
                 const bool app = tail && valid[u] && !(carry && lane == 31);
                 apply_segments<T>(app, d[u], agg[u], pd[u], left && right, INF, inc, nxt, obits, o);
-                if (o.staged > STAGE - 34) flush_stage(o, g, out, overt, opref, b.n);
+                if (o.staged > STAGE - 34) flush_stage(o, g, out, overt, opref, otstart, b.n);
             }
         }
-        if (o.staged) flush_stage(o, g, out, overt, opref, b.n);
+        if (o.staged) flush_stage(o, g, out, overt, opref, otstart, b.n);
     }
     end_of_pull<T>(o, out);
 }
@@ -624,6 +636,7 @@ __device__ __forceinline__ void sparse_pull_phase(const LoopCtx &c, uint64_t it,
                                                   int64_t sentinel, uint32_t *gbits, uint64_t ngroups_all,
                                                   uint32_t *stage, uint64_t gwarp, uint64_t nwarps) {
     using VT = ValTraits<T>;
+    constexpr int U = SPARSE_U;  // tiles per warp step: independent load chains in flight
     wg_iter_rec *out = ctx_out(c, it);
     // no read-only-cache loads of values here: the persistent loop rewrites them
     const T *prev = (const T *)(((it - 1) & 1) ? b.vals[1] : b.vals[0]);
@@ -631,6 +644,7 @@ __device__ __forceinline__ void sparse_pull_phase(const LoopCtx &c, uint64_t it,
     uint32_t *obits = ((it & 1) ? b.fbits[1] : b.fbits[0]);
     uint32_t *overt = ((it & 1) ? b.fvert[1] : b.fvert[0]);
     uint32_t *opref = ((it & 1) ? b.fpref[1] : b.fpref[0]);
+    uint32_t *otstart = ((it & 1) ? b.tstart[1] : b.tstart[0]);
     const T INF = VT::inf(sentinel);
     const unsigned lane = lane_id();
     const unsigned le = 0xffffffffu >> (31 - lane);
@@ -644,48 +658,68 @@ __device__ __forceinline__ void sparse_pull_phase(const LoopCtx &c, uint64_t it,
         if (*(volatile const uint64_t *)&out->reserved[1]) cov -= ngroups_all * vpg - g.nvec;
         out->covered_vectors = cov;
     }
-    for (uint64_t tile = gwarp; tile < ntiles; tile += nwarps) {
-        const uint64_t gi = tile * gpt + (lane >> shift);
-        const bool gvalid = gi < nsel;
-        const uint64_t grp = gvalid ? ((volatile const uint32_t *)b.glist)[gi] : 0;
-        const uint64_t p = (grp << shift) + j;
-        const bool valid = gvalid && p < g.nvec;
-        const uint32_t d = valid ? g.vdst[p] : NONE;
-        T pd = INF, agg = INF;
-        if (FILTER && valid) pd = prev[d];
-        const bool act = valid && !(FILTER && pd != INF);
-        if (act) {
-            uint32_t src[W], wt[W];
-            load_lanes<W>(g.vsrc, p, src);
-            if (WEIGHT) load_lanes<W>(g.vw, p, wt);
-            agg = fold_lanes<T, W, WEIGHT>(src, wt, prev, INF, o.ovf);
+    for (uint64_t t0 = gwarp * U; t0 < ntiles; t0 += nwarps * U) {
+        uint64_t grp[U], p[U];
+        uint32_t d[U];
+        bool gvalid[U], valid[U], act[U];
+        T pd[U], agg[U];
+        unsigned heads[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t gi = (t0 + u) * gpt + (lane >> shift);
+            gvalid[u] = gi < nsel;
+            grp[u] = gvalid[u] ? ((volatile const uint32_t *)b.glist)[gi] : 0;
         }
-        if (gvalid && j == 0) gbits[grp >> 5] = 0;  // every bit of this word was set this iteration
-        const unsigned am = __ballot_sync(FULL, act);
-        o.touched += __popc(am);
-        const uint32_t dp = __shfl_up_sync(FULL, d, 1);
-        const unsigned heads = __ballot_sync(FULL, j == 0 || dp != d);
-        const unsigned hl = 31u - __clz(heads & le);
-        const unsigned dist = lane - hl;
-        const unsigned maxd = __reduce_max_sync(FULL, dist);
-        for (unsigned off = 1; off <= maxd; off <<= 1) {
-            const T ov = shfl_up_t(agg, (int)off);
-            if (off <= dist && ov < agg) agg = ov;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            p[u] = (grp[u] << shift) + j;
+            valid[u] = gvalid[u] && p[u] < g.nvec;
+            d[u] = valid[u] ? g.vdst[p[u]] : NONE;
+            if (gvalid[u] && j == 0) gbits[grp[u] >> 5] = 0;  // all its bits were set this iteration
         }
-        const bool tail = (((heads >> 1) | 0x80000000u) >> lane) & 1u;
-        const bool app = tail && act;
-        bool complete = true;
-        if (app) {
-            if (!FILTER) pd = prev[d];
-            // left: the segment starts at the group's first vector -> look before it
-            if ((hl & jmask) == 0 && grp > 0 && g.vdst[(grp << shift) - 1] == d) complete = false;
-            // right: the segment ends at the group's last vector -> look after it
-            if (j == jmask && p + 1 < g.nvec && g.vdst[p + 1] == d) complete = false;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            pd[u] = INF;
+            agg[u] = INF;
+            if (FILTER && valid[u]) pd[u] = prev[d[u]];
+            act[u] = valid[u] && !(FILTER && pd[u] != INF);
+            const uint32_t dp = __shfl_up_sync(FULL, d[u], 1);
+            heads[u] = __ballot_sync(FULL, j == 0 || dp != d[u]);
+            if (act[u]) {
+                uint32_t src[W], wt[W];
+                load_lanes<W>(g.vsrc, p[u], src);
+                if (WEIGHT) load_lanes<W>(g.vw, p[u], wt);
+                agg[u] = fold_lanes<T, W, WEIGHT>(src, wt, prev, INF, o.ovf);
+                const bool tail = (((heads[u] >> 1) | 0x80000000u) >> lane) & 1u;
+                if (!FILTER && tail) pd[u] = prev[d[u]];
+            }
         }
-        apply_segments<T>(app, d, agg, pd, complete, INF, inc, nxt, obits, o);
-        if (o.staged > STAGE - 34) flush_stage(o, g, out, overt, opref, b.n);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (t0 + u >= ntiles) continue;
+            o.touched += __popc(__ballot_sync(FULL, act[u]));
+            const unsigned hl = 31u - __clz(heads[u] & le);
+            const unsigned dist = lane - hl;
+            const unsigned maxd = __reduce_max_sync(FULL, dist);
+            for (unsigned off = 1; off <= maxd; off <<= 1) {
+                const T ov = shfl_up_t(agg[u], (int)off);
+                if (off <= dist && ov < agg[u]) agg[u] = ov;
+            }
+            const bool tail = (((heads[u] >> 1) | 0x80000000u) >> lane) & 1u;
+            const bool app = tail && act[u];
+            bool complete = true;
+            if (app) {
+                const uint64_t g0 = grp[u] << shift;
+                // left: the segment starts at the group's first vector -> look before it
+                if ((hl & jmask) == 0 && g0 > 0 && g.vdst[g0 - 1] == d[u]) complete = false;
+                // right: the segment ends at the group's last vector -> look after it
+                if (j == jmask && p[u] + 1 < g.nvec && g.vdst[p[u] + 1] == d[u]) complete = false;
+            }
+            apply_segments<T>(app, d[u], agg[u], pd[u], complete, INF, inc, nxt, obits, o);
+            if (o.staged > STAGE - 34) flush_stage(o, g, out, overt, opref, otstart, b.n);
+        }
     }
-    if (o.staged) flush_stage(o, g, out, overt, opref, b.n);
+    if (o.staged) flush_stage(o, g, out, overt, opref, otstart, b.n);
     end_of_pull<T>(o, out);
 }
 
@@ -710,8 +744,8 @@ __global__ void __launch_bounds__(PULL_THREADS) pull_sparse_kernel(LoopCtx c, wg
 // bitmap of iteration it-1 (reused by it+1), finalises the record and zeroes
 // the record the next iteration will fill.
 template <typename T>
-__device__ __forceinline__ void finalize_phase(const LoopCtx &c, uint64_t it, int mode, const PullBufs &b,
-                                               uint64_t tid, uint64_t nthreads) {
+__device__ __forceinline__ void end_of_iteration(const LoopCtx &c, uint64_t it, int mode, const PullBufs &b,
+                                                 uint64_t tid, uint64_t nthreads, int zero_ahead) {
     if (mode != MODE_NONE) {
         const wg_iter_rec *out = ctx_out(c, it);
         const wg_iter_rec *in = ctx_in(c, it);
@@ -746,7 +780,7 @@ __device__ __forceinline__ void finalize_phase(const LoopCtx &c, uint64_t it, in
             out->frontier_out = (*(volatile uint64_t *)&out->nz_packed >> 32) + *(volatile uint64_t *)&out->z_count;
             out->active_edges = *(volatile const uint64_t *)&ctx_in(c, it)->out_edge_sum;
         }
-        uint64_t *q = (uint64_t *)&c.recs[(it + 1) % c.ring];
+        uint64_t *q = (uint64_t *)&c.recs[(it + zero_ahead) % c.ring];
 #pragma unroll
         for (int i = 0; i < 16; ++i) q[i] = 0;
     }
@@ -756,8 +790,8 @@ template <typename T>
 __global__ void __launch_bounds__(256) finalize_kernel(LoopCtx c, PullBufs b) {
     const uint64_t it = ctx_iter(c);
     const int mode = ctx_mode(c, it);
-    finalize_phase<T>(c, it, mode, b, (uint64_t)blockIdx.x * blockDim.x + threadIdx.x,
-                      (uint64_t)gridDim.x * blockDim.x);
+    end_of_iteration<T>(c, it, mode, b, (uint64_t)blockIdx.x * blockDim.x + threadIdx.x,
+                        (uint64_t)gridDim.x * blockDim.x, 1);
 }
 
 // ---------------- persistent sparse loop ----------------------------------
@@ -769,8 +803,24 @@ __global__ void __launch_bounds__(256) finalize_kernel(LoopCtx c, PullBufs b) {
 // ctrl[1]); the regular kernels of the loop graph take it from there.  This is
 // what keeps high-diameter runs (the 4096^2 grid: ~8.6K thin wavefronts) from
 // paying several kernel launches per iteration.
+// Optional phase timestamps of the persistent loop (tools/prof_persistent.py):
+// 4 x uint64 %globaltimer per iteration.
+__device__ uint64_t *g_phase_ts = nullptr;
+__device__ uint64_t g_phase_cap = 0;
+
+__device__ __forceinline__ uint64_t globaltimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__device__ __forceinline__ void phase_stamp(uint64_t it, int k) {
+    uint64_t *buf = g_phase_ts;
+    if (buf && it < g_phase_cap && blockIdx.x == 0 && threadIdx.x == 0) buf[it * 4 + k] = globaltimer();
+}
+
 template <typename T, int W, bool WEIGHT, bool FILTER>
-__global__ void __launch_bounds__(PULL_THREADS) sparse_loop_kernel(LoopCtx c, wg_graph g, PullBufs b,
+__global__ void __launch_bounds__(PULL_THREADS, SPARSE_MINB) sparse_loop_kernel(LoopCtx c, wg_graph g, PullBufs b,
                                                                    int shift, int64_t inc, int64_t sentinel,
                                                                    uint32_t *gbits, uint64_t ngroups) {
     __shared__ TransformSmem tsm;
@@ -781,21 +831,40 @@ __global__ void __launch_bounds__(PULL_THREADS) sparse_loop_kernel(LoopCtx c, wg
     const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
     uint64_t *ctrl = const_cast<uint64_t *>(c.ctrl);
-    while (true) {
-        const uint64_t it = *(volatile uint64_t *)&ctrl[0] + 1;
-        const int mode = ctx_mode(c, it);  // includes the launch limit
-        if (mode != MODE_WEDGE) break;
-        if (g.entries == 0) break;
+    const uint64_t first = *(volatile uint64_t *)&ctrl[0] + 1;
+    uint64_t it = first;
+    if (g.entries == 0) return;
+    // iteration `first`'s record was zeroed by whoever finished first-1; the
+    // end-of-iteration work below zeroes one record further ahead
+    if (tid == 0) {
+        uint64_t *q = (uint64_t *)&c.recs[(first + 1) % c.ring];
+        for (int i = 0; i < 16; ++i) q[i] = 0;
+    }
+    grid.sync();
+    while (ctx_mode(c, it) == MODE_WEDGE) {
+        phase_stamp(it, 0);
         if (tid == 0) ctx_out(c, it)->reserved[0] = 3;
-        transform_phase(c, it, b.fvert[0], b.fvert[1], b.fpref[0], b.fpref[1], g.idx_off, g.idx_pos, shift,
-                        gbits, 1, const_cast<uint32_t *>(b.glist), ngroups, tsm, blockIdx.x, gridDim.x);
+        // phase A: transform(it)  ||  end of iteration it-1 (buffer sync, bitmap
+        // clear, record) -- independent: it-1's end writes vals[it&1] and
+        // fbits[it&1], which only the pull of `it` touches, after the barrier
+        transform_phase(c, it, b.fvert[0], b.fvert[1], b.fpref[0], b.fpref[1], b.tstart[0], b.tstart[1],
+                        g.idx_off, g.idx_pos, shift, gbits, 1, const_cast<uint32_t *>(b.glist), ngroups, tsm,
+                        blockIdx.x, gridDim.x);
+        if (it > first) end_of_iteration<T>(c, it - 1, MODE_WEDGE, b, tid, nthreads, 2);
         grid.sync();
+        phase_stamp(it, 1);
+        // phase B: pull(it)
         sparse_pull_phase<T, W, WEIGHT, FILTER>(c, it, g, b, shift, inc, sentinel, gbits, ngroups,
                                                 s_stage[threadIdx.x >> 5], gwarp, nwarps);
         grid.sync();
-        finalize_phase<T>(c, it, MODE_WEDGE, b, tid, nthreads);
-        if (tid == 0) *(volatile uint64_t *)&ctrl[0] = it;
-        grid.sync();
+        phase_stamp(it, 2);
+        phase_stamp(it, 3);
+        ++it;
+    }
+    // the last iteration run here still needs its end-of-iteration work
+    if (it > first) {
+        end_of_iteration<T>(c, it - 1, MODE_WEDGE, b, tid, nthreads, 1);
+        if (tid == 0) *(volatile uint64_t *)&ctrl[0] = it - 1;
     }
 }
 

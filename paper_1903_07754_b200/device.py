@@ -332,9 +332,9 @@ class DeviceLoop:
         torch = _torch()
         self.g, self.shift, self.val_type, self.ring = g, int(shift), int(val_type), int(ring)
         L = _lib.load()
-        sizes = (ctypes.c_uint64 * 4)()
+        sizes = (ctypes.c_uint64 * 5)()
         check(L.wg_run_buffer_sizes(ctypes.byref(g.struct()), self.shift, sizes))
-        fwords, groups, gwords, nbc = (int(x) for x in sizes)
+        fwords, groups, gwords, nbc, ntst = (int(x) for x in sizes)
         n = max(g.n, 1)
         dt = torch.int32 if self.val_type == WG_VAL_U32 else torch.int64
         dev = "cuda"
@@ -342,6 +342,7 @@ class DeviceLoop:
         self.fbits = [torch.zeros(max(fwords, 1), dtype=torch.int32, device=dev) for _ in range(2)]
         self.fvert = [torch.empty(n, dtype=torch.int32, device=dev) for _ in range(2)]
         self.fpref = [torch.empty(n, dtype=torch.int32, device=dev) for _ in range(2)]
+        self.tstart = [torch.zeros(max(ntst, 1), dtype=torch.int32, device=dev) for _ in range(2)]
         self.gbits = torch.zeros(max(gwords, 1), dtype=torch.int32, device=dev)
         self.glist = torch.empty(max(groups, 1), dtype=torch.int32, device=dev)
         self.bcount = torch.empty(max(nbc, 1), dtype=torch.int64, device=dev)
@@ -354,6 +355,7 @@ class DeviceLoop:
             b.fbits[i] = _ptr(self.fbits[i])
             b.fvert[i] = _ptr(self.fvert[i])
             b.fpref[i] = _ptr(self.fpref[i])
+            b.tstart[i] = _ptr(self.tstart[i])
         b.gbits, b.glist, b.bcount = _ptr(self.gbits), _ptr(self.glist), _ptr(self.bcount)
         b.recs, b.ctrl, b.ring = _ptr(self.recs), _ptr(self.ctrl), self.ring
         self.bufs = b
