@@ -102,7 +102,7 @@ DenseFn pick_dense_wt(size_t *smem) {
         case 3:
             *smem = TmaSmem<W, WEIGHT, 2, 3>::BLOCK_BYTES;
             return pull_dense_tma_kernel<T, W, WEIGHT, 2, 3, 3>;
-        default:
+        default:  // 2 tiles x 4 stages
             *smem = TmaSmem<W, WEIGHT, 2, 4>::BLOCK_BYTES;
             return pull_dense_tma_kernel<T, W, WEIGHT, 2, 4, 1>;
     }
@@ -308,6 +308,20 @@ int launch_pull(const LoopCtx &c, const wg_graph *g, const PullBufs &pb, int val
         dn<<<grid, PULL_THREADS, smem, s>>>(c, *g, pb, shift, k->apply_increment, k->sentinel);
         ::wg::count_launch();
         WG_CHECK_LAUNCH("pull (dense, TMA)");
+        // the dense pull only sets bits: build the produced frontier from the bitmap
+        FrontierBufs fb;
+        for (int i = 0; i < 2; ++i) {
+            fb.fbits[i] = pb.fbits[i];
+            fb.fvert[i] = pb.fvert[i];
+            fb.fpref[i] = pb.fpref[i];
+            fb.tstart[i] = pb.tstart[i];
+        }
+        const uint64_t nb = cb_blocks(g->n ? g->n : 1);
+        loop_frontier_count_kernel<<<(unsigned)nb, CB_THREADS, 0, s>>>(c, fb, g->n, g->idx_off, g->outdeg,
+                                                                      pb.bcount);
+        loop_frontier_list_kernel<<<(unsigned)nb, CB_THREADS, 0, s>>>(c, fb, g->n, g->idx_off, pb.bcount);
+        ::wg::count_launch(2);
+        WG_CHECK_LAUNCH("dense frontier compaction");
         handles &= ~(1 << MODE_FULL);
         if (c.forced_mode == MODE_FULL || handles == 0) return WG_OK;
     }
@@ -399,6 +413,7 @@ static int pull_common(const wg_graph *g, const uint32_t *d_wedge_words, int shi
     pb.tstart[0] = ws.tstart[0];
     pb.tstart[1] = ws.tstart[1];
     pb.glist = ws.glist;
+    pb.bcount = ws.bcount;
     pb.n = g->n;
     if ((rc = launch_pull(c, g, pb, val_type, shift, k, items, s))) return rc;
     wg_iter_rec h[2];
@@ -537,6 +552,7 @@ static PullBufs pull_bufs(const wg_graph *g, const wg_run_bufs *b) {
         pb.tstart[i] = b->tstart[i];
     }
     pb.glist = b->glist;
+    pb.bcount = b->bcount;
     pb.n = g->n;
     return pb;
 }

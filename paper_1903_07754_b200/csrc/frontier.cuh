@@ -122,11 +122,9 @@ __global__ void __launch_bounds__(CB_THREADS) group_list_kernel(LoopCtx c, uint3
 // transform's load-balancing key); members without out-edges go to the back.
 // bcount holds 4 counters per block: nz members, their entries, zero-degree
 // members, out-degree sum.
-__global__ void __launch_bounds__(CB_THREADS) frontier_count_kernel(const uint32_t *words,
-                                                                    uint64_t nbits,
-                                                                    const uint64_t *idx_off,
-                                                                    const uint32_t *outdeg,
-                                                                    uint64_t *bcount) {
+__device__ __forceinline__ void frontier_count_body(const uint32_t *words, uint64_t nbits,
+                                                    const uint64_t *idx_off, const uint32_t *outdeg,
+                                                    uint64_t *bcount) {
     __shared__ uint64_t sm[33];
     uint64_t w0 = (uint64_t)blockIdx.x * CB_WORDS + threadIdx.x * CB_WPT;
     uint64_t nz = 0, ent = 0, z = 0, es = 0;
@@ -152,9 +150,10 @@ __global__ void __launch_bounds__(CB_THREADS) frontier_count_kernel(const uint32
     }
 }
 
-__global__ void __launch_bounds__(CB_THREADS) frontier_list_kernel(
-    const uint32_t *words, uint64_t nbits, const uint64_t *idx_off, const uint64_t *bcount,
-    uint32_t *fvert, uint32_t *fpref, uint32_t *tstart, wg_iter_rec *rec) {
+__device__ __forceinline__ void frontier_list_body(const uint32_t *words, uint64_t nbits,
+                                                   const uint64_t *idx_off, const uint64_t *bcount,
+                                                   uint32_t *fvert, uint32_t *fpref, uint32_t *tstart,
+                                                   wg_iter_rec *rec) {
     __shared__ uint64_t sm[33];
     uint64_t nz_base = prior_blocks_sum(bcount, blockIdx.x, 4, 0, sm);
     uint64_t ent_base = prior_blocks_sum(bcount, blockIdx.x, 4, 1, sm);
@@ -207,6 +206,45 @@ __global__ void __launch_bounds__(CB_THREADS) frontier_list_kernel(
         rec->frontier_out = nz_all + z_all;
         rec->out_edge_sum = es;
     }
+}
+
+__global__ void __launch_bounds__(CB_THREADS) frontier_count_kernel(const uint32_t *words, uint64_t nbits,
+                                                                    const uint64_t *idx_off,
+                                                                    const uint32_t *outdeg, uint64_t *bcount) {
+    frontier_count_body(words, nbits, idx_off, outdeg, bcount);
+}
+
+__global__ void __launch_bounds__(CB_THREADS) frontier_list_kernel(const uint32_t *words, uint64_t nbits,
+                                                                   const uint64_t *idx_off, const uint64_t *bcount,
+                                                                   uint32_t *fvert, uint32_t *fpref,
+                                                                   uint32_t *tstart, wg_iter_rec *rec) {
+    frontier_list_body(words, nbits, idx_off, bcount, fvert, fpref, tstart, rec);
+}
+
+// The same two passes inside the device loop after a dense pull, which only
+// sets next-frontier bits: build iteration it's member list, tile starts,
+// counts and out-degree sum from its bitmap (gated on the device mode).
+struct FrontierBufs {
+    uint32_t *fbits[2], *fvert[2], *fpref[2], *tstart[2];
+};
+
+__global__ void __launch_bounds__(CB_THREADS) loop_frontier_count_kernel(LoopCtx c, FrontierBufs f, uint64_t n,
+                                                                         const uint64_t *idx_off,
+                                                                         const uint32_t *outdeg,
+                                                                         uint64_t *bcount) {
+    const uint64_t it = ctx_iter(c);
+    if (ctx_mode(c, it) != MODE_FULL) return;
+    frontier_count_body((it & 1) ? f.fbits[1] : f.fbits[0], n, idx_off, outdeg, bcount);
+}
+
+__global__ void __launch_bounds__(CB_THREADS) loop_frontier_list_kernel(LoopCtx c, FrontierBufs f, uint64_t n,
+                                                                        const uint64_t *idx_off,
+                                                                        const uint64_t *bcount) {
+    const uint64_t it = ctx_iter(c);
+    if (ctx_mode(c, it) != MODE_FULL) return;
+    const int k = (int)(it & 1);
+    frontier_list_body(k ? f.fbits[1] : f.fbits[0], n, idx_off, bcount, k ? f.fvert[1] : f.fvert[0],
+                       k ? f.fpref[1] : f.fpref[0], k ? f.tstart[1] : f.tstart[0], ctx_out(c, it));
 }
 
 // ---------------- K3: Wedge transform --------------------------------------

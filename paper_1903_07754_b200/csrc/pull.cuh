@@ -52,6 +52,7 @@ struct PullBufs {
     uint32_t *fvert[2];
     uint32_t *fpref[2];
     uint32_t *tstart[2];
+    uint64_t *bcount;  // compaction scratch (dense-pull frontier build)
     const uint32_t *glist;
     uint32_t n;
 };
@@ -199,6 +200,34 @@ __device__ __forceinline__ void apply_segments(bool app, uint32_t d, T agg, T pd
     if (newly) o.stage[o.staged + __popc(nm & lanemask_lt())] = d;
     __syncwarp();
     o.staged += __popc(nm);
+}
+
+// Dense-mode apply: values and next-frontier bits only; the member list, its
+// index-length prefixes and the out-degree sum are produced afterwards by the
+// ordered bitmap compaction (frontier_count/list kernels), which is cheaper
+// than staging ~V appends inside the pull.
+template <typename T>
+__device__ __forceinline__ void apply_dense(bool app, uint32_t d, T agg, T pd, bool complete, T INF,
+                                            int64_t inc, T *nxt, uint32_t *obits, uint32_t &ovf) {
+    using VT = ValTraits<T>;
+    if (!app) return;
+    T cand;
+    if constexpr (VT::U32) {
+        if (agg == INF) return;
+        const uint64_t cc = (uint64_t)agg + (uint64_t)inc;
+        if (cc >= 0xffffffffull) {
+            ovf = 1;
+            return;
+        }
+        cand = (T)cc;
+    } else {
+        cand = agg + (T)inc;
+    }
+    if (!(cand < pd)) return;
+    if (complete) nxt[d] = cand;
+    else if constexpr (VT::U32) atomicMin((unsigned *)&nxt[d], (unsigned)cand);
+    else atomicMin((long long *)&nxt[d], (long long)cand);
+    atomicOr(&obits[d >> 5], 1u << (d & 31));
 }
 
 // Fold one vector's lanes into a minimum (messages prev[src] (+ weight)).
@@ -594,7 +623,7 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) pull_dense_tma_kernel(Loop
                     cin = cy.agg;
                     left0 = cy.left;
                 } else {
-                    apply_segments<T>(lane == 0, cy.d, cy.agg, cy.pd, cy.left, INF, inc, nxt, obits, o);
+                    apply_dense<T>(lane == 0, cy.d, cy.agg, cy.pd, cy.left, INF, inc, nxt, obits, o.ovf);
                     left0 = true;
                 }
                 // the head segment's tail lane takes the carried minimum
@@ -613,11 +642,9 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) pull_dense_tma_kernel(Loop
                 const bool left = (heads[u] & le & ~1u) ? true : left0;
                 const bool right = !(lane == 31 && last_tile && dright == d[u]);
                 const bool app = tail && valid[u] && !(carry && lane == 31);
-                apply_segments<T>(app, d[u], agg[u], pd[u], left && right, INF, inc, nxt, obits, o);
-                if (o.staged > STAGE - 34) flush_stage(o, g, out, overt, opref, otstart, b.n);
+                apply_dense<T>(app, d[u], agg[u], pd[u], left && right, INF, inc, nxt, obits, o.ovf);
             }
         }
-        if (o.staged) flush_stage(o, g, out, overt, opref, otstart, b.n);
     }
     end_of_pull<T>(o, out);
 }
