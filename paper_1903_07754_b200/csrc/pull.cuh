@@ -465,6 +465,46 @@ struct TmaSmem {
 
 __device__ __forceinline__ uint32_t pad16(uint32_t b) { return (b + 15u) & ~15u; }
 
+// One dense-pull chunk after its gathers were issued: destinations, segment
+// heads, the raw gathered messages (INF for padding lanes) and prev[d] of
+// segment tails.
+template <typename T, int W, bool WEIGHT, int CH>
+struct DenseChunk {
+    uint32_t d[CH];
+    unsigned heads[CH];
+    bool valid[CH];
+    T ps[CH][W];
+    uint32_t wt[CH][WEIGHT ? W : 1];
+    T pd[CH];
+};
+
+// fold_lanes over already-gathered messages (a lane whose source value is INF
+// never contributes: INF + w >= INF for both encodings)
+template <typename T, int W, bool WEIGHT>
+__device__ __forceinline__ T fold_gathered(const T (&ps)[W], const uint32_t (&wt)[WEIGHT ? W : 1], T INF,
+                                           uint32_t &ovf) {
+    using VT = ValTraits<T>;
+    T agg = INF;
+#pragma unroll
+    for (int l = 0; l < W; ++l) {
+        if constexpr (!WEIGHT) {
+            agg = ps[l] < agg ? ps[l] : agg;
+        } else if constexpr (VT::U32) {
+            if (ps[l] != INF) {
+                const uint64_t m = (uint64_t)ps[l] + wt[l];
+                if (m >= 0xffffffffull) ovf = 1;
+                else agg = (T)m < agg ? (T)m : agg;
+            }
+        } else {
+            if (ps[l] != INF) {
+                const T m = ps[l] + (T)wt[l];
+                agg = m < agg ? m : agg;
+            }
+        }
+    }
+    return agg;
+}
+
 // Dense pull, unfiltered programs (CC, SSSP, PageRank-like min-plus): the
 // warp streams its tile range with TMA and processes CH tiles per stage in
 // four phases so that independent work overlaps:
@@ -541,21 +581,21 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) pull_dense_tma_kernel(Loop
         dright = __shfl_sync(FULL, dright, 1);
         Carry<T> cy;
 
-        for (uint32_t ch = 0; ch < nchunks; ++ch) {
+        // software pipeline: chunk ch+1's gathers are in flight while chunk
+        // ch is reduced (two register sets, loop unrolled by two so that no
+        // copy touches a register with a load outstanding)
+        auto load = [&](uint32_t ch, DenseChunk<T, W, WEIGHT, CH> &k) {
             const int s = (int)(ch % TMA_S);
             mbar_wait(&bars[s], (ch / TMA_S) & 1u);
             const uint32_t *st = ring + (size_t)s * SM::STAGE_WORDS;
             const uint32_t tbase = tfirst + ch * CH;
-            // ---- phase 1: destinations, lanes, segment heads ----
-            uint32_t d[CH], src[CH][W], wt[CH][W];
-            unsigned heads[CH];
-            bool valid[CH];
+            uint32_t src[CH][W];
 #pragma unroll
             for (int u = 0; u < CH; ++u) {
                 const uint32_t tile = tbase + u;
                 const int j = u * 32 + lane;
-                valid[u] = tile < tend && (tile << 5) + lane < nvec;
-                d[u] = valid[u] ? st[SM::SRC_WORDS + j] : NONE;
+                k.valid[u] = tile < tend && (tile << 5) + lane < nvec;
+                k.d[u] = k.valid[u] ? st[SM::SRC_WORDS + j] : NONE;
                 if constexpr (W == 4) {
                     const uint4 v = *reinterpret_cast<const uint4 *>(st + j * 4);
                     src[u][0] = v.x; src[u][1] = v.y; src[u][2] = v.z; src[u][3] = v.w;
@@ -565,8 +605,8 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) pull_dense_tma_kernel(Loop
                 }
 #pragma unroll
                 for (int l = 0; l < W; ++l) {
-                    if (!valid[u]) src[u][l] = WG_NO_LANE;
-                    wt[u][l] = WEIGHT ? st[SM::SRC_WORDS + SM::VEC + j * W + l] : 0u;
+                    if (!k.valid[u]) src[u][l] = WG_NO_LANE;
+                    if constexpr (WEIGHT) k.wt[u][l] = st[SM::SRC_WORDS + SM::VEC + j * W + l];
                 }
             }
             // all lanes' generic-proxy reads of this stage precede the async-proxy
@@ -576,22 +616,30 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) pull_dense_tma_kernel(Loop
             if (lane == 0 && ch + TMA_S < nchunks) issue(ch + TMA_S);
 #pragma unroll
             for (int u = 0; u < CH; ++u) {
-                const uint32_t dp = __shfl_up_sync(FULL, d[u], 1);
-                heads[u] = __ballot_sync(FULL, lane == 0 || dp != d[u]);
+                const uint32_t dp = __shfl_up_sync(FULL, k.d[u], 1);
+                k.heads[u] = __ballot_sync(FULL, lane == 0 || dp != k.d[u]);
             }
-            // ---- phase 2: gathers (tails read prev[d]) ----
-            T pd[CH], agg[CH];
+            // the gathers (segment tails also read prev[d])
 #pragma unroll
             for (int u = 0; u < CH; ++u) {
-                const bool tail = (((heads[u] >> 1) | 0x80000000u) >> lane) & 1u;
-                pd[u] = (valid[u] && tail) ? prev[d[u]] : INF;
-                agg[u] = fold_lanes<T, W, WEIGHT>(src[u], wt[u], prev, INF, o.ovf);
+                const bool tail = (((k.heads[u] >> 1) | 0x80000000u) >> lane) & 1u;
+                k.pd[u] = (k.valid[u] && tail) ? prev[k.d[u]] : INF;
+#pragma unroll
+                for (int l = 0; l < W; ++l) k.ps[u][l] = src[u][l] != WG_NO_LANE ? prev[src[u][l]] : INF;
             }
-            // ---- phase 3: segmented min-scans, interleaved across tiles ----
+        };
+        auto reduce = [&](uint32_t ch, DenseChunk<T, W, WEIGHT, CH> &k) {
+            const uint32_t tbase = tfirst + ch * CH;
+            T agg[CH];
+#pragma unroll
+            for (int u = 0; u < CH; ++u) agg[u] = fold_gathered<T, W, WEIGHT>(k.ps[u], k.wt[u], INF, o.ovf);
+            // segmented min-scans, interleaved across tiles (none depends on
+            // the carry: the carried segment only ever joins a tile's HEAD
+            // segment, whose tail lane takes the carried minimum below)
             unsigned dist[CH], maxd = 0;
 #pragma unroll
             for (int u = 0; u < CH; ++u) {
-                dist[u] = lane - (31u - __clz(heads[u] & le));
+                dist[u] = lane - (31u - __clz(k.heads[u] & le));
                 maxd = dist[u] > maxd ? dist[u] : maxd;
             }
             maxd = __reduce_max_sync(FULL, maxd);
@@ -602,17 +650,17 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) pull_dense_tma_kernel(Loop
                     if (off <= dist[u] && ov < agg[u]) agg[u] = ov;
                 }
             }
-            // ---- phase 4: carry chain (warp-uniform), then applies ----
+            // warp-uniform carry chain across the CH tiles, then the applies
 #pragma unroll
             for (int u = 0; u < CH; ++u) {
                 const uint32_t tile = tbase + u;
                 if (tile >= tend) continue;
                 const bool last_tile = tile == tend - 1;
-                const uint32_t d0 = __shfl_sync(FULL, d[u], 0);
-                const uint32_t d31 = __shfl_sync(FULL, d[u], 31);
+                const uint32_t d0 = __shfl_sync(FULL, k.d[u], 0);
+                const uint32_t d31 = __shfl_sync(FULL, k.d[u], 31);
                 const T a31 = shfl_t(agg[u], 31);
-                const T p31 = shfl_t(pd[u], 31);
-                const unsigned first_tail = __ffs((heads[u] >> 1) | 0x80000000u) - 1;
+                const T p31 = shfl_t(k.pd[u], 31);
+                const unsigned first_tail = __ffs((k.heads[u] >> 1) | 0x80000000u) - 1;
                 bool left0;
                 bool merge = false;
                 T cin = INF;
@@ -626,24 +674,32 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) pull_dense_tma_kernel(Loop
                     apply_dense<T>(lane == 0, cy.d, cy.agg, cy.pd, cy.left, INF, inc, nxt, obits, o.ovf);
                     left0 = true;
                 }
-                // the head segment's tail lane takes the carried minimum
                 if (merge && lane == first_tail && cin < agg[u]) agg[u] = cin;
-                const bool whole = heads[u] == 1u;  // one segment spans the tile
+                const bool whole = k.heads[u] == 1u;  // one segment spans the tile
                 const bool carry = !last_tile && d31 != NONE;
                 if (carry) {
                     cy.d = d31;
                     cy.agg = (merge && whole && cin < a31) ? cin : a31;
                     cy.pd = p31;
-                    cy.left = (heads[u] >> 1) ? true : left0;  // a head after lane 0 precedes lane 31
+                    cy.left = (k.heads[u] >> 1) ? true : left0;  // a head after lane 0 precedes lane 31
                 } else {
                     cy.d = NONE;
                 }
-                const bool tail = (((heads[u] >> 1) | 0x80000000u) >> lane) & 1u;
-                const bool left = (heads[u] & le & ~1u) ? true : left0;
-                const bool right = !(lane == 31 && last_tile && dright == d[u]);
-                const bool app = tail && valid[u] && !(carry && lane == 31);
-                apply_dense<T>(app, d[u], agg[u], pd[u], left && right, INF, inc, nxt, obits, o.ovf);
+                const bool tail = (((k.heads[u] >> 1) | 0x80000000u) >> lane) & 1u;
+                const bool left = (k.heads[u] & le & ~1u) ? true : left0;
+                const bool right = !(lane == 31 && last_tile && dright == k.d[u]);
+                const bool app = tail && k.valid[u] && !(carry && lane == 31);
+                apply_dense<T>(app, k.d[u], agg[u], k.pd[u], left && right, INF, inc, nxt, obits, o.ovf);
             }
+        };
+        DenseChunk<T, W, WEIGHT, CH> ka, kb;
+        load(0, ka);
+        for (uint32_t ch = 0; ch < nchunks; ch += 2) {
+            if (ch + 1 < nchunks) load(ch + 1, kb);
+            reduce(ch, ka);
+            if (ch + 1 >= nchunks) break;
+            if (ch + 2 < nchunks) load(ch + 2, ka);
+            reduce(ch + 1, kb);
         }
     }
     end_of_pull<T>(o, out);
