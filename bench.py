@@ -186,11 +186,13 @@ def run_b200(args, wl):
     dinit = dv.encode_values(init, _lib.WG_VAL_U32)
     words = dv.all_words(n) if app == "cc" else dv.initial_words(n, np.array([root]))
     max_it = n + 16  # cli.py:162
+    # BFS is level-synchronous: first-hit early exit in the filtered pulls
+    fh = dv.first_hit_ok(kern, init, None if app == "cc" else np.array([root]))
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     stream = torch.cuda.current_stream()
 
     def step(timer=None):
-        p = loop.seed(dinit, words, kern, thr)
+        p = loop.seed(dinit, words, kern, thr, first_hit=fh)
         if timer is not None:
             p.timer = timer.handle
         return loop.drive(p, max_it)
@@ -259,7 +261,7 @@ def run_b200(args, wl):
     clocks = clk.summary()
     out["clocks"] = clocks
     if rank == 0 and not args.no_e2e:
-        out["e2e"] = e2e_b200(args, wl, g, loop, dinit, words, kern, thr, max_it)
+        out["e2e"] = e2e_b200(args, wl, g, loop, dinit, words, kern, thr, max_it, fh)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(wl, g, prog, thr, max_it, sample_runs=1)
     if rank == 0:
@@ -386,7 +388,7 @@ def roofline(rows, recs, n, E, weighted, filt, wl):
         t = by_it.get(r.iteration, {})
         pull_ms = t.get(2, 0.0)
         prep_ms = t.get(1, 0.0)
-        fin_ms = t.get(3, 0.0)
+        fin_ms = t.get(3, 0.0) + t.get(4, 0.0)  # end of iteration (+ list build after a dense pull)
         step_t += pull_ms + prep_ms + fin_ms
         U = r.frontier_out_size
         if r.mode == "FullScan":
@@ -406,7 +408,8 @@ def roofline(rows, recs, n, E, weighted, filt, wl):
         prev_out = U
     if dense_t > 0:
         ach = dense_b / (dense_t * 1e-3) / 1e9
-        kernel = "pull_kernel<u32,W4> dense (K6)"
+        kernel = (f"pull_dense_tma_kernel<u32,W{wl.get('W', 4)}> (K6, dense pull)" if not filt else
+                  f"pull_kernel<u32,W{wl.get('W', 4)},filter> (K6, dense filtered pull)")
         traffic = dense_b / max(1, sum(1 for r in recs if r.mode == "FullScan"))
     else:
         ach = wedge_b / (wedge_t * 1e-3) / 1e9 if wedge_t else 0.0
@@ -416,7 +419,8 @@ def roofline(rows, recs, n, E, weighted, filt, wl):
     measured_traffic = None
     if prof.exists():
         try:
-            measured_traffic = json.loads(prof.read_text()).get(wl["desc"])
+            ent = json.loads(prof.read_text()).get(wl["desc"])
+            measured_traffic = ent.get("dram_bytes_per_launch") if isinstance(ent, dict) else ent
         except Exception:
             pass
     return {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
@@ -429,7 +433,7 @@ def roofline(rows, recs, n, E, weighted, filt, wl):
             "iterations_timed": len(per_iter)}
 
 
-def e2e_b200(args, wl, g, loop, dinit, words, kern, thr, max_it):
+def e2e_b200(args, wl, g, loop, dinit, words, kern, thr, max_it, first_hit=False):
     """Same metric through the C ABI with the layout in pinned HOST memory:
     per step H2D of the layout, the device loop, D2H of the result."""
     import torch
@@ -453,7 +457,7 @@ def e2e_b200(args, wl, g, loop, dinit, words, kern, thr, max_it):
     def one():
         for k, v in host.items():
             dev[k].copy_(v, non_blocking=True)
-        p = loop2.seed(dinit, words, kern, thr)
+        p = loop2.seed(dinit, words, kern, thr, first_hit=first_hit)
         recs, conv, last = loop2.drive(p, max_it)
         out_host.copy_(loop2.values_after(last), non_blocking=True)
         return last

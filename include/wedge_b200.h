@@ -161,7 +161,17 @@ typedef struct wg_run_params {
     wg_minplus kern;
     uint64_t wedge_limit;   /* wedge iff E>0 and edge_sum < wedge_limit (= ceil(num*E/den)) */
     void *timer;            /* optional wg_timer*: CUDA events around each launch group */
+    int32_t flags;          /* WG_RUN_* */
 } wg_run_params;
+
+/* The caller asserts level-synchronous values (a filtered, unweighted kernel
+ * whose initially finite values are all equal and all in the initial
+ * frontier, e.g. bfs_program): then every finite in-neighbour of an
+ * unvisited destination carries the same level, so the first one found is
+ * the minimum and the filtered pulls skip the rest of that destination's
+ * vectors (bottom-up early exit).  Results and counters
+ * are unchanged. */
+#define WG_RUN_FIRST_HIT 1
 
 /* Element counts: [0] fbits words, [1] groups, [2] gbits words, [3] bcount
  * entries, [4] tstart entries (the caller multiplies by element sizes). */

@@ -47,7 +47,10 @@ class WgRunBufs(ctypes.Structure):
 
 class WgRunParams(ctypes.Structure):
     _fields_ = [("val_type", c_i32), ("shift", c_i32), ("kern", WgMinPlus), ("wedge_limit", c_u64),
-                ("timer", c_vp)]
+                ("timer", c_vp), ("flags", c_i32)]
+
+
+WG_RUN_FIRST_HIT = 1
 
 
 EXPORTS = [

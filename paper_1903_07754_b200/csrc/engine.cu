@@ -292,8 +292,11 @@ int launch_pull_sparse(const LoopCtx &c, const wg_graph *g, const PullBufs &pb, 
 
 // only: 0 = everything the gate may need (non-graph path); MODE_FULL / MODE_WEDGE
 // = just that mode's kernels (conditional graph bodies).
+// timer/slot (optional): the caller's open timer slot around the pull; the
+// frontier compaction after a dense pull is timed in its own slot (kind 4).
 int launch_pull(const LoopCtx &c, const wg_graph *g, const PullBufs &pb, int val_type, int shift,
-                const wg_minplus *k, uint64_t max_items, cudaStream_t s, int only = 0) {
+                const wg_minplus *k, uint64_t max_items, cudaStream_t s, int only = 0,
+                void *timer = nullptr, int *slot = nullptr) {
     const bool weight = k->use_weight != 0, filter = k->filter_unvisited != 0;
     WG_REQUIRE(!weight || g->vw, "weighted kernel on an unweighted layout");
     PullFn fn = pick_pull(val_type, (int)g->width, weight, filter);
@@ -308,6 +311,10 @@ int launch_pull(const LoopCtx &c, const wg_graph *g, const PullBufs &pb, int val
         dn<<<grid, PULL_THREADS, smem, s>>>(c, *g, pb, shift, k->apply_increment, k->sentinel);
         ::wg::count_launch();
         WG_CHECK_LAUNCH("pull (dense, TMA)");
+        if (slot) {
+            timer_end(timer, *slot, s);
+            *slot = timer_begin(timer, 4, (int64_t)c.it_arg, s);
+        }
         // the dense pull only sets bits: build the produced frontier from the bitmap
         FrontierBufs fb;
         for (int i = 0; i < 2; ++i) {
@@ -542,7 +549,7 @@ static LoopCtx loop_ctx(const wg_graph *g, const wg_run_bufs *b, const wg_run_pa
     return c;
 }
 
-static PullBufs pull_bufs(const wg_graph *g, const wg_run_bufs *b) {
+static PullBufs pull_bufs(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p) {
     PullBufs pb{};
     for (int i = 0; i < 2; ++i) {
         pb.vals[i] = b->vals[i];
@@ -554,6 +561,7 @@ static PullBufs pull_bufs(const wg_graph *g, const wg_run_bufs *b) {
     pb.glist = b->glist;
     pb.bcount = b->bcount;
     pb.n = g->n;
+    pb.first_hit = (p->flags & WG_RUN_FIRST_HIT) && p->kern.filter_unvisited && !p->kern.use_weight ? 1u : 0u;
     return pb;
 }
 
@@ -609,10 +617,11 @@ static int enqueue_one(const wg_graph *g, const wg_run_bufs *b, const wg_run_par
             return rc;
     }
     timer_end(p->timer, slot, s);
-    PullBufs pb = pull_bufs(g, b);
+    PullBufs pb = pull_bufs(g, b, p);
     slot = timer_begin(p->timer, 2, (int64_t)c.it_arg, s);
     if (g->nvec) {
-        if ((rc = launch_pull(c, g, pb, p->val_type, p->shift, &p->kern, g->nvec, s))) return rc;
+        if ((rc = launch_pull(c, g, pb, p->val_type, p->shift, &p->kern, g->nvec, s, 0, p->timer, &slot)))
+            return rc;
     }
     timer_end(p->timer, slot, s);
     unsigned grid = (unsigned)sm_count() * 2;
@@ -781,7 +790,7 @@ void *wg_run_loop_graph_create(const wg_graph *g, const wg_run_bufs *b, const wg
     uint32_t *fv[2] = {b->fvert[0], b->fvert[1]};
     uint32_t *fp[2] = {b->fpref[0], b->fpref[1]};
     uint32_t *ts[2] = {b->tstart[0], b->tstart[1]};
-    PullBufs pb = pull_bufs(g, b);
+    PullBufs pb = pull_bufs(g, b, &q);
     int rc = WG_OK;
     // 0. as many consecutive sparse Wedge iterations as possible, persistently
     if (g_sparse_loop && g->entries && g->nvec)
@@ -856,7 +865,7 @@ int wg_run_persistent(const wg_graph *g, const wg_run_bufs *b, const wg_run_para
     set_limit_kernel<<<1, 1, 0, s>>>(b->ctrl, max_iteration);
     ::wg::count_launch();
     LoopCtx c = loop_ctx(g, b, p, b->ctrl, 1);
-    PullBufs pb = pull_bufs(g, b);
+    PullBufs pb = pull_bufs(g, b, p);
     if (!g->entries || !g->nvec) return WG_OK;
     return launch_sparse_loop(c, g, pb, p->val_type, p->shift, &p->kern, b->gbits, groups_of(g, p->shift), s);
 }

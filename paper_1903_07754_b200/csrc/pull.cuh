@@ -55,6 +55,7 @@ struct PullBufs {
     uint64_t *bcount;  // compaction scratch (dense-pull frontier build)
     const uint32_t *glist;
     uint32_t n;
+    uint32_t first_hit;  // WG_RUN_FIRST_HIT (filtered pulls only)
 };
 
 constexpr int PULL_THREADS = 256;
@@ -419,6 +420,9 @@ __global__ void __launch_bounds__(PULL_THREADS) pull_kernel(LoopCtx c, wg_graph 
             uint32_t d[U];
             T pd[U], agg[U];
             bool act[U];
+            // first-hit programs: the destination carried into this step
+            // already has its (only possible) minimum; skip its gathers
+            const uint32_t hit_d = (FILTER && b.first_hit && cy.d != NONE && cy.act && cy.agg != INF) ? cy.d : NONE;
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const uint64_t p = (tile + u < t1)
@@ -429,7 +433,7 @@ __global__ void __launch_bounds__(PULL_THREADS) pull_kernel(LoopCtx c, wg_graph 
                 agg[u] = INF;
                 if (FILTER && d[u] != NONE) pd[u] = prev[d[u]];
                 act[u] = d[u] != NONE && !(FILTER && pd[u] != INF);
-                if (act[u]) {
+                if (act[u] && d[u] != hit_d) {
                     uint32_t src[W], wt[W];
                     load_lanes<W>(g.vsrc, p, src);
                     if (WEIGHT) load_lanes<W>(g.vw, p, wt);

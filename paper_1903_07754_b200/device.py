@@ -361,19 +361,21 @@ class DeviceLoop:
         self.bufs = b
         self.graph_cache = {}
 
-    def params(self, kern, threshold: Fraction) -> WgRunParams:
+    def params(self, kern, threshold: Fraction, first_hit: bool = False) -> WgRunParams:
         p = WgRunParams()
         p.val_type = self.val_type
         p.shift = self.shift
         p.kern = _minplus(kern, UNREACHED)
         p.wedge_limit = wedge_limit(threshold, self.g.edges) if self.g.edges > 0 else 0
+        p.flags = _lib.WG_RUN_FIRST_HIT if first_hit else 0
         return p
 
-    def seed(self, init_values, init_words, kern, threshold, stream=None) -> WgRunParams:
-        """Write both value buffers and build iteration 0 from the frontier bitmap."""
+    def seed(self, init_values, init_words, kern, threshold, stream=None, first_hit: bool = False) -> WgRunParams:
+        """Write both value buffers and build iteration 0 from the frontier bitmap.
+        first_hit: the caller checked first_hit_ok (level-synchronous values)."""
         for v in self.vals:
             v.copy_(init_values)
-        p = self.params(kern, threshold)
+        p = self.params(kern, threshold, first_hit)
         check(_lib.load().wg_run_init(ctypes.byref(self.g.struct()), ctypes.byref(self.bufs),
                                       ctypes.byref(p), _ptr(init_words), _lib.stream_ptr(stream)))
         return p
@@ -398,7 +400,7 @@ class DeviceLoop:
 
     def _graph_for(self, p: WgRunParams, stream=None):
         key = (p.val_type, p.shift, p.kern.filter_unvisited, p.kern.use_weight, p.kern.apply_increment,
-               p.kern.sentinel, p.wedge_limit)
+               p.kern.sentinel, p.wedge_limit, p.flags)
         exe = self.graph_cache.get(key)
         if exe is None:
             q = WgRunParams()
@@ -511,6 +513,29 @@ class DeviceLoop:
 
     def values_after(self, it: int):
         return self.vals[it & 1]
+
+
+def first_hit_ok(kern, init_values: np.ndarray, members: Optional[np.ndarray]) -> bool:
+    """True when the run is level-synchronous (WG_RUN_FIRST_HIT): a filtered,
+    unweighted kernel whose initially finite values are all equal and all in
+    the initial frontier (members None = every vertex).  By induction every
+    finite in-neighbour of a destination still unvisited at iteration k then
+    holds the same value, so any one of them gives the minimum."""
+    if not kern.filter_unvisited or kern.use_weight:
+        return False
+    v = np.asarray(init_values, dtype=np.int64)
+    fin = v != UNREACHED
+    if not fin.any():
+        return True
+    vals = v[fin]
+    if np.any(vals != vals[0]):
+        return False
+    if members is None:
+        return True
+    mem = np.zeros(v.shape[0], dtype=bool)
+    m = np.asarray(members, dtype=np.int64)
+    mem[m[(m >= 0) & (m < v.shape[0])]] = True
+    return bool(mem[fin].all())
 
 
 def initial_words(n: int, members: np.ndarray):

@@ -311,7 +311,8 @@ def device_run(be, topology, index, program: ApplicationProgram, degrees, config
         dinit = dv.encode_values(init, val_type)
         start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         start.record()
-        p = loop.seed(dinit, words, kern, config.threshold.fraction)
+        p = loop.seed(dinit, words, kern, config.threshold.fraction,
+                      first_hit=dv.first_hit_ok(kern, init, members))
         try:
             recs, converged, last = loop.drive(p, config.max_iterations, trace)
         except OverflowError32:

@@ -200,3 +200,20 @@ def test_genspec_parsing():
         wg.GenSpec.parse("rmat:14")
     with pytest.raises(ValueError):
         wg.GenSpec("rmat", scale=4, edge_factor=2, probs=(0.5, 0.5, 0.5, 0.5))
+
+
+def test_first_hit_condition():
+    """WG_RUN_FIRST_HIT only for level-synchronous runs (filtered, unweighted,
+    equal finite initial values that are all frontier members)."""
+    import paper_1903_07754_b200 as wg
+    from paper_1903_07754_b200.device import first_hit_ok
+    U = wg.UNREACHED
+    bfs = wg.bfs_program(0)
+    assert first_hit_ok(bfs.kernel, bfs.initial_values(5), np.array([0]))
+    assert not first_hit_ok(wg.cc_program().kernel, np.arange(5), None)
+    assert not first_hit_ok(wg.make_program("sssp", 0).kernel, bfs.initial_values(5), np.array([0]))
+    k = bfs.kernel
+    assert first_hit_ok(k, np.array([3, 3, U, U]), np.array([0, 1]))
+    assert not first_hit_ok(k, np.array([0, 5, U, U]), np.array([0, 1]))   # two levels
+    assert not first_hit_ok(k, np.array([0, 0, U, U]), np.array([0]))      # finite non-member
+    assert first_hit_ok(k, np.array([U, U]), np.array([0]))

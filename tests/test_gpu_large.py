@@ -1,6 +1,7 @@
 """GPU: larger graphs where warps split hub destinations and the TMA-fed
 dense pull runs many stages.  The conditional-graph + persistent path and
-the per-iteration path must agree bit-for-bit (values and traces), and the
+the per-iteration path must agree bit-for-bit (values and traces), with and
+without the BFS first-hit early exit, and the
 result must satisfy the shortest-path / BFS certificate on every edge:
 d[v] <= d[u] + w(u,v), and every reached vertex other than the root has a
 tight in-edge.  (This is the check that caught a TMA stage-reuse race.)"""
@@ -46,10 +47,12 @@ def test_paths_agree_and_certify(app, scale, sym):
     vpg, thr = (8, Fraction(1, 100)) if app == "bfs" else (4, Fraction(1, 5))
     init = dv.encode_values(prog.initial_values(g.n), _lib.WG_VAL_U32)
     words = dv.initial_words(g.n, np.array([0]))
+    fh = dv.first_hit_ok(prog.kernel, prog.initial_values(g.n), np.array([0]))
+    assert fh == (app == "bfs")
     outs = []
-    for graph in (True, False, True):
+    for graph, first_hit in ((True, False), (False, False), (True, False), (True, fh), (False, fh)):
         loop = dv.DeviceLoop(g, vpg.bit_length() - 1, _lib.WG_VAL_U32)
-        p = loop.seed(init, words, prog.kernel, thr)
+        p = loop.seed(init, words, prog.kernel, thr, first_hit=first_hit)
         recs, conv, last = loop.drive(p, g.n + 16, graph=graph)
         vals = dv.values_to_int64(loop.values_after(last), _lib.WG_VAL_U32)
         outs.append((vals, [(r.mode, r.active_edges, r.frontier_out_size, r.vectors_touched) for r in recs]))
