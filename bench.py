@@ -377,7 +377,8 @@ def roofline(rows, recs, n, E, weighted, filt, wl):
     peak, peak_src = peaks()
     by_it = {}
     for kind, it, ms in rows:
-        by_it.setdefault(it, {})[kind] = ms
+        d = by_it.setdefault(it, {})
+        d[kind] = d.get(kind, 0.0) + ms
     w = 1 if weighted else 0
     dense_b = dense_t = 0.0
     wedge_b = wedge_t = 0.0

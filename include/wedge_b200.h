@@ -172,6 +172,10 @@ typedef struct wg_run_params {
  * vectors (bottom-up early exit).  Results and counters
  * are unchanged. */
 #define WG_RUN_FIRST_HIT 1
+/* Build every produced frontier's member list (traces, exchange).  Without
+ * it a dense pull whose frontier gates the next iteration to FullScan skips
+ * the list (nothing consumes it; its record has reserved[2] = 1). */
+#define WG_RUN_KEEP_LISTS 2
 
 /* Element counts: [0] fbits words, [1] groups, [2] gbits words, [3] bcount
  * entries, [4] tstart entries (the caller multiplies by element sizes). */

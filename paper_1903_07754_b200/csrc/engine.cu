@@ -13,11 +13,7 @@ using namespace wg;
 
 namespace {
 
-// TMA-fed dense pull on/off (WG_DENSE_TMA=0 selects the direct-load kernel).
-bool g_dense_tma = [] {
-    const char *e = getenv("WG_DENSE_TMA");
-    return !(e && e[0] == '0');
-}();
+
 
 struct Occ {
     std::mutex mu;
@@ -77,50 +73,33 @@ PullFn pick_pull(int val_type, int width, bool weight, bool filter) {
                                   : pick_pull_t<int64_t>(width, weight, filter);
 }
 
-// TMA dense-pull configuration (tiles per stage, stages, min blocks/SM);
-// WG_TMA_CFG=0|1|2 selects among the compiled variants for experiments.
 // Persistent sparse loop on/off (WG_SPARSE_LOOP=0 disables it).
 bool g_sparse_loop = [] {
     const char *e = getenv("WG_SPARSE_LOOP");
     return !(e && e[0] == '0');
 }();
 
-int g_tma_cfg = [] {
-    const char *e = getenv("WG_TMA_CFG");
-    return e ? atoi(e) : 0;
-}();
-
-template <typename T, int W, bool WEIGHT>
-DenseFn pick_dense_wt(size_t *smem) {
-    switch (g_tma_cfg) {
-        case 1:
-            *smem = TmaSmem<W, WEIGHT, 4, 2>::BLOCK_BYTES;
-            return pull_dense_tma_kernel<T, W, WEIGHT, 4, 2, 1>;
-        case 2:
-            *smem = TmaSmem<W, WEIGHT, 4, 2>::BLOCK_BYTES;
-            return pull_dense_tma_kernel<T, W, WEIGHT, 4, 2, 2>;
-        case 3:
-            *smem = TmaSmem<W, WEIGHT, 2, 3>::BLOCK_BYTES;
-            return pull_dense_tma_kernel<T, W, WEIGHT, 2, 3, 3>;
-        default:  // 2 tiles x 4 stages
-            *smem = TmaSmem<W, WEIGHT, 2, 4>::BLOCK_BYTES;
-            return pull_dense_tma_kernel<T, W, WEIGHT, 2, 4, 1>;
-    }
+// TMA-streamed dense pull: 2 tiles per stage, 4 stages (measured best of the
+// (tiles, stages, blocks/SM) grid on CC s22 / SSSP s26).
+template <typename T, int W, bool WEIGHT, bool FILTER>
+DenseFn dense_fn(size_t *smem) {
+    *smem = TmaSmem<W, WEIGHT, 2, 4>::BLOCK_BYTES;
+    return pull_dense_tma_kernel<T, W, WEIGHT, FILTER, 2, 4, 1>;
 }
 
 template <typename T, int W>
-DenseFn pick_dense_w(bool weight, size_t *smem) {
-    return weight ? pick_dense_wt<T, W, true>(smem) : pick_dense_wt<T, W, false>(smem);
+DenseFn pick_dense_w(bool weight, bool filter, size_t *smem) {
+    if (weight) return filter ? dense_fn<T, W, true, true>(smem) : dense_fn<T, W, true, false>(smem);
+    return filter ? dense_fn<T, W, false, true>(smem) : dense_fn<T, W, false, false>(smem);
 }
 
-// TMA-streamed dense pull (unfiltered programs only).
-DenseFn pick_dense(int val_type, int width, bool weight, size_t *smem) {
+DenseFn pick_dense(int val_type, int width, bool weight, bool filter, size_t *smem) {
     bool u32 = val_type == WG_VAL_U32;
     switch (width) {
-        case 1: return u32 ? pick_dense_w<uint32_t, 1>(weight, smem) : pick_dense_w<int64_t, 1>(weight, smem);
-        case 2: return u32 ? pick_dense_w<uint32_t, 2>(weight, smem) : pick_dense_w<int64_t, 2>(weight, smem);
-        case 4: return u32 ? pick_dense_w<uint32_t, 4>(weight, smem) : pick_dense_w<int64_t, 4>(weight, smem);
-        case 8: return u32 ? pick_dense_w<uint32_t, 8>(weight, smem) : pick_dense_w<int64_t, 8>(weight, smem);
+        case 1: return u32 ? pick_dense_w<uint32_t, 1>(weight, filter, smem) : pick_dense_w<int64_t, 1>(weight, filter, smem);
+        case 2: return u32 ? pick_dense_w<uint32_t, 2>(weight, filter, smem) : pick_dense_w<int64_t, 2>(weight, filter, smem);
+        case 4: return u32 ? pick_dense_w<uint32_t, 4>(weight, filter, smem) : pick_dense_w<int64_t, 4>(weight, filter, smem);
+        case 8: return u32 ? pick_dense_w<uint32_t, 8>(weight, filter, smem) : pick_dense_w<int64_t, 8>(weight, filter, smem);
     }
     return nullptr;
 }
@@ -142,15 +121,26 @@ struct KernelWs {
     wg_iter_rec *recs;
     uint32_t *fvert[2], *fpref[2], *tstart[2], *glist;
     uint64_t *bcount;
+    unsigned *ticket;
 };
 
 uint64_t tstart_entries(const wg_graph *g) { return g->entries / TR_TILE + 2; }
 
+// Compaction scratch: per-block totals of the frontier (4 per block) or
+// group (1 per block) compactions, then one slot holding the frontier
+// compaction's completion ticket (zero between launches).
+uint64_t bcount_entries(const wg_graph *g, int shift) {
+    uint64_t n = g->n ? g->n : 1, groups = groups_of(g, shift);
+    uint64_t nb = fb_blocks(n) * 4, gb = cb_blocks(groups ? groups : 1);
+    return (nb > gb ? nb : gb) + 1;
+}
+unsigned *bcount_ticket(const wg_graph *g, int shift, uint64_t *bcount) {
+    return reinterpret_cast<unsigned *>(bcount + bcount_entries(g, shift) - 1);
+}
+
 int carve_kernel_ws(const wg_graph *g, int shift, void *ws, size_t bytes, KernelWs *k) {
     Carve cv{(char *)ws, 0, bytes};
     uint64_t n = g->n ? g->n : 1, groups = groups_of(g, shift);
-    uint64_t nb = cb_blocks(n) * 4;
-    uint64_t gb = cb_blocks(groups ? groups : 1);
     k->recs = cv.take<wg_iter_rec>(2);
     for (int i = 0; i < 2; ++i) {
         k->fvert[i] = cv.take<uint32_t>(n);
@@ -158,7 +148,8 @@ int carve_kernel_ws(const wg_graph *g, int shift, void *ws, size_t bytes, Kernel
         k->tstart[i] = cv.take<uint32_t>(tstart_entries(g));
     }
     k->glist = cv.take<uint32_t>(groups ? groups : 1);
-    k->bcount = cv.take<uint64_t>(nb > gb ? nb : gb);
+    k->bcount = cv.take<uint64_t>(bcount_entries(g, shift));
+    k->ticket = k->bcount ? bcount_ticket(g, shift, k->bcount) : nullptr;
     if (!k->recs || !k->fvert[1] || !k->fpref[1] || !k->tstart[1] || !k->glist || !k->bcount) {
         set_error("kernel workspace too small (%zu bytes)", bytes);
         return WG_ENOSPACE;
@@ -175,6 +166,7 @@ LoopCtx forced_ctx(wg_iter_rec *recs, int mode, uint64_t edges) {
     c.it_arg = 1;
     c.wedge_limit = 0;
     c.edges = edges;
+    c.keep_lists = 1;
     return c;
 }
 
@@ -189,11 +181,12 @@ int launch_group_compaction(const LoopCtx &c, uint32_t *words, uint64_t ngroups,
 }
 
 int launch_frontier_compaction(const wg_graph *g, const uint32_t *words, uint64_t *bcount,
-                               uint32_t *fvert, uint32_t *fpref, uint32_t *tstart, wg_iter_rec *rec,
-                               cudaStream_t s) {
-    uint64_t nb = cb_blocks(g->n ? g->n : 1);
+                               unsigned *ticket, uint32_t *fvert, uint32_t *fpref, uint32_t *tstart,
+                               wg_iter_rec *rec, cudaStream_t s) {
+    uint64_t nb = fb_blocks(g->n ? g->n : 1);
+    WG_CUDA(cudaMemsetAsync(ticket, 0, sizeof(unsigned), s));
     frontier_count_kernel<<<(unsigned)nb, CB_THREADS, 0, s>>>(words, g->n, g->idx_off, g->outdeg,
-                                                              bcount); ::wg::count_launch();
+                                                              bcount, ticket, rec); ::wg::count_launch();
     frontier_list_kernel<<<(unsigned)nb, CB_THREADS, 0, s>>>(words, g->n, g->idx_off, bcount, fvert,
                                                              fpref, tstart, rec); ::wg::count_launch();
     WG_CHECK_LAUNCH("frontier compaction");
@@ -304,9 +297,9 @@ int launch_pull(const LoopCtx &c, const wg_graph *g, const PullBufs &pb, int val
     int handles = (1 << MODE_FULL) | (1 << MODE_WEDGE);
     if (only) handles = 1 << only;
     const bool want_full = only == 0 || only == MODE_FULL;
-    if (!filter && g_dense_tma && want_full && (c.forced_mode == 0 || c.forced_mode == MODE_FULL)) {
+    if (want_full && (c.forced_mode == 0 || c.forced_mode == MODE_FULL)) {
         size_t smem = 0;
-        DenseFn dn = pick_dense(val_type, (int)g->width, weight, &smem);
+        DenseFn dn = pick_dense(val_type, (int)g->width, weight, filter, &smem);
         unsigned grid = persistent_grid(dn, PULL_THREADS, (g->nvec + 255) / 256, smem);
         dn<<<grid, PULL_THREADS, smem, s>>>(c, *g, pb, shift, k->apply_increment, k->sentinel);
         ::wg::count_launch();
@@ -323,12 +316,16 @@ int launch_pull(const LoopCtx &c, const wg_graph *g, const PullBufs &pb, int val
             fb.fpref[i] = pb.fpref[i];
             fb.tstart[i] = pb.tstart[i];
         }
-        const uint64_t nb = cb_blocks(g->n ? g->n : 1);
+        const uint64_t nb = fb_blocks(g->n ? g->n : 1);
         loop_frontier_count_kernel<<<(unsigned)nb, CB_THREADS, 0, s>>>(c, fb, g->n, g->idx_off, g->outdeg,
-                                                                      pb.bcount);
+                                                                      pb.bcount, pb.ticket);
         loop_frontier_list_kernel<<<(unsigned)nb, CB_THREADS, 0, s>>>(c, fb, g->n, g->idx_off, pb.bcount);
         ::wg::count_launch(2);
         WG_CHECK_LAUNCH("dense frontier compaction");
+        if (slot) {  // a Wedge iteration's pull (below) is timed as a pull again
+            timer_end(timer, *slot, s);
+            *slot = timer_begin(timer, 2, (int64_t)c.it_arg, s);
+        }
         handles &= ~(1 << MODE_FULL);
         if (c.forced_mode == MODE_FULL || handles == 0) return WG_OK;
     }
@@ -352,9 +349,8 @@ extern "C" {
 size_t wg_kernel_workspace_bytes(const wg_graph *g, int shift) {
     if (!g || shift < 0 || shift > 4) return 0;
     uint64_t n = g->n ? g->n : 1, groups = groups_of(g, shift);
-    uint64_t nb = cb_blocks(n) * 4, gb = cb_blocks(groups ? groups : 1);
     return carve_size(2 * sizeof(wg_iter_rec)) + 4 * carve_size(n * 4) + 2 * carve_size(tstart_entries(g) * 4) +
-           carve_size((groups ? groups : 1) * 4) + carve_size((nb > gb ? nb : gb) * 8) + 256;
+           carve_size((groups ? groups : 1) * 4) + carve_size(bcount_entries(g, shift) * 8) + 256;
 }
 
 int wg_transform(const wg_graph *g, const uint32_t *d_frontier_words, int shift,
@@ -370,7 +366,7 @@ int wg_transform(const wg_graph *g, const uint32_t *d_frontier_words, int shift,
     WG_CUDA(cudaMemsetAsync(k.recs, 0, 2 * sizeof(wg_iter_rec), s));
     *h_visited = 0;
     if (g->n == 0) return WG_OK;
-    if ((rc = launch_frontier_compaction(g, d_frontier_words, k.bcount, k.fvert[0], k.fpref[0],
+    if ((rc = launch_frontier_compaction(g, d_frontier_words, k.bcount, k.ticket, k.fvert[0], k.fpref[0],
                                          k.tstart[0], &k.recs[0], s)))
         return rc;
     if (g->entries) {
@@ -421,7 +417,9 @@ static int pull_common(const wg_graph *g, const uint32_t *d_wedge_words, int shi
     pb.tstart[1] = ws.tstart[1];
     pb.glist = ws.glist;
     pb.bcount = ws.bcount;
+    pb.ticket = ws.ticket;
     pb.n = g->n;
+    WG_CUDA(cudaMemsetAsync(ws.ticket, 0, sizeof(unsigned), s));
     if ((rc = launch_pull(c, g, pb, val_type, shift, k, items, s))) return rc;
     wg_iter_rec h[2];
     WG_CUDA(cudaMemcpyAsync(h, ws.recs, sizeof(h), cudaMemcpyDeviceToHost, s));
@@ -484,11 +482,10 @@ int wg_run_buffer_sizes(const wg_graph *g, int shift, uint64_t *h_sizes4) {  /* 
     if (rc) return rc;
     WG_REQUIRE(h_sizes4, "null argument");
     uint64_t groups = groups_of(g, shift);
-    uint64_t nb = cb_blocks(g->n ? g->n : 1) * 4, gb = cb_blocks(groups ? groups : 1);
     h_sizes4[0] = ((uint64_t)g->n + 31) >> 5;
     h_sizes4[1] = groups;
     h_sizes4[2] = (groups + 31) >> 5;
-    h_sizes4[3] = nb > gb ? nb : gb;
+    h_sizes4[3] = bcount_entries(g, shift);
     h_sizes4[4] = tstart_entries(g);
     return WG_OK;
 }
@@ -546,6 +543,7 @@ static LoopCtx loop_ctx(const wg_graph *g, const wg_run_bufs *b, const wg_run_pa
     c.it_arg = it;
     c.wedge_limit = p->wedge_limit;
     c.edges = g->edges;
+    c.keep_lists = (p->flags & WG_RUN_KEEP_LISTS) ? 1 : 0;
     return c;
 }
 
@@ -560,6 +558,7 @@ static PullBufs pull_bufs(const wg_graph *g, const wg_run_bufs *b, const wg_run_
     }
     pb.glist = b->glist;
     pb.bcount = b->bcount;
+    pb.ticket = bcount_ticket(g, p->shift, b->bcount);
     pb.n = g->n;
     pb.first_hit = (p->flags & WG_RUN_FIRST_HIT) && p->kern.filter_unvisited && !p->kern.use_weight ? 1u : 0u;
     return pb;
@@ -596,7 +595,9 @@ int wg_run_init(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p,
     WG_CUDA(cudaMemsetAsync(b->fbits[1], 0, words * 4, s));
     WG_CUDA(cudaMemsetAsync(b->gbits, 0, ((groups + 31) >> 5) * 4, s));
     if (g->n == 0) return WG_OK;
-    return launch_frontier_compaction(g, d_init_words, b->bcount, b->fvert[0], b->fpref[0], b->tstart[0],
+    WG_CUDA(cudaMemsetAsync(bcount_ticket(g, p->shift, b->bcount), 0, sizeof(unsigned), s));
+    return launch_frontier_compaction(g, d_init_words, b->bcount, bcount_ticket(g, p->shift, b->bcount),
+                                      b->fvert[0], b->fpref[0], b->tstart[0],
                                       &b->recs[0], s);
 }
 
@@ -966,7 +967,8 @@ int wg_exchange_apply(const wg_graph *g, const wg_run_bufs *b, const wg_run_para
     }
     // the global frontier of `it`: ordered list, index prefixes, counts and
     // the global out-degree sum (the next gate's input) from the bitmap
-    return launch_frontier_compaction(g, bits, b->bcount, b->fvert[it & 1], b->fpref[it & 1],
+    return launch_frontier_compaction(g, bits, b->bcount, bcount_ticket(g, p->shift, b->bcount),
+                                      b->fvert[it & 1], b->fpref[it & 1],
                                       b->tstart[it & 1], &b->recs[it % b->ring], s);
 }
 

@@ -122,108 +122,192 @@ __global__ void __launch_bounds__(CB_THREADS) group_list_kernel(LoopCtx c, uint3
 // transform's load-balancing key); members without out-edges go to the back.
 // bcount holds 4 counters per block: nz members, their entries, zero-degree
 // members, out-degree sum.
-__device__ __forceinline__ void frontier_count_body(const uint32_t *words, uint64_t nbits,
-                                                    const uint64_t *idx_off, const uint32_t *outdeg,
-                                                    uint64_t *bcount) {
-    __shared__ uint64_t sm[33];
-    uint64_t w0 = (uint64_t)blockIdx.x * CB_WORDS + threadIdx.x * CB_WPT;
-    uint64_t nz = 0, ent = 0, z = 0, es = 0;
-#pragma unroll
-    for (int i = 0; i < CB_WPT; ++i) {
-        uint32_t v = masked_word(words, w0 + i, nbits);
-        while (v) {
-            int b = __ffs(v) - 1;
-            v &= v - 1;
-            uint64_t u = ((w0 + i) << 5) + b;
-            uint64_t len = idx_off[u + 1] - idx_off[u];
-            if (len) { ++nz; ent += len; } else { ++z; }
-            es += outdeg[u];
+// Lane-per-vertex traversal: each warp owns one 32-word chunk (1024
+// vertices) and for each word the 32 lanes look at its 32 vertices, so the
+// index offsets / out-degrees of set bits are read with coalesced loads
+// whatever the frontier density; empty chunks cost one ballot.  Pass 1
+// writes per-block totals; the LAST block to finish (atomic ticket) turns
+// them into exclusive prefixes, writes the record's counts and decides
+// whether the ordered list is needed at all: after a dense pull whose output
+// frontier gates the next iteration to FullScan again, nothing consumes the
+// list (the next pull is dense, end-of-iteration syncs all values, the
+// bitmap is cleared whole), so pass 2 is skipped (record reserved[2] = 1).
+constexpr int FB_WORDS = CB_THREADS;  // words per block (one chunk per warp)
+
+__host__ __device__ inline uint64_t fb_blocks(uint64_t nbits) {
+    uint64_t words = (nbits + 31) >> 5;
+    return (words + FB_WORDS - 1) / FB_WORDS;
+}
+
+struct VertexInfo {
+    bool set;
+    uint32_t len;    // edge-index entries (0: member without out-edges)
+    uint32_t deg;    // out-degree
+};
+
+__device__ __forceinline__ VertexInfo vertex_info(uint32_t x, uint64_t wi, unsigned lane,
+                                                  const uint64_t *idx_off, const uint32_t *outdeg) {
+    VertexInfo r{((x >> lane) & 1u) != 0, 0u, 0u};
+    if (r.set) {
+        const uint64_t u = (wi << 5) + lane;
+        r.len = (uint32_t)(idx_off[u + 1] - idx_off[u]);
+        if (outdeg) r.deg = outdeg[u];
+    }
+    return r;
+}
+
+// Warp totals of the warp's 32-word chunk starting at word wbase.
+__device__ __forceinline__ void chunk_counts(const uint32_t *words, uint64_t nbits, uint64_t wbase,
+                                            const uint64_t *idx_off, const uint32_t *outdeg, uint64_t &nz,
+                                            uint64_t &ent, uint64_t &z, uint64_t &es) {
+    const unsigned lane = lane_id();
+    nz = ent = z = es = 0;
+    const uint32_t myw = masked_word(words, wbase + lane, nbits);
+    if (__ballot_sync(FULL, myw != 0) == 0) return;
+#pragma unroll 8
+    for (int j = 0; j < 32; ++j) {
+        const uint32_t x = __shfl_sync(FULL, myw, j);
+        const VertexInfo vi = vertex_info(x, wbase + j, lane, idx_off, outdeg);
+        if (vi.set) {
+            if (vi.len) { ++nz; ent += vi.len; } else { ++z; }
+            es += vi.deg;
         }
     }
-    nz = block_sum(nz, sm);
-    ent = block_sum(ent, sm);
-    z = block_sum(z, sm);
-    es = block_sum(es, sm);
+    nz = warp_sum(nz);
+    ent = warp_sum(ent);
+    z = warp_sum(z);
+    es = warp_sum(es);
+}
+
+// keep_list: 1 = always build the list; 0 = decide from the next gate
+// (edges, wedge_limit as in ctx_mode).  counter: zero-initialised ticket,
+// reset by the last block.
+__device__ __forceinline__ void frontier_count_body(const uint32_t *words, uint64_t nbits,
+                                                    const uint64_t *idx_off, const uint32_t *outdeg,
+                                                    uint64_t *bcount, unsigned *counter, wg_iter_rec *rec,
+                                                    int keep_list, uint64_t edges, uint64_t wedge_limit) {
+    __shared__ uint64_t s_w[4][CB_THREADS / 32];
+    __shared__ uint64_t sm[33];
+    __shared__ bool s_last;
+    const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+    uint64_t nz, ent, z, es;
+    chunk_counts(words, nbits, (uint64_t)blockIdx.x * FB_WORDS + (uint64_t)warp * 32, idx_off, outdeg, nz, ent,
+                 z, es);
+    if (lane == 0) {
+        s_w[0][warp] = nz; s_w[1][warp] = ent; s_w[2][warp] = z; s_w[3][warp] = es;
+    }
+    __syncthreads();
+    if (threadIdx.x < 4) {
+        uint64_t t = 0;
+        for (int w = 0; w < CB_THREADS / 32; ++w) t += s_w[threadIdx.x][w];
+        bcount[4ull * blockIdx.x + threadIdx.x] = t;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    // last block: exclusive prefixes of the per-block totals, in place
+    const uint64_t B = gridDim.x;
+    const uint64_t per = (B + blockDim.x - 1) / blockDim.x;
+    const uint64_t b0 = threadIdx.x * per, b1 = b0 + per < B ? b0 + per : B;
+    uint64_t loc[3] = {0, 0, 0}, les = 0;
+    for (uint64_t b = b0; b < b1; ++b) {
+        const volatile uint64_t *q = bcount + 4 * b;
+        loc[0] += q[0]; loc[1] += q[1]; loc[2] += q[2]; les += q[3];
+    }
+    uint64_t base[3], tot[3];
+    for (int f = 0; f < 3; ++f) base[f] = block_exclusive_sum(loc[f], sm, &tot[f]);
+    const uint64_t es_all = block_sum(les, sm);
+    for (uint64_t b = b0; b < b1; ++b) {
+        volatile uint64_t *q = bcount + 4 * b;
+        for (int f = 0; f < 3; ++f) {
+            const uint64_t v = q[f];
+            q[f] = base[f];
+            base[f] += v;
+        }
+    }
     if (threadIdx.x == 0) {
-        uint64_t *o = bcount + 4ull * blockIdx.x;
-        o[0] = nz; o[1] = ent; o[2] = z; o[3] = es;
+        rec->nz_packed = (tot[0] << 32) | tot[1];
+        rec->z_count = tot[2];
+        rec->frontier_out = tot[0] + tot[2];
+        rec->out_edge_sum = es_all;
+        // the list is consumed only by a Wedge iteration (or the caller)
+        const bool wedge_next = es_all > 0 && edges > 0 && es_all < wedge_limit;
+        rec->reserved[2] = (keep_list || wedge_next) ? 0 : 1;
+        *counter = 0;
     }
 }
 
 __device__ __forceinline__ void frontier_list_body(const uint32_t *words, uint64_t nbits,
                                                    const uint64_t *idx_off, const uint64_t *bcount,
                                                    uint32_t *fvert, uint32_t *fpref, uint32_t *tstart,
-                                                   wg_iter_rec *rec) {
-    __shared__ uint64_t sm[33];
-    uint64_t nz_base = prior_blocks_sum(bcount, blockIdx.x, 4, 0, sm);
-    uint64_t ent_base = prior_blocks_sum(bcount, blockIdx.x, 4, 1, sm);
-    uint64_t z_base = prior_blocks_sum(bcount, blockIdx.x, 4, 2, sm);
-    uint64_t w0 = (uint64_t)blockIdx.x * CB_WORDS + threadIdx.x * CB_WPT;
-    uint32_t x[CB_WPT];
-    uint64_t nz = 0, ent = 0, z = 0;
-#pragma unroll
-    for (int i = 0; i < CB_WPT; ++i) {
-        x[i] = masked_word(words, w0 + i, nbits);
-        uint32_t v = x[i];
-        while (v) {
-            int b = __ffs(v) - 1;
-            v &= v - 1;
-            uint64_t u = ((w0 + i) << 5) + b;
-            uint64_t len = idx_off[u + 1] - idx_off[u];
-            if (len) { ++nz; ent += len; } else { ++z; }
-        }
+                                                   const wg_iter_rec *rec) {
+    if (*(volatile const uint64_t *)&rec->reserved[2]) return;  // nobody consumes the list
+    __shared__ uint64_t s_w[3][CB_THREADS / 32];
+    const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    const uint64_t wbase = (uint64_t)blockIdx.x * FB_WORDS + (uint64_t)warp * 32;
+    uint64_t nz, ent, z, es;
+    chunk_counts(words, nbits, wbase, idx_off, nullptr, nz, ent, z, es);
+    if (lane == 0) {
+        s_w[0][warp] = nz; s_w[1][warp] = ent; s_w[2][warp] = z;
     }
-    uint64_t nz_tot, ent_tot, z_tot;
-    uint64_t nzp = nz_base + block_exclusive_sum(nz, sm, &nz_tot);
-    uint64_t entp = ent_base + block_exclusive_sum(ent, sm, &ent_tot);
-    uint64_t zp = z_base + block_exclusive_sum(z, sm, &z_tot);
-#pragma unroll
-    for (int i = 0; i < CB_WPT; ++i) {
-        uint32_t v = x[i];
-        while (v) {
-            int b = __ffs(v) - 1;
-            v &= v - 1;
-            uint64_t u = ((w0 + i) << 5) + b;
-            uint64_t len = idx_off[u + 1] - idx_off[u];
-            if (len) {
-                fvert[nzp] = (uint32_t)u;
-                fpref[nzp] = (uint32_t)entp;
-                if (tstart) mark_tile_starts(tstart, entp, len, (uint32_t)nzp);
-                ++nzp;
-                entp += len;
-            } else {
-                fvert[nbits - 1 - zp] = (uint32_t)u;
-                ++zp;
-            }
-        }
+    __syncthreads();
+    uint64_t nzp = bcount[4ull * blockIdx.x], entp = bcount[4ull * blockIdx.x + 1],
+             zp = bcount[4ull * blockIdx.x + 2];
+    for (unsigned w = 0; w < warp; ++w) {
+        nzp += s_w[0][w];
+        entp += s_w[1][w];
+        zp += s_w[2][w];
     }
-    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
-        uint64_t nz_all = nz_base + nz_tot, ent_all = ent_base + ent_tot, z_all = z_base + z_tot;
-        uint64_t es = 0;
-        for (uint64_t b = 0; b < gridDim.x; ++b) es += bcount[4 * b + 3];
-        rec->nz_packed = (nz_all << 32) | ent_all;
-        rec->z_count = z_all;
-        rec->frontier_out = nz_all + z_all;
-        rec->out_edge_sum = es;
+    const uint32_t myw = masked_word(words, wbase + lane, nbits);
+    if (__ballot_sync(FULL, myw != 0) == 0) return;
+#pragma unroll 4
+    for (int j = 0; j < 32; ++j) {
+        const uint32_t x = __shfl_sync(FULL, myw, j);
+        if (x == 0) continue;  // warp-uniform
+        const uint64_t wi = wbase + j;
+        const VertexInfo vi = vertex_info(x, wi, lane, idx_off, nullptr);
+        const bool hasd = vi.set && vi.len != 0, zero = vi.set && vi.len == 0;
+        const unsigned mnz = __ballot_sync(FULL, hasd), mz = __ballot_sync(FULL, zero);
+        const uint64_t elen = hasd ? vi.len : 0u;
+        const uint64_t incl = warp_inclusive_sum(elen);
+        const uint64_t u = (wi << 5) + lane;
+        if (hasd) {
+            const uint64_t pos = nzp + __popc(mnz & lt);
+            const uint64_t pref = entp + incl - elen;
+            fvert[pos] = (uint32_t)u;
+            fpref[pos] = (uint32_t)pref;
+            if (tstart) mark_tile_starts(tstart, pref, elen, (uint32_t)pos);
+        } else if (zero) {
+            fvert[nbits - 1 - (zp + __popc(mz & lt))] = (uint32_t)u;
+        }
+        nzp += __popc(mnz);
+        entp += __shfl_sync(FULL, incl, 31);
+        zp += __popc(mz);
     }
 }
 
 __global__ void __launch_bounds__(CB_THREADS) frontier_count_kernel(const uint32_t *words, uint64_t nbits,
                                                                     const uint64_t *idx_off,
-                                                                    const uint32_t *outdeg, uint64_t *bcount) {
-    frontier_count_body(words, nbits, idx_off, outdeg, bcount);
+                                                                    const uint32_t *outdeg, uint64_t *bcount,
+                                                                    unsigned *counter, wg_iter_rec *rec) {
+    frontier_count_body(words, nbits, idx_off, outdeg, bcount, counter, rec, 1, 0, 0);
 }
 
 __global__ void __launch_bounds__(CB_THREADS) frontier_list_kernel(const uint32_t *words, uint64_t nbits,
                                                                    const uint64_t *idx_off, const uint64_t *bcount,
                                                                    uint32_t *fvert, uint32_t *fpref,
-                                                                   uint32_t *tstart, wg_iter_rec *rec) {
+                                                                   uint32_t *tstart, const wg_iter_rec *rec) {
     frontier_list_body(words, nbits, idx_off, bcount, fvert, fpref, tstart, rec);
 }
 
 // The same two passes inside the device loop after a dense pull, which only
-// sets next-frontier bits: build iteration it's member list, tile starts,
-// counts and out-degree sum from its bitmap (gated on the device mode).
+// sets next-frontier bits: build iteration it's counts, out-degree sum and
+// (when a Wedge iteration follows) member list and tile starts from its
+// bitmap (gated on the device mode).
 struct FrontierBufs {
     uint32_t *fbits[2], *fvert[2], *fpref[2], *tstart[2];
 };
@@ -231,10 +315,11 @@ struct FrontierBufs {
 __global__ void __launch_bounds__(CB_THREADS) loop_frontier_count_kernel(LoopCtx c, FrontierBufs f, uint64_t n,
                                                                          const uint64_t *idx_off,
                                                                          const uint32_t *outdeg,
-                                                                         uint64_t *bcount) {
+                                                                         uint64_t *bcount, unsigned *counter) {
     const uint64_t it = ctx_iter(c);
     if (ctx_mode(c, it) != MODE_FULL) return;
-    frontier_count_body((it & 1) ? f.fbits[1] : f.fbits[0], n, idx_off, outdeg, bcount);
+    frontier_count_body((it & 1) ? f.fbits[1] : f.fbits[0], n, idx_off, outdeg, bcount, counter, ctx_out(c, it),
+                        c.keep_lists, c.edges, c.wedge_limit);
 }
 
 __global__ void __launch_bounds__(CB_THREADS) loop_frontier_list_kernel(LoopCtx c, FrontierBufs f, uint64_t n,

@@ -22,6 +22,7 @@ struct LoopCtx {
     uint64_t it_arg;
     uint64_t wedge_limit;   // wedge iff edges > 0 and edge_sum < wedge_limit
     uint64_t edges;
+    int32_t keep_lists;     // WG_RUN_KEEP_LISTS: build every frontier list (traces, exchange)
 };
 
 __device__ __forceinline__ uint64_t ctx_iter(const LoopCtx &c) {

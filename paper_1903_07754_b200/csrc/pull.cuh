@@ -53,6 +53,7 @@ struct PullBufs {
     uint32_t *fpref[2];
     uint32_t *tstart[2];
     uint64_t *bcount;  // compaction scratch (dense-pull frontier build)
+    unsigned *ticket;  // its completion ticket
     const uint32_t *glist;
     uint32_t n;
     uint32_t first_hit;  // WG_RUN_FIRST_HIT (filtered pulls only)
@@ -207,28 +208,35 @@ __device__ __forceinline__ void apply_segments(bool app, uint32_t d, T agg, T pd
 // index-length prefixes and the out-degree sum are produced afterwards by the
 // ordered bitmap compaction (frontier_count/list kernels), which is cheaper
 // than staging ~V appends inside the pull.
+// The dense pull writes EVERY destination it covers (min(prev[d], cand)), so
+// after a dense iteration nxt holds the full value vector and no buffer sync
+// is needed when the next iteration is dense too (end_of_iteration).  Shared
+// (incomplete) segments use atomicMin, which is exact because values never
+// increase: the stale nxt[d] (two iterations old) is >= prev[d].
 template <typename T>
 __device__ __forceinline__ void apply_dense(bool app, uint32_t d, T agg, T pd, bool complete, T INF,
                                             int64_t inc, T *nxt, uint32_t *obits, uint32_t &ovf) {
     using VT = ValTraits<T>;
     if (!app) return;
-    T cand;
+    T cand = INF;
     if constexpr (VT::U32) {
-        if (agg == INF) return;
-        const uint64_t cc = (uint64_t)agg + (uint64_t)inc;
-        if (cc >= 0xffffffffull) {
-            ovf = 1;
-            return;
+        if (agg != INF) {
+            const uint64_t cc = (uint64_t)agg + (uint64_t)inc;
+            if (cc >= 0xffffffffull) {
+                ovf = 1;
+                return;
+            }
+            cand = (T)cc;
         }
-        cand = (T)cc;
     } else {
         cand = agg + (T)inc;
     }
-    if (!(cand < pd)) return;
-    if (complete) nxt[d] = cand;
-    else if constexpr (VT::U32) atomicMin((unsigned *)&nxt[d], (unsigned)cand);
-    else atomicMin((long long *)&nxt[d], (long long)cand);
-    atomicOr(&obits[d >> 5], 1u << (d & 31));
+    const bool upd = cand < pd;
+    const T v = upd ? cand : pd;
+    if (complete) nxt[d] = v;
+    else if constexpr (VT::U32) atomicMin((unsigned *)&nxt[d], (unsigned)v);
+    else atomicMin((long long *)&nxt[d], (long long)v);
+    if (upd) atomicOr(&obits[d >> 5], 1u << (d & 31));
 }
 
 // Fold one vector's lanes into a minimum (messages prev[src] (+ weight)).
@@ -478,6 +486,7 @@ struct DenseChunk {
     unsigned heads[CH];
     bool valid[CH];
     T ps[CH][W];
+    uint32_t src[CH][W];  // filtered pulls: between the prev[d] and the lane gathers
     uint32_t wt[CH][WEIGHT ? W : 1];
     T pd[CH];
 };
@@ -509,9 +518,9 @@ __device__ __forceinline__ T fold_gathered(const T (&ps)[W], const uint32_t (&wt
     return agg;
 }
 
-// Dense pull, unfiltered programs (CC, SSSP, PageRank-like min-plus): the
-// warp streams its tile range with TMA and processes CH tiles per stage in
-// four phases so that independent work overlaps:
+// Dense pull (every min-plus program): the warp streams its tile range with
+// TMA and processes CH tiles per stage in four phases so that independent
+// work overlaps:
 //   1. destinations and lanes from shared memory; segment heads per tile
 //      (ballot) -> only segment TAILS gather prev[d];
 //   2. all gathers of the CH tiles in flight together; lane folds;
@@ -519,7 +528,13 @@ __device__ __forceinline__ T fold_gathered(const T (&ps)[W], const uint32_t (&wt
 //      the carried segment only ever joins a tile's HEAD segment, whose tail
 //      lane takes the carried minimum in phase 4);
 //   4. a warp-uniform carry chain across the CH tiles, then the applies.
-template <typename T, int W, bool WEIGHT, int TMA_CH, int TMA_S, int MINB>
+// Chunks are software-pipelined across the warp's range: unfiltered programs
+// gather chunk k+1 while chunk k reduces; filtered programs (BFS: only
+// destinations with prev[d] == INF pull, pulls.pyx:77-80) read prev[d] of
+// chunk k+2, gather chunk k+1 and reduce chunk k, so the dependent
+// prev[d] -> prev[src] chain never stalls the warp.  With WG_RUN_FIRST_HIT a
+// destination whose carried minimum is already finite gathers nothing more.
+template <typename T, int W, bool WEIGHT, bool FILTER, int TMA_CH, int TMA_S, int MINB>
 __global__ void __launch_bounds__(PULL_THREADS, MINB) pull_dense_tma_kernel(LoopCtx c, wg_graph g, PullBufs b,
                                                                       int shift, int64_t inc,
                                                                       int64_t sentinel) {
@@ -556,7 +571,7 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) pull_dense_tma_kernel(Loop
     if (t0w < t1w) {
         const uint32_t tfirst = (uint32_t)t0w, tend = (uint32_t)t1w;
         const uint32_t vend = (tend << 5) < nvec ? (tend << 5) : nvec;
-        o.touched = vend - (tfirst << 5);  // every vector of the range is processed
+        if (!FILTER) o.touched = vend - (tfirst << 5);  // every vector of the range is processed
         const uint32_t nchunks = (tend - tfirst + CH - 1) / CH;
         if (lane == 0) {
             for (int s = 0; s < TMA_S; ++s) mbar_init(&bars[s], 1);
@@ -588,12 +603,33 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) pull_dense_tma_kernel(Loop
         // software pipeline: chunk ch+1's gathers are in flight while chunk
         // ch is reduced (two register sets, loop unrolled by two so that no
         // copy touches a register with a load outstanding)
-        auto load = [&](uint32_t ch, DenseChunk<T, W, WEIGHT, CH> &k) {
+        using Chunk = DenseChunk<T, W, WEIGHT, CH>;
+        // lane gathers of a chunk whose prev[d] are known (filtered) or not
+        // needed first (unfiltered)
+        auto gath = [&](Chunk &k) {
+            uint32_t hit_d = NONE;
+            if (FILTER && b.first_hit && cy.d != NONE && cy.agg != INF) hit_d = cy.d;
+#pragma unroll
+            for (int u = 0; u < CH; ++u) {
+                bool pull = true;
+                if (FILTER) {
+                    const bool unv = k.valid[u] && k.pd[u] == INF;  // only unvisited destinations
+                    o.touched += __popc(__ballot_sync(FULL, unv));
+                    pull = unv && k.d[u] != hit_d;
+                }
+#pragma unroll
+                for (int l = 0; l < W; ++l)
+                    k.ps[u][l] = (pull && k.src[u][l] != WG_NO_LANE) ? prev[k.src[u][l]] : INF;
+            }
+        };
+        // destinations, lanes and segment heads of a chunk from shared memory;
+        // refills the stage; issues prev[d] (all lanes if filtered, else the
+        // segment tails) and, unfiltered, the gathers
+        auto load = [&](uint32_t ch, Chunk &k) {
             const int s = (int)(ch % TMA_S);
             mbar_wait(&bars[s], (ch / TMA_S) & 1u);
             const uint32_t *st = ring + (size_t)s * SM::STAGE_WORDS;
             const uint32_t tbase = tfirst + ch * CH;
-            uint32_t src[CH][W];
 #pragma unroll
             for (int u = 0; u < CH; ++u) {
                 const uint32_t tile = tbase + u;
@@ -602,14 +638,14 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) pull_dense_tma_kernel(Loop
                 k.d[u] = k.valid[u] ? st[SM::SRC_WORDS + j] : NONE;
                 if constexpr (W == 4) {
                     const uint4 v = *reinterpret_cast<const uint4 *>(st + j * 4);
-                    src[u][0] = v.x; src[u][1] = v.y; src[u][2] = v.z; src[u][3] = v.w;
+                    k.src[u][0] = v.x; k.src[u][1] = v.y; k.src[u][2] = v.z; k.src[u][3] = v.w;
                 } else {
 #pragma unroll
-                    for (int l = 0; l < W; ++l) src[u][l] = st[j * W + l];
+                    for (int l = 0; l < W; ++l) k.src[u][l] = st[j * W + l];
                 }
 #pragma unroll
                 for (int l = 0; l < W; ++l) {
-                    if (!k.valid[u]) src[u][l] = WG_NO_LANE;
+                    if (!k.valid[u]) k.src[u][l] = WG_NO_LANE;
                     if constexpr (WEIGHT) k.wt[u][l] = st[SM::SRC_WORDS + SM::VEC + j * W + l];
                 }
             }
@@ -623,16 +659,14 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) pull_dense_tma_kernel(Loop
                 const uint32_t dp = __shfl_up_sync(FULL, k.d[u], 1);
                 k.heads[u] = __ballot_sync(FULL, lane == 0 || dp != k.d[u]);
             }
-            // the gathers (segment tails also read prev[d])
 #pragma unroll
             for (int u = 0; u < CH; ++u) {
                 const bool tail = (((k.heads[u] >> 1) | 0x80000000u) >> lane) & 1u;
-                k.pd[u] = (k.valid[u] && tail) ? prev[k.d[u]] : INF;
-#pragma unroll
-                for (int l = 0; l < W; ++l) k.ps[u][l] = src[u][l] != WG_NO_LANE ? prev[src[u][l]] : INF;
+                k.pd[u] = (k.valid[u] && (FILTER || tail)) ? prev[k.d[u]] : INF;
             }
+            if (!FILTER) gath(k);
         };
-        auto reduce = [&](uint32_t ch, DenseChunk<T, W, WEIGHT, CH> &k) {
+        auto reduce = [&](uint32_t ch, Chunk &k) {
             const uint32_t tbase = tfirst + ch * CH;
             T agg[CH];
 #pragma unroll
@@ -696,14 +730,35 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) pull_dense_tma_kernel(Loop
                 apply_dense<T>(app, k.d[u], agg[u], k.pd[u], left && right, INF, inc, nxt, obits, o.ovf);
             }
         };
-        DenseChunk<T, W, WEIGHT, CH> ka, kb;
-        load(0, ka);
-        for (uint32_t ch = 0; ch < nchunks; ch += 2) {
-            if (ch + 1 < nchunks) load(ch + 1, kb);
-            reduce(ch, ka);
-            if (ch + 1 >= nchunks) break;
-            if (ch + 2 < nchunks) load(ch + 2, ka);
-            reduce(ch + 1, kb);
+        if constexpr (!FILTER) {
+            Chunk ka, kb;
+            load(0, ka);
+            for (uint32_t ch = 0; ch < nchunks; ch += 2) {
+                if (ch + 1 < nchunks) load(ch + 1, kb);
+                reduce(ch, ka);
+                if (ch + 1 >= nchunks) break;
+                if (ch + 2 < nchunks) load(ch + 2, ka);
+                reduce(ch + 1, kb);
+            }
+        } else {
+            // three register sets: A gathers in flight, B prev[d] in flight
+            Chunk ka, kb, kc;
+            load(0, ka);
+            if (1 < nchunks) load(1, kb);
+            gath(ka);
+            for (uint32_t ch = 0; ch < nchunks; ch += 3) {
+                if (ch + 2 < nchunks) load(ch + 2, kc);
+                if (ch + 1 < nchunks) gath(kb);
+                reduce(ch, ka);
+                if (ch + 1 >= nchunks) break;
+                if (ch + 3 < nchunks) load(ch + 3, ka);
+                if (ch + 2 < nchunks) gath(kc);
+                reduce(ch + 1, kb);
+                if (ch + 2 >= nchunks) break;
+                if (ch + 4 < nchunks) load(ch + 4, kb);
+                if (ch + 3 < nchunks) gath(ka);
+                reduce(ch + 2, kc);
+            }
         }
     }
     end_of_pull<T>(o, out);
@@ -841,9 +896,14 @@ __device__ __forceinline__ void end_of_iteration(const LoopCtx &c, uint64_t it, 
         const uint32_t *list = ((it & 1) ? b.fvert[1] : b.fvert[0]);
         const uint64_t nz = *(volatile const uint64_t *)&out->nz_packed >> 32;
         const uint64_t z = *(volatile const uint64_t *)&out->z_count;
-        for (uint64_t i = tid; i < nz + z; i += nthreads) {
-            const uint32_t v = i < nz ? list[i] : list[b.n - 1 - (i - nz)];
-            dst[v] = *(volatile const T *)&src[v];
+        if (*(volatile const uint64_t *)&out->reserved[2]) {
+            // no member list: the next iteration is a dense pull, which writes
+            // every destination (apply_dense), so nothing needs syncing
+        } else {
+            for (uint64_t i = tid; i < nz + z; i += nthreads) {
+                const uint32_t v = i < nz ? list[i] : list[b.n - 1 - (i - nz)];
+                dst[v] = *(volatile const T *)&src[v];
+            }
         }
         // clear bits of the frontier produced by it-1 (its bitmap is reused by it+1)
         uint32_t *obits = (((it - 1) & 1) ? b.fbits[1] : b.fbits[0]);
@@ -851,7 +911,7 @@ __device__ __forceinline__ void end_of_iteration(const LoopCtx &c, uint64_t it, 
         const uint64_t pnz = *(volatile const uint64_t *)&in->nz_packed >> 32;
         const uint64_t pz = *(volatile const uint64_t *)&in->z_count;
         const uint64_t words = ((uint64_t)b.n + 31) >> 5;
-        if (pnz + pz > words) {
+        if (pnz + pz > words || *(volatile const uint64_t *)&in->reserved[2]) {
             for (uint64_t w = tid; w < words; w += nthreads) obits[w] = 0;
         } else {
             for (uint64_t i = tid; i < pnz + pz; i += nthreads) {

@@ -475,6 +475,8 @@ class DeviceLoop:
         records: list[IterRecord] = []
         converged = False
         it, batch, last = 1, 2, 0
+        if trace is not None:  # frontier_members reads every produced list
+            p.flags |= _lib.WG_RUN_KEEP_LISTS
         cap_batch = min(256, self.ring - 2)
         while it <= max_iterations and not converged:
             cnt = 1 if trace is not None else min(batch, max_iterations - it + 1)

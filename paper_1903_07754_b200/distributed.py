@@ -161,6 +161,7 @@ class DeviceShard:
 
     def seed(self):
         self.p = self.loop.seed(self.init, self.words, self.kern, self.threshold)
+        self.p.flags |= self._lib.WG_RUN_KEEP_LISTS  # wg_exchange_pack reads the member lists
 
     def step(self, it: int):
         L = self._lib.load()
