@@ -448,7 +448,7 @@ def e2e_b200(args, wl, g, loop, dinit, words, kern, thr, max_it, first_hit=False
     # device buffers with readable slack past the end (TMA tail rounding, wedge_b200.h)
     dev = {k: torch.empty(v.numel() + 64, dtype=v.dtype, device="cuda")[: v.numel()] for k, v in host.items()}
     g2 = dv.DeviceGraph(g.n, g.width, g.edges, g.nvec, g.entries, dev["vsrc"], dev["vdst"], dev.get("vw"),
-                        dev["idx_off"], dev["idx_pos"], dev["outdeg"])
+                        dev["idx_off"], dev["idx_pos"], dev["outdeg"], lens_are_degrees=g.lens_are_degrees)
     loop2 = dv.DeviceLoop(g2, loop.shift, loop.val_type)
     out_host = torch.empty(g.n, dtype=torch.int32).pin_memory()
     h2d = sum(v.numel() * v.element_size() for v in host.values())

@@ -67,7 +67,13 @@ typedef struct wg_graph {
     const uint64_t *idx_off; /* [n+1] edge-index offsets */
     const uint32_t *idx_pos; /* [entries] ascending de-duplicated vector positions */
     const uint32_t *outdeg;  /* [n] out-degrees */
+    uint32_t flags;          /* WG_GRAPH_* */
 } wg_graph;
+
+/* Every vertex's edge-index length equals its out-degree (no parallel edges;
+ * set by the layout builders when verified): frontier compaction then reads
+ * only the 4-byte degrees. */
+#define WG_GRAPH_LENS_ARE_DEGREES 1
 
 /* MinPlusKernel (engine.py:50-63). */
 typedef struct wg_minplus {

@@ -26,7 +26,10 @@ c_u32, c_u64, c_i32, c_i64, c_vp = ctypes.c_uint32, ctypes.c_uint64, ctypes.c_in
 class WgGraph(ctypes.Structure):
     _fields_ = [("n", c_u32), ("width", c_u32), ("nvec", c_u64), ("edges", c_u64),
                 ("entries", c_u64), ("vsrc", c_vp), ("vdst", c_vp), ("vw", c_vp),
-                ("idx_off", c_vp), ("idx_pos", c_vp), ("outdeg", c_vp)]
+                ("idx_off", c_vp), ("idx_pos", c_vp), ("outdeg", c_vp), ("flags", c_u32)]
+
+
+WG_GRAPH_LENS_ARE_DEGREES = 1
 
 
 class WgMinPlus(ctypes.Structure):

@@ -126,6 +126,8 @@ struct KernelWs {
 
 uint64_t tstart_entries(const wg_graph *g) { return g->entries / TR_TILE + 2; }
 
+bool lens_are_degrees(const wg_graph *g) { return (g->flags & WG_GRAPH_LENS_ARE_DEGREES) != 0; }
+
 // Compaction scratch: per-block totals of the frontier (4 per block) or
 // group (1 per block) compactions, then one slot holding the frontier
 // compaction's completion ticket (zero between launches).
@@ -184,10 +186,11 @@ int launch_frontier_compaction(const wg_graph *g, const uint32_t *words, uint64_
                                unsigned *ticket, uint32_t *fvert, uint32_t *fpref, uint32_t *tstart,
                                wg_iter_rec *rec, cudaStream_t s) {
     uint64_t nb = fb_blocks(g->n ? g->n : 1);
+    const uint64_t *off = lens_are_degrees(g) ? nullptr : g->idx_off;
     WG_CUDA(cudaMemsetAsync(ticket, 0, sizeof(unsigned), s));
-    frontier_count_kernel<<<(unsigned)nb, CB_THREADS, 0, s>>>(words, g->n, g->idx_off, g->outdeg,
-                                                              bcount, ticket, rec); ::wg::count_launch();
-    frontier_list_kernel<<<(unsigned)nb, CB_THREADS, 0, s>>>(words, g->n, g->idx_off, bcount, fvert,
+    frontier_count_kernel<<<(unsigned)nb, CB_THREADS, 0, s>>>(words, g->n, off, g->outdeg, bcount, ticket,
+                                                              rec); ::wg::count_launch();
+    frontier_list_kernel<<<(unsigned)nb, CB_THREADS, 0, s>>>(words, g->n, off, g->outdeg, bcount, fvert,
                                                              fpref, tstart, rec); ::wg::count_launch();
     WG_CHECK_LAUNCH("frontier compaction");
     return WG_OK;
@@ -317,9 +320,10 @@ int launch_pull(const LoopCtx &c, const wg_graph *g, const PullBufs &pb, int val
             fb.tstart[i] = pb.tstart[i];
         }
         const uint64_t nb = fb_blocks(g->n ? g->n : 1);
-        loop_frontier_count_kernel<<<(unsigned)nb, CB_THREADS, 0, s>>>(c, fb, g->n, g->idx_off, g->outdeg,
+        const uint64_t *off = lens_are_degrees(g) ? nullptr : g->idx_off;
+        loop_frontier_count_kernel<<<(unsigned)nb, CB_THREADS, 0, s>>>(c, fb, g->n, off, g->outdeg,
                                                                       pb.bcount, pb.ticket);
-        loop_frontier_list_kernel<<<(unsigned)nb, CB_THREADS, 0, s>>>(c, fb, g->n, g->idx_off, pb.bcount);
+        loop_frontier_list_kernel<<<(unsigned)nb, CB_THREADS, 0, s>>>(c, fb, g->n, off, g->outdeg, pb.bcount);
         ::wg::count_launch(2);
         WG_CHECK_LAUNCH("dense frontier compaction");
         if (slot) {  // a Wedge iteration's pull (below) is timed as a pull again

@@ -145,13 +145,16 @@ struct VertexInfo {
     uint32_t deg;    // out-degree
 };
 
+// idx_off == nullptr: the layout has one index entry per edge (entries ==
+// edges, a de-duplicated graph), so a vertex's index length is its
+// out-degree and only the 4-byte degrees are read.
 __device__ __forceinline__ VertexInfo vertex_info(uint32_t x, uint64_t wi, unsigned lane,
                                                   const uint64_t *idx_off, const uint32_t *outdeg) {
     VertexInfo r{((x >> lane) & 1u) != 0, 0u, 0u};
     if (r.set) {
         const uint64_t u = (wi << 5) + lane;
-        r.len = (uint32_t)(idx_off[u + 1] - idx_off[u]);
-        if (outdeg) r.deg = outdeg[u];
+        r.deg = outdeg[u];
+        r.len = idx_off ? (uint32_t)(idx_off[u + 1] - idx_off[u]) : r.deg;
     }
     return r;
 }
@@ -241,7 +244,8 @@ __device__ __forceinline__ void frontier_count_body(const uint32_t *words, uint6
 }
 
 __device__ __forceinline__ void frontier_list_body(const uint32_t *words, uint64_t nbits,
-                                                   const uint64_t *idx_off, const uint64_t *bcount,
+                                                   const uint64_t *idx_off, const uint32_t *outdeg,
+                                                   const uint64_t *bcount,
                                                    uint32_t *fvert, uint32_t *fpref, uint32_t *tstart,
                                                    const wg_iter_rec *rec) {
     if (*(volatile const uint64_t *)&rec->reserved[2]) return;  // nobody consumes the list
@@ -250,7 +254,7 @@ __device__ __forceinline__ void frontier_list_body(const uint32_t *words, uint64
     const unsigned lt = (1u << lane) - 1u;
     const uint64_t wbase = (uint64_t)blockIdx.x * FB_WORDS + (uint64_t)warp * 32;
     uint64_t nz, ent, z, es;
-    chunk_counts(words, nbits, wbase, idx_off, nullptr, nz, ent, z, es);
+    chunk_counts(words, nbits, wbase, idx_off, outdeg, nz, ent, z, es);
     if (lane == 0) {
         s_w[0][warp] = nz; s_w[1][warp] = ent; s_w[2][warp] = z;
     }
@@ -269,7 +273,7 @@ __device__ __forceinline__ void frontier_list_body(const uint32_t *words, uint64
         const uint32_t x = __shfl_sync(FULL, myw, j);
         if (x == 0) continue;  // warp-uniform
         const uint64_t wi = wbase + j;
-        const VertexInfo vi = vertex_info(x, wi, lane, idx_off, nullptr);
+        const VertexInfo vi = vertex_info(x, wi, lane, idx_off, outdeg);
         const bool hasd = vi.set && vi.len != 0, zero = vi.set && vi.len == 0;
         const unsigned mnz = __ballot_sync(FULL, hasd), mz = __ballot_sync(FULL, zero);
         const uint64_t elen = hasd ? vi.len : 0u;
@@ -298,10 +302,11 @@ __global__ void __launch_bounds__(CB_THREADS) frontier_count_kernel(const uint32
 }
 
 __global__ void __launch_bounds__(CB_THREADS) frontier_list_kernel(const uint32_t *words, uint64_t nbits,
-                                                                   const uint64_t *idx_off, const uint64_t *bcount,
-                                                                   uint32_t *fvert, uint32_t *fpref,
-                                                                   uint32_t *tstart, const wg_iter_rec *rec) {
-    frontier_list_body(words, nbits, idx_off, bcount, fvert, fpref, tstart, rec);
+                                                                   const uint64_t *idx_off, const uint32_t *outdeg,
+                                                                   const uint64_t *bcount, uint32_t *fvert,
+                                                                   uint32_t *fpref, uint32_t *tstart,
+                                                                   const wg_iter_rec *rec) {
+    frontier_list_body(words, nbits, idx_off, outdeg, bcount, fvert, fpref, tstart, rec);
 }
 
 // The same two passes inside the device loop after a dense pull, which only
@@ -324,11 +329,12 @@ __global__ void __launch_bounds__(CB_THREADS) loop_frontier_count_kernel(LoopCtx
 
 __global__ void __launch_bounds__(CB_THREADS) loop_frontier_list_kernel(LoopCtx c, FrontierBufs f, uint64_t n,
                                                                         const uint64_t *idx_off,
+                                                                        const uint32_t *outdeg,
                                                                         const uint64_t *bcount) {
     const uint64_t it = ctx_iter(c);
     if (ctx_mode(c, it) != MODE_FULL) return;
     const int k = (int)(it & 1);
-    frontier_list_body(k ? f.fbits[1] : f.fbits[0], n, idx_off, bcount, k ? f.fvert[1] : f.fvert[0],
+    frontier_list_body(k ? f.fbits[1] : f.fbits[0], n, idx_off, outdeg, bcount, k ? f.fvert[1] : f.fvert[0],
                        k ? f.fpref[1] : f.fpref[0], k ? f.tstart[1] : f.tstart[0], ctx_out(c, it));
 }
 

@@ -68,11 +68,14 @@ class DeviceGraph:
     out-degrees.  Replaces PullTopology + EdgeIndex + out-degrees
     (graph.py:109-212) on the device."""
 
-    def __init__(self, n, width, edges, nvec, entries, vsrc, vdst, vw, idx_off, idx_pos, outdeg):
+    def __init__(self, n, width, edges, nvec, entries, vsrc, vdst, vw, idx_off, idx_pos, outdeg,
+                 lens_are_degrees: bool = False):
         self.n, self.width, self.edges = int(n), int(width), int(edges)
         self.nvec, self.entries = int(nvec), int(entries)
         self.vsrc, self.vdst, self.vw = vsrc, vdst, vw
         self.idx_off, self.idx_pos, self.outdeg = idx_off, idx_pos, outdeg
+        # every index length equals the out-degree (WG_GRAPH_LENS_ARE_DEGREES)
+        self.lens_are_degrees = bool(lens_are_degrees)
         self._struct = None
 
     # -- construction ------------------------------------------------------
@@ -105,9 +108,11 @@ class DeviceGraph:
                                 scratch.numel(), counts, _lib.stream_ptr(stream)))
         del scratch
         nvec, entries = int(counts[0]), int(counts[1])
+        # the built out-degrees count edges and index lengths never exceed
+        # them, so equal totals mean equal per vertex
         return cls(n, width, m, nvec, entries, vsrc[: max(nvec * width, 1)], vdst[: max(nvec, 1)],
                    vw[: max(nvec * width, 1)] if vw is not None else None, idx_off,
-                   idx_pos[: max(entries, 1)], outdeg)
+                   idx_pos[: max(entries, 1)], outdeg, lens_are_degrees=(entries == m))
 
     @classmethod
     def from_reference(cls, topology, index, degrees, device="cuda") -> "DeviceGraph":
@@ -140,13 +145,15 @@ class DeviceGraph:
                                       device), SLACK),
                    vw, off,
                    to_dev_u32(pos if pos.size else np.zeros(1, np.int64), device),
-                   to_dev_u32(deg if deg.size else np.zeros(1, np.int64), device))
+                   to_dev_u32(deg if deg.size else np.zeros(1, np.int64), device),
+                   lens_are_degrees=bool(np.array_equal(np.diff(np.asarray(index.offsets, np.int64)), deg)))
 
     def struct(self) -> WgGraph:
         if self._struct is None:
             self._struct = WgGraph(self.n, self.width, self.nvec, self.edges, self.entries,
                                    _ptr(self.vsrc), _ptr(self.vdst), _ptr(self.vw), _ptr(self.idx_off),
-                                   _ptr(self.idx_pos), _ptr(self.outdeg))
+                                   _ptr(self.idx_pos), _ptr(self.outdeg),
+                                   _lib.WG_GRAPH_LENS_ARE_DEGREES if self.lens_are_degrees else 0)
         return self._struct
 
     def weighted(self) -> bool:
