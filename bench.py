@@ -436,20 +436,27 @@ def roofline(rows, recs, n, E, weighted, filt, wl):
 
 
 def e2e_b200(args, wl, g, loop, dinit, words, kern, thr, max_it, first_hit=False):
-    """Same metric through the C ABI with the layout in pinned HOST memory:
-    per step H2D of the layout, the device loop, D2H of the result."""
+    """Same metric through the C ABI with the graph in pinned HOST memory.
+    Per step: H2D of the topology in its compact form (lanes vsrc [+ weights]
+    and per-destination vector offsets voff, i.e. PullTopology's lane_src /
+    lane_weight / vec_dst as uint32), on-device rebuild of vec_dst, the edge
+    index and the out-degrees (wg_expand_destinations + wg_build_index), the
+    device loop, D2H of the result."""
     import torch
     from paper_1903_07754_b200 import _lib, device as dv
 
-    host = {}
-    for name in ("vsrc", "vdst", "vw", "idx_off", "idx_pos", "outdeg"):
-        t = getattr(g, name)
-        if t is not None:
-            host[name] = t.cpu().pin_memory()
+    host = {"vsrc": g.vsrc.cpu().pin_memory(), "voff": g.vector_offsets().cpu().pin_memory()}
+    if g.vw is not None:
+        host["vw"] = g.vw.cpu().pin_memory()
     # device buffers with readable slack past the end (TMA tail rounding, wedge_b200.h)
     dev = {k: torch.empty(v.numel() + 64, dtype=v.dtype, device="cuda")[: v.numel()] for k, v in host.items()}
-    g2 = dv.DeviceGraph(g.n, g.width, g.edges, g.nvec, g.entries, dev["vsrc"], dev["vdst"], dev.get("vw"),
-                        dev["idx_off"], dev["idx_pos"], dev["outdeg"], lens_are_degrees=g.lens_are_degrees)
+    for k, v in host.items():
+        dev[k].copy_(v)
+    scratch = torch.empty(int(_lib.load().wg_index_scratch_bytes(g.nvec * g.width, g.n)), dtype=torch.uint8,
+                          device="cuda")
+    g2 = dv.DeviceGraph.from_lanes(g.n, g.width, g.edges, g.nvec, dev["vsrc"], dev.get("vw"), dev["voff"],
+                                   scratch)
+    assert g2.entries == g.entries and g2.lens_are_degrees == g.lens_are_degrees
     loop2 = dv.DeviceLoop(g2, loop.shift, loop.val_type)
     out_host = torch.empty(g.n, dtype=torch.int32).pin_memory()
     h2d = sum(v.numel() * v.element_size() for v in host.values())
@@ -459,6 +466,7 @@ def e2e_b200(args, wl, g, loop, dinit, words, kern, thr, max_it, first_hit=False
     def one():
         for k, v in host.items():
             dev[k].copy_(v, non_blocking=True)
+        g2.rebuild_derived(dev["voff"], scratch)
         p = loop2.seed(dinit, words, kern, thr, first_hit=first_hit)
         recs, conv, last = loop2.drive(p, max_it)
         out_host.copy_(loop2.values_after(last), non_blocking=True)
@@ -478,7 +486,7 @@ def e2e_b200(args, wl, g, loop, dinit, words, kern, thr, max_it, first_hit=False
     ms = float(np.mean(ts))
     return {"value": round(g.edges / (ms * 1e-3) / 1e9, 4), "unit": "GTEPS (|E|/time-to-solution)",
             "ms_per_step": round(ms, 3), "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-            "path": "pinned host layout -> H2D -> wg_run_init/wg_run_enqueue -> D2H labels"}
+            "path": "pinned host topology (vsrc[, vw], voff) -> H2D -> wg_expand_destinations + wg_build_index -> device loop -> D2H values"}
 
 
 def host_reference_layout(g):

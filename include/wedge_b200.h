@@ -102,6 +102,18 @@ int wg_build_layout(uint32_t n, uint64_t m, const uint32_t *d_src, const uint32_
                     uint32_t *d_outdeg, void *d_scratch, size_t scratch_bytes,
                     uint64_t *h_counts, void *stream);
 
+/* Rebuild the derived parts of a layout from its lanes (g->vsrc, n, width,
+ * nvec, edges = valid lanes): the edge index d_idx_off [n+1] / d_idx_pos
+ * [edges] (build_edge_index graph.py:283-301) and d_outdeg [n]
+ * (compute_out_degrees graph.py:277-280); h_entries (host) receives the
+ * index length.  Synchronises `stream`. */
+size_t wg_index_scratch_bytes(uint64_t lanes, uint32_t n);
+int wg_build_index(const wg_graph *g, uint64_t *d_idx_off, uint32_t *d_idx_pos, uint32_t *d_outdeg,
+                   void *d_scratch, size_t scratch_bytes, uint64_t *h_entries, void *stream);
+/* vec_dst from per-destination vector offsets d_voff [n+1] (the run-length
+ * form of PullTopology.vec_dst, graph.py:240-243).  Asynchronous. */
+int wg_expand_destinations(uint32_t n, const uint32_t *d_voff, uint64_t nvec, uint32_t *d_vdst, void *stream);
+
 /* ---------------- per-call kernels (backend protocol, kernels.py:55-125) --- */
 /* Workspace for wg_transform / wg_pull_wedge / wg_covered_groups. */
 size_t wg_kernel_workspace_bytes(const wg_graph *g, int shift);

@@ -66,7 +66,7 @@ EXPORTS = [
     "wg_timer_create", "wg_timer_destroy", "wg_timer_reset", "wg_timer_read", "wg_launch_count",
     "wg_exchange_pack", "wg_exchange_apply", "wg_run_graph_create", "wg_run_graph_launch",
     "wg_run_graph_destroy", "wg_run_loop_graph_create", "wg_run_loop_launch", "wg_run_persistent",
-    "wg_debug_phase_buffer",
+    "wg_debug_phase_buffer", "wg_index_scratch_bytes", "wg_build_index", "wg_expand_destinations",
 ]
 
 _LIB = None
@@ -143,6 +143,9 @@ def load(path: os.PathLike | str | None = None):
         "wg_run_loop_launch": (ctypes.c_int, [c_vp, B, c_u64, c_vp]),
         "wg_run_persistent": (ctypes.c_int, [G, B, P, c_u64, c_vp]),
         "wg_debug_phase_buffer": (ctypes.c_int, [c_vp, c_u64]),
+        "wg_index_scratch_bytes": (ctypes.c_size_t, [c_u64, c_u32]),
+        "wg_build_index": (ctypes.c_int, [G, c_vp, c_vp, c_vp, c_vp, ctypes.c_size_t, u64p, c_vp]),
+        "wg_expand_destinations": (ctypes.c_int, [c_u32, c_vp, c_u64, c_vp, c_vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

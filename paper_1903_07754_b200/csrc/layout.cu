@@ -83,6 +83,29 @@ __global__ void unpack_positions(uint64_t k, const uint64_t *keys, int vb, uint3
 
 unsigned grid_1d(uint64_t work) { return grid_for(work, 256 * 8, 16); }
 
+// index key of lane k: (source << vb) | vector; padding lanes get an all-ones
+// source field (sb is chosen so it exceeds every vertex id)
+__global__ void lane_keys(uint64_t lanes, const uint32_t *vsrc, int width, int vb, int sb, uint64_t *keys) {
+    const uint64_t pad = ((1ull << sb) - 1) << vb;
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < lanes;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t s = vsrc[k];
+        keys[k] = s == WG_NO_LANE ? (pad | (k / width)) : (((uint64_t)s << vb) | (k / width));
+    }
+}
+
+// vdst[v] = d for v in [voff[d], voff[d+1]); a warp per destination run
+// keeps hub runs coalesced
+__global__ void expand_destinations(uint32_t n, const uint32_t *voff, uint32_t *vdst) {
+    const uint64_t gwarp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const unsigned lane = threadIdx.x & 31;
+    for (uint64_t d = gwarp; d < n; d += nw) {
+        const uint32_t a = voff[d], b = voff[d + 1];
+        for (uint32_t v = a + lane; v < b; v += 32) vdst[v] = (uint32_t)d;
+    }
+}
+
 struct LayoutScratch {
     uint64_t *k0, *k1;     // m keys x2
     uint32_t *w0, *w1;     // m weights x2
@@ -235,6 +258,83 @@ int wg_build_layout(uint32_t n, uint64_t m, const uint32_t *d_src, const uint32_
     WG_CUDA(cudaStreamSynchronize(s));
     h_counts[0] = nvec;
     h_counts[1] = entries;
+    return WG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Rebuild the derived parts of a layout on the device from its lanes: the
+// edge index (graph.py:283-301), out-degrees (graph.py:277-280) and the
+// per-vector destinations from per-destination vector offsets.  Lets a caller
+// upload only vsrc (+ vw) and voff instead of the whole layout.
+// ---------------------------------------------------------------------------
+size_t wg_index_scratch_bytes(uint64_t lanes, uint32_t n) {
+    uint64_t mm = lanes ? lanes : 1;
+    return 2 * carve_size(mm * 8) + 3 * carve_size(((uint64_t)n + 1) * 8) + carve_size(32) +
+           carve_size(cub_temp_bytes(mm, n)) + 1024;
+}
+
+int wg_build_index(const wg_graph *g, uint64_t *d_idx_off, uint32_t *d_idx_pos, uint32_t *d_outdeg,
+                   void *d_scratch, size_t scratch_bytes, uint64_t *h_entries, void *stream) {
+    WG_REQUIRE(g && d_idx_off && d_outdeg && h_entries, "null argument");
+    WG_REQUIRE(g->width == 1 || g->width == 2 || g->width == 4 || g->width == 8, "unsupported width %u",
+               g->width);
+    WG_REQUIRE(g->n < 0xffffffffu, "vertex count must be < 2^32-1");
+    WG_REQUIRE(scratch_bytes >= wg_index_scratch_bytes(g->nvec * g->width, g->n), "index scratch too small");
+    cudaStream_t s = as_stream(stream);
+    const uint32_t n = g->n;
+    const uint64_t lanes = g->nvec * g->width;
+    *h_entries = 0;
+    WG_CUDA(cudaMemsetAsync(d_idx_off, 0, ((uint64_t)n + 1) * 8, s));
+    WG_CUDA(cudaMemsetAsync(d_outdeg, 0, (uint64_t)n * 4, s));
+    if (lanes == 0 || n == 0 || g->edges == 0) return WG_OK;
+    WG_REQUIRE(g->vsrc && d_idx_pos, "null argument");
+    Carve cv{(char *)d_scratch, 0, scratch_bytes};
+    uint64_t *k0 = cv.take<uint64_t>(lanes), *k1 = cv.take<uint64_t>(lanes);
+    uint64_t *first = cv.take<uint64_t>((uint64_t)n + 1), *last = cv.take<uint64_t>((uint64_t)n + 1);
+    uint64_t *base = cv.take<uint64_t>((uint64_t)n + 1), *count = cv.take<uint64_t>(4);
+    size_t tbytes = cub_temp_bytes(lanes, n);
+    void *temp = cv.take<char>(tbytes);
+    WG_REQUIRE(temp != nullptr, "index scratch too small");
+    // the source field must exceed every real source so padding lanes sort last
+    const int sb = bits_for((uint64_t)n + 1);
+    const int vb = bits_for(g->nvec);
+    WG_REQUIRE(sb + vb <= 64, "graph too large for 64-bit index keys");
+    lane_keys<<<grid_1d(lanes), 256, 0, s>>>(lanes, g->vsrc, (int)g->width, vb, sb, k0); ::wg::count_launch();
+    WG_CHECK_LAUNCH("lane_keys");
+    cub::DoubleBuffer<uint64_t> ib(k0, k1);
+    size_t tb = tbytes;
+    WG_CUDA(cub::DeviceRadixSort::SortKeys(temp, tb, ib, (int64_t)lanes, vb, vb + sb, s));
+    uint64_t *isorted = ib.Current();
+    uint64_t *ialt = ib.Alternate();
+    const uint64_t m = g->edges;  // valid lanes; the padding keys follow them
+    WG_CUDA(cudaMemsetAsync(first, 0xff, ((uint64_t)n + 1) * 8, s));
+    run_bounds<<<grid_1d(m), 256, 0, s>>>(m, isorted, vb, first, last); ::wg::count_launch();
+    run_counts<<<grid_1d(n), 256, 0, s>>>(n, first, last, 0, base, d_outdeg); ::wg::count_launch();
+    WG_CHECK_LAUNCH("src runs");
+    tb = tbytes;
+    WG_CUDA(cub::DeviceSelect::Unique(temp, tb, isorted, ialt, count, (int64_t)m, s));
+    uint64_t entries = 0;
+    WG_CUDA(cudaMemcpyAsync(&entries, count, 8, cudaMemcpyDeviceToHost, s));
+    WG_CUDA(cudaStreamSynchronize(s));
+    WG_CUDA(cudaMemsetAsync(first, 0xff, ((uint64_t)n + 1) * 8, s));
+    run_bounds<<<grid_1d(entries), 256, 0, s>>>(entries, ialt, vb, first, last); ::wg::count_launch();
+    run_counts<<<grid_1d(n), 256, 0, s>>>(n, first, last, 0, base, nullptr); ::wg::count_launch();
+    WG_CHECK_LAUNCH("index runs");
+    WG_CUDA(cudaMemsetAsync(base + n, 0, 8, s));
+    tb = tbytes;
+    WG_CUDA(cub::DeviceScan::ExclusiveSum(temp, tb, base, d_idx_off, (int64_t)n + 1, s));
+    unpack_positions<<<grid_1d(entries), 256, 0, s>>>(entries, ialt, vb, d_idx_pos); ::wg::count_launch();
+    WG_CHECK_LAUNCH("unpack_positions");
+    *h_entries = entries;
+    return WG_OK;
+}
+
+int wg_expand_destinations(uint32_t n, const uint32_t *d_voff, uint64_t nvec, uint32_t *d_vdst, void *stream) {
+    WG_REQUIRE(d_voff && (d_vdst || nvec == 0), "null argument");
+    cudaStream_t s = as_stream(stream);
+    if (nvec == 0 || n == 0) return WG_OK;
+    expand_destinations<<<grid_1d(n), 256, 0, s>>>(n, d_voff, d_vdst); ::wg::count_launch();
+    WG_CHECK_LAUNCH("expand_destinations");
     return WG_OK;
 }
 

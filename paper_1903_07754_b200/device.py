@@ -148,6 +148,57 @@ class DeviceGraph:
                    to_dev_u32(deg if deg.size else np.zeros(1, np.int64), device),
                    lens_are_degrees=bool(np.array_equal(np.diff(np.asarray(index.offsets, np.int64)), deg)))
 
+    # -- compact upload form -------------------------------------------------
+    def vector_offsets(self):
+        """Per-destination vector offsets voff [n+1] (uint32): the run-length
+        form of vdst (vec_dst of graph.py:240-243)."""
+        torch = _torch()
+        cnt = torch.bincount(self.vdst[: self.nvec].to(torch.int64) & 0xFFFFFFFF, minlength=self.n)
+        off = torch.zeros(self.n + 1, dtype=torch.int64, device=self.vdst.device)
+        off[1:] = torch.cumsum(cnt, 0)
+        return off.to(torch.int32)
+
+    @classmethod
+    def from_lanes(cls, n: int, width: int, edges: int, nvec: int, vsrc, vw, voff, scratch=None,
+                   stream=None) -> "DeviceGraph":
+        """Rebuild a layout from its lanes and per-destination vector offsets
+        (device tensors): vdst by wg_expand_destinations, the edge index and
+        out-degrees by wg_build_index.  vsrc needs SLACK vectors of readable
+        slack past nvec*width (TMA tail rounding); so does the vdst made here."""
+        torch = _torch()
+        L = _lib.load()
+        dev = vsrc.device
+        vdst = torch.empty(nvec + SLACK, dtype=torch.int32, device=dev)
+        check(L.wg_expand_destinations(n, _ptr(voff), nvec, _ptr(vdst), _lib.stream_ptr(stream)))
+        idx_off = torch.empty(n + 1, dtype=torch.int64, device=dev)
+        idx_pos = torch.empty(max(edges, 1), dtype=torch.int32, device=dev)
+        outdeg = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        g = cls(n, width, edges, nvec, 0, vsrc, vdst[: max(nvec, 1)], vw, idx_off, idx_pos, outdeg)
+        g.rebuild_derived(voff, scratch, stream)
+        return g
+
+    def rebuild_derived(self, voff, scratch=None, stream=None) -> int:
+        """Recompute vdst, the edge index and the out-degrees in place from
+        vsrc and voff (the arrays keep their addresses, so captured loop
+        graphs stay valid).  Returns the index length."""
+        torch = _torch()
+        L = _lib.load()
+        check(L.wg_expand_destinations(self.n, _ptr(voff), self.nvec, _ptr(self.vdst), _lib.stream_ptr(stream)))
+        need = int(L.wg_index_scratch_bytes(self.nvec * self.width, self.n))
+        if scratch is None or scratch.numel() < need:
+            scratch = torch.empty(need, dtype=torch.uint8, device=self.vsrc.device)
+        ent = ctypes.c_uint64(0)
+        check(L.wg_build_index(ctypes.byref(self.struct()), _ptr(self.idx_off), _ptr(self.idx_pos),
+                               _ptr(self.outdeg), _ptr(scratch), scratch.numel(), ctypes.byref(ent),
+                               _lib.stream_ptr(stream)))
+        entries = int(ent.value)
+        if entries != self.entries:
+            self.entries = entries
+            self.idx_pos = self.idx_pos[: max(entries, 1)] if self.idx_pos.numel() >= entries else self.idx_pos
+            self.lens_are_degrees = entries == self.edges
+            self._struct = None
+        return entries
+
     def struct(self) -> WgGraph:
         if self._struct is None:
             self._struct = WgGraph(self.n, self.width, self.nvec, self.edges, self.entries,

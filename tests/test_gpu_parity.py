@@ -65,6 +65,32 @@ def test_device_layout_edge_cases(wg):
     assert np.array_equal(wg.build_edge_index(t).positions, ri.positions)
 
 
+def test_layout_rebuilt_from_lanes(wg, golden):
+    """wg_expand_destinations + wg_build_index (the e2e upload form: lanes and
+    per-destination vector offsets only) reproduce vec_dst, the edge index
+    and the out-degrees of the full builder, duplicates included."""
+    import torch
+    from paper_1903_07754_b200 import device as dv
+    z = golden.npz("layout")
+    cases = [(c["n"], z[f"{c['name']}/src"], z[f"{c['name']}/dst"], c["width"]) for c in golden.meta("layout")]
+    cases.append((3, [0, 0, 1, 1, 2, 2, 2], [1, 1, 1, 2, 2, 0, 0], 2))
+    el = wg.drop_self_loops_dedup(wg.generate(wg.GenSpec("rmat", scale=12, edge_factor=8, seed=3)), True)
+    cases.append((el.vertex_count, el.src, el.dst, 4))
+    for n, src, dst, width in cases:
+        g = _graph(wg, n, src, dst, None, width).device
+        if g.nvec == 0:
+            continue
+        vs = torch.empty(g.vsrc.numel() + 64, dtype=torch.int32, device="cuda")[: g.vsrc.numel()]
+        vs.copy_(g.vsrc)
+        g2 = dv.DeviceGraph.from_lanes(g.n, g.width, g.edges, g.nvec, vs, None, g.vector_offsets())
+        assert g2.entries == g.entries
+        assert np.array_equal(g2.vec_dst_np(), g.vec_dst_np())
+        assert np.array_equal(g2.offsets_np(), g.offsets_np())
+        assert np.array_equal(g2.positions_np(), g.positions_np())
+        assert np.array_equal(g2.outdeg_np(), g.outdeg_np())
+        assert g2.lens_are_degrees == g.lens_are_degrees
+
+
 # ------------------------------------------------- backend protocol (Tier 1)
 @pytest.mark.parametrize("kind", ["pull_full", "pull_wedge", "transform"])
 def test_backend_protocol_bit_exact(wg, golden, kind):
