@@ -54,6 +54,9 @@ class _UploadCache:
 
 class B200Backend:
     name = "b200"
+    # run_until_convergence: time each iteration's kernels with CUDA events
+    # (one iteration per launch) instead of one whole-loop graph launch
+    per_iteration_timing = False
 
     def __init__(self):
         self._cache = _UploadCache()

@@ -313,6 +313,12 @@ def device_run(be, topology, index, program: ApplicationProgram, degrees, config
         start.record()
         p = loop.seed(dinit, words, kern, config.threshold.fraction,
                       first_hit=dv.first_hit_ok(kern, init, members))
+        timer = None
+        if getattr(be, "per_iteration_timing", False):
+            # CUDA events around each launch group (one iteration per launch)
+            from ._lib import EventTimer
+            timer = EventTimer(8 * min(config.max_iterations, 4096) + 64)
+            p.timer = timer.handle
         try:
             recs, converged, last = loop.drive(p, config.max_iterations, trace)
         except OverflowError32:
@@ -330,9 +336,16 @@ def device_run(be, topology, index, program: ApplicationProgram, degrees, config
     ms = start.elapsed_time(stop)
     values = dv.values_to_int64(loop.values_after(last), val_type)
     per = (ms / 1000.0) / max(len(recs), 1)
+    split = {}
+    if timer is not None:
+        for kind, it, t in timer.read():
+            d = split.setdefault(it, [0.0, 0.0])
+            d[0 if kind == 1 else 1] += t / 1000.0  # kind 1: transform; 2-4: pull + end of iteration
     stats = []
     for r in recs:
-        st = IterationStats(r.mode, per, r.vectors_touched, r.frontier_out_size, iteration=r.iteration,
+        tt, pt = split.get(r.iteration, (0.0, per))
+        st = IterationStats(r.mode, pt, r.vectors_touched, r.frontier_out_size, iteration=r.iteration,
+                            transform_time=tt if r.mode == MODE_WEDGE else 0.0,
                             active_edges=r.active_edges,
                             active_edge_fraction=Fraction(r.active_edges, total),
                             covered_vectors=r.covered_vectors, transform_entries=r.transform_entries)

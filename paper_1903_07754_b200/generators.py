@@ -6,7 +6,10 @@ bit for bit (numpy PCG64 stepped on the GPU with jump-ahead, graph_io.py:
 device radix sort + unique; ``synthesize_weights`` is the reference's
 multiplicative hash (graph_io.py:205-221).  ``grid_edges`` builds BASELINE
 config 3's road-like grid, for which the reference has no generator.
-Text ingest (parse_edge_list) stays with the reference.
+Edge-list ingest: the reference's text format (parse_edge_list /
+serialize_edge_list, graph_io.py:34-84) for the CLI, and a binary ``.npz``
+form (src, dst[, weight], vertex_count) that loads without parsing
+(SURVEY §8(f) row 4).
 """
 
 from __future__ import annotations
@@ -135,3 +138,90 @@ def synthesize_weights(edges: EdgeList, max_weight: int) -> EdgeList:
 def grid_graph(rows: int, cols: int, seed: int, keep: float = 0.9, max_weight: int = 1000) -> EdgeList:
     n, s, d, w = dv.grid_edges(rows, cols, seed, keep, max_weight)
     return EdgeList.from_device(n, s, d, w)
+
+
+# ---------------------------------------------------------------------------
+# Ingest (graph_io.py:34-84) and the binary form
+# ---------------------------------------------------------------------------
+class ParseError(ValueError):
+    """Malformed edge-list input, with the offending line number in the message."""
+
+
+def parse_edge_list(text: str) -> EdgeList:
+    """graph_io.py:34-73: ``src dst [weight]`` per line; ``#``/``%`` comments;
+    the first ``# vertices N`` header sets the vertex count (else 1 + max id);
+    mixed weighted/unweighted lines, negative ids, non-integer tokens and
+    weights < 1 are rejected with the line number."""
+    srcs, dsts, wts = [], [], []
+    weighted = None
+    header_n = None
+    for lineno, raw in enumerate(text.splitlines(), start=1):
+        line = raw.strip()
+        if not line:
+            continue
+        if line[0] in "#%":
+            tok = line[1:].split()
+            if header_n is None and len(tok) == 2 and tok[0] == "vertices" and tok[1].isdigit():
+                header_n = int(tok[1])
+            continue
+        tok = line.split()
+        if len(tok) not in (2, 3):
+            raise ParseError(f"line {lineno}: expected 2 or 3 fields, got {len(tok)}")
+        try:
+            f = [int(t) for t in tok]
+        except ValueError:
+            raise ParseError(f"line {lineno}: non-integer token") from None
+        if f[0] < 0 or f[1] < 0:
+            raise ParseError(f"line {lineno}: negative vertex id")
+        has_w = len(f) == 3
+        if weighted is None:
+            weighted = has_w
+        elif weighted != has_w:
+            raise ParseError(f"line {lineno}: mixed weighted and unweighted edges")
+        if has_w and f[2] < 1:
+            raise ParseError(f"line {lineno}: weight must be positive")
+        srcs.append(f[0])
+        dsts.append(f[1])
+        if has_w:
+            wts.append(f[2])
+    implied = 1 + max(max(srcs, default=-1), max(dsts, default=-1))
+    n = header_n if header_n is not None else implied
+    return EdgeList(n, srcs, dsts, wts if weighted else None)
+
+
+def serialize_edge_list(edges: EdgeList) -> str:
+    """graph_io.py:76-84: inverse of parse_edge_list; a vertex header only
+    when the count is not implied by the ids."""
+    src, dst = np.asarray(edges.src, np.int64), np.asarray(edges.dst, np.int64)
+    lines = []
+    implied = 1 + int(max(src.max(initial=-1), dst.max(initial=-1)))
+    if edges.vertex_count != implied:
+        lines.append(f"# vertices {edges.vertex_count}")
+    cols = [src, dst] + ([np.asarray(edges.weight, np.int64)] if edges.weight is not None else [])
+    body = np.stack(cols, 1) if src.size else np.empty((0, len(cols)), np.int64)
+    lines.extend(" ".join(map(str, row)) for row in body.tolist())
+    return "".join(line + "\n" for line in lines)
+
+
+def save_edge_list_binary(edges: EdgeList, path) -> None:
+    """Binary edge list (.npz: vertex_count, src, dst[, weight] as uint32)."""
+    arrs = {"vertex_count": np.array([edges.vertex_count], np.int64),
+            "src": np.asarray(edges.src, np.int64).astype(np.uint32),
+            "dst": np.asarray(edges.dst, np.int64).astype(np.uint32)}
+    if edges.weight is not None:
+        arrs["weight"] = np.asarray(edges.weight, np.int64).astype(np.uint32)
+    with open(path, "wb") as fh:
+        np.savez(fh, **arrs)
+
+
+def load_edge_list(path) -> EdgeList:
+    """Edge list from a file: ``.npz`` binary form (no parsing), else the
+    reference text format."""
+    path = str(path)
+    if path.endswith(".npz"):
+        with np.load(path) as z:
+            n = int(z["vertex_count"][0])
+            w = z["weight"].astype(np.int64) if "weight" in z.files else None
+            return EdgeList(n, z["src"].astype(np.int64), z["dst"].astype(np.int64), w)
+    with open(path, "r", encoding="utf-8") as fh:
+        return parse_edge_list(fh.read())
