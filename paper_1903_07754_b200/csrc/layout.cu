@@ -32,14 +32,31 @@ __global__ void make_dst_keys(uint64_t m, const uint32_t *src, const uint32_t *d
         keys[e] = ((uint64_t)dst[e] << sb) | src[e];
 }
 
-// first[k] / last[k] of each run of equal (key >> shift) in sorted keys.
-__global__ void run_bounds(uint64_t m, const uint64_t *keys, int shift, uint64_t *first,
-                           uint64_t *last) {
-    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m;
-         e += (uint64_t)gridDim.x * blockDim.x) {
-        uint64_t k = keys[e] >> shift;
-        if (e == 0 || (keys[e - 1] >> shift) != k) first[k] = e;
-        if (e == m - 1 || (keys[e + 1] >> shift) != k) last[k] = e;
+// first[k] / last[k] of each run of equal (key >> shift) in sorted keys, 4
+// consecutive keys per thread (independent loads in flight),
+// and an optional flag set when two adjacent keys are equal (a duplicate
+// (src, vector) pair: the index then needs de-duplication).
+__global__ void run_bounds4(uint64_t m, const uint64_t *keys, int shift, uint64_t *first, uint64_t *last,
+                            unsigned *dup) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * 4;
+    for (uint64_t b = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; b < m; b += stride) {
+        uint64_t k[6];
+#pragma unroll
+        for (int i = 0; i < 6; ++i) {
+            const uint64_t e = b + i - 1;  // b-1 .. b+4
+            k[i] = (i == 0 && b == 0) || e >= m ? ~0ull : keys[e];
+        }
+        bool d = false;
+#pragma unroll
+        for (int i = 1; i <= 4; ++i) {
+            const uint64_t e = b + i - 1;
+            if (e >= m) break;
+            const uint64_t r = k[i] >> shift;
+            if (e == 0 || (k[i - 1] >> shift) != r) first[r] = e;
+            if (e == m - 1 || (k[i + 1] >> shift) != r) last[r] = e;
+            d |= e > 0 && k[i - 1] == k[i];
+        }
+        if (dup && d) *dup = 1u;
     }
 }
 
@@ -94,15 +111,13 @@ __global__ void lane_keys(uint64_t lanes, const uint32_t *vsrc, int width, int v
     }
 }
 
-// vdst[v] = d for v in [voff[d], voff[d+1]); a warp per destination run
-// keeps hub runs coalesced
+// vdst[v] = d for v in [voff[d], voff[d+1]): a thread per destination (most
+// runs are one or two vectors; adjacent threads write adjacent vectors)
 __global__ void expand_destinations(uint32_t n, const uint32_t *voff, uint32_t *vdst) {
-    const uint64_t gwarp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    const unsigned lane = threadIdx.x & 31;
-    for (uint64_t d = gwarp; d < n; d += nw) {
+    for (uint64_t d = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; d < n;
+         d += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t a = voff[d], b = voff[d + 1];
-        for (uint32_t v = a + lane; v < b; v += 32) vdst[v] = (uint32_t)d;
+        for (uint32_t v = a; v < b; ++v) vdst[v] = (uint32_t)d;
     }
 }
 
@@ -208,7 +223,7 @@ int wg_build_layout(uint32_t n, uint64_t m, const uint32_t *d_src, const uint32_
 
     // 2. destination runs -> vectors per destination -> first vector per destination
     WG_CUDA(cudaMemsetAsync(ls.first, 0xff, ((uint64_t)n + 1) * 8, s));
-    run_bounds<<<grid_1d(m), 256, 0, s>>>(m, sorted, sb, ls.first, ls.last); ::wg::count_launch();
+    run_bounds4<<<grid_1d(m / 4 + 1), 256, 0, s>>>(m, sorted, sb, ls.first, ls.last, nullptr); ::wg::count_launch();
     run_counts<<<grid_1d(n), 256, 0, s>>>(n, ls.first, ls.last, (int)width, ls.base, nullptr); ::wg::count_launch();
     WG_CHECK_LAUNCH("dst runs");
     WG_CUDA(cudaMemsetAsync(ls.base + n, 0, 8, s));
@@ -237,7 +252,7 @@ int wg_build_layout(uint32_t n, uint64_t m, const uint32_t *d_src, const uint32_
     uint64_t *ialt = ib.Alternate();
     // out-degrees from the pre-dedup source runs (graph.py:277-280)
     WG_CUDA(cudaMemsetAsync(ls.first, 0xff, ((uint64_t)n + 1) * 8, s));
-    run_bounds<<<grid_1d(m), 256, 0, s>>>(m, isorted, vb, ls.first, ls.last); ::wg::count_launch();
+    run_bounds4<<<grid_1d(m / 4 + 1), 256, 0, s>>>(m, isorted, vb, ls.first, ls.last, nullptr); ::wg::count_launch();
     run_counts<<<grid_1d(n), 256, 0, s>>>(n, ls.first, ls.last, 0, ls.base, d_outdeg); ::wg::count_launch();
     WG_CHECK_LAUNCH("src runs");
     // de-duplicate (src, vector) pairs (graph.py:293-297)
@@ -247,7 +262,7 @@ int wg_build_layout(uint32_t n, uint64_t m, const uint32_t *d_src, const uint32_
     WG_CUDA(cudaMemcpyAsync(&entries, ls.count, 8, cudaMemcpyDeviceToHost, s));
     WG_CUDA(cudaStreamSynchronize(s));
     WG_CUDA(cudaMemsetAsync(ls.first, 0xff, ((uint64_t)n + 1) * 8, s));
-    run_bounds<<<grid_1d(entries), 256, 0, s>>>(entries, ialt, vb, ls.first, ls.last); ::wg::count_launch();
+    run_bounds4<<<grid_1d(entries / 4 + 1), 256, 0, s>>>(entries, ialt, vb, ls.first, ls.last, nullptr); ::wg::count_launch();
     run_counts<<<grid_1d(n), 256, 0, s>>>(n, ls.first, ls.last, 0, ls.base, nullptr); ::wg::count_launch();
     WG_CHECK_LAUNCH("index runs");
     WG_CUDA(cudaMemsetAsync(ls.base + n, 0, 8, s));
@@ -307,23 +322,34 @@ int wg_build_index(const wg_graph *g, uint64_t *d_idx_off, uint32_t *d_idx_pos, 
     uint64_t *isorted = ib.Current();
     uint64_t *ialt = ib.Alternate();
     const uint64_t m = g->edges;  // valid lanes; the padding keys follow them
+    unsigned *dup = reinterpret_cast<unsigned *>(count + 1);
     WG_CUDA(cudaMemsetAsync(first, 0xff, ((uint64_t)n + 1) * 8, s));
-    run_bounds<<<grid_1d(m), 256, 0, s>>>(m, isorted, vb, first, last); ::wg::count_launch();
+    WG_CUDA(cudaMemsetAsync(dup, 0, sizeof(unsigned), s));
+    run_bounds4<<<grid_1d(m / 4 + 1), 256, 0, s>>>(m, isorted, vb, first, last, dup); ::wg::count_launch();
     run_counts<<<grid_1d(n), 256, 0, s>>>(n, first, last, 0, base, d_outdeg); ::wg::count_launch();
     WG_CHECK_LAUNCH("src runs");
-    tb = tbytes;
-    WG_CUDA(cub::DeviceSelect::Unique(temp, tb, isorted, ialt, count, (int64_t)m, s));
-    uint64_t entries = 0;
-    WG_CUDA(cudaMemcpyAsync(&entries, count, 8, cudaMemcpyDeviceToHost, s));
+    unsigned h_dup = 0;
+    WG_CUDA(cudaMemcpyAsync(&h_dup, dup, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
     WG_CUDA(cudaStreamSynchronize(s));
-    WG_CUDA(cudaMemsetAsync(first, 0xff, ((uint64_t)n + 1) * 8, s));
-    run_bounds<<<grid_1d(entries), 256, 0, s>>>(entries, ialt, vb, first, last); ::wg::count_launch();
-    run_counts<<<grid_1d(n), 256, 0, s>>>(n, first, last, 0, base, nullptr); ::wg::count_launch();
-    WG_CHECK_LAUNCH("index runs");
+    uint64_t entries = m;
+    if (h_dup) {
+        // parallel edges share a (src, vector) pair: de-duplicate (graph.py:293-297)
+        tb = tbytes;
+        WG_CUDA(cub::DeviceSelect::Unique(temp, tb, isorted, ialt, count, (int64_t)m, s));
+        WG_CUDA(cudaMemcpyAsync(&entries, count, 8, cudaMemcpyDeviceToHost, s));
+        WG_CUDA(cudaStreamSynchronize(s));
+        WG_CUDA(cudaMemsetAsync(first, 0xff, ((uint64_t)n + 1) * 8, s));
+        run_bounds4<<<grid_1d(entries / 4 + 1), 256, 0, s>>>(entries, ialt, vb, first, last, nullptr);
+        ::wg::count_launch();
+        run_counts<<<grid_1d(n), 256, 0, s>>>(n, first, last, 0, base, nullptr); ::wg::count_launch();
+        WG_CHECK_LAUNCH("index runs");
+        isorted = ialt;
+    }
+    // without duplicates the index runs are the source runs: base holds them
     WG_CUDA(cudaMemsetAsync(base + n, 0, 8, s));
     tb = tbytes;
     WG_CUDA(cub::DeviceScan::ExclusiveSum(temp, tb, base, d_idx_off, (int64_t)n + 1, s));
-    unpack_positions<<<grid_1d(entries), 256, 0, s>>>(entries, ialt, vb, d_idx_pos); ::wg::count_launch();
+    unpack_positions<<<grid_1d(entries), 256, 0, s>>>(entries, isorted, vb, d_idx_pos); ::wg::count_launch();
     WG_CHECK_LAUNCH("unpack_positions");
     *h_entries = entries;
     return WG_OK;
