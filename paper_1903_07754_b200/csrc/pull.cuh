@@ -28,6 +28,7 @@
 
 #include "frontier.cuh"
 #include "loop.cuh"
+#include "tma.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -59,15 +60,13 @@ struct PullBufs {
     uint32_t first_hit;  // WG_RUN_FIRST_HIT (filtered pulls only)
 };
 
-constexpr int PULL_THREADS = 256;
+
 #ifndef SPARSE_MINB
 #define SPARSE_MINB 3
 #endif
 #ifndef SPARSE_U
 #define SPARSE_U 2
 #endif
-constexpr int PULL_WARPS = PULL_THREADS / 32;
-constexpr int STAGE = 96;  // per-warp staged frontier entries
 constexpr uint32_t NONE = 0xffffffffu;
 
 template <typename T>
@@ -332,46 +331,6 @@ __device__ __forceinline__ void finish_tile(uint32_t d, T agg, T pd, bool act, b
     if (o.staged > STAGE - 34) flush_stage(o, g, out, overt, opref, otstart, n);
 }
 
-// ---------------------------------------------------------------------------
-// TMA helpers (cp.async.bulk + mbarrier; per-warp pipeline)
-__device__ __forceinline__ uint32_t smem_u32(const void *p) {
-    return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void tma_1d(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-    uint32_t ok = 0;
-    const uint32_t a = smem_u32(bar);
-    while (true) {
-        asm volatile(
-            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
-            : "=r"(ok)
-            : "r"(a), "r"(parity)
-            : "memory");
-        if (ok) break;
-    }
-}
-
-// Range of tiles owned by this warp (contiguous; balanced).
-__device__ __forceinline__ void warp_range(uint64_t ntiles, uint64_t gwarp, uint64_t nwarps,
-                                           uint64_t &t0, uint64_t &t1) {
-    const uint64_t per = ntiles / nwarps, extra = ntiles % nwarps;
-    t0 = gwarp * per + (gwarp < extra ? gwarp : extra);
-    t1 = t0 + per + (gwarp < extra ? 1 : 0);
-}
-
 template <typename T>
 __device__ __forceinline__ void end_of_pull(PullOut &o, wg_iter_rec *out) {
     const uint64_t es = warp_sum(o.edge_sum);
@@ -461,21 +420,6 @@ __global__ void __launch_bounds__(PULL_THREADS) pull_kernel(LoopCtx c, wg_graph 
     end_of_pull<T>(o, out);
 }
 
-// ---------------------------------------------------------------------------
-// Dense unfiltered pull fed by TMA: each warp streams its range through an
-// S-stage ring of CH-tile chunks (vsrc, vdst, vw) in shared memory.
-template <int W, bool WEIGHT, int TMA_CH, int TMA_S>
-struct TmaSmem {
-    static constexpr int VEC = TMA_CH * 32;
-    static constexpr int SRC_WORDS = VEC * W;
-    static constexpr int STAGE_WORDS = SRC_WORDS + VEC + (WEIGHT ? SRC_WORDS : 0);
-    // 128-byte aligned per-warp slice (TMA destinations need 16 B, mbarriers 8 B)
-    static constexpr size_t WARP_BYTES =
-        ((size_t)TMA_S * STAGE_WORDS * 4 + TMA_S * 8 + STAGE * 4 + 127) & ~(size_t)127;
-    static constexpr size_t BLOCK_BYTES = PULL_WARPS * WARP_BYTES;
-};
-
-__device__ __forceinline__ uint32_t pad16(uint32_t b) { return (b + 15u) & ~15u; }
 
 // One dense-pull chunk after its gathers were issued: destinations, segment
 // heads, the raw gathered messages (INF for padding lanes) and prev[d] of
