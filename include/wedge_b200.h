@@ -171,6 +171,10 @@ typedef struct wg_run_bufs {
     wg_iter_rec *recs;      /* [ring] */
     uint64_t *ctrl;         /* [4]: base iteration, ... */
     uint32_t ring;          /* record ring length */
+    uint32_t *gbits_alt;    /* optional second group bitmap [ceil(groups/32)], zero on init, and */
+    uint32_t *glist_alt;    /* group list [groups]: with both, the persistent sparse loop fuses the
+                               transform of iteration k+1 into the pull of k (one barrier per
+                               iteration); without, it runs transform and pull as two phases */
 } wg_run_bufs;
 
 typedef struct wg_run_params {

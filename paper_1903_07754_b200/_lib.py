@@ -45,7 +45,8 @@ REC_U64 = 16  # record size in uint64 words
 class WgRunBufs(ctypes.Structure):
     _fields_ = [("vals", c_vp * 2), ("fbits", c_vp * 2), ("fvert", c_vp * 2), ("fpref", c_vp * 2),
                 ("tstart", c_vp * 2), ("gbits", c_vp), ("glist", c_vp), ("bcount", c_vp), ("recs", c_vp),
-                ("ctrl", c_vp), ("ring", c_u32)]
+                ("ctrl", c_vp), ("ring", c_u32), ("gbits_alt", c_vp),
+                ("glist_alt", c_vp)]
 
 
 class WgRunParams(ctypes.Structure):

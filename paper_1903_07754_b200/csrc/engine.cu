@@ -73,6 +73,8 @@ PullFn pick_pull(int val_type, int width, bool weight, bool filter) {
                                   : pick_pull_t<int64_t>(width, weight, filter);
 }
 
+
+
 // Persistent sparse loop on/off (WG_SPARSE_LOOP=0 disables it).
 bool g_sparse_loop = [] {
     const char *e = getenv("WG_SPARSE_LOOP");
@@ -561,6 +563,8 @@ static PullBufs pull_bufs(const wg_graph *g, const wg_run_bufs *b, const wg_run_
         pb.tstart[i] = b->tstart[i];
     }
     pb.glist = b->glist;
+    pb.gbits2 = b->gbits_alt;  // both set: fused persistent loop
+    pb.glist2 = b->glist_alt;
     pb.bcount = b->bcount;
     pb.ticket = bcount_ticket(g, p->shift, b->bcount);
     pb.n = g->n;
@@ -598,6 +602,7 @@ int wg_run_init(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p,
     WG_CUDA(cudaMemsetAsync(b->fbits[0], 0, words * 4, s));
     WG_CUDA(cudaMemsetAsync(b->fbits[1], 0, words * 4, s));
     WG_CUDA(cudaMemsetAsync(b->gbits, 0, ((groups + 31) >> 5) * 4, s));
+    if (b->gbits_alt) WG_CUDA(cudaMemsetAsync(b->gbits_alt, 0, ((groups + 31) >> 5) * 4, s));
     if (g->n == 0) return WG_OK;
     WG_CUDA(cudaMemsetAsync(bcount_ticket(g, p->shift, b->bcount), 0, sizeof(unsigned), s));
     return launch_frontier_compaction(g, d_init_words, b->bcount, bcount_ticket(g, p->shift, b->bcount),

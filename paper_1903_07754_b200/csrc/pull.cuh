@@ -56,6 +56,7 @@ struct PullBufs {
     uint64_t *bcount;  // compaction scratch (dense-pull frontier build)
     unsigned *ticket;  // its completion ticket
     const uint32_t *glist;
+    uint32_t *gbits2, *glist2;  // second group bitmap / list (fused persistent loop) or null
     uint32_t n;
     uint32_t first_hit;  // WG_RUN_FIRST_HIT (filtered pulls only)
 };
@@ -114,16 +115,89 @@ struct PullOut {
     uint32_t ovf;
 };
 
+// Fused transform of the NEXT iteration (persistent sparse loop): the warp
+// that adds vertices to the produced frontier also maps their edge-index
+// entries to Wedge groups (frontier.py:174-209), into the other group
+// bitmap / list buffer, so iteration it+1 needs no transform phase.
+constexpr uint32_t FUSED_MAX_LEN = 256;  // longer index lists: transform phase next iteration
+
+struct FusedT {
+    uint32_t *gbits;          // group bitmap of iteration it+1 (zero on entry)
+    uint32_t *glist;          // its appended group list
+    wg_iter_rec *rec;         // its record: groups, clipped-last-group flag
+    const uint32_t *idx_pos;
+    int shift;
+    uint64_t ngroups;
+};
+
+// The 32 staged vertices of one flush round own entry ranges [excl, excl+len)
+// of a warp-local prefix; lanes walk the concatenation 32 entries at a time
+// (owner found by a shuffle binary search), so a hub's entries are spread
+// over the warp.
+__device__ __forceinline__ void fused_append(const FusedT &fx, uint64_t off0, uint32_t excl, uint32_t tot) {
+    constexpr int R = 4;  // rounds of 32 entries whose loads / atomics are in flight together
+    const unsigned lane = lane_id();
+    for (uint32_t k0 = 0; k0 < tot; k0 += 32 * R) {
+        uint32_t gid[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const uint32_t k = k0 + r * 32 + lane;
+            int own = 0;
+#pragma unroll
+            for (int step = 16; step; step >>= 1) {
+                const int cand = own + step;
+                const uint32_t e = __shfl_sync(FULL, excl, cand & 31);
+                if (cand < 32 && e <= k) own = cand;
+            }
+            const uint64_t base = __shfl_sync(FULL, off0, own);
+            const uint32_t pre = __shfl_sync(FULL, excl, own);
+            gid[r] = k < tot ? fx.idx_pos[base + (k - pre)] >> fx.shift : NONE;
+        }
+        bool fresh[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            // a source's positions ascend: equal groups are adjacent
+            const uint32_t gprev = __shfl_up_sync(FULL, gid[r], 1);
+            fresh[r] = false;
+            if (gid[r] != NONE && !(lane > 0 && gprev == gid[r])) {
+                const uint32_t bit = 1u << (gid[r] & 31);
+                fresh[r] = !(atomicOr(&fx.gbits[gid[r] >> 5], bit) & bit);
+            }
+        }
+        unsigned fm[R], cnt = 0;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            fm[r] = __ballot_sync(FULL, fresh[r]);
+            cnt += __popc(fm[r]);
+        }
+        if (cnt) {
+            unsigned long long at = 0;
+            if (lane == 0) at = atomicAdd((unsigned long long *)&fx.rec->groups, (unsigned long long)cnt);
+            at = __shfl_sync(FULL, at, 0);
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                if (fresh[r]) {
+                    fx.glist[at + __popc(fm[r] & lanemask_lt())] = gid[r];
+                    if (gid[r] == fx.ngroups - 1) fx.rec->reserved[1] = 1;  // the clipped last group
+                }
+                at += __popc(fm[r]);
+            }
+        }
+    }
+}
+
 __device__ __forceinline__ void flush_stage(PullOut &o, const wg_graph &g, wg_iter_rec *out,
                                             uint32_t *overt, uint32_t *opref, uint32_t *otstart,
-                                            uint32_t n) {
+                                            uint32_t n, const FusedT *fx = nullptr) {
     const unsigned lane = lane_id();
     for (uint32_t base = 0; base < o.staged; base += 32) {
         const bool have = base + lane < o.staged;
         const uint32_t d = have ? o.stage[base + lane] : 0u;
         uint32_t len = 0;
+        uint64_t off0 = 0;
         if (have) {
-            len = (uint32_t)(g.idx_off[d + 1] - g.idx_off[d]);
+            off0 = g.idx_off[d];
+            len = (uint32_t)(g.idx_off[d + 1] - off0);
             o.edge_sum += g.outdeg[d];
         }
         const bool nz = have && len > 0;
@@ -148,6 +222,15 @@ __device__ __forceinline__ void flush_stage(PullOut &o, const wg_graph &g, wg_it
             if (otstart) mark_tile_starts(otstart, pref, len, (uint32_t)pos);
         } else if (have) {
             overt[n - 1 - (zb + __popc(zm & lanemask_lt()))] = d;
+        }
+        if (fx) {
+            // vertices with long index lists are left to a regular transform
+            // phase of the next iteration (one warp would serialise them)
+            const bool big = nz && len > FUSED_MAX_LEN;
+            if (__any_sync(FULL, big) && lane == 0) fx->rec->reserved[3] = 1;
+            const uint32_t flen = (nz && !big) ? len : 0u;
+            const uint32_t fincl = warp_inclusive_sum(flen);
+            fused_append(*fx, off0, fincl - flen, __shfl_sync(FULL, fincl, 31));
         }
     }
     __syncwarp();
@@ -720,7 +803,8 @@ template <typename T, int W, bool WEIGHT, bool FILTER>
 __device__ __forceinline__ void sparse_pull_phase(const LoopCtx &c, uint64_t it, const wg_graph &g,
                                                   const PullBufs &b, int shift, int64_t inc,
                                                   int64_t sentinel, uint32_t *gbits, uint64_t ngroups_all,
-                                                  uint32_t *stage, uint64_t gwarp, uint64_t nwarps) {
+                                                  uint32_t *stage, uint64_t gwarp, uint64_t nwarps,
+                                                  const uint32_t *glist, const FusedT *fx) {
     using VT = ValTraits<T>;
     constexpr int U = SPARSE_U;  // tiles per warp step: independent load chains in flight
     wg_iter_rec *out = ctx_out(c, it);
@@ -754,7 +838,7 @@ __device__ __forceinline__ void sparse_pull_phase(const LoopCtx &c, uint64_t it,
         for (int u = 0; u < U; ++u) {
             const uint64_t gi = (t0 + u) * gpt + (lane >> shift);
             gvalid[u] = gi < nsel;
-            grp[u] = gvalid[u] ? ((volatile const uint32_t *)b.glist)[gi] : 0;
+            grp[u] = gvalid[u] ? ((volatile const uint32_t *)glist)[gi] : 0;
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -802,10 +886,10 @@ __device__ __forceinline__ void sparse_pull_phase(const LoopCtx &c, uint64_t it,
                 if (j == jmask && p[u] + 1 < g.nvec && g.vdst[p[u] + 1] == d[u]) complete = false;
             }
             apply_segments<T>(app, d[u], agg[u], pd[u], complete, INF, inc, nxt, obits, o);
-            if (o.staged > STAGE - 34) flush_stage(o, g, out, overt, opref, otstart, b.n);
+            if (o.staged > STAGE - 34) flush_stage(o, g, out, overt, opref, otstart, b.n, fx);
         }
     }
-    if (o.staged) flush_stage(o, g, out, overt, opref, otstart, b.n);
+    if (o.staged) flush_stage(o, g, out, overt, opref, otstart, b.n, fx);
     end_of_pull<T>(o, out);
 }
 
@@ -819,7 +903,7 @@ __global__ void __launch_bounds__(PULL_THREADS) pull_sparse_kernel(LoopCtx c, wg
     const uint64_t gwarp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     sparse_pull_phase<T, W, WEIGHT, FILTER>(c, it, g, b, shift, inc, sentinel, gbits, ngroups_all,
-                                            s_stage[threadIdx.x >> 5], gwarp, nwarps);
+                                            s_stage[threadIdx.x >> 5], gwarp, nwarps, b.glist, nullptr);
 }
 
 // ---------------- K7: end of iteration -------------------------------------
@@ -925,35 +1009,131 @@ __global__ void __launch_bounds__(PULL_THREADS, SPARSE_MINB) sparse_loop_kernel(
     const uint64_t first = *(volatile uint64_t *)&ctrl[0] + 1;
     uint64_t it = first;
     if (g.entries == 0) return;
+    const bool fused = b.gbits2 != nullptr && b.glist2 != nullptr;
     // iteration `first`'s record was zeroed by whoever finished first-1; the
-    // end-of-iteration work below zeroes one record further ahead
+    // end-of-iteration work below zeroes records further ahead
     if (tid == 0) {
-        uint64_t *q = (uint64_t *)&c.recs[(first + 1) % c.ring];
-        for (int i = 0; i < 16; ++i) q[i] = 0;
+        for (int a = 1; a <= (fused ? 2 : 1); ++a) {
+            uint64_t *q = (uint64_t *)&c.recs[(first + a) % c.ring];
+            for (int i = 0; i < 16; ++i) q[i] = 0;
+        }
     }
     grid.sync();
-    while (ctx_mode(c, it) == MODE_WEDGE) {
-        phase_stamp(it, 0);
-        if (tid == 0) ctx_out(c, it)->reserved[0] = 3;
-        // phase A: transform(it)  ||  end of iteration it-1 (buffer sync, bitmap
-        // clear, record) -- independent: it-1's end writes vals[it&1] and
-        // fbits[it&1], which only the pull of `it` touches, after the barrier
+    if (!fused) {
+        while (ctx_mode(c, it) == MODE_WEDGE) {
+            phase_stamp(it, 0);
+            if (tid == 0) ctx_out(c, it)->reserved[0] = 3;
+            // phase A: transform(it)  ||  end of iteration it-1 (buffer sync, bitmap
+            // clear, record) -- independent: it-1's end writes vals[it&1] and
+            // fbits[it&1], which only the pull of `it` touches, after the barrier
+            transform_phase(c, it, b.fvert[0], b.fvert[1], b.fpref[0], b.fpref[1], b.tstart[0], b.tstart[1],
+                            g.idx_off, g.idx_pos, shift, gbits, 1, const_cast<uint32_t *>(b.glist), ngroups,
+                            tsm, blockIdx.x, gridDim.x);
+            if (it > first) end_of_iteration<T>(c, it - 1, MODE_WEDGE, b, tid, nthreads, 2);
+            grid.sync();
+            phase_stamp(it, 1);
+            // phase B: pull(it)
+            sparse_pull_phase<T, W, WEIGHT, FILTER>(c, it, g, b, shift, inc, sentinel, gbits, ngroups,
+                                                    s_stage[threadIdx.x >> 5], gwarp, nwarps, b.glist, nullptr);
+            grid.sync();
+            phase_stamp(it, 2);
+            phase_stamp(it, 3);
+            ++it;
+        }
+        // the last iteration run here still needs its end-of-iteration work
+        if (it > first) {
+            end_of_iteration<T>(c, it - 1, MODE_WEDGE, b, tid, nthreads, 1);
+            if (tid == 0) *(volatile uint64_t *)&ctrl[0] = it - 1;
+        }
+        return;
+    }
+    // Fused schedule: ONE phase and one barrier per iteration.  The pull of
+    // `it` reads the groups of `it` (slot it) and appends the groups of it+1
+    // into the other slot; the end of iteration it-1 runs in the same phase:
+    // its value sync into vals[it&1] uses atomicMin (a concurrent update by
+    // pull(it) is smaller: values never increase), and it clears the bitmap
+    // of frontier(it-1), which pull(it+1) reuses.  Slot of iteration k:
+    // (k - first) & 1, slot 0 = the run's regular buffers.
+    auto slot_bits = [&](uint64_t k) { return ((k - first) & 1) ? b.gbits2 : gbits; };
+    auto slot_list = [&](uint64_t k) { return ((k - first) & 1) ? b.glist2 : const_cast<uint32_t *>(b.glist); };
+    if (ctx_mode(c, it) == MODE_WEDGE) {
         transform_phase(c, it, b.fvert[0], b.fvert[1], b.fpref[0], b.fpref[1], b.tstart[0], b.tstart[1],
                         g.idx_off, g.idx_pos, shift, gbits, 1, const_cast<uint32_t *>(b.glist), ngroups, tsm,
                         blockIdx.x, gridDim.x);
-        if (it > first) end_of_iteration<T>(c, it - 1, MODE_WEDGE, b, tid, nthreads, 2);
         grid.sync();
+    }
+    while (ctx_mode(c, it) == MODE_WEDGE) {
+        phase_stamp(it, 0);
+        if (tid == 0) {
+            ctx_out(c, it)->reserved[0] = 3;
+            if (it > first)  // the fused transform's entry count (frontier.py:205)
+                ctx_out(c, it)->transform_entries =
+                    *(volatile const uint64_t *)&ctx_in(c, it)->nz_packed & 0xffffffffull;
+        }
+        // end of iteration it-1
+        {
+            const uint64_t ip = it - 1;
+            const wg_iter_rec *pr = ctx_out(c, ip);
+            const uint32_t *list = (ip & 1) ? b.fvert[1] : b.fvert[0];
+            const uint64_t nz = *(volatile const uint64_t *)&pr->nz_packed >> 32;
+            const uint64_t z = *(volatile const uint64_t *)&pr->z_count;
+            const bool nolist = *(volatile const uint64_t *)&pr->reserved[2] != 0;
+            if (it > first && !nolist) {
+                const T *src = (const T *)((ip & 1) ? b.vals[1] : b.vals[0]);
+                T *dst = (T *)((it & 1) ? b.vals[1] : b.vals[0]);
+                for (uint64_t i = tid; i < nz + z; i += nthreads) {
+                    const uint32_t v = i < nz ? list[i] : list[b.n - 1 - (i - nz)];
+                    const T x = *(volatile const T *)&src[v];
+                    if constexpr (ValTraits<T>::U32) atomicMin((unsigned *)&dst[v], (unsigned)x);
+                    else atomicMin((long long *)&dst[v], (long long)x);
+                }
+            }
+            uint32_t *pbits = (ip & 1) ? b.fbits[1] : b.fbits[0];
+            const uint64_t words = ((uint64_t)b.n + 31) >> 5;
+            if (nz + z > words || nolist) {
+                for (uint64_t w = tid; w < words; w += nthreads) pbits[w] = 0;
+            } else {
+                for (uint64_t i = tid; i < nz + z; i += nthreads) {
+                    const uint32_t v = i < nz ? list[i] : list[b.n - 1 - (i - nz)];
+                    pbits[v >> 5] = 0;
+                }
+            }
+            if (tid == 0) {
+                if (it > first) {
+                    wg_iter_rec *po = ctx_out(c, ip);
+                    po->mode = MODE_WEDGE;
+                    po->frontier_out = nz + z;
+                    po->active_edges = *(volatile const uint64_t *)&ctx_in(c, ip)->out_edge_sum;
+                }
+                uint64_t *q = (uint64_t *)&c.recs[(it + 2) % c.ring];
+                for (int i = 0; i < 16; ++i) q[i] = 0;
+            }
+        }
+        // a vertex with a long index list joined frontier(it-1): the groups of
+        // `it` still need the regular (load-balanced) transform
+        if (it > first && *(volatile const uint64_t *)&ctx_out(c, it)->reserved[3]) {
+            transform_phase(c, it, b.fvert[0], b.fvert[1], b.fpref[0], b.fpref[1], b.tstart[0], b.tstart[1],
+                            g.idx_off, g.idx_pos, shift, slot_bits(it), 1, slot_list(it), ngroups, tsm,
+                            blockIdx.x, gridDim.x);
+            grid.sync();
+        }
         phase_stamp(it, 1);
-        // phase B: pull(it)
-        sparse_pull_phase<T, W, WEIGHT, FILTER>(c, it, g, b, shift, inc, sentinel, gbits, ngroups,
-                                                s_stage[threadIdx.x >> 5], gwarp, nwarps);
+        FusedT fx{slot_bits(it + 1), slot_list(it + 1), ctx_out(c, it + 1), g.idx_pos, shift, ngroups};
+        sparse_pull_phase<T, W, WEIGHT, FILTER>(c, it, g, b, shift, inc, sentinel, slot_bits(it), ngroups,
+                                                s_stage[threadIdx.x >> 5], gwarp, nwarps, slot_list(it), &fx);
         grid.sync();
         phase_stamp(it, 2);
         phase_stamp(it, 3);
         ++it;
     }
-    // the last iteration run here still needs its end-of-iteration work
+    // `it` did not run: drop the groups appended for it, then the end of the
+    // last iteration that ran
+    const uint64_t napp = *(volatile const uint64_t *)&ctx_out(c, it)->groups;
+    grid.sync();
     if (it > first) {
+        uint32_t *lb = slot_bits(it);
+        const uint32_t *ll = slot_list(it);
+        for (uint64_t i = tid; i < napp; i += nthreads) lb[ll[i] >> 5] = 0;
         end_of_iteration<T>(c, it - 1, MODE_WEDGE, b, tid, nthreads, 1);
         if (tid == 0) *(volatile uint64_t *)&ctrl[0] = it - 1;
     }

@@ -378,6 +378,23 @@ def wedge_limit(threshold: Fraction, edges: int) -> int:
     return -((-num * edges) // den)
 
 
+FUSED_MAX_LEN = 256  # pull.cuh FUSED_MAX_LEN
+
+
+def fused_transform_pays(g: DeviceGraph) -> bool:
+    """Fuse the Wedge transform into the persistent loop's pull when no
+    vertex has more than FUSED_MAX_LEN out-edges (measured: grid SSSP 635 ->
+    505 ms; RMAT s26 BFS 11.2 -> 11.8 ms, so power-law graphs keep two phases).
+    WG_FUSED_LOOP=0/1 forces it."""
+    import os
+    env = os.environ.get("WG_FUSED_LOOP")
+    if env:
+        return env != "0"
+    if g.n == 0:
+        return False
+    return int(g.outdeg[: g.n].max().item()) <= FUSED_MAX_LEN
+
+
 class DeviceLoop:
     """Buffers and host driver of the device loop for one graph / precision.
 
@@ -386,7 +403,8 @@ class DeviceLoop:
     record, so the host only reads the records after each batch.
     """
 
-    def __init__(self, g: DeviceGraph, shift: int, val_type: int = WG_VAL_U32, ring: int = 1024):
+    def __init__(self, g: DeviceGraph, shift: int, val_type: int = WG_VAL_U32, ring: int = 1024,
+                 fused: Optional[bool] = None):
         torch = _torch()
         self.g, self.shift, self.val_type, self.ring = g, int(shift), int(val_type), int(ring)
         L = _lib.load()
@@ -403,6 +421,13 @@ class DeviceLoop:
         self.tstart = [torch.zeros(max(ntst, 1), dtype=torch.int32, device=dev) for _ in range(2)]
         self.gbits = torch.zeros(max(gwords, 1), dtype=torch.int32, device=dev)
         self.glist = torch.empty(max(groups, 1), dtype=torch.int32, device=dev)
+        # second group buffers: the persistent sparse loop fuses the next
+        # iteration's transform into the pull (wg_run_bufs.gbits_alt) on
+        # graphs without long index lists (meshes, road-like graphs); with
+        # hubs the separate load-balanced transform phase is faster
+        self.fused = fused_transform_pays(g) if fused is None else bool(fused)
+        self.gbits_alt = torch.zeros(max(gwords, 1), dtype=torch.int32, device=dev) if self.fused else None
+        self.glist_alt = torch.empty(max(groups, 1), dtype=torch.int32, device=dev) if self.fused else None
         self.bcount = torch.empty(max(nbc, 1), dtype=torch.int64, device=dev)
         self.recs = torch.zeros(self.ring * REC_U64, dtype=torch.int64, device=dev)
         self.ctrl = torch.zeros(4, dtype=torch.int64, device=dev)
@@ -415,6 +440,7 @@ class DeviceLoop:
             b.fpref[i] = _ptr(self.fpref[i])
             b.tstart[i] = _ptr(self.tstart[i])
         b.gbits, b.glist, b.bcount = _ptr(self.gbits), _ptr(self.glist), _ptr(self.bcount)
+        b.gbits_alt, b.glist_alt = _ptr(self.gbits_alt), _ptr(self.glist_alt)
         b.recs, b.ctrl, b.ring = _ptr(self.recs), _ptr(self.ctrl), self.ring
         self.bufs = b
         self.graph_cache = {}

@@ -61,3 +61,36 @@ def test_paths_agree_and_certify(app, scale, sym):
     assert all(outs[0][1] == o[1] for o in outs[1:])
     assert any(m == "FullScan" for m, *_ in outs[0][1])  # the TMA dense path ran
     assert _certificate(el, outs[0][0], app) == (0, 0)
+
+
+@pytest.mark.parametrize("kind", ["grid", "rmat"])
+def test_fused_persistent_loop_matches(kind):
+    """The persistent sparse loop with the transform fused into the pull
+    (double-buffered groups; long index lists fall back to a transform phase)
+    gives the same values and per-iteration records as the two-phase loop and
+    the per-iteration launches."""
+    import paper_1903_07754_b200 as wg
+    from paper_1903_07754_b200 import _lib, device as dv
+    if kind == "grid":
+        el = wg.grid_graph(256, 256, 5, 0.9, 1000)
+    else:
+        el = wg.synthesize_weights(wg.drop_self_loops_dedup(
+            wg.generate(wg.GenSpec("rmat", scale=16, edge_factor=16, seed=2)), False), 255)
+    g = wg.build_pull_topology(el, 4).device
+    prog = wg.make_program("sssp", 0)
+    init = dv.encode_values(prog.initial_values(g.n), _lib.WG_VAL_U32)
+    words = dv.initial_words(g.n, np.array([0]))
+    outs = []
+    for fused, graph in ((True, True), (False, True), (False, False)):
+        loop = dv.DeviceLoop(g, 2, _lib.WG_VAL_U32, fused=fused)
+        p = loop.seed(init, words, prog.kernel, Fraction(1, 5))
+        recs, conv, last = loop.drive(p, g.n + 16, graph=graph)
+        assert conv
+        outs.append((dv.values_to_int64(loop.values_after(last), _lib.WG_VAL_U32),
+                     [(r.mode, r.active_edges, r.frontier_out_size, r.vectors_touched, r.covered_vectors,
+                       r.transform_entries) for r in recs]))
+    assert len(outs[0][1]) > (20 if kind == "grid" else 5)
+    for o in outs[1:]:
+        assert np.array_equal(outs[0][0], o[0])
+        assert outs[0][1] == o[1]
+    assert _certificate(el, outs[0][0], "sssp") == (0, 0)
