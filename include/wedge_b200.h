@@ -184,6 +184,8 @@ typedef struct wg_run_params {
     uint64_t wedge_limit;   /* wedge iff E>0 and edge_sum < wedge_limit (= ceil(num*E/den)) */
     void *timer;            /* optional wg_timer*: CUDA events around each launch group */
     int32_t flags;          /* WG_RUN_* */
+    int64_t level_base;     /* WG_RUN_FIRST_HIT: the common value of the initial frontier (the
+                               members of frontier k then all hold level_base + k*increment) */
 } wg_run_params;
 
 /* The caller asserts level-synchronous values (a filtered, unweighted kernel
@@ -194,6 +196,9 @@ typedef struct wg_run_params {
  * vectors (bottom-up early exit).  Results and counters
  * are unchanged. */
 #define WG_RUN_FIRST_HIT 1
+/* (With WG_RUN_FIRST_HIT, dense pulls after the first iteration are
+ * bottom-up: an unvisited destination tests its sources against the
+ * previous frontier's bitmap instead of gathering their values.) */
 /* Build every produced frontier's member list (traces, exchange).  Without
  * it a dense pull whose frontier gates the next iteration to FullScan skips
  * the list (nothing consumes it; its record has reserved[2] = 1). */

@@ -51,7 +51,7 @@ class WgRunBufs(ctypes.Structure):
 
 class WgRunParams(ctypes.Structure):
     _fields_ = [("val_type", c_i32), ("shift", c_i32), ("kern", WgMinPlus), ("wedge_limit", c_u64),
-                ("timer", c_vp), ("flags", c_i32)]
+                ("timer", c_vp), ("flags", c_i32), ("level_base", c_i64)]
 
 
 WG_RUN_FIRST_HIT = 1

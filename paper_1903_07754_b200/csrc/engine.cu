@@ -342,11 +342,6 @@ int launch_pull(const LoopCtx &c, const wg_graph *g, const PullBufs &pb, int val
     return WG_OK;
 }
 
-int read_rec(const wg_iter_rec *d_rec, wg_iter_rec *h, cudaStream_t s) {
-    WG_CUDA(cudaMemcpyAsync(h, d_rec, sizeof(wg_iter_rec), cudaMemcpyDeviceToHost, s));
-    WG_CUDA(cudaStreamSynchronize(s));
-    return WG_OK;
-}
 
 }  // namespace
 
@@ -569,6 +564,7 @@ static PullBufs pull_bufs(const wg_graph *g, const wg_run_bufs *b, const wg_run_
     pb.ticket = bcount_ticket(g, p->shift, b->bcount);
     pb.n = g->n;
     pb.first_hit = (p->flags & WG_RUN_FIRST_HIT) && p->kern.filter_unvisited && !p->kern.use_weight ? 1u : 0u;
+    pb.level_base = p->level_base;
     return pb;
 }
 

@@ -59,6 +59,7 @@ struct PullBufs {
     uint32_t *gbits2, *glist2;  // second group bitmap / list (fused persistent loop) or null
     uint32_t n;
     uint32_t first_hit;  // WG_RUN_FIRST_HIT (filtered pulls only)
+    int64_t level_base;  // its frontier-0 value
 };
 
 
@@ -576,13 +577,17 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) pull_dense_tma_kernel(Loop
     const T *__restrict__ prev = (const T *)(((it - 1) & 1) ? b.vals[1] : b.vals[0]);
     T *__restrict__ nxt = (T *)((it & 1) ? b.vals[1] : b.vals[0]);
     uint32_t *__restrict__ obits = ((it & 1) ? b.fbits[1] : b.fbits[0]);
-    uint32_t *__restrict__ overt = ((it & 1) ? b.fvert[1] : b.fvert[0]);
-    uint32_t *__restrict__ opref = ((it & 1) ? b.fpref[1] : b.fpref[0]);
-    uint32_t *otstart = ((it & 1) ? b.tstart[1] : b.tstart[0]);
     const uint32_t nvec = (uint32_t)g.nvec;
     const T INF = VT::inf(sentinel);
     const unsigned lane = lane_id();
     const unsigned wib = threadIdx.x >> 5;
+    // bottom-up BFS (level-synchronous runs, WG_RUN_FIRST_HIT): every finite
+    // in-neighbour of an unvisited destination is in frontier(it-1) and holds
+    // level = base + (it-1)*inc, so its frontier bit replaces the value gather.
+    // Frontier 0 lives in the caller's initial words, hence it > 1.
+    const bool bottom_up = FILTER && b.first_hit && it > 1;
+    const uint32_t *__restrict__ inbits = (((it - 1) & 1) ? b.fbits[1] : b.fbits[0]);
+    const T level = (T)(b.level_base + (int64_t)(it - 1) * inc);
     const uint64_t gwarp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     const unsigned le = 0xffffffffu >> (31 - lane);
@@ -645,8 +650,13 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) pull_dense_tma_kernel(Loop
                     pull = unv && k.d[u] != hit_d;
                 }
 #pragma unroll
-                for (int l = 0; l < W; ++l)
-                    k.ps[u][l] = (pull && k.src[u][l] != WG_NO_LANE) ? prev[k.src[u][l]] : INF;
+                for (int l = 0; l < W; ++l) {
+                    const bool take = pull && k.src[u][l] != WG_NO_LANE;
+                    if (FILTER && bottom_up)  // the source's frontier word (8 MB at s26, L2-resident)
+                        k.ps[u][l] = take ? (T)inbits[k.src[u][l] >> 5] : (T)0;
+                    else
+                        k.ps[u][l] = take ? prev[k.src[u][l]] : INF;
+                }
             }
         };
         // destinations, lanes and segment heads of a chunk from shared memory;
@@ -697,7 +707,18 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) pull_dense_tma_kernel(Loop
             const uint32_t tbase = tfirst + ch * CH;
             T agg[CH];
 #pragma unroll
-            for (int u = 0; u < CH; ++u) agg[u] = fold_gathered<T, W, WEIGHT>(k.ps[u], k.wt[u], INF, o.ovf);
+            for (int u = 0; u < CH; ++u) {
+                if (FILTER && bottom_up) {
+                    // a source in the previous frontier holds exactly `level`
+                    bool any = false;
+#pragma unroll
+                    for (int l = 0; l < W; ++l)
+                        any |= k.src[u][l] != WG_NO_LANE && ((uint32_t)k.ps[u][l] >> (k.src[u][l] & 31)) & 1u;
+                    agg[u] = any ? level : INF;
+                } else {
+                    agg[u] = fold_gathered<T, W, WEIGHT>(k.ps[u], k.wt[u], INF, o.ovf);
+                }
+            }
             // segmented min-scans, interleaved across tiles (none depends on
             // the carry: the carried segment only ever joins a tile's HEAD
             // segment, whose tail lane takes the carried minimum below)

@@ -444,6 +444,7 @@ class DeviceLoop:
         b.recs, b.ctrl, b.ring = _ptr(self.recs), _ptr(self.ctrl), self.ring
         self.bufs = b
         self.graph_cache = {}
+        self._level_base = 0
 
     def params(self, kern, threshold: Fraction, first_hit: bool = False) -> WgRunParams:
         p = WgRunParams()
@@ -452,13 +453,17 @@ class DeviceLoop:
         p.kern = _minplus(kern, UNREACHED)
         p.wedge_limit = wedge_limit(threshold, self.g.edges) if self.g.edges > 0 else 0
         p.flags = _lib.WG_RUN_FIRST_HIT if first_hit else 0
+        p.level_base = int(self._level_base) if first_hit else 0
         return p
 
-    def seed(self, init_values, init_words, kern, threshold, stream=None, first_hit: bool = False) -> WgRunParams:
+    def seed(self, init_values, init_words, kern, threshold, stream=None, first_hit: bool = False,
+             level_base: int = 0) -> WgRunParams:
         """Write both value buffers and build iteration 0 from the frontier bitmap.
-        first_hit: the caller checked first_hit_ok (level-synchronous values)."""
+        first_hit: the caller checked first_hit_ok (level-synchronous values);
+        level_base: then the common value of the initial frontier (first_hit_level)."""
         for v in self.vals:
             v.copy_(init_values)
+        self._level_base = int(level_base)
         p = self.params(kern, threshold, first_hit)
         check(_lib.load().wg_run_init(ctypes.byref(self.g.struct()), ctypes.byref(self.bufs),
                                       ctypes.byref(p), _ptr(init_words), _lib.stream_ptr(stream)))
@@ -484,7 +489,7 @@ class DeviceLoop:
 
     def _graph_for(self, p: WgRunParams, stream=None):
         key = (p.val_type, p.shift, p.kern.filter_unvisited, p.kern.use_weight, p.kern.apply_increment,
-               p.kern.sentinel, p.wedge_limit, p.flags)
+               p.kern.sentinel, p.wedge_limit, p.flags, p.level_base)
         exe = self.graph_cache.get(key)
         if exe is None:
             q = WgRunParams()
@@ -622,6 +627,13 @@ def first_hit_ok(kern, init_values: np.ndarray, members: Optional[np.ndarray]) -
     m = np.asarray(members, dtype=np.int64)
     mem[m[(m >= 0) & (m < v.shape[0])]] = True
     return bool(mem[fin].all())
+
+
+def first_hit_level(init_values: np.ndarray) -> int:
+    """The common finite initial value of a first_hit_ok run (0 if none)."""
+    v = np.asarray(init_values, dtype=np.int64)
+    fin = v[v != UNREACHED]
+    return int(fin[0]) if fin.size else 0
 
 
 def initial_words(n: int, members: np.ndarray):

@@ -311,8 +311,9 @@ def device_run(be, topology, index, program: ApplicationProgram, degrees, config
         dinit = dv.encode_values(init, val_type)
         start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         start.record()
-        p = loop.seed(dinit, words, kern, config.threshold.fraction,
-                      first_hit=dv.first_hit_ok(kern, init, members))
+        fh = dv.first_hit_ok(kern, init, members)
+        p = loop.seed(dinit, words, kern, config.threshold.fraction, first_hit=fh,
+                      level_base=dv.first_hit_level(init) if fh else 0)
         timer = None
         if getattr(be, "per_iteration_timing", False):
             # CUDA events around each launch group (one iteration per launch)

@@ -318,3 +318,31 @@ def test_u32_overflow_falls_back_exactly(wg):
     r = wg.run_until_convergence(t, wg.build_edge_index(t), wg.sssp_program(0), wg.compute_out_degrees(el),
                                  wg.EngineConfig())
     assert r.values.tolist() == [0, 4_000_000_000, 8_000_000_000]
+
+
+def test_bottom_up_levels_follow_the_initial_value(wg):
+    """Level-synchronous runs (WG_RUN_FIRST_HIT) with a non-zero common
+    initial value and several roots: the bottom-up dense pulls must give
+    base + hops, like the oracle's reference loop."""
+    import dataclasses
+    el = wg.drop_self_loops_dedup(wg.generate(wg.GenSpec("rmat", scale=14, edge_factor=16, seed=4)), True)
+    n = el.vertex_count
+    roots = np.array([0, 5, 77])
+    base = 9
+
+    def init(n_):
+        v = np.full(n_, UNREACHED, np.int64)
+        v[roots] = base
+        return v
+    prog = dataclasses.replace(wg.bfs_program(0), initial_value=lambda v: base if v in set(roots) else UNREACHED,
+                               initial_frontier=lambda n_: tuple(roots), initial_values=init)
+    topo = wg.build_pull_topology(el, 4)
+    idx = wg.build_edge_index(topo)
+    deg = wg.compute_out_degrees(el)
+    cfg = wg.EngineConfig(threshold=wg.FullnessThreshold.of("0.01"), precision=wg.FrontierPrecision(8))
+    res = wg.run_until_convergence(topo, idx, prog, deg, cfg)
+    assert any(s.mode == wg.MODE_FULL for s in res.stats[1:])  # a bottom-up dense pull ran
+    tp = oracle.build_pull_topology(n, el.src, el.dst, None, 4)
+    ref = oracle.run_until_convergence(tp, oracle.build_edge_index(tp), oracle.compute_out_degrees(n, el.src),
+                                       oracle.kern_of("bfs"), init(n), roots, Fraction(1, 100), 8)
+    assert np.array_equal(res.values, ref.values)
