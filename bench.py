@@ -447,16 +447,27 @@ def e2e_b200(args, wl, g, loop, dinit, words, kern, thr, max_it, first_hit=False
     from paper_1903_07754_b200 import _lib, device as dv
 
     host = {"vsrc": g.vsrc.cpu().pin_memory(), "voff": g.vector_offsets().cpu().pin_memory()}
-    if g.vw is not None:
+    if g.vw8 is not None:  # weights <= 255 travel as bytes and are widened on the device
+        host["vw8"] = g.vw8[: g.nvec * g.width].cpu().pin_memory()
+    elif g.vw is not None:
         host["vw"] = g.vw.cpu().pin_memory()
     # device buffers with readable slack past the end (TMA tail rounding, wedge_b200.h)
     dev = {k: torch.empty(v.numel() + 64, dtype=v.dtype, device="cuda")[: v.numel()] for k, v in host.items()}
     for k, v in host.items():
         dev[k].copy_(v)
+    if "vw8" in dev:
+        dev["vw"] = torch.empty(g.nvec * g.width + 64, dtype=torch.int32, device="cuda")[: g.nvec * g.width]
+    lanes = g.nvec * g.width
     scratch = torch.empty(int(_lib.load().wg_index_scratch_bytes(g.nvec * g.width, g.n)), dtype=torch.uint8,
                           device="cuda")
+    if "vw8" in dev:
+        _lib.check(_lib.load().wg_widen_weights(lanes, dev["vw8"].data_ptr(), dev["vw"].data_ptr(),
+                                                _lib.stream_ptr()))
     g2 = dv.DeviceGraph.from_lanes(g.n, g.width, g.edges, g.nvec, dev["vsrc"], dev.get("vw"), dev["voff"],
                                    scratch)
+    if "vw8" in dev:
+        g2.vw8 = dev["vw8"]
+        g2._struct = None
     assert g2.entries == g.entries and g2.lens_are_degrees == g.lens_are_degrees
     loop2 = dv.DeviceLoop(g2, loop.shift, loop.val_type)
     out_host = torch.empty(g.n, dtype=torch.int32).pin_memory()
@@ -467,6 +478,9 @@ def e2e_b200(args, wl, g, loop, dinit, words, kern, thr, max_it, first_hit=False
     def one():
         for k, v in host.items():
             dev[k].copy_(v, non_blocking=True)
+        if "vw8" in dev:
+            _lib.check(_lib.load().wg_widen_weights(lanes, dev["vw8"].data_ptr(), dev["vw"].data_ptr(),
+                                                    _lib.stream_ptr()))
         g2.rebuild_derived(dev["voff"], scratch)
         p = loop2.seed(dinit, words, kern, thr, first_hit=first_hit, level_base=level_base)
         recs, conv, last = loop2.drive(p, max_it)
@@ -487,7 +501,7 @@ def e2e_b200(args, wl, g, loop, dinit, words, kern, thr, max_it, first_hit=False
     ms = float(np.mean(ts))
     return {"value": round(g.edges / (ms * 1e-3) / 1e9, 4), "unit": "GTEPS (|E|/time-to-solution)",
             "ms_per_step": round(ms, 3), "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-            "path": "pinned host topology (vsrc[, vw], voff) -> H2D -> wg_expand_destinations + wg_build_index -> device loop -> D2H values"}
+            "path": "pinned host topology (vsrc, voff[, weights as bytes when <= 255]) -> H2D -> wg_widen_weights + wg_expand_destinations + wg_build_index -> device loop -> D2H values"}
 
 
 def host_reference_layout(g):

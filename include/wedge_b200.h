@@ -68,6 +68,9 @@ typedef struct wg_graph {
     const uint32_t *idx_pos; /* [entries] ascending de-duplicated vector positions */
     const uint32_t *outdeg;  /* [n] out-degrees */
     uint32_t flags;          /* WG_GRAPH_* */
+    const uint8_t *vw8;      /* optional [nvec*width] lane weights as bytes (every weight <= 255,
+                                wg_narrow_weights); the dense pull then streams these instead of
+                                vw (16 bytes of readable slack past the end) */
 } wg_graph;
 
 /* Every vertex's edge-index length equals its out-degree (no parallel edges;
@@ -113,6 +116,12 @@ int wg_build_index(const wg_graph *g, uint64_t *d_idx_off, uint32_t *d_idx_pos, 
 /* vec_dst from per-destination vector offsets d_voff [n+1] (the run-length
  * form of PullTopology.vec_dst, graph.py:240-243).  Asynchronous. */
 int wg_expand_destinations(uint32_t n, const uint32_t *d_voff, uint64_t nvec, uint32_t *d_vdst, void *stream);
+
+/* Lane weights as bytes: writes d_vw8 [nvec*width] and sets *h_fits (host) to
+ * 1 iff every weight is <= 255 (else d_vw8 must not be used).  Synchronises. */
+int wg_narrow_weights(const wg_graph *g, uint8_t *d_vw8, int *h_fits, void *stream);
+/* The inverse: vw [lanes] = vw8 (e2e uploads of byte weights). Asynchronous. */
+int wg_widen_weights(uint64_t lanes, const uint8_t *d_vw8, uint32_t *d_vw, void *stream);
 
 /* ---------------- per-call kernels (backend protocol, kernels.py:55-125) --- */
 /* Workspace for wg_transform / wg_pull_wedge / wg_covered_groups. */

@@ -26,7 +26,7 @@ c_u32, c_u64, c_i32, c_i64, c_vp = ctypes.c_uint32, ctypes.c_uint64, ctypes.c_in
 class WgGraph(ctypes.Structure):
     _fields_ = [("n", c_u32), ("width", c_u32), ("nvec", c_u64), ("edges", c_u64),
                 ("entries", c_u64), ("vsrc", c_vp), ("vdst", c_vp), ("vw", c_vp),
-                ("idx_off", c_vp), ("idx_pos", c_vp), ("outdeg", c_vp), ("flags", c_u32)]
+                ("idx_off", c_vp), ("idx_pos", c_vp), ("outdeg", c_vp), ("flags", c_u32), ("vw8", c_vp)]
 
 
 WG_GRAPH_LENS_ARE_DEGREES = 1
@@ -68,6 +68,7 @@ EXPORTS = [
     "wg_exchange_pack", "wg_exchange_apply", "wg_run_graph_create", "wg_run_graph_launch",
     "wg_run_graph_destroy", "wg_run_loop_graph_create", "wg_run_loop_launch", "wg_run_persistent",
     "wg_debug_phase_buffer", "wg_index_scratch_bytes", "wg_build_index", "wg_expand_destinations",
+    "wg_narrow_weights", "wg_widen_weights",
 ]
 
 _LIB = None
@@ -147,6 +148,8 @@ def load(path: os.PathLike | str | None = None):
         "wg_index_scratch_bytes": (ctypes.c_size_t, [c_u64, c_u32]),
         "wg_build_index": (ctypes.c_int, [G, c_vp, c_vp, c_vp, c_vp, ctypes.c_size_t, u64p, c_vp]),
         "wg_expand_destinations": (ctypes.c_int, [c_u32, c_vp, c_u64, c_vp, c_vp]),
+        "wg_narrow_weights": (ctypes.c_int, [G, c_vp, ctypes.POINTER(ctypes.c_int), c_vp]),
+        "wg_widen_weights": (ctypes.c_int, [c_u64, c_vp, c_vp, c_vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -111,6 +111,21 @@ __global__ void lane_keys(uint64_t lanes, const uint32_t *vsrc, int width, int v
     }
 }
 
+__global__ void narrow_weights(uint64_t lanes, const uint32_t *vw, uint8_t *vw8, unsigned *over) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < lanes;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t w = vw[i];
+        vw8[i] = (uint8_t)w;
+        if (w > 255u) *over = 1u;
+    }
+}
+
+__global__ void widen_weights(uint64_t lanes, const uint8_t *vw8, uint32_t *vw) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < lanes;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        vw[i] = vw8[i];
+}
+
 // vdst[v] = d for v in [voff[d], voff[d+1]): a thread per destination (most
 // runs are one or two vectors; adjacent threads write adjacent vectors)
 __global__ void expand_destinations(uint32_t n, const uint32_t *voff, uint32_t *vdst) {
@@ -352,6 +367,36 @@ int wg_build_index(const wg_graph *g, uint64_t *d_idx_off, uint32_t *d_idx_pos, 
     unpack_positions<<<grid_1d(entries), 256, 0, s>>>(entries, isorted, vb, d_idx_pos); ::wg::count_launch();
     WG_CHECK_LAUNCH("unpack_positions");
     *h_entries = entries;
+    return WG_OK;
+}
+
+int wg_narrow_weights(const wg_graph *g, uint8_t *d_vw8, int *h_fits, void *stream) {
+    WG_REQUIRE(g && d_vw8 && h_fits, "null argument");
+    cudaStream_t s = as_stream(stream);
+    const uint64_t lanes = g->nvec * g->width;
+    *h_fits = 0;
+    if (!g->vw) return WG_OK;
+    unsigned *flag = nullptr;
+    WG_CUDA(cudaMallocAsync((void **)&flag, sizeof(unsigned), s));
+    WG_CUDA(cudaMemsetAsync(flag, 0, sizeof(unsigned), s));
+    if (lanes) {
+        narrow_weights<<<grid_1d(lanes), 256, 0, s>>>(lanes, g->vw, d_vw8, flag); ::wg::count_launch();
+        WG_CHECK_LAUNCH("narrow_weights");
+    }
+    unsigned h = 1;
+    WG_CUDA(cudaMemcpyAsync(&h, flag, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+    WG_CUDA(cudaFreeAsync(flag, s));
+    WG_CUDA(cudaStreamSynchronize(s));
+    *h_fits = h ? 0 : 1;
+    return WG_OK;
+}
+
+int wg_widen_weights(uint64_t lanes, const uint8_t *d_vw8, uint32_t *d_vw, void *stream) {
+    WG_REQUIRE((d_vw8 && d_vw) || lanes == 0, "null argument");
+    cudaStream_t s = as_stream(stream);
+    if (lanes == 0) return WG_OK;
+    widen_weights<<<grid_1d(lanes), 256, 0, s>>>(lanes, d_vw8, d_vw); ::wg::count_launch();
+    WG_CHECK_LAUNCH("widen_weights");
     return WG_OK;
 }
 

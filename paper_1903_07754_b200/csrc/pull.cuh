@@ -581,6 +581,7 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) pull_dense_tma_kernel(Loop
     const T INF = VT::inf(sentinel);
     const unsigned lane = lane_id();
     const unsigned wib = threadIdx.x >> 5;
+    const bool w8 = WEIGHT && g.vw8 != nullptr;  // byte weights: a quarter of the weight stream
     // bottom-up BFS (level-synchronous runs, WG_RUN_FIRST_HIT): every finite
     // in-neighbour of an unvisited destination is in frontier(it-1) and holds
     // level = base + (it-1)*inc, so its frontier bit replaces the value gather.
@@ -618,10 +619,14 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) pull_dense_tma_kernel(Loop
             const uint32_t nv = v1 - v0;
             uint32_t *st = ring + (size_t)s * SM::STAGE_WORDS;
             const uint32_t b_src = pad16(nv * W * 4), b_dst = pad16(nv * 4);
-            mbar_expect_tx(&bars[s], b_src + b_dst + (WEIGHT ? b_src : 0));
+            const uint32_t b_w = w8 ? pad16(nv * W) : b_src;
+            mbar_expect_tx(&bars[s], b_src + b_dst + (WEIGHT ? b_w : 0));
             tma_1d(st, g.vsrc + (uint64_t)v0 * W, b_src, &bars[s]);
             tma_1d(st + SM::SRC_WORDS, g.vdst + v0, b_dst, &bars[s]);
-            if (WEIGHT) tma_1d(st + SM::SRC_WORDS + SM::VEC, g.vw + (uint64_t)v0 * W, b_src, &bars[s]);
+            if (WEIGHT) {
+                if (w8) tma_1d(st + SM::SRC_WORDS + SM::VEC, g.vw8 + (uint64_t)v0 * W, b_w, &bars[s]);
+                else tma_1d(st + SM::SRC_WORDS + SM::VEC, g.vw + (uint64_t)v0 * W, b_w, &bars[s]);
+            }
         };
         if (lane == 0)
             for (uint32_t ch = 0; ch < nchunks && ch < (uint32_t)TMA_S; ++ch) issue(ch);
@@ -683,7 +688,9 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) pull_dense_tma_kernel(Loop
 #pragma unroll
                 for (int l = 0; l < W; ++l) {
                     if (!k.valid[u]) k.src[u][l] = WG_NO_LANE;
-                    if constexpr (WEIGHT) k.wt[u][l] = st[SM::SRC_WORDS + SM::VEC + j * W + l];
+                    if constexpr (WEIGHT)
+                        k.wt[u][l] = w8 ? (uint32_t)reinterpret_cast<const uint8_t *>(st + SM::SRC_WORDS + SM::VEC)[j * W + l]
+                                        : st[SM::SRC_WORDS + SM::VEC + j * W + l];
                 }
             }
             // all lanes' generic-proxy reads of this stage precede the async-proxy

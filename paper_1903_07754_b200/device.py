@@ -69,14 +69,29 @@ class DeviceGraph:
     (graph.py:109-212) on the device."""
 
     def __init__(self, n, width, edges, nvec, entries, vsrc, vdst, vw, idx_off, idx_pos, outdeg,
-                 lens_are_degrees: bool = False):
+                 lens_are_degrees: bool = False, vw8=None):
         self.n, self.width, self.edges = int(n), int(width), int(edges)
         self.nvec, self.entries = int(nvec), int(entries)
         self.vsrc, self.vdst, self.vw = vsrc, vdst, vw
         self.idx_off, self.idx_pos, self.outdeg = idx_off, idx_pos, outdeg
         # every index length equals the out-degree (WG_GRAPH_LENS_ARE_DEGREES)
         self.lens_are_degrees = bool(lens_are_degrees)
+        self.vw8 = vw8  # byte copy of vw when every weight <= 255 (the dense pull streams it)
         self._struct = None
+
+    def narrow_weights(self, stream=None) -> bool:
+        """Keep a byte copy of the lane weights when all fit (wg_narrow_weights)."""
+        torch = _torch()
+        if self.vw is None or self.nvec == 0:
+            return False
+        lanes = self.nvec * self.width
+        buf = torch.empty(lanes + 64, dtype=torch.uint8, device=self.vw.device)  # TMA tail slack
+        fits = ctypes.c_int(0)
+        check(_lib.load().wg_narrow_weights(ctypes.byref(self.struct()), _ptr(buf), ctypes.byref(fits),
+                                            _lib.stream_ptr(stream)))
+        self.vw8 = buf if fits.value else None
+        self._struct = None
+        return bool(fits.value)
 
     # -- construction ------------------------------------------------------
     @classmethod
@@ -110,9 +125,12 @@ class DeviceGraph:
         nvec, entries = int(counts[0]), int(counts[1])
         # the built out-degrees count edges and index lengths never exceed
         # them, so equal totals mean equal per vertex
-        return cls(n, width, m, nvec, entries, vsrc[: max(nvec * width, 1)], vdst[: max(nvec, 1)],
-                   vw[: max(nvec * width, 1)] if vw is not None else None, idx_off,
-                   idx_pos[: max(entries, 1)], outdeg, lens_are_degrees=(entries == m))
+        g = cls(n, width, m, nvec, entries, vsrc[: max(nvec * width, 1)], vdst[: max(nvec, 1)],
+                vw[: max(nvec * width, 1)] if vw is not None else None, idx_off,
+                idx_pos[: max(entries, 1)], outdeg, lens_are_degrees=(entries == m))
+        if vw is not None:
+            g.narrow_weights(stream)
+        return g
 
     @classmethod
     def from_reference(cls, topology, index, degrees, device="cuda") -> "DeviceGraph":
@@ -204,7 +222,8 @@ class DeviceGraph:
             self._struct = WgGraph(self.n, self.width, self.nvec, self.edges, self.entries,
                                    _ptr(self.vsrc), _ptr(self.vdst), _ptr(self.vw), _ptr(self.idx_off),
                                    _ptr(self.idx_pos), _ptr(self.outdeg),
-                                   _lib.WG_GRAPH_LENS_ARE_DEGREES if self.lens_are_degrees else 0)
+                                   _lib.WG_GRAPH_LENS_ARE_DEGREES if self.lens_are_degrees else 0,
+                                   _ptr(self.vw8))
         return self._struct
 
     def weighted(self) -> bool:
@@ -239,7 +258,7 @@ class DeviceGraph:
         return u32_to_np64(self.outdeg[: self.n]) if self.n else np.empty(0, np.int64)
 
     def memory_bytes(self) -> int:
-        t = [self.vsrc, self.vdst, self.vw, self.idx_off, self.idx_pos, self.outdeg]
+        t = [self.vsrc, self.vdst, self.vw, self.vw8, self.idx_off, self.idx_pos, self.outdeg]
         return sum(x.numel() * x.element_size() for x in t if x is not None)
 
 
