@@ -347,32 +347,6 @@ __global__ void __launch_bounds__(CB_THREADS) loop_frontier_list_kernel(LoopCtx 
 // skipping repeats (a source's positions ascend, so equal groups are adjacent).
 
 
-// Last index i in [lo, hi) with pref[i] <= e (block-cooperative k-ary search;
-// pref ascending, pref[lo] <= e).  All threads return the same value.
-__device__ __forceinline__ uint64_t block_search(const uint32_t *pref, uint64_t lo, uint64_t hi,
-                                                 uint64_t e, uint64_t *sh) {
-    while (hi - lo > 1) {
-        uint64_t span = hi - lo;
-        uint64_t step = (span + blockDim.x - 1) / blockDim.x;
-        uint64_t probe = lo + threadIdx.x * step;
-        bool ok = probe < hi && pref[probe] <= e;
-        // the largest ok probe
-        unsigned b = __ballot_sync(FULL, ok);
-        if (threadIdx.x == 0) sh[0] = 0;
-        __syncthreads();
-        if ((threadIdx.x & 31) == 0 && b) atomicMax((unsigned long long *)&sh[0],
-                                                    (unsigned long long)(threadIdx.x + 31 - __clz(b)));
-        __syncthreads();
-        uint64_t best = sh[0];
-        __syncthreads();
-        uint64_t nlo = lo + best * step;
-        uint64_t nhi = nlo + step < hi ? nlo + step : hi;
-        lo = nlo;
-        hi = nhi;
-        if (step == 1) break;
-    }
-    return lo;
-}
 
 struct TransformSmem {
     uint32_t pref[TR_TILE + 1];

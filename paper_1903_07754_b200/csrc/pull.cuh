@@ -7,22 +7,24 @@
 // not count their vectors as touched.
 //
 // B200 mapping.  Every warp owns a contiguous range of 32-item tiles (dense:
-// consecutive vectors; wedge: the vectors of the selected groups, ascending)
-// and walks it in order, one vector per lane.  Lanes gather prev[src] for
-// their W lanes and fold them; equal destinations are combined with a single
-// REDUX min over the segment's lane mask (uint32) or a 5-step shuffle scan
-// (int64).  The segment touching lane 31 is CARRIED into the next tile, so a
-// destination is applied once, by one lane, with a plain store -- atomicMin is
-// only needed for the (at most two) segments that cross the ends of a warp's
-// range.  The next-frontier bitmap (one atomicOr per bitmap-word run), the
-// produced member list (staged per warp in shared memory, flushed with one
-// atomic per 32 members), the out-degree sum (the next gate's input) and the
-// work counter are all produced in the same kernel.
+// consecutive vectors; wedge: the vectors of the selected groups) and walks it
+// in order, one vector per lane.  Lanes gather prev[src] for their W lanes and
+// fold them; equal destinations are combined with a shuffle min-scan limited
+// to the longest segment of the tile (a REDUX with per-segment lane masks
+// serialises per mask).  The segment touching lane 31 is CARRIED into the next
+// tile, so a destination is applied once, by one lane, with a plain store --
+// atomicMin only for a run shared with a neighbouring warp's range.  Sparse /
+// Wedge pulls also produce the next-frontier member list (staged per warp in
+// shared memory, one atomic per 32 members), its out-degree sum (the next
+// gate's input) and the work counter in the same kernel; dense pulls set
+// bitmap bits only and the list is built afterwards when a Wedge iteration
+// will consume it.
 //
-// Dense, unfiltered pulls stream the edge layout with TMA bulk copies
-// (cp.async.bulk + mbarrier, a per-warp S-stage ring in shared memory), so the
-// HBM stream runs ahead of the dependent gathers independently of register
-// pressure; wedge / filtered pulls load their vectors directly.
+// Dense pulls stream the edge layout with TMA bulk copies (cp.async.bulk +
+// mbarrier, a per-warp ring in shared memory, tma.cuh) and software-pipeline
+// the gathers across chunks; Wedge pulls load their vectors directly.  The
+// persistent sparse loop runs consecutive sparse Wedge iterations in one
+// cooperative launch (grid barriers between phases).
 #pragma once
 #include <cooperative_groups.h>
 
@@ -82,20 +84,6 @@ __device__ __forceinline__ T shfl_up_t(T v, int off) {
     else return (T)__shfl_up_sync(FULL, (unsigned)v, off);
 }
 
-// Segmented inclusive min-scan keyed by destination (equal destinations are
-// contiguous in a tile): the tail lane of each segment ends with its minimum.
-// (A REDUX with per-segment lane masks serialises per mask, so shuffles win.)
-template <typename T>
-__device__ __forceinline__ T segment_min(T v, uint32_t d) {
-    const unsigned lane = lane_id();
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-        T o = shfl_up_t(v, off);
-        uint32_t od = __shfl_up_sync(FULL, d, off);
-        if ((int)lane >= off && od == d && o < v) v = o;
-    }
-    return v;
-}
 
 // Map work item k to a vector position (or ~0 when out of range).
 __device__ __forceinline__ uint64_t item_pos(uint64_t k, uint64_t nitems, bool wedge,
