@@ -189,11 +189,12 @@ def run_b200(args, wl):
     # BFS is level-synchronous: first-hit early exit in the filtered pulls
     fh = dv.first_hit_ok(kern, init, None if app == "cc" else np.array([root]))
     lvl = dv.first_hit_level(init) if fh else 0
+    ident = dv.identity_values(init)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     stream = torch.cuda.current_stream()
 
     def step(timer=None):
-        p = loop.seed(dinit, words, kern, thr, first_hit=fh, level_base=lvl)
+        p = loop.seed(dinit, words, kern, thr, first_hit=fh, level_base=lvl, identity_init=ident)
         if timer is not None:
             p.timer = timer.handle
         return loop.drive(p, max_it)
@@ -262,7 +263,7 @@ def run_b200(args, wl):
     clocks = clk.summary()
     out["clocks"] = clocks
     if rank == 0 and not args.no_e2e:
-        out["e2e"] = e2e_b200(args, wl, g, loop, dinit, words, kern, thr, max_it, fh, lvl)
+        out["e2e"] = e2e_b200(args, wl, g, loop, dinit, words, kern, thr, max_it, fh, lvl, ident)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(wl, g, prog, thr, max_it, sample_runs=1,
                                            gpu_active=[r.active_edges for r in recs])
@@ -436,7 +437,8 @@ def roofline(rows, recs, n, E, weighted, filt, wl):
             "iterations_timed": len(per_iter)}
 
 
-def e2e_b200(args, wl, g, loop, dinit, words, kern, thr, max_it, first_hit=False, level_base=0):
+def e2e_b200(args, wl, g, loop, dinit, words, kern, thr, max_it, first_hit=False, level_base=0,
+             identity_init=False):
     """Same metric through the C ABI with the graph in pinned HOST memory.
     Per step: H2D of the topology in its compact form (lanes vsrc [+ weights]
     and per-destination vector offsets voff, i.e. PullTopology's lane_src /
@@ -482,7 +484,8 @@ def e2e_b200(args, wl, g, loop, dinit, words, kern, thr, max_it, first_hit=False
             _lib.check(_lib.load().wg_widen_weights(lanes, dev["vw8"].data_ptr(), dev["vw"].data_ptr(),
                                                     _lib.stream_ptr()))
         g2.rebuild_derived(dev["voff"], scratch)
-        p = loop2.seed(dinit, words, kern, thr, first_hit=first_hit, level_base=level_base)
+        p = loop2.seed(dinit, words, kern, thr, first_hit=first_hit, level_base=level_base,
+                       identity_init=identity_init)
         recs, conv, last = loop2.drive(p, max_it)
         out_host.copy_(loop2.values_after(last), non_blocking=True)
         return last

@@ -212,6 +212,11 @@ typedef struct wg_run_params {
  * it a dense pull whose frontier gates the next iteration to FullScan skips
  * the list (nothing consumes it; its record has reserved[2] = 1). */
 #define WG_RUN_KEEP_LISTS 2
+/* The caller asserts that the initial values are the vertex ids (value[v] ==
+ * v, e.g. cc_program): the first iteration's unweighted, unfiltered dense
+ * pull then uses each lane's source id as its message instead of gathering
+ * it.  Results and counters unchanged. */
+#define WG_RUN_IDENTITY_INIT 8
 
 /* Element counts: [0] fbits words, [1] groups, [2] gbits words, [3] bcount
  * entries, [4] tstart entries (the caller multiplies by element sizes). */

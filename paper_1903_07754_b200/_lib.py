@@ -56,6 +56,7 @@ class WgRunParams(ctypes.Structure):
 
 WG_RUN_FIRST_HIT = 1
 WG_RUN_KEEP_LISTS = 2
+WG_RUN_IDENTITY_INIT = 8
 
 
 EXPORTS = [

@@ -565,6 +565,7 @@ static PullBufs pull_bufs(const wg_graph *g, const wg_run_bufs *b, const wg_run_
     pb.n = g->n;
     pb.first_hit = (p->flags & WG_RUN_FIRST_HIT) && p->kern.filter_unvisited && !p->kern.use_weight ? 1u : 0u;
     pb.level_base = p->level_base;
+    pb.ident = (p->flags & WG_RUN_IDENTITY_INIT) ? 1u : 0u;
     return pb;
 }
 

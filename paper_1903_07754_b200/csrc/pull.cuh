@@ -61,6 +61,7 @@ struct PullBufs {
     uint32_t *gbits2, *glist2;  // second group bitmap / list (fused persistent loop) or null
     uint32_t n;
     uint32_t first_hit;  // WG_RUN_FIRST_HIT (filtered pulls only)
+    uint32_t ident;      // WG_RUN_IDENTITY_INIT
     int64_t level_base;  // its frontier-0 value
 };
 
@@ -284,18 +285,20 @@ __device__ __forceinline__ void apply_segments(bool app, uint32_t d, T agg, T pd
 // is needed when the next iteration is dense too (end_of_iteration).  Shared
 // (incomplete) segments use atomicMin, which is exact because values never
 // increase: the stale nxt[d] (two iterations old) is >= prev[d].
+// The value part of a dense apply; returns the next-frontier bit to set (0 if
+// d did not improve).
 template <typename T>
-__device__ __forceinline__ void apply_dense(bool app, uint32_t d, T agg, T pd, bool complete, T INF,
-                                            int64_t inc, T *nxt, uint32_t *obits, uint32_t &ovf) {
+__device__ __forceinline__ uint32_t apply_dense_value(bool app, uint32_t d, T agg, T pd, bool complete, T INF,
+                                                      int64_t inc, T *nxt, uint32_t &ovf) {
     using VT = ValTraits<T>;
-    if (!app) return;
+    if (!app) return 0u;
     T cand = INF;
     if constexpr (VT::U32) {
         if (agg != INF) {
             const uint64_t cc = (uint64_t)agg + (uint64_t)inc;
             if (cc >= 0xffffffffull) {
                 ovf = 1;
-                return;
+                return 0u;
             }
             cand = (T)cc;
         }
@@ -307,8 +310,17 @@ __device__ __forceinline__ void apply_dense(bool app, uint32_t d, T agg, T pd, b
     if (complete) nxt[d] = v;
     else if constexpr (VT::U32) atomicMin((unsigned *)&nxt[d], (unsigned)v);
     else atomicMin((long long *)&nxt[d], (long long)v);
-    if (upd) atomicOr(&obits[d >> 5], 1u << (d & 31));
+    return upd ? 1u << (d & 31) : 0u;
 }
+
+template <typename T>
+__device__ __forceinline__ void apply_dense(bool app, uint32_t d, T agg, T pd, bool complete, T INF,
+                                            int64_t inc, T *nxt, uint32_t *obits, uint32_t &ovf) {
+    const uint32_t bit = apply_dense_value<T>(app, d, agg, pd, complete, INF, inc, nxt, ovf);
+    if (bit) atomicOr(&obits[d >> 5], bit);
+}
+
+
 
 // Fold one vector's lanes into a minimum (messages prev[src] (+ weight)).
 template <typename T, int W, bool WEIGHT>
@@ -575,6 +587,8 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) pull_dense_tma_kernel(Loop
     // level = base + (it-1)*inc, so its frontier bit replaces the value gather.
     // Frontier 0 lives in the caller's initial words, hence it > 1.
     const bool bottom_up = FILTER && b.first_hit && it > 1;
+    // identity initial values: iteration 1's message from src is src itself
+    const bool ident = !FILTER && !WEIGHT && b.ident && it == 1;
     const uint32_t *__restrict__ inbits = (((it - 1) & 1) ? b.fbits[1] : b.fbits[0]);
     const T level = (T)(b.level_base + (int64_t)(it - 1) * inc);
     const uint64_t gwarp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -647,6 +661,8 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) pull_dense_tma_kernel(Loop
                     const bool take = pull && k.src[u][l] != WG_NO_LANE;
                     if (FILTER && bottom_up)  // the source's frontier word (8 MB at s26, L2-resident)
                         k.ps[u][l] = take ? (T)inbits[k.src[u][l] >> 5] : (T)0;
+                    else if (!FILTER && !WEIGHT && ident)
+                        k.ps[u][l] = take ? (T)k.src[u][l] : INF;
                     else
                         k.ps[u][l] = take ? prev[k.src[u][l]] : INF;
                 }

@@ -465,25 +465,26 @@ class DeviceLoop:
         self.graph_cache = {}
         self._level_base = 0
 
-    def params(self, kern, threshold: Fraction, first_hit: bool = False) -> WgRunParams:
+    def params(self, kern, threshold: Fraction, first_hit: bool = False,
+               identity_init: bool = False) -> WgRunParams:
         p = WgRunParams()
         p.val_type = self.val_type
         p.shift = self.shift
         p.kern = _minplus(kern, UNREACHED)
         p.wedge_limit = wedge_limit(threshold, self.g.edges) if self.g.edges > 0 else 0
-        p.flags = _lib.WG_RUN_FIRST_HIT if first_hit else 0
+        p.flags = (_lib.WG_RUN_FIRST_HIT if first_hit else 0) | (_lib.WG_RUN_IDENTITY_INIT if identity_init else 0)
         p.level_base = int(self._level_base) if first_hit else 0
         return p
 
     def seed(self, init_values, init_words, kern, threshold, stream=None, first_hit: bool = False,
-             level_base: int = 0) -> WgRunParams:
+             level_base: int = 0, identity_init: bool = False) -> WgRunParams:
         """Write both value buffers and build iteration 0 from the frontier bitmap.
         first_hit: the caller checked first_hit_ok (level-synchronous values);
         level_base: then the common value of the initial frontier (first_hit_level)."""
         for v in self.vals:
             v.copy_(init_values)
         self._level_base = int(level_base)
-        p = self.params(kern, threshold, first_hit)
+        p = self.params(kern, threshold, first_hit, identity_init)
         check(_lib.load().wg_run_init(ctypes.byref(self.g.struct()), ctypes.byref(self.bufs),
                                       ctypes.byref(p), _ptr(init_words), _lib.stream_ptr(stream)))
         return p
@@ -646,6 +647,12 @@ def first_hit_ok(kern, init_values: np.ndarray, members: Optional[np.ndarray]) -
     m = np.asarray(members, dtype=np.int64)
     mem[m[(m >= 0) & (m < v.shape[0])]] = True
     return bool(mem[fin].all())
+
+
+def identity_values(init_values: np.ndarray) -> bool:
+    """True when the initial values are the vertex ids (WG_RUN_IDENTITY_INIT)."""
+    v = np.asarray(init_values, dtype=np.int64)
+    return bool(np.array_equal(v, np.arange(v.shape[0], dtype=np.int64)))
 
 
 def first_hit_level(init_values: np.ndarray) -> int:

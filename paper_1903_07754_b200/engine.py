@@ -313,7 +313,8 @@ def device_run(be, topology, index, program: ApplicationProgram, degrees, config
         start.record()
         fh = dv.first_hit_ok(kern, init, members)
         p = loop.seed(dinit, words, kern, config.threshold.fraction, first_hit=fh,
-                      level_base=dv.first_hit_level(init) if fh else 0)
+                      level_base=dv.first_hit_level(init) if fh else 0,
+                      identity_init=dv.identity_values(init))
         timer = None
         if getattr(be, "per_iteration_timing", False):
             # CUDA events around each launch group (one iteration per launch)
