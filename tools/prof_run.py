@@ -28,7 +28,8 @@ loop = dv.DeviceLoop(g, shift, _lib.WG_VAL_U32)
 dinit = dv.encode_values(_initial_values(prog, g.n), _lib.WG_VAL_U32)
 words = dv.all_words(g.n) if wl["app"] == "cc" else dv.initial_words(g.n, np.array([0]))
 for _ in range(runs):
-    p = loop.seed(dinit, words, prog.kernel, Fraction(wl["thr"]), first_hit=(wl["app"] == "bfs"))
+    p = loop.seed(dinit, words, prog.kernel, Fraction(wl["thr"]), first_hit=(wl["app"] == "bfs"),
+                  identity_init=(wl["app"] == "cc"))
     recs, conv, last = loop.drive(p, g.n + 16)
 torch.cuda.synchronize()
 print("iterations", len(recs), "converged", conv)
