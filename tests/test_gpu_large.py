@@ -94,3 +94,35 @@ def test_fused_persistent_loop_matches(kind):
         assert np.array_equal(outs[0][0], o[0])
         assert outs[0][1] == o[1]
     assert _certificate(el, outs[0][0], "sssp") == (0, 0)
+
+
+@pytest.mark.parametrize("app", ["bfs", "cc", "sssp"])
+def test_int64_values_match_uint32(app):
+    """The exact int64 value path (WG_VAL_I64) of every kernel the loop uses
+    (dense TMA / bottom-up, Wedge, persistent sparse loop) agrees with the
+    uint32 path on a graph that needs all of them."""
+    import paper_1903_07754_b200 as wg
+    from paper_1903_07754_b200 import _lib, device as dv
+    el = wg.drop_self_loops_dedup(wg.generate(wg.GenSpec("rmat", scale=15, edge_factor=16, seed=7)),
+                                  app == "cc")
+    if app == "sssp":
+        el = wg.synthesize_weights(el, 255)
+    g = wg.build_pull_topology(el, 4).device
+    prog = wg.make_program(app, None if app == "cc" else 0)
+    init = prog.initial_values(g.n)
+    members = None if app == "cc" else np.array([0])
+    words = dv.all_words(g.n) if members is None else dv.initial_words(g.n, members)
+    thr = Fraction(1, 100) if app == "bfs" else Fraction(1, 5)
+    fh = dv.first_hit_ok(prog.kernel, init, members)
+    outs = []
+    for vt in (_lib.WG_VAL_U32, _lib.WG_VAL_I64):
+        loop = dv.DeviceLoop(g, 3 if app == "bfs" else 2, vt)
+        p = loop.seed(dv.encode_values(init, vt), words, prog.kernel, thr, first_hit=fh,
+                      level_base=dv.first_hit_level(init) if fh else 0, identity_init=dv.identity_values(init))
+        recs, conv, last = loop.drive(p, g.n + 16)
+        assert conv
+        outs.append((dv.values_to_int64(loop.values_after(last), vt),
+                     [(r.mode, r.active_edges, r.frontier_out_size, r.vectors_touched) for r in recs]))
+    assert np.array_equal(outs[0][0], outs[1][0])
+    assert outs[0][1] == outs[1][1]
+    assert {m for m, *_ in outs[0][1]} == {"FullScan", "Wedge"}
