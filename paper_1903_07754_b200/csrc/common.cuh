@@ -91,7 +91,9 @@ __device__ __forceinline__ T warp_sum(T v) {
     return v;
 }
 
-// Streaming (read-once) loads: bypass L1, evict-first in L2.
+// Streaming (read-once) loads: bypass L1.  (An L2 evict-first cache hint
+// here measured neutral to slightly negative; the TMA stream of the dense
+// pull uses one, tma.cuh.)
 __device__ __forceinline__ uint32_t ld_stream(const uint32_t *p) {
     uint32_t r;
     asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));

@@ -623,11 +623,12 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) pull_dense_tma_kernel(Loop
             const uint32_t b_src = pad16(nv * W * 4), b_dst = pad16(nv * 4);
             const uint32_t b_w = w8 ? pad16(nv * W) : b_src;
             mbar_expect_tx(&bars[s], b_src + b_dst + (WEIGHT ? b_w : 0));
-            tma_1d(st, g.vsrc + (uint64_t)v0 * W, b_src, &bars[s]);
-            tma_1d(st + SM::SRC_WORDS, g.vdst + v0, b_dst, &bars[s]);
+            const uint64_t pol = l2_evict_first();
+            tma_1d_stream(st, g.vsrc + (uint64_t)v0 * W, b_src, &bars[s], pol);
+            tma_1d_stream(st + SM::SRC_WORDS, g.vdst + v0, b_dst, &bars[s], pol);
             if (WEIGHT) {
-                if (w8) tma_1d(st + SM::SRC_WORDS + SM::VEC, g.vw8 + (uint64_t)v0 * W, b_w, &bars[s]);
-                else tma_1d(st + SM::SRC_WORDS + SM::VEC, g.vw + (uint64_t)v0 * W, b_w, &bars[s]);
+                if (w8) tma_1d_stream(st + SM::SRC_WORDS + SM::VEC, g.vw8 + (uint64_t)v0 * W, b_w, &bars[s], pol);
+                else tma_1d_stream(st + SM::SRC_WORDS + SM::VEC, g.vw + (uint64_t)v0 * W, b_w, &bars[s], pol);
             }
         };
         if (lane == 0)

@@ -29,6 +29,21 @@ __device__ __forceinline__ void tma_1d(void *dst, const void *src, uint32_t byte
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
+// Streamed (read-once) data: an L2 evict-first policy keeps the stream from
+// displacing the gathered value lines.
+__device__ __forceinline__ uint64_t l2_evict_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void tma_1d_stream(void *dst, const void *src, uint32_t bytes, uint64_t *bar,
+                                              uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], "
+        "%4;" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     uint32_t ok = 0;
     const uint32_t a = smem_u32(bar);
