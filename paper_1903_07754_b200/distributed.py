@@ -78,6 +78,33 @@ def all_gather_var(t, group=None):
     return torch.cat([p[:c] for p, c in zip(parts, counts)])
 
 
+def all_gather_pairs(verts, vals, group=None):
+    """All-gather (vertex, value) update lists of different lengths with one
+    count exchange and one padded all-gather: each rank sends its vertices
+    and values as the int32 words of a single buffer."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    k = int(verts.numel())
+    a = verts.element_size() // 4  # int32 words per vertex id
+    b = vals.element_size() // 4   # int32 words per value
+    cnt = torch.tensor([k], dtype=torch.int64, device=verts.device)
+    counts = [torch.zeros_like(cnt) for _ in range(world)]
+    dist.all_gather(counts, cnt, group=group)
+    counts = torch.cat(counts).cpu().tolist()
+    maxc = max(counts)
+    if maxc == 0:
+        return verts[:0], vals[:0]
+    buf = torch.zeros(maxc * (a + b), dtype=torch.int32, device=verts.device)
+    buf[: k * a].copy_(verts.contiguous().view(torch.int32))
+    buf[maxc * a: maxc * a + k * b].copy_(vals.contiguous().view(torch.int32))
+    parts = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(parts, buf, group=group)
+    av = torch.cat([p[: c * a] for p, c in zip(parts, counts)]).view(verts.dtype)
+    ax = torch.cat([p[maxc * a: maxc * a + c * b] for p, c in zip(parts, counts)]).view(vals.dtype)
+    return av, ax
+
+
 @dataclass
 class ShardRecord:
     iteration: int
@@ -90,9 +117,11 @@ class ShardRecord:
     transform_entries: int = 0
 
 
-def run_sharded(shard, max_iterations: int, group=None):
+def run_sharded(shard, max_iterations: int, group=None, values: bool = True):
     """The reference loop (engine.py:330-388) over destination shards:
-    local step, exchange of updated values, global frontier for the gate."""
+    local step, exchange of updated values, global frontier for the gate.
+    values=False skips the host copy of the final values (timed runs; read
+    them afterwards with shard.values_int64())."""
     import torch
     import torch.distributed as dist
     shard.seed()
@@ -102,8 +131,7 @@ def run_sharded(shard, max_iterations: int, group=None):
     while it < max_iterations:
         it += 1
         verts, vals = shard.step(it)
-        all_v = all_gather_var(verts, group)
-        all_x = all_gather_var(vals, group)
+        all_v, all_x = all_gather_pairs(verts, vals, group)
         rec = shard.apply(it, all_v, all_x)
         recs.append(rec)
         if rec.out_edge_sum == 0:
@@ -117,7 +145,7 @@ def run_sharded(shard, max_iterations: int, group=None):
         dist.all_reduce(w, group=group)
         for r, row in zip(recs, w.cpu().tolist()):
             r.vectors_touched, r.covered_vectors, r.transform_entries = row
-    return shard.values_int64(), recs, converged
+    return (shard.values_int64() if values else None), recs, converged
 
 
 # ---------------------------------------------------------------------------
