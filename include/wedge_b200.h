@@ -280,6 +280,20 @@ int wg_exchange_pack(const wg_graph *g, const wg_run_bufs *b, const wg_run_param
                      void *stream);
 int wg_exchange_apply(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p, uint64_t it,
                       const uint32_t *d_verts, const void *d_vals, uint64_t count, void *stream);
+/* Host-sync-free form for fixed-size collectives.  A message is a 16-byte
+ * header (u64 entry count) + (vertex, value) entries of 8 bytes (WG_VAL_U32)
+ * or 16 bytes (WG_VAL_I64); wg_exchange_bytes(k, val_type) is the size of a
+ * message truncated to k entries.  pack_all writes this rank's members of
+ * iteration `it` (up to `capacity`); after an all-gather of equal prefixes
+ * of cap entries, apply_all applies every rank's first min(count, cap)
+ * entries, rebuilds the global frontier and writes the largest count into
+ * *d_status (> cap: gather a longer prefix and apply again -- idempotent). */
+uint64_t wg_exchange_bytes(uint64_t entries, int val_type);
+int wg_exchange_pack_all(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p, uint64_t it,
+                         void *d_buf, uint64_t capacity, void *stream);
+int wg_exchange_apply_all(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p, uint64_t it,
+                          const void *d_parts, uint32_t world, uint64_t cap, uint64_t *d_status,
+                          void *stream);
 
 /* ---------------- measurement --------------------------------------------- */
 /* Event timer: when attached to wg_run_params.timer, wg_run_enqueue records a

@@ -69,7 +69,8 @@ EXPORTS = [
     "wg_exchange_pack", "wg_exchange_apply", "wg_run_graph_create", "wg_run_graph_launch",
     "wg_run_graph_destroy", "wg_run_loop_graph_create", "wg_run_loop_launch", "wg_run_persistent",
     "wg_debug_phase_buffer", "wg_index_scratch_bytes", "wg_build_index", "wg_expand_destinations",
-    "wg_narrow_weights", "wg_widen_weights",
+    "wg_narrow_weights", "wg_widen_weights", "wg_exchange_bytes", "wg_exchange_pack_all",
+    "wg_exchange_apply_all",
 ]
 
 _LIB = None
@@ -151,6 +152,9 @@ def load(path: os.PathLike | str | None = None):
         "wg_expand_destinations": (ctypes.c_int, [c_u32, c_vp, c_u64, c_vp, c_vp]),
         "wg_narrow_weights": (ctypes.c_int, [G, c_vp, ctypes.POINTER(ctypes.c_int), c_vp]),
         "wg_widen_weights": (ctypes.c_int, [c_u64, c_vp, c_vp, c_vp]),
+        "wg_exchange_bytes": (c_u64, [c_u64, ctypes.c_int]),
+        "wg_exchange_pack_all": (ctypes.c_int, [G, B, P, c_u64, c_vp, c_u64, c_vp]),
+        "wg_exchange_apply_all": (ctypes.c_int, [G, B, P, c_u64, c_vp, c_u32, c_u64, c_vp, c_vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -916,9 +916,114 @@ __global__ void exchange_apply_kernel(const uint32_t *verts, const T *in, uint64
     }
 }
 
+// Packed exchange: a rank's buffer is a 16-byte header (u64 entry count)
+// followed by (vertex, value) entries, 8 bytes (u32 values) or 16 bytes
+// (int64 values); any prefix of it is a valid, truncated message.
+template <typename T>
+struct XEntry {
+    uint32_t v;
+    uint32_t pad;
+    T x;
+};
+template <>
+struct XEntry<uint32_t> {
+    uint32_t v;
+    uint32_t x;
+};
+
+template <typename T>
+__global__ void exchange_pack_all_kernel(const wg_iter_rec *rec, const uint32_t *list, uint32_t n, const T *vals,
+                                         unsigned char *buf, uint64_t capacity) {
+    const uint64_t nz = rec->nz_packed >> 32, z = rec->z_count;
+    const uint64_t cnt = nz + z;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *reinterpret_cast<uint64_t *>(buf) = cnt;
+    XEntry<T> *e = reinterpret_cast<XEntry<T> *>(buf + 16);
+    const uint64_t m = cnt < capacity ? cnt : capacity;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t v = i < nz ? list[i] : list[n - 1 - (i - nz)];
+        XEntry<T> t{};
+        t.v = v;
+        t.x = vals[v];
+        e[i] = t;
+    }
+}
+
+// Applies the first min(count, cap) entries of every rank's part; status[0]
+// receives the largest count (> cap: the gather was truncated, redo it).
+template <typename T>
+__global__ void exchange_apply_all_kernel(const unsigned char *parts, uint32_t world, uint64_t cap,
+                                          uint64_t stride, T *v0, T *v1, uint32_t *bits, uint64_t *status) {
+    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+    for (uint32_t r = 0; r < world; ++r) {
+        const unsigned char *pr = parts + (uint64_t)r * stride;
+        const uint64_t cnt = *reinterpret_cast<const uint64_t *>(pr);
+        if (tid == 0) atomicMax((unsigned long long *)status, (unsigned long long)cnt);
+        const uint64_t m = cnt < cap ? cnt : cap;
+        const XEntry<T> *e = reinterpret_cast<const XEntry<T> *>(pr + 16);
+        for (uint64_t i = tid; i < m; i += nth) {
+            const XEntry<T> t = e[i];
+            v0[t.v] = t.x;
+            v1[t.v] = t.x;
+            atomicOr(&bits[t.v >> 5], 1u << (t.v & 31));
+        }
+    }
+}
+
 }  // namespace
 
 extern "C" {
+
+uint64_t wg_exchange_bytes(uint64_t entries, int val_type) {
+    return 16 + entries * (val_type == WG_VAL_U32 ? sizeof(XEntry<uint32_t>) : sizeof(XEntry<int64_t>));
+}
+
+int wg_exchange_pack_all(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p, uint64_t it,
+                         void *d_buf, uint64_t capacity, void *stream) {
+    int rc = check_run(g, b, p);
+    if (rc) return rc;
+    WG_REQUIRE(d_buf, "null argument");
+    cudaStream_t s = as_stream(stream);
+    unsigned grid = grid_for(capacity ? capacity : 1, 256 * 4, 8);
+    const uint32_t *list = b->fvert[it & 1];
+    const wg_iter_rec *rec = &b->recs[it % b->ring];
+    if (p->val_type == WG_VAL_U32)
+        exchange_pack_all_kernel<uint32_t><<<grid, 256, 0, s>>>(rec, list, g->n, (const uint32_t *)b->vals[it & 1],
+                                                                (unsigned char *)d_buf, capacity);
+    else
+        exchange_pack_all_kernel<int64_t><<<grid, 256, 0, s>>>(rec, list, g->n, (const int64_t *)b->vals[it & 1],
+                                                               (unsigned char *)d_buf, capacity);
+    ::wg::count_launch();
+    WG_CHECK_LAUNCH("exchange_pack_all");
+    return WG_OK;
+}
+
+int wg_exchange_apply_all(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p, uint64_t it,
+                          const void *d_parts, uint32_t world, uint64_t cap, uint64_t *d_status,
+                          void *stream) {
+    int rc = check_run(g, b, p);
+    if (rc) return rc;
+    WG_REQUIRE(d_parts && d_status && world >= 1, "null argument");
+    cudaStream_t s = as_stream(stream);
+    uint32_t *bits = b->fbits[it & 1];
+    const uint64_t stride = wg_exchange_bytes(cap, p->val_type);
+    WG_CUDA(cudaMemsetAsync(d_status, 0, sizeof(uint64_t), s));
+    unsigned grid = grid_for(cap ? cap : 1, 256 * 4, 8);
+    if (p->val_type == WG_VAL_U32)
+        exchange_apply_all_kernel<uint32_t><<<grid, 256, 0, s>>>((const unsigned char *)d_parts, world, cap, stride,
+                                                                 (uint32_t *)b->vals[0], (uint32_t *)b->vals[1],
+                                                                 bits, d_status);
+    else
+        exchange_apply_all_kernel<int64_t><<<grid, 256, 0, s>>>((const unsigned char *)d_parts, world, cap, stride,
+                                                                (int64_t *)b->vals[0], (int64_t *)b->vals[1],
+                                                                bits, d_status);
+    ::wg::count_launch();
+    WG_CHECK_LAUNCH("exchange_apply_all");
+    return launch_frontier_compaction(g, bits, b->bcount, bcount_ticket(g, p->shift, b->bcount),
+                                      b->fvert[it & 1], b->fpref[it & 1], b->tstart[it & 1],
+                                      &b->recs[it % b->ring], s);
+}
 
 int wg_exchange_pack(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p, uint64_t it,
                      uint32_t *d_verts, void *d_vals, uint64_t capacity, uint64_t *h_count,

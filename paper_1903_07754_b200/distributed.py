@@ -105,6 +105,9 @@ def all_gather_pairs(verts, vals, group=None):
     return av, ax
 
 
+PACKED_MIN_CAP = 4096  # smallest message capacity (entries) of the packed exchange
+
+
 @dataclass
 class ShardRecord:
     iteration: int
@@ -128,11 +131,23 @@ def run_sharded(shard, max_iterations: int, group=None, values: bool = True):
     recs: list[ShardRecord] = []
     converged = False
     it = 0
+    packed = hasattr(shard, "exchange")
+    cap = getattr(shard, "capacity", 0)
     while it < max_iterations:
         it += 1
-        verts, vals = shard.step(it)
-        all_v, all_x = all_gather_pairs(verts, vals, group)
-        rec = shard.apply(it, all_v, all_x)
+        if packed:
+            # one fixed-size all-gather of truncated messages per iteration;
+            # the largest count (global, so every rank decides alike) sizes
+            # the next one and triggers a full-size redo when exceeded
+            shard.step(it)
+            rec, maxc = shard.exchange(it, cap, group)
+            if maxc > cap:
+                rec, maxc = shard.exchange(it, shard.capacity, group)
+            cap = min(shard.capacity, max(PACKED_MIN_CAP, 2 * maxc))
+        else:
+            verts, vals = shard.step(it)
+            all_v, all_x = all_gather_pairs(verts, vals, group)
+            rec = shard.apply(it, all_v, all_x)
         recs.append(rec)
         if rec.out_edge_sum == 0:
             converged = True
@@ -185,6 +200,16 @@ class DeviceShard:
         self.out_v = torch.empty(cap, dtype=torch.int32, device="cuda")
         self.out_x = torch.empty(cap, dtype=torch.int32 if val_type == _lib.WG_VAL_U32 else torch.int64,
                                  device="cuda")
+        # packed exchange buffers: capacity = the largest shard's destination
+        # count (a rank updates only its own destinations)
+        world = len(bounds) - 1
+        self.capacity = max(bounds[r + 1] - bounds[r] for r in range(world)) if world else 1
+        L = _lib.load()
+        nb = int(L.wg_exchange_bytes(self.capacity, val_type))
+        self.send = torch.zeros(nb, dtype=torch.uint8, device="cuda")
+        self.recv = torch.empty(world * nb, dtype=torch.uint8, device="cuda")
+        self.status = torch.zeros(1, dtype=torch.int64, device="cuda")
+        self.host_status = torch.zeros(1, dtype=torch.int64).pin_memory()
         self.p = None
 
     def seed(self):
@@ -192,6 +217,39 @@ class DeviceShard:
         self.p.flags |= self._lib.WG_RUN_KEEP_LISTS  # wg_exchange_pack reads the member lists
 
     def step(self, it: int):
+        """Local iteration + pack of its members (no host synchronisation)."""
+        L = self._lib.load()
+        self.loop.enqueue(self.p, it, 1)
+        self._lib.check(L.wg_exchange_pack_all(ctypes.byref(self.g.struct()), ctypes.byref(self.loop.bufs),
+                                               ctypes.byref(self.p), it, self.send.data_ptr(), self.capacity,
+                                               self._lib.stream_ptr()))
+
+    def exchange(self, it: int, cap: int, group=None):
+        """All-gather every rank's message truncated to `cap` entries, apply
+        them and rebuild the global frontier; returns (record, largest count)."""
+        import torch.distributed as dist
+        nb = self.message_bytes(cap)
+        world = dist.get_world_size(group)
+        recv = self.recv[: world * nb]
+        dist.all_gather_into_tensor(recv, self.send[:nb], group=group)
+        return self.apply_packed(it, recv, world, cap)
+
+    def message_bytes(self, cap: int) -> int:
+        return int(self._lib.load().wg_exchange_bytes(cap, self.val_type))
+
+    def apply_packed(self, it: int, recv, world: int, cap: int):
+        """Apply gathered messages (world parts of message_bytes(cap) bytes)."""
+        L = self._lib.load()
+        self._lib.check(L.wg_exchange_apply_all(ctypes.byref(self.g.struct()), ctypes.byref(self.loop.bufs),
+                                                ctypes.byref(self.p), it, recv.data_ptr(), world, cap,
+                                                self.status.data_ptr(), self._lib.stream_ptr()))
+        self.host_status.copy_(self.status, non_blocking=True)
+        rec = self._record(it)  # synchronises
+        return rec, int(self.host_status[0])
+
+    def step_pairs(self, it: int):
+        """Variable-size form (wg_exchange_pack): the local iteration and its
+        (vertex, value) pairs, for callers that exchange them themselves."""
         L = self._lib.load()
         self.loop.enqueue(self.p, it, 1)
         cnt = ctypes.c_uint64(0)
@@ -208,6 +266,9 @@ class DeviceShard:
                                             ctypes.byref(self.p), it, verts.data_ptr() if verts.numel() else None,
                                             vals.data_ptr() if vals.numel() else None, int(verts.numel()),
                                             self._lib.stream_ptr()))
+        return self._record(it)
+
+    def _record(self, it: int) -> ShardRecord:
         r = self.loop._read(it, 1)[0]
         if int(r[10]):
             raise self._lib.OverflowError32(self._lib.WG_EOVERFLOW, "uint32 overflow in sharded loop")

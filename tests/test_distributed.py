@@ -79,6 +79,41 @@ class OracleShard:
         return self.prev
 
 
+class PackedOracleShard(OracleShard):
+    """The fixed-size exchange protocol of DeviceShard (step packs; exchange
+    all-gathers messages truncated to `cap` entries and reports the largest
+    count) in numpy, so run_sharded's capacity / redo logic runs on gloo."""
+
+    def __init__(self, *a, **k):
+        super().__init__(*a, **k)
+        b = a[5]  # the bounds argument
+        self.capacity = max(b[r + 1] - b[r] for r in range(len(b) - 1))
+        self.exchanged_caps = []
+
+    def step(self, it):
+        v, x = OracleShard.step(self, it)
+        self.msg = np.zeros(1 + 2 * self.capacity, np.int64)
+        self.msg[0] = v.numel()
+        self.msg[1: 1 + v.numel()] = v.numpy()
+        self.msg[1 + self.capacity: 1 + self.capacity + v.numel()] = x.numpy()
+
+    def exchange(self, it, cap, group=None):
+        world = dist.get_world_size(group)
+        mine = torch.from_numpy(np.concatenate([self.msg[:1 + cap],
+                                                self.msg[1 + self.capacity: 1 + self.capacity + cap]]))
+        parts = [torch.empty_like(mine) for _ in range(world)]
+        dist.all_gather(parts, mine, group=group)
+        vs, xs, maxc = [], [], 0
+        for p in parts:
+            c = int(p[0])
+            maxc = max(maxc, c)
+            m = min(c, cap)
+            vs.append(p[1:1 + m])
+            xs.append(p[1 + cap: 1 + cap + m])
+        self.exchanged_caps.append(cap)
+        return OracleShard.apply(self, it, torch.cat(vs), torch.cat(xs)), maxc
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -87,14 +122,21 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, case, q):
+def _worker(rank, world, port, case, q, packed=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         n, src, dst, w, app, thr, vpg = case
         bounds = destination_bounds(np.bincount(dst, minlength=n), 4, world)
-        shard = OracleShard(n, src, dst, w, 4, bounds, rank, app, 0, thr, vpg)
+        if packed:
+            import paper_1903_07754_b200.distributed as D
+            D.PACKED_MIN_CAP = 4  # small messages, so truncated gathers and full-size redos both run
+            shard = PackedOracleShard(n, src, dst, w, 4, bounds, rank, app, 0, thr, vpg)
+        else:
+            shard = OracleShard(n, src, dst, w, 4, bounds, rank, app, 0, thr, vpg)
         vals, recs, conv = run_sharded(shard, 10_000)
+        if packed and rank == 0:
+            assert any(c < shard.capacity for c in shard.exchanged_caps)  # truncated gathers happened
         if rank == 0:
             q.put((vals, [(r.iteration, r.mode, r.active_edges, r.frontier_out_size) for r in recs], conv,
                    bounds))
@@ -122,13 +164,14 @@ def _case(app, scale=10):
     return n, s, d, w, app, thr, vpg
 
 
-@pytest.mark.parametrize("app", ["bfs", "cc", "sssp"])
-def test_two_rank_sharded_run_matches_single(app):
+@pytest.mark.parametrize("app,packed", [("bfs", False), ("cc", False), ("sssp", False), ("cc", True),
+                                        ("sssp", True)])
+def test_two_rank_sharded_run_matches_single(app, packed):
     case = _case(app)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, case, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, case, q, packed)) for r in range(2)]
     for p in procs:
         p.start()
     vals, trace, conv, bounds = q.get(timeout=300)

@@ -17,15 +17,32 @@ import oracle
 pytestmark = pytest.mark.gpu
 
 
-def _lockstep(shards, max_it=10_000):
+def _lockstep(shards, max_it=10_000, packed=False):
+    """packed: the fixed-size protocol (wg_exchange_pack_all / apply_all) with
+    a deliberately small first capacity, so the truncated-message redo runs."""
     for s in shards:
         s.seed()
     recs = []
+    cap = 16
     for it in range(1, max_it + 1):
-        outs = [s.step(it) for s in shards]
-        V = torch.cat([o[0] for o in outs])
-        X = torch.cat([o[1] for o in outs])
-        rs = [s.apply(it, V, X) for s in shards]
+        if packed:
+            for s in shards:
+                s.step(it)
+
+            def gather(c):
+                nb = shards[0].message_bytes(c)
+                return torch.cat([s.send[:nb] for s in shards])
+            out = [s.apply_packed(it, gather(cap), len(shards), cap) for s in shards]
+            if out[0][1] > cap:
+                full = shards[0].capacity
+                out = [s.apply_packed(it, gather(full), len(shards), full) for s in shards]
+            rs = [o[0] for o in out]
+            cap = min(shards[0].capacity, max(16, 2 * out[0][1]))
+        else:
+            outs = [s.step_pairs(it) for s in shards]
+            V = torch.cat([o[0] for o in outs])
+            X = torch.cat([o[1] for o in outs])
+            rs = [s.apply(it, V, X) for s in shards]
         for r in rs[1:]:
             assert (r.mode, r.active_edges, r.frontier_out_size, r.out_edge_sum) == \
                    (rs[0].mode, rs[0].active_edges, rs[0].frontier_out_size, rs[0].out_edge_sum)
@@ -35,8 +52,10 @@ def _lockstep(shards, max_it=10_000):
     return shards[0].values_int64(), recs
 
 
-@pytest.mark.parametrize("app,world", [("bfs", 2), ("cc", 2), ("sssp", 2), ("cc", 3)])
-def test_device_shards_match_single_run(app, world):
+@pytest.mark.parametrize("app,world,packed", [("bfs", 2, False), ("cc", 2, False), ("sssp", 2, False),
+                                              ("cc", 3, False), ("bfs", 2, True), ("cc", 3, True),
+                                              ("sssp", 2, True)])
+def test_device_shards_match_single_run(app, world, packed):
     import paper_1903_07754_b200 as wg
     from paper_1903_07754_b200 import _lib
     from paper_1903_07754_b200.distributed import DeviceShard, destination_bounds
@@ -53,7 +72,7 @@ def test_device_shards_match_single_run(app, world):
     members = None if app == "cc" else np.array([0])
     shards = [DeviceShard(n, src, dst, w, 4, bounds, r, prog.kernel, init, members, thr,
                           vpg.bit_length() - 1, _lib.WG_VAL_U32) for r in range(world)]
-    vals, recs = _lockstep(shards)
+    vals, recs = _lockstep(shards, packed=packed)
     # single-process reference (oracle)
     topo = oracle.build_pull_topology(n, src, dst, w, 4)
     idx = oracle.build_edge_index(topo)
