@@ -87,29 +87,70 @@ def peaks():
 
 # ----------------------------------------------------------------- clocks --
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clock and throttle reasons sampled DURING the timed region: NVML
+    (sub-millisecond queries, a sample every ~1 ms) with an nvidia-smi
+    fallback (a sample every 0.2 s)."""
 
+    # NVML clocks-event-reason bits (nvmlClocksEventReason*)
+    NVML_REASONS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
+                    "hw_thermal_slowdown": 0x40}
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index: int = 0):
         self.index = index
-        self.rows = []
+        self.rows = []  # (sm_mhz, max_mhz, set of reasons)
         self._stop = threading.Event()
         self._t = None
+        self._nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nvml = (pynvml, pynvml.nvmlDeviceGetHandleByIndex(index))
+        except Exception:
+            self._nvml = None
+
+    def _sample_nvml(self):
+        nv, h = self._nvml
+        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        try:
+            bits = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        except Exception:
+            bits = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+        self.rows.append((float(sm), float(mx), {k for k, b in self.NVML_REASONS.items() if bits & b}))
+
+    def _sample_smi(self):
+        out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                             timeout=5).stdout.strip()
+        if out:
+            r = [x.strip() for x in out.split(",")]
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            num = lambda x: float(x) if x.replace(".", "").isdigit() else None
+            self.rows.append((num(r[0]), num(r[1]),
+                              {names[i] for i in range(4) if len(r) > 3 + i and r[3 + i].lower() == "active"}))
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([x.strip() for x in out.split(",")])
+                if self._nvml:
+                    self._sample_nvml()
+                else:
+                    self._sample_smi()
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.001 if self._nvml else 0.2)
+
+    def tick(self):
+        """Synchronous sample (between timed steps: the timed region of a
+        small workload is shorter than the sampler thread's GIL turns)."""
+        try:
+            if self._nvml:
+                self._sample_nvml()
+        except Exception:
+            pass
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -123,13 +164,11 @@ class ClockSampler:
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4)
-                          if len(r) > 3 + i and r[3 + i].lower() == "active"})
+        sm = [r[0] for r in self.rows if r[0] is not None]
+        mx = [r[1] for r in self.rows if r[1] is not None]
+        reasons = sorted(set().union(*(r[2] for r in self.rows)))
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(self.rows), "source": "nvml" if self._nvml else "nvidia-smi"}
 
 
 # -------------------------------------------------------------- workload --
@@ -223,6 +262,7 @@ def run_b200(args, wl):
             ev[k][0].record(stream)
             step()
             ev[k][1].record(stream)
+            clk.tick()
         torch.cuda.synchronize()
         wall = time.perf_counter() - wall0
     launches = _lib.launch_count() - launches0
@@ -321,6 +361,7 @@ def run_b200_sharded(args, wl, rank, world, local):
             a.record(stream)
             _, recs, conv = run_sharded(shard, max_it, values=False)
             b.record(stream)
+            clk.tick()
             b.synchronize()
             ts.append(a.elapsed_time(b))
     dist.barrier()
@@ -582,6 +623,7 @@ def run_pagerank(args, wl, el, topo, build_s):
             a.record(stream)
             dv.pagerank(g, 20, 0.85, bufs=bufs)
             b.record(stream)
+            clk.tick()
             b.synchronize()
             ts.append(a.elapsed_time(b))
     ms = float(np.mean(ts))

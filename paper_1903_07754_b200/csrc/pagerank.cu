@@ -62,18 +62,19 @@ __global__ void __launch_bounds__(256) pr_pull(wg_graph g, const float *contrib,
             for (int l = 0; l < W; ++l)
                 if (src[l] != WG_NO_LANE) sum += contrib[src[l]];
         }
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            float o = __shfl_up_sync(FULL, sum, off);
-            uint32_t od = __shfl_up_sync(FULL, d, off);
-            if ((int)lane >= off && od == d) sum += o;
-        }
         const uint32_t dn = __shfl_down_sync(FULL, d, 1);
         const uint32_t dp = __shfl_up_sync(FULL, d, 1);
         const bool head = lane == 0 || dp != d;
         const bool tail = lane == 31 || dn != d;
         const unsigned heads = __ballot_sync(FULL, head);
         const unsigned head_lane = 31 - __clz(heads & (0xffffffffu >> (31 - lane)));
+        // segmented sum limited to the longest segment of the tile
+        const unsigned dist = lane - head_lane;
+        const unsigned maxd = __reduce_max_sync(FULL, dist);
+        for (unsigned off = 1; off <= maxd; off <<= 1) {
+            const float o = __shfl_up_sync(FULL, sum, off);
+            if (off <= dist) sum += o;
+        }
         if (tail && valid) {
             bool complete = true;
             if (head_lane == 0 && p >= lane + 1 && g.vdst[p - lane - 1] == d) complete = false;
