@@ -44,12 +44,17 @@ WORKLOADS = {
     "sssp16": dict(app="sssp", scale=16, ef=16, sym=True, vpg=4, thr="0.2", weights=255,
                    desc="SSSP on symmetrized RMAT s16 ef16, hash weights <= 255",
                    expect_digest="7d2c2554722fbf74"),
+    # expected digests of the full-size configs: the reference's own kernels
+    # on the same inputs (tests/golden/full_size.json)
     "sssp_grid": dict(app="sssp", grid=(4096, 4096), vpg=4, thr="0.2",
-                      desc="SSSP on 4096x4096 grid, p=0.9, w in [1,1000] (BASELINE configs[2])"),
+                      desc="SSSP on 4096x4096 grid, p=0.9, w in [1,1000] (BASELINE configs[2])",
+                      expect_digest="3895390ac91e5500"),
     "bfs26": dict(app="bfs", scale=26, ef=16, sym=False, vpg=8, thr="0.01", weights=None,
-                  desc="BFS on directed dedup RMAT s26 ef16 (BASELINE configs[3])"),
+                  desc="BFS on directed dedup RMAT s26 ef16 (BASELINE configs[3])",
+                  expect_digest="8494a0a1f8a0196d"),
     "sssp26": dict(app="sssp", scale=26, ef=16, sym=False, vpg=4, thr="0.2", weights=255,
-                   desc="SSSP on directed dedup RMAT s26 ef16, w<=255 (BASELINE configs[3])"),
+                   desc="SSSP on directed dedup RMAT s26 ef16, w<=255 (BASELINE configs[3])",
+                   expect_digest="184036ba61690aac"),
     "pr25": dict(app="pr", scale=25, ef=32, sym=False, desc="PageRank 20 it on directed dedup RMAT s25 ef32 "
                  "(BASELINE configs[4])"),
 }

@@ -100,16 +100,61 @@ __global__ void unpack_positions(uint64_t k, const uint64_t *keys, int vb, uint3
 
 unsigned grid_1d(uint64_t work) { return grid_for(work, 256 * 8, 16); }
 
-// index key of lane k: (source << vb) | vector; padding lanes get an all-ones
-// source field (sb is chosen so it exceeds every vertex id)
-__global__ void lane_keys(uint64_t lanes, const uint32_t *vsrc, int width, int vb, int sb, uint64_t *keys) {
-    const uint64_t pad = ((1ull << sb) - 1) << vb;
+// (source, vector) pair of lane k; padding lanes get `pad` (> every source)
+__global__ void lane_pairs(uint64_t lanes, const uint32_t *vsrc, int width, uint32_t pad, uint32_t *keys,
+                           uint32_t *vals) {
     for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < lanes;
          k += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t s = vsrc[k];
-        keys[k] = s == WG_NO_LANE ? (pad | (k / width)) : (((uint64_t)s << vb) | (k / width));
+        keys[k] = s == WG_NO_LANE ? pad : s;
+        vals[k] = (uint32_t)(k / width);
     }
 }
+
+// first/last position of each source's run in the sorted pairs (4 per
+// thread) and a flag when two adjacent pairs are equal (a parallel edge)
+__global__ void pair_bounds(uint64_t m, const uint32_t *keys, const uint32_t *vals, uint64_t *first,
+                            uint64_t *last, unsigned *dup) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * 4;
+    for (uint64_t b = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; b < m; b += stride) {
+        uint32_t k[6], v[6];
+#pragma unroll
+        for (int i = 0; i < 6; ++i) {
+            const uint64_t e = b + i - 1;  // b-1 .. b+4
+            const bool ok = !(i == 0 && b == 0) && e < m;
+            k[i] = ok ? keys[e] : 0xffffffffu;
+            v[i] = ok ? vals[e] : 0xffffffffu;
+        }
+        bool d = false;
+#pragma unroll
+        for (int i = 1; i <= 4; ++i) {
+            const uint64_t e = b + i - 1;
+            if (e >= m) break;
+            if (e == 0 || k[i - 1] != k[i]) first[k[i]] = e;
+            if (e == m - 1 || k[i + 1] != k[i]) last[k[i]] = e;
+            d |= e > 0 && k[i - 1] == k[i] && v[i - 1] == v[i];
+        }
+        if (d) *dup = 1u;
+    }
+}
+
+__global__ void pack_pairs(uint64_t m, const uint32_t *keys, const uint32_t *vals, uint64_t *out) {
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m;
+         e += (uint64_t)gridDim.x * blockDim.x)
+        out[e] = ((uint64_t)keys[e] << 32) | vals[e];
+}
+
+size_t index_temp_bytes(uint64_t m, uint32_t n) {
+    size_t a = 0, b = 0, c = 0;
+    cub::DoubleBuffer<uint32_t> kb(nullptr, nullptr), vb(nullptr, nullptr);
+    cub::DeviceRadixSort::SortPairs(nullptr, a, kb, vb, (int64_t)m, 0, 32);
+    cub::DeviceScan::ExclusiveSum(nullptr, b, (uint64_t *)nullptr, (uint64_t *)nullptr, (int64_t)n + 1);
+    cub::DeviceSelect::Unique(nullptr, c, (uint64_t *)nullptr, (uint64_t *)nullptr, (uint64_t *)nullptr,
+                              (int64_t)m);
+    size_t t = a > b ? a : b;
+    return t > c ? t : c;
+}
+
 
 __global__ void narrow_weights(uint64_t lanes, const uint32_t *vw, uint8_t *vw8, unsigned *over) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < lanes;
@@ -299,8 +344,9 @@ int wg_build_layout(uint32_t n, uint64_t m, const uint32_t *d_src, const uint32_
 // ---------------------------------------------------------------------------
 size_t wg_index_scratch_bytes(uint64_t lanes, uint32_t n) {
     uint64_t mm = lanes ? lanes : 1;
-    return 2 * carve_size(mm * 8) + 3 * carve_size(((uint64_t)n + 1) * 8) + carve_size(32) +
-           carve_size(cub_temp_bytes(mm, n)) + 1024;
+    // pairs (4 x uint32 per lane) + bounds + the de-duplication buffers (2 x uint64 per lane)
+    return 4 * carve_size(mm * 4) + 3 * carve_size(((uint64_t)n + 1) * 8) + carve_size(32) +
+           carve_size(index_temp_bytes(mm, n)) + 2 * carve_size(mm * 8) + 1024;
 }
 
 int wg_build_index(const wg_graph *g, uint64_t *d_idx_off, uint32_t *d_idx_pos, uint32_t *d_outdeg,
@@ -318,54 +364,62 @@ int wg_build_index(const wg_graph *g, uint64_t *d_idx_off, uint32_t *d_idx_pos, 
     WG_CUDA(cudaMemsetAsync(d_outdeg, 0, (uint64_t)n * 4, s));
     if (lanes == 0 || n == 0 || g->edges == 0) return WG_OK;
     WG_REQUIRE(g->vsrc && d_idx_pos, "null argument");
+    WG_REQUIRE(g->nvec < (1ull << 32), "too many vectors");
+    // (source, vector) pairs as two uint32 arrays: a stable sort by source
+    // keeps each source's vectors ascending, and the sorted values ARE the
+    // index positions (graph.py:283-301)
     Carve cv{(char *)d_scratch, 0, scratch_bytes};
-    uint64_t *k0 = cv.take<uint64_t>(lanes), *k1 = cv.take<uint64_t>(lanes);
+    uint32_t *k0 = cv.take<uint32_t>(lanes), *k1 = cv.take<uint32_t>(lanes);
+    uint32_t *v0 = cv.take<uint32_t>(lanes), *v1 = cv.take<uint32_t>(lanes);
     uint64_t *first = cv.take<uint64_t>((uint64_t)n + 1), *last = cv.take<uint64_t>((uint64_t)n + 1);
     uint64_t *base = cv.take<uint64_t>((uint64_t)n + 1), *count = cv.take<uint64_t>(4);
-    size_t tbytes = cub_temp_bytes(lanes, n);
+    size_t tbytes = index_temp_bytes(lanes, n);
     void *temp = cv.take<char>(tbytes);
     WG_REQUIRE(temp != nullptr, "index scratch too small");
-    // the source field must exceed every real source so padding lanes sort last
+    // the padding key must exceed every real source so padding lanes sort last
     const int sb = bits_for((uint64_t)n + 1);
-    const int vb = bits_for(g->nvec);
-    WG_REQUIRE(sb + vb <= 64, "graph too large for 64-bit index keys");
-    lane_keys<<<grid_1d(lanes), 256, 0, s>>>(lanes, g->vsrc, (int)g->width, vb, sb, k0); ::wg::count_launch();
-    WG_CHECK_LAUNCH("lane_keys");
-    cub::DoubleBuffer<uint64_t> ib(k0, k1);
+    const uint32_t pad = sb >= 32 ? 0xffffffffu : (1u << sb) - 1u;
+    lane_pairs<<<grid_1d(lanes), 256, 0, s>>>(lanes, g->vsrc, (int)g->width, pad, k0, v0);
+    ::wg::count_launch();
+    WG_CHECK_LAUNCH("lane_pairs");
+    cub::DoubleBuffer<uint32_t> kb(k0, k1), vb(v0, v1);
     size_t tb = tbytes;
-    WG_CUDA(cub::DeviceRadixSort::SortKeys(temp, tb, ib, (int64_t)lanes, vb, vb + sb, s));
-    uint64_t *isorted = ib.Current();
-    uint64_t *ialt = ib.Alternate();
+    WG_CUDA(cub::DeviceRadixSort::SortPairs(temp, tb, kb, vb, (int64_t)lanes, 0, sb, s));
+    const uint32_t *ks = kb.Current(), *vs = vb.Current();
     const uint64_t m = g->edges;  // valid lanes; the padding keys follow them
     unsigned *dup = reinterpret_cast<unsigned *>(count + 1);
     WG_CUDA(cudaMemsetAsync(first, 0xff, ((uint64_t)n + 1) * 8, s));
     WG_CUDA(cudaMemsetAsync(dup, 0, sizeof(unsigned), s));
-    run_bounds4<<<grid_1d(m / 4 + 1), 256, 0, s>>>(m, isorted, vb, first, last, dup); ::wg::count_launch();
+    pair_bounds<<<grid_1d(m / 4 + 1), 256, 0, s>>>(m, ks, vs, first, last, dup); ::wg::count_launch();
     run_counts<<<grid_1d(n), 256, 0, s>>>(n, first, last, 0, base, d_outdeg); ::wg::count_launch();
     WG_CHECK_LAUNCH("src runs");
     unsigned h_dup = 0;
     WG_CUDA(cudaMemcpyAsync(&h_dup, dup, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
     WG_CUDA(cudaStreamSynchronize(s));
     uint64_t entries = m;
-    if (h_dup) {
+    if (!h_dup) {
+        // without parallel edges every pair is an index entry
+        WG_CUDA(cudaMemcpyAsync(d_idx_pos, vs, m * 4, cudaMemcpyDeviceToDevice, s));
+    } else {
         // parallel edges share a (src, vector) pair: de-duplicate (graph.py:293-297)
+        uint64_t *packed = cv.take<uint64_t>(m), *uniq = cv.take<uint64_t>(m);
+        WG_REQUIRE(packed && uniq, "index scratch too small");
+        pack_pairs<<<grid_1d(m), 256, 0, s>>>(m, ks, vs, packed); ::wg::count_launch();
         tb = tbytes;
-        WG_CUDA(cub::DeviceSelect::Unique(temp, tb, isorted, ialt, count, (int64_t)m, s));
+        WG_CUDA(cub::DeviceSelect::Unique(temp, tb, packed, uniq, count, (int64_t)m, s));
         WG_CUDA(cudaMemcpyAsync(&entries, count, 8, cudaMemcpyDeviceToHost, s));
         WG_CUDA(cudaStreamSynchronize(s));
         WG_CUDA(cudaMemsetAsync(first, 0xff, ((uint64_t)n + 1) * 8, s));
-        run_bounds4<<<grid_1d(entries / 4 + 1), 256, 0, s>>>(entries, ialt, vb, first, last, nullptr);
+        run_bounds4<<<grid_1d(entries / 4 + 1), 256, 0, s>>>(entries, uniq, 32, first, last, nullptr);
         ::wg::count_launch();
         run_counts<<<grid_1d(n), 256, 0, s>>>(n, first, last, 0, base, nullptr); ::wg::count_launch();
+        unpack_positions<<<grid_1d(entries), 256, 0, s>>>(entries, uniq, 32, d_idx_pos); ::wg::count_launch();
         WG_CHECK_LAUNCH("index runs");
-        isorted = ialt;
     }
-    // without duplicates the index runs are the source runs: base holds them
+    // the index runs: base holds their lengths
     WG_CUDA(cudaMemsetAsync(base + n, 0, 8, s));
     tb = tbytes;
     WG_CUDA(cub::DeviceScan::ExclusiveSum(temp, tb, base, d_idx_off, (int64_t)n + 1, s));
-    unpack_positions<<<grid_1d(entries), 256, 0, s>>>(entries, isorted, vb, d_idx_pos); ::wg::count_launch();
-    WG_CHECK_LAUNCH("unpack_positions");
     *h_entries = entries;
     return WG_OK;
 }

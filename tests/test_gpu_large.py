@@ -126,3 +126,30 @@ def test_int64_values_match_uint32(app):
     assert np.array_equal(outs[0][0], outs[1][0])
     assert outs[0][1] == outs[1][1]
     assert {m for m, *_ in outs[0][1]} == {"FullScan", "Wedge"}
+
+
+@pytest.mark.parametrize("workload", ["sssp_grid", "bfs26", "sssp26"])
+def test_full_size_digests_equal_reference(workload):
+    """BASELINE configs[2] and [3] at full size: the device loop's digest equals
+    the digest the reference's own kernels produced on the same inputs
+    (tests/golden/full_size.json, generated on the GPU host's CPU)."""
+    import json
+    from pathlib import Path
+    import bench
+    import paper_1903_07754_b200 as wg
+    from paper_1903_07754_b200 import _lib, device as dv
+    want = json.loads((Path(__file__).parent / "golden" / "full_size.json").read_text())[workload]
+    assert want["equal"]
+    wl = bench.WORKLOADS[workload]
+    el, topo = bench.make_graph(wl)
+    g = topo.device
+    prog = wg.make_program(wl["app"], 0)
+    init = prog.initial_values(g.n)
+    fh = dv.first_hit_ok(prog.kernel, init, np.array([0]))
+    loop = dv.DeviceLoop(g, {4: 2, 8: 3}[wl["vpg"]], _lib.WG_VAL_U32)
+    p = loop.seed(dv.encode_values(init, _lib.WG_VAL_U32), dv.initial_words(g.n, np.array([0])), prog.kernel,
+                  Fraction(wl["thr"]), first_hit=fh, level_base=dv.first_hit_level(init) if fh else 0)
+    recs, conv, last = loop.drive(p, g.n + 16)
+    assert conv and len(recs) == want["iterations"]
+    assert wg.result_digest(dv.values_to_int64(loop.values_after(last), _lib.WG_VAL_U32)) == \
+        want["reference_digest"]
