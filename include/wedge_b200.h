@@ -113,6 +113,20 @@ int wg_build_layout(uint32_t n, uint64_t m, const uint32_t *d_src, const uint32_
 size_t wg_index_scratch_bytes(uint64_t lanes, uint32_t n);
 int wg_build_index(const wg_graph *g, uint64_t *d_idx_off, uint32_t *d_idx_pos, uint32_t *d_outdeg,
                    void *d_scratch, size_t scratch_bytes, uint64_t *h_entries, void *stream);
+/* The same index built chunk by chunk as the lanes arrive (chunks in
+ * ascending vector order, each of at most max_chunk_lanes lanes; chunk 0
+ * first): wg_index_chunk sorts a chunk's (source, vector) pairs and ranks
+ * them behind the earlier chunks' entries (asynchronous); wg_index_finish
+ * scatters every entry to its place and writes d_idx_off / d_idx_pos /
+ * d_outdeg (synchronises; falls back to wg_build_index -- then the scratch
+ * must also hold wg_index_scratch_bytes -- when the graph has parallel
+ * edges). */
+size_t wg_index_chunked_scratch_bytes(uint64_t lanes, uint64_t max_chunk_lanes, uint32_t n);
+int wg_index_chunk(const wg_graph *g, uint64_t v_begin, uint64_t v_end, uint32_t chunk,
+                   uint64_t max_chunk_lanes, void *d_scratch, size_t scratch_bytes, void *stream);
+int wg_index_finish(const wg_graph *g, uint64_t max_chunk_lanes, uint64_t *d_idx_off, uint32_t *d_idx_pos,
+                    uint32_t *d_outdeg, void *d_scratch, size_t scratch_bytes, uint64_t *h_entries,
+                    void *stream);
 /* vec_dst from per-destination vector offsets d_voff [n+1] (the run-length
  * form of PullTopology.vec_dst, graph.py:240-243).  Asynchronous. */
 int wg_expand_destinations(uint32_t n, const uint32_t *d_voff, uint64_t nvec, uint32_t *d_vdst, void *stream);

@@ -70,7 +70,7 @@ EXPORTS = [
     "wg_run_graph_destroy", "wg_run_loop_graph_create", "wg_run_loop_launch", "wg_run_persistent",
     "wg_debug_phase_buffer", "wg_index_scratch_bytes", "wg_build_index", "wg_expand_destinations",
     "wg_narrow_weights", "wg_widen_weights", "wg_exchange_bytes", "wg_exchange_pack_all",
-    "wg_exchange_apply_all",
+    "wg_exchange_apply_all", "wg_index_chunked_scratch_bytes", "wg_index_chunk", "wg_index_finish",
 ]
 
 _LIB = None
@@ -153,6 +153,9 @@ def load(path: os.PathLike | str | None = None):
         "wg_narrow_weights": (ctypes.c_int, [G, c_vp, ctypes.POINTER(ctypes.c_int), c_vp]),
         "wg_widen_weights": (ctypes.c_int, [c_u64, c_vp, c_vp, c_vp]),
         "wg_exchange_bytes": (c_u64, [c_u64, ctypes.c_int]),
+        "wg_index_chunked_scratch_bytes": (ctypes.c_size_t, [c_u64, c_u64, c_u32]),
+        "wg_index_chunk": (ctypes.c_int, [G, c_u64, c_u64, c_u32, c_u64, c_vp, ctypes.c_size_t, c_vp]),
+        "wg_index_finish": (ctypes.c_int, [G, c_u64, c_vp, c_vp, c_vp, c_vp, ctypes.c_size_t, u64p, c_vp]),
         "wg_exchange_pack_all": (ctypes.c_int, [G, B, P, c_u64, c_vp, c_u64, c_vp]),
         "wg_exchange_apply_all": (ctypes.c_int, [G, B, P, c_u64, c_vp, c_u32, c_u64, c_vp, c_vp]),
     }

@@ -114,7 +114,7 @@ __global__ void lane_pairs(uint64_t lanes, const uint32_t *vsrc, int width, uint
 // first/last position of each source's run in the sorted pairs (4 per
 // thread) and a flag when two adjacent pairs are equal (a parallel edge)
 __global__ void pair_bounds(uint64_t m, const uint32_t *keys, const uint32_t *vals, uint64_t *first,
-                            uint64_t *last, unsigned *dup) {
+                            uint64_t *last, unsigned *dup, uint32_t pad) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * 4;
     for (uint64_t b = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; b < m; b += stride) {
         uint32_t k[6], v[6];
@@ -130,12 +130,19 @@ __global__ void pair_bounds(uint64_t m, const uint32_t *keys, const uint32_t *va
         for (int i = 1; i <= 4; ++i) {
             const uint64_t e = b + i - 1;
             if (e >= m) break;
+            if (k[i] == pad) continue;  // padding lanes (sorted last)
             if (e == 0 || k[i - 1] != k[i]) first[k[i]] = e;
             if (e == m - 1 || k[i + 1] != k[i]) last[k[i]] = e;
             d |= e > 0 && k[i - 1] == k[i] && v[i - 1] == v[i];
         }
         if (d) *dup = 1u;
     }
+}
+
+__global__ void offset_vectors(uint64_t m, uint32_t base, uint32_t *vals) {
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m;
+         e += (uint64_t)gridDim.x * blockDim.x)
+        vals[e] += base;
 }
 
 __global__ void pack_pairs(uint64_t m, const uint32_t *keys, const uint32_t *vals, uint64_t *out) {
@@ -390,7 +397,7 @@ int wg_build_index(const wg_graph *g, uint64_t *d_idx_off, uint32_t *d_idx_pos, 
     unsigned *dup = reinterpret_cast<unsigned *>(count + 1);
     WG_CUDA(cudaMemsetAsync(first, 0xff, ((uint64_t)n + 1) * 8, s));
     WG_CUDA(cudaMemsetAsync(dup, 0, sizeof(unsigned), s));
-    pair_bounds<<<grid_1d(m / 4 + 1), 256, 0, s>>>(m, ks, vs, first, last, dup); ::wg::count_launch();
+    pair_bounds<<<grid_1d(m / 4 + 1), 256, 0, s>>>(m, ks, vs, first, last, dup, pad); ::wg::count_launch();
     run_counts<<<grid_1d(n), 256, 0, s>>>(n, first, last, 0, base, d_outdeg); ::wg::count_launch();
     WG_CHECK_LAUNCH("src runs");
     unsigned h_dup = 0;
@@ -421,6 +428,173 @@ int wg_build_index(const wg_graph *g, uint64_t *d_idx_off, uint32_t *d_idx_pos, 
     tb = tbytes;
     WG_CUDA(cub::DeviceScan::ExclusiveSum(temp, tb, base, d_idx_off, (int64_t)n + 1, s));
     *h_entries = entries;
+    return WG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Chunked index build: vector chunks are processed in order as their lanes
+// arrive (e.g. while the next chunk is still being copied to the device).
+// Every entry of chunk c for source s lies after those of chunks < c, so an
+// entry's final offset inside its source's run is (entries of s in earlier
+// chunks) + (its rank inside the chunk's sorted run); one scatter at the end
+// places all of them once the per-source totals (the out-degrees) are known.
+struct ChunkScratch {
+    uint32_t *keys, *vals, *rank;  // [lanes] each: sorted per chunk, in place
+    uint32_t *kalt, *valt;         // [max chunk lanes] sort double buffers
+    uint64_t *first, *last;        // [n+1]
+    uint32_t *pre;                 // [n] entries of each source in the chunks so far
+    uint64_t *off;                 // [n+1] final run offsets
+    unsigned *dup;                 // parallel-edge flag
+    void *temp;
+    size_t temp_bytes;
+};
+
+static int carve_chunks(uint64_t lanes, uint64_t max_chunk, uint32_t n, void *scratch, size_t bytes,
+                        ChunkScratch *cs) {
+    Carve cv{(char *)scratch, 0, bytes};
+    const uint64_t L = lanes ? lanes : 1, C = max_chunk ? max_chunk : 1;
+    cs->keys = cv.take<uint32_t>(L);
+    cs->vals = cv.take<uint32_t>(L);
+    cs->rank = cv.take<uint32_t>(L);
+    cs->kalt = cv.take<uint32_t>(C);
+    cs->valt = cv.take<uint32_t>(C);
+    cs->first = cv.take<uint64_t>((uint64_t)n + 1);
+    cs->last = cv.take<uint64_t>((uint64_t)n + 1);
+    cs->pre = cv.take<uint32_t>((uint64_t)n + 1);
+    cs->off = cv.take<uint64_t>((uint64_t)n + 1);
+    cs->dup = cv.take<unsigned>(4);
+    cs->temp_bytes = index_temp_bytes(C > n ? C : (uint64_t)n + 1, n);
+    cs->temp = cv.take<char>(cs->temp_bytes);
+    if (!cs->temp) {
+        set_error("chunked index scratch too small (%zu bytes)", bytes);
+        return WG_ENOSPACE;
+    }
+    return WG_OK;
+}
+
+}  // extern "C"
+namespace {
+
+// rank of each sorted entry inside its source's run, offset by the entries
+// of that source in earlier chunks; valid entries only (padding sorts last)
+__global__ void chunk_ranks(uint64_t m, const uint32_t *keys, const uint64_t *first, const uint32_t *pre,
+                            uint32_t pad, uint32_t *rank) {
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t s = keys[e];
+        if (s != pad) rank[e] = pre[s] + (uint32_t)(e - first[s]);
+    }
+}
+
+__global__ void chunk_totals(uint32_t n, const uint64_t *first, const uint64_t *last, uint32_t *pre) {
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
+         v += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t f = first[v];
+        if (f != ~0ull) pre[v] += (uint32_t)(last[v] - f + 1);
+    }
+}
+
+__global__ void widen_counts(uint32_t n, const uint32_t *pre, uint64_t *out, uint32_t *deg) {
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
+         v += (uint64_t)gridDim.x * blockDim.x) {
+        out[v] = pre[v];
+        deg[v] = pre[v];
+    }
+}
+
+__global__ void scatter_entries(uint64_t lanes, const uint32_t *keys, const uint32_t *vals, const uint32_t *rank,
+                                uint32_t pad, const uint64_t *off, uint32_t *pos) {
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < lanes;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t s = keys[e];
+        if (s != pad) pos[off[s] + rank[e]] = vals[e];
+    }
+}
+
+}  // namespace
+extern "C" {
+
+size_t wg_index_chunked_scratch_bytes(uint64_t lanes, uint64_t max_chunk_lanes, uint32_t n) {
+    const uint64_t L = lanes ? lanes : 1, C = max_chunk_lanes ? max_chunk_lanes : 1;
+    return 3 * carve_size(L * 4) + 2 * carve_size(C * 4) + 2 * carve_size(((uint64_t)n + 1) * 8) +
+           carve_size(((uint64_t)n + 1) * 4) + carve_size(((uint64_t)n + 1) * 8) + carve_size(16) +
+           carve_size(index_temp_bytes(C > n ? C : (uint64_t)n + 1, n)) + 1024;
+}
+
+int wg_index_chunk(const wg_graph *g, uint64_t v_begin, uint64_t v_end, uint32_t chunk,
+                   uint64_t max_chunk_lanes, void *d_scratch, size_t scratch_bytes, void *stream) {
+    WG_REQUIRE(g && g->vsrc, "null argument");
+    WG_REQUIRE(v_begin <= v_end && v_end <= g->nvec, "bad vector range");
+    const uint64_t lanes = g->nvec * g->width, w = g->width;
+    const uint64_t c0 = v_begin * w, cl = (v_end - v_begin) * w;
+    WG_REQUIRE(cl <= max_chunk_lanes, "chunk larger than max_chunk_lanes");
+    WG_REQUIRE(g->n < 0xffffffffu && g->nvec < (1ull << 32), "graph too large for the index");
+    ChunkScratch cs;
+    int rc = carve_chunks(lanes, max_chunk_lanes, g->n, d_scratch, scratch_bytes, &cs);
+    if (rc) return rc;
+    cudaStream_t s = as_stream(stream);
+    const uint32_t n = g->n;
+    if (chunk == 0) {
+        WG_CUDA(cudaMemsetAsync(cs.pre, 0, ((uint64_t)n + 1) * 4, s));
+        WG_CUDA(cudaMemsetAsync(cs.dup, 0, 16, s));
+    }
+    if (cl == 0 || n == 0) return WG_OK;
+    const int sb = bits_for((uint64_t)n + 1);
+    const uint32_t pad = sb >= 32 ? 0xffffffffu : (1u << sb) - 1u;
+    uint32_t *k = cs.keys + c0, *v = cs.vals + c0;
+    lane_pairs<<<grid_1d(cl), 256, 0, s>>>(cl, g->vsrc + c0, (int)w, pad, k, v);
+    ::wg::count_launch();
+    // lane_pairs numbered vectors from 0 inside the chunk: shift to global ids
+    WG_CHECK_LAUNCH("lane_pairs");
+    cub::DoubleBuffer<uint32_t> kb(k, cs.kalt), vb(v, cs.valt);
+    size_t tb = cs.temp_bytes;
+    WG_CUDA(cub::DeviceRadixSort::SortPairs(cs.temp, tb, kb, vb, (int64_t)cl, 0, sb, s));
+    if (kb.Current() != k) WG_CUDA(cudaMemcpyAsync(k, kb.Current(), cl * 4, cudaMemcpyDeviceToDevice, s));
+    if (vb.Current() != v) WG_CUDA(cudaMemcpyAsync(v, vb.Current(), cl * 4, cudaMemcpyDeviceToDevice, s));
+    offset_vectors<<<grid_1d(cl), 256, 0, s>>>(cl, (uint32_t)v_begin, v);
+    ::wg::count_launch();
+    // valid entries of the chunk = all but its padding lanes (sorted last);
+    // bounds over the whole chunk, padding runs land in first/last[pad] <= n
+    WG_CUDA(cudaMemsetAsync(cs.first, 0xff, ((uint64_t)n + 1) * 8, s));
+    pair_bounds<<<grid_1d(cl / 4 + 1), 256, 0, s>>>(cl, k, v, cs.first, cs.last, cs.dup, pad); ::wg::count_launch();
+    chunk_ranks<<<grid_1d(cl), 256, 0, s>>>(cl, k, cs.first, cs.pre, pad, cs.rank + c0); ::wg::count_launch();
+    chunk_totals<<<grid_1d(n), 256, 0, s>>>(n, cs.first, cs.last, cs.pre); ::wg::count_launch();
+    WG_CHECK_LAUNCH("index chunk");
+    return WG_OK;
+}
+
+int wg_index_finish(const wg_graph *g, uint64_t max_chunk_lanes, uint64_t *d_idx_off, uint32_t *d_idx_pos,
+                    uint32_t *d_outdeg, void *d_scratch, size_t scratch_bytes, uint64_t *h_entries,
+                    void *stream) {
+    WG_REQUIRE(g && d_idx_off && d_idx_pos && d_outdeg && h_entries, "null argument");
+    const uint64_t lanes = g->nvec * g->width;
+    ChunkScratch cs;
+    int rc = carve_chunks(lanes, max_chunk_lanes, g->n, d_scratch, scratch_bytes, &cs);
+    if (rc) return rc;
+    cudaStream_t s = as_stream(stream);
+    const uint32_t n = g->n;
+    unsigned h_dup = 0;
+    WG_CUDA(cudaMemcpyAsync(&h_dup, cs.dup, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+    WG_CUDA(cudaStreamSynchronize(s));
+    if (h_dup) {
+        // parallel edges: the one-shot builder de-duplicates (the lanes are all on the device now)
+        const size_t need = wg_index_scratch_bytes(lanes, n);
+        WG_REQUIRE(scratch_bytes >= need, "scratch too small for the de-duplicating index build");
+        return wg_build_index(g, d_idx_off, d_idx_pos, d_outdeg, d_scratch, scratch_bytes, h_entries, stream);
+    }
+    *h_entries = g->edges;
+    if (n == 0) return WG_OK;
+    widen_counts<<<grid_1d(n), 256, 0, s>>>(n, cs.pre, cs.off, d_outdeg); ::wg::count_launch();
+    WG_CUDA(cudaMemsetAsync(cs.off + n, 0, 8, s));
+    size_t tb = cs.temp_bytes;
+    WG_CUDA(cub::DeviceScan::ExclusiveSum(cs.temp, tb, cs.off, d_idx_off, (int64_t)n + 1, s));
+    const int sb = bits_for((uint64_t)n + 1);
+    const uint32_t pad = sb >= 32 ? 0xffffffffu : (1u << sb) - 1u;
+    if (lanes) {
+        scatter_entries<<<grid_1d(lanes), 256, 0, s>>>(lanes, cs.keys, cs.vals, cs.rank, pad, d_idx_off, d_idx_pos);
+        ::wg::count_launch();
+    }
+    WG_CHECK_LAUNCH("index finish");
     return WG_OK;
 }
 

@@ -195,6 +195,59 @@ class DeviceGraph:
         g.rebuild_derived(voff, scratch, stream)
         return g
 
+    def upload_rebuild(self, host: dict, dev: dict, chunks: int = 4, scratch=None, copy_stream=None) -> int:
+        """Copy the compact topology from pinned host memory (host["vsrc"],
+        host["voff"], optional host["vw8"] / host["vw"]) into this graph's
+        device arrays (dev[...] views of them) and rebuild vec_dst, the edge
+        index and the out-degrees, with the index built chunk by chunk so each
+        chunk's sort overlaps the copy of the next (wg_index_chunk /
+        wg_index_finish).  Returns the index length."""
+        torch = _torch()
+        L = _lib.load()
+        cs = copy_stream or torch.cuda.Stream()
+        main = torch.cuda.current_stream()
+        W = self.width
+        cuts = [self.nvec * c // chunks for c in range(chunks + 1)]
+        max_lanes = max(cuts[c + 1] - cuts[c] for c in range(chunks)) * W
+        need = max(int(L.wg_index_chunked_scratch_bytes(self.nvec * W, max_lanes, self.n)),
+                   int(L.wg_index_scratch_bytes(self.nvec * W, self.n)))
+        if scratch is None or scratch.numel() < need:
+            scratch = torch.empty(need, dtype=torch.uint8, device=self.vsrc.device)
+        cs.wait_stream(main)  # the previous use of the buffers is done
+        evs = []
+        with torch.cuda.stream(cs):
+            dev["voff"].copy_(host["voff"], non_blocking=True)
+            e = torch.cuda.Event()
+            e.record(cs)
+            evs.append(e)
+            for c in range(chunks):
+                a, b = cuts[c] * W, cuts[c + 1] * W
+                dev["vsrc"][a:b].copy_(host["vsrc"][a:b], non_blocking=True)
+                e = torch.cuda.Event()
+                e.record(cs)
+                evs.append(e)
+            for k in ("vw8", "vw"):
+                if k in host:
+                    dev[k].copy_(host[k], non_blocking=True)
+            e = torch.cuda.Event()
+            e.record(cs)
+            evs.append(e)
+        st = _lib.stream_ptr()
+        main.wait_event(evs[0])
+        check(L.wg_expand_destinations(self.n, _ptr(dev["voff"]), self.nvec, _ptr(self.vdst), st))
+        gs = ctypes.byref(self.struct())
+        for c in range(chunks):
+            main.wait_event(evs[1 + c])
+            check(L.wg_index_chunk(gs, cuts[c], cuts[c + 1], c, max_lanes, _ptr(scratch), scratch.numel(), st))
+        ent = ctypes.c_uint64(0)
+        check(L.wg_index_finish(gs, max_lanes, _ptr(self.idx_off), _ptr(self.idx_pos), _ptr(self.outdeg),
+                                _ptr(scratch), scratch.numel(), ctypes.byref(ent), st))
+        main.wait_event(evs[-1])
+        if "vw8" in host and self.vw is not None:
+            check(L.wg_widen_weights(self.nvec * W, _ptr(dev["vw8"]), _ptr(self.vw), st))
+        self._upload_scratch = scratch
+        return int(ent.value)
+
     def rebuild_derived(self, voff, scratch=None, stream=None) -> int:
         """Recompute vdst, the edge index and the out-degrees in place from
         vsrc and voff (the arrays keep their addresses, so captured loop

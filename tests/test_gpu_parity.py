@@ -84,6 +84,17 @@ def test_layout_rebuilt_from_lanes(wg, golden):
         vs.copy_(g.vsrc)
         g2 = dv.DeviceGraph.from_lanes(g.n, g.width, g.edges, g.nvec, vs, None, g.vector_offsets())
         assert g2.entries == g.entries
+        # the pipelined form (chunked index, falls back on parallel edges)
+        host = {"vsrc": g.vsrc.cpu().pin_memory(), "voff": g.vector_offsets().cpu().pin_memory()}
+        g2.vdst.zero_()
+        g2.idx_pos.zero_()
+        for chunks in (1, 3):
+            assert g2.upload_rebuild(host, {"vsrc": g2.vsrc, "voff": torch.empty_like(host["voff"], device="cuda")},
+                                     chunks=chunks) == g.entries
+            assert np.array_equal(g2.vec_dst_np(), g.vec_dst_np())
+            assert np.array_equal(g2.offsets_np(), g.offsets_np())
+            assert np.array_equal(g2.positions_np(), g.positions_np())
+            assert np.array_equal(g2.outdeg_np(), g.outdeg_np())
         assert np.array_equal(g2.vec_dst_np(), g.vec_dst_np())
         assert np.array_equal(g2.offsets_np(), g.offsets_np())
         assert np.array_equal(g2.positions_np(), g.positions_np())
