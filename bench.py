@@ -527,7 +527,7 @@ def e2e_b200(args, wl, g, loop, dinit, words, kern, thr, max_it, first_hit=False
 
     def one():
         # pipelined: each chunk's index sort overlaps the copy of the next
-        g2.upload_rebuild(host, dev, chunks=4, copy_stream=copy_stream)
+        g2.upload_rebuild(host, dev, chunks=int(os.environ.get("WG_E2E_CHUNKS", "8")), copy_stream=copy_stream)
         p = loop2.seed(dinit, words, kern, thr, first_hit=first_hit, level_base=level_base,
                        identity_init=identity_init)
         recs, conv, last = loop2.drive(p, max_it)
@@ -548,7 +548,7 @@ def e2e_b200(args, wl, g, loop, dinit, words, kern, thr, max_it, first_hit=False
     ms = float(np.mean(ts))
     return {"value": round(g.edges / (ms * 1e-3) / 1e9, 4), "unit": "GTEPS (|E|/time-to-solution)",
             "ms_per_step": round(ms, 3), "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-            "path": "pinned host topology (vsrc, voff[, weights as bytes when <= 255]) -> H2D in 4 chunks overlapped with wg_index_chunk, wg_index_finish, wg_expand_destinations, wg_widen_weights -> device loop -> D2H values"}
+            "path": "pinned host topology (vsrc, voff[, weights as bytes when <= 255]) -> H2D in 8 chunks overlapped with wg_index_chunk, wg_index_finish, wg_expand_destinations, wg_widen_weights -> device loop -> D2H values"}
 
 
 def host_reference_layout(g):
