@@ -523,7 +523,7 @@ __global__ void decide_kernel(LoopCtx c, cudaGraphConditionalHandle hf, cudaGrap
         variant = 1;
     } else if (mode == MODE_WEDGE) {
         const uint64_t entries = ctx_in(c, it)->nz_packed & 0xffffffffull;
-        variant = (has_entries && entries * 8 < ngroups) ? 3 : 2;
+        variant = (has_entries && entries * SPARSE_ENTRY_RATIO < ngroups) ? 3 : 2;
     }
     ctx_out(c, it)->reserved[0] = (uint64_t)variant;
     cudaGraphSetConditional(hf, variant == 1 ? 1u : 0u);

@@ -72,6 +72,9 @@ struct PullBufs {
 #ifndef SPARSE_U
 #define SPARSE_U 2
 #endif
+// a Wedge iteration is "sparse" when its index entries * this < groups
+constexpr uint64_t SPARSE_ENTRY_RATIO = 8;
+constexpr uint64_t PERSIST_MAX_ENTRIES = 1ull << 24;
 constexpr uint32_t NONE = 0xffffffffu;
 
 template <typename T>
@@ -1013,6 +1016,17 @@ __global__ void __launch_bounds__(256) finalize_kernel(LoopCtx c, PullBufs b) {
 // paying several kernel launches per iteration.
 // Optional phase timestamps of the persistent loop (tools/prof_persistent.py):
 // 4 x uint64 %globaltimer per iteration.
+// The persistent loop takes a Wedge iteration when its transform is small
+// in absolute terms (a few index entries per thread of the grid) or sparse
+// relative to the group space (decide_kernel's sparse variant); very large
+// Wedge frontiers (SSSP s26 iteration 6: 126M entries) run faster through the
+// sorted transform + group compaction path of the graph body.
+__device__ __forceinline__ bool sparse_wedge(const LoopCtx &c, uint64_t it, uint64_t ngroups) {
+    if (ctx_mode(c, it) != MODE_WEDGE) return false;
+    const uint64_t entries = *(volatile const uint64_t *)&ctx_in(c, it)->nz_packed & 0xffffffffull;
+    return entries < PERSIST_MAX_ENTRIES || entries * SPARSE_ENTRY_RATIO < ngroups;
+}
+
 __device__ uint64_t *g_phase_ts = nullptr;
 __device__ uint64_t g_phase_cap = 0;
 
@@ -1053,7 +1067,7 @@ __global__ void __launch_bounds__(PULL_THREADS, SPARSE_MINB) sparse_loop_kernel(
     }
     grid.sync();
     if (!fused) {
-        while (ctx_mode(c, it) == MODE_WEDGE) {
+        while (sparse_wedge(c, it, ngroups)) {
             phase_stamp(it, 0);
             if (tid == 0) ctx_out(c, it)->reserved[0] = 3;
             // phase A: transform(it)  ||  end of iteration it-1 (buffer sync, bitmap
@@ -1089,13 +1103,13 @@ __global__ void __launch_bounds__(PULL_THREADS, SPARSE_MINB) sparse_loop_kernel(
     // (k - first) & 1, slot 0 = the run's regular buffers.
     auto slot_bits = [&](uint64_t k) { return ((k - first) & 1) ? b.gbits2 : gbits; };
     auto slot_list = [&](uint64_t k) { return ((k - first) & 1) ? b.glist2 : const_cast<uint32_t *>(b.glist); };
-    if (ctx_mode(c, it) == MODE_WEDGE) {
+    if (sparse_wedge(c, it, ngroups)) {
         transform_phase(c, it, b.fvert[0], b.fvert[1], b.fpref[0], b.fpref[1], b.tstart[0], b.tstart[1],
                         g.idx_off, g.idx_pos, shift, gbits, 1, const_cast<uint32_t *>(b.glist), ngroups, tsm,
                         blockIdx.x, gridDim.x);
         grid.sync();
     }
-    while (ctx_mode(c, it) == MODE_WEDGE) {
+    while (sparse_wedge(c, it, ngroups)) {
         phase_stamp(it, 0);
         if (tid == 0) {
             ctx_out(c, it)->reserved[0] = 3;
