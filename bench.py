@@ -525,9 +525,12 @@ def e2e_b200(args, wl, g, loop, dinit, words, kern, thr, max_it, first_hit=False
 
     copy_stream = torch.cuda.Stream()
 
+    # pipelined: each chunk's index sort overlaps the copy of the next (chunks
+    # of >= 4M lanes; small graphs upload in one piece)
+    chunks = int(os.environ.get("WG_E2E_CHUNKS", "0")) or max(1, min(8, (g.nvec * g.width) >> 22))
+
     def one():
-        # pipelined: each chunk's index sort overlaps the copy of the next
-        g2.upload_rebuild(host, dev, chunks=int(os.environ.get("WG_E2E_CHUNKS", "8")), copy_stream=copy_stream)
+        g2.upload_rebuild(host, dev, chunks=chunks, copy_stream=copy_stream)
         p = loop2.seed(dinit, words, kern, thr, first_hit=first_hit, level_base=level_base,
                        identity_init=identity_init)
         recs, conv, last = loop2.drive(p, max_it)
@@ -548,7 +551,7 @@ def e2e_b200(args, wl, g, loop, dinit, words, kern, thr, max_it, first_hit=False
     ms = float(np.mean(ts))
     return {"value": round(g.edges / (ms * 1e-3) / 1e9, 4), "unit": "GTEPS (|E|/time-to-solution)",
             "ms_per_step": round(ms, 3), "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-            "path": "pinned host topology (vsrc, voff[, weights as bytes when <= 255]) -> H2D in 8 chunks overlapped with wg_index_chunk, wg_index_finish, wg_expand_destinations, wg_widen_weights -> device loop -> D2H values"}
+            "path": "pinned host topology (vsrc, voff[, weights as bytes when <= 255]) -> H2D in up to 8 chunks overlapped with wg_index_chunk, wg_index_finish, wg_expand_destinations, wg_widen_weights -> device loop -> D2H values"}
 
 
 def host_reference_layout(g):
@@ -646,7 +649,7 @@ def run_pagerank(args, wl, el, topo, build_s):
     if not args.no_e2e:
         out["e2e"] = e2e_pagerank(args, g, bufs)
     if not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline_pagerank(g)
+        out["cpu_baseline"], out["parity"] = cpu_baseline_pagerank(g, bufs[0])
     print(json.dumps(out), flush=True)
 
 
@@ -687,19 +690,23 @@ def e2e_pagerank(args, g, bufs):
             "path": "pinned host layout -> H2D -> wg_pagerank -> D2H ranks"}
 
 
-def cpu_baseline_pagerank(g, sample_iters=1):
-    """The C restatement of the PR iteration (no reference PR exists,
-    SURVEY 8(a) a17) on all host threads: sample_iters iterations timed and
-    scaled to 20."""
+def cpu_baseline_pagerank(g, ranks=None):
+    """The float64 C restatement of the PR iteration (no reference PR exists,
+    SURVEY 8(a) a17) on all host threads, 20 iterations; with the device ranks
+    it also returns the parity (max |r_gpu - r_cpu| per vertex, tolerance 1e-6)."""
     import oracle
     threads = os.cpu_count() or 1
     topo, _, deg = host_reference_layout(g)
     t0 = time.perf_counter()
-    oracle.pagerank(topo, deg, sample_iters, 0.85, threads)
-    t = (time.perf_counter() - t0) * 20 / sample_iters
-    return {"value": round(20 * g.edges / t / 1e9, 5), "unit": "GTEPS (20*|E|/time, PageRank)", "cores": threads,
-            "kind": "port", "seconds_per_run": round(t, 3),
-            "sample": f"{sample_iters} of 20 iterations timed, scaled by 20/{sample_iters}"}
+    ref = oracle.pagerank(topo, deg, 20, 0.85, threads)
+    t = time.perf_counter() - t0
+    out = {"value": round(20 * g.edges / t / 1e9, 5), "unit": "GTEPS (20*|E|/time, PageRank)", "cores": threads,
+           "kind": "port", "seconds_per_run": round(t, 3), "sample": "1 full run of 20 iterations (float64)"}
+    parity = None
+    if ranks is not None:
+        err = float(np.max(np.abs(ranks.cpu().numpy().astype(np.float64) - ref)))
+        parity = {"max_abs_error": err, "tolerance": 1e-6, "ok": err <= 1e-6, "oracle": "float64 C port"}
+    return out, parity
 
 
 def run_reference(args, wl):
