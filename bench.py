@@ -204,7 +204,7 @@ def run_b200(args, wl):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    if (world > 1 or args.sharded) and wl["app"] != "pr":
+    if world > 1 or args.sharded:
         return run_b200_sharded(args, wl, rank, world, local)
 
     t0 = time.perf_counter()
@@ -345,6 +345,8 @@ def run_b200_sharded(args, wl, rank, world, local):
     indeg = torch.bincount(d.to(torch.int64) & 0xFFFFFFFF, minlength=n).cpu().numpy()
     bounds = destination_bounds(indeg, 4, world)
     app = wl["app"]
+    if app == "pr":
+        return run_pagerank_sharded_bench(args, wl, rank, world, local, n, E, s, d, bounds, t0)
     prog = wg.make_program(app, None if app == "cc" else 0)
     shift = {1: 0, 2: 1, 4: 2, 8: 3, 16: 4}[wl["vpg"]]
     shard = DeviceShard(n, s, d, w, 4, bounds, rank, prog.kernel, prog.initial_values(n),
@@ -385,6 +387,52 @@ def run_b200_sharded(args, wl, rank, world, local):
                    "l2": "inputs larger than L2"},
         "parity": {"digest": digest, "expected": wl.get("expect_digest"),
                    "ok": (digest == wl["expect_digest"]) if wl.get("expect_digest") else None},
+        "gpu_launches": int(launches), "clocks": clk.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    dist.destroy_process_group()
+
+
+def run_pagerank_sharded_bench(args, wl, rank, world, local, n, E, s, d, bounds, t0):
+    """PageRank over destination shards: per iteration one NCCL all-gather of
+    the padded per-rank sum slices (paper_1903_07754_b200.distributed)."""
+    import torch
+    import torch.distributed as dist
+    from paper_1903_07754_b200 import _lib
+    from paper_1903_07754_b200.distributed import DevicePageRankShard, run_pagerank_sharded
+    shard = DevicePageRankShard(n, s, d, 4, bounds, rank)
+    del s, d
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t0
+    for _ in range(args.warmup):
+        r = run_pagerank_sharded(shard, 20)
+    dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = _lib.launch_count()
+    stream = torch.cuda.current_stream()
+    ts = []
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            r = run_pagerank_sharded(shard, 20)
+            b.record(stream)
+            clk.tick()
+            b.synchronize()
+            ts.append(a.elapsed_time(b))
+    dist.barrier()
+    launches = _lib.launch_count() - launches0
+    t = torch.tensor([float(np.mean(ts))], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    out = {
+        "metric": METRIC, "value": round(20 * E / (ms * 1e-3) / 1e9, 4), "unit": "GTEPS (20*|E|/time, PageRank)",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": wl["desc"], "V": n, "E": E, "W": 4, "parallelism": f"dst-shard x{world}",
+                   "bounds": bounds, "build_s": round(build_s, 2), "l2": "inputs larger than L2"},
+        "parity": {"rank_sum": float(r.double().sum().item()), "sum_ok": abs(float(r.double().sum()) - 1) < 1e-3},
         "gpu_launches": int(launches), "clocks": clk.summary(),
     }
     if rank == 0:

@@ -71,6 +71,7 @@ EXPORTS = [
     "wg_debug_phase_buffer", "wg_index_scratch_bytes", "wg_build_index", "wg_expand_destinations",
     "wg_narrow_weights", "wg_widen_weights", "wg_exchange_bytes", "wg_exchange_pack_all",
     "wg_exchange_apply_all", "wg_index_chunked_scratch_bytes", "wg_index_chunk", "wg_index_finish",
+    "wg_pagerank_prep", "wg_pagerank_pull",
 ]
 
 _LIB = None
@@ -124,6 +125,9 @@ def load(path: os.PathLike | str | None = None):
         "wg_run_enqueue": (ctypes.c_int, [G, B, P, c_u64, c_u32, c_vp]),
         "wg_run_enqueue_counter": (ctypes.c_int, [G, B, P, c_u32, c_vp]),
         "wg_pagerank": (ctypes.c_int, [G, ctypes.c_int, ctypes.c_double, c_vp, c_vp, c_vp, c_vp, c_vp]),
+        "wg_pagerank_prep": (ctypes.c_int, [c_u32, ctypes.c_int, ctypes.c_double, c_vp, c_vp, c_vp, c_vp,
+                                            c_vp, c_vp]),
+        "wg_pagerank_pull": (ctypes.c_int, [G, c_vp, c_vp, c_u32, c_vp]),
         "wg_rmat_edges": (ctypes.c_int, [c_u32, c_u64, c_u64, c_u64, c_u64, c_u64,
                                          ctypes.POINTER(ctypes.c_double), c_vp, c_vp, c_vp]),
         "wg_canonical_scratch_bytes": (ctypes.c_size_t, [c_u64]),

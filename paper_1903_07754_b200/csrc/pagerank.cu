@@ -45,7 +45,7 @@ __global__ void __launch_bounds__(256) pr_prep(uint32_t n, int it, double dampin
 }
 
 template <int W>
-__global__ void __launch_bounds__(256) pr_pull(wg_graph g, const float *contrib, float *acc) {
+__global__ void __launch_bounds__(256) pr_pull(wg_graph g, const float *contrib, float *acc, uint32_t base) {
     const unsigned lane = lane_id();
     const uint64_t gwarp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -79,13 +79,13 @@ __global__ void __launch_bounds__(256) pr_pull(wg_graph g, const float *contrib,
             bool complete = true;
             if (head_lane == 0 && p >= lane + 1 && g.vdst[p - lane - 1] == d) complete = false;
             if (lane == 31 && p + 1 < g.nvec && g.vdst[p + 1] == d) complete = false;
-            if (complete) acc[d] = sum;
-            else atomicAdd(&acc[d], sum);
+            if (complete) acc[d - base] = sum;
+            else atomicAdd(&acc[d - base], sum);
         }
     }
 }
 
-using PrPull = void (*)(wg_graph, const float *, float *);
+using PrPull = void (*)(wg_graph, const float *, float *, uint32_t);
 
 PrPull pick(int w) {
     switch (w) {
@@ -95,6 +95,13 @@ PrPull pick(int w) {
         case 8: return pr_pull<8>;
     }
     return nullptr;
+}
+
+unsigned pull_grid(const wg_graph *g, PrPull pull) {
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pull, 256, 0);
+    if (per_sm < 1) per_sm = 1;
+    return grid_for(g->nvec, 256, (unsigned)per_sm);
 }
 
 }  // namespace
@@ -110,14 +117,11 @@ extern "C" int wg_pagerank(const wg_graph *g, int iterations, double damping, fl
     WG_CUDA(cudaMemsetAsync(d_acc, 0, (uint64_t)g->n * 4, s));
     WG_CUDA(cudaMemsetAsync(d_scal, 0, 4 * sizeof(double), s));
     unsigned vgrid = grid_for(g->n, 256 * 4, 8);
-    int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pull, 256, 0);
-    if (per_sm < 1) per_sm = 1;
-    unsigned egrid = grid_for(g->nvec, 256, (unsigned)per_sm);
+    unsigned egrid = pull_grid(g, pull);
     for (int it = 0; it < iterations; ++it) {
         pr_prep<<<vgrid, 256, 0, s>>>(g->n, it, damping, g->outdeg, d_acc, d_contrib, nullptr, d_scal); ::wg::count_launch();
         if (g->nvec) {
-            pull<<<egrid, 256, 0, s>>>(*g, d_contrib, d_acc);
+            pull<<<egrid, 256, 0, s>>>(*g, d_contrib, d_acc, 0u);
             ::wg::count_launch();
         }
     }
@@ -125,5 +129,32 @@ extern "C" int wg_pagerank(const wg_graph *g, int iterations, double damping, fl
     pr_prep<<<vgrid, 256, 0, s>>>(g->n, iterations, damping, g->outdeg, d_acc, d_contrib, d_rank,
                                   d_scal); ::wg::count_launch();
     WG_CHECK_LAUNCH("pagerank");
+    return WG_OK;
+}
+
+extern "C" int wg_pagerank_prep(uint32_t n, int it, double damping, const uint32_t *d_outdeg,
+                                float *d_acc, float *d_contrib, float *d_rank, double *d_scal,
+                                void *stream) {
+    WG_REQUIRE(n > 0 && d_outdeg && d_acc && d_contrib && d_scal, "null argument");
+    WG_REQUIRE(it >= 0, "iteration must be >= 0");
+    cudaStream_t s = as_stream(stream);
+    if (it == 0) WG_CUDA(cudaMemsetAsync(d_scal, 0, 4 * sizeof(double), s));
+    pr_prep<<<grid_for(n, 256 * 4, 8), 256, 0, s>>>(n, it, damping, d_outdeg, d_acc, d_contrib, d_rank,
+                                                    d_scal);
+    ::wg::count_launch();
+    WG_CHECK_LAUNCH("pagerank_prep");
+    return WG_OK;
+}
+
+extern "C" int wg_pagerank_pull(const wg_graph *g, const float *d_contrib, float *d_acc,
+                                uint32_t dst_base, void *stream) {
+    WG_REQUIRE(g && d_contrib && d_acc, "null argument");
+    PrPull pull = pick((int)g->width);
+    WG_REQUIRE(pull, "unsupported width %u", g->width);
+    if (!g->nvec) return WG_OK;
+    cudaStream_t s = as_stream(stream);
+    pull<<<pull_grid(g, pull), 256, 0, s>>>(*g, d_contrib, d_acc, dst_base);
+    ::wg::count_launch();
+    WG_CHECK_LAUNCH("pagerank_pull");
     return WG_OK;
 }

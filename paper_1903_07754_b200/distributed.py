@@ -298,3 +298,94 @@ def run_sharded_device(n: int, src, dst, weight, width: int, program, config, gr
     shard = DeviceShard(n, src, dst, weight, width, bounds, rank, program.kernel, init, members,
                         config.threshold.fraction, config.precision.shift, _lib.WG_VAL_U32)
     return run_sharded(shard, config.max_iterations, group)
+
+
+# ---------------------------------------------------------------------------
+# PageRank over destination shards ("PR: allgather of rank (or
+# contrib) slices")
+# ---------------------------------------------------------------------------
+def run_pagerank_sharded(shard, iterations: int, group=None):
+    """Per iteration: every rank applies the previous sums to the full rank
+    vector and builds the contributions (replicated, V-sized), pulls its own
+    destinations, and one all-gather of the padded per-rank sum slices
+    rebuilds the full sum vector on every rank.  The dangling mass needs no
+    collective: each rank derives it from the replicated ranks."""
+    import torch.distributed as dist
+    for it in range(iterations):
+        shard.prep(it)
+        part = shard.pull()
+        dist.all_gather_into_tensor(shard.gathered, part, group=group)
+        shard.unpack()
+    return shard.finish(iterations)
+
+
+class DevicePageRankShard:
+    """One rank's PageRank shard: its destinations' vectors, the global
+    out-degrees, replicated float32 sums/contributions, and the padded slice
+    buffers of the all-gather (slot r*S holds rank r's destinations)."""
+
+    device = "cuda"
+
+    def __init__(self, n: int, src, dst, width: int, bounds: list[int], rank: int, damping: float = 0.85):
+        import torch
+        from . import device as dv
+        from . import _lib
+        self._lib = _lib
+        lo, hi = bounds[rank], bounds[rank + 1]
+        s = dv.to_dev_u32(src)
+        d = dv.to_dev_u32(dst)
+        d64 = d.to(torch.int64) & 0xFFFFFFFF
+        mask = (d64 >= lo) & (d64 < hi)
+        self.outdeg = torch.bincount(s.to(torch.int64) & 0xFFFFFFFF, minlength=n).to(torch.int32)
+        self.g = dv.DeviceGraph.build(n, s[mask], d[mask], None, width)
+        self.n, self.lo, self.hi, self.rank, self.bounds = n, lo, hi, rank, list(bounds)
+        self.damping = float(damping)
+        world = len(bounds) - 1
+        self.S = max(max(bounds[r + 1] - bounds[r] for r in range(world)), 1)
+        f32 = dict(dtype=torch.float32, device="cuda")
+        self.acc = torch.zeros(n, **f32)
+        self.contrib = torch.empty(n, **f32)
+        self.rank_out = torch.empty(n, **f32)
+        self.scal = torch.zeros(4, dtype=torch.float64, device="cuda")
+        self.part = torch.zeros(self.S, **f32)
+        self.gathered = torch.empty(world * self.S, **f32)
+
+    def prep(self, it: int, rank_out=None):
+        L = self._lib.load()
+        self._lib.check(L.wg_pagerank_prep(self.n, it, self.damping, self.outdeg.data_ptr(), self.acc.data_ptr(),
+                                           self.contrib.data_ptr(),
+                                           rank_out.data_ptr() if rank_out is not None else None,
+                                           self.scal.data_ptr(), self._lib.stream_ptr()))
+
+    def pull(self):
+        L = self._lib.load()
+        self.part.zero_()
+        self._lib.check(L.wg_pagerank_pull(ctypes.byref(self.g.struct()), self.contrib.data_ptr(),
+                                           self.part.data_ptr(), self.lo, self._lib.stream_ptr()))
+        return self.part
+
+    def unpack(self):
+        for r in range(len(self.bounds) - 1):
+            lo, hi = self.bounds[r], self.bounds[r + 1]
+            if hi > lo:
+                self.acc[lo:hi].copy_(self.gathered[r * self.S: r * self.S + hi - lo])
+
+    def finish(self, iterations: int):
+        self.prep(iterations, self.rank_out)
+        return self.rank_out
+
+
+def run_pagerank_sharded_device(n: int, src, dst, width: int = 4, iterations: int = 20, damping: float = 0.85,
+                                group=None):
+    """Device entry point (one rank per GPU, torch.distributed initialised by
+    the caller): float32 ranks of all n vertices on every rank."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    from . import device as dv
+    d = dv.to_dev_u32(dst)
+    indeg = torch.bincount(d.to(torch.int64) & 0xFFFFFFFF, minlength=n).cpu().numpy()
+    bounds = destination_bounds(indeg, width, world)
+    shard = DevicePageRankShard(n, src, dst, width, bounds, rank, damping)
+    return run_pagerank_sharded(shard, iterations, group)

@@ -195,3 +195,79 @@ def test_destination_bounds_balance_and_alignment():
         parts = [vec[b[i]:b[i + 1]].sum() for i in range(world)]
         assert sum(parts) == vec.sum()
         assert max(parts) - min(parts) <= 2 * vec.max() + 1
+
+
+class OraclePageRankShard:
+    """CPU stand-in for DevicePageRankShard (float64, edge-list form of the
+    oracle's PageRank semantics) behind the same prep / pull / unpack protocol."""
+
+    device = "cpu"
+
+    def __init__(self, n, src, dst, bounds, rank, damping=0.85):
+        lo, hi = bounds[rank], bounds[rank + 1]
+        m = (dst >= lo) & (dst < hi)
+        self.src, self.dst = src[m].astype(np.int64), dst[m].astype(np.int64)
+        self.deg = np.bincount(src, minlength=n).astype(np.float64)
+        self.n, self.lo, self.hi, self.bounds, self.d = n, lo, hi, bounds, damping
+        world = len(bounds) - 1
+        self.S = max(max(bounds[r + 1] - bounds[r] for r in range(world)), 1)
+        self.acc = np.zeros(n)
+        self.r = None
+        self.gathered = torch.zeros(world * self.S, dtype=torch.float64)
+
+    def prep(self, it):
+        self.r = np.full(self.n, 1.0 / self.n) if it == 0 else \
+            (1 - self.d) / self.n + self.d * (self.acc + self.dangling / self.n)
+        self.contrib = np.where(self.deg > 0, self.r / np.maximum(self.deg, 1), 0.0)
+        self.dangling = self.r[self.deg == 0].sum()
+
+    def pull(self):
+        part = np.zeros(self.S)
+        part[: self.hi - self.lo] = np.bincount(self.dst - self.lo, weights=self.contrib[self.src],
+                                                minlength=self.hi - self.lo)[: self.hi - self.lo]
+        return torch.from_numpy(part)
+
+    def unpack(self):
+        g = self.gathered.numpy()
+        for r in range(len(self.bounds) - 1):
+            lo, hi = self.bounds[r], self.bounds[r + 1]
+            self.acc[lo:hi] = g[r * self.S: r * self.S + hi - lo]
+
+    def finish(self, iterations):
+        self.prep(iterations)
+        return self.r
+
+
+def _pr_worker(rank, world, port, case, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1903_07754_b200.distributed import run_pagerank_sharded
+        n, src, dst = case
+        bounds = destination_bounds(np.bincount(dst, minlength=n), 4, world)
+        r = run_pagerank_sharded(OraclePageRankShard(n, src, dst, bounds, rank), 20)
+        q.put((rank, r, bounds))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_pagerank_matches_single(world):
+    n, s, d = oracle.rmat_edges(10, 8, 7)
+    keep = s != d
+    s, d = s[keep], d[keep]  # directed, with dangling vertices
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_pr_worker, args=(r, world, port, (n, s, d), q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = oracle.pagerank_numpy(n, s, d, 20)
+    assert (np.bincount(s, minlength=n) == 0).any()
+    for rank, r, bounds in got:
+        assert len(set(bounds)) == world + 1
+        assert np.max(np.abs(r - want)) <= 1e-12, rank

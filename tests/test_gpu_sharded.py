@@ -86,3 +86,31 @@ def test_device_shards_match_single_run(app, world, packed):
     for r, s in zip(recs, want.stats):
         if r.mode == "FullScan":
             assert sum(sh_touched for sh_touched in [r.vectors_touched]) <= topo.vector_count
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_device_pagerank_shards_match_single_run(world):
+    """Destination-sharded PageRank (wg_pagerank_prep / wg_pagerank_pull) in
+    lockstep: the all-gather of padded sum slices is a concatenation here."""
+    from paper_1903_07754_b200 import device as dv
+    from paper_1903_07754_b200.distributed import DevicePageRankShard, destination_bounds
+    n, s, d = oracle.rmat_edges(12, 16, 3)
+    keep = s != d
+    s, d = s[keep], d[keep]
+    bounds = destination_bounds(np.bincount(d, minlength=n), 4, world)
+    shards = [DevicePageRankShard(n, s, d, 4, bounds, r) for r in range(world)]
+    for it in range(20):
+        parts = []
+        for sh in shards:
+            sh.prep(it)
+            parts.append(sh.pull().clone())
+        cat = torch.cat(parts)
+        for sh in shards:
+            sh.gathered.copy_(cat)
+            sh.unpack()
+    got = [sh.finish(20).cpu().numpy().astype(np.float64) for sh in shards]
+    want = oracle.pagerank_numpy(n, s, d, 20)
+    single = dv.pagerank(dv.DeviceGraph.build(n, dv.to_dev_u32(s), dv.to_dev_u32(d), None, 4)).cpu().numpy()
+    for r in got:
+        assert np.max(np.abs(r - want)) <= 1e-6  # north_star tolerance vs the float64 oracle
+        assert np.max(np.abs(r - single)) <= 1e-7
