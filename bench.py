@@ -542,7 +542,32 @@ def e2e_b200(args, wl, g, loop, dinit, words, kern, thr, max_it, first_hit=False
     import torch
     from paper_1903_07754_b200 import _lib, device as dv
 
-    host = {"vsrc": g.vsrc.cpu().pin_memory(), "voff": g.vector_offsets().cpu().pin_memory()}
+    p0 = loop.seed(dinit, words, kern, thr, first_hit=first_hit, level_base=level_base,
+                   identity_init=identity_init)
+    ref_vals = loop.values_after(loop.drive(p0, max_it)[2]).clone()
+    # lane sources travel delta-coded (default), as wg_lane_bits(n)-bit fields
+    # or as uint32 (WG_E2E_FORMAT = coded | bits | raw)
+    fmt = os.environ.get("WG_E2E_FORMAT", "coded")
+    if fmt == "bits" and g.lane_bits() >= 32:
+        fmt = "raw"
+    pack = fmt == "bits"
+    t_fmt = time.perf_counter()
+    host = {"voff": g.vector_offsets().cpu().pin_memory()}
+    if fmt == "coded":
+        host.update({k: v.cpu().pin_memory() for k, v in g.encode_lanes().items()})
+    elif pack:
+        host["vsrc_bits"] = g.pack_lanes()[0].cpu().pin_memory()
+    else:
+        host["vsrc"] = g.vsrc.cpu().pin_memory()
+    # the out-degrees travel too (the reference call's `degrees` input): the
+    # index is then placed chunk by chunk instead of sorted
+    # (auto: while the index fits in ~8x L2; at s25/s26 its random slot writes
+    # cost more than the chunk sorts, measured in profiles/r01_e2e_index.txt)
+    mode = os.environ.get("WG_E2E_INDEX", "auto")
+    placed = mode == "placed" or (mode == "auto" and g.edges * 4 <= (1 << 30))
+    if placed:
+        host["outdeg"] = g.outdeg[: g.n].cpu().pin_memory()
+    t_fmt = time.perf_counter() - t_fmt
     if g.vw8 is not None:  # weights <= 255 travel as bytes and are widened on the device
         host["vw8"] = g.vw8[: g.nvec * g.width].cpu().pin_memory()
     elif g.vw is not None:
@@ -551,6 +576,9 @@ def e2e_b200(args, wl, g, loop, dinit, words, kern, thr, max_it, first_hit=False
     dev = {k: torch.empty(v.numel() + 64, dtype=v.dtype, device="cuda")[: v.numel()] for k, v in host.items()}
     for k, v in host.items():
         dev[k].copy_(v)
+    if fmt != "raw":
+        dev["vsrc"] = torch.empty(g.nvec * g.width + 64, dtype=torch.int32, device="cuda")[: g.nvec * g.width]
+        dev["vsrc"].copy_(g.vsrc)  # first build only; every timed step re-decodes it from the upload
     if "vw8" in dev:
         dev["vw"] = torch.empty(g.nvec * g.width + 64, dtype=torch.int32, device="cuda")[: g.nvec * g.width]
     lanes = g.nvec * g.width
@@ -597,9 +625,15 @@ def e2e_b200(args, wl, g, loop, dinit, words, kern, thr, max_it, first_hit=False
         b.synchronize()
         ts.append(a.elapsed_time(b))
     ms = float(np.mean(ts))
+    # the last step's decoded layout and result equal the resident run's
+    same = bool(torch.equal(g2.vsrc, g.vsrc)) and bool(torch.equal(out_host.cuda(), ref_vals))
     return {"value": round(g.edges / (ms * 1e-3) / 1e9, 4), "unit": "GTEPS (|E|/time-to-solution)",
             "ms_per_step": round(ms, 3), "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-            "path": "pinned host topology (vsrc, voff[, weights as bytes when <= 255]) -> H2D in up to 8 chunks overlapped with wg_index_chunk, wg_index_finish, wg_expand_destinations, wg_widen_weights -> device loop -> D2H values"}
+            "result_equal": same, "lane_format": fmt, "lane_bits_per_lane": round(
+                8 * sum(host[k].numel() * host[k].element_size() for k in host if k.startswith(("lane_", "vsrc")))
+                / max(1, g.nvec * g.width), 2),
+            "host_format_build_s": round(t_fmt, 2), "index": "placed from the degrees" if placed else "chunked sort",
+            "path": "pinned host topology (lane sources delta-coded per vector [wg_encode_lanes], voff[, weights as bytes when <= 255]) -> H2D in up to 8 chunks overlapped with wg_decode_lanes + wg_index_chunk, wg_index_finish, wg_expand_destinations, wg_widen_weights -> device loop -> D2H values"}
 
 
 def host_reference_layout(g):

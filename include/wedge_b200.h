@@ -128,14 +128,81 @@ int wg_index_finish(const wg_graph *g, uint64_t max_chunk_lanes, uint64_t *d_idx
                     uint32_t *d_outdeg, void *d_scratch, size_t scratch_bytes, uint64_t *h_entries,
                     void *stream);
 /* vec_dst from per-destination vector offsets d_voff [n+1] (the run-length
- * form of PullTopology.vec_dst, graph.py:240-243).  Asynchronous. */
-int wg_expand_destinations(uint32_t n, const uint32_t *d_voff, uint64_t nvec, uint32_t *d_vdst, void *stream);
+ * form of PullTopology.vec_dst, graph.py:240-243): run heads + max-scan, with
+ * d_scratch of wg_expand_scratch_bytes(nvec) bytes.  Asynchronous. */
+size_t wg_expand_scratch_bytes(uint64_t nvec);
+int wg_expand_destinations(uint32_t n, const uint32_t *d_voff, uint64_t nvec, uint32_t *d_vdst, void *d_scratch,
+                           size_t scratch_bytes, void *stream);
 
 /* Lane weights as bytes: writes d_vw8 [nvec*width] and sets *h_fits (host) to
  * 1 iff every weight is <= 255 (else d_vw8 must not be used).  Synchronises. */
 int wg_narrow_weights(const wg_graph *g, uint8_t *d_vw8, int *h_fits, void *stream);
 /* The inverse: vw [lanes] = vw8 (e2e uploads of byte weights). Asynchronous. */
 int wg_widen_weights(uint64_t lanes, const uint8_t *d_vw8, uint32_t *d_vw, void *stream);
+
+/* Lane sources as fixed-width bit fields (the compact e2e upload format):
+ * bits = wg_lane_bits(n) = bit length of n, so every id < n and the empty
+ * lane (all ones) fit; lane l occupies bits [l*bits, (l+1)*bits) of the
+ * little-endian uint32 word stream of wg_packed_lane_words(lanes, bits)
+ * words.  Lane ranges whose begin is a multiple of 32 start on a word, so
+ * chunks of the stream can be copied and unpacked independently. */
+uint32_t wg_lane_bits(uint32_t n);
+uint64_t wg_packed_lane_words(uint64_t lanes, uint32_t bits);
+int wg_pack_lanes(uint64_t lanes, const uint32_t *d_lanes, uint32_t bits, uint32_t *d_packed,
+                  void *stream);
+/* d_lanes[l] for l in [lane_begin, lane_end) from the packed stream. */
+int wg_unpack_lanes(const uint32_t *d_packed, uint32_t bits, uint64_t lane_begin, uint64_t lane_end,
+                    uint32_t *d_lanes, void *stream);
+
+/* Delta-coded lane sources (the compact e2e upload format, codec.cu): lane
+ * codes 0 = empty, src+1 at the first lane of a destination or of a block,
+ * else src - previous src + 1; each vector's W codes take width[v] (its
+ * largest code's bit length) bits, the vectors of a block of
+ * WG_CODED_BLOCK_VECTORS back to back, every block starting on a uint32 word
+ * at bit block_base[b] (block_base has wg_coded_blocks(nvec) + 1 entries, the
+ * last = total bits).  Lanes must ascend within each destination (the pull
+ * layout, graph.py:220-263). */
+#define WG_CODED_BLOCK_VECTORS 1024
+uint64_t wg_coded_blocks(uint64_t nvec);
+uint64_t wg_coded_max_words(uint64_t nvec, uint32_t width);
+size_t wg_coded_scratch_bytes(uint64_t nvec);
+/* Encode g's lanes: d_stream [wg_coded_max_words], d_widths [nvec],
+ * d_block_base [blocks + 1]; *h_words = stream words used.  Synchronises;
+ * WG_EINVAL when a destination's lanes are not ascending. */
+int wg_encode_lanes(const wg_graph *g, uint32_t *d_stream, uint8_t *d_widths, uint64_t *d_block_base,
+                    void *d_scratch, size_t scratch_bytes, uint64_t *h_words, void *stream);
+/* Decode blocks [block_begin, block_end) into d_vsrc (needs d_vdst of every
+ * vector of those blocks and the one before). */
+int wg_decode_lanes(uint64_t nvec, uint32_t width, const uint32_t *d_vdst, const uint32_t *d_stream,
+                    const uint8_t *d_widths, const uint64_t *d_block_base, uint64_t block_begin,
+                    uint64_t block_end, uint32_t *d_vsrc, void *stream);
+
+/* Placed index: the edge index of wg_build_index up to the order inside each
+ * source's position list (the engine does not depend on it), built without a
+ * sort from the out-degrees g->outdeg (the `degrees` input of
+ * run_until_convergence, engine.py:330) under the claim that every index
+ * length equals the degree (no parallel edges).  begin: d_idx_off = scan of
+ * the degrees; chunk / coded: each lane of the vectors (blocks) takes the
+ * next slot of its source (coded also decodes the blocks into g->vsrc);
+ * end: synchronises, *h_ok = 1 iff the claim held and the index is complete
+ * (else rebuild it with wg_build_index).  Scratch of
+ * wg_index_placed_scratch_bytes(n) bytes, shared by the calls. */
+size_t wg_index_placed_scratch_bytes(uint32_t n);
+int wg_index_place_begin(const wg_graph *g, uint64_t *d_idx_off, void *d_scratch, size_t scratch_bytes,
+                         void *stream);
+int wg_index_place_chunk(const wg_graph *g, uint64_t v_begin, uint64_t v_end, uint64_t *d_idx_off,
+                         uint32_t *d_idx_pos, void *d_scratch, size_t scratch_bytes, void *stream);
+int wg_index_place_coded(const wg_graph *g, const uint32_t *d_stream, const uint8_t *d_widths,
+                         const uint64_t *d_block_base, uint64_t block_begin, uint64_t block_end,
+                         uint64_t *d_idx_off, uint32_t *d_idx_pos, void *d_scratch, size_t scratch_bytes,
+                         void *stream);
+int wg_index_place_end(const wg_graph *g, void *d_scratch, size_t scratch_bytes, int *h_ok, void *stream);
+
+/* wg_index_chunk over delta-coded blocks [block_begin, block_end): decodes
+ * them into g->vsrc (needs g->vdst) and adds their index entries. */
+int wg_index_chunk_coded(const wg_graph *g, const uint32_t *d_stream, const uint8_t *d_widths,
+                         const uint64_t *d_block_base, uint64_t block_begin, uint64_t block_end, uint32_t chunk,
+                         uint64_t max_chunk_lanes, void *d_scratch, size_t scratch_bytes, void *stream);
 
 /* ---------------- per-call kernels (backend protocol, kernels.py:55-125) --- */
 /* Workspace for wg_transform / wg_pull_wedge / wg_covered_groups. */

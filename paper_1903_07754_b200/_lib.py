@@ -57,6 +57,7 @@ class WgRunParams(ctypes.Structure):
 WG_RUN_FIRST_HIT = 1
 WG_RUN_KEEP_LISTS = 2
 WG_RUN_IDENTITY_INIT = 8
+WG_CODED_BLOCK_VECTORS = 1024
 
 
 EXPORTS = [
@@ -71,7 +72,10 @@ EXPORTS = [
     "wg_debug_phase_buffer", "wg_index_scratch_bytes", "wg_build_index", "wg_expand_destinations",
     "wg_narrow_weights", "wg_widen_weights", "wg_exchange_bytes", "wg_exchange_pack_all",
     "wg_exchange_apply_all", "wg_index_chunked_scratch_bytes", "wg_index_chunk", "wg_index_finish",
-    "wg_pagerank_prep", "wg_pagerank_pull",
+    "wg_pagerank_prep", "wg_pagerank_pull", "wg_lane_bits", "wg_packed_lane_words", "wg_pack_lanes",
+    "wg_unpack_lanes", "wg_coded_blocks", "wg_coded_max_words", "wg_coded_scratch_bytes", "wg_encode_lanes",
+    "wg_decode_lanes", "wg_index_chunk_coded", "wg_expand_scratch_bytes", "wg_index_placed_scratch_bytes",
+    "wg_index_place_begin", "wg_index_place_chunk", "wg_index_place_coded", "wg_index_place_end",
 ]
 
 _LIB = None
@@ -128,6 +132,17 @@ def load(path: os.PathLike | str | None = None):
         "wg_pagerank_prep": (ctypes.c_int, [c_u32, ctypes.c_int, ctypes.c_double, c_vp, c_vp, c_vp, c_vp,
                                             c_vp, c_vp]),
         "wg_pagerank_pull": (ctypes.c_int, [G, c_vp, c_vp, c_u32, c_vp]),
+        "wg_lane_bits": (c_u32, [c_u32]),
+        "wg_packed_lane_words": (c_u64, [c_u64, c_u32]),
+        "wg_pack_lanes": (ctypes.c_int, [c_u64, c_vp, c_u32, c_vp, c_vp]),
+        "wg_unpack_lanes": (ctypes.c_int, [c_vp, c_u32, c_u64, c_u64, c_vp, c_vp]),
+        "wg_coded_blocks": (c_u64, [c_u64]),
+        "wg_coded_max_words": (c_u64, [c_u64, c_u32]),
+        "wg_coded_scratch_bytes": (ctypes.c_size_t, [c_u64]),
+        "wg_encode_lanes": (ctypes.c_int, [G, c_vp, c_vp, c_vp, c_vp, ctypes.c_size_t, u64p, c_vp]),
+        "wg_decode_lanes": (ctypes.c_int, [c_u64, c_u32, c_vp, c_vp, c_vp, c_vp, c_u64, c_u64, c_vp, c_vp]),
+        "wg_index_chunk_coded": (ctypes.c_int, [G, c_vp, c_vp, c_vp, c_u64, c_u64, c_u32, c_u64, c_vp,
+                                                ctypes.c_size_t, c_vp]),
         "wg_rmat_edges": (ctypes.c_int, [c_u32, c_u64, c_u64, c_u64, c_u64, c_u64,
                                          ctypes.POINTER(ctypes.c_double), c_vp, c_vp, c_vp]),
         "wg_canonical_scratch_bytes": (ctypes.c_size_t, [c_u64]),
@@ -153,7 +168,14 @@ def load(path: os.PathLike | str | None = None):
         "wg_debug_phase_buffer": (ctypes.c_int, [c_vp, c_u64]),
         "wg_index_scratch_bytes": (ctypes.c_size_t, [c_u64, c_u32]),
         "wg_build_index": (ctypes.c_int, [G, c_vp, c_vp, c_vp, c_vp, ctypes.c_size_t, u64p, c_vp]),
-        "wg_expand_destinations": (ctypes.c_int, [c_u32, c_vp, c_u64, c_vp, c_vp]),
+        "wg_expand_destinations": (ctypes.c_int, [c_u32, c_vp, c_u64, c_vp, c_vp, ctypes.c_size_t, c_vp]),
+        "wg_expand_scratch_bytes": (ctypes.c_size_t, [c_u64]),
+        "wg_index_placed_scratch_bytes": (ctypes.c_size_t, [c_u32]),
+        "wg_index_place_begin": (ctypes.c_int, [G, c_vp, c_vp, ctypes.c_size_t, c_vp]),
+        "wg_index_place_chunk": (ctypes.c_int, [G, c_u64, c_u64, c_vp, c_vp, c_vp, ctypes.c_size_t, c_vp]),
+        "wg_index_place_coded": (ctypes.c_int, [G, c_vp, c_vp, c_vp, c_u64, c_u64, c_vp, c_vp, c_vp,
+                                                ctypes.c_size_t, c_vp]),
+        "wg_index_place_end": (ctypes.c_int, [G, c_vp, ctypes.c_size_t, ctypes.POINTER(ctypes.c_int), c_vp]),
         "wg_narrow_weights": (ctypes.c_int, [G, c_vp, ctypes.POINTER(ctypes.c_int), c_vp]),
         "wg_widen_weights": (ctypes.c_int, [c_u64, c_vp, c_vp, c_vp]),
         "wg_exchange_bytes": (c_u64, [c_u64, ctypes.c_int]),

@@ -34,6 +34,18 @@ int cuda_fail(cudaError_t e, const char *what);
     } while (0)
 
 int sm_count();
+// codec.cu: decode delta-coded blocks [b0, b1) into vsrc; with keys/vals also
+// the chunk-relative (source or pad, vector) pairs of the chunked index build
+int launch_decode_lanes(uint64_t nvec, uint32_t width, const uint32_t *vdst, const uint32_t *stream,
+                        const uint8_t *widths, const uint64_t *block_base, uint64_t b0, uint64_t b1, uint32_t *vsrc,
+                        uint32_t *keys, uint32_t *vals, uint32_t pad, cudaStream_t s);
+// codec.cu: decode blocks [b0, b1) and place each lane in the index
+// (layout.cu place_one: slot = fill[source]++ behind off[source])
+int launch_decode_place(uint64_t nvec, uint32_t width, const uint32_t *vdst, const uint32_t *stream,
+                        const uint8_t *widths, const uint64_t *block_base, uint64_t b0, uint64_t b1, uint32_t *vsrc,
+                        const uint64_t *off, const uint32_t *deg, uint32_t *fill, uint32_t *pos, unsigned *bad,
+                        cudaStream_t s);
+
 void count_launch(uint64_t k = 1);
 int timer_begin(void *timer, int kind, int64_t it, cudaStream_t s);
 void timer_end(void *timer, int slot, cudaStream_t s);
@@ -158,6 +170,24 @@ __device__ __forceinline__ T block_sum(T v, T *smem) {
     T t;
     block_exclusive_sum(v, smem, &t);
     return t;
+}
+
+// Placed index (layout.cu): lane (source s, vector vec) takes the next slot of
+// s's list behind off[s]; lanes of a warp with the same source share one
+// atomic (RMAT hubs open most destination runs).  Warp-collective.
+__device__ __forceinline__ void place_one(uint32_t s, bool live, uint32_t vec, const uint64_t *off,
+                                          const uint32_t *deg, uint32_t *fill, uint32_t *pos, unsigned *bad) {
+    const uint32_t key = live ? s : WG_NO_LANE;
+    const unsigned group = __match_any_sync(FULL, key);
+    if (!live) return;
+    const unsigned lane = threadIdx.x & 31u;
+    const unsigned leader = __ffs(group) - 1;
+    uint32_t base = 0;
+    if (lane == leader) base = atomicAdd(&fill[s], (uint32_t)__popc(group));
+    base = __shfl_sync(group, base, leader);
+    const uint32_t slot = base + __popc(group & lanemask_lt());
+    if (slot < deg[s]) pos[off[s] + slot] = vec;
+    else *bad = 1u;
 }
 
 }  // namespace wg

@@ -102,12 +102,12 @@ unsigned grid_1d(uint64_t work) { return grid_for(work, 256 * 8, 16); }
 
 // (source, vector) pair of lane k; padding lanes get `pad` (> every source)
 __global__ void lane_pairs(uint64_t lanes, const uint32_t *vsrc, int width, uint32_t pad, uint32_t *keys,
-                           uint32_t *vals) {
+                           uint32_t *vals, uint32_t vbase) {
     for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < lanes;
          k += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t s = vsrc[k];
         keys[k] = s == WG_NO_LANE ? pad : s;
-        vals[k] = (uint32_t)(k / width);
+        vals[k] = vbase + (uint32_t)(k / width);
     }
 }
 
@@ -137,12 +137,6 @@ __global__ void pair_bounds(uint64_t m, const uint32_t *keys, const uint32_t *va
         }
         if (d) *dup = 1u;
     }
-}
-
-__global__ void offset_vectors(uint64_t m, uint32_t base, uint32_t *vals) {
-    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m;
-         e += (uint64_t)gridDim.x * blockDim.x)
-        vals[e] += base;
 }
 
 __global__ void pack_pairs(uint64_t m, const uint32_t *keys, const uint32_t *vals, uint64_t *out) {
@@ -178,13 +172,53 @@ __global__ void widen_weights(uint64_t lanes, const uint8_t *vw8, uint32_t *vw) 
         vw[i] = vw8[i];
 }
 
-// vdst[v] = d for v in [voff[d], voff[d+1]): a thread per destination (most
-// runs are one or two vectors; adjacent threads write adjacent vectors)
-__global__ void expand_destinations(uint32_t n, const uint32_t *voff, uint32_t *vdst) {
+// Lane sources as fixed-width bit fields (the e2e upload format): lane l
+// occupies bits [l*bits, (l+1)*bits) of the little-endian word stream, the
+// empty lane (0xFFFFFFFF) is the all-ones field.  pack: a thread per output
+// word ORs in the fields overlapping it; unpack: a thread per lane.
+__global__ void pack_lanes(uint64_t lanes, const uint32_t *src, uint32_t bits, uint64_t words,
+                           uint32_t *out) {
+    const uint32_t mask = bits >= 32 ? 0xffffffffu : (1u << bits) - 1u;
+    for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < words;
+         w += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t bit0 = w << 5;
+        const uint64_t l0 = bit0 / bits;
+        uint64_t l1 = (bit0 + 31) / bits;
+        if (l1 >= lanes) l1 = lanes - 1;
+        uint32_t acc = 0;
+        for (uint64_t l = l0; l <= l1; ++l) {
+            const uint32_t v = src[l] & mask;  // 0xFFFFFFFF -> all ones
+            const int64_t off = (int64_t)(l * bits) - (int64_t)bit0;
+            acc |= off >= 0 ? v << off : v >> (-off);
+        }
+        out[w] = acc;
+    }
+}
+
+__global__ void unpack_lanes(const uint32_t *packed, uint32_t bits, uint64_t lane0, uint64_t lane1,
+                             uint32_t *dst) {
+    const uint32_t mask = (1u << bits) - 1u;
+    for (uint64_t l = lane0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; l < lane1;
+         l += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t bit = l * bits;
+        const uint64_t w = bit >> 5;
+        const uint32_t sh = (uint32_t)(bit & 31);
+        uint64_t x = packed[w];
+        if (sh + bits > 32) x |= (uint64_t)packed[w + 1] << 32;
+        const uint32_t v = (uint32_t)(x >> sh) & mask;
+        dst[l] = v == mask ? WG_NO_LANE : v;
+    }
+}
+
+// vdst[v] = d for v in [voff[d], voff[d+1]): every non-empty destination
+// writes its id at its first vector, an inclusive max-scan fills the runs
+// (balanced by vectors; RMAT's low ids hold most of the vectors, so any
+// per-destination work split is badly skewed).
+__global__ void mark_run_heads(uint32_t n, const uint32_t *voff, uint32_t *vdst) {
     for (uint64_t d = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; d < n;
          d += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t a = voff[d], b = voff[d + 1];
-        for (uint32_t v = a; v < b; ++v) vdst[v] = (uint32_t)d;
+        const uint32_t a = voff[d];
+        if (voff[d + 1] > a) vdst[a] = (uint32_t)d;
     }
 }
 
@@ -386,7 +420,7 @@ int wg_build_index(const wg_graph *g, uint64_t *d_idx_off, uint32_t *d_idx_pos, 
     // the padding key must exceed every real source so padding lanes sort last
     const int sb = bits_for((uint64_t)n + 1);
     const uint32_t pad = sb >= 32 ? 0xffffffffu : (1u << sb) - 1u;
-    lane_pairs<<<grid_1d(lanes), 256, 0, s>>>(lanes, g->vsrc, (int)g->width, pad, k0, v0);
+    lane_pairs<<<grid_1d(lanes), 256, 0, s>>>(lanes, g->vsrc, (int)g->width, pad, k0, v0, 0u);
     ::wg::count_launch();
     WG_CHECK_LAUNCH("lane_pairs");
     cub::DoubleBuffer<uint32_t> kb(k0, k1), vb(v0, v1);
@@ -521,8 +555,82 @@ size_t wg_index_chunked_scratch_bytes(uint64_t lanes, uint64_t max_chunk_lanes, 
            carve_size(index_temp_bytes(C > n ? C : (uint64_t)n + 1, n)) + 1024;
 }
 
-int wg_index_chunk(const wg_graph *g, uint64_t v_begin, uint64_t v_end, uint32_t chunk,
-                   uint64_t max_chunk_lanes, void *d_scratch, size_t scratch_bytes, void *stream) {
+}  // extern "C"
+
+namespace {
+
+// Placed index: with the out-degrees known up front (the `degrees` input of
+// run_until_convergence, engine.py:330), every source's list starts at the
+// exclusive scan of the degrees, and each lane takes the next slot of its
+// source with an atomic as its chunk arrives -- no sort, and the work
+// overlaps the upload.  The lists are those of the sorted builder up to the
+// order inside each list (the engine never relies on it: group bits are
+// idempotent, appends test the old bit).  The claim "lens = degrees" is
+// verified: a lane repeating the (source, vector) pair before it, a slot past
+// the source's degree, or a list left short sets *bad, and the caller falls
+// back to the sorted, de-duplicating builder.
+__global__ void place_lanes(uint64_t c0, uint64_t cl, int width, const uint32_t *vsrc, const uint64_t *off,
+                            const uint32_t *deg, uint32_t *fill, uint32_t *pos, unsigned *bad) {
+    const unsigned lane = threadIdx.x & 31u;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); b < cl; b += stride) {
+        const uint64_t l = c0 + b + lane;
+        const bool in = b + lane < cl;
+        const uint32_t s = in ? vsrc[l] : WG_NO_LANE;
+        bool live = s != WG_NO_LANE;
+        if (live && (l % width) != 0 && vsrc[l - 1] == s) {  // repeated (source, vector) pair
+            *bad = 1u;
+            live = false;
+        }
+        place_one(s, live, (uint32_t)(l / width), off, deg, fill, pos, bad);
+    }
+}
+
+__global__ void check_fill(uint32_t n, const uint32_t *deg, const uint32_t *fill, unsigned *bad) {
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
+         v += (uint64_t)gridDim.x * blockDim.x)
+        if (fill[v] != deg[v]) *bad = 1u;
+}
+
+struct PlaceScratch {
+    uint64_t *deg64;  // [n+1]
+    uint32_t *fill;   // [n+1]
+    unsigned *bad;
+    void *temp;
+    size_t temp_bytes;
+};
+
+int carve_place(uint32_t n, void *scratch, size_t bytes, PlaceScratch *ps) {
+    Carve cv{(char *)scratch, 0, bytes};
+    const uint64_t m = (uint64_t)n + 1;
+    ps->deg64 = cv.take<uint64_t>(m);
+    ps->fill = cv.take<uint32_t>(m);
+    ps->bad = cv.take<unsigned>(4);
+    ps->temp_bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, ps->temp_bytes, (uint64_t *)nullptr, (uint64_t *)nullptr, (int64_t)m);
+    ps->temp = cv.take<char>(ps->temp_bytes);
+    if (!ps->temp) {
+        set_error("placed index scratch too small (%zu bytes)", bytes);
+        return WG_ENOSPACE;
+    }
+    return WG_OK;
+}
+
+__global__ void widen_degrees(uint32_t n, const uint32_t *deg, uint64_t *deg64) {
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
+         v += (uint64_t)gridDim.x * blockDim.x)
+        deg64[v] = deg[v];
+}
+
+struct CodedIn {
+    const uint32_t *stream;
+    const uint8_t *widths;
+    const uint64_t *block_base;
+    uint64_t b0, b1;
+};
+
+int index_chunk(const wg_graph *g, uint64_t v_begin, uint64_t v_end, uint32_t chunk, uint64_t max_chunk_lanes,
+                void *d_scratch, size_t scratch_bytes, cudaStream_t s, const CodedIn *coded) {
     WG_REQUIRE(g && g->vsrc, "null argument");
     WG_REQUIRE(v_begin <= v_end && v_end <= g->nvec, "bad vector range");
     const uint64_t lanes = g->nvec * g->width, w = g->width;
@@ -532,7 +640,6 @@ int wg_index_chunk(const wg_graph *g, uint64_t v_begin, uint64_t v_end, uint32_t
     ChunkScratch cs;
     int rc = carve_chunks(lanes, max_chunk_lanes, g->n, d_scratch, scratch_bytes, &cs);
     if (rc) return rc;
-    cudaStream_t s = as_stream(stream);
     const uint32_t n = g->n;
     if (chunk == 0) {
         WG_CUDA(cudaMemsetAsync(cs.pre, 0, ((uint64_t)n + 1) * 4, s));
@@ -542,17 +649,24 @@ int wg_index_chunk(const wg_graph *g, uint64_t v_begin, uint64_t v_end, uint32_t
     const int sb = bits_for((uint64_t)n + 1);
     const uint32_t pad = sb >= 32 ? 0xffffffffu : (1u << sb) - 1u;
     uint32_t *k = cs.keys + c0, *v = cs.vals + c0;
-    lane_pairs<<<grid_1d(cl), 256, 0, s>>>(cl, g->vsrc + c0, (int)w, pad, k, v);
-    ::wg::count_launch();
-    // lane_pairs numbered vectors from 0 inside the chunk: shift to global ids
-    WG_CHECK_LAUNCH("lane_pairs");
-    cub::DoubleBuffer<uint32_t> kb(k, cs.kalt), vb(v, cs.valt);
+    // the pairs go where an odd / even number of 8-bit passes leaves the sorted
+    // result in k / v (a copy fixes a wrong guess)
+    const bool odd = ((sb + 7) / 8) & 1;
+    uint32_t *kin = odd ? cs.kalt : k, *vin = odd ? cs.valt : v;
+    if (coded) {
+        rc = launch_decode_lanes(g->nvec, g->width, g->vdst, coded->stream, coded->widths, coded->block_base,
+                                 coded->b0, coded->b1, const_cast<uint32_t *>(g->vsrc), kin, vin, pad, s);
+        if (rc) return rc;
+    } else {
+        lane_pairs<<<grid_1d(cl), 256, 0, s>>>(cl, g->vsrc + c0, (int)w, pad, kin, vin, (uint32_t)v_begin);
+        ::wg::count_launch();
+        WG_CHECK_LAUNCH("lane_pairs");
+    }
+    cub::DoubleBuffer<uint32_t> kb(kin, odd ? k : cs.kalt), vb(vin, odd ? v : cs.valt);
     size_t tb = cs.temp_bytes;
     WG_CUDA(cub::DeviceRadixSort::SortPairs(cs.temp, tb, kb, vb, (int64_t)cl, 0, sb, s));
     if (kb.Current() != k) WG_CUDA(cudaMemcpyAsync(k, kb.Current(), cl * 4, cudaMemcpyDeviceToDevice, s));
     if (vb.Current() != v) WG_CUDA(cudaMemcpyAsync(v, vb.Current(), cl * 4, cudaMemcpyDeviceToDevice, s));
-    offset_vectors<<<grid_1d(cl), 256, 0, s>>>(cl, (uint32_t)v_begin, v);
-    ::wg::count_launch();
     // valid entries of the chunk = all but its padding lanes (sorted last);
     // bounds over the whole chunk, padding runs land in first/last[pad] <= n
     WG_CUDA(cudaMemsetAsync(cs.first, 0xff, ((uint64_t)n + 1) * 8, s));
@@ -560,6 +674,108 @@ int wg_index_chunk(const wg_graph *g, uint64_t v_begin, uint64_t v_end, uint32_t
     chunk_ranks<<<grid_1d(cl), 256, 0, s>>>(cl, k, cs.first, cs.pre, pad, cs.rank + c0); ::wg::count_launch();
     chunk_totals<<<grid_1d(n), 256, 0, s>>>(n, cs.first, cs.last, cs.pre); ::wg::count_launch();
     WG_CHECK_LAUNCH("index chunk");
+    return WG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int wg_index_chunk(const wg_graph *g, uint64_t v_begin, uint64_t v_end, uint32_t chunk,
+                   uint64_t max_chunk_lanes, void *d_scratch, size_t scratch_bytes, void *stream) {
+    return index_chunk(g, v_begin, v_end, chunk, max_chunk_lanes, d_scratch, scratch_bytes, as_stream(stream),
+                       nullptr);
+}
+
+int wg_index_chunk_coded(const wg_graph *g, const uint32_t *d_stream, const uint8_t *d_widths,
+                         const uint64_t *d_block_base, uint64_t block_begin, uint64_t block_end, uint32_t chunk,
+                         uint64_t max_chunk_lanes, void *d_scratch, size_t scratch_bytes, void *stream) {
+    WG_REQUIRE(g && d_stream && d_widths && d_block_base && g->vdst, "null argument");
+    WG_REQUIRE(block_begin <= block_end && block_end <= wg_coded_blocks(g->nvec), "bad block range");
+    const uint64_t v0 = block_begin * WG_CODED_BLOCK_VECTORS;
+    const uint64_t v1 = block_end * WG_CODED_BLOCK_VECTORS < g->nvec ? block_end * WG_CODED_BLOCK_VECTORS : g->nvec;
+    CodedIn in{d_stream, d_widths, d_block_base, block_begin, block_end};
+    return index_chunk(g, v0 < v1 ? v0 : v1, v1, chunk, max_chunk_lanes, d_scratch, scratch_bytes, as_stream(stream),
+                       &in);
+}
+
+size_t wg_index_placed_scratch_bytes(uint32_t n) {
+    const uint64_t m = (uint64_t)n + 1;
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, (uint64_t *)nullptr, (uint64_t *)nullptr, (int64_t)m);
+    return carve_size(m * 8) + carve_size(m * 4) + carve_size(16) + carve_size(tb) + 1024;
+}
+
+int wg_index_place_begin(const wg_graph *g, uint64_t *d_idx_off, void *d_scratch, size_t scratch_bytes,
+                         void *stream) {
+    WG_REQUIRE(g && g->outdeg && d_idx_off, "null argument");
+    WG_REQUIRE(g->n < 0xffffffffu && g->nvec < (1ull << 32), "graph too large for the index");
+    cudaStream_t s = as_stream(stream);
+    PlaceScratch ps;
+    int rc = carve_place(g->n, d_scratch, scratch_bytes, &ps);
+    if (rc) return rc;
+    const uint32_t n = g->n;
+    WG_CUDA(cudaMemsetAsync(ps.fill, 0, ((uint64_t)n + 1) * 4, s));
+    WG_CUDA(cudaMemsetAsync(ps.bad, 0, 16, s));
+    WG_CUDA(cudaMemsetAsync(ps.deg64 + n, 0, 8, s));
+    if (n) {
+        widen_degrees<<<grid_1d(n), 256, 0, s>>>(n, g->outdeg, ps.deg64);
+        ::wg::count_launch();
+    }
+    size_t tb = ps.temp_bytes;
+    WG_CUDA(cub::DeviceScan::ExclusiveSum(ps.temp, tb, ps.deg64, d_idx_off, (int64_t)n + 1, s));
+    WG_CHECK_LAUNCH("index place begin");
+    return WG_OK;
+}
+
+int wg_index_place_chunk(const wg_graph *g, uint64_t v_begin, uint64_t v_end, uint64_t *d_idx_off,
+                         uint32_t *d_idx_pos, void *d_scratch, size_t scratch_bytes, void *stream) {
+    WG_REQUIRE(g && g->vsrc && g->outdeg && d_idx_off && d_idx_pos, "null argument");
+    WG_REQUIRE(v_begin <= v_end && v_end <= g->nvec, "bad vector range");
+    cudaStream_t s = as_stream(stream);
+    PlaceScratch ps;
+    int rc = carve_place(g->n, d_scratch, scratch_bytes, &ps);
+    if (rc) return rc;
+    const uint64_t c0 = v_begin * g->width, cl = (v_end - v_begin) * g->width;
+    if (cl) {
+        place_lanes<<<grid_for(cl, 256, 8), 256, 0, s>>>(c0, cl, (int)g->width, g->vsrc, d_idx_off, g->outdeg,
+                                                         ps.fill, d_idx_pos, ps.bad);
+        ::wg::count_launch();
+    }
+    WG_CHECK_LAUNCH("index place");
+    return WG_OK;
+}
+
+int wg_index_place_coded(const wg_graph *g, const uint32_t *d_stream, const uint8_t *d_widths,
+                         const uint64_t *d_block_base, uint64_t block_begin, uint64_t block_end,
+                         uint64_t *d_idx_off, uint32_t *d_idx_pos, void *d_scratch, size_t scratch_bytes,
+                         void *stream) {
+    WG_REQUIRE(g && g->vsrc && g->vdst && g->outdeg && d_idx_off && d_idx_pos, "null argument");
+    WG_REQUIRE(d_stream && d_widths && d_block_base, "null argument");
+    WG_REQUIRE(block_begin <= block_end && block_end <= wg_coded_blocks(g->nvec), "bad block range");
+    PlaceScratch ps;
+    int rc = carve_place(g->n, d_scratch, scratch_bytes, &ps);
+    if (rc) return rc;
+    return launch_decode_place(g->nvec, g->width, g->vdst, d_stream, d_widths, d_block_base, block_begin, block_end,
+                               const_cast<uint32_t *>(g->vsrc), d_idx_off, g->outdeg, ps.fill, d_idx_pos, ps.bad,
+                               as_stream(stream));
+}
+
+int wg_index_place_end(const wg_graph *g, void *d_scratch, size_t scratch_bytes, int *h_ok, void *stream) {
+    WG_REQUIRE(g && g->outdeg && h_ok, "null argument");
+    cudaStream_t s = as_stream(stream);
+    PlaceScratch ps;
+    int rc = carve_place(g->n, d_scratch, scratch_bytes, &ps);
+    if (rc) return rc;
+    if (g->n) {
+        check_fill<<<grid_1d(g->n), 256, 0, s>>>(g->n, g->outdeg, ps.fill, ps.bad);
+        ::wg::count_launch();
+    }
+    WG_CHECK_LAUNCH("index place end");
+    unsigned bad = 1;
+    WG_CUDA(cudaMemcpyAsync(&bad, ps.bad, 4, cudaMemcpyDeviceToHost, s));
+    WG_CUDA(cudaStreamSynchronize(s));
+    *h_ok = bad ? 0 : 1;
     return WG_OK;
 }
 
@@ -628,12 +844,58 @@ int wg_widen_weights(uint64_t lanes, const uint8_t *d_vw8, uint32_t *d_vw, void 
     return WG_OK;
 }
 
-int wg_expand_destinations(uint32_t n, const uint32_t *d_voff, uint64_t nvec, uint32_t *d_vdst, void *stream) {
+uint32_t wg_lane_bits(uint32_t n) {
+    uint32_t b = 1;
+    while (b < 32 && (n >> b) != 0) ++b;  // bit length of n: n itself is never a vertex id
+    return b;
+}
+
+uint64_t wg_packed_lane_words(uint64_t lanes, uint32_t bits) { return (lanes * bits + 31) / 32; }
+
+int wg_pack_lanes(uint64_t lanes, const uint32_t *d_lanes, uint32_t bits, uint32_t *d_packed,
+                  void *stream) {
+    WG_REQUIRE(bits >= 1 && bits <= 31, "lane bit width must be in [1, 31], got %u", bits);
+    WG_REQUIRE((d_lanes && d_packed) || lanes == 0, "null argument");
+    if (lanes == 0) return WG_OK;
+    cudaStream_t s = as_stream(stream);
+    const uint64_t words = wg_packed_lane_words(lanes, bits);
+    pack_lanes<<<grid_1d(words), 256, 0, s>>>(lanes, d_lanes, bits, words, d_packed); ::wg::count_launch();
+    WG_CHECK_LAUNCH("pack_lanes");
+    return WG_OK;
+}
+
+int wg_unpack_lanes(const uint32_t *d_packed, uint32_t bits, uint64_t lane_begin, uint64_t lane_end,
+                    uint32_t *d_lanes, void *stream) {
+    WG_REQUIRE(bits >= 1 && bits <= 31, "lane bit width must be in [1, 31], got %u", bits);
+    WG_REQUIRE(lane_begin <= lane_end, "bad lane range");
+    if (lane_end == lane_begin) return WG_OK;
+    WG_REQUIRE(d_packed && d_lanes, "null argument");
+    cudaStream_t s = as_stream(stream);
+    unpack_lanes<<<grid_1d(lane_end - lane_begin), 256, 0, s>>>(d_packed, bits, lane_begin, lane_end, d_lanes);
+    ::wg::count_launch();
+    WG_CHECK_LAUNCH("unpack_lanes");
+    return WG_OK;
+}
+
+size_t wg_expand_scratch_bytes(uint64_t nvec) {
+    size_t tb = 0;
+    cub::DeviceScan::InclusiveScan(nullptr, tb, (uint32_t *)nullptr, (uint32_t *)nullptr, cub::Max(),
+                                   (int64_t)(nvec ? nvec : 1));
+    return tb + 256;
+}
+
+int wg_expand_destinations(uint32_t n, const uint32_t *d_voff, uint64_t nvec, uint32_t *d_vdst, void *d_scratch,
+                           size_t scratch_bytes, void *stream) {
     WG_REQUIRE(d_voff && (d_vdst || nvec == 0), "null argument");
     cudaStream_t s = as_stream(stream);
     if (nvec == 0 || n == 0) return WG_OK;
-    expand_destinations<<<grid_1d(n), 256, 0, s>>>(n, d_voff, d_vdst); ::wg::count_launch();
-    WG_CHECK_LAUNCH("expand_destinations");
+    size_t tb = 0;
+    WG_CUDA(cub::DeviceScan::InclusiveScan(nullptr, tb, d_vdst, d_vdst, cub::Max(), (int64_t)nvec, s));
+    WG_REQUIRE(d_scratch && scratch_bytes >= tb, "scratch too small (wg_expand_scratch_bytes)");
+    WG_CUDA(cudaMemsetAsync(d_vdst, 0, nvec * 4, s));
+    mark_run_heads<<<grid_1d(n), 256, 0, s>>>(n, d_voff, d_vdst); ::wg::count_launch();
+    WG_CHECK_LAUNCH("mark_run_heads");
+    WG_CUDA(cub::DeviceScan::InclusiveScan(d_scratch, tb, d_vdst, d_vdst, cub::Max(), (int64_t)nvec, s));
     return WG_OK;
 }
 

@@ -187,7 +187,6 @@ class DeviceGraph:
         L = _lib.load()
         dev = vsrc.device
         vdst = torch.empty(nvec + SLACK, dtype=torch.int32, device=dev)
-        check(L.wg_expand_destinations(n, _ptr(voff), nvec, _ptr(vdst), _lib.stream_ptr(stream)))
         idx_off = torch.empty(n + 1, dtype=torch.int64, device=dev)
         idx_pos = torch.empty(max(edges, 1), dtype=torch.int32, device=dev)
         outdeg = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
@@ -195,37 +194,106 @@ class DeviceGraph:
         g.rebuild_derived(voff, scratch, stream)
         return g
 
-    def upload_rebuild(self, host: dict, dev: dict, chunks: int = 4, scratch=None, copy_stream=None) -> int:
+    def lane_bits(self) -> int:
+        """Bit width of one lane in the packed upload format (wg_lane_bits)."""
+        return int(_lib.load().wg_lane_bits(self.n))
+
+    def pack_lanes(self, stream=None):
+        """vsrc as fixed-width bit fields (wg_pack_lanes): (int32 words, bits)."""
+        torch = _torch()
+        L = _lib.load()
+        bits = self.lane_bits()
+        lanes = self.nvec * self.width
+        words = int(L.wg_packed_lane_words(lanes, bits))
+        out = torch.empty(max(words, 1), dtype=torch.int32, device=self.vsrc.device)
+        check(L.wg_pack_lanes(lanes, _ptr(self.vsrc), bits, _ptr(out), _lib.stream_ptr(stream)))
+        return out[:words], bits
+
+    def encode_lanes(self, stream=None) -> dict:
+        """vsrc in the delta-coded upload format (wg_encode_lanes): device
+        tensors "lane_stream" (int32 words), "lane_widths" (uint8 per vector)
+        and "lane_blocks" (int64 block bit offsets, blocks + 1)."""
+        torch = _torch()
+        L = _lib.load()
+        dev = self.vsrc.device
+        nb = int(L.wg_coded_blocks(self.nvec))
+        words = torch.empty(max(int(L.wg_coded_max_words(self.nvec, self.width)), 1), dtype=torch.int32, device=dev)
+        widths = torch.empty(max(self.nvec, 1), dtype=torch.uint8, device=dev)
+        blocks = torch.empty(nb + 1, dtype=torch.int64, device=dev)
+        scratch = torch.empty(int(L.wg_coded_scratch_bytes(self.nvec)), dtype=torch.uint8, device=dev)
+        used = ctypes.c_uint64(0)
+        check(L.wg_encode_lanes(ctypes.byref(self.struct()), _ptr(words), _ptr(widths), _ptr(blocks), _ptr(scratch),
+                                scratch.numel(), ctypes.byref(used), _lib.stream_ptr(stream)))
+        return {"lane_stream": words[: int(used.value)], "lane_widths": widths[: self.nvec], "lane_blocks": blocks}
+
+    def upload_rebuild(self, host: dict, dev: dict, chunks: int = 4, scratch=None, copy_stream=None,
+                       trace=None) -> int:
         """Copy the compact topology from pinned host memory (host["vsrc"],
-        host["voff"], optional host["vw8"] / host["vw"]) into this graph's
-        device arrays (dev[...] views of them) and rebuild vec_dst, the edge
-        index and the out-degrees, with the index built chunk by chunk so each
-        chunk's sort overlaps the copy of the next (wg_index_chunk /
-        wg_index_finish).  Returns the index length."""
+        its bit-packed form host["vsrc_bits"] or its delta-coded form
+        host["lane_stream"/"lane_widths"/"lane_blocks"], host["voff"], optional
+        host["vw8"] / host["vw"]) into this graph's device arrays (dev[...]
+        views of them; dev["vsrc_bits"] receives the packed words) and rebuild
+        vsrc (unpacked chunk by chunk), vec_dst, the edge index and the
+        out-degrees, with the index built chunk by chunk so each chunk's sort
+        overlaps the copy of the next (wg_unpack_lanes, wg_index_chunk /
+        wg_index_finish).  With host["outdeg"] (the out-degrees, the
+        `degrees` input of the reference call) the index is placed instead:
+        offsets from the degrees, every chunk's lanes take their slots as the
+        chunk arrives (wg_index_place_*; the same lists with the order inside
+        each list unspecified, no sort), verified at the end, with the
+        sort-based builder as the fallback.  Returns the index length.  trace: an optional list that
+        receives (label, event) pairs (profiling)."""
         torch = _torch()
         L = _lib.load()
         cs = copy_stream or torch.cuda.Stream()
         main = torch.cuda.current_stream()
         W = self.width
-        cuts = [self.nvec * c // chunks for c in range(chunks + 1)]
-        max_lanes = max(cuts[c + 1] - cuts[c] for c in range(chunks)) * W
+        packed = "vsrc_bits" in host
+        coded = "lane_stream" in host
+        placed = "outdeg" in host
+        bits = self.lane_bits() if packed else 32
+        # packed chunks start on a word: lane offsets multiples of 32; coded
+        # chunks are runs of whole blocks
+        align = max(1, 32 // W) if packed else (_lib.WG_CODED_BLOCK_VECTORS if coded else 1)
+        cuts = [min(self.nvec, (self.nvec * c // chunks) // align * align) for c in range(chunks)] + [self.nvec]
+        if coded:
+            base = host["lane_blocks"].numpy()
+        max_lanes = max(max(cuts[c + 1] - cuts[c] for c in range(chunks)) * W, 1)
         need = max(int(L.wg_index_chunked_scratch_bytes(self.nvec * W, max_lanes, self.n)),
-                   int(L.wg_index_scratch_bytes(self.nvec * W, self.n)))
+                   int(L.wg_index_scratch_bytes(self.nvec * W, self.n)), int(L.wg_expand_scratch_bytes(self.nvec)),
+                   int(L.wg_index_placed_scratch_bytes(self.n)))
         if scratch is None or scratch.numel() < need:
             scratch = torch.empty(need, dtype=torch.uint8, device=self.vsrc.device)
+        words = int(host["vsrc_bits"].numel()) if packed else 0
         cs.wait_stream(main)  # the previous use of the buffers is done
         evs = []
         with torch.cuda.stream(cs):
             dev["voff"].copy_(host["voff"], non_blocking=True)
+            if placed:
+                self.outdeg[: self.n].copy_(host["outdeg"], non_blocking=True)
+            if coded:
+                dev["lane_blocks"].copy_(host["lane_blocks"], non_blocking=True)
             e = torch.cuda.Event()
             e.record(cs)
             evs.append(e)
             for c in range(chunks):
                 a, b = cuts[c] * W, cuts[c + 1] * W
-                dev["vsrc"][a:b].copy_(host["vsrc"][a:b], non_blocking=True)
-                e = torch.cuda.Event()
+                if packed:
+                    wa, wb = a * bits // 32, (words if c == chunks - 1 else b * bits // 32)
+                    dev["vsrc_bits"][wa:wb].copy_(host["vsrc_bits"][wa:wb], non_blocking=True)
+                elif coded:
+                    ba, bb = cuts[c] // align, -(-cuts[c + 1] // align)
+                    wa, wb = int(base[ba]) // 32, int(base[bb]) // 32
+                    dev["lane_stream"][wa:wb].copy_(host["lane_stream"][wa:wb], non_blocking=True)
+                    dev["lane_widths"][cuts[c]:cuts[c + 1]].copy_(host["lane_widths"][cuts[c]:cuts[c + 1]],
+                                                                  non_blocking=True)
+                else:
+                    dev["vsrc"][a:b].copy_(host["vsrc"][a:b], non_blocking=True)
+                e = torch.cuda.Event(enable_timing=trace is not None)
                 e.record(cs)
                 evs.append(e)
+                if trace is not None:
+                    trace.append((f"copied {c}", e))
             for k in ("vw8", "vw"):
                 if k in host:
                     dev[k].copy_(host[k], non_blocking=True)
@@ -234,14 +302,51 @@ class DeviceGraph:
             evs.append(e)
         st = _lib.stream_ptr()
         main.wait_event(evs[0])
-        check(L.wg_expand_destinations(self.n, _ptr(dev["voff"]), self.nvec, _ptr(self.vdst), st))
+        check(L.wg_expand_destinations(self.n, _ptr(dev["voff"]), self.nvec, _ptr(self.vdst), _ptr(scratch),
+                                       scratch.numel(), st))
         gs = ctypes.byref(self.struct())
+        if placed:
+            check(L.wg_index_place_begin(gs, _ptr(self.idx_off), _ptr(scratch), scratch.numel(), st))
         for c in range(chunks):
             main.wait_event(evs[1 + c])
-            check(L.wg_index_chunk(gs, cuts[c], cuts[c + 1], c, max_lanes, _ptr(scratch), scratch.numel(), st))
+            if packed:
+                check(L.wg_unpack_lanes(_ptr(dev["vsrc_bits"]), bits, cuts[c] * W, cuts[c + 1] * W,
+                                        _ptr(self.vsrc), st))
+            if trace is not None:
+                trace.append((f"decoded {c}", torch.cuda.Event(enable_timing=True)))
+                trace[-1][1].record(main)
+            if placed and coded:  # decode fused with the placement
+                check(L.wg_index_place_coded(gs, _ptr(dev["lane_stream"]), _ptr(dev["lane_widths"]),
+                                             _ptr(dev["lane_blocks"]), cuts[c] // align, -(-cuts[c + 1] // align),
+                                             _ptr(self.idx_off), _ptr(self.idx_pos), _ptr(scratch), scratch.numel(),
+                                             st))
+            elif placed:
+                check(L.wg_index_place_chunk(gs, cuts[c], cuts[c + 1], _ptr(self.idx_off), _ptr(self.idx_pos),
+                                             _ptr(scratch), scratch.numel(), st))
+            elif coded:  # decode fused into the chunk's pair generation
+                check(L.wg_index_chunk_coded(gs, _ptr(dev["lane_stream"]), _ptr(dev["lane_widths"]),
+                                             _ptr(dev["lane_blocks"]), cuts[c] // align, -(-cuts[c + 1] // align), c,
+                                             max_lanes, _ptr(scratch), scratch.numel(), st))
+            else:
+                check(L.wg_index_chunk(gs, cuts[c], cuts[c + 1], c, max_lanes, _ptr(scratch), scratch.numel(), st))
+            if trace is not None:
+                trace.append((f"indexed {c}", torch.cuda.Event(enable_timing=True)))
+                trace[-1][1].record(main)
         ent = ctypes.c_uint64(0)
-        check(L.wg_index_finish(gs, max_lanes, _ptr(self.idx_off), _ptr(self.idx_pos), _ptr(self.outdeg),
-                                _ptr(scratch), scratch.numel(), ctypes.byref(ent), st))
+        if placed:
+            ok = ctypes.c_int(0)
+            check(L.wg_index_place_end(gs, _ptr(scratch), scratch.numel(), ctypes.byref(ok), st))
+            if ok.value:
+                ent.value = self.edges
+            else:  # parallel edges or degrees that do not match the lanes
+                check(L.wg_build_index(gs, _ptr(self.idx_off), _ptr(self.idx_pos), _ptr(self.outdeg), _ptr(scratch),
+                                       scratch.numel(), ctypes.byref(ent), st))
+        else:
+            check(L.wg_index_finish(gs, max_lanes, _ptr(self.idx_off), _ptr(self.idx_pos), _ptr(self.outdeg),
+                                    _ptr(scratch), scratch.numel(), ctypes.byref(ent), st))
+        if trace is not None:
+            trace.append(("finished", torch.cuda.Event(enable_timing=True)))
+            trace[-1][1].record(main)
         main.wait_event(evs[-1])
         if "vw8" in host and self.vw is not None:
             check(L.wg_widen_weights(self.nvec * W, _ptr(dev["vw8"]), _ptr(self.vw), st))
@@ -254,10 +359,12 @@ class DeviceGraph:
         graphs stay valid).  Returns the index length."""
         torch = _torch()
         L = _lib.load()
-        check(L.wg_expand_destinations(self.n, _ptr(voff), self.nvec, _ptr(self.vdst), _lib.stream_ptr(stream)))
-        need = int(L.wg_index_scratch_bytes(self.nvec * self.width, self.n))
+        need = max(int(L.wg_index_scratch_bytes(self.nvec * self.width, self.n)),
+                   int(L.wg_expand_scratch_bytes(self.nvec)))
         if scratch is None or scratch.numel() < need:
             scratch = torch.empty(need, dtype=torch.uint8, device=self.vsrc.device)
+        check(L.wg_expand_destinations(self.n, _ptr(voff), self.nvec, _ptr(self.vdst), _ptr(scratch), scratch.numel(),
+                                       _lib.stream_ptr(stream)))
         ent = ctypes.c_uint64(0)
         check(L.wg_build_index(ctypes.byref(self.struct()), _ptr(self.idx_off), _ptr(self.idx_pos),
                                _ptr(self.outdeg), _ptr(scratch), scratch.numel(), ctypes.byref(ent),

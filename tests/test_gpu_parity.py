@@ -65,6 +65,52 @@ def test_device_layout_edge_cases(wg):
     assert np.array_equal(wg.build_edge_index(t).positions, ri.positions)
 
 
+def _pack_np(lanes, bits):
+    """The packed-lane format restated (wedge_b200.h wg_pack_lanes): lane l in
+    bits [l*bits, (l+1)*bits) of a little-endian bit stream, empty = all ones."""
+    mask = (1 << bits) - 1
+    v = lanes.astype(np.uint64) & mask
+    stream = np.zeros(len(lanes) * bits, dtype=np.uint8)
+    for b in range(bits):
+        stream[b::bits] = (v >> np.uint64(b)) & np.uint64(1)
+    pad = (-len(stream)) % 32
+    stream = np.concatenate([stream, np.zeros(pad, np.uint8)])
+    return np.packbits(stream.reshape(-1, 32)[:, ::-1], axis=1).view(">u4").ravel().astype(np.uint32)
+
+
+def _sorted_lists(off, pos):
+    out = pos.copy()
+    for a, b in zip(off[:-1], off[1:]):
+        out[a:b].sort()
+    return out
+
+
+def _decode_np(h, vdst, W, BV=1024):
+    """The delta-coded lane format restated (wedge_b200.h wg_encode_lanes),
+    decoded sequentially on the host."""
+    words = h["lane_stream"].numpy().view(np.uint32)
+    widths = h["lane_widths"].numpy()
+    base = h["lane_blocks"].numpy()
+    bits = np.unpackbits(words.view(np.uint8), bitorder="little")
+    out = np.empty(len(widths) * W, np.uint32)
+    pos = 0
+    prev = 0
+    for v in range(len(widths)):
+        if v % BV == 0:
+            pos = int(base[v // BV])
+        head = v % BV == 0 or vdst[v] != vdst[v - 1]
+        w = int(widths[v])
+        for j in range(W):
+            c = int(np.dot(bits[pos: pos + w].astype(np.int64), 1 << np.arange(w, dtype=np.int64)))
+            pos += w
+            if c == 0:
+                out[v * W + j] = 0xFFFFFFFF
+                continue
+            prev = c - 1 if (head and j == 0) else prev + c - 1
+            out[v * W + j] = prev
+    return out
+
+
 def test_layout_rebuilt_from_lanes(wg, golden):
     """wg_expand_destinations + wg_build_index (the e2e upload form: lanes and
     per-destination vector offsets only) reproduce vec_dst, the edge index
@@ -95,9 +141,47 @@ def test_layout_rebuilt_from_lanes(wg, golden):
             assert np.array_equal(g2.offsets_np(), g.offsets_np())
             assert np.array_equal(g2.positions_np(), g.positions_np())
             assert np.array_equal(g2.outdeg_np(), g.outdeg_np())
+        # the bit-packed upload (lanes unpacked chunk by chunk)
+        words, bits = g.pack_lanes()
+        assert np.array_equal(words.cpu().numpy().view(np.uint32), _pack_np(g.vsrc.cpu().numpy().view(np.uint32), bits))
+        hp = {"vsrc_bits": words.cpu().pin_memory(), "voff": host["voff"]}
+        for chunks in (1, 3, 7):
+            g2.vsrc.fill_(-7)
+            g2.idx_pos.zero_()
+            dp = {"vsrc_bits": torch.empty(words.numel() + 1, dtype=torch.int32, device="cuda")[: words.numel()],
+                  "voff": torch.empty_like(host["voff"], device="cuda")}
+            assert g2.upload_rebuild(hp, dp, chunks=chunks) == g.entries
+            assert torch.equal(g2.vsrc, g.vsrc)
+            assert np.array_equal(g2.positions_np(), g.positions_np())
+        # the delta-coded upload (blocks decoded chunk by chunk)
+        enc = g.encode_lanes()
+        hc = {k: v.cpu().pin_memory() for k, v in enc.items()}
+        hc["voff"] = host["voff"]
+        assert _decode_np(hc, g.vec_dst_np(), g.width).tobytes() == g.vsrc.cpu().numpy().tobytes()
+        for chunks, counted in ((1, False), (2, False), (5, False), (1, True), (3, True)):
+            g2.vsrc.fill_(-7)
+            g2.idx_pos.zero_()
+            g2.outdeg.zero_()
+            h = dict(hc, outdeg=g.outdeg[: g.n].cpu().pin_memory()) if counted else hc
+            dc = {k: torch.empty(v.numel() + 1, dtype=v.dtype, device="cuda")[: v.numel()] for k, v in h.items()}
+            # placed (degrees given): same lists up to their order; parallel
+            # edges make it fall back to the sorted builder
+            assert g2.upload_rebuild(h, dc, chunks=chunks) == g.entries
+            assert torch.equal(g2.vsrc, g.vsrc)
+            assert np.array_equal(g2.offsets_np(), g.offsets_np())
+            assert np.array_equal(g2.outdeg_np(), g.outdeg_np())
+            if counted:  # same lists, order inside each list unspecified
+                assert np.array_equal(_sorted_lists(g2.offsets_np(), g2.positions_np()), g.positions_np())
+            else:
+                assert np.array_equal(g2.positions_np(), g.positions_np())
+        # placed over raw uint32 lanes too
+        g2.idx_pos.zero_()
+        assert g2.upload_rebuild(dict(host, outdeg=g.outdeg[: g.n].cpu().pin_memory()),
+                                 {"vsrc": g2.vsrc, "voff": torch.empty_like(host["voff"], device="cuda")},
+                                 chunks=2) == g.entries
+        assert np.array_equal(_sorted_lists(g2.offsets_np(), g2.positions_np()), g.positions_np())
         assert np.array_equal(g2.vec_dst_np(), g.vec_dst_np())
         assert np.array_equal(g2.offsets_np(), g.offsets_np())
-        assert np.array_equal(g2.positions_np(), g.positions_np())
         assert np.array_equal(g2.outdeg_np(), g.outdeg_np())
         assert g2.lens_are_degrees == g.lens_are_degrees
 
