@@ -534,11 +534,17 @@ def roofline(rows, recs, n, E, weighted, filt, wl):
 def e2e_b200(args, wl, g, loop, dinit, words, kern, thr, max_it, first_hit=False, level_base=0,
              identity_init=False):
     """Same metric through the C ABI with the graph in pinned HOST memory.
-    Per step: H2D of the topology in its compact form (lanes vsrc [+ weights]
-    and per-destination vector offsets voff, i.e. PullTopology's lane_src /
-    lane_weight / vec_dst as uint32), on-device rebuild of vec_dst, the edge
-    index and the out-degrees (wg_expand_destinations + wg_build_index), the
-    device loop, D2H of the result."""
+    Per step: H2D of the topology in its compact form -- the lane sources
+    delta-coded per vector (wg_encode_lanes, ~15 bits per lane at s22), the
+    per-destination vector offsets voff, weights as bytes when <= 255, and the
+    out-degrees (the reference call's `degrees` input) -- in up to 8 chunks on
+    a copy stream; on the compute stream vec_dst from voff
+    (wg_expand_destinations), then per arrived chunk the lanes decoded and
+    either placed into the edge index at offsets scanned from the degrees
+    (wg_index_place_*, verified at the end) or sorted into it
+    (wg_index_chunk_coded / wg_index_finish, for indexes over 1 GiB); then the
+    device loop and the D2H of the values.
+    """
     import torch
     from paper_1903_07754_b200 import _lib, device as dv
 
@@ -633,7 +639,7 @@ def e2e_b200(args, wl, g, loop, dinit, words, kern, thr, max_it, first_hit=False
                 8 * sum(host[k].numel() * host[k].element_size() for k in host if k.startswith(("lane_", "vsrc")))
                 / max(1, g.nvec * g.width), 2),
             "host_format_build_s": round(t_fmt, 2), "index": "placed from the degrees" if placed else "chunked sort",
-            "path": "pinned host topology (lane sources delta-coded per vector [wg_encode_lanes], voff[, weights as bytes when <= 255]) -> H2D in up to 8 chunks overlapped with wg_decode_lanes + wg_index_chunk, wg_index_finish, wg_expand_destinations, wg_widen_weights -> device loop -> D2H values"}
+            "path": "pinned host topology (lane sources delta-coded per vector [wg_encode_lanes], voff, out-degrees[, weights as bytes when <= 255]) -> H2D in up to 8 chunks; wg_expand_destinations, per chunk wg_index_place_coded (decode + index slots; or wg_index_chunk_coded + wg_index_finish), wg_index_place_end, wg_widen_weights -> device loop -> D2H values"}
 
 
 def host_reference_layout(g):
