@@ -742,22 +742,33 @@ def run_pagerank(args, wl, el, topo, build_s):
 
 
 def e2e_pagerank(args, g, bufs):
-    """PageRank through the C ABI with the layout in pinned host memory:
-    H2D of the lanes, destinations and degrees, 20 iterations, D2H ranks."""
+    """PageRank through the C ABI with the layout in pinned host memory: H2D
+    of the compact topology (delta-coded lanes, per-destination vector
+    offsets, out-degrees; PageRank reads no edge index) in chunks on a copy
+    stream, decoded on the device as they land (wg_expand_destinations,
+    wg_decode_lanes), 20 iterations, D2H ranks."""
     import torch
     from paper_1903_07754_b200 import device as dv
-    # what wg_pagerank reads (the edge index is not used by PageRank)
-    host = {k: getattr(g, k).cpu().pin_memory() for k in ("vsrc", "vdst", "outdeg")}
+    ref = dv.pagerank(g, 20, 0.85, bufs=bufs).clone()
+    t_fmt = time.perf_counter()
+    host = {"voff": g.vector_offsets().cpu().pin_memory(), "outdeg": g.outdeg[: g.n].cpu().pin_memory()}
+    host.update({k: v.cpu().pin_memory() for k, v in g.encode_lanes().items()})
+    t_fmt = time.perf_counter() - t_fmt
     dev = {k: torch.empty(v.numel() + 64, dtype=v.dtype, device="cuda")[: v.numel()] for k, v in host.items()}
-    g2 = dv.DeviceGraph(g.n, g.width, g.edges, g.nvec, g.entries, dev["vsrc"], dev["vdst"], None,
-                        g.idx_off, g.idx_pos, dev["outdeg"])
+    lanes = g.nvec * g.width
+    vsrc = torch.empty(lanes + 64, dtype=torch.int32, device="cuda")
+    vdst = torch.empty(g.nvec + 64, dtype=torch.int32, device="cuda")
+    outdeg = torch.empty(g.n + 64, dtype=torch.int32, device="cuda")
+    g2 = dv.DeviceGraph(g.n, g.width, g.edges, g.nvec, g.entries, vsrc[:lanes], vdst[: g.nvec], None,
+                        g.idx_off, g.idx_pos, outdeg[: g.n])
     out_host = torch.empty(g.n, dtype=torch.float32).pin_memory()
     h2d = sum(v.numel() * v.element_size() for v in host.values())
     stream = torch.cuda.current_stream()
+    copy_stream = torch.cuda.Stream()
+    chunks = int(os.environ.get("WG_E2E_CHUNKS", "0")) or max(1, min(8, lanes >> 22))
 
     def one():
-        for k, v in host.items():
-            dev[k].copy_(v, non_blocking=True)
+        g2.upload_rebuild(host, dev, chunks=chunks, copy_stream=copy_stream, index=False)
         r = dv.pagerank(g2, 20, 0.85, bufs=bufs)
         out_host.copy_(r, non_blocking=True)
 
@@ -773,9 +784,12 @@ def e2e_pagerank(args, g, bufs):
         b.synchronize()
         ts.append(a.elapsed_time(b))
     ms = float(np.mean(ts))
+    same = bool(torch.equal(g2.vsrc, g.vsrc[:lanes])) and float((out_host.cuda() - ref).abs().max()) <= 1e-7
     return {"value": round(20 * g.edges / (ms * 1e-3) / 1e9, 4), "unit": "GTEPS (20*|E|/time, PageRank)",
             "ms_per_step": round(ms, 3), "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": g.n * 4,
-            "path": "pinned host layout -> H2D -> wg_pagerank -> D2H ranks"}
+            "result_equal": same, "host_format_build_s": round(t_fmt, 2),
+            "path": "pinned host topology (lane sources delta-coded per vector, voff, out-degrees) -> H2D in "
+                    "chunks; wg_expand_destinations, wg_decode_lanes per chunk -> wg_pagerank -> D2H ranks"}
 
 
 def cpu_baseline_pagerank(g, ranks=None):

@@ -44,8 +44,9 @@ __global__ void __launch_bounds__(256) pr_prep(uint32_t n, int it, double dampin
     }
 }
 
-template <int W>
-__global__ void __launch_bounds__(256) pr_pull(wg_graph g, const float *contrib, float *acc, uint32_t base) {
+template <int W, bool SHIFT>
+__global__ void __launch_bounds__(256) pr_pull(wg_graph g, const float *contrib, float *acc, uint32_t base_) {
+    const uint32_t base = SHIFT ? base_ : 0u;  // destination-sharded runs index a slice
     const unsigned lane = lane_id();
     const uint64_t gwarp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -87,12 +88,12 @@ __global__ void __launch_bounds__(256) pr_pull(wg_graph g, const float *contrib,
 
 using PrPull = void (*)(wg_graph, const float *, float *, uint32_t);
 
-PrPull pick(int w) {
+PrPull pick(int w, bool shift = false) {
     switch (w) {
-        case 1: return pr_pull<1>;
-        case 2: return pr_pull<2>;
-        case 4: return pr_pull<4>;
-        case 8: return pr_pull<8>;
+        case 1: return shift ? pr_pull<1, true> : pr_pull<1, false>;
+        case 2: return shift ? pr_pull<2, true> : pr_pull<2, false>;
+        case 4: return shift ? pr_pull<4, true> : pr_pull<4, false>;
+        case 8: return shift ? pr_pull<8, true> : pr_pull<8, false>;
     }
     return nullptr;
 }
@@ -149,7 +150,7 @@ extern "C" int wg_pagerank_prep(uint32_t n, int it, double damping, const uint32
 extern "C" int wg_pagerank_pull(const wg_graph *g, const float *d_contrib, float *d_acc,
                                 uint32_t dst_base, void *stream) {
     WG_REQUIRE(g && d_contrib && d_acc, "null argument");
-    PrPull pull = pick((int)g->width);
+    PrPull pull = pick((int)g->width, dst_base != 0);
     WG_REQUIRE(pull, "unsupported width %u", g->width);
     if (!g->nvec) return WG_OK;
     cudaStream_t s = as_stream(stream);

@@ -227,7 +227,7 @@ class DeviceGraph:
         return {"lane_stream": words[: int(used.value)], "lane_widths": widths[: self.nvec], "lane_blocks": blocks}
 
     def upload_rebuild(self, host: dict, dev: dict, chunks: int = 4, scratch=None, copy_stream=None,
-                       trace=None) -> int:
+                       trace=None, index: bool = True) -> int:
         """Copy the compact topology from pinned host memory (host["vsrc"],
         its bit-packed form host["vsrc_bits"] or its delta-coded form
         host["lane_stream"/"lane_widths"/"lane_blocks"], host["voff"], optional
@@ -241,7 +241,9 @@ class DeviceGraph:
         offsets from the degrees, every chunk's lanes take their slots as the
         chunk arrives (wg_index_place_*; the same lists with the order inside
         each list unspecified, no sort), verified at the end, with the
-        sort-based builder as the fallback.  Returns the index length.  trace: an optional list that
+        sort-based builder as the fallback.  index=False rebuilds only
+        vsrc and vec_dst (PageRank reads no index; host["outdeg"] then just
+        lands in the out-degrees).  Returns the index length (0 without).  trace: an optional list that
         receives (label, event) pairs (profiling)."""
         torch = _torch()
         L = _lib.load()
@@ -250,7 +252,7 @@ class DeviceGraph:
         W = self.width
         packed = "vsrc_bits" in host
         coded = "lane_stream" in host
-        placed = "outdeg" in host
+        placed = "outdeg" in host and index
         bits = self.lane_bits() if packed else 32
         # packed chunks start on a word: lane offsets multiples of 32; coded
         # chunks are runs of whole blocks
@@ -269,7 +271,7 @@ class DeviceGraph:
         evs = []
         with torch.cuda.stream(cs):
             dev["voff"].copy_(host["voff"], non_blocking=True)
-            if placed:
+            if "outdeg" in host:
                 self.outdeg[: self.n].copy_(host["outdeg"], non_blocking=True)
             if coded:
                 dev["lane_blocks"].copy_(host["lane_blocks"], non_blocking=True)
@@ -315,7 +317,12 @@ class DeviceGraph:
             if trace is not None:
                 trace.append((f"decoded {c}", torch.cuda.Event(enable_timing=True)))
                 trace[-1][1].record(main)
-            if placed and coded:  # decode fused with the placement
+            if not index:  # lanes only
+                if coded:
+                    check(L.wg_decode_lanes(self.nvec, W, _ptr(self.vdst), _ptr(dev["lane_stream"]),
+                                            _ptr(dev["lane_widths"]), _ptr(dev["lane_blocks"]), cuts[c] // align,
+                                            -(-cuts[c + 1] // align), _ptr(self.vsrc), st))
+            elif placed and coded:  # decode fused with the placement
                 check(L.wg_index_place_coded(gs, _ptr(dev["lane_stream"]), _ptr(dev["lane_widths"]),
                                              _ptr(dev["lane_blocks"]), cuts[c] // align, -(-cuts[c + 1] // align),
                                              _ptr(self.idx_off), _ptr(self.idx_pos), _ptr(scratch), scratch.numel(),
@@ -333,7 +340,9 @@ class DeviceGraph:
                 trace.append((f"indexed {c}", torch.cuda.Event(enable_timing=True)))
                 trace[-1][1].record(main)
         ent = ctypes.c_uint64(0)
-        if placed:
+        if not index:
+            pass
+        elif placed:
             ok = ctypes.c_int(0)
             check(L.wg_index_place_end(gs, _ptr(scratch), scratch.numel(), ctypes.byref(ok), st))
             if ok.value:
