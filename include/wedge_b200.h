@@ -295,8 +295,10 @@ typedef struct wg_run_params {
 #define WG_RUN_KEEP_LISTS 2
 /* The caller asserts that the initial values are the vertex ids (value[v] ==
  * v, e.g. cc_program): the first iteration's unweighted, unfiltered dense
- * pull then uses each lane's source id as its message instead of gathering
- * it.  Results and counters unchanged. */
+ * pull then needs no gathers -- a destination's smallest message is its
+ * smallest source, lane 0 of its first vector (the layout's lanes ascend
+ * within a destination, graph.py:235), one load per destination.  Results
+ * and counters unchanged. */
 #define WG_RUN_IDENTITY_INIT 8
 
 /* Element counts: [0] fbits words, [1] groups, [2] gbits words, [3] bcount

@@ -303,6 +303,21 @@ int launch_pull(const LoopCtx &c, const wg_graph *g, const PullBufs &pb, int val
     if (only) handles = 1 << only;
     const bool want_full = only == 0 || only == MODE_FULL;
     if (want_full && (c.forced_mode == 0 || c.forced_mode == MODE_FULL)) {
+        if (pb.ident && !weight && !filter) {  // iteration 1 of an identity-initialised run
+            using IdentFn = void (*)(LoopCtx, wg_graph, PullBufs, int64_t, int64_t);
+            IdentFn fi = nullptr;
+            const bool u32 = val_type == WG_VAL_U32;
+            switch (g->width) {
+                case 1: fi = u32 ? pull_ident_kernel<uint32_t, 1> : pull_ident_kernel<int64_t, 1>; break;
+                case 2: fi = u32 ? pull_ident_kernel<uint32_t, 2> : pull_ident_kernel<int64_t, 2>; break;
+                case 4: fi = u32 ? pull_ident_kernel<uint32_t, 4> : pull_ident_kernel<int64_t, 4>; break;
+                case 8: fi = u32 ? pull_ident_kernel<uint32_t, 8> : pull_ident_kernel<int64_t, 8>; break;
+            }
+            WG_REQUIRE(fi != nullptr, "no identity pull for width %u", g->width);
+            fi<<<grid_for(g->nvec, 256 * 4, 8), 256, 0, s>>>(c, *g, pb, k->apply_increment, k->sentinel);
+            ::wg::count_launch();
+            WG_CHECK_LAUNCH("pull (identity)");
+        }
         size_t smem = 0;
         DenseFn dn = pick_dense(val_type, (int)g->width, weight, filter, &smem);
         unsigned grid = persistent_grid(dn, PULL_THREADS, (g->nvec + 255) / 256, smem);

@@ -508,6 +508,50 @@ __global__ void __launch_bounds__(PULL_THREADS) pull_kernel(LoopCtx c, wg_graph 
 }
 
 
+// First dense pull of a run whose initial values are the vertex ids
+// (WG_RUN_IDENTITY_INIT, CC): every message is its source id and a
+// destination's lanes ascend (graph.py:235), so its minimum message is lane 0
+// of its first vector -- one load per destination instead of a pass over all
+// lanes and gathers.  Full occupancy, K vectors per thread in flight; every
+// vector still counts as touched (the reference's full scan).
+template <typename T, int W>
+__global__ void __launch_bounds__(256) pull_ident_kernel(LoopCtx c, wg_graph g, PullBufs b, int64_t inc,
+                                                         int64_t sentinel) {
+    using VT = ValTraits<T>;
+    const uint64_t it = ctx_iter(c);
+    if (it != 1 || ctx_mode(c, it) != MODE_FULL) return;
+    wg_iter_rec *out = ctx_out(c, it);
+    const T *__restrict__ prev = (const T *)b.vals[0];
+    T *__restrict__ nxt = (T *)b.vals[1];
+    uint32_t *__restrict__ obits = b.fbits[1];
+    const T INF = VT::inf(sentinel);
+    const uint64_t nvec = g.nvec;
+    const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+    uint32_t ovf = 0;
+    constexpr int K = 4;
+    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; base < nvec; base += K * nth) {
+        uint32_t d[K], s0[K];
+        bool head[K];
+        T pd[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const uint64_t v = base + k * nth;
+            d[k] = v < nvec ? g.vdst[v] : NONE;
+            head[k] = v < nvec && (v == 0 || g.vdst[v - 1] != d[k]);
+        }
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            s0[k] = head[k] ? g.vsrc[(base + k * nth) * W] : 0u;
+            pd[k] = head[k] ? prev[d[k]] : INF;
+        }
+#pragma unroll
+        for (int k = 0; k < K; ++k) apply_dense<T>(head[k], d[k], (T)s0[k], pd[k], true, INF, inc, nxt, obits, ovf);
+    }
+    if (ovf) out->overflow = 1;
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        atomicAdd((unsigned long long *)&out->vectors_touched, (unsigned long long)nvec);
+}
+
 // One dense-pull chunk after its gathers were issued: destinations, segment
 // heads, the raw gathered messages (INF for padding lanes) and prev[d] of
 // segment tails.
@@ -590,7 +634,7 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) pull_dense_tma_kernel(Loop
     // level = base + (it-1)*inc, so its frontier bit replaces the value gather.
     // Frontier 0 lives in the caller's initial words, hence it > 1.
     const bool bottom_up = FILTER && b.first_hit && it > 1;
-    // identity initial values: iteration 1's message from src is src itself
+    // identity initial values: iteration 1 belongs to pull_ident_kernel
     const bool ident = !FILTER && !WEIGHT && b.ident && it == 1;
     const uint32_t *__restrict__ inbits = (((it - 1) & 1) ? b.fbits[1] : b.fbits[0]);
     const T level = (T)(b.level_base + (int64_t)(it - 1) * inc);
@@ -606,6 +650,7 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) pull_dense_tma_kernel(Loop
 
     uint64_t t0w, t1w;
     warp_range(((uint64_t)nvec + 31) >> 5, gwarp, nwarps, t0w, t1w);
+    if (ident) return;  // pull_ident_kernel did this iteration
     if (t0w < t1w) {
         const uint32_t tfirst = (uint32_t)t0w, tend = (uint32_t)t1w;
         const uint32_t vend = (tend << 5) < nvec ? (tend << 5) : nvec;
@@ -665,8 +710,6 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) pull_dense_tma_kernel(Loop
                     const bool take = pull && k.src[u][l] != WG_NO_LANE;
                     if (FILTER && bottom_up)  // the source's frontier word (8 MB at s26, L2-resident)
                         k.ps[u][l] = take ? (T)inbits[k.src[u][l] >> 5] : (T)0;
-                    else if (!FILTER && !WEIGHT && ident)
-                        k.ps[u][l] = take ? (T)k.src[u][l] : INF;
                     else
                         k.ps[u][l] = take ? prev[k.src[u][l]] : INF;
                 }
