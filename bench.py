@@ -287,7 +287,7 @@ def run_b200(args, wl):
     recs_t, _, _ = step(timer)
     torch.cuda.synchronize()
     rows = timer.read()
-    roof = roofline(rows, recs_t, n, E, g.weighted(), kern.filter_unvisited, wl)
+    roof = roofline(rows, recs_t, n, E, g.weighted(), kern.filter_unvisited, wl, ident_first=ident)
 
     out = {
         "metric": METRIC, "value": round(gteps, 4), "unit": "GTEPS (|E|/time-to-solution)",
@@ -468,9 +468,12 @@ def certificate(el, values, app):
             "reached": int(reached.sum()) + 1, "ok": viol == 0 and untight == 0}
 
 
-def roofline(rows, recs, n, E, weighted, filt, wl):
+def roofline(rows, recs, n, E, weighted, filt, wl, ident_first=False):
     """achieved = algorithmic bytes per pull launch / its CUDA-event duration
-    (dense launches: the dominant kernel); wedge iterations reported beside."""
+    (dense launches: the dominant kernel); wedge iterations reported beside.
+    ident_first: iteration 1 ran pull_ident_kernel (one lane per destination,
+    WG_RUN_IDENTITY_INIT), which does not move the dense formula's bytes, so
+    it is reported on its own and kept out of the dense figure."""
     peak, peak_src = peaks()
     by_it = {}
     for kind, it, ms in rows:
@@ -489,7 +492,9 @@ def roofline(rows, recs, n, E, weighted, filt, wl):
         fin_ms = t.get(3, 0.0) + t.get(4, 0.0)  # end of iteration (+ list build after a dense pull)
         step_t += pull_ms + prep_ms + fin_ms
         U = r.frontier_out_size
-        if r.mode == "FullScan":
+        if r.mode == "FullScan" and ident_first and r.iteration == 1:
+            b = 4 * n + 4 * n + 4 * U + n / 8  # vec_dst run heads + one lane per destination + apply
+        elif r.mode == "FullScan":
             ep = E if not filt else min(E, 4 * r.vectors_touched)
             b = 4 * ep * (1 + w) + 4 * n + 4 * U + n / 8
             dense_b += b
@@ -508,7 +513,8 @@ def roofline(rows, recs, n, E, weighted, filt, wl):
         ach = dense_b / (dense_t * 1e-3) / 1e9
         kernel = (f"pull_dense_tma_kernel<u32,W{wl.get('W', 4)}> (K6, dense pull)" if not filt else
                   f"pull_dense_tma_kernel<u32,W{wl.get('W', 4)},filter> (K6, dense filtered pull)")
-        traffic = dense_b / max(1, sum(1 for r in recs if r.mode == "FullScan"))
+        traffic = dense_b / max(1, sum(1 for r in recs if r.mode == "FullScan"
+                                       and not (ident_first and r.iteration == 1)))
     else:
         ach = wedge_b / (wedge_t * 1e-3) / 1e9 if wedge_t else 0.0
         kernel = "transform + wedge pull (K3+K4+K5)"
