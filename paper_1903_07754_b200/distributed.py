@@ -196,6 +196,12 @@ class DeviceShard:
         self.loop = dv.DeviceLoop(self.g, shift, val_type)
         self.init = dv.encode_values(init_values, val_type)
         self.words = dv.all_words(n) if init_members is None else dv.initial_words(n, init_members)
+        # the run flags the single-GPU engine derives from the initial state
+        # (results and counters unchanged; the lockstep GPU test checks them)
+        iv = np.asarray(init_values, dtype=np.int64)
+        self.first_hit = dv.first_hit_ok(kern, iv, init_members)
+        self.level_base = dv.first_hit_level(iv) if self.first_hit else 0
+        self.identity = dv.identity_values(iv)
         cap = max(hi - lo, 1)
         self.out_v = torch.empty(cap, dtype=torch.int32, device="cuda")
         self.out_x = torch.empty(cap, dtype=torch.int32 if val_type == _lib.WG_VAL_U32 else torch.int64,
@@ -213,7 +219,8 @@ class DeviceShard:
         self.p = None
 
     def seed(self):
-        self.p = self.loop.seed(self.init, self.words, self.kern, self.threshold)
+        self.p = self.loop.seed(self.init, self.words, self.kern, self.threshold, first_hit=self.first_hit,
+                                level_base=self.level_base, identity_init=self.identity)
         self.p.flags |= self._lib.WG_RUN_KEEP_LISTS  # wg_exchange_pack reads the member lists
 
     def step(self, it: int):
