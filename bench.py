@@ -563,29 +563,39 @@ def e2e_b200(args, wl, g, loop, dinit, words, kern, thr, max_it, first_hit=False
     if fmt == "bits" and g.lane_bits() >= 32:
         fmt = "raw"
     pack = fmt == "bits"
-    t_fmt = time.perf_counter()
-    host = {"voff": g.vector_offsets().cpu().pin_memory()}
-    if fmt == "coded":
-        host.update({k: v.cpu().pin_memory() for k, v in g.encode_lanes().items()})
-    elif pack:
-        host["vsrc_bits"] = g.pack_lanes()[0].cpu().pin_memory()
-    else:
-        host["vsrc"] = g.vsrc.cpu().pin_memory()
     # the out-degrees travel too (the reference call's `degrees` input): the
     # index is then placed chunk by chunk instead of sorted
     # (auto: while the index fits in ~8x L2; at s25/s26 its random slot writes
     # cost more than the chunk sorts, measured in profiles/r01_e2e_index.txt)
     mode = os.environ.get("WG_E2E_INDEX", "auto")
     placed = mode == "placed" or (mode == "auto" and g.edges * 4 <= (1 << 30))
-    if placed:
-        host["outdeg"] = g.outdeg[: g.n].cpu().pin_memory()
+    t_fmt = time.perf_counter()
+    rebuild_kw = {}
+    if fmt == "coded":
+        # compact degrees (a byte per vertex + the large ones); a symmetric
+        # input ships no out-degrees (= in-degrees, verified by the placement)
+        symmetric = bool(wl.get("sym") or "grid" in wl)
+        host = g.host_format(symmetric=symmetric)
+        if not placed:
+            host.pop("outdeg8", None)
+            host.pop("outdeg_big", None)
+        rebuild_kw["outdeg_is_indeg"] = symmetric and placed
+    else:
+        host = {"voff": g.vector_offsets().cpu().pin_memory()}
+        if pack:
+            host["vsrc_bits"] = g.pack_lanes()[0].cpu().pin_memory()
+        else:
+            host["vsrc"] = g.vsrc.cpu().pin_memory()
+        if placed:
+            host["outdeg"] = g.outdeg[: g.n].cpu().pin_memory()
     t_fmt = time.perf_counter() - t_fmt
     if g.vw8 is not None:  # weights <= 255 travel as bytes and are widened on the device
         host["vw8"] = g.vw8[: g.nvec * g.width].cpu().pin_memory()
     elif g.vw is not None:
         host["vw"] = g.vw.cpu().pin_memory()
     # device buffers with readable slack past the end (TMA tail rounding, wedge_b200.h)
-    dev = {k: torch.empty(v.numel() + 64, dtype=v.dtype, device="cuda")[: v.numel()] for k, v in host.items()}
+    dev = {k: torch.empty(v.numel() + 64, dtype=v.dtype, device="cuda")[: v.numel()].view(v.shape)
+           for k, v in host.items()}
     for k, v in host.items():
         dev[k].copy_(v)
     if fmt != "raw":
@@ -599,8 +609,8 @@ def e2e_b200(args, wl, g, loop, dinit, words, kern, thr, max_it, first_hit=False
     if "vw8" in dev:
         _lib.check(_lib.load().wg_widen_weights(lanes, dev["vw8"].data_ptr(), dev["vw"].data_ptr(),
                                                 _lib.stream_ptr()))
-    g2 = dv.DeviceGraph.from_lanes(g.n, g.width, g.edges, g.nvec, dev["vsrc"], dev.get("vw"), dev["voff"],
-                                   scratch)
+    g2 = dv.DeviceGraph.from_lanes(g.n, g.width, g.edges, g.nvec, dev["vsrc"], dev.get("vw"),
+                                   dev["voff"] if "voff" in dev else g.vector_offsets(), scratch)
     if "vw8" in dev:
         g2.vw8 = dev["vw8"]
         g2._struct = None
@@ -618,7 +628,7 @@ def e2e_b200(args, wl, g, loop, dinit, words, kern, thr, max_it, first_hit=False
     chunks = int(os.environ.get("WG_E2E_CHUNKS", "0")) or max(1, min(8, (g.nvec * g.width) >> 22))
 
     def one():
-        g2.upload_rebuild(host, dev, chunks=chunks, copy_stream=copy_stream)
+        g2.upload_rebuild(host, dev, chunks=chunks, copy_stream=copy_stream, **rebuild_kw)
         p = loop2.seed(dinit, words, kern, thr, first_hit=first_hit, level_base=level_base,
                        identity_init=identity_init)
         recs, conv, last = loop2.drive(p, max_it)
@@ -645,7 +655,7 @@ def e2e_b200(args, wl, g, loop, dinit, words, kern, thr, max_it, first_hit=False
                 8 * sum(host[k].numel() * host[k].element_size() for k in host if k.startswith(("lane_", "vsrc")))
                 / max(1, g.nvec * g.width), 2),
             "host_format_build_s": round(t_fmt, 2), "index": "placed from the degrees" if placed else "chunked sort",
-            "path": "pinned host topology (lane sources delta-coded per vector [wg_encode_lanes], voff, out-degrees[, weights as bytes when <= 255]) -> H2D in up to 8 chunks; wg_expand_destinations, per chunk wg_index_place_coded (decode + index slots; or wg_index_chunk_coded + wg_index_finish), wg_index_place_end, wg_widen_weights -> device loop -> D2H values"}
+            "path": "pinned host topology (lane sources delta-coded per vector [wg_encode_lanes], in-degrees and out-degrees (none for a symmetric input) as a byte per vertex + the large ones[, weights as bytes when <= 255]) -> H2D in up to 8 chunks; wg_widen_degrees, wg_vector_offsets, wg_expand_destinations, per chunk wg_index_place_coded (decode + index slots; or wg_index_chunk_coded + wg_index_finish), wg_index_place_end, wg_widen_weights -> device loop -> D2H values"}
 
 
 def host_reference_layout(g):
@@ -751,16 +761,17 @@ def e2e_pagerank(args, g, bufs):
     """PageRank through the C ABI with the layout in pinned host memory: H2D
     of the compact topology (delta-coded lanes, per-destination vector
     offsets, out-degrees; PageRank reads no edge index) in chunks on a copy
-    stream, decoded on the device as they land (wg_expand_destinations,
-    wg_decode_lanes), 20 iterations, D2H ranks."""
+    stream, decoded on the device as they land (wg_widen_degrees,
+    wg_vector_offsets, wg_expand_destinations, wg_decode_lanes), 20
+    iterations, D2H ranks."""
     import torch
     from paper_1903_07754_b200 import device as dv
     ref = dv.pagerank(g, 20, 0.85, bufs=bufs).clone()
     t_fmt = time.perf_counter()
-    host = {"voff": g.vector_offsets().cpu().pin_memory(), "outdeg": g.outdeg[: g.n].cpu().pin_memory()}
-    host.update({k: v.cpu().pin_memory() for k, v in g.encode_lanes().items()})
+    host = g.host_format(symmetric=False)
     t_fmt = time.perf_counter() - t_fmt
-    dev = {k: torch.empty(v.numel() + 64, dtype=v.dtype, device="cuda")[: v.numel()] for k, v in host.items()}
+    dev = {k: torch.empty(v.numel() + 64, dtype=v.dtype, device="cuda")[: v.numel()].view(v.shape)
+           for k, v in host.items()}
     lanes = g.nvec * g.width
     vsrc = torch.empty(lanes + 64, dtype=torch.int32, device="cuda")
     vdst = torch.empty(g.nvec + 64, dtype=torch.int32, device="cuda")
@@ -794,7 +805,7 @@ def e2e_pagerank(args, g, bufs):
     return {"value": round(20 * g.edges / (ms * 1e-3) / 1e9, 4), "unit": "GTEPS (20*|E|/time, PageRank)",
             "ms_per_step": round(ms, 3), "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": g.n * 4,
             "result_equal": same, "host_format_build_s": round(t_fmt, 2),
-            "path": "pinned host topology (lane sources delta-coded per vector, voff, out-degrees) -> H2D in "
+            "path": "pinned host topology (lane sources delta-coded per vector, in/out-degrees as bytes + large ones) -> H2D in "
                     "chunks; wg_expand_destinations, wg_decode_lanes per chunk -> wg_pagerank -> D2H ranks"}
 
 

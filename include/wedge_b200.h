@@ -131,6 +131,15 @@ int wg_index_finish(const wg_graph *g, uint64_t max_chunk_lanes, uint64_t *d_idx
  * form of PullTopology.vec_dst, graph.py:240-243): run heads + max-scan, with
  * d_scratch of wg_expand_scratch_bytes(nvec) bytes.  Asynchronous. */
 size_t wg_expand_scratch_bytes(uint64_t nvec);
+/* Degrees in the compact upload form: d_deg[v] = d_deg8[v] (min(deg, 255)),
+ * then d_big holds nbig (vertex, degree) pairs for the larger ones. */
+int wg_widen_degrees(uint32_t n, const uint8_t *d_deg8, const uint32_t *d_big, uint64_t nbig, uint32_t *d_deg,
+                     void *stream);
+/* d_voff [n+1] = exclusive scan of ceil(indeg / width): the per-destination
+ * vector offsets from the in-degrees. */
+size_t wg_vector_offsets_scratch_bytes(uint32_t n);
+int wg_vector_offsets(uint32_t n, const uint32_t *d_indeg, uint32_t width, uint32_t *d_voff, void *d_scratch,
+                      size_t scratch_bytes, void *stream);
 int wg_expand_destinations(uint32_t n, const uint32_t *d_voff, uint64_t nvec, uint32_t *d_vdst, void *d_scratch,
                            size_t scratch_bytes, void *stream);
 
@@ -165,16 +174,19 @@ int wg_unpack_lanes(const uint32_t *d_packed, uint32_t bits, uint64_t lane_begin
 #define WG_CODED_BLOCK_VECTORS 1024
 uint64_t wg_coded_blocks(uint64_t nvec);
 uint64_t wg_coded_max_words(uint64_t nvec, uint32_t width);
+/* uint32 words of the width array: width - 1 of each vector in 5 bits, 160
+ * words per block. */
+uint64_t wg_coded_width_words(uint64_t nvec);
 size_t wg_coded_scratch_bytes(uint64_t nvec);
-/* Encode g's lanes: d_stream [wg_coded_max_words], d_widths [nvec],
+/* Encode g's lanes: d_stream [wg_coded_max_words], d_widths [wg_coded_width_words],
  * d_block_base [blocks + 1]; *h_words = stream words used.  Synchronises;
  * WG_EINVAL when a destination's lanes are not ascending. */
-int wg_encode_lanes(const wg_graph *g, uint32_t *d_stream, uint8_t *d_widths, uint64_t *d_block_base,
+int wg_encode_lanes(const wg_graph *g, uint32_t *d_stream, uint32_t *d_widths, uint64_t *d_block_base,
                     void *d_scratch, size_t scratch_bytes, uint64_t *h_words, void *stream);
 /* Decode blocks [block_begin, block_end) into d_vsrc (needs d_vdst of every
  * vector of those blocks and the one before). */
 int wg_decode_lanes(uint64_t nvec, uint32_t width, const uint32_t *d_vdst, const uint32_t *d_stream,
-                    const uint8_t *d_widths, const uint64_t *d_block_base, uint64_t block_begin,
+                    const uint32_t *d_widths, const uint64_t *d_block_base, uint64_t block_begin,
                     uint64_t block_end, uint32_t *d_vsrc, void *stream);
 
 /* Placed index: the edge index of wg_build_index up to the order inside each
@@ -192,7 +204,7 @@ int wg_index_place_begin(const wg_graph *g, uint64_t *d_idx_off, void *d_scratch
                          void *stream);
 int wg_index_place_chunk(const wg_graph *g, uint64_t v_begin, uint64_t v_end, uint64_t *d_idx_off,
                          uint32_t *d_idx_pos, void *d_scratch, size_t scratch_bytes, void *stream);
-int wg_index_place_coded(const wg_graph *g, const uint32_t *d_stream, const uint8_t *d_widths,
+int wg_index_place_coded(const wg_graph *g, const uint32_t *d_stream, const uint32_t *d_widths,
                          const uint64_t *d_block_base, uint64_t block_begin, uint64_t block_end,
                          uint64_t *d_idx_off, uint32_t *d_idx_pos, void *d_scratch, size_t scratch_bytes,
                          void *stream);
@@ -200,7 +212,7 @@ int wg_index_place_end(const wg_graph *g, void *d_scratch, size_t scratch_bytes,
 
 /* wg_index_chunk over delta-coded blocks [block_begin, block_end): decodes
  * them into g->vsrc (needs g->vdst) and adds their index entries. */
-int wg_index_chunk_coded(const wg_graph *g, const uint32_t *d_stream, const uint8_t *d_widths,
+int wg_index_chunk_coded(const wg_graph *g, const uint32_t *d_stream, const uint32_t *d_widths,
                          const uint64_t *d_block_base, uint64_t block_begin, uint64_t block_end, uint32_t chunk,
                          uint64_t max_chunk_lanes, void *d_scratch, size_t scratch_bytes, void *stream);
 

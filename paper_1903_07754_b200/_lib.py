@@ -73,7 +73,8 @@ EXPORTS = [
     "wg_narrow_weights", "wg_widen_weights", "wg_exchange_bytes", "wg_exchange_pack_all",
     "wg_exchange_apply_all", "wg_index_chunked_scratch_bytes", "wg_index_chunk", "wg_index_finish",
     "wg_pagerank_prep", "wg_pagerank_pull", "wg_lane_bits", "wg_packed_lane_words", "wg_pack_lanes",
-    "wg_unpack_lanes", "wg_coded_blocks", "wg_coded_max_words", "wg_coded_scratch_bytes", "wg_encode_lanes",
+    "wg_unpack_lanes", "wg_coded_blocks", "wg_coded_max_words", "wg_coded_width_words", "wg_widen_degrees",
+    "wg_vector_offsets_scratch_bytes", "wg_vector_offsets", "wg_coded_scratch_bytes", "wg_encode_lanes",
     "wg_decode_lanes", "wg_index_chunk_coded", "wg_expand_scratch_bytes", "wg_index_placed_scratch_bytes",
     "wg_index_place_begin", "wg_index_place_chunk", "wg_index_place_coded", "wg_index_place_end",
 ]
@@ -138,6 +139,10 @@ def load(path: os.PathLike | str | None = None):
         "wg_unpack_lanes": (ctypes.c_int, [c_vp, c_u32, c_u64, c_u64, c_vp, c_vp]),
         "wg_coded_blocks": (c_u64, [c_u64]),
         "wg_coded_max_words": (c_u64, [c_u64, c_u32]),
+        "wg_coded_width_words": (c_u64, [c_u64]),
+        "wg_widen_degrees": (ctypes.c_int, [c_u32, c_vp, c_vp, c_u64, c_vp, c_vp]),
+        "wg_vector_offsets_scratch_bytes": (ctypes.c_size_t, [c_u32]),
+        "wg_vector_offsets": (ctypes.c_int, [c_u32, c_vp, c_u32, c_vp, c_vp, ctypes.c_size_t, c_vp]),
         "wg_coded_scratch_bytes": (ctypes.c_size_t, [c_u64]),
         "wg_encode_lanes": (ctypes.c_int, [G, c_vp, c_vp, c_vp, c_vp, ctypes.c_size_t, u64p, c_vp]),
         "wg_decode_lanes": (ctypes.c_int, [c_u64, c_u32, c_vp, c_vp, c_vp, c_vp, c_u64, c_u64, c_vp, c_vp]),

@@ -7,7 +7,8 @@
 //   code = 0                       empty lane (WG_NO_LANE)
 //        = src + 1                 first lane of a destination, or of a block
 //        = src - prev_src + 1      otherwise (prev_src = the lane before)
-// Each vector stores its W codes in width[v] = max bit length bits, the
+// Each vector stores its W codes in width[v] = max bit length bits (width - 1
+// kept in 5 bits per vector, block-aligned: WWORDS words per block), the
 // vectors of a block of WG_CODED_BLOCK_VECTORS back to back; blocks start on
 // a 32-bit word (block_base[b] = first bit, block_base[nblocks] = total), so
 // runs of blocks can be copied and decoded independently.  At s22 this is
@@ -29,6 +30,19 @@ constexpr int BV = WG_CODED_BLOCK_VECTORS;
 constexpr int CT = 256;       // threads per block
 constexpr int VPT = BV / CT;  // vectors per thread
 static_assert(BV % CT == 0, "block size");
+constexpr int WBITS = 5;                  // a vector's width - 1 in 5 bits
+constexpr int WWORDS = BV * WBITS / 32;  // width words per block (block-aligned)
+static_assert(VPT == 4, "a thread's widths are one 20-bit field");
+
+// the 20-bit field of the VPT widths of thread t's vectors in block b
+__device__ __forceinline__ uint32_t width_field(const uint32_t *wp, uint64_t b, unsigned t) {
+    const uint32_t bit = t * (VPT * WBITS);
+    const uint32_t *w = wp + b * WWORDS + (bit >> 5);
+    const uint32_t sh = bit & 31;
+    uint64_t x = w[0];
+    if (sh + VPT * WBITS > 32) x |= (uint64_t)w[1] << 32;
+    return (uint32_t)(x >> sh) & ((1u << (VPT * WBITS)) - 1u);
+}
 
 __device__ __forceinline__ uint32_t bitlen(uint32_t x) { return x ? 32u - __clz(x) : 0u; }
 
@@ -64,20 +78,27 @@ __device__ __forceinline__ uint32_t vector_codes(const uint32_t *vsrc, const uin
 
 template <int W>
 __global__ void __launch_bounds__(CT) encode_widths(uint64_t nvec, const uint32_t *vsrc, const uint32_t *vdst,
-                                                    uint8_t *widths, uint64_t *block_bits, unsigned *bad) {
+                                                    uint32_t *widths, uint64_t *block_bits, unsigned *bad) {
     using Reduce = cub::BlockReduce<uint64_t, CT>;
     __shared__ typename Reduce::TempStorage tmp;
     const uint64_t b = blockIdx.x;
     uint64_t bits = 0;
+    uint32_t field = 0;
 #pragma unroll
     for (int k = 0; k < VPT; ++k) {
         const uint64_t v = b * BV + (uint64_t)threadIdx.x * VPT + k;
         if (v < nvec) {
             uint32_t code[W];
             const uint32_t w = vector_codes<W>(vsrc, vdst, v, code, bad);
-            widths[v] = (uint8_t)w;
+            field |= (w - 1) << (k * WBITS);
             bits += (uint64_t)W * w;
         }
+    }
+    if (field) {  // zeroed before: OR the 20-bit field in (it may straddle two words)
+        const uint32_t bit = threadIdx.x * (VPT * WBITS), sh = bit & 31;
+        uint32_t *w = widths + b * WWORDS + (bit >> 5);
+        atomicOr(&w[0], field << sh);
+        if (sh + VPT * WBITS > 32) atomicOr(&w[1], field >> (32 - sh));
     }
     const uint64_t tot = Reduce(tmp).Sum(bits);
     if (threadIdx.x == 0) block_bits[b] = (tot + 31) & ~uint64_t(31);
@@ -85,16 +106,17 @@ __global__ void __launch_bounds__(CT) encode_widths(uint64_t nvec, const uint32_
 
 template <int W>
 __global__ void __launch_bounds__(CT) encode_fields(uint64_t nvec, const uint32_t *vsrc, const uint32_t *vdst,
-                                                    const uint8_t *widths, const uint64_t *block_base,
+                                                    const uint32_t *widths, const uint64_t *block_base,
                                                     uint32_t *stream, unsigned *bad) {
     using Scan = cub::BlockScan<uint64_t, CT>;
     __shared__ typename Scan::TempStorage tmp;
     const uint64_t b = blockIdx.x;
     const uint64_t v0 = b * BV + (uint64_t)threadIdx.x * VPT;
     uint64_t bits = 0;
+    const uint32_t field = width_field(widths, b, threadIdx.x);
 #pragma unroll
     for (int k = 0; k < VPT; ++k)
-        if (v0 + k < nvec) bits += (uint64_t)W * widths[v0 + k];
+        if (v0 + k < nvec) bits += (uint64_t)W * (((field >> (k * WBITS)) & 31u) + 1);
     uint64_t off;
     Scan(tmp).ExclusiveSum(bits, off);
     off += block_base[b];
@@ -104,7 +126,7 @@ __global__ void __launch_bounds__(CT) encode_fields(uint64_t nvec, const uint32_
         if (v >= nvec) break;
         uint32_t code[W];
         vector_codes<W>(vsrc, vdst, v, code, bad);
-        const uint32_t w = widths[v];
+        const uint32_t w = ((field >> (k * WBITS)) & 31u) + 1;
 #pragma unroll
         for (int j = 0; j < W; ++j) {
             const uint64_t pos = off + (uint64_t)j * w;
@@ -129,7 +151,7 @@ struct SegSum {
 
 template <int W>
 __global__ void __launch_bounds__(CT) decode_lanes(uint64_t nvec, const uint32_t *vdst, const uint32_t *stream,
-                                                   const uint8_t *widths, const uint64_t *block_base,
+                                                   const uint32_t *widths, const uint64_t *block_base,
                                                    uint64_t block0, uint32_t *vsrc, uint32_t *keys,
                                                    uint32_t *vals, uint32_t pad, const uint64_t *ioff,
                                                    const uint32_t *deg, uint32_t *fill, uint32_t *pos,
@@ -144,9 +166,10 @@ __global__ void __launch_bounds__(CT) decode_lanes(uint64_t nvec, const uint32_t
     const uint64_t v0 = b * BV + (uint64_t)threadIdx.x * VPT;
     uint32_t w[VPT];
     uint64_t bits = 0;
+    const uint32_t field = width_field(widths, b, threadIdx.x);
 #pragma unroll
     for (int k = 0; k < VPT; ++k) {
-        w[k] = v0 + k < nvec ? widths[v0 + k] : 0u;
+        w[k] = v0 + k < nvec ? ((field >> (k * WBITS)) & 31u) + 1 : 0u;
         bits += (uint64_t)W * w[k];
     }
     uint64_t off;
@@ -210,7 +233,7 @@ __global__ void __launch_bounds__(CT) decode_lanes(uint64_t nvec, const uint32_t
 }
 
 template <int W>
-int encode_w(const wg_graph *g, uint32_t *d_stream, uint8_t *d_widths, uint64_t *d_block_base, void *d_scratch,
+int encode_w(const wg_graph *g, uint32_t *d_stream, uint32_t *d_widths, uint64_t *d_block_base, void *d_scratch,
              size_t scratch_bytes, uint64_t *h_words, cudaStream_t s) {
     const uint64_t nb = wg_coded_blocks(g->nvec);
     Carve c{(char *)d_scratch, 0, scratch_bytes};
@@ -223,6 +246,7 @@ int encode_w(const wg_graph *g, uint32_t *d_stream, uint8_t *d_widths, uint64_t 
     WG_CUDA(cudaMemsetAsync(bad, 0, sizeof(unsigned), s));
     WG_CUDA(cudaMemsetAsync(bb + nb, 0, sizeof(uint64_t), s));
     WG_CUDA(cudaMemsetAsync(d_stream, 0, wg_coded_max_words(g->nvec, g->width) * 4, s));
+    WG_CUDA(cudaMemsetAsync(d_widths, 0, wg_coded_width_words(g->nvec) * 4, s));
     if (nb) {
         encode_widths<W><<<(unsigned)nb, CT, 0, s>>>(g->nvec, g->vsrc, g->vdst, d_widths, bb, bad);
         ::wg::count_launch();
@@ -248,7 +272,7 @@ int encode_w(const wg_graph *g, uint32_t *d_stream, uint8_t *d_widths, uint64_t 
 
 namespace wg {
 int launch_decode_lanes(uint64_t nvec, uint32_t width, const uint32_t *vdst, const uint32_t *stream,
-                        const uint8_t *widths, const uint64_t *block_base, uint64_t b0, uint64_t b1, uint32_t *vsrc,
+                        const uint32_t *widths, const uint64_t *block_base, uint64_t b0, uint64_t b1, uint32_t *vsrc,
                         uint32_t *keys, uint32_t *vals, uint32_t pad, cudaStream_t s) {
     if (b1 == b0) return WG_OK;
     const unsigned grid = (unsigned)(b1 - b0);
@@ -264,7 +288,7 @@ int launch_decode_lanes(uint64_t nvec, uint32_t width, const uint32_t *vdst, con
     return WG_OK;
 }
 int launch_decode_place(uint64_t nvec, uint32_t width, const uint32_t *vdst, const uint32_t *stream,
-                        const uint8_t *widths, const uint64_t *block_base, uint64_t b0, uint64_t b1, uint32_t *vsrc,
+                        const uint32_t *widths, const uint64_t *block_base, uint64_t b0, uint64_t b1, uint32_t *vsrc,
                         const uint64_t *off, const uint32_t *deg, uint32_t *fill, uint32_t *pos, unsigned *bad,
                         cudaStream_t s) {
     if (b1 == b0) return WG_OK;
@@ -286,6 +310,8 @@ extern "C" {
 
 uint64_t wg_coded_blocks(uint64_t nvec) { return (nvec + BV - 1) / BV; }
 
+uint64_t wg_coded_width_words(uint64_t nvec) { return wg_coded_blocks(nvec) * WWORDS; }
+
 uint64_t wg_coded_max_words(uint64_t nvec, uint32_t width) { return nvec * width + wg_coded_blocks(nvec) + 1; }
 
 size_t wg_coded_scratch_bytes(uint64_t nvec) {
@@ -295,7 +321,7 @@ size_t wg_coded_scratch_bytes(uint64_t nvec) {
     return carve_size((nb + 1) * 8) + carve_size(4) + carve_size(tb) + 256;
 }
 
-int wg_encode_lanes(const wg_graph *g, uint32_t *d_stream, uint8_t *d_widths, uint64_t *d_block_base,
+int wg_encode_lanes(const wg_graph *g, uint32_t *d_stream, uint32_t *d_widths, uint64_t *d_block_base,
                     void *d_scratch, size_t scratch_bytes, uint64_t *h_words, void *stream) {
     WG_REQUIRE(g && d_stream && d_block_base && d_scratch && h_words, "null argument");
     WG_REQUIRE(g->nvec == 0 || (g->vsrc && g->vdst && d_widths), "null argument");
@@ -310,7 +336,7 @@ int wg_encode_lanes(const wg_graph *g, uint32_t *d_stream, uint8_t *d_widths, ui
 }
 
 int wg_decode_lanes(uint64_t nvec, uint32_t width, const uint32_t *d_vdst, const uint32_t *d_stream,
-                    const uint8_t *d_widths, const uint64_t *d_block_base, uint64_t block_begin,
+                    const uint32_t *d_widths, const uint64_t *d_block_base, uint64_t block_begin,
                     uint64_t block_end, uint32_t *d_vsrc, void *stream) {
     WG_REQUIRE(block_begin <= block_end && block_end <= wg_coded_blocks(nvec), "bad block range");
     if (block_end == block_begin) return WG_OK;

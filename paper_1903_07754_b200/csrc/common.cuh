@@ -37,12 +37,12 @@ int sm_count();
 // codec.cu: decode delta-coded blocks [b0, b1) into vsrc; with keys/vals also
 // the chunk-relative (source or pad, vector) pairs of the chunked index build
 int launch_decode_lanes(uint64_t nvec, uint32_t width, const uint32_t *vdst, const uint32_t *stream,
-                        const uint8_t *widths, const uint64_t *block_base, uint64_t b0, uint64_t b1, uint32_t *vsrc,
+                        const uint32_t *widths, const uint64_t *block_base, uint64_t b0, uint64_t b1, uint32_t *vsrc,
                         uint32_t *keys, uint32_t *vals, uint32_t pad, cudaStream_t s);
 // codec.cu: decode blocks [b0, b1) and place each lane in the index
 // (layout.cu place_one: slot = fill[source]++ behind off[source])
 int launch_decode_place(uint64_t nvec, uint32_t width, const uint32_t *vdst, const uint32_t *stream,
-                        const uint8_t *widths, const uint64_t *block_base, uint64_t b0, uint64_t b1, uint32_t *vsrc,
+                        const uint32_t *widths, const uint64_t *block_base, uint64_t b0, uint64_t b1, uint32_t *vsrc,
                         const uint64_t *off, const uint32_t *deg, uint32_t *fill, uint32_t *pos, unsigned *bad,
                         cudaStream_t s);
 

@@ -210,6 +210,28 @@ __global__ void unpack_lanes(const uint32_t *packed, uint32_t bits, uint64_t lan
     }
 }
 
+// Degrees in the compact upload form: a byte per vertex (min(deg, 255)) and
+// (vertex, degree) pairs for the rest.
+__global__ void widen_degrees(uint32_t n, const uint8_t *deg8, uint32_t *deg) {
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
+         v += (uint64_t)gridDim.x * blockDim.x)
+        deg[v] = deg8[v];
+}
+
+__global__ void scatter_big_degrees(uint64_t nbig, const uint32_t *big, uint32_t *deg) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nbig;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        deg[big[2 * i]] = big[2 * i + 1];
+}
+
+struct VectorsOf {  // in-degree -> vectors of the destination's run
+    const uint32_t *indeg;
+    uint32_t n, width;
+    __host__ __device__ uint32_t operator()(uint64_t d) const {
+        return d < n ? (indeg[d] + width - 1) / width : 0u;
+    }
+};
+
 // vdst[v] = d for v in [voff[d], voff[d+1]): every non-empty destination
 // writes its id at its first vector, an inclusive max-scan fills the runs
 // (balanced by vectors; RMAT's low ids hold most of the vectors, so any
@@ -624,7 +646,7 @@ __global__ void widen_degrees(uint32_t n, const uint32_t *deg, uint64_t *deg64) 
 
 struct CodedIn {
     const uint32_t *stream;
-    const uint8_t *widths;
+    const uint32_t *widths;
     const uint64_t *block_base;
     uint64_t b0, b1;
 };
@@ -687,7 +709,7 @@ int wg_index_chunk(const wg_graph *g, uint64_t v_begin, uint64_t v_end, uint32_t
                        nullptr);
 }
 
-int wg_index_chunk_coded(const wg_graph *g, const uint32_t *d_stream, const uint8_t *d_widths,
+int wg_index_chunk_coded(const wg_graph *g, const uint32_t *d_stream, const uint32_t *d_widths,
                          const uint64_t *d_block_base, uint64_t block_begin, uint64_t block_end, uint32_t chunk,
                          uint64_t max_chunk_lanes, void *d_scratch, size_t scratch_bytes, void *stream) {
     WG_REQUIRE(g && d_stream && d_widths && d_block_base && g->vdst, "null argument");
@@ -746,7 +768,7 @@ int wg_index_place_chunk(const wg_graph *g, uint64_t v_begin, uint64_t v_end, ui
     return WG_OK;
 }
 
-int wg_index_place_coded(const wg_graph *g, const uint32_t *d_stream, const uint8_t *d_widths,
+int wg_index_place_coded(const wg_graph *g, const uint32_t *d_stream, const uint32_t *d_widths,
                          const uint64_t *d_block_base, uint64_t block_begin, uint64_t block_end,
                          uint64_t *d_idx_off, uint32_t *d_idx_pos, void *d_scratch, size_t scratch_bytes,
                          void *stream) {
@@ -874,6 +896,46 @@ int wg_unpack_lanes(const uint32_t *d_packed, uint32_t bits, uint64_t lane_begin
     unpack_lanes<<<grid_1d(lane_end - lane_begin), 256, 0, s>>>(d_packed, bits, lane_begin, lane_end, d_lanes);
     ::wg::count_launch();
     WG_CHECK_LAUNCH("unpack_lanes");
+    return WG_OK;
+}
+
+int wg_widen_degrees(uint32_t n, const uint8_t *d_deg8, const uint32_t *d_big, uint64_t nbig, uint32_t *d_deg,
+                     void *stream) {
+    WG_REQUIRE((d_deg8 && d_deg) || n == 0, "null argument");
+    WG_REQUIRE(d_big || nbig == 0, "null argument");
+    cudaStream_t s = as_stream(stream);
+    if (n) {
+        widen_degrees<<<grid_1d(n), 256, 0, s>>>(n, d_deg8, d_deg);
+        ::wg::count_launch();
+    }
+    if (nbig) {
+        scatter_big_degrees<<<grid_1d(nbig), 256, 0, s>>>(nbig, d_big, d_deg);
+        ::wg::count_launch();
+    }
+    WG_CHECK_LAUNCH("widen_degrees");
+    return WG_OK;
+}
+
+size_t wg_vector_offsets_scratch_bytes(uint32_t n) {
+    size_t tb = 0;
+    cub::CountingInputIterator<uint64_t> it(0);
+    cub::TransformInputIterator<uint32_t, VectorsOf, cub::CountingInputIterator<uint64_t>> in(
+        it, VectorsOf{nullptr, n, 1});
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, in, (uint32_t *)nullptr, (int64_t)n + 1);
+    return tb + 256;
+}
+
+int wg_vector_offsets(uint32_t n, const uint32_t *d_indeg, uint32_t width, uint32_t *d_voff, void *d_scratch,
+                      size_t scratch_bytes, void *stream) {
+    WG_REQUIRE(d_voff && (d_indeg || n == 0) && width >= 1, "null argument");
+    cudaStream_t s = as_stream(stream);
+    cub::CountingInputIterator<uint64_t> it(0);
+    cub::TransformInputIterator<uint32_t, VectorsOf, cub::CountingInputIterator<uint64_t>> in(
+        it, VectorsOf{d_indeg, n, width});
+    size_t tb = 0;
+    WG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, in, d_voff, (int64_t)n + 1, s));
+    WG_REQUIRE(d_scratch && scratch_bytes >= tb, "scratch too small (wg_vector_offsets_scratch_bytes)");
+    WG_CUDA(cub::DeviceScan::ExclusiveSum(d_scratch, tb, in, d_voff, (int64_t)n + 1, s));
     return WG_OK;
 }
 

@@ -39,6 +39,9 @@ def _padded(t, extra: int):
     return out[: t.numel()]
 
 
+WIDTH_WORDS = 160  # uint32 words of 5-bit vector widths per coded block (wg_coded_width_words)
+
+
 def to_dev_u32(a, device="cuda"):
     """numpy / torch integer array -> device int32 tensor holding uint32 bits."""
     torch = _torch()
@@ -211,23 +214,56 @@ class DeviceGraph:
 
     def encode_lanes(self, stream=None) -> dict:
         """vsrc in the delta-coded upload format (wg_encode_lanes): device
-        tensors "lane_stream" (int32 words), "lane_widths" (uint8 per vector)
-        and "lane_blocks" (int64 block bit offsets, blocks + 1)."""
+        tensors "lane_stream" (int32 words), "lane_widths" (int32 words, 5
+        bits per vector, WIDTH_WORDS per block) and "lane_blocks" (int64 block
+        bit offsets, blocks + 1)."""
         torch = _torch()
         L = _lib.load()
         dev = self.vsrc.device
         nb = int(L.wg_coded_blocks(self.nvec))
         words = torch.empty(max(int(L.wg_coded_max_words(self.nvec, self.width)), 1), dtype=torch.int32, device=dev)
-        widths = torch.empty(max(self.nvec, 1), dtype=torch.uint8, device=dev)
+        widths = torch.empty(max(int(L.wg_coded_width_words(self.nvec)), 1), dtype=torch.int32, device=dev)
         blocks = torch.empty(nb + 1, dtype=torch.int64, device=dev)
         scratch = torch.empty(int(L.wg_coded_scratch_bytes(self.nvec)), dtype=torch.uint8, device=dev)
         used = ctypes.c_uint64(0)
         check(L.wg_encode_lanes(ctypes.byref(self.struct()), _ptr(words), _ptr(widths), _ptr(blocks), _ptr(scratch),
                                 scratch.numel(), ctypes.byref(used), _lib.stream_ptr(stream)))
-        return {"lane_stream": words[: int(used.value)], "lane_widths": widths[: self.nvec], "lane_blocks": blocks}
+        return {"lane_stream": words[: int(used.value)], "lane_widths": widths[: int(L.wg_coded_width_words(self.nvec))],
+                "lane_blocks": blocks}
+
+    def in_degrees(self):
+        """Real lanes per destination (device int32 [n])."""
+        torch = _torch()
+        lanes = self.vsrc[: self.nvec * self.width].view(self.nvec, self.width)
+        real = (lanes != -1).sum(1).to(torch.int32)
+        deg = torch.zeros(self.n, dtype=torch.int32, device=self.vsrc.device)
+        return deg.index_add_(0, self.vdst[: self.nvec].to(torch.int64) & 0xFFFFFFFF, real)
+
+    @staticmethod
+    def compact_degrees(deg):
+        """(min(deg, 255) as uint8, int32 [k, 2] (vertex, degree) for the rest)
+        -- the upload form wg_widen_degrees reads."""
+        torch = _torch()
+        big = torch.nonzero(deg >= 255).flatten()
+        pairs = torch.stack([big.to(torch.int32), deg[big].to(torch.int32)], 1).contiguous()
+        return deg.clamp(max=255).to(torch.uint8), pairs
+
+    def host_format(self, symmetric: bool = False) -> dict:
+        """The compact host-resident topology of the e2e upload (pinned):
+        delta-coded lanes, in-degrees (from which voff is rebuilt) and, unless
+        the caller declares the graph symmetric (out-degrees = in-degrees,
+        verified on the device by the placed index), the out-degrees, both as
+        a byte per vertex plus the larger ones as (vertex, degree) pairs."""
+        host = {k: v.cpu().pin_memory() for k, v in self.encode_lanes().items()}
+        d8, big = self.compact_degrees(self.in_degrees())
+        host["indeg8"], host["indeg_big"] = d8.cpu().pin_memory(), big.cpu().pin_memory()
+        if not symmetric:
+            o8, obig = self.compact_degrees(self.outdeg[: self.n])
+            host["outdeg8"], host["outdeg_big"] = o8.cpu().pin_memory(), obig.cpu().pin_memory()
+        return host
 
     def upload_rebuild(self, host: dict, dev: dict, chunks: int = 4, scratch=None, copy_stream=None,
-                       trace=None, index: bool = True) -> int:
+                       trace=None, index: bool = True, outdeg_is_indeg: bool = False) -> int:
         """Copy the compact topology from pinned host memory (host["vsrc"],
         its bit-packed form host["vsrc_bits"] or its delta-coded form
         host["lane_stream"/"lane_widths"/"lane_blocks"], host["voff"], optional
@@ -243,8 +279,12 @@ class DeviceGraph:
         each list unspecified, no sort), verified at the end, with the
         sort-based builder as the fallback.  index=False rebuilds only
         vsrc and vec_dst (PageRank reads no index; host["outdeg"] then just
-        lands in the out-degrees).  Returns the index length (0 without).  trace: an optional list that
-        receives (label, event) pairs (profiling)."""
+        lands in the out-degrees).  The compact degree form (host_format:
+        "indeg8"/"indeg_big" instead of voff, "outdeg8"/"outdeg_big" or
+        outdeg_is_indeg for a symmetric graph) is widened on the device
+        (wg_widen_degrees, wg_vector_offsets).  Returns the index length (0
+        without).  trace: an optional list that receives (label, event)
+        pairs (profiling)."""
         torch = _torch()
         L = _lib.load()
         cs = copy_stream or torch.cuda.Stream()
@@ -252,7 +292,16 @@ class DeviceGraph:
         W = self.width
         packed = "vsrc_bits" in host
         coded = "lane_stream" in host
-        placed = "outdeg" in host and index
+        compact = "indeg8" in host
+        has_deg = "outdeg" in host or "outdeg8" in host or (compact and outdeg_is_indeg)
+        placed = has_deg and index
+        if compact and getattr(self, "_indeg", None) is None:
+            self._indeg = torch.empty(self.n + 1, dtype=torch.int32, device=self.vsrc.device)
+            self._voff = torch.empty(self.n + 1, dtype=torch.int32, device=self.vsrc.device)
+        for k in ("indeg8", "indeg_big", "outdeg8", "outdeg_big"):
+            if k in host and k not in dev:
+                dev[k] = torch.empty(max(host[k].numel(), 1), dtype=host[k].dtype,
+                                     device=self.vsrc.device)[: host[k].numel()].view(host[k].shape)
         bits = self.lane_bits() if packed else 32
         # packed chunks start on a word: lane offsets multiples of 32; coded
         # chunks are runs of whole blocks
@@ -263,14 +312,16 @@ class DeviceGraph:
         max_lanes = max(max(cuts[c + 1] - cuts[c] for c in range(chunks)) * W, 1)
         need = max(int(L.wg_index_chunked_scratch_bytes(self.nvec * W, max_lanes, self.n)),
                    int(L.wg_index_scratch_bytes(self.nvec * W, self.n)), int(L.wg_expand_scratch_bytes(self.nvec)),
-                   int(L.wg_index_placed_scratch_bytes(self.n)))
+                   int(L.wg_index_placed_scratch_bytes(self.n)), int(L.wg_vector_offsets_scratch_bytes(self.n)))
         if scratch is None or scratch.numel() < need:
             scratch = torch.empty(need, dtype=torch.uint8, device=self.vsrc.device)
         words = int(host["vsrc_bits"].numel()) if packed else 0
         cs.wait_stream(main)  # the previous use of the buffers is done
         evs = []
         with torch.cuda.stream(cs):
-            dev["voff"].copy_(host["voff"], non_blocking=True)
+            for k in ("voff", "indeg8", "indeg_big", "outdeg8", "outdeg_big"):
+                if k in host and host[k].numel():
+                    dev[k].copy_(host[k], non_blocking=True)
             if "outdeg" in host:
                 self.outdeg[: self.n].copy_(host["outdeg"], non_blocking=True)
             if coded:
@@ -287,8 +338,8 @@ class DeviceGraph:
                     ba, bb = cuts[c] // align, -(-cuts[c + 1] // align)
                     wa, wb = int(base[ba]) // 32, int(base[bb]) // 32
                     dev["lane_stream"][wa:wb].copy_(host["lane_stream"][wa:wb], non_blocking=True)
-                    dev["lane_widths"][cuts[c]:cuts[c + 1]].copy_(host["lane_widths"][cuts[c]:cuts[c + 1]],
-                                                                  non_blocking=True)
+                    dev["lane_widths"][ba * WIDTH_WORDS: bb * WIDTH_WORDS].copy_(
+                        host["lane_widths"][ba * WIDTH_WORDS: bb * WIDTH_WORDS], non_blocking=True)
                 else:
                     dev["vsrc"][a:b].copy_(host["vsrc"][a:b], non_blocking=True)
                 e = torch.cuda.Event(enable_timing=trace is not None)
@@ -304,7 +355,19 @@ class DeviceGraph:
             evs.append(e)
         st = _lib.stream_ptr()
         main.wait_event(evs[0])
-        check(L.wg_expand_destinations(self.n, _ptr(dev["voff"]), self.nvec, _ptr(self.vdst), _ptr(scratch),
+        voff = dev.get("voff")
+        if compact:  # in-degrees -> voff; out-degrees
+            check(L.wg_widen_degrees(self.n, _ptr(dev["indeg8"]), _ptr(dev["indeg_big"]), host["indeg_big"].shape[0],
+                                     _ptr(self._indeg), st))
+            check(L.wg_vector_offsets(self.n, _ptr(self._indeg), W, _ptr(self._voff), _ptr(scratch), scratch.numel(),
+                                      st))
+            voff = self._voff
+            if "outdeg8" in host:
+                check(L.wg_widen_degrees(self.n, _ptr(dev["outdeg8"]), _ptr(dev["outdeg_big"]),
+                                         host["outdeg_big"].shape[0], _ptr(self.outdeg), st))
+            elif outdeg_is_indeg:
+                self.outdeg[: self.n].copy_(self._indeg[: self.n])
+        check(L.wg_expand_destinations(self.n, _ptr(voff), self.nvec, _ptr(self.vdst), _ptr(scratch),
                                        scratch.numel(), st))
         gs = ctypes.byref(self.struct())
         if placed:

@@ -89,7 +89,10 @@ def _decode_np(h, vdst, W, BV=1024):
     """The delta-coded lane format restated (wedge_b200.h wg_encode_lanes),
     decoded sequentially on the host."""
     words = h["lane_stream"].numpy().view(np.uint32)
-    widths = h["lane_widths"].numpy()
+    wbits = np.unpackbits(h["lane_widths"].numpy().view(np.uint8), bitorder="little")
+    nvec = len(vdst)
+    widths = np.array([1 + int(np.dot(wbits[(v // BV) * 5120 + (v % BV) * 5:][:5].astype(np.int64),
+                                      1 << np.arange(5))) for v in range(nvec)])
     base = h["lane_blocks"].numpy()
     bits = np.unpackbits(words.view(np.uint8), bitorder="little")
     out = np.empty(len(widths) * W, np.uint32)
@@ -174,6 +177,22 @@ def test_layout_rebuilt_from_lanes(wg, golden):
                 assert np.array_equal(_sorted_lists(g2.offsets_np(), g2.positions_np()), g.positions_np())
             else:
                 assert np.array_equal(g2.positions_np(), g.positions_np())
+        # the compact host format: degrees as bytes + large ones, voff rebuilt
+        # from the in-degrees; a symmetric claim ships no out-degrees (a false
+        # claim fails the placement check and falls back to the sorted build)
+        for sym in (False, True):
+            hf = g.host_format(symmetric=sym)
+            df = {k: torch.empty(v.numel() + 1, dtype=v.dtype, device="cuda")[: v.numel()].view(v.shape)
+                  for k, v in hf.items()}
+            g2.vsrc.fill_(-7)
+            g2.vdst.fill_(-7)
+            g2.idx_pos.zero_()
+            g2.outdeg.zero_()
+            assert g2.upload_rebuild(hf, df, chunks=3, outdeg_is_indeg=sym) == g.entries
+            assert torch.equal(g2.vsrc, g.vsrc) and np.array_equal(g2.vec_dst_np(), g.vec_dst_np())
+            assert np.array_equal(g2.offsets_np(), g.offsets_np())
+            assert np.array_equal(g2.outdeg_np(), g.outdeg_np())
+            assert np.array_equal(_sorted_lists(g2.offsets_np(), g2.positions_np()), g.positions_np())
         # placed over raw uint32 lanes too
         g2.idx_pos.zero_()
         assert g2.upload_rebuild(dict(host, outdeg=g.outdeg[: g.n].cpu().pin_memory()),
