@@ -197,7 +197,8 @@ int wg_decode_lanes(uint64_t nvec, uint32_t width, const uint32_t *d_vdst, const
  * the degrees; chunk / coded: each lane of the vectors (blocks) takes the
  * next slot of its source (coded also decodes the blocks into g->vsrc);
  * end: synchronises, *h_ok = 1 iff the claim held and the index is complete
- * (else rebuild it with wg_build_index).  Scratch of
+ * (else rebuild it with wg_build_index; placement never writes past
+ * g->entries slots).  Scratch of
  * wg_index_placed_scratch_bytes(n) bytes, shared by the calls. */
 size_t wg_index_placed_scratch_bytes(uint32_t n);
 int wg_index_place_begin(const wg_graph *g, uint64_t *d_idx_off, void *d_scratch, size_t scratch_bytes,

@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(CT) decode_lanes(uint64_t nvec, const uint32_t
                                                    uint64_t block0, uint32_t *vsrc, uint32_t *keys,
                                                    uint32_t *vals, uint32_t pad, const uint64_t *ioff,
                                                    const uint32_t *deg, uint32_t *fill, uint32_t *pos,
-                                                   unsigned *bad) {
+                                                   unsigned *bad, uint64_t cap) {
     using Scan = cub::BlockScan<uint64_t, CT>;
     using SScan = cub::BlockScan<Seg, CT>;
     __shared__ union {
@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(CT) decode_lanes(uint64_t nvec, const uint32_t
                     *bad = 1u;  // repeated (source, vector) pair
                     live = false;
                 }
-                place_one(src, live, (uint32_t)(v0 + k), ioff, deg, fill, pos, bad);
+                place_one(src, live, (uint32_t)(v0 + k), ioff, deg, fill, pos, bad, cap);
             }
         }
     }
@@ -277,10 +277,10 @@ int launch_decode_lanes(uint64_t nvec, uint32_t width, const uint32_t *vdst, con
     if (b1 == b0) return WG_OK;
     const unsigned grid = (unsigned)(b1 - b0);
     switch (width) {
-        case 1: decode_lanes<1><<<grid, CT, 0, s>>>(nvec, vdst, stream, widths, block_base, b0, vsrc, keys, vals, pad, nullptr, nullptr, nullptr, nullptr, nullptr); break;
-        case 2: decode_lanes<2><<<grid, CT, 0, s>>>(nvec, vdst, stream, widths, block_base, b0, vsrc, keys, vals, pad, nullptr, nullptr, nullptr, nullptr, nullptr); break;
-        case 4: decode_lanes<4><<<grid, CT, 0, s>>>(nvec, vdst, stream, widths, block_base, b0, vsrc, keys, vals, pad, nullptr, nullptr, nullptr, nullptr, nullptr); break;
-        case 8: decode_lanes<8><<<grid, CT, 0, s>>>(nvec, vdst, stream, widths, block_base, b0, vsrc, keys, vals, pad, nullptr, nullptr, nullptr, nullptr, nullptr); break;
+        case 1: decode_lanes<1><<<grid, CT, 0, s>>>(nvec, vdst, stream, widths, block_base, b0, vsrc, keys, vals, pad, nullptr, nullptr, nullptr, nullptr, nullptr, 0); break;
+        case 2: decode_lanes<2><<<grid, CT, 0, s>>>(nvec, vdst, stream, widths, block_base, b0, vsrc, keys, vals, pad, nullptr, nullptr, nullptr, nullptr, nullptr, 0); break;
+        case 4: decode_lanes<4><<<grid, CT, 0, s>>>(nvec, vdst, stream, widths, block_base, b0, vsrc, keys, vals, pad, nullptr, nullptr, nullptr, nullptr, nullptr, 0); break;
+        case 8: decode_lanes<8><<<grid, CT, 0, s>>>(nvec, vdst, stream, widths, block_base, b0, vsrc, keys, vals, pad, nullptr, nullptr, nullptr, nullptr, nullptr, 0); break;
         default: WG_REQUIRE(false, "unsupported width %u", width);
     }
     ::wg::count_launch();
@@ -290,14 +290,14 @@ int launch_decode_lanes(uint64_t nvec, uint32_t width, const uint32_t *vdst, con
 int launch_decode_place(uint64_t nvec, uint32_t width, const uint32_t *vdst, const uint32_t *stream,
                         const uint32_t *widths, const uint64_t *block_base, uint64_t b0, uint64_t b1, uint32_t *vsrc,
                         const uint64_t *off, const uint32_t *deg, uint32_t *fill, uint32_t *pos, unsigned *bad,
-                        cudaStream_t s) {
+                        uint64_t cap, cudaStream_t s) {
     if (b1 == b0) return WG_OK;
     const unsigned grid = (unsigned)(b1 - b0);
     switch (width) {
-        case 1: decode_lanes<1><<<grid, CT, 0, s>>>(nvec, vdst, stream, widths, block_base, b0, vsrc, nullptr, nullptr, 0u, off, deg, fill, pos, bad); break;
-        case 2: decode_lanes<2><<<grid, CT, 0, s>>>(nvec, vdst, stream, widths, block_base, b0, vsrc, nullptr, nullptr, 0u, off, deg, fill, pos, bad); break;
-        case 4: decode_lanes<4><<<grid, CT, 0, s>>>(nvec, vdst, stream, widths, block_base, b0, vsrc, nullptr, nullptr, 0u, off, deg, fill, pos, bad); break;
-        case 8: decode_lanes<8><<<grid, CT, 0, s>>>(nvec, vdst, stream, widths, block_base, b0, vsrc, nullptr, nullptr, 0u, off, deg, fill, pos, bad); break;
+        case 1: decode_lanes<1><<<grid, CT, 0, s>>>(nvec, vdst, stream, widths, block_base, b0, vsrc, nullptr, nullptr, 0u, off, deg, fill, pos, bad, cap); break;
+        case 2: decode_lanes<2><<<grid, CT, 0, s>>>(nvec, vdst, stream, widths, block_base, b0, vsrc, nullptr, nullptr, 0u, off, deg, fill, pos, bad, cap); break;
+        case 4: decode_lanes<4><<<grid, CT, 0, s>>>(nvec, vdst, stream, widths, block_base, b0, vsrc, nullptr, nullptr, 0u, off, deg, fill, pos, bad, cap); break;
+        case 8: decode_lanes<8><<<grid, CT, 0, s>>>(nvec, vdst, stream, widths, block_base, b0, vsrc, nullptr, nullptr, 0u, off, deg, fill, pos, bad, cap); break;
         default: WG_REQUIRE(false, "unsupported width %u", width);
     }
     ::wg::count_launch();

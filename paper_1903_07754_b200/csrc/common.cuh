@@ -44,7 +44,7 @@ int launch_decode_lanes(uint64_t nvec, uint32_t width, const uint32_t *vdst, con
 int launch_decode_place(uint64_t nvec, uint32_t width, const uint32_t *vdst, const uint32_t *stream,
                         const uint32_t *widths, const uint64_t *block_base, uint64_t b0, uint64_t b1, uint32_t *vsrc,
                         const uint64_t *off, const uint32_t *deg, uint32_t *fill, uint32_t *pos, unsigned *bad,
-                        cudaStream_t s);
+                        uint64_t cap, cudaStream_t s);
 
 void count_launch(uint64_t k = 1);
 int timer_begin(void *timer, int kind, int64_t it, cudaStream_t s);
@@ -176,7 +176,8 @@ __device__ __forceinline__ T block_sum(T v, T *smem) {
 // s's list behind off[s]; lanes of a warp with the same source share one
 // atomic (RMAT hubs open most destination runs).  Warp-collective.
 __device__ __forceinline__ void place_one(uint32_t s, bool live, uint32_t vec, const uint64_t *off,
-                                          const uint32_t *deg, uint32_t *fill, uint32_t *pos, unsigned *bad) {
+                                          const uint32_t *deg, uint32_t *fill, uint32_t *pos, unsigned *bad,
+                                          uint64_t cap) {
     const uint32_t key = live ? s : WG_NO_LANE;
     const unsigned group = __match_any_sync(FULL, key);
     if (!live) return;
@@ -186,8 +187,8 @@ __device__ __forceinline__ void place_one(uint32_t s, bool live, uint32_t vec, c
     if (lane == leader) base = atomicAdd(&fill[s], (uint32_t)__popc(group));
     base = __shfl_sync(group, base, leader);
     const uint32_t slot = base + __popc(group & lanemask_lt());
-    if (slot < deg[s]) pos[off[s] + slot] = vec;
-    else *bad = 1u;
+    if (slot < deg[s] && off[s] + slot < cap) pos[off[s] + slot] = vec;
+    else *bad = 1u;  // (claimed degrees that overrun the index never write past it)
 }
 
 }  // namespace wg

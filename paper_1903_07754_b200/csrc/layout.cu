@@ -592,7 +592,7 @@ namespace {
 // the source's degree, or a list left short sets *bad, and the caller falls
 // back to the sorted, de-duplicating builder.
 __global__ void place_lanes(uint64_t c0, uint64_t cl, int width, const uint32_t *vsrc, const uint64_t *off,
-                            const uint32_t *deg, uint32_t *fill, uint32_t *pos, unsigned *bad) {
+                            const uint32_t *deg, uint32_t *fill, uint32_t *pos, unsigned *bad, uint64_t cap) {
     const unsigned lane = threadIdx.x & 31u;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); b < cl; b += stride) {
@@ -604,7 +604,7 @@ __global__ void place_lanes(uint64_t c0, uint64_t cl, int width, const uint32_t 
             *bad = 1u;
             live = false;
         }
-        place_one(s, live, (uint32_t)(l / width), off, deg, fill, pos, bad);
+        place_one(s, live, (uint32_t)(l / width), off, deg, fill, pos, bad, cap);
     }
 }
 
@@ -761,7 +761,7 @@ int wg_index_place_chunk(const wg_graph *g, uint64_t v_begin, uint64_t v_end, ui
     const uint64_t c0 = v_begin * g->width, cl = (v_end - v_begin) * g->width;
     if (cl) {
         place_lanes<<<grid_for(cl, 256, 8), 256, 0, s>>>(c0, cl, (int)g->width, g->vsrc, d_idx_off, g->outdeg,
-                                                         ps.fill, d_idx_pos, ps.bad);
+                                                         ps.fill, d_idx_pos, ps.bad, g->entries);
         ::wg::count_launch();
     }
     WG_CHECK_LAUNCH("index place");
@@ -780,7 +780,7 @@ int wg_index_place_coded(const wg_graph *g, const uint32_t *d_stream, const uint
     if (rc) return rc;
     return launch_decode_place(g->nvec, g->width, g->vdst, d_stream, d_widths, d_block_base, block_begin, block_end,
                                const_cast<uint32_t *>(g->vsrc), d_idx_off, g->outdeg, ps.fill, d_idx_pos, ps.bad,
-                               as_stream(stream));
+                               g->entries, as_stream(stream));
 }
 
 int wg_index_place_end(const wg_graph *g, void *d_scratch, size_t scratch_bytes, int *h_ok, void *stream) {
