@@ -243,6 +243,13 @@ def run_b200(args, wl):
             p.timer = timer.handle
         return loop.drive(p, max_it)
 
+    # clock ramp: small workloads (C1: 0.4 ms per step) would otherwise time
+    # steps taken before the SMs leave their idle clocks; untimed, like the
+    # warm-up steps that follow
+    t_ramp = time.perf_counter()
+    while time.perf_counter() - t_ramp < float(os.environ.get("WG_RAMP_S", "0.3")):
+        step()
+        torch.cuda.synchronize()
     for _ in range(args.warmup):
         recs, conv, last = step()
     torch.cuda.synchronize()

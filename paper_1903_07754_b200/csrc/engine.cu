@@ -184,14 +184,18 @@ int launch_group_compaction(const LoopCtx &c, uint32_t *words, uint64_t ngroups,
     return WG_OK;
 }
 
+// keep_list = 0: the member list is built only when the gate (edges,
+// wedge_limit) sends the next iteration to Wedge (the seed of a run whose
+// first iteration is dense needs none)
 int launch_frontier_compaction(const wg_graph *g, const uint32_t *words, uint64_t *bcount,
                                unsigned *ticket, uint32_t *fvert, uint32_t *fpref, uint32_t *tstart,
-                               wg_iter_rec *rec, cudaStream_t s) {
+                               wg_iter_rec *rec, cudaStream_t s, int keep_list = 1, uint64_t wedge_limit = 0) {
     uint64_t nb = fb_blocks(g->n ? g->n : 1);
     const uint64_t *off = lens_are_degrees(g) ? nullptr : g->idx_off;
     WG_CUDA(cudaMemsetAsync(ticket, 0, sizeof(unsigned), s));
     frontier_count_kernel<<<(unsigned)nb, CB_THREADS, 0, s>>>(words, g->n, off, g->outdeg, bcount, ticket,
-                                                              rec); ::wg::count_launch();
+                                                              rec, keep_list, g->edges, wedge_limit);
+    ::wg::count_launch();
     frontier_list_kernel<<<(unsigned)nb, CB_THREADS, 0, s>>>(words, g->n, off, g->outdeg, bcount, fvert,
                                                              fpref, tstart, rec); ::wg::count_launch();
     WG_CHECK_LAUNCH("frontier compaction");
@@ -619,7 +623,7 @@ int wg_run_init(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p,
     WG_CUDA(cudaMemsetAsync(bcount_ticket(g, p->shift, b->bcount), 0, sizeof(unsigned), s));
     return launch_frontier_compaction(g, d_init_words, b->bcount, bcount_ticket(g, p->shift, b->bcount),
                                       b->fvert[0], b->fpref[0], b->tstart[0],
-                                      &b->recs[0], s);
+                                      &b->recs[0], s, (p->flags & WG_RUN_KEEP_LISTS) ? 1 : 0, p->wedge_limit);
 }
 
 static int enqueue_one(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p,

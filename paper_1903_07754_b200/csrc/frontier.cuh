@@ -297,8 +297,10 @@ __device__ __forceinline__ void frontier_list_body(const uint32_t *words, uint64
 __global__ void __launch_bounds__(CB_THREADS) frontier_count_kernel(const uint32_t *words, uint64_t nbits,
                                                                     const uint64_t *idx_off,
                                                                     const uint32_t *outdeg, uint64_t *bcount,
-                                                                    unsigned *counter, wg_iter_rec *rec) {
-    frontier_count_body(words, nbits, idx_off, outdeg, bcount, counter, rec, 1, 0, 0);
+                                                                    unsigned *counter, wg_iter_rec *rec,
+                                                                    int keep_list, uint64_t edges,
+                                                                    uint64_t wedge_limit) {
+    frontier_count_body(words, nbits, idx_off, outdeg, bcount, counter, rec, keep_list, edges, wedge_limit);
 }
 
 __global__ void __launch_bounds__(CB_THREADS) frontier_list_kernel(const uint32_t *words, uint64_t nbits,
