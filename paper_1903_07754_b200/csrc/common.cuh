@@ -187,7 +187,10 @@ __device__ __forceinline__ void place_one(uint32_t s, bool live, uint32_t vec, c
     if (lane == leader) base = atomicAdd(&fill[s], (uint32_t)__popc(group));
     base = __shfl_sync(group, base, leader);
     const uint32_t slot = base + __popc(group & lanemask_lt());
-    if (slot < deg[s] && off[s] + slot < cap) pos[off[s] + slot] = vec;
+    // slot < deg[s] as off[s] + slot < off[s+1]: the neighbouring offset shares
+    // the line, one random access instead of two
+    const uint64_t at = off[s] + slot;
+    if (at < off[s + 1] && at < cap) pos[at] = vec;
     else *bad = 1u;  // (claimed degrees that overrun the index never write past it)
 }
 

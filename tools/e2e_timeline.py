@@ -21,8 +21,16 @@ g = topo.device
 chunks = int(sys.argv[3]) if len(sys.argv) > 3 else max(1, min(8, (g.nvec * g.width) >> 22))
 placed = len(sys.argv) > 4 and sys.argv[4] == "placed"
 prog = wg.make_program(wl["app"], None if wl["app"] == "cc" else 0)
-host = {"voff": g.vector_offsets().cpu().pin_memory()}
-if fmt == "coded":
+kw = {}
+if fmt == "compact":  # bench.py's default host format
+    host = g.host_format(symmetric=bool(wl.get("sym") or "grid" in wl))
+    kw["outdeg_is_indeg"] = bool(wl.get("sym") or "grid" in wl)
+    placed = False
+else:
+    host = {"voff": g.vector_offsets().cpu().pin_memory()}
+if fmt == "compact":
+    pass
+elif fmt == "coded":
     host.update({k: v.cpu().pin_memory() for k, v in g.encode_lanes().items()})
 elif fmt == "bits":
     host["vsrc_bits"] = g.pack_lanes()[0].cpu().pin_memory()
@@ -32,7 +40,7 @@ if placed:
     host["outdeg"] = g.outdeg[: g.n].cpu().pin_memory()
 if g.vw8 is not None:
     host["vw8"] = g.vw8[: g.nvec * g.width].cpu().pin_memory()
-dev = {k: torch.empty(v.numel() + 64, dtype=v.dtype, device="cuda")[: v.numel()] for k, v in host.items()}
+dev = {k: torch.empty(v.numel() + 64, dtype=v.dtype, device="cuda")[: v.numel()].view(v.shape) for k, v in host.items()}
 for k, v in host.items():
     dev[k].copy_(v)
 dev["vsrc"] = torch.empty(g.nvec * g.width + 64, dtype=torch.int32, device="cuda")[: g.nvec * g.width]
@@ -41,7 +49,8 @@ vw = None
 if g.vw8 is not None:
     vw = torch.empty(g.nvec * g.width + 64, dtype=torch.int32, device="cuda")[: g.nvec * g.width]
     vw.copy_(g.vw)
-g2 = dv.DeviceGraph.from_lanes(g.n, g.width, g.edges, g.nvec, dev["vsrc"], vw, dev["voff"])
+g2 = dv.DeviceGraph.from_lanes(g.n, g.width, g.edges, g.nvec, dev["vsrc"], vw,
+                               dev["voff"] if "voff" in dev else g.vector_offsets())
 if g.vw8 is not None:
     g2.vw8 = dev["vw8"]
     g2._struct = None
@@ -64,7 +73,7 @@ rows = []
 for rep in range(5):
     tr = []
     ev("start", tr)
-    g2.upload_rebuild(host, dev, chunks=chunks, copy_stream=cs, trace=tr)
+    g2.upload_rebuild(host, dev, chunks=chunks, copy_stream=cs, trace=tr, **kw)
     ev("rebuilt", tr)
     p = loop.seed(init, words, prog.kernel, Fraction(wl["thr"]))
     recs, conv, last = loop.drive(p, g.n + 16)
