@@ -59,6 +59,10 @@ loop = dv.DeviceLoop(g2, shift, _lib.WG_VAL_U32)
 init = dv.encode_values(_initial_values(prog, g.n), _lib.WG_VAL_U32)
 words = dv.all_words(g.n) if wl["app"] == "cc" else dv.initial_words(g.n, np.array([0]))
 out_host = torch.empty(g.n, dtype=torch.int32).pin_memory()
+iv = _initial_values(prog, g.n)
+members = None if wl["app"] == "cc" else np.array([0])
+fh = dv.first_hit_ok(prog.kernel, iv, members)
+flags = dict(first_hit=fh, level_base=dv.first_hit_level(iv) if fh else 0, identity_init=dv.identity_values(iv))
 cs = torch.cuda.Stream()
 h2d = sum(v.numel() * v.element_size() for v in host.values())
 
@@ -75,11 +79,14 @@ for rep in range(5):
     ev("start", tr)
     g2.upload_rebuild(host, dev, chunks=chunks, copy_stream=cs, trace=tr, **kw)
     ev("rebuilt", tr)
-    p = loop.seed(init, words, prog.kernel, Fraction(wl["thr"]))
+    p = loop.seed(init, words, prog.kernel, Fraction(wl["thr"]), **flags)
     recs, conv, last = loop.drive(p, g.n + 16)
     ev("loop", tr)
     out_host.copy_(loop.values_after(last), non_blocking=True)
     ev("d2h", tr)
+    p = loop.seed(init, words, prog.kernel, Fraction(wl["thr"]), **flags)
+    loop.drive(p, g.n + 16)
+    ev("loop again", tr)
     torch.cuda.synchronize()
     t0 = tr[0][1]
     rows.append([(lab, t0.elapsed_time(e)) for lab, e in tr])
