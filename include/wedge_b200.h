@@ -313,6 +313,11 @@ typedef struct wg_run_params {
  * within a destination, graph.py:235), one load per destination.  Results
  * and counters unchanged. */
 #define WG_RUN_IDENTITY_INIT 8
+/* uint32 values, unfiltered program: a dense pull reads prev[d] ahead and a
+ * destination already at 0 -- below which no candidate can go -- gathers
+ * nothing (it is still counted as touched).  Results and counters
+ * unchanged. */
+#define WG_RUN_FLOOR_SKIP 16
 
 /* Element counts: [0] fbits words, [1] groups, [2] gbits words, [3] bcount
  * entries, [4] tstart entries (the caller multiplies by element sizes). */

@@ -57,6 +57,7 @@ class WgRunParams(ctypes.Structure):
 WG_RUN_FIRST_HIT = 1
 WG_RUN_KEEP_LISTS = 2
 WG_RUN_IDENTITY_INIT = 8
+WG_RUN_FLOOR_SKIP = 16
 WG_CODED_BLOCK_VECTORS = 1024
 
 

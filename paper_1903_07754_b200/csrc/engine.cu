@@ -323,7 +323,8 @@ int launch_pull(const LoopCtx &c, const wg_graph *g, const PullBufs &pb, int val
             WG_CHECK_LAUNCH("pull (identity)");
         }
         size_t smem = 0;
-        DenseFn dn = pick_dense(val_type, (int)g->width, weight, filter, &smem);
+        // floor skipping runs an unfiltered program on the filtered pipeline
+        DenseFn dn = pick_dense(val_type, (int)g->width, weight, filter || pb.floor_skip, &smem);
         unsigned grid = persistent_grid(dn, PULL_THREADS, (g->nvec + 255) / 256, smem);
         dn<<<grid, PULL_THREADS, smem, s>>>(c, *g, pb, shift, k->apply_increment, k->sentinel);
         ::wg::count_launch();
@@ -585,6 +586,7 @@ static PullBufs pull_bufs(const wg_graph *g, const wg_run_bufs *b, const wg_run_
     pb.first_hit = (p->flags & WG_RUN_FIRST_HIT) && p->kern.filter_unvisited && !p->kern.use_weight ? 1u : 0u;
     pb.level_base = p->level_base;
     pb.ident = (p->flags & WG_RUN_IDENTITY_INIT) ? 1u : 0u;
+    pb.floor_skip = (p->flags & WG_RUN_FLOOR_SKIP) && p->val_type == WG_VAL_U32 && !p->kern.filter_unvisited ? 1u : 0u;
     return pb;
 }
 

@@ -62,6 +62,7 @@ struct PullBufs {
     uint32_t n;
     uint32_t first_hit;  // WG_RUN_FIRST_HIT (filtered pulls only)
     uint32_t ident;      // WG_RUN_IDENTITY_INIT
+    uint32_t floor_skip; // WG_RUN_FLOOR_SKIP: dense pulls skip destinations already at 0
     int64_t level_base;  // its frontier-0 value
 };
 
@@ -634,8 +635,13 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) pull_dense_tma_kernel(Loop
     // level = base + (it-1)*inc, so its frontier bit replaces the value gather.
     // Frontier 0 lives in the caller's initial words, hence it > 1.
     const bool bottom_up = FILTER && b.first_hit && it > 1;
+    // unfiltered program run on the filtered pipeline: prev[d] of every
+    // destination is read ahead and one already at 0 (the floor of any
+    // min-plus candidate over uint32) gathers nothing -- CC from iteration 2
+    // on, where the giant component's label 0 spreads over most vertices
+    const bool floor = FILTER && b.floor_skip;
     // identity initial values: iteration 1 belongs to pull_ident_kernel
-    const bool ident = !FILTER && !WEIGHT && b.ident && it == 1;
+    const bool ident = (!FILTER || floor) && !WEIGHT && b.ident && it == 1;
     const uint32_t *__restrict__ inbits = (((it - 1) & 1) ? b.fbits[1] : b.fbits[0]);
     const T level = (T)(b.level_base + (int64_t)(it - 1) * inc);
     const uint64_t gwarp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -654,7 +660,7 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) pull_dense_tma_kernel(Loop
     if (t0w < t1w) {
         const uint32_t tfirst = (uint32_t)t0w, tend = (uint32_t)t1w;
         const uint32_t vend = (tend << 5) < nvec ? (tend << 5) : nvec;
-        if (!FILTER) o.touched = vend - (tfirst << 5);  // every vector of the range is processed
+        if (!FILTER || floor) o.touched = vend - (tfirst << 5);  // every vector of the range is processed
         const uint32_t nchunks = (tend - tfirst + CH - 1) / CH;
         if (lane == 0) {
             for (int s = 0; s < TMA_S; ++s) mbar_init(&bars[s], 1);
@@ -700,7 +706,9 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) pull_dense_tma_kernel(Loop
 #pragma unroll
             for (int u = 0; u < CH; ++u) {
                 bool pull = true;
-                if (FILTER) {
+                if (FILTER && floor) {
+                    pull = k.valid[u] && k.pd[u] != (T)0;
+                } else if (FILTER) {
                     const bool unv = k.valid[u] && k.pd[u] == INF;  // only unvisited destinations
                     o.touched += __popc(__ballot_sync(FULL, unv));
                     pull = unv && k.d[u] != hit_d;

@@ -9,6 +9,7 @@ uint32 device data is stored in ``torch.int32`` tensors (same bits).
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass, field
 from fractions import Fraction
 from typing import Optional
@@ -705,6 +706,8 @@ class DeviceLoop:
         p.kern = _minplus(kern, UNREACHED)
         p.wedge_limit = wedge_limit(threshold, self.g.edges) if self.g.edges > 0 else 0
         p.flags = (_lib.WG_RUN_FIRST_HIT if first_hit else 0) | (_lib.WG_RUN_IDENTITY_INIT if identity_init else 0)
+        if identity_init and os.environ.get("WG_FLOOR_SKIP", "1") != "0":
+            p.flags |= _lib.WG_RUN_FLOOR_SKIP  # CC-like runs: label 0 spreads over the giant component
         p.level_base = int(self._level_base) if first_hit else 0
         return p
 
