@@ -518,8 +518,13 @@ def roofline(rows, recs, n, E, weighted, filt, wl, ident_first=False):
         prev_out = U
     if dense_t > 0:
         ach = dense_b / (dense_t * 1e-3) / 1e9
-        kernel = (f"pull_dense_tma_kernel<u32,W{wl.get('W', 4)}> (K6, dense pull)" if not filt else
-                  f"pull_dense_tma_kernel<u32,W{wl.get('W', 4)},filter> (K6, dense filtered pull)")
+        if filt:
+            kernel = f"pull_dense_tma_kernel<u32,W{wl.get('W', 4)},filter> (K6, dense filtered pull)"
+        elif ident_first and os.environ.get("WG_FLOOR_SKIP", "1") != "0":
+            kernel = (f"pull_dense_tma_kernel<u32,W{wl.get('W', 4)},filtered pipeline> (K6, dense pull with "
+                      "floor skipping: destinations at label 0 gather nothing, every lane still streamed)")
+        else:
+            kernel = f"pull_dense_tma_kernel<u32,W{wl.get('W', 4)}> (K6, dense pull)"
         traffic = dense_b / max(1, sum(1 for r in recs if r.mode == "FullScan"
                                        and not (ident_first and r.iteration == 1)))
     else:
