@@ -795,10 +795,14 @@ class DeviceLoop:
         while it <= max_iterations and not converged:
             limit = min(max_iterations, it - 1 + self.ring - 2)
             check(L.wg_run_loop_launch(exe, ctypes.byref(self.bufs), limit, _lib.stream_ptr(stream)))
+            # the control word and the whole record ring in one round trip (a
+            # launch runs at most ring - 2 iterations, so its records are all there)
             ctrl_host.copy_(self.ctrl, non_blocking=True)
+            self.host_recs.copy_(self.recs, non_blocking=True)
             s.synchronize()
             done = min(int(ctrl_host[0]), limit)
-            rows = self._read(it, done - it + 1, stream) if done >= it else []
+            arr = self.host_recs.numpy().view(np.uint64).reshape(self.ring, REC_U64)
+            rows = [arr[(it + j) % self.ring] for j in range(done - it + 1)] if done >= it else []
             conv, at = self._parse(rows, it, records, None)
             if records:
                 last = records[-1].iteration
