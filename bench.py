@@ -247,7 +247,7 @@ def run_b200(args, wl):
     # steps taken before the SMs leave their idle clocks; untimed, like the
     # warm-up steps that follow
     t_ramp = time.perf_counter()
-    while time.perf_counter() - t_ramp < float(os.environ.get("WG_RAMP_S", "0.3")):
+    while time.perf_counter() - t_ramp < float(os.environ.get("WG_RAMP_S", "1.0")):
         step()
         torch.cuda.synchronize()
     for _ in range(args.warmup):
