@@ -742,6 +742,12 @@ class DeviceLoop:
         arr = self.host_recs.numpy().view(np.uint64).reshape(self.ring, REC_U64)
         return [arr[(it_begin + j) % self.ring] for j in range(count)]
 
+    def launch(self, p: WgRunParams, limit: int, stream=None) -> None:
+        """Run the loop graph up to iteration `limit` without reading anything
+        back (one launch instead of one per kernel; the caller synchronises)."""
+        check(_lib.load().wg_run_loop_launch(self._graph_for(p, stream), ctypes.byref(self.bufs), int(limit),
+                                             _lib.stream_ptr(stream)))
+
     def _graph_for(self, p: WgRunParams, stream=None):
         key = (p.val_type, p.shift, p.kern.filter_unvisited, p.kern.use_weight, p.kern.apply_increment,
                p.kern.sentinel, p.wedge_limit, p.flags, p.level_base)

@@ -26,6 +26,7 @@ the device shard (``DeviceShard``) runs the sm_100a kernels.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass, field
 from fractions import Fraction
 from typing import Optional
@@ -226,7 +227,10 @@ class DeviceShard:
     def step(self, it: int):
         """Local iteration + pack of its members (no host synchronisation)."""
         L = self._lib.load()
-        self.loop.enqueue(self.p, it, 1)
+        if os.environ.get("WG_SHARD_GRAPH", "1") != "0":
+            self.loop.launch(self.p, it)  # the loop graph, stopped after iteration `it`
+        else:
+            self.loop.enqueue(self.p, it, 1)
         self._lib.check(L.wg_exchange_pack_all(ctypes.byref(self.g.struct()), ctypes.byref(self.loop.bufs),
                                                ctypes.byref(self.p), it, self.send.data_ptr(), self.capacity,
                                                self._lib.stream_ptr()))
