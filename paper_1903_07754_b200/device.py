@@ -243,8 +243,8 @@ class DeviceGraph:
     @staticmethod
     def compact_degrees(deg):
         """(min(deg, 255) as uint8, int32 [k, 2] (vertex, degree) for the rest)
-        -- the upload form wg_widen_degrees reads."""
-        torch = _torch()
+        -- the upload form wg_widen_degrees reads (a tensor op on deg's device)."""
+        import torch
         big = torch.nonzero(deg >= 255).flatten()
         pairs = torch.stack([big.to(torch.int32), deg[big].to(torch.int32)], 1).contiguous()
         return deg.clamp(max=255).to(torch.uint8), pairs

@@ -217,3 +217,21 @@ def test_first_hit_condition():
     assert not first_hit_ok(k, np.array([0, 5, U, U]), np.array([0, 1]))   # two levels
     assert not first_hit_ok(k, np.array([0, 0, U, U]), np.array([0]))      # finite non-member
     assert first_hit_ok(k, np.array([U, U]), np.array([0]))
+
+
+def test_compact_degree_form_round_trips():
+    """The e2e host format's degrees (DeviceGraph.compact_degrees): a byte per
+    vertex plus (vertex, degree) pairs for the rest -- what wg_widen_degrees
+    expands on the device -- restated here with numpy on CPU tensors."""
+    import torch
+    from paper_1903_07754_b200.device import DeviceGraph
+    rng = np.random.default_rng(3)
+    deg = torch.from_numpy((rng.pareto(0.8, 5000) * 40).astype(np.int32))
+    deg[7] = 255
+    deg[9] = 254
+    d8, big = DeviceGraph.compact_degrees(deg)
+    assert d8.dtype == torch.uint8 and big.dtype == torch.int32 and big.shape[1] == 2
+    back = d8.numpy().astype(np.int64)
+    back[big[:, 0].numpy()] = big[:, 1].numpy()
+    assert np.array_equal(back, deg.numpy())
+    assert 7 in big[:, 0].tolist() and 9 not in big[:, 0].tolist()
