@@ -322,13 +322,35 @@ int launch_pull(const LoopCtx &c, const wg_graph *g, const PullBufs &pb, int val
             ::wg::count_launch();
             WG_CHECK_LAUNCH("pull (identity)");
         }
-        size_t smem = 0;
-        // floor skipping runs an unfiltered program on the filtered pipeline
-        DenseFn dn = pick_dense(val_type, (int)g->width, weight, filter || pb.floor_skip, &smem);
-        unsigned grid = persistent_grid(dn, PULL_THREADS, (g->nvec + 255) / 256, smem);
-        dn<<<grid, PULL_THREADS, smem, s>>>(c, *g, pb, shift, k->apply_increment, k->sentinel);
-        ::wg::count_launch();
-        WG_CHECK_LAUNCH("pull (dense, TMA)");
+        if (pb.floor_kernels && !weight && !filter) {
+            // floor skipping from iteration 2 on: init pass + sparse-style pull
+            // (iteration 1 is pull_ident_kernel's; these return there)
+            using FiFn = void (*)(LoopCtx, wg_graph, PullBufs);
+            using FpFn = void (*)(LoopCtx, wg_graph, PullBufs, int64_t, int64_t);
+            const bool u32 = val_type == WG_VAL_U32;
+            FiFn fi = u32 ? floor_init_kernel<uint32_t> : floor_init_kernel<int64_t>;
+            FpFn fp = nullptr;
+            switch (g->width) {
+                case 1: fp = u32 ? floor_pull_kernel<uint32_t, 1> : floor_pull_kernel<int64_t, 1>; break;
+                case 2: fp = u32 ? floor_pull_kernel<uint32_t, 2> : floor_pull_kernel<int64_t, 2>; break;
+                case 4: fp = u32 ? floor_pull_kernel<uint32_t, 4> : floor_pull_kernel<int64_t, 4>; break;
+                case 8: fp = u32 ? floor_pull_kernel<uint32_t, 8> : floor_pull_kernel<int64_t, 8>; break;
+            }
+            WG_REQUIRE(fp != nullptr, "no floor pull for width %u", g->width);
+            fi<<<grid_for(g->nvec, 256 * 4, 8), 256, 0, s>>>(c, *g, pb);
+            fp<<<grid_for(g->nvec, 256 * 4, 8), 256, 0, s>>>(c, *g, pb, k->apply_increment, k->sentinel);
+            ::wg::count_launch(2);
+            WG_CHECK_LAUNCH("pull (floor)");
+        }
+        {
+            size_t smem = 0;
+            // floor skipping runs an unfiltered program on the filtered pipeline
+            DenseFn dn = pick_dense(val_type, (int)g->width, weight, filter || pb.floor_skip, &smem);
+            unsigned grid = persistent_grid(dn, PULL_THREADS, (g->nvec + 255) / 256, smem);
+            dn<<<grid, PULL_THREADS, smem, s>>>(c, *g, pb, shift, k->apply_increment, k->sentinel);
+            ::wg::count_launch();
+            WG_CHECK_LAUNCH("pull (dense, TMA)");
+        }
         if (slot) {
             timer_end(timer, *slot, s);
             *slot = timer_begin(timer, 4, (int64_t)c.it_arg, s);
@@ -587,6 +609,10 @@ static PullBufs pull_bufs(const wg_graph *g, const wg_run_bufs *b, const wg_run_
     pb.level_base = p->level_base;
     pb.ident = (p->flags & WG_RUN_IDENTITY_INIT) ? 1u : 0u;
     pb.floor_skip = (p->flags & WG_RUN_FLOOR_SKIP) && p->val_type == WG_VAL_U32 && !p->kern.filter_unvisited ? 1u : 0u;
+    {
+        const char *e = getenv("WG_FLOOR_KERNELS");
+        pb.floor_kernels = pb.floor_skip && !p->kern.use_weight && !(e && e[0] == '0') ? 1u : 0u;
+    }
     return pb;
 }
 
