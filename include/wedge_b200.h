@@ -315,8 +315,10 @@ typedef struct wg_run_params {
 #define WG_RUN_IDENTITY_INIT 8
 /* uint32 values, unfiltered program: a dense pull reads prev[d] ahead and a
  * destination already at 0 -- below which no candidate can go -- gathers
- * nothing (it is still counted as touched).  Results and counters
- * unchanged. */
+ * nothing (it is still counted as touched); unweighted, from the third
+ * iteration on, the dense pull is an init pass plus an atomic-min pull over
+ * the vectors of destinations not at 0 (env WG_FLOOR_KERNELS=0 keeps the
+ * pipeline).  Results and counters unchanged. */
 #define WG_RUN_FLOOR_SKIP 16
 
 /* Element counts: [0] fbits words, [1] groups, [2] gbits words, [3] bcount
