@@ -498,6 +498,9 @@ def roofline(rows, recs, n, E, weighted, filt, wl, ident_first=False):
     step_t = 0.0
     prev_out = None
     per_iter = []
+    # iterations >= 3 of a floor-skipping run use floor_init/floor_pull
+    floor_k = (ident_first and os.environ.get("WG_FLOOR_SKIP", "1") != "0"
+               and os.environ.get("WG_FLOOR_KERNELS", "1") != "0")
     for r in recs:
         t = by_it.get(r.iteration, {})
         pull_ms = t.get(2, 0.0)
@@ -507,6 +510,11 @@ def roofline(rows, recs, n, E, weighted, filt, wl, ident_first=False):
         U = r.frontier_out_size
         if r.mode == "FullScan" and ident_first and r.iteration == 1:
             b = 4 * n + 4 * n + 4 * U + n / 8  # vec_dst run heads + one lane per destination + apply
+        elif r.mode == "FullScan" and floor_k and r.iteration >= 3:
+            # floor_init/floor_pull: vec_dst twice, prev[d], nxt[d], lanes of non-floor
+            # destinations only (a few per mille here) -- reported on its own, not as
+            # the pipeline's dense figure
+            b = 2 * 4 * (E // 4) + 4 * n + 4 * n + 4 * U + n / 8
         elif r.mode == "FullScan":
             ep = E if not filt else min(E, 4 * r.vectors_touched)
             b = 4 * ep * (1 + w) + 4 * n + 4 * U + n / 8
@@ -532,7 +540,8 @@ def roofline(rows, recs, n, E, weighted, filt, wl, ident_first=False):
         else:
             kernel = f"pull_dense_tma_kernel<u32,W{wl.get('W', 4)}> (K6, dense pull)"
         traffic = dense_b / max(1, sum(1 for r in recs if r.mode == "FullScan"
-                                       and not (ident_first and r.iteration == 1)))
+                                       and not (ident_first and r.iteration == 1)
+                                       and not (floor_k and r.iteration >= 3)))
     else:
         ach = wedge_b / (wedge_t * 1e-3) / 1e9 if wedge_t else 0.0
         kernel = "transform + wedge pull (K3+K4+K5)"
