@@ -323,12 +323,10 @@ int launch_pull(const LoopCtx &c, const wg_graph *g, const PullBufs &pb, int val
             WG_CHECK_LAUNCH("pull (identity)");
         }
         if (pb.floor_kernels && !weight && !filter) {
-            // floor skipping from iteration 2 on: init pass + sparse-style pull
-            // (iteration 1 is pull_ident_kernel's; these return there)
-            using FiFn = void (*)(LoopCtx, wg_graph, PullBufs);
+            // floor skipping from FLOOR_KERNELS_FROM on: one atomic-min pass
+            // (earlier iterations return at once)
             using FpFn = void (*)(LoopCtx, wg_graph, PullBufs, int64_t, int64_t);
             const bool u32 = val_type == WG_VAL_U32;
-            FiFn fi = u32 ? floor_init_kernel<uint32_t> : floor_init_kernel<int64_t>;
             FpFn fp = nullptr;
             switch (g->width) {
                 case 1: fp = u32 ? floor_pull_kernel<uint32_t, 1> : floor_pull_kernel<int64_t, 1>; break;
@@ -337,9 +335,8 @@ int launch_pull(const LoopCtx &c, const wg_graph *g, const PullBufs &pb, int val
                 case 8: fp = u32 ? floor_pull_kernel<uint32_t, 8> : floor_pull_kernel<int64_t, 8>; break;
             }
             WG_REQUIRE(fp != nullptr, "no floor pull for width %u", g->width);
-            fi<<<grid_for(g->nvec, 256 * 4, 8), 256, 0, s>>>(c, *g, pb);
             fp<<<grid_for(g->nvec, 256 * 4, 8), 256, 0, s>>>(c, *g, pb, k->apply_increment, k->sentinel);
-            ::wg::count_launch(2);
+            ::wg::count_launch();
             WG_CHECK_LAUNCH("pull (floor)");
         }
         {

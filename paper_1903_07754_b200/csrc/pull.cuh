@@ -557,27 +557,14 @@ __global__ void __launch_bounds__(256) pull_ident_kernel(LoopCtx c, wg_graph g, 
 // Floor-skipping dense pull (WG_RUN_FLOOR_SKIP, iterations >= 3; CC): the
 // same result as pull_dense_tma_kernel without streaming the layout through
 // a pipeline -- after two iterations almost every in-edge belongs to a
-// destination already at 0.  floor_init: every destination's first vector
-// writes nxt[d] = prev[d]; floor_pull (stream-ordered after it): a vector
-// whose destination is not at 0 gathers its lanes and lowers nxt[d] with an
-// atomic min, setting d's frontier bit when its candidate beats prev[d].
+// destination already at 0.  A thread per vector: the destination's first
+// vector lowers nxt[d] to prev[d], a vector whose destination is not at 0
+// gathers its lanes and lowers nxt[d] with an atomic min, setting d's
+// frontier bit when its candidate beats prev[d].
 // Every vector counts as touched (the reference's full scan).  Iteration 2,
 // where a third of the in-edges still gather (CC s22), stays on the TMA
 // pipeline (0.43 vs 0.52 ms); iteration 3 gathers for 0.2% (0.18 vs 0.38 ms).
 constexpr uint64_t FLOOR_KERNELS_FROM = 3;
-
-template <typename T>
-__global__ void __launch_bounds__(256) floor_init_kernel(LoopCtx c, wg_graph g, PullBufs b) {
-    const uint64_t it = ctx_iter(c);
-    if (ctx_mode(c, it) != MODE_FULL || it < FLOOR_KERNELS_FROM) return;
-    const T *__restrict__ prev = (const T *)(((it - 1) & 1) ? b.vals[1] : b.vals[0]);
-    T *__restrict__ nxt = (T *)((it & 1) ? b.vals[1] : b.vals[0]);
-    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < g.nvec;
-         v += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t d = g.vdst[v];
-        if (v == 0 || g.vdst[v - 1] != d) nxt[d] = prev[d];
-    }
-}
 
 template <typename T, int W>
 __global__ void __launch_bounds__(256) floor_pull_kernel(LoopCtx c, wg_graph g, PullBufs b, int64_t inc,
@@ -591,30 +578,61 @@ __global__ void __launch_bounds__(256) floor_pull_kernel(LoopCtx c, wg_graph g, 
     uint32_t *__restrict__ obits = ((it & 1) ? b.fbits[1] : b.fbits[0]);
     const T INF = VT::inf(sentinel);
     uint32_t ovf = 0;
-    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < g.nvec;
-         v += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t d = g.vdst[v];
-        const T pd = prev[d];
-        if (pd == (T)0) continue;  // at the floor: nothing can lower it
-        uint32_t src[W], wt[W];
-        load_lanes<W>(g.vsrc, v, src);
-        const T agg = fold_lanes<T, W, false>(src, wt, prev, INF, ovf);
-        if (agg == INF) continue;
-        T cand;
-        if constexpr (VT::U32) {
-            const uint64_t cc = (uint64_t)agg + (uint64_t)inc;
-            if (cc >= 0xffffffffull) {
-                ovf = 1;
-                continue;
-            }
-            cand = (T)cc;
-        } else {
-            cand = agg + (T)inc;
+    // K vectors per thread in flight: destinations, then prev[d], then the
+    // lanes and gathers of those not at the floor, then the atomics
+    constexpr int K = 4;
+    const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; base < g.nvec; base += K * nth) {
+        uint32_t d[K];
+        T pd[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const uint64_t v = base + k * nth;
+            d[k] = v < g.nvec ? g.vdst[v] : NONE;
         }
-        if (cand < pd) {
-            if constexpr (VT::U32) atomicMin((unsigned *)&nxt[d], (unsigned)cand);
-            else atomicMin((long long *)&nxt[d], (long long)cand);
-            atomicOr(&obits[d >> 5], 1u << (d & 31));
+#pragma unroll
+        for (int k = 0; k < K; ++k) pd[k] = d[k] != NONE ? prev[d[k]] : (T)0;  // 0: nothing to do
+        // a destination's first vector lowers nxt[d] to prev[d]: the buffer holds
+        // the values of two iterations ago, never below prev (values only
+        // decrease), so every destination ends at min(prev[d], its candidates)
+        // in any order of the atomics -- no separate init pass
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const uint64_t v = base + k * nth;
+            if (d[k] != NONE && (v == 0 || g.vdst[v - 1] != d[k])) {
+                if constexpr (VT::U32) atomicMin((unsigned *)&nxt[d[k]], (unsigned)pd[k]);
+                else atomicMin((long long *)&nxt[d[k]], (long long)pd[k]);
+            }
+        }
+        T agg[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            agg[k] = INF;
+            if (pd[k] != (T)0) {  // at the floor nothing can lower it
+                uint32_t src[W], wt[W];
+                load_lanes<W>(g.vsrc, base + k * nth, src);
+                agg[k] = fold_lanes<T, W, false>(src, wt, prev, INF, ovf);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            if (agg[k] == INF) continue;
+            T cand;
+            if constexpr (VT::U32) {
+                const uint64_t cc = (uint64_t)agg[k] + (uint64_t)inc;
+                if (cc >= 0xffffffffull) {
+                    ovf = 1;
+                    continue;
+                }
+                cand = (T)cc;
+            } else {
+                cand = agg[k] + (T)inc;
+            }
+            if (cand < pd[k]) {
+                if constexpr (VT::U32) atomicMin((unsigned *)&nxt[d[k]], (unsigned)cand);
+                else atomicMin((long long *)&nxt[d[k]], (long long)cand);
+                atomicOr(&obits[d[k] >> 5], 1u << (d[k] & 31));
+            }
         }
     }
     if (ovf) out->overflow = 1;
