@@ -63,7 +63,7 @@ struct PullBufs {
     uint32_t first_hit;  // WG_RUN_FIRST_HIT (filtered pulls only)
     uint32_t ident;      // WG_RUN_IDENTITY_INIT
     uint32_t floor_skip; // WG_RUN_FLOOR_SKIP: dense pulls skip destinations already at 0
-    uint32_t floor_kernels;  // ... and from FLOOR_KERNELS_FROM on run floor_init/floor_pull
+    uint32_t floor_kernels;  // ... and from FLOOR_KERNELS_FROM on run floor_pull_kernel
     int64_t level_base;  // its frontier-0 value
 };
 
@@ -744,7 +744,7 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) pull_dense_tma_kernel(Loop
     uint64_t t0w, t1w;
     warp_range(((uint64_t)nvec + 31) >> 5, gwarp, nwarps, t0w, t1w);
     if (ident) return;  // pull_ident_kernel did this iteration
-    if (floor && b.floor_kernels && it >= FLOOR_KERNELS_FROM) return;  // floor_init/floor_pull did
+    if (floor && b.floor_kernels && it >= FLOOR_KERNELS_FROM) return;  // floor_pull_kernel did
     if (t0w < t1w) {
         const uint32_t tfirst = (uint32_t)t0w, tend = (uint32_t)t1w;
         const uint32_t vend = (tend << 5) < nvec ? (tend << 5) : nvec;
