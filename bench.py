@@ -498,7 +498,7 @@ def roofline(rows, recs, n, E, weighted, filt, wl, ident_first=False):
     step_t = 0.0
     prev_out = None
     per_iter = []
-    # iterations >= 3 of a floor-skipping run use floor_init/floor_pull
+    # iterations >= 3 of a floor-skipping run use floor_pull_kernel
     floor_k = (ident_first and os.environ.get("WG_FLOOR_SKIP", "1") != "0"
                and os.environ.get("WG_FLOOR_KERNELS", "1") != "0")
     for r in recs:
@@ -511,10 +511,10 @@ def roofline(rows, recs, n, E, weighted, filt, wl, ident_first=False):
         if r.mode == "FullScan" and ident_first and r.iteration == 1:
             b = 4 * n + 4 * n + 4 * U + n / 8  # vec_dst run heads + one lane per destination + apply
         elif r.mode == "FullScan" and floor_k and r.iteration >= 3:
-            # floor_init/floor_pull: vec_dst twice, prev[d], nxt[d], lanes of non-floor
-            # destinations only (a few per mille here) -- reported on its own, not as
-            # the pipeline's dense figure
-            b = 2 * 4 * (E // 4) + 4 * n + 4 * n + 4 * U + n / 8
+            # floor_pull_kernel: vec_dst, prev[d], nxt[d], lanes of non-floor destinations
+            # only (a few per mille here) -- reported on its own, not as the
+            # pipeline's dense figure
+            b = 4 * (E // 4) + 4 * n + 4 * n + 4 * U + n / 8
         elif r.mode == "FullScan":
             ep = E if not filt else min(E, 4 * r.vectors_touched)
             b = 4 * ep * (1 + w) + 4 * n + 4 * U + n / 8
