@@ -609,6 +609,9 @@ static PullBufs pull_bufs(const wg_graph *g, const wg_run_bufs *b, const wg_run_
     {
         const char *e = getenv("WG_FLOOR_KERNELS");
         pb.floor_kernels = pb.floor_skip && !p->kern.use_weight && !(e && e[0] == '0') ? 1u : 0u;
+        const char *f = getenv("WG_FLOOR_FROM");
+        pb.floor_from = f ? (uint32_t)atoi(f) : (uint32_t)FLOOR_KERNELS_FROM;
+        if (pb.floor_from < 2) pb.floor_from = 2;  // iteration 1 is pull_ident_kernel's
     }
     return pb;
 }

@@ -63,7 +63,8 @@ struct PullBufs {
     uint32_t first_hit;  // WG_RUN_FIRST_HIT (filtered pulls only)
     uint32_t ident;      // WG_RUN_IDENTITY_INIT
     uint32_t floor_skip; // WG_RUN_FLOOR_SKIP: dense pulls skip destinations already at 0
-    uint32_t floor_kernels;  // ... and from FLOOR_KERNELS_FROM on run floor_pull_kernel
+    uint32_t floor_kernels;  // ... and from iteration floor_from on run floor_pull_kernel
+    uint32_t floor_from;
     int64_t level_base;  // its frontier-0 value
 };
 
@@ -571,7 +572,7 @@ __global__ void __launch_bounds__(256) floor_pull_kernel(LoopCtx c, wg_graph g, 
                                                          int64_t sentinel) {
     using VT = ValTraits<T>;
     const uint64_t it = ctx_iter(c);
-    if (ctx_mode(c, it) != MODE_FULL || it < FLOOR_KERNELS_FROM) return;
+    if (ctx_mode(c, it) != MODE_FULL || it < b.floor_from) return;
     wg_iter_rec *out = ctx_out(c, it);
     const T *__restrict__ prev = (const T *)(((it - 1) & 1) ? b.vals[1] : b.vals[0]);
     T *__restrict__ nxt = (T *)((it & 1) ? b.vals[1] : b.vals[0]);
@@ -744,7 +745,7 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) pull_dense_tma_kernel(Loop
     uint64_t t0w, t1w;
     warp_range(((uint64_t)nvec + 31) >> 5, gwarp, nwarps, t0w, t1w);
     if (ident) return;  // pull_ident_kernel did this iteration
-    if (floor && b.floor_kernels && it >= FLOOR_KERNELS_FROM) return;  // floor_pull_kernel did
+    if (floor && b.floor_kernels && it >= b.floor_from) return;  // floor_pull_kernel did
     if (t0w < t1w) {
         const uint32_t tfirst = (uint32_t)t0w, tend = (uint32_t)t1w;
         const uint32_t vend = (tend << 5) < nvec ? (tend << 5) : nvec;
