@@ -322,6 +322,21 @@ int launch_pull(const LoopCtx &c, const wg_graph *g, const PullBufs &pb, int val
             ::wg::count_launch();
             WG_CHECK_LAUNCH("pull (identity)");
         }
+        if (pb.floor_kernels && filter && pb.first_hit && !weight) {
+            using BuFn = void (*)(LoopCtx, wg_graph, PullBufs, int64_t, int64_t);
+            const bool u32 = val_type == WG_VAL_U32;
+            BuFn fb = nullptr;
+            switch (g->width) {
+                case 1: fb = u32 ? bottom_up_pull_kernel<uint32_t, 1> : bottom_up_pull_kernel<int64_t, 1>; break;
+                case 2: fb = u32 ? bottom_up_pull_kernel<uint32_t, 2> : bottom_up_pull_kernel<int64_t, 2>; break;
+                case 4: fb = u32 ? bottom_up_pull_kernel<uint32_t, 4> : bottom_up_pull_kernel<int64_t, 4>; break;
+                case 8: fb = u32 ? bottom_up_pull_kernel<uint32_t, 8> : bottom_up_pull_kernel<int64_t, 8>; break;
+            }
+            WG_REQUIRE(fb != nullptr, "no bottom-up pull for width %u", g->width);
+            fb<<<grid_for(g->nvec, 256 * 4, 8), 256, 0, s>>>(c, *g, pb, k->apply_increment, k->sentinel);
+            ::wg::count_launch();
+            WG_CHECK_LAUNCH("pull (bottom-up)");
+        }
         if (pb.floor_kernels && !weight && !filter) {
             // floor skipping from FLOOR_KERNELS_FROM on: one atomic-min pass
             // (earlier iterations return at once)
@@ -608,10 +623,15 @@ static PullBufs pull_bufs(const wg_graph *g, const wg_run_bufs *b, const wg_run_
     pb.floor_skip = (p->flags & WG_RUN_FLOOR_SKIP) && p->val_type == WG_VAL_U32 && !p->kern.filter_unvisited ? 1u : 0u;
     {
         const char *e = getenv("WG_FLOOR_KERNELS");
-        pb.floor_kernels = pb.floor_skip && !p->kern.use_weight && !(e && e[0] == '0') ? 1u : 0u;
+        // floor skipping (CC) and bottom-up BFS both switch to a plain kernel
+        pb.floor_kernels = (pb.floor_skip || pb.first_hit) && !p->kern.use_weight && !(e && e[0] == '0') ? 1u : 0u;
         const char *f = getenv("WG_FLOOR_FROM");
         pb.floor_from = f ? (uint32_t)atoi(f) : (uint32_t)FLOOR_KERNELS_FROM;
         if (pb.floor_from < 2) pb.floor_from = 2;  // iteration 1 is pull_ident_kernel's
+        // the plain kernels exist for unweighted floor-skipping and bottom-up
+        // (first-hit, filtered) pulls only
+        const bool plain = pb.floor_kernels && ((pb.floor_skip && !p->kern.filter_unvisited) || pb.first_hit);
+        pb.pipeline_until = plain ? pb.floor_from : ~0ull;
     }
     return pb;
 }

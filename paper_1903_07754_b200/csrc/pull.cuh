@@ -65,6 +65,7 @@ struct PullBufs {
     uint32_t floor_skip; // WG_RUN_FLOOR_SKIP: dense pulls skip destinations already at 0
     uint32_t floor_kernels;  // ... and from iteration floor_from on run floor_pull_kernel
     uint32_t floor_from;
+    uint64_t pipeline_until = ~0ull;  // dense iterations >= this one skip the TMA pipeline (plain kernels)
     int64_t level_base;  // its frontier-0 value
 };
 
@@ -641,6 +642,80 @@ __global__ void __launch_bounds__(256) floor_pull_kernel(LoopCtx c, wg_graph g, 
         atomicAdd((unsigned long long *)&out->vectors_touched, (unsigned long long)g.nvec);
 }
 
+// Bottom-up BFS dense pull from iteration `floor_from` on (WG_RUN_FIRST_HIT,
+// level-synchronous): a thread per vector; a visited destination only lowers
+// nxt[d] to prev[d] from its first vector (the buffer holds older, never
+// smaller values); a vector of an unvisited destination tests its sources'
+// bits in the previous frontier and, on a hit, lowers nxt[d] to the new level.
+// Counts the vectors of unvisited destinations as touched (pulls.pyx:77-80).
+template <typename T, int W>
+__global__ void __launch_bounds__(256) bottom_up_pull_kernel(LoopCtx c, wg_graph g, PullBufs b, int64_t inc,
+                                                             int64_t sentinel) {
+    using VT = ValTraits<T>;
+    const uint64_t it = ctx_iter(c);
+    if (ctx_mode(c, it) != MODE_FULL || it < b.floor_from || it < 2) return;
+    wg_iter_rec *out = ctx_out(c, it);
+    const T *__restrict__ prev = (const T *)(((it - 1) & 1) ? b.vals[1] : b.vals[0]);
+    T *__restrict__ nxt = (T *)((it & 1) ? b.vals[1] : b.vals[0]);
+    uint32_t *__restrict__ obits = ((it & 1) ? b.fbits[1] : b.fbits[0]);
+    const uint32_t *__restrict__ inbits = (((it - 1) & 1) ? b.fbits[1] : b.fbits[0]);
+    const T INF = VT::inf(sentinel);
+    const T level = (T)(b.level_base + (int64_t)(it - 1) * inc);
+    uint32_t ovf = 0;
+    T cand = INF;
+    if constexpr (VT::U32) {
+        const uint64_t cc = (uint64_t)level + (uint64_t)inc;
+        if (cc >= 0xffffffffull) ovf = 1;
+        else cand = (T)cc;
+    } else {
+        cand = level + (T)inc;
+    }
+    constexpr int K = 4;
+    const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+    uint64_t touched = 0;
+    for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; base < g.nvec; base += K * nth) {
+        uint32_t d[K];
+        T pd[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const uint64_t v = base + k * nth;
+            d[k] = v < g.nvec ? g.vdst[v] : NONE;
+        }
+#pragma unroll
+        for (int k = 0; k < K; ++k) pd[k] = d[k] != NONE ? prev[d[k]] : (T)0;
+        bool hit[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const uint64_t v = base + k * nth;
+            hit[k] = false;
+            if (d[k] == NONE) continue;
+            if (pd[k] != INF) {  // visited: only keep prev[d] in this buffer
+                if (v == 0 || g.vdst[v - 1] != d[k]) {
+                    if constexpr (VT::U32) atomicMin((unsigned *)&nxt[d[k]], (unsigned)pd[k]);
+                    else atomicMin((long long *)&nxt[d[k]], (long long)pd[k]);
+                }
+                continue;
+            }
+            ++touched;
+            uint32_t src[W];
+            load_lanes<W>(g.vsrc, v, src);
+#pragma unroll
+            for (int l = 0; l < W; ++l)
+                hit[k] |= src[l] != WG_NO_LANE && ((inbits[src[l] >> 5] >> (src[l] & 31)) & 1u);
+        }
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            if (!hit[k] || cand == INF) continue;
+            if constexpr (VT::U32) atomicMin((unsigned *)&nxt[d[k]], (unsigned)cand);
+            else atomicMin((long long *)&nxt[d[k]], (long long)cand);
+            atomicOr(&obits[d[k] >> 5], 1u << (d[k] & 31));
+        }
+    }
+    if (ovf) out->overflow = 1;
+    const uint64_t t = warp_sum(touched);
+    if (lane_id() == 0 && t) atomicAdd((unsigned long long *)&out->vectors_touched, (unsigned long long)t);
+}
+
 // One dense-pull chunk after its gathers were issued: destinations, segment
 // heads, the raw gathered messages (INF for padding lanes) and prev[d] of
 // segment tails.
@@ -745,7 +820,7 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) pull_dense_tma_kernel(Loop
     uint64_t t0w, t1w;
     warp_range(((uint64_t)nvec + 31) >> 5, gwarp, nwarps, t0w, t1w);
     if (ident) return;  // pull_ident_kernel did this iteration
-    if (floor && b.floor_kernels && it >= b.floor_from) return;  // floor_pull_kernel did
+    if (it >= b.pipeline_until) return;  // floor_pull_kernel / bottom_up_pull_kernel did
     if (t0w < t1w) {
         const uint32_t tfirst = (uint32_t)t0w, tend = (uint32_t)t1w;
         const uint32_t vend = (tend << 5) < nvec ? (tend << 5) : nvec;
