@@ -46,7 +46,7 @@ WORKLOADS = {
                    expect_digest="7d2c2554722fbf74"),
     # expected digests of the full-size configs: the reference's own kernels
     # on the same inputs (tests/golden/full_size.json)
-    "sssp_grid": dict(app="sssp", grid=(4096, 4096), vpg=4, thr="0.2",
+    "sssp_grid": dict(app="sssp", grid=(4096, 4096), vpg=4, thr="0.2", iterations=8627, ref_iteration_cap=64,
                       desc="SSSP on 4096x4096 grid, p=0.9, w in [1,1000] (BASELINE configs[2])",
                       expect_digest="3895390ac91e5500"),
     "bfs26": dict(app="bfs", scale=26, ef=16, sym=False, vpg=8, thr="0.01", weights=None,
@@ -60,6 +60,15 @@ WORKLOADS = {
 }
 GRID_SEED = 2
 METRIC = "GTEPS"
+DATA_DESC = "synthetic (seeded RMAT on the reference's PCG64 stream / fixed-seed grid)"
+L2_NOTE = "inputs larger than L2 + 256 MB L2 flush between timed steps"
+
+
+def workload_config(wl, n, E):
+    """The `config` object, identical in both arms (static workload keys only;
+    run-specific figures go to `run`)."""
+    return {"workload": wl["desc"], "app": wl["app"], "V": int(n), "E": int(E), "W": 4,
+            "vpg": wl.get("vpg"), "threshold": wl.get("thr"), "l2": L2_NOTE}
 
 
 def rle_modes(recs) -> str:
@@ -302,11 +311,10 @@ def run_b200(args, wl):
         "metric": METRIC, "value": round(gteps, 4), "unit": "GTEPS (|E|/time-to-solution)",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
-        "data": "synthetic (device RMAT, reference PCG64 stream)",
-        "config": {"workload": wl["desc"], "app": app, "V": n, "E": E, "W": 4, "vpg": wl["vpg"],
-                   "threshold": wl["thr"], "iterations": iters, "modes": modes, "parallelism": "1 GPU",
-                   "l2": "inputs larger than L2 + 256 MB flush between steps",
-                   "build_s": round(build_s, 2), "tts_ms": round(ms, 4)},
+        "data": DATA_DESC,
+        "config": workload_config(wl, n, E),
+        "run": {"iterations": iters, "modes": modes, "parallelism": "1 GPU", "build_s": round(build_s, 2),
+                "tts_ms": round(ms, 4)},
         "parity": {"digest": digest, "expected": wl.get("expect_digest"),
                    "ok": (digest == wl["expect_digest"]) if wl.get("expect_digest") else cert["ok"],
                    "certificate": cert},
@@ -323,8 +331,7 @@ def run_b200(args, wl):
     if rank == 0 and not args.no_e2e:
         out["e2e"] = e2e_b200(args, wl, g, loop, dinit, words, kern, thr, max_it, fh, lvl, ident)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline(wl, g, prog, thr, max_it, sample_runs=1,
-                                           gpu_active=[r.active_edges for r in recs])
+        out["cpu_baseline"] = cpu_baseline(wl, args)
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:
@@ -696,46 +703,29 @@ def host_reference_layout(g):
     return topo, idx, g.outdeg_np()
 
 
-def cpu_baseline(wl, g, prog, thr, max_it, sample_runs=1, kind=None, threads=None, gpu_active=None,
-                 max_sample_iters=64):
-    """The reference CPU path on this host: the reference's own compiled
-    kernels (oracle/_ref, built from /root/reference by oracle/Makefile) in
-    the reference driver restated (oracle.run_until_convergence), all host
-    threads; falls back to the C restatement ("port") when _ref is absent.
-    Runs with more than max_sample_iters iterations (the grid: ~8.6K) are
-    sampled: the first max_sample_iters iterations are timed and scaled by the
-    iteration count (the reference's per-iteration cost there is dominated by
-    O(V) frontier/buffer work, not by the edges)."""
-    import oracle
-    threads = threads or os.cpu_count() or 1
-    topo, idx, deg = host_reference_layout(g)
-    if oracle.ref_kernels() is not None:
-        be, kind = oracle.RefBackend(threads), "reference"
-    else:
-        be, kind = oracle.PortBackend(threads), "port"
-    init = np.asarray(prog.initial_values(g.n), dtype=np.int64)
-    front = np.arange(g.n) if wl["app"] == "cc" else np.array([0])
-    kern = oracle.kern_of(wl["app"])
-    times = []
-    out = None
-    sampled = gpu_active is not None and len(gpu_active) > max_sample_iters
-    cap = max_sample_iters if sampled else max_it
-    for _ in range(sample_runs):
-        t0 = time.perf_counter()
-        out = oracle.run_until_convergence(topo, idx, deg, kern, init, front, thr, wl["vpg"], cap,
-                                           backend=be)
-        times.append(time.perf_counter() - t0)
-    t = min(times)
-    if sampled:
-        t_full = t * len(gpu_active) / cap
-        sample = (f"first {cap} of {len(gpu_active)} iterations timed ({t:.2f} s), scaled by the iteration "
-                  f"count to a full-run estimate")
-    else:
-        t_full = t
-        sample = (f"{sample_runs} full run(s) of the same workload (E={g.edges}), {len(out.stats)} iterations, "
-                  f"digest {oracle.result_digest(out.values)}")
-    return {"value": round(g.edges / t_full / 1e9, 6), "unit": "GTEPS (|E|/time-to-solution)",
-            "cores": threads, "kind": kind, "seconds_per_run": round(t_full, 3), "sample": sample}
+def cpu_baseline(wl, args):
+    """The reference CPU path on this host, beside the GPU number: the
+    reference arm (`--impl reference`: the stock reference driver and its
+    compiled kernels from baseline/_ref, every host core, plus the workers=1
+    best-of-3 figure) run in a child process -- so the reference never shares
+    a process with the product library -- on a bounded sample of the same
+    workload (2 timed runs after 1 warm-up)."""
+    cmd = [sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--workload", args.workload,
+           "--steps", "2", "--warmup", "1"]
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env)
+        line = [ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1]
+        d = json.loads(line)
+    except Exception as e:  # reported, never fatal to the GPU line
+        return {"value": None, "unavailable": f"reference arm failed: {e!r}"}
+    if "unavailable" in d:
+        return {"value": None, "unavailable": d["unavailable"]}
+    cb = dict(d["cpu_baseline"])
+    cb["ms_per_step"] = d["ms_per_step"]
+    if "parity" in d:
+        cb["digest"] = d["parity"].get("digest")
+    return cb
 
 
 def run_pagerank(args, wl, el, topo, build_s):
@@ -855,82 +845,172 @@ def cpu_baseline_pagerank(g, ranks=None):
     return out, parity
 
 
+def import_reference():
+    """The UNMODIFIED reference package installed in baseline/_ref
+    (baseline/install_ref.sh), never the product package."""
+    ref_dir = ROOT / "baseline" / "_ref"
+    if not (ref_dir / "wedgegraph" / "__init__.py").exists():
+        return None, "baseline/_ref not installed (baseline/install_ref.sh)"
+    sys.path.insert(0, str(ref_dir))
+    import wedgegraph
+    import wedgegraph.kernels as rk
+    if not str(Path(wedgegraph.__file__).resolve()).startswith(str(ref_dir.resolve())):
+        return None, f"wedgegraph resolved outside baseline/_ref: {wedgegraph.__file__}"
+    if "native" not in rk.available_backends():
+        return None, "reference native (Cython) backend not built in baseline/_ref"
+    return wedgegraph, None
+
+
+def prepare_reference_input(wl):
+    """Seeded input of the workload in the reference layout (int64 host
+    arrays), prepared with the oracle's restated generators / builders (the
+    reference's own take minutes at s22; equality with them is pinned by
+    tests/test_oracle.py).  Returns (n, E, topology_arrays, index_arrays, degrees)."""
+    import oracle
+    if "grid" in wl:
+        n, s, d, w = oracle.grid_edges(wl["grid"][0], wl["grid"][1], GRID_SEED)
+    else:
+        n, s, d = oracle.rmat_edges_fast(wl["scale"], wl["ef"], 1)
+        s, d = oracle.prepare_unweighted(n, s, d, wl["sym"])
+        w = oracle.synthesize_weights(s, d, wl["weights"]) if wl.get("weights") else None
+    tp = oracle.build_pull_topology(n, s, d, w, 4)
+    idx = oracle.build_edge_index(tp)
+    deg = oracle.compute_out_degrees(n, s)
+    return n, len(s), tp, idx, deg, (s, d)
+
+
 def run_reference(args, wl):
-    """--impl reference: the reference's CPU implementation on the host cores."""
+    """--impl reference: the reference's own CPU implementation of the path --
+    the stock driver wedgegraph.run_until_convergence (engine.py:330-388) over
+    its compiled native backend (kernels.py:72-125, _kernels.pyx) from
+    baseline/_ref, workers = every host core -- on the same workload, config,
+    metric and unit as the b200 arm.  Never imports the product package.
+    Under torchrun only rank 0 runs."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import oracle
     threads = os.cpu_count() or 1
-    # input preparation (not timed): the graph on the GPU when present, else the oracle
-    try:
-        import torch
-        have_gpu = torch.cuda.is_available()
-    except Exception:
-        have_gpu = False
-    if have_gpu:
-        import paper_1903_07754_b200 as wg
-        el, topo = make_graph(wl)
-        g = topo.device
-        tp, idx, deg = host_reference_layout(g)
-        n, E = g.n, g.edges
-    else:
-        if "grid" in wl:
-            n, s, d, w = oracle.grid_edges(wl["grid"][0], wl["grid"][1], GRID_SEED)
-        else:
-            n, s, d = oracle.rmat_edges(wl["scale"], wl["ef"], 1)
-            keep = s != d
-            if wl["sym"]:
-                s, d, _ = oracle.symmetrize(s[keep], d[keep], None, dedup=True)
-            else:
-                s, d = oracle.dedup_directed(s[keep], d[keep])
-            w = oracle.synthesize_weights(s, d, wl["weights"]) if wl.get("weights") else None
-        tp = oracle.build_pull_topology(n, s, d, w, 4)
-        idx = oracle.build_edge_index(tp)
-        deg = oracle.compute_out_degrees(n, s)
-        E = len(s)
     if wl["app"] == "pr":
-        t0 = time.perf_counter()
-        oracle.pagerank(tp, deg, 20, 0.85, threads)
-        t = time.perf_counter() - t0
-        val = 20 * E / t / 1e9
-        print(json.dumps({"impl": "reference", "metric": METRIC, "value": round(val, 5),
-                          "unit": "GTEPS (20*|E|/time, PageRank)", "n_gpus": 1, "steps": 1, "warmup": 0,
-                          "higher_is_better": True, "cpu_baseline": {"value": round(val, 5), "cores": threads,
-                          "kind": "port", "sample": "1 run of 20 iterations (no reference PR exists)"},
-                          "e2e": {"value": round(val, 5), "unit": "GTEPS", "h2d_bytes_per_step": 0,
-                                  "d2h_bytes_per_step": 0}, "config": {"workload": wl["desc"]}}))
+        return run_reference_pagerank(args, wl, threads)
+    ref, why = import_reference()
+    if ref is None:
+        print(json.dumps({"impl": "reference", "unavailable": why}), flush=True)
         return
-    if oracle.ref_kernels() is not None:
-        be, kind = oracle.RefBackend(threads), "reference"
-    else:
-        be, kind = oracle.PortBackend(threads), "port"
+    t0 = time.perf_counter()
+    n, E, tp, idx, deg, _ = prepare_reference_input(wl)
+    prep_s = time.perf_counter() - t0
+    topo = ref.PullTopology(n, 4, E, tp.vec_dst, tp.lane_src, tp.lane_weight, tp.lane_count)
+    index = ref.EdgeIndex(n, tp.vector_count, idx.offsets, idx.positions)
     app = wl["app"]
-    init, front = oracle.initial_state(app, n, 0)
-    kern = oracle.kern_of(app)
-    thr = Fraction(wl["thr"])
-    ts = []
-    out = None
-    for i in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        out = oracle.run_until_convergence(tp, idx, deg, kern, init, front, thr, wl["vpg"], n + 16,
-                                           backend=be)
-        dt = time.perf_counter() - t0
-        if i >= args.warmup:
-            ts.append(dt)
-    ms = float(np.mean(ts)) * 1e3
+    prog = ref.make_program(app, None if app == "cc" else 0)
+    # a bounded sample per step: runs longer than the cap (grid SSSP, ~8.6K
+    # iterations at ~0.1 s each) time their first `cap` iterations, scaled
+    cap = int(wl.get("ref_iteration_cap", n + 16))
+    full_iters = wl.get("iterations")
+
+    def cfg(workers):
+        return ref.EngineConfig(threshold=ref.FullnessThreshold.of(wl["thr"]),
+                                precision=ref.FrontierPrecision(wl["vpg"]), workers=workers,
+                                max_iterations=cap)
+
+    def timed(workers, k):
+        ts, res = [], None
+        for _ in range(k):
+            a = time.perf_counter()
+            res = ref.run_until_convergence(topo, index, prog, deg, cfg(workers), backend="native")
+            ts.append(time.perf_counter() - a)
+        return ts, res
+
+    # warm-up + the timed steps on every host core (the reference's CLI
+    # reads WEDGE_WORKERS, cli.py:149-153)
+    for _ in range(args.warmup):
+        timed(threads, 1)
+    ts, res = timed(threads, args.steps)
+    iters = len(res.stats)
+    scale = (full_iters / iters) if (full_iters and iters < full_iters) else 1.0
+    ms = float(np.mean(ts)) * 1e3 * scale
+    best_ms = float(np.min(ts)) * 1e3 * scale
+    # BASELINE.md protocol: also one worker, warm best-of-3
+    one = None
+    if not args.no_single_worker:
+        t1, _ = timed(1, 3)
+        one = {"workers": 1, "best_of_3_ms": round(min(t1) * 1e3 * scale, 3),
+               "value": round(E / (min(t1) * scale) / 1e9, 6)}
     val = E / (ms * 1e-3) / 1e9
-    print(json.dumps({
-        "impl": "reference", "metric": METRIC, "value": round(val, 5),
+    digest = ref.result_digest(res.values)
+    sample = (f"each step = 1 full run of the stock reference driver to convergence ({iters} iterations, "
+              f"workers={threads})") if scale == 1.0 else (
+              f"each step = the first {iters} of {full_iters} iterations of the stock reference driver "
+              f"(workers={threads}), scaled by the iteration count")
+    out = {
+        "impl": "reference", "metric": METRIC, "value": round(val, 6),
         "unit": "GTEPS (|E|/time-to-solution)", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-        "config": {"workload": wl["desc"], "V": n, "E": E, "iterations": len(out.stats)},
-        "parity": {"digest": oracle.result_digest(out.values), "expected": wl.get("expect_digest")},
-        "cpu_baseline": {"value": round(val, 5), "unit": "GTEPS", "cores": threads, "kind": kind,
-                         "sample": f"each step = 1 full run to convergence ({len(out.stats)} iterations)"},
-        "e2e": {"value": round(val, 5), "unit": "GTEPS (|E|/time-to-solution)", "h2d_bytes_per_step": 0,
+        "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": DATA_DESC,
+        "config": workload_config(wl, n, E),
+        "parity": {"digest": digest, "expected": wl.get("expect_digest"),
+                   "ok": digest == wl.get("expect_digest") if scale == 1.0 else None,
+                   "trace": rle_modes(res.stats), "iterations": iters},
+        "cpu_baseline": {"value": round(val, 6), "unit": "GTEPS (|E|/time-to-solution)", "cores": threads,
+                         "kind": "reference", "sample": sample, "best_ms": round(best_ms, 3),
+                         "single_worker": one, "host": host_cpu()},
+        "e2e": {"value": round(val, 6), "unit": "GTEPS (|E|/time-to-solution)", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "reference": {"package": "wedgegraph " + getattr(ref, "__version__", "?"),
+                      "path": str(Path(ref.__file__).resolve().parent.relative_to(ROOT)),
+                      "driver": "wedgegraph.run_until_convergence (engine.py:330-388)",
+                      "backend": "native (compiled _kernels.pyx)", "input_prep_s": round(prep_s, 1),
+                      "input_prep": "oracle restated generators/builders (untimed)"},
+        "loaded_so": loaded_native_libs(),
+    }
+    print(json.dumps(out), flush=True)
+
+
+def run_reference_pagerank(args, wl, threads):
+    """PageRank has no reference implementation (the reference
+    rejects it, test_apps.py:167-169): the arm times the float64 C port of the
+    a17 semantics on every host core (kind "port")."""
+    import oracle
+    n, E, tp, _, deg, _ = prepare_reference_input(wl)
+    ts = []
+    for i in range(args.warmup + args.steps):
+        a = time.perf_counter()
+        oracle.pagerank(tp, deg, 20, 0.85, threads)
+        if i >= args.warmup:
+            ts.append(time.perf_counter() - a)
+    t = float(np.mean(ts))
+    val = 20 * E / t / 1e9
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(val, 6), "unit": "GTEPS (20*|E|/time, PageRank)",
+        "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": DATA_DESC, "config": workload_config(wl, n, E),
+        "cpu_baseline": {"value": round(val, 6), "unit": "GTEPS (20*|E|/time, PageRank)", "cores": threads,
+                         "kind": "port", "sample": "each step = 20 iterations (no reference PR exists)",
+                         "host": host_cpu()},
+        "e2e": {"value": round(val, 6), "unit": "GTEPS (20*|E|/time, PageRank)", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0}}), flush=True)
+
+
+def loaded_native_libs():
+    """Shared objects under the repo mapped into this process."""
+    try:
+        maps = Path("/proc/self/maps").read_text().splitlines()
+    except Exception:
+        return None
+    root = str(ROOT.resolve())
+    return sorted({ln.split()[-1][len(root) + 1:] for ln in maps
+                   if ln.split()[-1].startswith(root) and ".so" in ln.split()[-1]})
+
+
+def host_cpu() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return f"{line.split(':', 1)[1].strip()} x{os.cpu_count()}"
+    except Exception:
+        pass
+    return f"x{os.cpu_count()}"
 
 
 def main():
@@ -943,6 +1023,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sharded", action="store_true", help="use the multi-GPU sharded path even at N=1")
+    ap.add_argument("--no-single-worker", action="store_true",
+                    help="reference arm: skip the workers=1 best-of-3 figure")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
     wl = WORKLOADS[args.workload]

@@ -86,6 +86,11 @@ def lib():
         L.orc_pagerank.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _i64p, _i64p,
                                    _i64p, _i64p, ctypes.c_int, ctypes.c_double, _f64p, ctypes.c_int]
         L.orc_max_threads.restype = ctypes.c_int
+        L.orc_rmat.restype = None
+        L.orc_rmat.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_uint64, ctypes.c_uint64,
+                               ctypes.c_uint64, ctypes.c_uint64, _f64p, _i64p, _i64p]
+        L.orc_sort_unique_u64.restype = ctypes.c_int64
+        L.orc_sort_unique_u64.argtypes = [_u64p, ctypes.c_int64, ctypes.c_int]
         _LIB = L
     return _LIB
 
@@ -508,6 +513,44 @@ def rmat_edges(scale: int, edge_factor: int, seed: int = 1, probs=RMAT_PROBS, ch
             d |= (q[:, level] & 1) << sh
         src[lo:hi], dst[lo:hi] = s, d
     return n, src, dst
+
+
+def rmat_edges_fast(scale: int, edge_factor: int, seed: int = 1, probs=RMAT_PROBS):
+    """rmat_edges in threaded C (orc_rmat): the same PCG64 stream jumped ahead
+    per row chunk; identical output (tests/test_oracle.py)."""
+    n = 1 << scale
+    m = edge_factor * n
+    st = np.random.PCG64(seed).state["state"]
+    state, inc = int(st["state"]), int(st["inc"])
+    a, b, c, _ = probs
+    th = np.array([a, a + b, a + b + c], np.float64)
+    src = np.empty(m, np.int64)
+    dst = np.empty(m, np.int64)
+    M = (1 << 64) - 1
+    lib().orc_rmat(scale, m, state >> 64, state & M, inc >> 64, inc & M, _p(th, _f64p),
+                   _p(src, _i64p), _p(dst, _i64p))
+    return n, src, dst
+
+
+def _sorted_unique_pairs(src, dst, n):
+    bits = max(1, int(n - 1).bit_length()) if n > 1 else 1
+    key = (np.asarray(src, np.int64).astype(np.uint64) << np.uint64(bits)) | np.asarray(dst, np.int64).astype(np.uint64)
+    k = int(lib().orc_sort_unique_u64(_p(key, _u64p), key.size, 2 * bits))
+    key = key[:k]
+    return (key >> np.uint64(bits)).astype(np.int64), (key & np.uint64((1 << bits) - 1)).astype(np.int64)
+
+
+def prepare_unweighted(n, src, dst, symmetric: bool):
+    """Drop self-loops, then symmetrize(dedup=True) (graph_io.py:87-112) or
+    de-duplicate directed edges; (src, dst)-sorted like oracle.symmetrize /
+    dedup_directed, computed with the threaded radix sort."""
+    src = np.asarray(src, np.int64)
+    dst = np.asarray(dst, np.int64)
+    keep = src != dst
+    s, d = src[keep], dst[keep]
+    if symmetric:
+        s, d = np.concatenate([s, d]), np.concatenate([d, s])
+    return _sorted_unique_pairs(s, d, n)
 
 
 def symmetrize(src, dst, weight=None, dedup=False):

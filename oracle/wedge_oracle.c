@@ -346,6 +346,109 @@ void orc_pagerank(int64_t n, int64_t nvec, int64_t width, const int64_t *vec_dst
     free(acc);
 }
 
+/* ------------------------------------------------------------------------ */
+/* Input preparation for the CPU arms (graph_io.py:87-112, 188-202),        */
+/* multi-threaded so the --impl reference leg prepares a 128M-edge input in */
+/* seconds instead of the reference generators' minutes.  Same outputs as  */
+/* the numpy restatements in oracle/__init__.py (tests/test_oracle.py).     */
+/* ------------------------------------------------------------------------ */
+typedef unsigned __int128 u128_t;
+
+/* numpy PCG64: 128-bit LCG, XSL-RR output taken after the step; random()
+ * = (next >> 11) * 2^-53 */
+static inline uint64_t pcg_xslrr(u128_t st) {
+    uint64_t x = (uint64_t)(st >> 64) ^ (uint64_t)st;
+    unsigned rot = (unsigned)(st >> 122);
+    return (x >> rot) | (x << ((64u - rot) & 63u));
+}
+
+static u128_t pcg_jump(u128_t state, u128_t inc, u128_t mult, uint64_t delta) {
+    u128_t am = 1, ap = 0, cm = mult, cp = inc;
+    while (delta) {
+        if (delta & 1u) {
+            am *= cm;
+            ap = ap * cm + cp;
+        }
+        cp = (cm + 1) * cp;
+        cm *= cm;
+        delta >>= 1;
+    }
+    return am * state + ap;
+}
+
+/* R-MAT rows [0, m): row r uses draws r*scale .. r*scale+scale-1 of the
+ * stream; quadrant q = [u>=t0]+[u>=t1]+[u>=t2], src bit q>>1, dst bit q&1,
+ * most significant level first (graph_io.py:195-201). */
+void orc_rmat(int scale, int64_t m, uint64_t shi, uint64_t slo, uint64_t ihi, uint64_t ilo,
+              const double *th, int64_t *src, int64_t *dst) {
+    const u128_t mult = ((u128_t)0x2360ED051FC65DA4ull << 64) | 0x4385DF649FCCF645ull;
+    const u128_t st0 = ((u128_t)shi << 64) | slo, inc = ((u128_t)ihi << 64) | ilo;
+    const int64_t chunk = 1 << 16;
+    #pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t lo = 0; lo < m; lo += chunk) {
+        int64_t hi = lo + chunk < m ? lo + chunk : m;
+        u128_t st = pcg_jump(st0, inc, mult, (uint64_t)lo * (uint64_t)scale);
+        for (int64_t r = lo; r < hi; ++r) {
+            int64_t s = 0, d = 0;
+            for (int l = 0; l < scale; ++l) {
+                st = st * mult + inc;
+                double u = (double)(pcg_xslrr(st) >> 11) * (1.0 / 9007199254740992.0);
+                int q = (u >= th[0]) + (u >= th[1]) + (u >= th[2]);
+                int sh = scale - 1 - l;
+                s |= (int64_t)(q >> 1) << sh;
+                d |= (int64_t)(q & 1) << sh;
+            }
+            src[r] = s;
+            dst[r] = d;
+        }
+    }
+}
+
+/* Sort 64-bit keys ascending (LSD radix, 8-bit digits, threaded) and drop
+ * duplicates; `bits` = significant key bits.  Returns the unique count. */
+int64_t orc_sort_unique_u64(uint64_t *keys, int64_t m, int bits) {
+    if (m <= 0) return 0;
+    uint64_t *tmp = (uint64_t *)malloc((size_t)m * sizeof(uint64_t));
+    uint64_t *a = keys, *b = tmp;
+    int T = 1;
+#ifdef _OPENMP
+    T = omp_get_max_threads();
+#endif
+    int64_t *hist = (int64_t *)calloc((size_t)T * 256, sizeof(int64_t));
+    for (int shift = 0; shift < bits; shift += 8) {
+        memset(hist, 0, (size_t)T * 256 * sizeof(int64_t));
+        #pragma omp parallel num_threads(T)
+        {
+            int t = 0;
+#ifdef _OPENMP
+            t = omp_get_thread_num();
+#endif
+            int64_t lo = m * t / T, hi = m * (t + 1) / T;
+            int64_t *h = hist + (size_t)t * 256;
+            for (int64_t i = lo; i < hi; ++i) h[(a[i] >> shift) & 255]++;
+            #pragma omp barrier
+            #pragma omp single
+            {
+                int64_t run = 0;
+                for (int dgt = 0; dgt < 256; ++dgt)
+                    for (int u = 0; u < T; ++u) {
+                        int64_t c = hist[(size_t)u * 256 + dgt];
+                        hist[(size_t)u * 256 + dgt] = run;
+                        run += c;
+                    }
+            }
+            for (int64_t i = lo; i < hi; ++i) b[h[(a[i] >> shift) & 255]++] = a[i];
+        }
+        uint64_t *x = a; a = b; b = x;
+    }
+    int64_t k = 0;
+    for (int64_t i = 0; i < m; ++i)
+        if (i == 0 || a[i] != a[i - 1]) keys[k++] = a[i];
+    free(hist);
+    free(tmp);
+    return k;
+}
+
 int orc_max_threads(void) {
 #ifdef _OPENMP
     return omp_get_max_threads();

@@ -31,16 +31,24 @@ from . import device as _dev
 
 class _UploadCache:
     """Device copies of reference-layout host structures, keyed by object
-    identity and dropped when the host object dies."""
+    identity and dropped when the host object dies (objects without weak
+    references -- the reference's __slots__ classes -- are held strongly,
+    so the cache keeps at most `capacity` entries, oldest evicted first)."""
 
-    def __init__(self):
+    def __init__(self, capacity: int = 16):
         self._items = {}
+        self.capacity = capacity
+
+    def clear(self):
+        self._items.clear()
 
     def get(self, key_objs, make):
         key = tuple(id(o) for o in key_objs)
         hit = self._items.get(key)
         if hit is not None and all(r() is o for r, o in zip(hit[0], key_objs)):
             return hit[1]
+        while len(self._items) >= self.capacity:
+            self._items.pop(next(iter(self._items)))
         val = make()
         refs = []
         for o in key_objs:

@@ -136,7 +136,7 @@ def stats_signature(stats: Sequence) -> tuple:
 
 
 def _initial_values(program: ApplicationProgram, n: int) -> np.ndarray:
-    if program.initial_values is not None:
+    if getattr(program, "initial_values", None) is not None:
         return np.ascontiguousarray(program.initial_values(n), dtype=np.int64)
     return np.fromiter((program.initial_value(v) for v in range(n)), dtype=np.int64, count=n)
 
