@@ -329,7 +329,9 @@ def run_b200(args, wl):
     clocks = clk.summary()
     out["clocks"] = clocks
     if rank == 0 and not args.no_e2e:
-        out["e2e"] = e2e_b200(args, wl, g, loop, dinit, words, kern, thr, max_it, fh, lvl, ident)
+        out["e2e"] = e2e_api(args, wl, g, prog, values)
+        if args.e2e_compact:
+            out["e2e_compact"] = e2e_b200(args, wl, g, loop, dinit, words, kern, thr, max_it, fh, lvl, ident)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(wl, args)
     if rank == 0:
@@ -571,9 +573,69 @@ def roofline(rows, recs, n, E, weighted, filt, wl, ident_first=False):
             "iterations_timed": len(per_iter)}
 
 
+def e2e_api(args, wl, g, prog, expect_values):
+    """`e2e`: the same metric through the public API call a reference user
+    makes -- ``run_until_convergence(topology, index, program, degrees,
+    config, backend=B200Backend(reupload=True))`` (engine.py:330-388 /
+    kernels.py:137-151) -- on the reference's own host layout: int64
+    PullTopology / EdgeIndex / out-degree arrays (graph.py:109-212) in pinned
+    host memory.  Per step the backend copies every one of those arrays to the
+    device raw (reupload: nothing cached between steps), narrows / validates
+    them there (wg_ingest_*), uploads and scans the initial values, runs the
+    loop and returns int64 values with the reference sentinel in host memory."""
+    import torch
+    import paper_1903_07754_b200 as wg
+
+    def pinned(a):
+        if a is None:
+            return None
+        t = torch.empty(a.shape, dtype=torch.int64, pin_memory=True)
+        t.numpy()[...] = a
+        return t.numpy()
+
+    lane_src, lane_w, lane_count = g.lanes_np()
+    topo = wg.PullTopology(g.n, g.width, g.edges, pinned(g.vec_dst_np()), pinned(lane_src), pinned(lane_w),
+                           pinned(lane_count))
+    idx = wg.EdgeIndex(g.n, g.nvec, pinned(g.offsets_np()), pinned(g.positions_np()))
+    deg = pinned(g.outdeg_np())
+    del lane_src, lane_w, lane_count
+    cfg = wg.EngineConfig(threshold=wg.FullnessThreshold.of(wl["thr"]),
+                          precision=wg.FrontierPrecision(wl["vpg"]), max_iterations=g.n + 16)
+    be = wg.B200Backend(reupload=True)
+    arrays = [topo.vec_dst, topo.lane_src, topo.lane_weight, topo.lane_count, idx.offsets, idx.positions, deg]
+    h2d = sum(a.nbytes for a in arrays if a is not None) + 8 * g.n  # + the int64 initial values
+    d2h = 8 * g.n
+    stream = torch.cuda.current_stream()
+    res = None
+    for _ in range(max(1, args.warmup)):
+        res = wg.run_until_convergence(topo, idx, prog, deg, cfg, backend=be)
+    ok = bool(np.array_equal(res.values, expect_values))
+    ts, walls = [], []
+    for _ in range(args.steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        w0 = time.perf_counter()
+        a.record(stream)
+        res = wg.run_until_convergence(topo, idx, prog, deg, cfg, backend=be)
+        b.record(stream)
+        b.synchronize()
+        walls.append(time.perf_counter() - w0)
+        ts.append(a.elapsed_time(b))
+    ms = float(np.mean(ts))
+    ok = ok and bool(np.array_equal(res.values, expect_values))
+    return {"value": round(g.edges / (ms * 1e-3) / 1e9, 4), "unit": "GTEPS (|E|/time-to-solution)",
+            "ms_per_step": round(ms, 3), "wall_ms_per_step": round(1e3 * float(np.mean(walls)), 3),
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "result_equal": ok,
+            "device_loop_ms": round(float(res.device_ms), 4),
+            "path": "wg.run_until_convergence(PullTopology(int64 host arrays), EdgeIndex(int64), program, "
+                    "int64 degrees, EngineConfig, backend=B200Backend(reupload=True)): per step H2D of every "
+                    "reference-layout array + initial values (pinned host memory, chunked behind the copy "
+                    "engine), device narrowing/validation (wg_ingest_*, wg_values_scan), device loop, D2H of "
+                    "int64 values"}
+
+
 def e2e_b200(args, wl, g, loop, dinit, words, kern, thr, max_it, first_hit=False, level_base=0,
              identity_init=False):
-    """Same metric through the C ABI with the graph in pinned HOST memory.
+    """`e2e_compact` (--e2e-compact): the loop through the C ABI with the graph in pinned HOST memory.
     Per step: H2D of the topology in its compact form -- the lane sources
     delta-coded per vector (wg_encode_lanes, ~15 bits per lane at s22), the
     per-destination vector offsets voff, weights as bytes when <= 255, and the
@@ -1021,6 +1083,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=("b200", "reference"))
     ap.add_argument("--workload", default="cc22", choices=sorted(WORKLOADS))
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-compact", action="store_true",
+                    help="also time the compact delta-coded upload format (encode time reported, untimed)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sharded", action="store_true", help="use the multi-GPU sharded path even at N=1")
     ap.add_argument("--no-single-worker", action="store_true",

@@ -457,6 +457,46 @@ int wg_grid_edges(uint32_t rows, uint32_t cols, uint64_t seed, uint32_t keep_per
                   uint32_t max_weight, uint32_t *d_src, uint32_t *d_dst, uint32_t *d_w,
                   uint64_t *d_counter, uint64_t *h_m_out, void *stream);
 
+/* ---------------------------------------------------------------------- */
+/* Ingest of the plugin call's reference-layout host arrays (ingest.cu).   */
+/* The backend copies the caller's int64 arrays to the device raw, chunk by */
+/* chunk, and narrows/validates each chunk here (B200Backend, backend.py):  */
+/*   PullTopology vec_dst / lane_count / lane_src / lane_weight  graph.py:109-164 */
+/*   EdgeIndex offsets / positions                            graph.py:190-212 */
+/*   out-degrees (compute_out_degrees)                        graph.py:277-280 */
+/*   initial values (ValueBuffers.initialize)                 engine.py:90-116 */
+/* Violations OR bits into *d_err (read once by the caller).                */
+/* ---------------------------------------------------------------------- */
+#define WG_INGEST_BAD_DST 1u      /* vec_dst outside [0, n) */
+#define WG_INGEST_BAD_SRC 2u      /* a valid lane's source outside [0, n) */
+#define WG_INGEST_BAD_COUNT 4u    /* lane_count outside [0, width] */
+#define WG_INGEST_BAD_WEIGHT 8u   /* a valid lane's weight outside [0, 2^32) */
+#define WG_INGEST_BAD_POS 16u     /* an index position outside [0, nvec) */
+#define WG_INGEST_BAD_DEGREE 32u  /* an out-degree outside [0, 2^32) */
+#define WG_INGEST_BAD_OFFSETS 64u /* offsets not monotone / not [0 .. entries] */
+#define WG_INGEST_LENS_DIFFER 128u /* some index length differs from the out-degree (informational) */
+
+/* count vectors: vdst[p] = vec_dst[p], vsrc[p*W+k] = lane_src[p*W+k] for k <
+ * lane_count[p] else WG_NO_LANE, vw likewise (0 in padding); pointers are the
+ * chunk's (already offset) device arrays. */
+int wg_ingest_vectors(uint64_t count, uint32_t width, uint32_t n, const int64_t *d_vec_dst,
+                      const int64_t *d_lane_count, const int64_t *d_lane_src, const int64_t *d_lane_w,
+                      uint32_t *d_vdst, uint32_t *d_vsrc, uint32_t *d_vw, uint32_t *d_err, void *stream);
+/* out[i] = in[i] as uint32; `flag` set in *d_err when in[i] is outside [0, limit). */
+int wg_ingest_u32(uint64_t count, const int64_t *d_in, int64_t limit, uint32_t *d_out, uint32_t flag,
+                  uint32_t *d_err, void *stream);
+/* validate the CSR offsets (0 .. entries, monotone); WG_INGEST_LENS_DIFFER
+ * when d_outdeg is given and some offsets[v+1]-offsets[v] != outdeg[v]. */
+int wg_ingest_offsets(uint32_t n, const uint64_t *d_idx_off, uint64_t entries, const uint32_t *d_outdeg,
+                      uint32_t *d_err, void *stream);
+
+#define WG_VALUES_NOT_U32 1u      /* some finite value outside [0, 0xFFFFFFFF) */
+#define WG_VALUES_NOT_IDENTITY 2u /* init[v] != v for some v */
+/* d_enc[v] = uint32 encoding (sentinel -> 0xFFFFFFFF); d_stats4 = {flags,
+ * finite count, min finite, max finite (int64 bits)}. */
+int wg_values_scan(uint32_t n, const int64_t *d_init, int64_t sentinel, uint32_t *d_enc, uint64_t *d_stats4,
+                   void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -17,7 +17,7 @@ CSRC = PKG / "csrc"
 OUT = PKG / "libwedge_b200.so"
 BUILD = ROOT / "build" / "wedge_b200"
 
-SOURCES = ["capi.cu", "engine.cu", "layout.cu", "pagerank.cu", "codec.cu"]
+SOURCES = ["capi.cu", "engine.cu", "layout.cu", "pagerank.cu", "codec.cu", "ingest.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",

@@ -59,6 +59,9 @@ WG_RUN_KEEP_LISTS = 2
 WG_RUN_IDENTITY_INIT = 8
 WG_RUN_FLOOR_SKIP = 16
 WG_CODED_BLOCK_VECTORS = 1024
+WG_INGEST_BAD_DST, WG_INGEST_BAD_SRC, WG_INGEST_BAD_COUNT, WG_INGEST_BAD_WEIGHT = 1, 2, 4, 8
+WG_INGEST_BAD_POS, WG_INGEST_BAD_DEGREE, WG_INGEST_BAD_OFFSETS, WG_INGEST_LENS_DIFFER = 16, 32, 64, 128
+WG_VALUES_NOT_U32, WG_VALUES_NOT_IDENTITY = 1, 2
 
 
 EXPORTS = [
@@ -78,6 +81,7 @@ EXPORTS = [
     "wg_vector_offsets_scratch_bytes", "wg_vector_offsets", "wg_coded_scratch_bytes", "wg_encode_lanes",
     "wg_decode_lanes", "wg_index_chunk_coded", "wg_expand_scratch_bytes", "wg_index_placed_scratch_bytes",
     "wg_index_place_begin", "wg_index_place_chunk", "wg_index_place_coded", "wg_index_place_end",
+    "wg_ingest_vectors", "wg_ingest_u32", "wg_ingest_offsets", "wg_values_scan",
 ]
 
 _LIB = None
@@ -190,6 +194,11 @@ def load(path: os.PathLike | str | None = None):
         "wg_index_finish": (ctypes.c_int, [G, c_u64, c_vp, c_vp, c_vp, c_vp, ctypes.c_size_t, u64p, c_vp]),
         "wg_exchange_pack_all": (ctypes.c_int, [G, B, P, c_u64, c_vp, c_u64, c_vp]),
         "wg_exchange_apply_all": (ctypes.c_int, [G, B, P, c_u64, c_vp, c_u32, c_u64, c_vp, c_vp]),
+        "wg_ingest_vectors": (ctypes.c_int, [c_u64, c_u32, c_u32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                             c_vp, c_vp]),
+        "wg_ingest_u32": (ctypes.c_int, [c_u64, c_vp, c_i64, c_vp, c_u32, c_vp, c_vp]),
+        "wg_ingest_offsets": (ctypes.c_int, [c_u32, c_vp, c_u64, c_vp, c_vp, c_vp]),
+        "wg_values_scan": (ctypes.c_int, [c_u32, c_vp, c_i64, c_vp, c_vp, c_vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

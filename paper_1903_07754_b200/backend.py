@@ -66,8 +66,13 @@ class B200Backend:
     # (one iteration per launch) instead of one whole-loop graph launch
     per_iteration_timing = False
 
-    def __init__(self):
+    def __init__(self, reupload: bool = False):
+        """reupload: re-read the caller's host arrays on every call (into the
+        cached device buffers) instead of trusting an upload made earlier for
+        the same objects -- for callers that mutate arrays in place, and the
+        end-to-end measurement of the plugin call (bench.py e2e)."""
         self._cache = _UploadCache()
+        self.reupload = bool(reupload)
 
     # -- device graph resolution -------------------------------------------
     def device_graph(self, topology, index=None, degrees=None) -> _dev.DeviceGraph:
@@ -78,11 +83,17 @@ class B200Backend:
         # are only needed by the loop and the transform
         def make():
             if index is not None:
-                return _dev.DeviceGraph.from_reference(topology, index, degrees)
+                g = _dev.DeviceGraph.from_reference(topology, index, degrees)
+                g._fresh = True  # uploaded by this very call
+                return g
             return _dev.DeviceGraph.from_reference(topology, _EmptyIndex(topology.vertex_count),
                                                    np.zeros(topology.vertex_count, np.int64))
         keys = [topology] + ([index] if index is not None else [])
-        return self._cache.get(keys, make)
+        g = self._cache.get(keys, make)
+        if self.reupload and getattr(g, "_fresh", False) is False and index is not None:
+            g = _dev.DeviceGraph.from_reference(topology, index, degrees, into=g)
+        g._fresh = False
+        return g
 
     def _index_graph(self, offsets, positions, vertex_count, groups, shift) -> _dev.DeviceGraph:
         g = getattr(offsets, "device", None)

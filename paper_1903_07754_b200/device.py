@@ -63,6 +63,47 @@ def u32_to_np64(t) -> np.ndarray:
     return t.cpu().numpy().view(np.uint32).astype(np.int64)
 
 
+_INGEST_FLAGS = {"vec_dst outside [0, n)": _lib.WG_INGEST_BAD_DST, "lane source outside [0, n)": _lib.WG_INGEST_BAD_SRC,
+                 "lane_count outside [0, W]": _lib.WG_INGEST_BAD_COUNT,
+                 "lane weight outside [0, 2^32)": _lib.WG_INGEST_BAD_WEIGHT,
+                 "index position outside [0, vector_count)": _lib.WG_INGEST_BAD_POS,
+                 "out-degree outside [0, 2^32)": _lib.WG_INGEST_BAD_DEGREE,
+                 "index offsets not monotone from 0 to len(positions)": _lib.WG_INGEST_BAD_OFFSETS}
+
+
+class _IngestStaging:
+    """Two device staging slots (int64 chunks) + a copy stream, shared by
+    every reference-layout upload on a device (DeviceGraph.from_reference)."""
+
+    _cache = {}
+
+    def __init__(self, device, chunk, width, weighted):
+        torch = _torch()
+        self.chunk, self.width, self.weighted = chunk, width, weighted
+        self.copy = torch.cuda.Stream(device=device)
+        self.copy_done = torch.cuda.Event()
+        self.err = torch.zeros(1, dtype=torch.int32, device=device)
+        self.slots = []
+        for _ in range(2):
+            sl = {"dst": torch.empty(chunk, dtype=torch.int64, device=device),
+                  "cnt": torch.empty(chunk, dtype=torch.int64, device=device),
+                  "src": torch.empty(chunk * width, dtype=torch.int64, device=device),
+                  "w": torch.empty(chunk * width, dtype=torch.int64, device=device) if weighted else None,
+                  "ready": torch.cuda.Event(), "free": torch.cuda.Event()}
+            self.slots.append(sl)
+
+    def slot(self, k):
+        return self.slots[k & 1]
+
+    @classmethod
+    def get(cls, device, chunk, width, weighted):
+        key = (str(device), chunk, width)
+        st = cls._cache.get(key)
+        if st is None or (weighted and not st.weighted):
+            st = cls._cache[key] = cls(device, chunk, width, weighted)
+        return st
+
+
 # ---------------------------------------------------------------------------
 # Device graph (SURVEY Appendix B.1)
 # ---------------------------------------------------------------------------
@@ -137,38 +178,120 @@ class DeviceGraph:
         return g
 
     @classmethod
-    def from_reference(cls, topology, index, degrees, device="cuda") -> "DeviceGraph":
+    def from_reference(cls, topology, index, degrees, device="cuda", into=None, stream=None,
+                       chunk_vectors: int = 1 << 22) -> "DeviceGraph":
         """Upload a reference-layout PullTopology / EdgeIndex / degrees
-        (int64 host arrays, graph.py:109-212) into the device layout."""
+        (int64 host arrays, graph.py:109-212) into the device layout.
+
+        The caller's int64 arrays travel raw, in chunks of `chunk_vectors`
+        vectors (index entries / degrees in chunks of as many lanes) through
+        two device staging slots: the copy engine moves chunk k+1 while the
+        compute stream narrows and validates chunk k (wg_ingest_*), so nothing
+        is converted on the host.  `into`: a graph of the same shape whose
+        buffers are refilled (the caller's arrays may have changed in place).
+        Raises ValueError when an id, weight, degree or offset does not fit
+        the layout (a reference kernel would read out of bounds there)."""
         torch = _torch()
+        L = _lib.load()
         n, width = int(topology.vertex_count), int(topology.vector_width)
         if width not in (1, 2, 4, 8):
             raise ValueError(f"vector width {width} is not supported by the B200 engine (1, 2, 4, 8)")
         nvec = int(topology.vector_count)
-        lane_src = np.asarray(topology.lane_src, dtype=np.int64).reshape(nvec, width)
-        valid = np.asarray(topology.lane_count)[:, None] > np.arange(width)[None, :]
-        vs = np.where(valid, lane_src, NO_LANE).astype(np.uint32)
-        vw = None
-        if topology.lane_weight is not None:
-            lw = np.asarray(topology.lane_weight, dtype=np.int64).reshape(nvec, width)
-            if lw.size and (lw.min() < 0 or lw.max() > 0xFFFFFFFF):
-                raise ValueError("lane weights do not fit in uint32")
-            vw = to_dev_u32(np.where(valid, lw, 0).astype(np.uint32).ravel(), device)
-        deg = np.asarray(degrees, dtype=np.int64)
-        if deg.size and deg.max() > 0xFFFFFFFF:
-            raise ValueError("degrees do not fit in uint32")
-        off = torch.from_numpy(np.ascontiguousarray(index.offsets, dtype=np.int64)).to(device)
-        pos = np.asarray(index.positions, dtype=np.int64)
-        if vw is not None:
-            vw = _padded(vw, SLACK * width)
-        return cls(n, width, int(topology.edge_count), nvec, int(pos.size),
-                   _padded(to_dev_u32(vs.ravel() if vs.size else np.zeros(1, np.uint32), device), SLACK * width),
-                   _padded(to_dev_u32(np.asarray(topology.vec_dst, np.int64) if nvec else np.zeros(1, np.int64),
-                                      device), SLACK),
-                   vw, off,
-                   to_dev_u32(pos if pos.size else np.zeros(1, np.int64), device),
-                   to_dev_u32(deg if deg.size else np.zeros(1, np.int64), device),
-                   lens_are_degrees=bool(np.array_equal(np.diff(np.asarray(index.offsets, np.int64)), deg)))
+        i64 = lambda a: np.ascontiguousarray(a, dtype=np.int64)
+        h_dst = i64(topology.vec_dst).reshape(-1)
+        h_cnt = i64(topology.lane_count).reshape(-1)
+        h_src = i64(topology.lane_src).reshape(-1)
+        h_w = None if topology.lane_weight is None else i64(topology.lane_weight).reshape(-1)
+        h_off = i64(index.offsets).reshape(-1)
+        h_pos = i64(index.positions).reshape(-1)
+        h_deg = i64(degrees).reshape(-1)
+        entries = int(h_pos.size)
+        if h_src.size != nvec * width or h_cnt.size != nvec or (h_w is not None and h_w.size != nvec * width):
+            raise ValueError("lane arrays do not match vector_count x vector_width")
+        if h_off.size != n + 1 or h_deg.size != n:
+            raise ValueError("index offsets / degrees do not match vertex_count")
+        weighted = h_w is not None
+        shape = (n, width, nvec, entries, weighted)
+        g = into if (into is not None and getattr(into, "_ingest_shape", None) == shape) else None
+        if g is None:
+            vsrc = torch.empty(max(nvec, 1) * width + SLACK * width, dtype=torch.int32, device=device)
+            vdst = torch.empty(max(nvec, 1) + SLACK, dtype=torch.int32, device=device)
+            vw = torch.empty(max(nvec, 1) * width + SLACK * width, dtype=torch.int32, device=device) if weighted else None
+            g = cls(n, width, int(topology.edge_count), nvec, entries,
+                    vsrc[: max(nvec * width, 1)], vdst[: max(nvec, 1)],
+                    vw[: max(nvec * width, 1)] if weighted else None,
+                    torch.empty(n + 1, dtype=torch.int64, device=device),
+                    torch.empty(max(entries, 1), dtype=torch.int32, device=device),
+                    torch.empty(max(n, 1), dtype=torch.int32, device=device))
+            if nvec == 0:
+                vsrc.fill_(-1)
+            g._ingest_shape = shape
+        g.edges = int(topology.edge_count)
+        comp = stream or torch.cuda.current_stream()
+        st = _IngestStaging.get(device, chunk_vectors, width, weighted)
+        st.copy.wait_stream(comp)  # `into`'s buffers may still be read by earlier work
+        err = st.err
+        err.zero_()
+        tens = lambda a: torch.from_numpy(a)
+        p = _ptr
+        sp = _lib.stream_ptr(comp)
+
+        def run_chunks(total, per, stage, kernel):
+            for k, lo in enumerate(range(0, total, per)):
+                hi = min(total, lo + per)
+                slot = st.slot(k)
+                st.copy.wait_event(slot["free"])
+                with torch.cuda.stream(st.copy):
+                    stage(slot, lo, hi)
+                    slot["ready"].record(st.copy)
+                comp.wait_event(slot["ready"])
+                kernel(slot, lo, hi)
+                slot["free"].record(comp)
+
+        # vectors: vdst, vsrc (padding from lane_count), vw
+        C = st.chunk
+
+        def stage_vec(slot, lo, hi):
+            slot["dst"][: hi - lo].copy_(tens(h_dst[lo:hi]), non_blocking=True)
+            slot["cnt"][: hi - lo].copy_(tens(h_cnt[lo:hi]), non_blocking=True)
+            slot["src"][: (hi - lo) * width].copy_(tens(h_src[lo * width: hi * width]), non_blocking=True)
+            if weighted:
+                slot["w"][: (hi - lo) * width].copy_(tens(h_w[lo * width: hi * width]), non_blocking=True)
+
+        def ingest_vec(slot, lo, hi):
+            check(L.wg_ingest_vectors(hi - lo, width, n, p(slot["dst"]), p(slot["cnt"]), p(slot["src"]),
+                                      p(slot["w"]) if weighted else None, p(g.vdst) + 4 * lo,
+                                      p(g.vsrc) + 4 * lo * width, (p(g.vw) + 4 * lo * width) if weighted else None,
+                                      p(err), sp))
+        run_chunks(nvec, C, stage_vec, ingest_vec)
+
+        # index positions and degrees through the lane slot
+        def stage_lin(arr):
+            return lambda slot, lo, hi: slot["src"][: hi - lo].copy_(tens(arr[lo:hi]), non_blocking=True)
+
+        run_chunks(entries, C * width, stage_lin(h_pos),
+                   lambda slot, lo, hi: check(L.wg_ingest_u32(hi - lo, p(slot["src"]), nvec, p(g.idx_pos) + 4 * lo,
+                                                              _lib.WG_INGEST_BAD_POS, p(err), sp)))
+        run_chunks(n, C * width, stage_lin(h_deg),
+                   lambda slot, lo, hi: check(L.wg_ingest_u32(hi - lo, p(slot["src"]), 1 << 32, p(g.outdeg) + 4 * lo,
+                                                              _lib.WG_INGEST_BAD_DEGREE, p(err), sp)))
+        with torch.cuda.stream(st.copy):
+            g.idx_off.copy_(tens(h_off), non_blocking=True)
+            st.copy_done.record(st.copy)
+        comp.wait_event(st.copy_done)
+        check(L.wg_ingest_offsets(n, p(g.idx_off), entries, p(g.outdeg), p(err), sp))
+        bits = int(err.item())  # the one synchronisation of the upload
+        bad = bits & ~_lib.WG_INGEST_LENS_DIFFER
+        if bad:
+            raise ValueError(f"reference layout does not fit the device layout (wg_ingest flags 0x{bad:x}): "
+                             + ", ".join(k for k, b in _INGEST_FLAGS.items() if bad & b))
+        g.lens_are_degrees = not (bits & _lib.WG_INGEST_LENS_DIFFER)
+        g._struct = None
+        g._degrees_src = degrees  # the out-degrees this graph holds (engine._with_degrees)
+        g.vw8 = None
+        if weighted:
+            g.narrow_weights(comp)
+        return g
 
     # -- compact upload form -------------------------------------------------
     def vector_offsets(self):
@@ -616,11 +739,17 @@ class LoopResult:
 
 
 def values_to_int64(t, val_type: int) -> np.ndarray:
+    """Device values -> host int64 with the reference sentinel (engine.py:43),
+    widened on the device and read into pinned host memory."""
+    torch = _torch()
     if val_type == WG_VAL_I64:
-        return t.cpu().numpy().astype(np.int64)
-    v = t.cpu().numpy().view(np.uint32).astype(np.int64)
-    v[v == U32_INF] = UNREACHED
-    return v
+        v = t
+    else:
+        v = t.to(torch.int64) & U32_INF
+        v.masked_fill_(v == U32_INF, UNREACHED)
+    out = torch.empty(v.shape, dtype=torch.int64, pin_memory=True)
+    out.copy_(v)
+    return out.numpy()
 
 
 def wedge_limit(threshold: Fraction, edges: int) -> int:
@@ -937,6 +1066,45 @@ def encode_values(values: np.ndarray, val_type: int):
     if u.size and np.any((u == U32_INF) & (v != UNREACHED)):
         raise ValueError("value 0xFFFFFFFF collides with the uint32 sentinel")
     return torch.from_numpy(u.astype(np.uint32).view(np.int32)).cuda()
+
+
+@dataclass
+class InitialValues:
+    """Initial values on the device plus the facts the loop specialises on,
+    derived by one device pass (wg_values_scan) instead of host scans."""
+    i64: object            # device int64 copy (the WG_VAL_I64 seed)
+    u32: object            # device uint32 encoding (valid when fits_u32)
+    fits_u32: bool
+    identity: bool         # init[v] == v (WG_RUN_IDENTITY_INIT)
+    first_hit: bool        # level-synchronous run (WG_RUN_FIRST_HIT, see first_hit_ok)
+    level_base: int
+
+    def seed(self, val_type: int):
+        return self.u32 if val_type == WG_VAL_U32 else self.i64
+
+
+def prepare_initial_values(init: np.ndarray, kern, members: Optional[np.ndarray], stream=None) -> InitialValues:
+    """Upload int64 initial values (engine.py:90-116) and scan them on the
+    device: the same decisions as fits_u32 / identity_values / first_hit_ok /
+    first_hit_level, one 32-byte read back."""
+    torch = _torch()
+    v = np.ascontiguousarray(init, dtype=np.int64)
+    n = int(v.shape[0])
+    d64 = torch.from_numpy(v).to("cuda", non_blocking=False)
+    enc = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+    stats = torch.empty(4, dtype=torch.int64, device="cuda")
+    check(_lib.load().wg_values_scan(n, _ptr(d64), UNREACHED, _ptr(enc), _ptr(stats), _lib.stream_ptr(stream)))
+    flags, cnt, lo, hi = (int(x) for x in stats.cpu().tolist())
+    fits = not flags & _lib.WG_VALUES_NOT_U32
+    identity = n > 0 and not flags & _lib.WG_VALUES_NOT_IDENTITY
+    fh = bool(kern.filter_unvisited) and not kern.use_weight
+    if fh and cnt:
+        fh = lo == hi
+        if fh and members is not None:
+            m = np.asarray(members, dtype=np.int64)
+            m = m[(m >= 0) & (m < n)]
+            fh = int(np.count_nonzero(v[m] != UNREACHED)) == cnt  # members are unique
+    return InitialValues(d64, enc[:n], fits, bool(identity), bool(fh), lo if (fh and cnt) else 0)
 
 
 def fits_u32(values: np.ndarray, kern, g: DeviceGraph) -> bool:

@@ -297,7 +297,8 @@ def device_run(be, topology, index, program: ApplicationProgram, degrees, config
 
     g = be.device_graph(topology, index, degrees)
     g = _with_degrees(be, g, degrees)
-    val_type = WG_VAL_U32 if dv.fits_u32(init, kern, g) else WG_VAL_I64
+    iv = dv.prepare_initial_values(init, kern, members)
+    val_type = WG_VAL_U32 if iv.fits_u32 else WG_VAL_I64
     words = dv.all_words(n) if members is None else dv.initial_words(n, members)
     while True:
         loop = _loop_for(be, g, config.precision.shift, val_type)
@@ -308,13 +309,10 @@ def device_run(be, topology, index, program: ApplicationProgram, degrees, config
                     frontier_log.append(lp.frontier_members(it))
                 if value_log is not None:
                     value_log.append(dv.values_to_int64(lp.values_after(it), val_type))
-        dinit = dv.encode_values(init, val_type)
         start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         start.record()
-        fh = dv.first_hit_ok(kern, init, members)
-        p = loop.seed(dinit, words, kern, config.threshold.fraction, first_hit=fh,
-                      level_base=dv.first_hit_level(init) if fh else 0,
-                      identity_init=dv.identity_values(init))
+        p = loop.seed(iv.seed(val_type), words, kern, config.threshold.fraction, first_hit=iv.first_hit,
+                      level_base=iv.level_base, identity_init=iv.identity)
         timer = None
         if getattr(be, "per_iteration_timing", False):
             # CUDA events around each launch group (one iteration per launch)
@@ -360,6 +358,8 @@ def _with_degrees(be, g, degrees):
     differs from the layout's own (uploaded once per degrees object)."""
     if degrees is None:
         return g
+    if getattr(g, "_degrees_src", None) is degrees:
+        return g  # the graph was uploaded with exactly these degrees
     deg = np.asarray(degrees)
     own = getattr(g, "_outdeg_host", None)
     if own is None:

@@ -130,22 +130,39 @@ class EdgeList:
 
 
 class PullTopology:
-    """Destination-grouped W-lane vectors (graph.py:109-164), resident on the
-    device as a DeviceGraph.  Reference-layout host arrays are lazy."""
+    """Destination-grouped W-lane vectors (graph.py:109-164).
 
-    def __init__(self, device_graph: DeviceGraph):
-        self.device = device_graph
+    Two forms: ``PullTopology(device_graph)`` -- resident on the device (what
+    build_pull_topology returns; reference-layout host arrays are then lazy
+    downloads) -- or the reference's own constructor
+    ``PullTopology(vertex_count, vector_width, edge_count, vec_dst, lane_src,
+    lane_weight, lane_count)`` over host int64 arrays, which the backend
+    uploads (and narrows on the device) when a run needs them."""
+
+    def __init__(self, *args):
         self._lanes = None
         self._vec_dst = None
         self._valid = None
+        if len(args) == 1 and isinstance(args[0], DeviceGraph):
+            self.device = args[0]
+            self._host = None
+            return
+        if len(args) != 7:
+            raise TypeError("PullTopology(device_graph) or PullTopology(vertex_count, vector_width, "
+                            "edge_count, vec_dst, lane_src, lane_weight, lane_count)")
+        n, w, m, vec_dst, lane_src, lane_weight, lane_count = args
+        self.device = None
+        self._host = (int(n), int(w), int(m))
+        self._vec_dst = vec_dst
+        self._lanes = (lane_src, lane_weight, lane_count)
 
-    vertex_count = property(lambda self: self.device.n)
-    vector_width = property(lambda self: self.device.width)
-    edge_count = property(lambda self: self.device.edges)
-    vector_count = property(lambda self: self.device.nvec)
+    vertex_count = property(lambda self: self._host[0] if self._host else self.device.n)
+    vector_width = property(lambda self: self._host[1] if self._host else self.device.width)
+    edge_count = property(lambda self: self._host[2] if self._host else self.device.edges)
+    vector_count = property(lambda self: int(self._vec_dst.shape[0]) if self._host else self.device.nvec)
 
     def is_weighted(self) -> bool:
-        return self.device.weighted()
+        return self._lanes[1] is not None if self._host else self.device.weighted()
 
     @property
     def vec_dst(self) -> np.ndarray:
@@ -176,20 +193,31 @@ class PullTopology:
 
     def __repr__(self) -> str:
         return (f"PullTopology(|V|={self.vertex_count}, |E|={self.edge_count}, "
-                f"vectors={self.vector_count}, W={self.vector_width}, device)")
+                f"vectors={self.vector_count}, W={self.vector_width}, {'host' if self._host else 'device'})")
 
 
 class EdgeIndex:
-    """Per-source ascending, de-duplicated vector positions (graph.py:190-212),
-    sharing the topology's device graph."""
+    """Per-source ascending, de-duplicated vector positions (graph.py:190-212).
 
-    def __init__(self, device_graph: DeviceGraph):
-        self.device = device_graph
+    ``EdgeIndex(device_graph)`` shares the topology's device graph;
+    ``EdgeIndex(vertex_count, vector_count, offsets, positions)`` is the
+    reference's constructor over host int64 arrays."""
+
+    def __init__(self, *args):
         self._off = None
         self._pos = None
+        if len(args) == 1 and isinstance(args[0], DeviceGraph):
+            self.device = args[0]
+            self._host = None
+            return
+        if len(args) != 4:
+            raise TypeError("EdgeIndex(device_graph) or EdgeIndex(vertex_count, vector_count, offsets, positions)")
+        self.device = None
+        self._host = (int(args[0]), int(args[1]))
+        self._off, self._pos = args[2], args[3]
 
-    vertex_count = property(lambda self: self.device.n)
-    vector_count = property(lambda self: self.device.nvec)
+    vertex_count = property(lambda self: self._host[0] if self._host else self.device.n)
+    vector_count = property(lambda self: self._host[1] if self._host else self.device.nvec)
 
     @property
     def offsets(self) -> np.ndarray:
@@ -207,6 +235,8 @@ class EdgeIndex:
         return self.positions[self.offsets[v]: self.offsets[v + 1]]
 
     def __repr__(self) -> str:
+        if self._host:
+            return f"EdgeIndex(|V|={self.vertex_count}, entries={len(self._pos)}, host)"
         return f"EdgeIndex(|V|={self.vertex_count}, entries={self.device.entries}, device)"
 
 
@@ -224,9 +254,10 @@ def build_edge_index(topology) -> EdgeIndex:
     """graph.py:283-301.  For a device topology the index already exists;
     a reference-layout topology is uploaded (its index is then rebuilt on the
     device from the lanes)."""
-    if isinstance(topology, PullTopology):
+    if isinstance(topology, PullTopology) and topology.device is not None:
         return EdgeIndex(topology.device)
-    raise TypeError("build_edge_index expects a PullTopology built by this package")
+    raise TypeError("build_edge_index expects a device PullTopology built by this package "
+                    "(host reference-layout topologies carry their own EdgeIndex)")
 
 
 def compute_out_degrees(edges: EdgeList) -> np.ndarray:

@@ -460,3 +460,114 @@ def test_bottom_up_levels_follow_the_initial_value(wg):
     ref = oracle.run_until_convergence(tp, oracle.build_edge_index(tp), oracle.compute_out_degrees(n, el.src),
                                        oracle.kern_of("bfs"), init(n), roots, Fraction(1, 100), 8)
     assert np.array_equal(res.values, ref.values)
+
+
+# ------------------------------------------- host reference-layout ingest ---
+def _oracle_graph(scale, app, sym=True):
+    n, s, d = oracle.rmat_edges_fast(scale, 16, 1)
+    s, d = oracle.prepare_unweighted(n, s, d, sym)
+    w = oracle.synthesize_weights(s, d, 255) if app == "sssp" else None
+    topo = oracle.build_pull_topology(n, s, d, w, 4)
+    return n, topo, oracle.build_edge_index(topo), oracle.compute_out_degrees(n, s)
+
+
+def _host_objects(wg, n, topo, idx):
+    """The package's PullTopology / EdgeIndex over the reference's own host
+    arrays (the reference constructors, graph.py:109-212)."""
+    return (wg.PullTopology(n, topo.vector_width, topo.edge_count, topo.vec_dst, topo.lane_src,
+                            topo.lane_weight, topo.lane_count),
+            wg.EdgeIndex(n, topo.vector_count, idx.offsets, idx.positions))
+
+
+@pytest.mark.parametrize("app", ["bfs", "cc", "sssp"])
+def test_run_from_host_reference_layout(wg, app):
+    """run_until_convergence on int64 host arrays: raw H2D + device narrowing
+    (wg_ingest_*) + device value scan give the oracle's values and trace."""
+    n, topo, idx, deg = _oracle_graph(12, app)
+    ht, hi = _host_objects(wg, n, topo, idx)
+    vpg, thr = (8, Fraction(1, 100)) if app == "bfs" else (4, Fraction(1, 5))
+    cfg = wg.EngineConfig(threshold=wg.FullnessThreshold(thr), precision=wg.FrontierPrecision(vpg))
+    be = wg.B200Backend(reupload=True)
+    prog = wg.make_program(app, None if app == "cc" else 0)
+    vals, front = oracle.initial_state(app, n, 0)
+    want = oracle.run_until_convergence(topo, idx, deg, oracle.kern_of(app), vals, front, thr, vpg)
+    for _ in range(2):  # the second call re-uploads into the cached buffers
+        res = wg.run_until_convergence(ht, hi, prog, deg, cfg, backend=be)
+        assert np.array_equal(res.values, want.values)
+        assert wg.stats_signature(res.stats) == oracle.signature(want.stats)
+
+
+def test_reupload_sees_arrays_changed_in_place(wg):
+    n, topo, idx, deg = _oracle_graph(10, "sssp")
+    ht, hi = _host_objects(wg, n, topo, idx)
+    cfg = wg.EngineConfig()
+    be = wg.B200Backend(reupload=True)
+    prog = wg.make_program("sssp", 0)
+    wg.run_until_convergence(ht, hi, prog, deg, cfg, backend=be)
+    topo.lane_weight[topo.lane_weight > 0] += 7  # same objects, new weights
+    res = wg.run_until_convergence(ht, hi, prog, deg, cfg, backend=be)
+    vals, front = oracle.initial_state("sssp", n, 0)
+    want = oracle.run_until_convergence(topo, idx, deg, oracle.SSSP, vals, front, Fraction(1, 5), 4)
+    assert np.array_equal(res.values, want.values)
+
+
+def test_ingest_rejects_out_of_range_ids(wg):
+    n, topo, idx, deg = _oracle_graph(8, "cc")
+    bad = topo.lane_src.copy()
+    bad[0, 0] = n + 5
+    ht = wg.PullTopology(n, 4, topo.edge_count, topo.vec_dst, bad, None, topo.lane_count)
+    hi = wg.EdgeIndex(n, topo.vector_count, idx.offsets, idx.positions)
+    with pytest.raises(ValueError, match="lane source"):
+        wg.run_until_convergence(ht, hi, wg.cc_program(), deg, wg.EngineConfig(), backend=wg.B200Backend())
+
+
+@pytest.mark.parametrize("app", ["bfs", "cc", "sssp"])
+def test_value_log_matches_reference(wg, app):
+    """value_log (engine.py:337-338, 381-385): one value snapshot per
+    iteration, equal to the reference loop's, with frontier_log beside it."""
+    n, topo, idx, deg = _oracle_graph(10, app)
+    ht, hi = _host_objects(wg, n, topo, idx)
+    cfg = wg.EngineConfig(threshold=wg.FullnessThreshold(Fraction(1, 5)), precision=wg.FrontierPrecision(4))
+    vlog, flog = [], []
+    res = wg.run_until_convergence(ht, hi, wg.make_program(app, None if app == "cc" else 0), deg, cfg,
+                                   frontier_log=flog, value_log=vlog)
+    want_v, want_f = [], []
+    vals, front = oracle.initial_state(app, n, 0)
+    want = oracle.run_until_convergence(topo, idx, deg, oracle.kern_of(app), vals, front, Fraction(1, 5), 4,
+                                        frontier_log=want_f, value_log=want_v)
+    assert len(vlog) == len(want_v) == len(res.stats) == len(want.stats)
+    for got, exp in zip(vlog, want_v):
+        assert got.dtype == np.int64 and np.array_equal(got, exp)
+    for got, exp in zip(flog, want_f):
+        assert np.array_equal(got, exp)
+    assert np.array_equal(vlog[-1], res.values)
+
+
+@pytest.mark.parametrize("case", ["cc_floor", "bfs_bottom_up", "bfs_bottom_up_i64", "bfs_level_base"])
+def test_plain_dense_kernels_from_iteration_2(wg, monkeypatch, case):
+    """floor_pull_kernel (CC floor skipping) and bottom_up_pull_kernel (BFS)
+    normally start at iteration 3 (WG_FLOOR_FROM); forced from iteration 2
+    on a small graph they must still give the oracle's values and work
+    counters -- including the int64 path (values >= 2^32) and a non-zero
+    level base.  Both loop drivers (graph / per-iteration launches)."""
+    import dataclasses
+    monkeypatch.setenv("WG_FLOOR_FROM", "2")
+    app = "cc" if case.startswith("cc") else "bfs"
+    n, topo, idx, deg = _oracle_graph(12, app)
+    ht, hi = _host_objects(wg, n, topo, idx)
+    prog = wg.make_program(app, None if app == "cc" else 0)
+    vals, front = oracle.initial_state(app, n, 0)
+    base = {"bfs_bottom_up_i64": 5_000_000_000, "bfs_level_base": 7}.get(case)
+    if base is not None:
+        vals = vals.copy()
+        vals[0] = base
+        prog = dataclasses.replace(prog, initial_values=lambda k, v=vals: v.copy())
+    thr = Fraction(1, 5)  # dense iterations early enough to reach the plain kernels
+    want = oracle.run_until_convergence(topo, idx, deg, oracle.kern_of(app), vals, front, thr, 4)
+    assert sum(s.mode == "FullScan" for s in want.stats[1:]) >= 1
+    for graph in ("1", "0"):
+        monkeypatch.setenv("WG_GRAPH", graph)
+        cfg = wg.EngineConfig(threshold=wg.FullnessThreshold(thr), precision=wg.FrontierPrecision(4))
+        res = wg.run_until_convergence(ht, hi, prog, deg, cfg, backend=wg.B200Backend())
+        assert np.array_equal(res.values, want.values), (case, graph)
+        assert wg.stats_signature(res.stats) == oracle.signature(want.stats), (case, graph)

@@ -164,3 +164,19 @@ def test_survey_digests_s16_bfs():
                                        backend=oracle.PortBackend(4))
     assert oracle.result_digest(out.values) == "591673cb243fad4e"
     assert len(out.stats) == 5
+
+
+def test_threaded_input_prep_matches_golden(golden):
+    """The reference arm's fast input preparation (orc_rmat + radix-sort
+    dedup) reproduces the reference generators' golden outputs."""
+    z = golden.npz("gen")
+    n, s, d = oracle.rmat_edges_fast(8, 16, 1)
+    assert np.array_equal(s, z["rmat8_src"]) and np.array_equal(d, z["rmat8_dst"])
+    n, s, d = oracle.rmat_edges_fast(11, 4, 7)
+    assert np.array_equal(s, z["rmat11_s7_src"]) and np.array_equal(d, z["rmat11_s7_dst"])
+    ss, dd = oracle.prepare_unweighted(n, s, d, True)
+    assert np.array_equal(ss, z["rmat11_s7_sym_src"]) and np.array_equal(dd, z["rmat11_s7_sym_dst"])
+    keep = s != d
+    a, b = oracle.dedup_directed(s[keep], d[keep])
+    ss, dd = oracle.prepare_unweighted(n, s, d, False)
+    assert np.array_equal(ss, a) and np.array_equal(dd, b)
