@@ -71,6 +71,9 @@ typedef struct wg_graph {
     const uint8_t *vw8;      /* optional [nvec*width] lane weights as bytes (every weight <= 255,
                                 wg_narrow_weights); the dense pull then streams these instead of
                                 vw (16 bytes of readable slack past the end) */
+    const uint32_t *voff;    /* optional [n+1] first vector of each destination (the run-length form
+                                of vdst, wg_vector_offsets_from_dst): enables the destination-major
+                                dense pulls (a thread / warp per destination, no vdst stream) */
 } wg_graph;
 
 /* Every vertex's edge-index length equals its out-degree (no parallel edges;
@@ -278,6 +281,9 @@ typedef struct wg_run_bufs {
     uint32_t *glist_alt;    /* group list [groups]: with both, the persistent sparse loop fuses the
                                transform of iteration k+1 into the pull of k (one barrier per
                                iteration); without, it runs transform and pull as two phases */
+    uint32_t *work;         /* optional [n] scratch of the destination-major dense pulls (their list of
+                               destinations with long in-lists, handled a warp each); required when
+                               the graph carries voff */
 } wg_run_bufs;
 
 typedef struct wg_run_params {
@@ -456,6 +462,11 @@ int wg_weights_hash(uint64_t m, const uint32_t *d_src, const uint32_t *d_dst, ui
 int wg_grid_edges(uint32_t rows, uint32_t cols, uint64_t seed, uint32_t keep_per_million,
                   uint32_t max_weight, uint32_t *d_src, uint32_t *d_dst, uint32_t *d_w,
                   uint64_t *d_counter, uint64_t *h_m_out, void *stream);
+
+/* voff[d] = first vector of destination d (lower bound of d in the sorted
+ * vdst), voff[n] = nvec: the per-destination form of PullTopology.vec_dst
+ * (graph.py:240-243).  d_voff: [n+1]. */
+int wg_vector_offsets_from_dst(const wg_graph *g, uint32_t *d_voff, void *stream);
 
 /* ---------------------------------------------------------------------- */
 /* Ingest of the plugin call's reference-layout host arrays (ingest.cu).   */

@@ -26,7 +26,8 @@ c_u32, c_u64, c_i32, c_i64, c_vp = ctypes.c_uint32, ctypes.c_uint64, ctypes.c_in
 class WgGraph(ctypes.Structure):
     _fields_ = [("n", c_u32), ("width", c_u32), ("nvec", c_u64), ("edges", c_u64),
                 ("entries", c_u64), ("vsrc", c_vp), ("vdst", c_vp), ("vw", c_vp),
-                ("idx_off", c_vp), ("idx_pos", c_vp), ("outdeg", c_vp), ("flags", c_u32), ("vw8", c_vp)]
+                ("idx_off", c_vp), ("idx_pos", c_vp), ("outdeg", c_vp), ("flags", c_u32), ("vw8", c_vp),
+                ("voff", c_vp)]
 
 
 WG_GRAPH_LENS_ARE_DEGREES = 1
@@ -46,7 +47,7 @@ class WgRunBufs(ctypes.Structure):
     _fields_ = [("vals", c_vp * 2), ("fbits", c_vp * 2), ("fvert", c_vp * 2), ("fpref", c_vp * 2),
                 ("tstart", c_vp * 2), ("gbits", c_vp), ("glist", c_vp), ("bcount", c_vp), ("recs", c_vp),
                 ("ctrl", c_vp), ("ring", c_u32), ("gbits_alt", c_vp),
-                ("glist_alt", c_vp)]
+                ("glist_alt", c_vp), ("work", c_vp)]
 
 
 class WgRunParams(ctypes.Structure):
@@ -81,7 +82,7 @@ EXPORTS = [
     "wg_vector_offsets_scratch_bytes", "wg_vector_offsets", "wg_coded_scratch_bytes", "wg_encode_lanes",
     "wg_decode_lanes", "wg_index_chunk_coded", "wg_expand_scratch_bytes", "wg_index_placed_scratch_bytes",
     "wg_index_place_begin", "wg_index_place_chunk", "wg_index_place_coded", "wg_index_place_end",
-    "wg_ingest_vectors", "wg_ingest_u32", "wg_ingest_offsets", "wg_values_scan",
+    "wg_ingest_vectors", "wg_ingest_u32", "wg_ingest_offsets", "wg_values_scan", "wg_vector_offsets_from_dst",
 ]
 
 _LIB = None
@@ -199,6 +200,7 @@ def load(path: os.PathLike | str | None = None):
         "wg_ingest_u32": (ctypes.c_int, [c_u64, c_vp, c_i64, c_vp, c_u32, c_vp, c_vp]),
         "wg_ingest_offsets": (ctypes.c_int, [c_u32, c_vp, c_u64, c_vp, c_vp, c_vp]),
         "wg_values_scan": (ctypes.c_int, [c_u32, c_vp, c_i64, c_vp, c_vp, c_vp]),
+        "wg_vector_offsets_from_dst": (ctypes.c_int, [G, c_vp, c_vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -307,6 +307,29 @@ int launch_pull(const LoopCtx &c, const wg_graph *g, const PullBufs &pb, int val
     if (only) handles = 1 << only;
     const bool want_full = only == 0 || only == MODE_FULL;
     if (want_full && (c.forced_mode == 0 || c.forced_mode == MODE_FULL)) {
+      if (pb.dst_major) {
+        using DstFn = void (*)(LoopCtx, wg_graph, PullBufs, int64_t, int64_t);
+        DstFn fd = nullptr, fh = nullptr;
+        const bool u32 = val_type == WG_VAL_U32;
+#define WG_PICK_DST(KIND)                                                                                    \
+    switch (g->width) {                                                                                      \
+        case 1: fd = u32 ? dense_dst_kernel<uint32_t, 1, KIND> : dense_dst_kernel<int64_t, 1, KIND>;         \
+                fh = u32 ? dense_heavy_kernel<uint32_t, 1, KIND> : dense_heavy_kernel<int64_t, 1, KIND>; break; \
+        case 2: fd = u32 ? dense_dst_kernel<uint32_t, 2, KIND> : dense_dst_kernel<int64_t, 2, KIND>;         \
+                fh = u32 ? dense_heavy_kernel<uint32_t, 2, KIND> : dense_heavy_kernel<int64_t, 2, KIND>; break; \
+        case 4: fd = u32 ? dense_dst_kernel<uint32_t, 4, KIND> : dense_dst_kernel<int64_t, 4, KIND>;         \
+                fh = u32 ? dense_heavy_kernel<uint32_t, 4, KIND> : dense_heavy_kernel<int64_t, 4, KIND>; break; \
+        case 8: fd = u32 ? dense_dst_kernel<uint32_t, 8, KIND> : dense_dst_kernel<int64_t, 8, KIND>;         \
+                fh = u32 ? dense_heavy_kernel<uint32_t, 8, KIND> : dense_heavy_kernel<int64_t, 8, KIND>; break; \
+    }
+        if (filter) { WG_PICK_DST(DSTK_BOTTOM_UP) } else { WG_PICK_DST(DSTK_FLOOR) }
+#undef WG_PICK_DST
+        WG_REQUIRE(fd && fh, "no destination-major pull for width %u", g->width);
+        fd<<<grid_for(g->n ? g->n : 1, 256, 8), 256, 0, s>>>(c, *g, pb, k->apply_increment, k->sentinel);
+        fh<<<grid_for(g->n ? g->n : 1, 256 * 64, 8), 256, 0, s>>>(c, *g, pb, k->apply_increment, k->sentinel);
+        ::wg::count_launch(2);
+        WG_CHECK_LAUNCH("pull (dense, destination-major)");
+      } else {
         if (pb.ident && !weight && !filter) {  // iteration 1 of an identity-initialised run
             using IdentFn = void (*)(LoopCtx, wg_graph, PullBufs, int64_t, int64_t);
             IdentFn fi = nullptr;
@@ -363,6 +386,7 @@ int launch_pull(const LoopCtx &c, const wg_graph *g, const PullBufs &pb, int val
             ::wg::count_launch();
             WG_CHECK_LAUNCH("pull (dense, TMA)");
         }
+      }
         if (slot) {
             timer_end(timer, *slot, s);
             *slot = timer_begin(timer, 4, (int64_t)c.it_arg, s);
@@ -633,6 +657,12 @@ static PullBufs pull_bufs(const wg_graph *g, const wg_run_bufs *b, const wg_run_
         const bool plain = pb.floor_kernels && ((pb.floor_skip && !p->kern.filter_unvisited) || pb.first_hit);
         pb.pipeline_until = plain ? pb.floor_from : ~0ull;
     }
+    // destination-major dense pulls: CC-like floor runs and level-synchronous
+    // BFS, unweighted, when the graph carries voff and the run a work list
+    pb.work = b->work;
+    pb.dst_major = g->voff && b->work && !p->kern.use_weight &&
+                           ((pb.floor_skip && !p->kern.filter_unvisited) || (pb.first_hit && p->kern.filter_unvisited))
+                       ? 1u : 0u;
     return pb;
 }
 

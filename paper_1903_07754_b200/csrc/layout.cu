@@ -1205,3 +1205,30 @@ int wg_grid_edges(uint32_t rows, uint32_t cols, uint64_t seed, uint32_t keep_per
 }
 
 }  // extern "C"
+
+namespace {
+// voff[d] = lower bound of d in the sorted vdst (destination runs, graph.py:235)
+__global__ void voff_from_dst_kernel(uint32_t n, uint64_t nvec, const uint32_t *vdst, uint32_t *voff) {
+    for (uint64_t d = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; d <= n;
+         d += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t lo = 0, hi = nvec;
+        while (lo < hi) {
+            const uint64_t mid = (lo + hi) >> 1;
+            if (vdst[mid] < d) lo = mid + 1;
+            else hi = mid;
+        }
+        voff[d] = (uint32_t)lo;
+    }
+}
+}  // namespace
+
+extern "C" int wg_vector_offsets_from_dst(const wg_graph *g, uint32_t *d_voff, void *stream) {
+    WG_REQUIRE(g && d_voff, "null argument");
+    WG_REQUIRE(g->nvec < (1ull << 32), "more than 2^32 vectors");
+    WG_REQUIRE(g->nvec == 0 || g->vdst, "null vdst");
+    cudaStream_t s = as_stream(stream);
+    voff_from_dst_kernel<<<grid_for((uint64_t)g->n + 1, 256, 8), 256, 0, s>>>(g->n, g->nvec, g->vdst, d_voff);
+    ::wg::count_launch();
+    WG_CHECK_LAUNCH("voff_from_dst");
+    return WG_OK;
+}

@@ -67,6 +67,8 @@ struct PullBufs {
     uint32_t floor_from;
     uint64_t pipeline_until = ~0ull;  // dense iterations >= this one skip the TMA pipeline (plain kernels)
     int64_t level_base;  // its frontier-0 value
+    uint32_t *work;      // wg_run_bufs.work: destination list of the destination-major dense pulls
+    uint32_t dst_major;  // dense iterations run dense_dst_kernel (DSTK_FLOOR / DSTK_BOTTOM_UP)
 };
 
 
@@ -85,6 +87,17 @@ template <typename T>
 __device__ __forceinline__ T shfl_t(T v, int src) {
     if constexpr (sizeof(T) == 8) return (T)__shfl_sync(FULL, (unsigned long long)v, src);
     else return (T)__shfl_sync(FULL, (unsigned)v, src);
+}
+template <typename T>
+__device__ __forceinline__ T warp_min_t(T v) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        T o;
+        if constexpr (sizeof(T) == 8) o = (T)__shfl_xor_sync(FULL, (unsigned long long)v, off);
+        else o = (T)__shfl_xor_sync(FULL, (unsigned)v, off);
+        v = o < v ? o : v;
+    }
+    return v;
 }
 template <typename T>
 __device__ __forceinline__ T shfl_up_t(T v, int off) {
@@ -714,6 +727,240 @@ __global__ void __launch_bounds__(256) bottom_up_pull_kernel(LoopCtx c, wg_graph
     if (ovf) out->overflow = 1;
     const uint64_t t = warp_sum(touched);
     if (lane_id() == 0 && t) atomicAdd((unsigned long long *)&out->vectors_touched, (unsigned long long)t);
+}
+
+// ---------------------------------------------------------------------------
+// Destination-major dense pulls (g.voff present, PullBufs::dst_major).
+//
+// A thread per destination d walks d's own vectors [voff[d], voff[d+1]) --
+// no per-vector vdst stream -- and stops as soon as d's result is decided:
+//
+//  * FLOOR (WG_RUN_FLOOR_SKIP, unweighted, uint32: CC-like min-label runs).
+//    0 is the smallest uint32 value, so a destination already at 0 gathers
+//    nothing and a destination whose running minimum reaches 0 stops
+//    gathering.  The first lane probed is the destination's smallest source
+//    (lanes ascend, graph.py:235), the likeliest to carry the smallest label;
+//    with identity initial values at iteration 1 it IS the minimum message
+//    (no gather at all).  CC s22, iteration 2: 2.23M destinations not at 0,
+//    all but 0.34M decided by that probe.
+//  * BOTTOM-UP (WG_RUN_FIRST_HIT, filtered, unweighted: level-synchronous
+//    BFS).  Visited destinations keep prev[d] and count as untouched
+//    (_kernels.pyx:77-80); an unvisited destination tests its sources' bits in
+//    the previous frontier -- every finite in-neighbour of it sits there --
+//    and stops at the first hit (cand = level + inc).
+//
+// Destinations with more than DST_LIGHT vectors that are still undecided go
+// to a work list (b.work, count in the record's reserved[4]) and are finished
+// by dense_heavy_kernel, a warp each.  Values: every destination's nxt[d] is
+// written (prev[d] or its improvement), so no buffer sync is needed after a
+// dense iteration (end_of_iteration); next-frontier bits are set one warp
+// word at a time (a warp owns 32 consecutive destinations).  Results and
+// counters are those of the reference's full scan (every vector touched;
+// bottom-up: the vectors of unvisited destinations).
+constexpr uint32_t DST_LIGHT = 8;  // vectors walked by one thread
+constexpr int DSTK_FLOOR = 0, DSTK_BOTTOM_UP = 1;
+
+template <typename T, int W, int KIND>
+__global__ void __launch_bounds__(256) dense_dst_kernel(LoopCtx c, wg_graph g, PullBufs b, int64_t inc,
+                                                        int64_t sentinel) {
+    using VT = ValTraits<T>;
+    const uint64_t it = ctx_iter(c);
+    if (ctx_mode(c, it) != MODE_FULL) return;
+    wg_iter_rec *out = ctx_out(c, it);
+    const T *__restrict__ prev = (const T *)(((it - 1) & 1) ? b.vals[1] : b.vals[0]);
+    T *__restrict__ nxt = (T *)((it & 1) ? b.vals[1] : b.vals[0]);
+    uint32_t *__restrict__ obits = ((it & 1) ? b.fbits[1] : b.fbits[0]);
+    const uint32_t *__restrict__ inbits = (((it - 1) & 1) ? b.fbits[1] : b.fbits[0]);
+    const uint32_t *__restrict__ voff = g.voff;
+    const T INF = VT::inf(sentinel);
+    // iteration 1 reads no bitmap (the initial frontier lives in the caller's
+    // words): a level-synchronous run's finite vertices ARE that frontier
+    const auto in_prev_frontier = [&](uint32_t v) -> bool {
+        return it == 1 ? prev[v] != INF : ((inbits[v >> 5] >> (v & 31)) & 1u) != 0u;
+    };
+    const bool exact_first = KIND == DSTK_FLOOR && b.ident && it == 1;  // identity values: lane 0 is the min
+    // bottom-up candidate: the level after the previous frontier's
+    uint32_t ovf = 0;
+    T bu_cand = INF;
+    if constexpr (KIND == DSTK_BOTTOM_UP) {
+        const T level = (T)(b.level_base + (int64_t)(it - 1) * inc);
+        if constexpr (VT::U32) {
+            const uint64_t cc = (uint64_t)level + (uint64_t)inc;
+            if (cc >= 0xffffffffull) ovf = 1;
+            else bu_cand = (T)cc;
+        } else {
+            bu_cand = level + (T)inc;
+        }
+    }
+    uint64_t touched = 0;
+    const uint64_t n = g.n;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;  // a multiple of 32: warps stay word-aligned
+    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
+        const uint64_t d = base + threadIdx.x;
+        bool upd = false;
+        if (d < n) {
+            const T p = prev[d];
+            const uint32_t v0 = voff[d], v1 = voff[d + 1];
+            T res = p;
+            if constexpr (KIND == DSTK_FLOOR) {
+                if (p != (T)0 && v1 > v0) {
+                    const uint32_t s0 = g.vsrc[(uint64_t)v0 * W];
+                    T agg = exact_first ? (T)s0 : prev[s0];
+                    bool decided = exact_first || agg == (T)0;
+                    if (!decided) {
+                        if (v1 - v0 <= DST_LIGHT) {
+                            for (uint32_t v = v0; v < v1 && agg != (T)0; ++v) {
+                                uint32_t src[W], wt[W];
+                                load_lanes<W>(g.vsrc, v, src);
+                                const T m = fold_lanes<T, W, false>(src, wt, prev, INF, ovf);
+                                agg = m < agg ? m : agg;
+                            }
+                        } else {
+                            const unsigned slot = atomicAdd((unsigned *)&out->reserved[4], 1u);
+                            b.work[slot] = (uint32_t)d;
+                            agg = INF;  // finished by dense_heavy_kernel
+                        }
+                    }
+                    if (agg != INF) {
+                        T cand;
+                        bool ok = true;
+                        if constexpr (VT::U32) {
+                            const uint64_t cc = (uint64_t)agg + (uint64_t)inc;
+                            ok = cc < 0xffffffffull;
+                            if (!ok) ovf = 1;
+                            cand = (T)cc;
+                        } else {
+                            cand = agg + (T)inc;
+                        }
+                        if (ok && cand < p) {
+                            res = cand;
+                            upd = true;
+                        }
+                    }
+                }
+            } else {
+                if (p == INF && v1 > v0) {
+                    touched += v1 - v0;
+                    if (v1 - v0 <= DST_LIGHT) {
+                        bool hit = false;
+                        for (uint32_t v = v0; v < v1 && !hit; ++v) {
+                            uint32_t src[W];
+                            load_lanes<W>(g.vsrc, v, src);
+#pragma unroll
+                            for (int l = 0; l < W; ++l)
+                                hit |= src[l] != WG_NO_LANE && in_prev_frontier(src[l]);
+                        }
+                        if (hit && bu_cand != INF) {
+                            res = bu_cand;
+                            upd = true;
+                        }
+                    } else {
+                        const unsigned slot = atomicAdd((unsigned *)&out->reserved[4], 1u);
+                        b.work[slot] = (uint32_t)d;
+                    }
+                }
+            }
+            nxt[d] = res;
+        }
+        const unsigned word = __ballot_sync(FULL, upd);
+        if (word && lane_id() == 0) atomicOr(&obits[(base + (threadIdx.x & ~31u)) >> 5], word);
+    }
+    if (ovf) out->overflow = 1;
+    if constexpr (KIND == DSTK_FLOOR) {
+        if (blockIdx.x == 0 && threadIdx.x == 0)
+            atomicAdd((unsigned long long *)&out->vectors_touched, (unsigned long long)g.nvec);
+    } else {
+        const uint64_t t = warp_sum(touched);
+        if (lane_id() == 0 && t) atomicAdd((unsigned long long *)&out->vectors_touched, (unsigned long long)t);
+    }
+}
+
+// The work list of dense_dst_kernel: a warp per destination, lanes strided
+// over its vectors, stopping once any lane reached the floor (FLOOR) or hit
+// the previous frontier (BOTTOM-UP).
+template <typename T, int W, int KIND>
+__global__ void __launch_bounds__(256) dense_heavy_kernel(LoopCtx c, wg_graph g, PullBufs b, int64_t inc,
+                                                          int64_t sentinel) {
+    using VT = ValTraits<T>;
+    const uint64_t it = ctx_iter(c);
+    if (ctx_mode(c, it) != MODE_FULL) return;
+    wg_iter_rec *out = ctx_out(c, it);
+    const uint64_t count = *(volatile const uint64_t *)&out->reserved[4] & 0xffffffffull;
+    if (count == 0) return;
+    const T *__restrict__ prev = (const T *)(((it - 1) & 1) ? b.vals[1] : b.vals[0]);
+    T *__restrict__ nxt = (T *)((it & 1) ? b.vals[1] : b.vals[0]);
+    uint32_t *__restrict__ obits = ((it & 1) ? b.fbits[1] : b.fbits[0]);
+    const uint32_t *__restrict__ inbits = (((it - 1) & 1) ? b.fbits[1] : b.fbits[0]);
+    const T INF = VT::inf(sentinel);
+    const auto in_prev_frontier = [&](uint32_t v) -> bool {
+        return it == 1 ? prev[v] != INF : ((inbits[v >> 5] >> (v & 31)) & 1u) != 0u;
+    };
+    uint32_t ovf = 0;
+    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const unsigned lane = lane_id();
+    for (uint64_t i = warp; i < count; i += nwarps) {
+        const uint32_t d = b.work[i];
+        const uint32_t v0 = g.voff[d], v1 = g.voff[d + 1];
+        const T p = prev[d];
+        if constexpr (KIND == DSTK_FLOOR) {
+            T agg = INF;
+            for (uint32_t v = v0 + lane;; v += 32) {
+                if (v < v1) {
+                    uint32_t src[W], wt[W];
+                    load_lanes<W>(g.vsrc, v, src);
+                    const T m = fold_lanes<T, W, false>(src, wt, prev, INF, ovf);
+                    agg = m < agg ? m : agg;
+                }
+                if (__any_sync(FULL, agg == (T)0) || v - lane + 32 >= v1) break;
+            }
+            agg = warp_min_t(agg);
+            if (lane == 0 && agg != INF) {
+                T cand;
+                bool ok = true;
+                if constexpr (VT::U32) {
+                    const uint64_t cc = (uint64_t)agg + (uint64_t)inc;
+                    ok = cc < 0xffffffffull;
+                    if (!ok) ovf = 1;
+                    cand = (T)cc;
+                } else {
+                    cand = agg + (T)inc;
+                }
+                if (ok && cand < p) {
+                    nxt[d] = cand;
+                    atomicOr(&obits[d >> 5], 1u << (d & 31));
+                }
+            }
+        } else {
+            bool hit = false;
+            for (uint32_t v = v0 + lane;; v += 32) {
+                if (v < v1) {
+                    uint32_t src[W];
+                    load_lanes<W>(g.vsrc, v, src);
+#pragma unroll
+                    for (int l = 0; l < W; ++l)
+                        hit |= src[l] != WG_NO_LANE && in_prev_frontier(src[l]);
+                }
+                if (__any_sync(FULL, hit) || v - lane + 32 >= v1) break;
+            }
+            hit = __any_sync(FULL, hit);
+            if (lane == 0 && hit) {
+                const T level = (T)(b.level_base + (int64_t)(it - 1) * inc);
+                if constexpr (VT::U32) {
+                    const uint64_t cc = (uint64_t)level + (uint64_t)inc;
+                    if (cc >= 0xffffffffull) ovf = 1;
+                    else {
+                        nxt[d] = (T)cc;
+                        atomicOr(&obits[d >> 5], 1u << (d & 31));
+                    }
+                } else {
+                    nxt[d] = level + (T)inc;
+                    atomicOr(&obits[d >> 5], 1u << (d & 31));
+                }
+            }
+        }
+    }
+    if (ovf) out->overflow = 1;
 }
 
 // One dense-pull chunk after its gathers were issued: destinations, segment

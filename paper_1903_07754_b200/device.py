@@ -122,6 +122,7 @@ class DeviceGraph:
         # every index length equals the out-degree (WG_GRAPH_LENS_ARE_DEGREES)
         self.lens_are_degrees = bool(lens_are_degrees)
         self.vw8 = vw8  # byte copy of vw when every weight <= 255 (the dense pull streams it)
+        self.voff = None  # [n+1] per-destination vector offsets (ensure_voff; destination-major pulls)
         self._struct = None
 
     def narrow_weights(self, stream=None) -> bool:
@@ -130,7 +131,10 @@ class DeviceGraph:
         if self.vw is None or self.nvec == 0:
             return False
         lanes = self.nvec * self.width
-        buf = torch.empty(lanes + 64, dtype=torch.uint8, device=self.vw.device)  # TMA tail slack
+        buf = getattr(self, "_vw8_buf", None)  # reused across re-uploads (stable loop-graph pointers)
+        if buf is None or buf.numel() != lanes + 64:
+            buf = torch.empty(lanes + 64, dtype=torch.uint8, device=self.vw.device)  # TMA tail slack
+            self._vw8_buf = buf
         fits = ctypes.c_int(0)
         check(_lib.load().wg_narrow_weights(ctypes.byref(self.struct()), _ptr(buf), ctypes.byref(fits),
                                             _lib.stream_ptr(stream)))
@@ -287,6 +291,8 @@ class DeviceGraph:
                              + ", ".join(k for k, b in _INGEST_FLAGS.items() if bad & b))
         g.lens_are_degrees = not (bits & _lib.WG_INGEST_LENS_DIFFER)
         g._struct = None
+        if g.voff is not None:
+            g.ensure_voff(comp, refresh=True)
         g._degrees_src = degrees  # the out-degrees this graph holds (engine._with_degrees)
         g.vw8 = None
         if weighted:
@@ -579,8 +585,33 @@ class DeviceGraph:
                                    _ptr(self.vsrc), _ptr(self.vdst), _ptr(self.vw), _ptr(self.idx_off),
                                    _ptr(self.idx_pos), _ptr(self.outdeg),
                                    _lib.WG_GRAPH_LENS_ARE_DEGREES if self.lens_are_degrees else 0,
-                                   _ptr(self.vw8))
+                                   _ptr(self.vw8), _ptr(self.voff))
         return self._struct
+
+    def ensure_voff(self, stream=None, refresh: bool = False):
+        """Per-destination vector offsets (wg_vector_offsets_from_dst), kept
+        resident for the destination-major dense pulls (WG_DST_MAJOR=0
+        disables them)."""
+        if os.environ.get("WG_DST_MAJOR", "1") == "0":
+            if self.voff is not None:
+                self.voff = None
+                self._struct = None
+            return None
+        if self.voff is not None and not refresh:
+            return self.voff
+        torch = _torch()
+        if self.voff is None or self.voff.numel() != self.n + 1:
+            self.voff = torch.empty(self.n + 1, dtype=torch.int32, device=self.vdst.device)
+        self._struct = None
+        check(_lib.load().wg_vector_offsets_from_dst(ctypes.byref(self.struct()), _ptr(self.voff),
+                                                     _lib.stream_ptr(stream)))
+        return self.voff
+
+    def signature(self) -> tuple:
+        """Every field of the C struct: a loop graph captured for one
+        signature must not be replayed after any of them changed."""
+        st = self.struct()
+        return tuple(getattr(st, f) for f, _ in WgGraph._fields_)
 
     def weighted(self) -> bool:
         return self.vw is not None
@@ -810,6 +841,8 @@ class DeviceLoop:
         self.gbits_alt = torch.zeros(max(gwords, 1), dtype=torch.int32, device=dev) if self.fused else None
         self.glist_alt = torch.empty(max(groups, 1), dtype=torch.int32, device=dev) if self.fused else None
         self.bcount = torch.empty(max(nbc, 1), dtype=torch.int64, device=dev)
+        g.ensure_voff()
+        self.work = torch.empty(n, dtype=torch.int32, device=dev)
         self.recs = torch.zeros(self.ring * REC_U64, dtype=torch.int64, device=dev)
         self.ctrl = torch.zeros(4, dtype=torch.int64, device=dev)
         self.host_recs = torch.zeros(self.ring * REC_U64, dtype=torch.int64).pin_memory()
@@ -823,6 +856,7 @@ class DeviceLoop:
         b.gbits, b.glist, b.bcount = _ptr(self.gbits), _ptr(self.glist), _ptr(self.bcount)
         b.gbits_alt, b.glist_alt = _ptr(self.gbits_alt), _ptr(self.glist_alt)
         b.recs, b.ctrl, b.ring = _ptr(self.recs), _ptr(self.ctrl), self.ring
+        b.work = _ptr(self.work)
         self.bufs = b
         self.graph_cache = {}
         self._level_base = 0
@@ -879,7 +913,7 @@ class DeviceLoop:
 
     def _graph_for(self, p: WgRunParams, stream=None):
         key = (p.val_type, p.shift, p.kern.filter_unvisited, p.kern.use_weight, p.kern.apply_increment,
-               p.kern.sentinel, p.wedge_limit, p.flags, p.level_base)
+               p.kern.sentinel, p.wedge_limit, p.flags, p.level_base, self.g.signature())
         exe = self.graph_cache.get(key)
         if exe is None:
             q = WgRunParams()
@@ -890,6 +924,10 @@ class DeviceLoop:
                                              ctypes.byref(q), _lib.stream_ptr(stream))
             if not exe:
                 raise _lib.WedgeError(_lib.WG_ECUDA, L.wg_last_error().decode())
+            if len(self.graph_cache) >= 8:  # keep a few (the stream is ordered: no replay in flight reads it)
+                old = self.graph_cache.pop(next(iter(self.graph_cache)))
+                _torch().cuda.current_stream().synchronize()
+                L.wg_run_graph_destroy(old)
             self.graph_cache[key] = exe
         return exe
 
