@@ -307,29 +307,27 @@ int launch_pull(const LoopCtx &c, const wg_graph *g, const PullBufs &pb, int val
     if (only) handles = 1 << only;
     const bool want_full = only == 0 || only == MODE_FULL;
     if (want_full && (c.forced_mode == 0 || c.forced_mode == MODE_FULL)) {
-      if (pb.dst_major) {
+      if (pb.dst_major) {  // bottom-up kind: returns at once until the visited set is large (dst_major_active)
         using DstFn = void (*)(LoopCtx, wg_graph, PullBufs, int64_t, int64_t);
-        DstFn fd = nullptr, fh = nullptr;
+        DstFn fd = nullptr;
         const bool u32 = val_type == WG_VAL_U32;
-#define WG_PICK_DST(KIND)                                                                                    \
-    switch (g->width) {                                                                                      \
-        case 1: fd = u32 ? dense_dst_kernel<uint32_t, 1, KIND> : dense_dst_kernel<int64_t, 1, KIND>;         \
-                fh = u32 ? dense_heavy_kernel<uint32_t, 1, KIND> : dense_heavy_kernel<int64_t, 1, KIND>; break; \
-        case 2: fd = u32 ? dense_dst_kernel<uint32_t, 2, KIND> : dense_dst_kernel<int64_t, 2, KIND>;         \
-                fh = u32 ? dense_heavy_kernel<uint32_t, 2, KIND> : dense_heavy_kernel<int64_t, 2, KIND>; break; \
-        case 4: fd = u32 ? dense_dst_kernel<uint32_t, 4, KIND> : dense_dst_kernel<int64_t, 4, KIND>;         \
-                fh = u32 ? dense_heavy_kernel<uint32_t, 4, KIND> : dense_heavy_kernel<int64_t, 4, KIND>; break; \
-        case 8: fd = u32 ? dense_dst_kernel<uint32_t, 8, KIND> : dense_dst_kernel<int64_t, 8, KIND>;         \
-                fh = u32 ? dense_heavy_kernel<uint32_t, 8, KIND> : dense_heavy_kernel<int64_t, 8, KIND>; break; \
+#define WG_PICK_DST(KIND)                                                                          \
+    switch (g->width) {                                                                            \
+        case 1: fd = u32 ? dense_dst_kernel<uint32_t, 1, KIND> : dense_dst_kernel<int64_t, 1, KIND>; break; \
+        case 2: fd = u32 ? dense_dst_kernel<uint32_t, 2, KIND> : dense_dst_kernel<int64_t, 2, KIND>; break; \
+        case 4: fd = u32 ? dense_dst_kernel<uint32_t, 4, KIND> : dense_dst_kernel<int64_t, 4, KIND>; break; \
+        case 8: fd = u32 ? dense_dst_kernel<uint32_t, 8, KIND> : dense_dst_kernel<int64_t, 8, KIND>; break; \
     }
         if (filter) { WG_PICK_DST(DSTK_BOTTOM_UP) } else { WG_PICK_DST(DSTK_FLOOR) }
 #undef WG_PICK_DST
-        WG_REQUIRE(fd && fh, "no destination-major pull for width %u", g->width);
-        fd<<<grid_for(g->n ? g->n : 1, 256, 8), 256, 0, s>>>(c, *g, pb, k->apply_increment, k->sentinel);
-        fh<<<grid_for(g->n ? g->n : 1, 256 * 64, 8), 256, 0, s>>>(c, *g, pb, k->apply_increment, k->sentinel);
-        ::wg::count_launch(2);
+        WG_REQUIRE(fd, "no destination-major pull for width %u", g->width);
+        // one full wave of resident blocks (grid-stride over destinations)
+        fd<<<persistent_grid(fd, 256, ((uint64_t)g->n + 255) / 256), 256, 0, s>>>(c, *g, pb, k->apply_increment,
+                                                                                k->sentinel);
+        ::wg::count_launch();
         WG_CHECK_LAUNCH("pull (dense, destination-major)");
-      } else {
+      }
+      if (!pb.dst_major || filter) {  // the vector-parallel kernels (they return when dense_dst_kernel ran)
         if (pb.ident && !weight && !filter) {  // iteration 1 of an identity-initialised run
             using IdentFn = void (*)(LoopCtx, wg_graph, PullBufs, int64_t, int64_t);
             IdentFn fi = nullptr;
@@ -399,12 +397,17 @@ int launch_pull(const LoopCtx &c, const wg_graph *g, const PullBufs &pb, int val
             fb.fpref[i] = pb.fpref[i];
             fb.tstart[i] = pb.tstart[i];
         }
+        fb.dst_major = pb.dst_major;
+        fb.dst_bottom_up = filter ? 1u : 0u;
         const uint64_t nb = fb_blocks(g->n ? g->n : 1);
         const uint64_t *off = lens_are_degrees(g) ? nullptr : g->idx_off;
-        loop_frontier_count_kernel<<<(unsigned)nb, CB_THREADS, 0, s>>>(c, fb, g->n, off, g->outdeg,
-                                                                      pb.bcount, pb.ticket);
+        if (!(pb.dst_major && !filter)) {  // a floor-kind destination-major pull always counts its own frontier
+            loop_frontier_count_kernel<<<(unsigned)nb, CB_THREADS, 0, s>>>(c, fb, g->n, off, g->outdeg,
+                                                                          pb.bcount, pb.ticket);
+            ::wg::count_launch();
+        }
         loop_frontier_list_kernel<<<(unsigned)nb, CB_THREADS, 0, s>>>(c, fb, g->n, off, g->outdeg, pb.bcount);
-        ::wg::count_launch(2);
+        ::wg::count_launch();
         WG_CHECK_LAUNCH("dense frontier compaction");
         if (slot) {  // a Wedge iteration's pull (below) is timed as a pull again
             timer_end(timer, *slot, s);
@@ -697,6 +700,8 @@ int wg_run_init(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p,
     WG_CUDA(cudaMemsetAsync(b->fbits[1], 0, words * 4, s));
     WG_CUDA(cudaMemsetAsync(b->gbits, 0, ((groups + 31) >> 5) * 4, s));
     if (b->gbits_alt) WG_CUDA(cudaMemsetAsync(b->gbits_alt, 0, ((groups + 31) >> 5) * 4, s));
+    // the destination-major pulls' per-chunk frontier counters (zeroed again by each pull's last block)
+    if (b->work) WG_CUDA(cudaMemsetAsync(b->work, 0, 4 * sizeof(uint64_t) * fb_blocks(g->n ? g->n : 1), s));
     if (g->n == 0) return WG_OK;
     WG_CUDA(cudaMemsetAsync(bcount_ticket(g, p->shift, b->bcount), 0, sizeof(unsigned), s));
     return launch_frontier_compaction(g, d_init_words, b->bcount, bcount_ticket(g, p->shift, b->bcount),

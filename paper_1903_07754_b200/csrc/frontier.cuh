@@ -182,6 +182,59 @@ __device__ __forceinline__ void chunk_counts(const uint32_t *words, uint64_t nbi
     es = warp_sum(es);
 }
 
+// End of a count pass (every block calls it): the LAST block to arrive
+// (atomic ticket) turns the per-chunk totals -- 4 counters per chunk: nz
+// members, their index entries, zero-degree members, out-degree sum -- into
+// exclusive prefixes in `prefix` (the list pass's starting points), writes
+// the record's counts and decides whether the ordered list is needed at all:
+// after a dense pull whose output frontier gates the next iteration to
+// FullScan again, nothing consumes it (record reserved[2] = 1).  totals may
+// alias prefix; zero_totals clears them after reading (atomic accumulators).
+__device__ __forceinline__ void count_epilogue(uint64_t B, uint64_t *totals, uint64_t *prefix, bool zero_totals,
+                                               unsigned *counter, wg_iter_rec *rec, int keep_list, uint64_t edges,
+                                               uint64_t wedge_limit) {
+    __shared__ uint64_t sm[33];
+    __shared__ bool s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const uint64_t per = (B + blockDim.x - 1) / blockDim.x;
+    const uint64_t b0 = threadIdx.x * per, b1 = b0 + per < B ? b0 + per : B;
+    uint64_t loc[3] = {0, 0, 0}, les = 0;
+    for (uint64_t b = b0; b < b1; ++b) {
+        const volatile uint64_t *q = totals + 4 * b;
+        loc[0] += q[0]; loc[1] += q[1]; loc[2] += q[2]; les += q[3];
+    }
+    uint64_t base[3], tot[3];
+    for (int f = 0; f < 3; ++f) base[f] = block_exclusive_sum(loc[f], sm, &tot[f]);
+    const uint64_t es_all = block_sum(les, sm);
+    for (uint64_t b = b0; b < b1; ++b) {
+        volatile uint64_t *q = totals + 4 * b;
+        volatile uint64_t *o = prefix + 4 * b;
+        for (int f = 0; f < 3; ++f) {
+            const uint64_t v = q[f];
+            o[f] = base[f];
+            base[f] += v;
+        }
+        if (zero_totals) {
+            q[0] = 0; q[1] = 0; q[2] = 0; q[3] = 0;
+        }
+    }
+    if (threadIdx.x == 0) {
+        rec->nz_packed = (tot[0] << 32) | tot[1];
+        rec->z_count = tot[2];
+        rec->frontier_out = tot[0] + tot[2];
+        rec->out_edge_sum = es_all;
+        // the list is consumed only by a Wedge iteration (or the caller)
+        const bool wedge_next = es_all > 0 && edges > 0 && es_all < wedge_limit;
+        rec->reserved[2] = (keep_list || wedge_next) ? 0 : 1;
+        *counter = 0;
+    }
+}
+
 // keep_list: 1 = always build the list; 0 = decide from the next gate
 // (edges, wedge_limit as in ctx_mode).  counter: zero-initialised ticket,
 // reset by the last block.
@@ -190,8 +243,6 @@ __device__ __forceinline__ void frontier_count_body(const uint32_t *words, uint6
                                                     uint64_t *bcount, unsigned *counter, wg_iter_rec *rec,
                                                     int keep_list, uint64_t edges, uint64_t wedge_limit) {
     __shared__ uint64_t s_w[4][CB_THREADS / 32];
-    __shared__ uint64_t sm[33];
-    __shared__ bool s_last;
     const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
     uint64_t nz, ent, z, es;
     chunk_counts(words, nbits, (uint64_t)blockIdx.x * FB_WORDS + (uint64_t)warp * 32, idx_off, outdeg, nz, ent,
@@ -205,42 +256,7 @@ __device__ __forceinline__ void frontier_count_body(const uint32_t *words, uint6
         for (int w = 0; w < CB_THREADS / 32; ++w) t += s_w[threadIdx.x][w];
         bcount[4ull * blockIdx.x + threadIdx.x] = t;
     }
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    // last block: exclusive prefixes of the per-block totals, in place
-    const uint64_t B = gridDim.x;
-    const uint64_t per = (B + blockDim.x - 1) / blockDim.x;
-    const uint64_t b0 = threadIdx.x * per, b1 = b0 + per < B ? b0 + per : B;
-    uint64_t loc[3] = {0, 0, 0}, les = 0;
-    for (uint64_t b = b0; b < b1; ++b) {
-        const volatile uint64_t *q = bcount + 4 * b;
-        loc[0] += q[0]; loc[1] += q[1]; loc[2] += q[2]; les += q[3];
-    }
-    uint64_t base[3], tot[3];
-    for (int f = 0; f < 3; ++f) base[f] = block_exclusive_sum(loc[f], sm, &tot[f]);
-    const uint64_t es_all = block_sum(les, sm);
-    for (uint64_t b = b0; b < b1; ++b) {
-        volatile uint64_t *q = bcount + 4 * b;
-        for (int f = 0; f < 3; ++f) {
-            const uint64_t v = q[f];
-            q[f] = base[f];
-            base[f] += v;
-        }
-    }
-    if (threadIdx.x == 0) {
-        rec->nz_packed = (tot[0] << 32) | tot[1];
-        rec->z_count = tot[2];
-        rec->frontier_out = tot[0] + tot[2];
-        rec->out_edge_sum = es_all;
-        // the list is consumed only by a Wedge iteration (or the caller)
-        const bool wedge_next = es_all > 0 && edges > 0 && es_all < wedge_limit;
-        rec->reserved[2] = (keep_list || wedge_next) ? 0 : 1;
-        *counter = 0;
-    }
+    count_epilogue(gridDim.x, bcount, bcount, false, counter, rec, keep_list, edges, wedge_limit);
 }
 
 __device__ __forceinline__ void frontier_list_body(const uint32_t *words, uint64_t nbits,
@@ -317,6 +333,7 @@ __global__ void __launch_bounds__(CB_THREADS) frontier_list_kernel(const uint32_
 // bitmap (gated on the device mode).
 struct FrontierBufs {
     uint32_t *fbits[2], *fvert[2], *fpref[2], *tstart[2];
+    uint32_t dst_major, dst_bottom_up;  // a destination-major pull may have counted the frontier already
 };
 
 __global__ void __launch_bounds__(CB_THREADS) loop_frontier_count_kernel(LoopCtx c, FrontierBufs f, uint64_t n,
@@ -325,6 +342,7 @@ __global__ void __launch_bounds__(CB_THREADS) loop_frontier_count_kernel(LoopCtx
                                                                          uint64_t *bcount, unsigned *counter) {
     const uint64_t it = ctx_iter(c);
     if (ctx_mode(c, it) != MODE_FULL) return;
+    if (dst_major_active(c, it, n, f.dst_major, f.dst_bottom_up != 0)) return;  // counted by dense_dst_kernel
     frontier_count_body((it & 1) ? f.fbits[1] : f.fbits[0], n, idx_off, outdeg, bcount, counter, ctx_out(c, it),
                         c.keep_lists, c.edges, c.wedge_limit);
 }

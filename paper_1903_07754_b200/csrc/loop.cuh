@@ -49,4 +49,22 @@ __device__ __forceinline__ const wg_iter_rec *ctx_in(const LoopCtx &c, uint64_t 
     return &c.recs[(it - 1) % c.ring];
 }
 
+// Destination-major dense pulls (pull.cuh dense_dst_kernel): always for the
+// floor (CC-like) kind; for the bottom-up (BFS) kind only once the visited
+// set is large (record reserved[4]: members of the initial and every
+// produced frontier so far) -- an early dense pull of a thin frontier finds
+// few hits and scans whole in-lists, which the vector-parallel kernels do at
+// higher memory parallelism.
+constexpr uint64_t DST_BU_VISITED_DIV = 16;
+
+__device__ __forceinline__ bool dst_major_active(const LoopCtx &c, uint64_t it, uint64_t n, uint32_t dst_major,
+                                                 bool bottom_up) {
+    if (!dst_major) return false;
+    if (!bottom_up) return true;
+    const wg_iter_rec *in = ctx_in(c, it);
+    const uint64_t seen = it == 1 ? *(volatile const uint64_t *)&in->frontier_out
+                                  : *(volatile const uint64_t *)&in->reserved[4];
+    return seen * DST_BU_VISITED_DIV >= n;
+}
+
 }  // namespace wg

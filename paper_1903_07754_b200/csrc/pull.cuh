@@ -667,6 +667,7 @@ __global__ void __launch_bounds__(256) bottom_up_pull_kernel(LoopCtx c, wg_graph
     using VT = ValTraits<T>;
     const uint64_t it = ctx_iter(c);
     if (ctx_mode(c, it) != MODE_FULL || it < b.floor_from || it < 2) return;
+    if (dst_major_active(c, it, b.n, b.dst_major, true)) return;  // dense_dst_kernel's iteration
     wg_iter_rec *out = ctx_out(c, it);
     const T *__restrict__ prev = (const T *)(((it - 1) & 1) ? b.vals[1] : b.vals[0]);
     T *__restrict__ nxt = (T *)((it & 1) ? b.vals[1] : b.vals[0]);
@@ -745,19 +746,24 @@ __global__ void __launch_bounds__(256) bottom_up_pull_kernel(LoopCtx c, wg_graph
 //    all but 0.34M decided by that probe.
 //  * BOTTOM-UP (WG_RUN_FIRST_HIT, filtered, unweighted: level-synchronous
 //    BFS).  Visited destinations keep prev[d] and count as untouched
-//    (_kernels.pyx:77-80); an unvisited destination tests its sources' bits in
-//    the previous frontier -- every finite in-neighbour of it sits there --
-//    and stops at the first hit (cand = level + inc).
+//    (_kernels.pyx:77-80); an unvisited destination tests its sources'
+//    membership in the previous frontier -- every finite in-neighbour of it
+//    sits there -- and stops at the first hit (cand = level + inc).
 //
-// Destinations with more than DST_LIGHT vectors that are still undecided go
-// to a work list (b.work, count in the record's reserved[4]) and are finished
-// by dense_heavy_kernel, a warp each.  Values: every destination's nxt[d] is
-// written (prev[d] or its improvement), so no buffer sync is needed after a
-// dense iteration (end_of_iteration); next-frontier bits are set one warp
-// word at a time (a warp owns 32 consecutive destinations).  Results and
+// Destinations with more than DST_LIGHT vectors that are still undecided are
+// finished by their whole warp (lanes strided over the vectors, early exit
+// by vote).  Every destination's nxt[d] is written (prev[d] or its
+// improvement), so no buffer sync is needed after a dense iteration
+// (end_of_iteration); a warp owns 32 consecutive destinations = one
+// next-frontier word.  The same pass counts the produced frontier per
+// 8192-vertex chunk (members with / without out-edges, their index entries
+// and out-degree sum: atomics of one warp each into b.work) and the last
+// block turns those into the record and the list pass's prefixes
+// (count_epilogue) -- no separate count pass over the bitmap.  Results and
 // counters are those of the reference's full scan (every vector touched;
 // bottom-up: the vectors of unvisited destinations).
 constexpr uint32_t DST_LIGHT = 8;  // vectors walked by one thread
+constexpr int DST_K = 4;           // destinations per thread in flight (one warp = DST_K words)
 constexpr int DSTK_FLOOR = 0, DSTK_BOTTOM_UP = 1;
 
 template <typename T, int W, int KIND>
@@ -766,22 +772,24 @@ __global__ void __launch_bounds__(256) dense_dst_kernel(LoopCtx c, wg_graph g, P
     using VT = ValTraits<T>;
     const uint64_t it = ctx_iter(c);
     if (ctx_mode(c, it) != MODE_FULL) return;
+    if (!dst_major_active(c, it, b.n, b.dst_major, KIND == DSTK_BOTTOM_UP)) return;
     wg_iter_rec *out = ctx_out(c, it);
     const T *__restrict__ prev = (const T *)(((it - 1) & 1) ? b.vals[1] : b.vals[0]);
     T *__restrict__ nxt = (T *)((it & 1) ? b.vals[1] : b.vals[0]);
     uint32_t *__restrict__ obits = ((it & 1) ? b.fbits[1] : b.fbits[0]);
     const uint32_t *__restrict__ inbits = (((it - 1) & 1) ? b.fbits[1] : b.fbits[0]);
     const uint32_t *__restrict__ voff = g.voff;
+    unsigned long long *totals = (unsigned long long *)b.work;  // 4 counters per 8192-vertex chunk
     const T INF = VT::inf(sentinel);
+    const bool lens_deg = (g.flags & WG_GRAPH_LENS_ARE_DEGREES) != 0;
     // iteration 1 reads no bitmap (the initial frontier lives in the caller's
     // words): a level-synchronous run's finite vertices ARE that frontier
     const auto in_prev_frontier = [&](uint32_t v) -> bool {
         return it == 1 ? prev[v] != INF : ((inbits[v >> 5] >> (v & 31)) & 1u) != 0u;
     };
     const bool exact_first = KIND == DSTK_FLOOR && b.ident && it == 1;  // identity values: lane 0 is the min
-    // bottom-up candidate: the level after the previous frontier's
     uint32_t ovf = 0;
-    T bu_cand = INF;
+    T bu_cand = INF;  // bottom-up: the level after the previous frontier's
     if constexpr (KIND == DSTK_BOTTOM_UP) {
         const T level = (T)(b.level_base + (int64_t)(it - 1) * inc);
         if constexpr (VT::U32) {
@@ -792,78 +800,166 @@ __global__ void __launch_bounds__(256) dense_dst_kernel(LoopCtx c, wg_graph g, P
             bu_cand = level + (T)inc;
         }
     }
+    const unsigned lane = lane_id();
     uint64_t touched = 0;
     const uint64_t n = g.n;
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;  // a multiple of 32: warps stay word-aligned
-    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
-        const uint64_t d = base + threadIdx.x;
-        bool upd = false;
-        if (d < n) {
-            const T p = prev[d];
-            const uint32_t v0 = voff[d], v1 = voff[d + 1];
-            T res = p;
+    const uint64_t span = 32ull * DST_K;  // destinations per warp step, word-aligned
+    const uint64_t warp0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t wb = warp0 * span; wb < n; wb += nwarps * span) {
+        T p[DST_K], agg[DST_K];
+        uint32_t v0[DST_K], v1[DST_K];
+        bool need[DST_K];
+        // (a) prev[d] and d's vector range, DST_K destinations in flight
+#pragma unroll
+        for (int k = 0; k < DST_K; ++k) {
+            const uint64_t d = wb + 32 * k + lane;
+            const bool ok = d < n;
+            p[k] = ok ? prev[d] : (T)0;
+            v0[k] = ok ? voff[d] : 0u;
+            v1[k] = ok ? voff[d + 1] : 0u;
+        }
+        // (b) FLOOR: the first lane of every destination not at the floor;
+        // the out-degree of every destination that may join the frontier
+        // (read now, consumed by the counts at the end of the step)
+        uint32_t deg[DST_K];
+#pragma unroll
+        for (int k = 0; k < DST_K; ++k) {
+            need[k] = v1[k] > v0[k] && (KIND == DSTK_FLOOR ? p[k] != (T)0 : p[k] == INF);
+            agg[k] = INF;
+            deg[k] = need[k] ? g.outdeg[wb + 32 * k + lane] : 0u;
+        }
+        if constexpr (KIND == DSTK_FLOOR) {
+            uint32_t s0[DST_K];
+#pragma unroll
+            for (int k = 0; k < DST_K; ++k) s0[k] = need[k] ? g.vsrc[(uint64_t)v0[k] * W] : 0u;
+#pragma unroll
+            for (int k = 0; k < DST_K; ++k)
+                if (need[k]) agg[k] = exact_first ? (T)s0[k] : prev[s0[k]];
+        } else {
+#pragma unroll
+            for (int k = 0; k < DST_K; ++k) touched += need[k] ? v1[k] - v0[k] : 0u;
+        }
+        // (c) undecided destinations: short in-lists by their thread ...
+        bool heavy[DST_K];
+#pragma unroll
+        for (int k = 0; k < DST_K; ++k) {
+            const bool undecided = need[k] && (KIND == DSTK_FLOOR ? (!exact_first && agg[k] != (T)0) : true);
+            heavy[k] = undecided && v1[k] - v0[k] > DST_LIGHT;
+            if (!undecided || heavy[k]) continue;
+            // two vectors per round trip (the second may be the next one's
+            // padding-free first: v+1 < v1 is checked)
             if constexpr (KIND == DSTK_FLOOR) {
-                if (p != (T)0 && v1 > v0) {
-                    const uint32_t s0 = g.vsrc[(uint64_t)v0 * W];
-                    T agg = exact_first ? (T)s0 : prev[s0];
-                    bool decided = exact_first || agg == (T)0;
-                    if (!decided) {
-                        if (v1 - v0 <= DST_LIGHT) {
-                            for (uint32_t v = v0; v < v1 && agg != (T)0; ++v) {
-                                uint32_t src[W], wt[W];
-                                load_lanes<W>(g.vsrc, v, src);
-                                const T m = fold_lanes<T, W, false>(src, wt, prev, INF, ovf);
-                                agg = m < agg ? m : agg;
-                            }
-                        } else {
-                            const unsigned slot = atomicAdd((unsigned *)&out->reserved[4], 1u);
-                            b.work[slot] = (uint32_t)d;
-                            agg = INF;  // finished by dense_heavy_kernel
-                        }
+                T a = agg[k];
+                for (uint32_t v = v0[k]; v < v1[k] && a != (T)0; v += 2) {
+                    uint32_t src[W], src2[W], wt[W];
+                    load_lanes<W>(g.vsrc, v, src);
+                    const bool two = v + 1 < v1[k];
+                    if (two) load_lanes<W>(g.vsrc, v + 1, src2);
+                    T m = fold_lanes<T, W, false>(src, wt, prev, INF, ovf);
+                    if (two) {
+                        const T m2 = fold_lanes<T, W, false>(src2, wt, prev, INF, ovf);
+                        m = m2 < m ? m2 : m;
                     }
-                    if (agg != INF) {
-                        T cand;
-                        bool ok = true;
-                        if constexpr (VT::U32) {
-                            const uint64_t cc = (uint64_t)agg + (uint64_t)inc;
-                            ok = cc < 0xffffffffull;
-                            if (!ok) ovf = 1;
-                            cand = (T)cc;
-                        } else {
-                            cand = agg + (T)inc;
-                        }
-                        if (ok && cand < p) {
-                            res = cand;
-                            upd = true;
-                        }
+                    a = m < a ? m : a;
+                }
+                agg[k] = a;
+            } else {
+                bool hit = false;
+                for (uint32_t v = v0[k]; v < v1[k] && !hit; v += 2) {
+                    uint32_t src[W], src2[W];
+                    load_lanes<W>(g.vsrc, v, src);
+                    const bool two = v + 1 < v1[k];
+                    if (two) load_lanes<W>(g.vsrc, v + 1, src2);
+#pragma unroll
+                    for (int l = 0; l < W; ++l) hit |= src[l] != WG_NO_LANE && in_prev_frontier(src[l]);
+                    if (two) {
+#pragma unroll
+                        for (int l = 0; l < W; ++l) hit |= src2[l] != WG_NO_LANE && in_prev_frontier(src2[l]);
                     }
                 }
-            } else {
-                if (p == INF && v1 > v0) {
-                    touched += v1 - v0;
-                    if (v1 - v0 <= DST_LIGHT) {
-                        bool hit = false;
-                        for (uint32_t v = v0; v < v1 && !hit; ++v) {
-                            uint32_t src[W];
-                            load_lanes<W>(g.vsrc, v, src);
+                agg[k] = hit ? (T)0 : INF;  // hit marker
+            }
+        }
+        // ... long ones by the whole warp, one at a time (early exit by vote)
 #pragma unroll
-                            for (int l = 0; l < W; ++l)
-                                hit |= src[l] != WG_NO_LANE && in_prev_frontier(src[l]);
+        for (int k = 0; k < DST_K; ++k) {
+            for (unsigned hv = __ballot_sync(FULL, heavy[k]); hv; hv &= hv - 1) {
+                const int j = __ffs(hv) - 1;
+                const uint32_t h0 = __shfl_sync(FULL, v0[k], j), h1 = __shfl_sync(FULL, v1[k], j);
+                T hagg = KIND == DSTK_FLOOR ? shfl_t(agg[k], j) : INF;  // FLOOR: the probe's value
+                bool hit = false;
+                for (uint32_t v = h0 + lane;; v += 32) {
+                    if (v < h1) {
+                        uint32_t src[W], wt[W];
+                        load_lanes<W>(g.vsrc, v, src);
+                        if constexpr (KIND == DSTK_FLOOR) {
+                            const T m = fold_lanes<T, W, false>(src, wt, prev, INF, ovf);
+                            hagg = m < hagg ? m : hagg;
+                        } else {
+#pragma unroll
+                            for (int l = 0; l < W; ++l) hit |= src[l] != WG_NO_LANE && in_prev_frontier(src[l]);
                         }
-                        if (hit && bu_cand != INF) {
-                            res = bu_cand;
-                            upd = true;
-                        }
-                    } else {
-                        const unsigned slot = atomicAdd((unsigned *)&out->reserved[4], 1u);
-                        b.work[slot] = (uint32_t)d;
                     }
+                    const bool done = KIND == DSTK_FLOOR ? __any_sync(FULL, hagg == (T)0) : __any_sync(FULL, hit);
+                    if (done || v - lane + 32 >= h1) break;
+                }
+                if constexpr (KIND == DSTK_FLOOR) hagg = warp_min_t(hagg);
+                else hagg = __any_sync(FULL, hit) ? (T)0 : INF;
+                if (lane == (unsigned)j) agg[k] = hagg;
+            }
+        }
+        // (d) apply: every destination's nxt[d]; bits one word per k; counts
+        uint64_t nz = 0, ent = 0, z = 0, es = 0;
+        bool any = false;
+#pragma unroll
+        for (int k = 0; k < DST_K; ++k) {
+            const uint64_t d = wb + 32 * k + lane;
+            bool upd = false;
+            T res = p[k];
+            if (d < n && agg[k] != INF) {
+                T cand = INF;
+                if constexpr (KIND == DSTK_BOTTOM_UP) {
+                    cand = bu_cand;
+                } else if constexpr (VT::U32) {
+                    const uint64_t cc = (uint64_t)agg[k] + (uint64_t)inc;
+                    if (cc >= 0xffffffffull) ovf = 1;
+                    else cand = (T)cc;
+                } else {
+                    cand = agg[k] + (T)inc;
+                }
+                if (cand != INF && cand < p[k]) {
+                    res = cand;
+                    upd = true;
                 }
             }
-            nxt[d] = res;
+            if (d < n) nxt[d] = res;
+            const unsigned word = __ballot_sync(FULL, upd);
+            if (word) {
+                any = true;
+                if (lane == 0) atomicOr(&obits[(wb >> 5) + k], word);
+                if (upd) {
+                    const uint64_t len = lens_deg ? deg[k] : g.idx_off[d + 1] - g.idx_off[d];
+                    nz += len != 0;
+                    ent += len;
+                    z += len == 0;
+                    es += deg[k];
+                }
+            }
         }
-        const unsigned word = __ballot_sync(FULL, upd);
-        if (word && lane_id() == 0) atomicOr(&obits[(base + (threadIdx.x & ~31u)) >> 5], word);
+        if (any) {  // warp-uniform: the produced frontier's counts of this 8192-vertex chunk
+            nz = warp_sum(nz);
+            ent = warp_sum(ent);
+            z = warp_sum(z);
+            es = warp_sum(es);
+            if (lane == 0) {
+                unsigned long long *t = totals + 4 * ((wb >> 5) / FB_WORDS);
+                if (nz) atomicAdd(&t[0], (unsigned long long)nz);
+                if (ent) atomicAdd(&t[1], (unsigned long long)ent);
+                if (z) atomicAdd(&t[2], (unsigned long long)z);
+                if (es) atomicAdd(&t[3], (unsigned long long)es);
+            }
+        }
     }
     if (ovf) out->overflow = 1;
     if constexpr (KIND == DSTK_FLOOR) {
@@ -871,96 +967,10 @@ __global__ void __launch_bounds__(256) dense_dst_kernel(LoopCtx c, wg_graph g, P
             atomicAdd((unsigned long long *)&out->vectors_touched, (unsigned long long)g.nvec);
     } else {
         const uint64_t t = warp_sum(touched);
-        if (lane_id() == 0 && t) atomicAdd((unsigned long long *)&out->vectors_touched, (unsigned long long)t);
+        if (lane == 0 && t) atomicAdd((unsigned long long *)&out->vectors_touched, (unsigned long long)t);
     }
-}
-
-// The work list of dense_dst_kernel: a warp per destination, lanes strided
-// over its vectors, stopping once any lane reached the floor (FLOOR) or hit
-// the previous frontier (BOTTOM-UP).
-template <typename T, int W, int KIND>
-__global__ void __launch_bounds__(256) dense_heavy_kernel(LoopCtx c, wg_graph g, PullBufs b, int64_t inc,
-                                                          int64_t sentinel) {
-    using VT = ValTraits<T>;
-    const uint64_t it = ctx_iter(c);
-    if (ctx_mode(c, it) != MODE_FULL) return;
-    wg_iter_rec *out = ctx_out(c, it);
-    const uint64_t count = *(volatile const uint64_t *)&out->reserved[4] & 0xffffffffull;
-    if (count == 0) return;
-    const T *__restrict__ prev = (const T *)(((it - 1) & 1) ? b.vals[1] : b.vals[0]);
-    T *__restrict__ nxt = (T *)((it & 1) ? b.vals[1] : b.vals[0]);
-    uint32_t *__restrict__ obits = ((it & 1) ? b.fbits[1] : b.fbits[0]);
-    const uint32_t *__restrict__ inbits = (((it - 1) & 1) ? b.fbits[1] : b.fbits[0]);
-    const T INF = VT::inf(sentinel);
-    const auto in_prev_frontier = [&](uint32_t v) -> bool {
-        return it == 1 ? prev[v] != INF : ((inbits[v >> 5] >> (v & 31)) & 1u) != 0u;
-    };
-    uint32_t ovf = 0;
-    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    const unsigned lane = lane_id();
-    for (uint64_t i = warp; i < count; i += nwarps) {
-        const uint32_t d = b.work[i];
-        const uint32_t v0 = g.voff[d], v1 = g.voff[d + 1];
-        const T p = prev[d];
-        if constexpr (KIND == DSTK_FLOOR) {
-            T agg = INF;
-            for (uint32_t v = v0 + lane;; v += 32) {
-                if (v < v1) {
-                    uint32_t src[W], wt[W];
-                    load_lanes<W>(g.vsrc, v, src);
-                    const T m = fold_lanes<T, W, false>(src, wt, prev, INF, ovf);
-                    agg = m < agg ? m : agg;
-                }
-                if (__any_sync(FULL, agg == (T)0) || v - lane + 32 >= v1) break;
-            }
-            agg = warp_min_t(agg);
-            if (lane == 0 && agg != INF) {
-                T cand;
-                bool ok = true;
-                if constexpr (VT::U32) {
-                    const uint64_t cc = (uint64_t)agg + (uint64_t)inc;
-                    ok = cc < 0xffffffffull;
-                    if (!ok) ovf = 1;
-                    cand = (T)cc;
-                } else {
-                    cand = agg + (T)inc;
-                }
-                if (ok && cand < p) {
-                    nxt[d] = cand;
-                    atomicOr(&obits[d >> 5], 1u << (d & 31));
-                }
-            }
-        } else {
-            bool hit = false;
-            for (uint32_t v = v0 + lane;; v += 32) {
-                if (v < v1) {
-                    uint32_t src[W];
-                    load_lanes<W>(g.vsrc, v, src);
-#pragma unroll
-                    for (int l = 0; l < W; ++l)
-                        hit |= src[l] != WG_NO_LANE && in_prev_frontier(src[l]);
-                }
-                if (__any_sync(FULL, hit) || v - lane + 32 >= v1) break;
-            }
-            hit = __any_sync(FULL, hit);
-            if (lane == 0 && hit) {
-                const T level = (T)(b.level_base + (int64_t)(it - 1) * inc);
-                if constexpr (VT::U32) {
-                    const uint64_t cc = (uint64_t)level + (uint64_t)inc;
-                    if (cc >= 0xffffffffull) ovf = 1;
-                    else {
-                        nxt[d] = (T)cc;
-                        atomicOr(&obits[d >> 5], 1u << (d & 31));
-                    }
-                } else {
-                    nxt[d] = level + (T)inc;
-                    atomicOr(&obits[d >> 5], 1u << (d & 31));
-                }
-            }
-        }
-    }
-    if (ovf) out->overflow = 1;
+    count_epilogue(fb_blocks(n ? n : 1), (uint64_t *)totals, b.bcount, true, b.ticket, out, c.keep_lists, c.edges,
+                   c.wedge_limit);
 }
 
 // One dense-pull chunk after its gathers were issued: destinations, segment
@@ -1031,6 +1041,7 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) pull_dense_tma_kernel(Loop
     const uint64_t it = ctx_iter(c);
     const int mode = ctx_mode(c, it);
     if (mode != MODE_FULL) return;  // wedge iterations use pull_kernel
+    if (FILTER && b.dst_major && dst_major_active(c, it, b.n, 1u, !b.floor_skip)) return;  // dense_dst_kernel's
     wg_iter_rec *out = ctx_out(c, it);
     const T *__restrict__ prev = (const T *)(((it - 1) & 1) ? b.vals[1] : b.vals[0]);
     T *__restrict__ nxt = (T *)((it & 1) ? b.vals[1] : b.vals[0]);
@@ -1452,6 +1463,10 @@ __device__ __forceinline__ void end_of_iteration(const LoopCtx &c, uint64_t it, 
             out->mode = (uint64_t)mode;
             out->frontier_out = (*(volatile uint64_t *)&out->nz_packed >> 32) + *(volatile uint64_t *)&out->z_count;
             out->active_edges = *(volatile const uint64_t *)&ctx_in(c, it)->out_edge_sum;
+            // members of the initial and every produced frontier so far (dst_major_active)
+            const wg_iter_rec *pin = ctx_in(c, it);
+            out->reserved[4] = (it == 1 ? *(volatile const uint64_t *)&pin->frontier_out
+                                        : *(volatile const uint64_t *)&pin->reserved[4]) + out->frontier_out;
         }
         uint64_t *q = (uint64_t *)&c.recs[(it + zero_ahead) % c.ring];
 #pragma unroll

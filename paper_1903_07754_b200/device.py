@@ -842,7 +842,7 @@ class DeviceLoop:
         self.glist_alt = torch.empty(max(groups, 1), dtype=torch.int32, device=dev) if self.fused else None
         self.bcount = torch.empty(max(nbc, 1), dtype=torch.int64, device=dev)
         g.ensure_voff()
-        self.work = torch.empty(n, dtype=torch.int32, device=dev)
+        self.work = torch.zeros(n + 64, dtype=torch.int32, device=dev)  # >= 8 words per 8192-vertex chunk
         self.recs = torch.zeros(self.ring * REC_U64, dtype=torch.int64, device=dev)
         self.ctrl = torch.zeros(4, dtype=torch.int64, device=dev)
         self.host_recs = torch.zeros(self.ring * REC_U64, dtype=torch.int64).pin_memory()

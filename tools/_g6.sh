@@ -1,0 +1,3 @@
+timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/g6_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/g6_pytest.log
+timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/g6_bench.json 2> gpurun_out/g6_bench.err
+timeout 600 python bench.py --workload bfs26 --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/g6_bfs26.json 2> gpurun_out/g6_bfs26.err
