@@ -335,6 +335,12 @@ int wg_run_buffer_sizes(const wg_graph *g, int shift, uint64_t *h_sizes5);
  * already written vals[0] == vals[1] == initial values. */
 int wg_run_init(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p,
                 const uint32_t *d_init_words, void *stream);
+/* wg_run_init plus both value buffers written from d_init_values ([n] values
+ * of p->val_type) -- one launch for the whole initialisation
+ * (ValueBuffers.initialize, engine.py:100; VertexFrontier.from_vertices,
+ * frontier.py:79). */
+int wg_run_seed(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p, const void *d_init_values,
+                const uint32_t *d_init_words, void *stream);
 /* Enqueue iterations [it_begin, it_begin + count) (1-based).  Each kernel
  * re-derives the gate and the converged flag on device from the previous
  * record, so iterations after convergence are no-ops.  Asynchronous. */
@@ -371,6 +377,11 @@ int wg_run_persistent(const wg_graph *g, const wg_run_bufs *b, const wg_run_para
 /* Profiling aid: record 4 %globaltimer stamps per persistent-loop iteration
  * (start, after transform, after pull, after end-of-iteration) into d_buf
  * (4*iterations uint64); pass NULL to disable. */
+/* Debug: kernel timeline of the device loop.  d_buf: [iterations][wg_debug_kernel_ids()][2]
+ * uint64 (start = earliest block start, initialise to ~0; end = latest block end, initialise
+ * to 0; %globaltimer ns); null switches it off. */
+int wg_debug_kernel_timeline(uint64_t *d_buf, uint64_t iterations);
+uint32_t wg_debug_kernel_ids(void);
 int wg_debug_phase_buffer(uint64_t *d_buf, uint64_t iterations);
 
 /* ---------------- multi-GPU exchange ----------------------- */

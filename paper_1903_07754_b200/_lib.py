@@ -83,6 +83,7 @@ EXPORTS = [
     "wg_decode_lanes", "wg_index_chunk_coded", "wg_expand_scratch_bytes", "wg_index_placed_scratch_bytes",
     "wg_index_place_begin", "wg_index_place_chunk", "wg_index_place_coded", "wg_index_place_end",
     "wg_ingest_vectors", "wg_ingest_u32", "wg_ingest_offsets", "wg_values_scan", "wg_vector_offsets_from_dst",
+    "wg_run_seed", "wg_debug_kernel_timeline", "wg_debug_kernel_ids",
 ]
 
 _LIB = None
@@ -201,6 +202,9 @@ def load(path: os.PathLike | str | None = None):
         "wg_ingest_offsets": (ctypes.c_int, [c_u32, c_vp, c_u64, c_vp, c_vp, c_vp]),
         "wg_values_scan": (ctypes.c_int, [c_u32, c_vp, c_i64, c_vp, c_vp, c_vp]),
         "wg_vector_offsets_from_dst": (ctypes.c_int, [G, c_vp, c_vp]),
+        "wg_run_seed": (ctypes.c_int, [G, B, P, c_vp, c_vp, c_vp]),
+        "wg_debug_kernel_timeline": (ctypes.c_int, [c_vp, c_u64]),
+        "wg_debug_kernel_ids": (c_u32, []),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

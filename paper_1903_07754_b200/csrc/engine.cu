@@ -581,6 +581,7 @@ namespace {
 __global__ void loop_step_kernel(cudaGraphConditionalHandle h, uint64_t *ctrl, const wg_iter_rec *recs,
                                  uint32_t ring) {
     const uint64_t it = ctrl[0] + 1;
+    WG_KTS(it, KTS_STEP);
     if (it > ctrl[1]) {  // the persistent sparse loop already reached the launch limit
         cudaGraphSetConditional(h, 0u);
         return;
@@ -592,12 +593,25 @@ __global__ void loop_step_kernel(cudaGraphConditionalHandle h, uint64_t *ctrl, c
 }
 __global__ void set_limit_kernel(uint64_t *ctrl, uint64_t limit) { ctrl[1] = limit; }
 
+// Gate of the persistent sparse loop (its cooperative launch costs several
+// microseconds even when it returns at once, so it sits behind an IF node).
+// It also takes destination-major dense iterations (dense_ok: unweighted
+// run with a work list) -- sparse_loop_kernel runs those as phases too.
+__global__ void sparse_gate_kernel(LoopCtx c, cudaGraphConditionalHandle h, uint64_t ngroups, uint32_t dense_ok,
+                                   uint64_t n, int bottom_up) {
+    const uint64_t it = ctx_iter(c);
+    WG_KTS(it, KTS_SPARSE_GATE);
+    const bool dense = dense_ok && ctx_mode(c, it) == MODE_FULL && dst_major_active(c, it, n, 1u, bottom_up != 0);
+    cudaGraphSetConditional(h, (dense || sparse_wedge(c, it, ngroups)) ? 1u : 0u);
+}
+
 // Device-side gate of the graph body: FullScan, Wedge through the ordered
 // group list, or Wedge through the sparse (append) path when the transform
 // work is small against the group bitmap (no bitmap scans are worth it).
 __global__ void decide_kernel(LoopCtx c, cudaGraphConditionalHandle hf, cudaGraphConditionalHandle hs,
                               cudaGraphConditionalHandle hp, uint64_t ngroups, int has_entries) {
     const uint64_t it = ctx_iter(c);
+    WG_KTS(it, KTS_DECIDE);
     const int mode = ctx_mode(c, it);
     int variant = 0;
     if (mode == MODE_FULL) {
@@ -666,6 +680,14 @@ static PullBufs pull_bufs(const wg_graph *g, const wg_run_bufs *b, const wg_run_
     pb.dst_major = g->voff && b->work && !p->kern.use_weight &&
                            ((pb.floor_skip && !p->kern.filter_unvisited) || (pb.first_hit && p->kern.filter_unvisited))
                        ? 1u : 0u;
+    {
+        // the floor kind only: the bottom-up pulls of large BFS graphs run
+        // faster as their own kernel (more registers, no persistent-loop spills:
+        // BFS s26 iteration 3 1.31 vs 1.76 ms); WG_LOOP_DENSE=0/1 overrides
+        const char *e = getenv("WG_LOOP_DENSE");
+        const bool want = e ? e[0] != '0' : !p->kern.filter_unvisited;
+        pb.loop_dense = pb.dst_major && want ? 1u : 0u;
+    }
     return pb;
 }
 
@@ -685,28 +707,96 @@ static int check_run(const wg_graph *g, const wg_run_bufs *b, const wg_run_param
     return WG_OK;
 }
 
-int wg_run_init(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p,
+}  // extern "C" (reopened below)
+
+namespace {
+// One launch for the whole run initialisation: zero ranges (uint32 words),
+// the control words, and both value buffers from the initial values.
+struct InitRanges {
+    uint32_t *ptr[8];
+    uint64_t words[8];
+    int count;
+    uint64_t *ctrl;
+    const void *init;  // [n] values of val_type, or null
+    void *vals[2];
+    uint64_t n, vbytes;
+};
+
+__global__ void run_init_kernel(InitRanges r) {
+    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+    if (tid == 0) {
+        r.ctrl[0] = 0;
+        r.ctrl[1] = ~0ull;  // no iteration limit
+        r.ctrl[2] = 0;
+        r.ctrl[3] = 0;
+    }
+    for (int k = 0; k < r.count; ++k)
+        for (uint64_t i = tid; i < r.words[k]; i += nth) r.ptr[k][i] = 0u;
+    if (r.init) {
+        if (r.vbytes == 4) {
+            const uint32_t *src = (const uint32_t *)r.init;
+            for (uint64_t i = tid; i < r.n; i += nth) {
+                const uint32_t v = src[i];
+                ((uint32_t *)r.vals[0])[i] = v;
+                ((uint32_t *)r.vals[1])[i] = v;
+            }
+        } else {
+            const uint64_t *src = (const uint64_t *)r.init;
+            for (uint64_t i = tid; i < r.n; i += nth) {
+                const uint64_t v = src[i];
+                ((uint64_t *)r.vals[0])[i] = v;
+                ((uint64_t *)r.vals[1])[i] = v;
+            }
+        }
+    }
+}
+}  // namespace
+
+extern "C" {
+
+int wg_run_seed(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p, const void *d_init_values,
                 const uint32_t *d_init_words, void *stream) {
     int rc = check_run(g, b, p);
     if (rc) return rc;
     WG_REQUIRE(d_init_words, "null initial frontier");
     cudaStream_t s = as_stream(stream);
-    uint64_t words = ((uint64_t)g->n + 31) >> 5;
-    uint64_t groups = groups_of(g, p->shift);
-    WG_CUDA(cudaMemsetAsync(b->recs, 0, sizeof(wg_iter_rec) * b->ring, s));
-    WG_CUDA(cudaMemsetAsync(b->ctrl, 0, 4 * sizeof(uint64_t), s));
-    WG_CUDA(cudaMemsetAsync(b->ctrl + 1, 0xff, sizeof(uint64_t), s));  // no iteration limit
-    WG_CUDA(cudaMemsetAsync(b->fbits[0], 0, words * 4, s));
-    WG_CUDA(cudaMemsetAsync(b->fbits[1], 0, words * 4, s));
-    WG_CUDA(cudaMemsetAsync(b->gbits, 0, ((groups + 31) >> 5) * 4, s));
-    if (b->gbits_alt) WG_CUDA(cudaMemsetAsync(b->gbits_alt, 0, ((groups + 31) >> 5) * 4, s));
+    const uint64_t words = ((uint64_t)g->n + 31) >> 5;
+    const uint64_t gwords = (groups_of(g, p->shift) + 31) >> 5;
+    InitRanges r{};
+    auto add = [&](void *ptr, uint64_t w) {
+        if (ptr && w) {
+            r.ptr[r.count] = (uint32_t *)ptr;
+            r.words[r.count] = w;
+            ++r.count;
+        }
+    };
+    add(b->recs, sizeof(wg_iter_rec) * b->ring / 4);
+    add(b->fbits[0], words);
+    add(b->fbits[1], words);
+    add(b->gbits, gwords);
+    add(b->gbits_alt, gwords);
     // the destination-major pulls' per-chunk frontier counters (zeroed again by each pull's last block)
-    if (b->work) WG_CUDA(cudaMemsetAsync(b->work, 0, 4 * sizeof(uint64_t) * fb_blocks(g->n ? g->n : 1), s));
+    add(b->work, 8 * fb_blocks(g->n ? g->n : 1));
+    if (g->n) add(bcount_ticket(g, p->shift, b->bcount), 1);
+    r.ctrl = b->ctrl;
+    r.init = d_init_values;
+    r.vals[0] = b->vals[0];
+    r.vals[1] = b->vals[1];
+    r.n = g->n;
+    r.vbytes = p->val_type == WG_VAL_U32 ? 4 : 8;
+    run_init_kernel<<<grid_for(words * 32 + 1, 256 * 4, 4), 256, 0, s>>>(r);
+    ::wg::count_launch();
+    WG_CHECK_LAUNCH("run_init");
     if (g->n == 0) return WG_OK;
-    WG_CUDA(cudaMemsetAsync(bcount_ticket(g, p->shift, b->bcount), 0, sizeof(unsigned), s));
     return launch_frontier_compaction(g, d_init_words, b->bcount, bcount_ticket(g, p->shift, b->bcount),
                                       b->fvert[0], b->fpref[0], b->tstart[0],
                                       &b->recs[0], s, (p->flags & WG_RUN_KEEP_LISTS) ? 1 : 0, p->wedge_limit);
+}
+
+int wg_run_init(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p,
+                const uint32_t *d_init_words, void *stream) {
+    return wg_run_seed(g, b, p, nullptr, d_init_words, stream);
 }
 
 static int enqueue_one(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p,
@@ -881,8 +971,9 @@ void *wg_run_loop_graph_create(const wg_graph *g, const wg_run_bufs *b, const wg
         return nullptr;
     }
     cudaGraph_t body = cp.conditional.phGraph_out[0];
-    cudaGraphConditionalHandle hf, hs, hp;
+    cudaGraphConditionalHandle hf, hs, hp, hl;
     e = cudaGraphConditionalHandleCreate(&hf, body, 0, cudaGraphCondAssignDefault);
+    if (e == cudaSuccess) e = cudaGraphConditionalHandleCreate(&hl, body, 0, cudaGraphCondAssignDefault);
     if (e == cudaSuccess) e = cudaGraphConditionalHandleCreate(&hs, body, 0, cudaGraphCondAssignDefault);
     if (e == cudaSuccess) e = cudaGraphConditionalHandleCreate(&hp, body, 0, cudaGraphCondAssignDefault);
     if (e == cudaSuccess)
@@ -901,15 +992,27 @@ void *wg_run_loop_graph_create(const wg_graph *g, const wg_run_bufs *b, const wg
     uint32_t *ts[2] = {b->tstart[0], b->tstart[1]};
     PullBufs pb = pull_bufs(g, b, &q);
     int rc = WG_OK;
-    // 0. as many consecutive sparse Wedge iterations as possible, persistently
-    if (g_sparse_loop && g->entries && g->nvec)
-        rc = launch_sparse_loop(c, g, pb, q.val_type, q.shift, &q.kern, b->gbits, groups, s);
-    // 1. device-side gate: which of the three bodies runs this iteration
-    decide_kernel<<<1, 1, 0, s>>>(c, hf, hs, hp, groups, g->entries > 0 ? 1 : 0);
-    ::wg::count_launch();
-    // 2. IF FullScan: dense pull
     cudaGraph_t inner;
-    if ((e = capture_if_node(s, hf, &inner)) == cudaSuccess &&
+    // 0. as many consecutive sparse Wedge iterations as possible, persistently
+    //    (IF the iteration about to run is one)
+    if (g_sparse_loop && g->entries && g->nvec) {
+        sparse_gate_kernel<<<1, 1, 0, s>>>(c, hl, groups, pb.loop_dense && !q.kern.use_weight ? 1u : 0u, g->n,
+                                           q.kern.filter_unvisited ? 1 : 0);
+        ::wg::count_launch();
+        if ((e = capture_if_node(s, hl, &inner)) == cudaSuccess &&
+            (e = cudaStreamBeginCaptureToGraph(s2, inner, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal)) ==
+                cudaSuccess) {
+            rc = launch_sparse_loop(c, g, pb, q.val_type, q.shift, &q.kern, b->gbits, groups, s2);
+            e = cudaStreamEndCapture(s2, &inner);
+        }
+    }
+    // 1. device-side gate: which of the three bodies runs this iteration
+    if (rc == WG_OK && e == cudaSuccess) {
+        decide_kernel<<<1, 1, 0, s>>>(c, hf, hs, hp, groups, g->entries > 0 ? 1 : 0);
+        ::wg::count_launch();
+    }
+    // 2. IF FullScan: dense pull
+    if (rc == WG_OK && e == cudaSuccess && (e = capture_if_node(s, hf, &inner)) == cudaSuccess &&
         (e = cudaStreamBeginCaptureToGraph(s2, inner, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal)) ==
             cudaSuccess) {
         if (g->nvec) rc = launch_pull(c, g, pb, q.val_type, q.shift, &q.kern, g->nvec, s2, MODE_FULL);
@@ -960,6 +1063,14 @@ void *wg_run_loop_graph_create(const wg_graph *g, const wg_run_bufs *b, const wg
 }
 
 // Debug: phase timestamps of the persistent loop into a device buffer.
+int wg_debug_kernel_timeline(uint64_t *d_buf, uint64_t iterations) {
+    WG_CUDA(cudaMemcpyToSymbol(g_kts, &d_buf, sizeof(d_buf)));
+    WG_CUDA(cudaMemcpyToSymbol(g_kts_cap, &iterations, sizeof(iterations)));
+    return WG_OK;
+}
+
+uint32_t wg_debug_kernel_ids(void) { return (uint32_t)KTS_IDS; }
+
 int wg_debug_phase_buffer(uint64_t *d_buf, uint64_t iterations) {
     WG_CUDA(cudaMemcpyToSymbol(g_phase_ts, &d_buf, sizeof(d_buf)));
     WG_CUDA(cudaMemcpyToSymbol(g_phase_cap, &iterations, sizeof(iterations)));

@@ -57,6 +57,7 @@ __device__ __forceinline__ uint64_t prior_blocks_sum(const uint64_t *bcount, uin
 // ---------------- K4: group bitmap -> ascending group list ----------------
 __global__ void __launch_bounds__(CB_THREADS) group_count_kernel(LoopCtx c, const uint32_t *words,
                                                                  uint64_t nbits, uint64_t *bcount) {
+    WG_KTS(ctx_iter(c), KTS_GROUP_COUNT);
     if (ctx_mode(c, ctx_iter(c)) != MODE_WEDGE) return;
     __shared__ uint64_t sm[33];
     uint64_t w0 = (uint64_t)blockIdx.x * CB_WORDS + threadIdx.x * CB_WPT;
@@ -75,6 +76,7 @@ __global__ void __launch_bounds__(CB_THREADS) group_list_kernel(LoopCtx c, uint3
                                                                 uint32_t *glist, int clear,
                                                                 int shift, uint64_t nvec) {
     uint64_t it = ctx_iter(c);
+    WG_KTS(it, KTS_GROUP_LIST);
     if (ctx_mode(c, it) != MODE_WEDGE) return;
     __shared__ uint64_t sm[33];
     uint64_t base = prior_blocks_sum(bcount, blockIdx.x, 1, 0, sm);
@@ -190,17 +192,11 @@ __device__ __forceinline__ void chunk_counts(const uint32_t *words, uint64_t nbi
 // after a dense pull whose output frontier gates the next iteration to
 // FullScan again, nothing consumes it (record reserved[2] = 1).  totals may
 // alias prefix; zero_totals clears them after reading (atomic accumulators).
-__device__ __forceinline__ void count_epilogue(uint64_t B, uint64_t *totals, uint64_t *prefix, bool zero_totals,
-                                               unsigned *counter, wg_iter_rec *rec, int keep_list, uint64_t edges,
-                                               uint64_t wedge_limit) {
+// The scan of a count pass, by ONE block: per-chunk totals -> exclusive
+// prefixes (see count_epilogue).
+__device__ __forceinline__ void count_tail(uint64_t B, uint64_t *totals, uint64_t *prefix, bool zero_totals,
+                                           wg_iter_rec *rec, int keep_list, uint64_t edges, uint64_t wedge_limit) {
     __shared__ uint64_t sm[33];
-    __shared__ bool s_last;
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
     const uint64_t per = (B + blockDim.x - 1) / blockDim.x;
     const uint64_t b0 = threadIdx.x * per, b1 = b0 + per < B ? b0 + per : B;
     uint64_t loc[3] = {0, 0, 0}, les = 0;
@@ -231,8 +227,29 @@ __device__ __forceinline__ void count_epilogue(uint64_t B, uint64_t *totals, uin
         // the list is consumed only by a Wedge iteration (or the caller)
         const bool wedge_next = es_all > 0 && edges > 0 && es_all < wedge_limit;
         rec->reserved[2] = (keep_list || wedge_next) ? 0 : 1;
-        *counter = 0;
     }
+}
+
+// End of a count pass (every block calls it): the LAST block to arrive
+// (atomic ticket) turns the per-chunk totals -- 4 counters per chunk: nz
+// members, their index entries, zero-degree members, out-degree sum -- into
+// exclusive prefixes in `prefix` (the list pass's starting points), writes
+// the record's counts and decides whether the ordered list is needed at all:
+// after a dense pull whose output frontier gates the next iteration to
+// FullScan again, nothing consumes it (record reserved[2] = 1).  totals may
+// alias prefix; zero_totals clears them after reading (atomic accumulators).
+__device__ __forceinline__ void count_epilogue(uint64_t B, uint64_t *totals, uint64_t *prefix, bool zero_totals,
+                                               unsigned *counter, wg_iter_rec *rec, int keep_list, uint64_t edges,
+                                               uint64_t wedge_limit) {
+    __shared__ bool s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    count_tail(B, totals, prefix, zero_totals, rec, keep_list, edges, wedge_limit);
+    if (threadIdx.x == 0) *counter = 0;
 }
 
 // keep_list: 1 = always build the list; 0 = decide from the next gate
@@ -263,20 +280,20 @@ __device__ __forceinline__ void frontier_list_body(const uint32_t *words, uint64
                                                    const uint64_t *idx_off, const uint32_t *outdeg,
                                                    const uint64_t *bcount,
                                                    uint32_t *fvert, uint32_t *fpref, uint32_t *tstart,
-                                                   const wg_iter_rec *rec) {
+                                                   const wg_iter_rec *rec, uint64_t chunk = ~0ull) {
     if (*(volatile const uint64_t *)&rec->reserved[2]) return;  // nobody consumes the list
+    if (chunk == ~0ull) chunk = blockIdx.x;
     __shared__ uint64_t s_w[3][CB_THREADS / 32];
     const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1u;
-    const uint64_t wbase = (uint64_t)blockIdx.x * FB_WORDS + (uint64_t)warp * 32;
+    const uint64_t wbase = chunk * FB_WORDS + (uint64_t)warp * 32;
     uint64_t nz, ent, z, es;
     chunk_counts(words, nbits, wbase, idx_off, outdeg, nz, ent, z, es);
     if (lane == 0) {
         s_w[0][warp] = nz; s_w[1][warp] = ent; s_w[2][warp] = z;
     }
     __syncthreads();
-    uint64_t nzp = bcount[4ull * blockIdx.x], entp = bcount[4ull * blockIdx.x + 1],
-             zp = bcount[4ull * blockIdx.x + 2];
+    uint64_t nzp = bcount[4ull * chunk], entp = bcount[4ull * chunk + 1], zp = bcount[4ull * chunk + 2];
     for (unsigned w = 0; w < warp; ++w) {
         nzp += s_w[0][w];
         entp += s_w[1][w];
@@ -341,6 +358,7 @@ __global__ void __launch_bounds__(CB_THREADS) loop_frontier_count_kernel(LoopCtx
                                                                          const uint32_t *outdeg,
                                                                          uint64_t *bcount, unsigned *counter) {
     const uint64_t it = ctx_iter(c);
+    WG_KTS(it, KTS_FCOUNT);
     if (ctx_mode(c, it) != MODE_FULL) return;
     if (dst_major_active(c, it, n, f.dst_major, f.dst_bottom_up != 0)) return;  // counted by dense_dst_kernel
     frontier_count_body((it & 1) ? f.fbits[1] : f.fbits[0], n, idx_off, outdeg, bcount, counter, ctx_out(c, it),
@@ -352,6 +370,7 @@ __global__ void __launch_bounds__(CB_THREADS) loop_frontier_list_kernel(LoopCtx 
                                                                         const uint32_t *outdeg,
                                                                         const uint64_t *bcount) {
     const uint64_t it = ctx_iter(c);
+    WG_KTS(it, KTS_FLIST);
     if (ctx_mode(c, it) != MODE_FULL) return;
     const int k = (int)(it & 1);
     frontier_list_body(k ? f.fbits[1] : f.fbits[0], n, idx_off, outdeg, bcount, k ? f.fvert[1] : f.fvert[0],
@@ -489,6 +508,7 @@ __global__ void __launch_bounds__(TR_THREADS) transform_kernel(
     const uint32_t *fpref1, const uint32_t *tstart0, const uint32_t *tstart1, const uint64_t *idx_off,
     const uint32_t *idx_pos, int shift, uint32_t *gbits, int append, uint32_t *glist, uint64_t ngroups) {
     const uint64_t it = ctx_iter(c);
+    WG_KTS(it, KTS_TRANSFORM);
     if (ctx_mode(c, it) != MODE_WEDGE) return;
     __shared__ TransformSmem sm;
     transform_phase(c, it, fvert0, fvert1, fpref0, fpref1, tstart0, tstart1, idx_off, idx_pos, shift, gbits,

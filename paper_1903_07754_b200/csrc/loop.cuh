@@ -42,6 +42,39 @@ __device__ __forceinline__ int ctx_mode(const LoopCtx &c, uint64_t it) {
     return (c.edges > 0 && sum < c.wedge_limit) ? MODE_WEDGE : MODE_FULL;
 }
 
+// Debug timeline of the loop's kernels (wg_debug_kernel_timeline; null =
+// off): per (iteration, kernel id) the earliest block start and the latest
+// block end, %globaltimer ns, stamped by thread 0 of every block.
+enum : int {
+    KTS_DECIDE = 0, KTS_SPARSE_GATE, KTS_TRANSFORM, KTS_GROUP_COUNT, KTS_GROUP_LIST, KTS_PULL_WEDGE,
+    KTS_PULL_SPARSE, KTS_DENSE_DST, KTS_DENSE_TMA, KTS_BOTTOM_UP, KTS_FLOOR, KTS_IDENT, KTS_FCOUNT, KTS_FLIST,
+    KTS_FINALIZE, KTS_STEP, KTS_IDS
+};
+static __device__ uint64_t *g_kts = nullptr;
+static __device__ uint64_t g_kts_cap = 0;
+
+__device__ __forceinline__ uint64_t kts_now() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+template <int ID>
+struct KtsScope {
+    uint64_t it;  // the only state kept live across the kernel
+    __device__ __forceinline__ explicit KtsScope(uint64_t i) : it(i) {
+        uint64_t *buf = g_kts;
+        if (buf != nullptr && threadIdx.x == 0 && it < g_kts_cap)
+            atomicMin((unsigned long long *)(buf + (it * KTS_IDS + ID) * 2), (unsigned long long)kts_now());
+    }
+    __device__ __forceinline__ ~KtsScope() {
+        uint64_t *buf = g_kts;
+        if (buf != nullptr && threadIdx.x == 0 && it < g_kts_cap)
+            atomicMax((unsigned long long *)(buf + (it * KTS_IDS + ID) * 2 + 1), (unsigned long long)kts_now());
+    }
+};
+#define WG_KTS(it, id) ::wg::KtsScope<id> _wg_kts_scope((it))
+
 __device__ __forceinline__ wg_iter_rec *ctx_out(const LoopCtx &c, uint64_t it) {
     return &c.recs[it % c.ring];
 }

@@ -69,6 +69,7 @@ struct PullBufs {
     int64_t level_base;  // its frontier-0 value
     uint32_t *work;      // wg_run_bufs.work: destination list of the destination-major dense pulls
     uint32_t dst_major;  // dense iterations run dense_dst_kernel (DSTK_FLOOR / DSTK_BOTTOM_UP)
+    uint32_t loop_dense; // ... and the persistent loop runs them as phases (WG_LOOP_DENSE=0: off)
 };
 
 
@@ -455,6 +456,7 @@ __global__ void __launch_bounds__(PULL_THREADS) pull_kernel(LoopCtx c, wg_graph 
     using VT = ValTraits<T>;
     __shared__ uint32_t s_stage[PULL_WARPS][STAGE];
     const uint64_t it = ctx_iter(c);
+    WG_KTS(it, KTS_PULL_WEDGE);
     const int mode = ctx_mode(c, it);
     if (mode == MODE_NONE || !((handles >> mode) & 1)) return;
     const bool wedge = (mode == MODE_WEDGE);
@@ -536,6 +538,7 @@ __global__ void __launch_bounds__(256) pull_ident_kernel(LoopCtx c, wg_graph g, 
                                                          int64_t sentinel) {
     using VT = ValTraits<T>;
     const uint64_t it = ctx_iter(c);
+    WG_KTS(it, KTS_IDENT);
     if (it != 1 || ctx_mode(c, it) != MODE_FULL) return;
     wg_iter_rec *out = ctx_out(c, it);
     const T *__restrict__ prev = (const T *)b.vals[0];
@@ -586,6 +589,7 @@ __global__ void __launch_bounds__(256) floor_pull_kernel(LoopCtx c, wg_graph g, 
                                                          int64_t sentinel) {
     using VT = ValTraits<T>;
     const uint64_t it = ctx_iter(c);
+    WG_KTS(it, KTS_FLOOR);
     if (ctx_mode(c, it) != MODE_FULL || it < b.floor_from) return;
     wg_iter_rec *out = ctx_out(c, it);
     const T *__restrict__ prev = (const T *)(((it - 1) & 1) ? b.vals[1] : b.vals[0]);
@@ -666,6 +670,7 @@ __global__ void __launch_bounds__(256) bottom_up_pull_kernel(LoopCtx c, wg_graph
                                                              int64_t sentinel) {
     using VT = ValTraits<T>;
     const uint64_t it = ctx_iter(c);
+    WG_KTS(it, KTS_BOTTOM_UP);
     if (ctx_mode(c, it) != MODE_FULL || it < b.floor_from || it < 2) return;
     if (dst_major_active(c, it, b.n, b.dst_major, true)) return;  // dense_dst_kernel's iteration
     wg_iter_rec *out = ctx_out(c, it);
@@ -766,13 +771,13 @@ constexpr uint32_t DST_LIGHT = 8;  // vectors walked by one thread
 constexpr int DST_K = 4;           // destinations per thread in flight (one warp = DST_K words)
 constexpr int DSTK_FLOOR = 0, DSTK_BOTTOM_UP = 1;
 
+// One destination-major dense iteration over warps [warp0, warp0 + nwarps)
+// of a grid-stride split; per-chunk frontier totals into b.work (the caller
+// then runs count_tail / count_epilogue).
 template <typename T, int W, int KIND>
-__global__ void __launch_bounds__(256) dense_dst_kernel(LoopCtx c, wg_graph g, PullBufs b, int64_t inc,
-                                                        int64_t sentinel) {
+__device__ __forceinline__ void dense_dst_phase(const LoopCtx &c, uint64_t it, const wg_graph &g, const PullBufs &b,
+                                                int64_t inc, int64_t sentinel, uint64_t warp0, uint64_t nwarps) {
     using VT = ValTraits<T>;
-    const uint64_t it = ctx_iter(c);
-    if (ctx_mode(c, it) != MODE_FULL) return;
-    if (!dst_major_active(c, it, b.n, b.dst_major, KIND == DSTK_BOTTOM_UP)) return;
     wg_iter_rec *out = ctx_out(c, it);
     const T *__restrict__ prev = (const T *)(((it - 1) & 1) ? b.vals[1] : b.vals[0]);
     T *__restrict__ nxt = (T *)((it & 1) ? b.vals[1] : b.vals[0]);
@@ -804,8 +809,6 @@ __global__ void __launch_bounds__(256) dense_dst_kernel(LoopCtx c, wg_graph g, P
     uint64_t touched = 0;
     const uint64_t n = g.n;
     const uint64_t span = 32ull * DST_K;  // destinations per warp step, word-aligned
-    const uint64_t warp0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     for (uint64_t wb = warp0 * span; wb < n; wb += nwarps * span) {
         T p[DST_K], agg[DST_K];
         uint32_t v0[DST_K], v1[DST_K];
@@ -935,9 +938,11 @@ __global__ void __launch_bounds__(256) dense_dst_kernel(LoopCtx c, wg_graph g, P
             }
             if (d < n) nxt[d] = res;
             const unsigned word = __ballot_sync(FULL, upd);
+            // the warp owns this word: a plain store, zeros included (the
+            // bitmap need not be cleared before a destination-major pull)
+            if (lane == 0 && d - lane < n) obits[(wb >> 5) + k] = word;
             if (word) {
                 any = true;
-                if (lane == 0) atomicOr(&obits[(wb >> 5) + k], word);
                 if (upd) {
                     const uint64_t len = lens_deg ? deg[k] : g.idx_off[d + 1] - g.idx_off[d];
                     nz += len != 0;
@@ -969,8 +974,19 @@ __global__ void __launch_bounds__(256) dense_dst_kernel(LoopCtx c, wg_graph g, P
         const uint64_t t = warp_sum(touched);
         if (lane == 0 && t) atomicAdd((unsigned long long *)&out->vectors_touched, (unsigned long long)t);
     }
-    count_epilogue(fb_blocks(n ? n : 1), (uint64_t *)totals, b.bcount, true, b.ticket, out, c.keep_lists, c.edges,
-                   c.wedge_limit);
+}
+
+template <typename T, int W, int KIND>
+__global__ void __launch_bounds__(256) dense_dst_kernel(LoopCtx c, wg_graph g, PullBufs b, int64_t inc,
+                                                        int64_t sentinel) {
+    const uint64_t it = ctx_iter(c);
+    WG_KTS(it, KTS_DENSE_DST);
+    if (ctx_mode(c, it) != MODE_FULL) return;
+    if (!dst_major_active(c, it, b.n, b.dst_major, KIND == DSTK_BOTTOM_UP)) return;
+    dense_dst_phase<T, W, KIND>(c, it, g, b, inc, sentinel, ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5,
+                                ((uint64_t)gridDim.x * blockDim.x) >> 5);
+    count_epilogue(fb_blocks(b.n ? b.n : 1), (uint64_t *)b.work, b.bcount, true, b.ticket, ctx_out(c, it),
+                   c.keep_lists, c.edges, c.wedge_limit);
 }
 
 // One dense-pull chunk after its gathers were issued: destinations, segment
@@ -1408,6 +1424,7 @@ __global__ void __launch_bounds__(PULL_THREADS) pull_sparse_kernel(LoopCtx c, wg
                                                                    uint32_t *gbits, uint64_t ngroups_all) {
     __shared__ uint32_t s_stage[PULL_WARPS][STAGE];
     const uint64_t it = ctx_iter(c);
+    WG_KTS(it, KTS_PULL_SPARSE);
     if (ctx_mode(c, it) != MODE_WEDGE) return;
     const uint64_t gwarp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -1422,10 +1439,14 @@ __global__ void __launch_bounds__(PULL_THREADS) pull_sparse_kernel(LoopCtx c, wg
 // copied into the buffer the next iteration writes.  Also clears the output
 // bitmap of iteration it-1 (reused by it+1), finalises the record and zeroes
 // the record the next iteration will fill.
+// records_only: the next iteration is a destination-major dense pull, which
+// writes every value and every bitmap word it produces -- neither the buffer
+// sync nor the bitmap clear is needed, only the record.
 template <typename T>
 __device__ __forceinline__ void end_of_iteration(const LoopCtx &c, uint64_t it, int mode, const PullBufs &b,
-                                                 uint64_t tid, uint64_t nthreads, int zero_ahead) {
-    if (mode != MODE_NONE) {
+                                                 uint64_t tid, uint64_t nthreads, int zero_ahead,
+                                                 bool records_only = false) {
+    if (mode != MODE_NONE && !records_only) {
         const wg_iter_rec *out = ctx_out(c, it);
         const wg_iter_rec *in = ctx_in(c, it);
         const T *src = (const T *)((it & 1) ? b.vals[1] : b.vals[0]);
@@ -1477,6 +1498,7 @@ __device__ __forceinline__ void end_of_iteration(const LoopCtx &c, uint64_t it, 
 template <typename T>
 __global__ void __launch_bounds__(256) finalize_kernel(LoopCtx c, PullBufs b) {
     const uint64_t it = ctx_iter(c);
+    WG_KTS(it, KTS_FINALIZE);
     const int mode = ctx_mode(c, it);
     end_of_iteration<T>(c, it, mode, b, (uint64_t)blockIdx.x * blockDim.x + threadIdx.x,
                         (uint64_t)gridDim.x * blockDim.x, 1);
@@ -1544,7 +1566,42 @@ __global__ void __launch_bounds__(PULL_THREADS, SPARSE_MINB) sparse_loop_kernel(
     }
     grid.sync();
     if (!fused) {
-        while (sparse_wedge(c, it, ngroups)) {
+        // destination-major dense iterations run here too (unweighted, dst_major):
+        // pull -> barrier -> one block's count scan -> barrier -> the ordered
+        // member list when a Wedge iteration follows
+        constexpr int KIND = FILTER ? DSTK_BOTTOM_UP : DSTK_FLOOR;
+        const uint64_t nchunks = fb_blocks(b.n ? b.n : 1);
+        int prev_mode = MODE_NONE;
+        while (true) {
+            const bool dense = !WEIGHT && b.dst_major && b.loop_dense && ctx_mode(c, it) == MODE_FULL &&
+                               dst_major_active(c, it, b.n, 1u, FILTER);
+            if (!dense && !sparse_wedge(c, it, ngroups)) break;
+            if (dense) {
+                phase_stamp(it, 0);
+                if (it > first) end_of_iteration<T>(c, it - 1, prev_mode, b, tid, nthreads, 2, true);
+                dense_dst_phase<T, W, KIND>(c, it, g, b, inc, sentinel, gwarp, nwarps);
+                grid.sync();
+                phase_stamp(it, 1);
+                if (blockIdx.x == 0)
+                    count_tail(nchunks, (uint64_t *)b.work, b.bcount, true, ctx_out(c, it), c.keep_lists, c.edges,
+                               c.wedge_limit);
+                grid.sync();
+                phase_stamp(it, 2);
+                if (!*(volatile const uint64_t *)&ctx_out(c, it)->reserved[2]) {  // a Wedge iteration follows
+                    const int k = (int)(it & 1);
+                    const uint64_t *off = (g.flags & WG_GRAPH_LENS_ARE_DEGREES) ? nullptr : g.idx_off;
+                    for (uint64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+                        frontier_list_body(b.fbits[k], b.n, off, g.outdeg, b.bcount, b.fvert[k], b.fpref[k],
+                                           b.tstart[k], ctx_out(c, it), ch);
+                        __syncthreads();
+                    }
+                    grid.sync();
+                }
+                phase_stamp(it, 3);
+                prev_mode = MODE_FULL;
+                ++it;
+                continue;
+            }
             phase_stamp(it, 0);
             if (tid == 0) ctx_out(c, it)->reserved[0] = 3;
             // phase A: transform(it)  ||  end of iteration it-1 (buffer sync, bitmap
@@ -1553,7 +1610,7 @@ __global__ void __launch_bounds__(PULL_THREADS, SPARSE_MINB) sparse_loop_kernel(
             transform_phase(c, it, b.fvert[0], b.fvert[1], b.fpref[0], b.fpref[1], b.tstart[0], b.tstart[1],
                             g.idx_off, g.idx_pos, shift, gbits, 1, const_cast<uint32_t *>(b.glist), ngroups,
                             tsm, blockIdx.x, gridDim.x);
-            if (it > first) end_of_iteration<T>(c, it - 1, MODE_WEDGE, b, tid, nthreads, 2);
+            if (it > first) end_of_iteration<T>(c, it - 1, prev_mode, b, tid, nthreads, 2);
             grid.sync();
             phase_stamp(it, 1);
             // phase B: pull(it)
@@ -1562,11 +1619,12 @@ __global__ void __launch_bounds__(PULL_THREADS, SPARSE_MINB) sparse_loop_kernel(
             grid.sync();
             phase_stamp(it, 2);
             phase_stamp(it, 3);
+            prev_mode = MODE_WEDGE;
             ++it;
         }
         // the last iteration run here still needs its end-of-iteration work
         if (it > first) {
-            end_of_iteration<T>(c, it - 1, MODE_WEDGE, b, tid, nthreads, 1);
+            end_of_iteration<T>(c, it - 1, prev_mode, b, tid, nthreads, 1);
             if (tid == 0) *(volatile uint64_t *)&ctrl[0] = it - 1;
         }
         return;

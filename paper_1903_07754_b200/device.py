@@ -846,6 +846,7 @@ class DeviceLoop:
         self.recs = torch.zeros(self.ring * REC_U64, dtype=torch.int64, device=dev)
         self.ctrl = torch.zeros(4, dtype=torch.int64, device=dev)
         self.host_recs = torch.zeros(self.ring * REC_U64, dtype=torch.int64).pin_memory()
+        self.ctrl_host = torch.zeros(4, dtype=torch.int64).pin_memory()
         b = WgRunBufs()
         for i in range(2):
             b.vals[i] = _ptr(self.vals[i])
@@ -879,12 +880,12 @@ class DeviceLoop:
         """Write both value buffers and build iteration 0 from the frontier bitmap.
         first_hit: the caller checked first_hit_ok (level-synchronous values);
         level_base: then the common value of the initial frontier (first_hit_level)."""
-        for v in self.vals:
-            v.copy_(init_values)
+        if init_values.numel() < self.g.n or init_values.dtype != self.vals[0].dtype:
+            raise ValueError("initial values do not match the loop's value buffers")
         self._level_base = int(level_base)
         p = self.params(kern, threshold, first_hit, identity_init)
-        check(_lib.load().wg_run_init(ctypes.byref(self.g.struct()), ctypes.byref(self.bufs),
-                                      ctypes.byref(p), _ptr(init_words), _lib.stream_ptr(stream)))
+        check(_lib.load().wg_run_seed(ctypes.byref(self.g.struct()), ctypes.byref(self.bufs), ctypes.byref(p),
+                                      _ptr(init_values), _ptr(init_words), _lib.stream_ptr(stream)))
         return p
 
     def enqueue(self, p: WgRunParams, it_begin: int, count: int, stream=None) -> None:
@@ -964,7 +965,7 @@ class DeviceLoop:
         exe = self._graph_for(p, stream)
         records: list[IterRecord] = []
         it, converged, last = 1, False, 0
-        ctrl_host = torch.zeros(4, dtype=torch.int64).pin_memory()
+        ctrl_host = self.ctrl_host
         while it <= max_iterations and not converged:
             limit = min(max_iterations, it - 1 + self.ring - 2)
             check(L.wg_run_loop_launch(exe, ctypes.byref(self.bufs), limit, _lib.stream_ptr(stream)))
