@@ -305,7 +305,7 @@ def run_b200(args, wl):
     torch.cuda.synchronize()
     kernels_per_step = _lib.launch_count() - l0  # launched one by one here (no graph)
     rows = timer.read()
-    roof = roofline(rows, recs_t, n, E, g.weighted(), kern.filter_unvisited, wl, ident_first=ident)
+    roof = roofline(rows, recs_t, n, E, g.weighted(), kern.filter_unvisited, wl)
 
     out = {
         "metric": METRIC, "value": round(gteps, 4), "unit": "GTEPS (|E|/time-to-solution)",
@@ -490,85 +490,87 @@ def certificate(el, values, app):
             "reached": int(reached.sum()) + 1, "ok": viol == 0 and untight == 0}
 
 
-def roofline(rows, recs, n, E, weighted, filt, wl, ident_first=False):
-    """achieved = algorithmic bytes per pull launch / its CUDA-event duration
-    (dense launches: the dominant kernel); wedge iterations reported beside.
-    ident_first: iteration 1 ran pull_ident_kernel (one lane per destination,
-    WG_RUN_IDENTITY_INIT), which does not move the dense formula's bytes, so
-    it is reported on its own and kept out of the dense figure."""
+def roofline(rows, recs, n, E, weighted, filt, wl):
+    """Roofline of the dominant kernel: achieved = algorithmic bytes of its
+    launches / their CUDA-event durations (per launch, on the launching
+    stream: the library's timer, one iteration per launch group).
+
+    Algorithmic bytes (uint32 ids/values, w = 1 if weighted):
+    * destination-major dense pull (dense_dst_kernel; CC floor / BFS
+      bottom-up): what that algorithm must touch -- prev[d], voff[d..d+1],
+      nxt[d] and the next-frontier bit of every vertex (12V + V/8), the lanes
+      it reads and the values / frontier bits it gathers (4 B each, device
+      counters lanes_read / gathers) and the out-degree of each produced
+      member (4U).  The 8(d) dense formula (every in-edge of every processed
+      destination) does not describe it: a destination decided by its first
+      lane (floor 0 / first frontier hit) provably needs none of its other
+      lanes.
+    * TMA dense pull: 4*E_p*(1+w) + 4V + 4U + V/8 (E_p = E, or the lanes of
+      unvisited destinations when filtered).
+    * Wedge iteration (transform + pull): 4A(1+w) + 4|F| + 4U + V/8 + [V/8 +
+      8|F| + 4A]."""
     peak, peak_src = peaks()
     by_it = {}
     for kind, it, ms in rows:
         d = by_it.setdefault(it, {})
         d[kind] = d.get(kind, 0.0) + ms
     w = 1 if weighted else 0
-    dense_b = dense_t = 0.0
-    wedge_b = wedge_t = 0.0
+    kern = {"dense_dst": [0.0, 0.0, 0], "dense_tma": [0.0, 0.0, 0], "wedge": [0.0, 0.0, 0]}
     step_t = 0.0
     prev_out = None
     per_iter = []
-    # iterations >= 3 of a floor-skipping run use floor_pull_kernel
-    floor_k = (ident_first and os.environ.get("WG_FLOOR_SKIP", "1") != "0"
-               and os.environ.get("WG_FLOOR_KERNELS", "1") != "0")
     for r in recs:
         t = by_it.get(r.iteration, {})
-        pull_ms = t.get(2, 0.0)
-        prep_ms = t.get(1, 0.0)
+        pull_ms, prep_ms = t.get(2, 0.0), t.get(1, 0.0)
         fin_ms = t.get(3, 0.0) + t.get(4, 0.0)  # end of iteration (+ list build after a dense pull)
         step_t += pull_ms + prep_ms + fin_ms
         U = r.frontier_out_size
-        if r.mode == "FullScan" and ident_first and r.iteration == 1:
-            b = 4 * n + 4 * n + 4 * U + n / 8  # vec_dst run heads + one lane per destination + apply
-        elif r.mode == "FullScan" and floor_k and r.iteration >= 3:
-            # floor_pull_kernel: vec_dst, prev[d], nxt[d], lanes of non-floor destinations
-            # only (a few per mille here) -- reported on its own, not as the
-            # pipeline's dense figure
-            b = 4 * (E // 4) + 4 * n + 4 * n + 4 * U + n / 8
+        if r.mode == "FullScan" and (r.lanes_read or r.gathers):
+            name = "dense_dst"
+            b = 12 * n + n / 8 + 4 * r.lanes_read + 4 * r.gathers + 4 * U
+            kt = pull_ms
         elif r.mode == "FullScan":
+            name = "dense_tma"
             ep = E if not filt else min(E, 4 * r.vectors_touched)
             b = 4 * ep * (1 + w) + 4 * n + 4 * U + n / 8
-            dense_b += b
-            dense_t += pull_ms
+            kt = pull_ms
         else:
+            name = "wedge"
             A = r.active_edges
             F = prev_out if prev_out is not None else 0
             b = 4 * A * (1 + w) + 4 * F + 4 * U + n / 8 + (n / 8 + 8 * F + 4 * A)
-            wedge_b += b
-            wedge_t += pull_ms + prep_ms
-        per_iter.append({"it": r.iteration, "mode": r.mode, "pull_ms": round(pull_ms, 4),
-                         "prep_ms": round(prep_ms, 4), "end_ms": round(fin_ms, 4),
-                         "alg_MB": round(b / 1e6, 2)})
+            kt = pull_ms + prep_ms
+        kern[name][0] += b
+        kern[name][1] += kt
+        kern[name][2] += 1
+        per_iter.append({"it": r.iteration, "mode": r.mode, "kernel": name, "pull_ms": round(pull_ms, 4),
+                         "prep_ms": round(prep_ms, 4), "end_ms": round(fin_ms, 4), "alg_MB": round(b / 1e6, 2),
+                         "lanes_read": r.lanes_read, "gathers": r.gathers})
         prev_out = U
-    if dense_t > 0:
-        ach = dense_b / (dense_t * 1e-3) / 1e9
-        if filt:
-            kernel = f"pull_dense_tma_kernel<u32,W{wl.get('W', 4)},filter> (K6, dense filtered pull)"
-        elif ident_first and os.environ.get("WG_FLOOR_SKIP", "1") != "0":
-            kernel = (f"pull_dense_tma_kernel<u32,W{wl.get('W', 4)},filtered pipeline> (K6, dense pull with "
-                      "floor skipping: destinations at label 0 gather nothing, every lane still streamed)")
-        else:
-            kernel = f"pull_dense_tma_kernel<u32,W{wl.get('W', 4)}> (K6, dense pull)"
-        traffic = dense_b / max(1, sum(1 for r in recs if r.mode == "FullScan"
-                                       and not (ident_first and r.iteration == 1)
-                                       and not (floor_k and r.iteration >= 3)))
-    else:
-        ach = wedge_b / (wedge_t * 1e-3) / 1e9 if wedge_t else 0.0
-        kernel = "transform + wedge pull (K3+K4+K5)"
-        traffic = None
+    dom = max(kern, key=lambda k: kern[k][1])
+    bts, ms, launches = kern[dom]
+    ach = bts / (ms * 1e-3) / 1e9 if ms else 0.0
+    desc = {"dense_dst": "dense_dst_kernel (destination-major dense pull%s)" % (
+                ": bottom-up BFS" if filt else ": floor-probing min-label pull"),
+            "dense_tma": "pull_dense_tma_kernel (K6, TMA-streamed dense pull)",
+            "wedge": "transform + group compaction + wedge pull (K3+K4+K5)"}[dom]
     prof = ROOT / "profiles" / "traffic.json"
     measured_traffic = None
     if prof.exists():
         try:
-            ent = json.loads(prof.read_text()).get(wl["desc"])
+            ent = json.loads(prof.read_text()).get(f"{wl['desc']}|{dom}")
             measured_traffic = ent.get("dram_bytes_per_launch") if isinstance(ent, dict) else ent
         except Exception:
             pass
+    other = {k: {"alg_MB": round(v[0] / 1e6, 2), "ms": round(v[1], 4), "launches": v[2],
+                 "achieved_gbs": round(v[0] / (v[1] * 1e-3) / 1e9, 1) if v[1] else None}
+             for k, v in kern.items() if v[2]}
     return {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
-            "frac": round(ach / peak, 4), "traffic": measured_traffic, "kernel": kernel,
-            "peak_source": peak_src,
-            "algorithmic_bytes_per_launch": round(traffic, 1) if traffic else None,
-            "wedge_iters_achieved_gbs": round(wedge_b / (wedge_t * 1e-3) / 1e9, 1) if wedge_t else None,
-            "kernel_sum_ms": round(step_t, 4),
+            "frac": round(ach / peak, 4), "traffic": measured_traffic, "kernel": desc,
+            "peak_source": peak_src, "launches": launches,
+            "algorithmic_bytes_per_launch": round(bts / max(1, launches), 1),
+            "kernel_ms_per_launch": round(ms / max(1, launches), 4),
+            "by_kernel": other, "kernel_sum_ms": round(step_t, 4),
             "per_iteration": per_iter if len(per_iter) <= 16 else per_iter[:8] + per_iter[-2:],
             "iterations_timed": len(per_iter)}
 

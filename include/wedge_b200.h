@@ -74,6 +74,9 @@ typedef struct wg_graph {
     const uint32_t *voff;    /* optional [n+1] first vector of each destination (the run-length form
                                 of vdst, wg_vector_offsets_from_dst): enables the destination-major
                                 dense pulls (a thread / warp per destination, no vdst stream) */
+    const uint32_t *vfirst;  /* optional (with voff) [n] first lane of each destination's first vector =
+                                its smallest source, WG_NO_LANE without in-edges: the destination-major
+                                pulls' first probe as one coalesced load */
 } wg_graph;
 
 /* Every vertex's edge-index length equals its out-degree (no parallel edges;
@@ -260,6 +263,10 @@ typedef struct wg_iter_rec {
     uint64_t groups;           /* selected wedge groups */
     uint64_t overflow;         /* WG_VAL_U32 overflow flag */
     uint64_t reserved[5];
+    uint64_t lanes_read;       /* destination-major dense pulls: edge lanes read (vectors x W, or
+                                  single first-lane probes) ... */
+    uint64_t gathers;          /* ... and value gathers / frontier-bit tests made */
+    uint64_t spare[14];        /* (records are 32 words) */
 } wg_iter_rec;
 
 /* Device buffers of a run; all caller-allocated (sizes from
@@ -338,9 +345,13 @@ int wg_run_init(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p,
 /* wg_run_init plus both value buffers written from d_init_values ([n] values
  * of p->val_type) -- one launch for the whole initialisation
  * (ValueBuffers.initialize, engine.py:100; VertexFrontier.from_vertices,
- * frontier.py:79). */
+ * frontier.py:79).  h_all_counts4 (optional, host): frontier 0 is EVERY vertex
+ * (engine apps: CC) and these are its counts -- members with index entries,
+ * their entries, members without, out-degree sum -- so no compaction pass
+ * runs; only valid when iteration 1 is dense and no member lists are kept
+ * (WG_EINVAL otherwise); d_init_words may then be null. */
 int wg_run_seed(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p, const void *d_init_values,
-                const uint32_t *d_init_words, void *stream);
+                const uint32_t *d_init_words, const uint64_t *h_all_counts4, void *stream);
 /* Enqueue iterations [it_begin, it_begin + count) (1-based).  Each kernel
  * re-derives the gate and the converged flag on device from the previous
  * record, so iterations after convergence are no-ops.  Asynchronous. */
@@ -478,6 +489,8 @@ int wg_grid_edges(uint32_t rows, uint32_t cols, uint64_t seed, uint32_t keep_per
  * vdst), voff[n] = nvec: the per-destination form of PullTopology.vec_dst
  * (graph.py:240-243).  d_voff: [n+1]. */
 int wg_vector_offsets_from_dst(const wg_graph *g, uint32_t *d_voff, void *stream);
+/* vfirst[d] = vsrc[voff[d] * width] (WG_NO_LANE when d has no vectors); needs d_voff. */
+int wg_first_lanes(const wg_graph *g, const uint32_t *d_voff, uint32_t *d_vfirst, void *stream);
 
 /* ---------------------------------------------------------------------- */
 /* Ingest of the plugin call's reference-layout host arrays (ingest.cu).   */

@@ -27,7 +27,7 @@ class WgGraph(ctypes.Structure):
     _fields_ = [("n", c_u32), ("width", c_u32), ("nvec", c_u64), ("edges", c_u64),
                 ("entries", c_u64), ("vsrc", c_vp), ("vdst", c_vp), ("vw", c_vp),
                 ("idx_off", c_vp), ("idx_pos", c_vp), ("outdeg", c_vp), ("flags", c_u32), ("vw8", c_vp),
-                ("voff", c_vp)]
+                ("voff", c_vp), ("vfirst", c_vp)]
 
 
 WG_GRAPH_LENS_ARE_DEGREES = 1
@@ -39,8 +39,9 @@ class WgMinPlus(ctypes.Structure):
 
 
 REC_FIELDS = ["mode", "active_edges", "vectors_touched", "frontier_out", "out_edge_sum",
-              "nz_packed", "z_count", "covered_vectors", "transform_entries", "groups", "overflow"]
-REC_U64 = 16  # record size in uint64 words
+              "nz_packed", "z_count", "covered_vectors", "transform_entries", "groups", "overflow",
+              "reserved0", "reserved1", "reserved2", "reserved3", "reserved4", "lanes_read", "gathers"]
+REC_U64 = 32  # record size in uint64 words
 
 
 class WgRunBufs(ctypes.Structure):
@@ -83,7 +84,7 @@ EXPORTS = [
     "wg_decode_lanes", "wg_index_chunk_coded", "wg_expand_scratch_bytes", "wg_index_placed_scratch_bytes",
     "wg_index_place_begin", "wg_index_place_chunk", "wg_index_place_coded", "wg_index_place_end",
     "wg_ingest_vectors", "wg_ingest_u32", "wg_ingest_offsets", "wg_values_scan", "wg_vector_offsets_from_dst",
-    "wg_run_seed", "wg_debug_kernel_timeline", "wg_debug_kernel_ids",
+    "wg_run_seed", "wg_debug_kernel_timeline", "wg_debug_kernel_ids", "wg_first_lanes",
 ]
 
 _LIB = None
@@ -202,9 +203,10 @@ def load(path: os.PathLike | str | None = None):
         "wg_ingest_offsets": (ctypes.c_int, [c_u32, c_vp, c_u64, c_vp, c_vp, c_vp]),
         "wg_values_scan": (ctypes.c_int, [c_u32, c_vp, c_i64, c_vp, c_vp, c_vp]),
         "wg_vector_offsets_from_dst": (ctypes.c_int, [G, c_vp, c_vp]),
-        "wg_run_seed": (ctypes.c_int, [G, B, P, c_vp, c_vp, c_vp]),
+        "wg_run_seed": (ctypes.c_int, [G, B, P, c_vp, c_vp, u64p, c_vp]),
         "wg_debug_kernel_timeline": (ctypes.c_int, [c_vp, c_u64]),
         "wg_debug_kernel_ids": (c_u32, []),
+        "wg_first_lanes": (ctypes.c_int, [G, c_vp, c_vp, c_vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -722,7 +722,17 @@ struct InitRanges {
     uint64_t n, vbytes;
 };
 
+// frontier 0 = every vertex: its counts are the graph's own totals
+__global__ void seed_all_record_kernel(wg_iter_rec *rec, uint64_t nz, uint64_t ent, uint64_t z, uint64_t es) {
+    rec->nz_packed = (nz << 32) | ent;
+    rec->z_count = z;
+    rec->frontier_out = nz + z;
+    rec->out_edge_sum = es;
+    rec->reserved[2] = 1;  // no member list: the caller checked that iteration 1 is dense
+}
+
 __global__ void run_init_kernel(InitRanges r) {
+    WG_KTS(0, KTS_SEED);
     const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
     if (tid == 0) {
@@ -756,10 +766,10 @@ __global__ void run_init_kernel(InitRanges r) {
 extern "C" {
 
 int wg_run_seed(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p, const void *d_init_values,
-                const uint32_t *d_init_words, void *stream) {
+                const uint32_t *d_init_words, const uint64_t *h_all_counts4, void *stream) {
     int rc = check_run(g, b, p);
     if (rc) return rc;
-    WG_REQUIRE(d_init_words, "null initial frontier");
+    WG_REQUIRE(d_init_words || h_all_counts4, "null initial frontier");
     cudaStream_t s = as_stream(stream);
     const uint64_t words = ((uint64_t)g->n + 31) >> 5;
     const uint64_t gwords = (groups_of(g, p->shift) + 31) >> 5;
@@ -789,6 +799,18 @@ int wg_run_seed(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p,
     ::wg::count_launch();
     WG_CHECK_LAUNCH("run_init");
     if (g->n == 0) return WG_OK;
+    if (h_all_counts4) {
+        // every vertex in frontier 0 with a dense first iteration (the caller's
+        // check): the counts are the graph's totals, no compaction pass
+        const uint64_t es = h_all_counts4[3];
+        WG_REQUIRE(!(p->flags & WG_RUN_KEEP_LISTS) && !(g->edges > 0 && es < p->wedge_limit),
+                   "all-vertices seed needs a dense first iteration without member lists");
+        seed_all_record_kernel<<<1, 1, 0, s>>>(&b->recs[0], h_all_counts4[0], h_all_counts4[1], h_all_counts4[2],
+                                               es);
+        ::wg::count_launch();
+        WG_CHECK_LAUNCH("seed record");
+        return WG_OK;
+    }
     return launch_frontier_compaction(g, d_init_words, b->bcount, bcount_ticket(g, p->shift, b->bcount),
                                       b->fvert[0], b->fpref[0], b->tstart[0],
                                       &b->recs[0], s, (p->flags & WG_RUN_KEEP_LISTS) ? 1 : 0, p->wedge_limit);
@@ -796,7 +818,7 @@ int wg_run_seed(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p,
 
 int wg_run_init(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p,
                 const uint32_t *d_init_words, void *stream) {
-    return wg_run_seed(g, b, p, nullptr, d_init_words, stream);
+    return wg_run_seed(g, b, p, nullptr, d_init_words, nullptr, stream);
 }
 
 static int enqueue_one(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p,

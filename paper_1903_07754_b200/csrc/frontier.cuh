@@ -327,6 +327,47 @@ __device__ __forceinline__ void frontier_list_body(const uint32_t *words, uint64
     }
 }
 
+// The same ordered list, one WORD per thread (block = FB_WORDS threads = one
+// chunk): the thread counts its word's members (index lengths of its set
+// bits only), the block scans the three counts once on top of the chunk's
+// prefix (bcount, from the count pass) and each thread writes its members.
+// Reads the bitmap once and the degrees of members only -- no recount of
+// the whole chunk (frontier_list_body) -- so a sparse frontier costs little.
+__device__ __forceinline__ void frontier_list_words(const uint32_t *words, uint64_t nbits,
+                                                    const uint64_t *idx_off, const uint32_t *outdeg,
+                                                    const uint64_t *bcount, uint32_t *fvert, uint32_t *fpref,
+                                                    uint32_t *tstart, const wg_iter_rec *rec, uint64_t chunk) {
+    __shared__ uint64_t sm[33];
+    if (*(volatile const uint64_t *)&rec->reserved[2]) return;  // nobody consumes the list (block-uniform)
+    const uint64_t w = chunk * FB_WORDS + threadIdx.x;
+    const uint32_t x = masked_word(words, w, nbits);
+    uint64_t nz = 0, ent = 0, z = 0;
+    for (uint32_t m = x; m; m &= m - 1) {
+        const uint64_t u = (w << 5) + __ffs(m) - 1;
+        const uint64_t len = idx_off ? idx_off[u + 1] - idx_off[u] : outdeg[u];
+        nz += len != 0;
+        ent += len;
+        z += len == 0;
+    }
+    uint64_t nzp = block_exclusive_sum(nz, sm, (uint64_t *)nullptr) + bcount[4 * chunk];
+    uint64_t entp = block_exclusive_sum(ent, sm, (uint64_t *)nullptr) + bcount[4 * chunk + 1];
+    uint64_t zp = block_exclusive_sum(z, sm, (uint64_t *)nullptr) + bcount[4 * chunk + 2];
+    for (uint32_t m = x; m; m &= m - 1) {
+        const uint64_t u = (w << 5) + __ffs(m) - 1;
+        const uint64_t len = idx_off ? idx_off[u + 1] - idx_off[u] : outdeg[u];
+        if (len) {
+            fvert[nzp] = (uint32_t)u;
+            fpref[nzp] = (uint32_t)entp;
+            if (tstart) mark_tile_starts(tstart, entp, len, (uint32_t)nzp);
+            ++nzp;
+            entp += len;
+        } else {
+            fvert[nbits - 1 - zp] = (uint32_t)u;
+            ++zp;
+        }
+    }
+}
+
 __global__ void __launch_bounds__(CB_THREADS) frontier_count_kernel(const uint32_t *words, uint64_t nbits,
                                                                     const uint64_t *idx_off,
                                                                     const uint32_t *outdeg, uint64_t *bcount,
@@ -373,8 +414,8 @@ __global__ void __launch_bounds__(CB_THREADS) loop_frontier_list_kernel(LoopCtx 
     WG_KTS(it, KTS_FLIST);
     if (ctx_mode(c, it) != MODE_FULL) return;
     const int k = (int)(it & 1);
-    frontier_list_body(k ? f.fbits[1] : f.fbits[0], n, idx_off, outdeg, bcount, k ? f.fvert[1] : f.fvert[0],
-                       k ? f.fpref[1] : f.fpref[0], k ? f.tstart[1] : f.tstart[0], ctx_out(c, it));
+    frontier_list_words(k ? f.fbits[1] : f.fbits[0], n, idx_off, outdeg, bcount, k ? f.fvert[1] : f.fvert[0],
+                        k ? f.fpref[1] : f.fpref[0], k ? f.tstart[1] : f.tstart[0], ctx_out(c, it), blockIdx.x);
 }
 
 // ---------------- K3: Wedge transform --------------------------------------

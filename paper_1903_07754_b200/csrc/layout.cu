@@ -1232,3 +1232,24 @@ extern "C" int wg_vector_offsets_from_dst(const wg_graph *g, uint32_t *d_voff, v
     WG_CHECK_LAUNCH("voff_from_dst");
     return WG_OK;
 }
+
+namespace {
+__global__ void first_lanes_kernel(uint32_t n, uint32_t width, const uint32_t *voff, const uint32_t *vsrc,
+                                   uint32_t *vfirst) {
+    for (uint64_t d = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; d < n; d += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t v0 = voff[d], v1 = voff[d + 1];
+        vfirst[d] = v1 > v0 ? vsrc[(uint64_t)v0 * width] : WG_NO_LANE;
+    }
+}
+}  // namespace
+
+extern "C" int wg_first_lanes(const wg_graph *g, const uint32_t *d_voff, uint32_t *d_vfirst, void *stream) {
+    WG_REQUIRE(g && d_voff && d_vfirst, "null argument");
+    WG_REQUIRE(g->nvec == 0 || g->vsrc, "null vsrc");
+    cudaStream_t s = as_stream(stream);
+    if (g->n == 0) return WG_OK;
+    first_lanes_kernel<<<grid_for(g->n, 256, 8), 256, 0, s>>>(g->n, g->width, d_voff, g->vsrc, d_vfirst);
+    ::wg::count_launch();
+    WG_CHECK_LAUNCH("first_lanes");
+    return WG_OK;
+}

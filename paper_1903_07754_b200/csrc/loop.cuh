@@ -48,7 +48,7 @@ __device__ __forceinline__ int ctx_mode(const LoopCtx &c, uint64_t it) {
 enum : int {
     KTS_DECIDE = 0, KTS_SPARSE_GATE, KTS_TRANSFORM, KTS_GROUP_COUNT, KTS_GROUP_LIST, KTS_PULL_WEDGE,
     KTS_PULL_SPARSE, KTS_DENSE_DST, KTS_DENSE_TMA, KTS_BOTTOM_UP, KTS_FLOOR, KTS_IDENT, KTS_FCOUNT, KTS_FLIST,
-    KTS_FINALIZE, KTS_STEP, KTS_IDS
+    KTS_FINALIZE, KTS_STEP, KTS_SEED, KTS_PERSIST, KTS_IDS
 };
 static __device__ uint64_t *g_kts = nullptr;
 static __device__ uint64_t g_kts_cap = 0;

@@ -767,6 +767,7 @@ __global__ void __launch_bounds__(256) bottom_up_pull_kernel(LoopCtx c, wg_graph
 // (count_epilogue) -- no separate count pass over the bitmap.  Results and
 // counters are those of the reference's full scan (every vector touched;
 // bottom-up: the vectors of unvisited destinations).
+static_assert(PULL_THREADS == FB_WORDS, "the persistent loop runs frontier_list_words with one word per thread");
 constexpr uint32_t DST_LIGHT = 8;  // vectors walked by one thread
 constexpr int DST_K = 4;           // destinations per thread in flight (one warp = DST_K words)
 constexpr int DSTK_FLOOR = 0, DSTK_BOTTOM_UP = 1;
@@ -806,14 +807,15 @@ __device__ __forceinline__ void dense_dst_phase(const LoopCtx &c, uint64_t it, c
         }
     }
     const unsigned lane = lane_id();
-    uint64_t touched = 0;
+    uint64_t touched = 0, lanes_rd = 0, gath = 0;  // algorithmic work (the record's lanes_read / gathers)
     const uint64_t n = g.n;
     const uint64_t span = 32ull * DST_K;  // destinations per warp step, word-aligned
     for (uint64_t wb = warp0 * span; wb < n; wb += nwarps * span) {
         T p[DST_K], agg[DST_K];
-        uint32_t v0[DST_K], v1[DST_K];
+        uint32_t v0[DST_K], v1[DST_K], s0[DST_K];
         bool need[DST_K];
-        // (a) prev[d] and d's vector range, DST_K destinations in flight
+        // (a) prev[d], d's vector range and (FLOOR) its smallest source, DST_K
+        // destinations in flight
 #pragma unroll
         for (int k = 0; k < DST_K; ++k) {
             const uint64_t d = wb + 32 * k + lane;
@@ -821,6 +823,7 @@ __device__ __forceinline__ void dense_dst_phase(const LoopCtx &c, uint64_t it, c
             p[k] = ok ? prev[d] : (T)0;
             v0[k] = ok ? voff[d] : 0u;
             v1[k] = ok ? voff[d + 1] : 0u;
+            if constexpr (KIND == DSTK_FLOOR) s0[k] = ok && g.vfirst ? g.vfirst[d] : WG_NO_LANE;
         }
         // (b) FLOOR: the first lane of every destination not at the floor;
         // the out-degree of every destination that may join the frontier
@@ -833,12 +836,17 @@ __device__ __forceinline__ void dense_dst_phase(const LoopCtx &c, uint64_t it, c
             deg[k] = need[k] ? g.outdeg[wb + 32 * k + lane] : 0u;
         }
         if constexpr (KIND == DSTK_FLOOR) {
-            uint32_t s0[DST_K];
+            if (!g.vfirst) {
 #pragma unroll
-            for (int k = 0; k < DST_K; ++k) s0[k] = need[k] ? g.vsrc[(uint64_t)v0[k] * W] : 0u;
+                for (int k = 0; k < DST_K; ++k) s0[k] = need[k] ? g.vsrc[(uint64_t)v0[k] * W] : 0u;
+            }
 #pragma unroll
             for (int k = 0; k < DST_K; ++k)
-                if (need[k]) agg[k] = exact_first ? (T)s0[k] : prev[s0[k]];
+                if (need[k]) {
+                    agg[k] = exact_first ? (T)s0[k] : prev[s0[k]];
+                    lanes_rd += 1;
+                    gath += exact_first ? 0 : 1;
+                }
         } else {
 #pragma unroll
             for (int k = 0; k < DST_K; ++k) touched += need[k] ? v1[k] - v0[k] : 0u;
@@ -858,6 +866,8 @@ __device__ __forceinline__ void dense_dst_phase(const LoopCtx &c, uint64_t it, c
                     uint32_t src[W], src2[W], wt[W];
                     load_lanes<W>(g.vsrc, v, src);
                     const bool two = v + 1 < v1[k];
+                    lanes_rd += two ? 2 * W : W;
+                    gath += two ? 2 * W : W;
                     if (two) load_lanes<W>(g.vsrc, v + 1, src2);
                     T m = fold_lanes<T, W, false>(src, wt, prev, INF, ovf);
                     if (two) {
@@ -873,6 +883,8 @@ __device__ __forceinline__ void dense_dst_phase(const LoopCtx &c, uint64_t it, c
                     uint32_t src[W], src2[W];
                     load_lanes<W>(g.vsrc, v, src);
                     const bool two = v + 1 < v1[k];
+                    lanes_rd += two ? 2 * W : W;
+                    gath += two ? 2 * W : W;
                     if (two) load_lanes<W>(g.vsrc, v + 1, src2);
 #pragma unroll
                     for (int l = 0; l < W; ++l) hit |= src[l] != WG_NO_LANE && in_prev_frontier(src[l]);
@@ -896,6 +908,8 @@ __device__ __forceinline__ void dense_dst_phase(const LoopCtx &c, uint64_t it, c
                     if (v < h1) {
                         uint32_t src[W], wt[W];
                         load_lanes<W>(g.vsrc, v, src);
+                        lanes_rd += W;
+                        gath += W;
                         if constexpr (KIND == DSTK_FLOOR) {
                             const T m = fold_lanes<T, W, false>(src, wt, prev, INF, ovf);
                             hagg = m < hagg ? m : hagg;
@@ -967,6 +981,10 @@ __device__ __forceinline__ void dense_dst_phase(const LoopCtx &c, uint64_t it, c
         }
     }
     if (ovf) out->overflow = 1;
+    lanes_rd = warp_sum(lanes_rd);
+    gath = warp_sum(gath);
+    if (lane == 0 && lanes_rd) atomicAdd((unsigned long long *)&out->lanes_read, (unsigned long long)lanes_rd);
+    if (lane == 0 && gath) atomicAdd((unsigned long long *)&out->gathers, (unsigned long long)gath);
     if constexpr (KIND == DSTK_FLOOR) {
         if (blockIdx.x == 0 && threadIdx.x == 0)
             atomicAdd((unsigned long long *)&out->vectors_touched, (unsigned long long)g.nvec);
@@ -1491,7 +1509,7 @@ __device__ __forceinline__ void end_of_iteration(const LoopCtx &c, uint64_t it, 
         }
         uint64_t *q = (uint64_t *)&c.recs[(it + zero_ahead) % c.ring];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) q[i] = 0;
+        for (int i = 0; i < (int)(sizeof(wg_iter_rec) / 8); ++i) q[i] = 0;
     }
 }
 
@@ -1553,6 +1571,7 @@ __global__ void __launch_bounds__(PULL_THREADS, SPARSE_MINB) sparse_loop_kernel(
     const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
     uint64_t *ctrl = const_cast<uint64_t *>(c.ctrl);
     const uint64_t first = *(volatile uint64_t *)&ctrl[0] + 1;
+    WG_KTS(first, KTS_PERSIST);
     uint64_t it = first;
     if (g.entries == 0) return;
     const bool fused = b.gbits2 != nullptr && b.glist2 != nullptr;
@@ -1561,7 +1580,7 @@ __global__ void __launch_bounds__(PULL_THREADS, SPARSE_MINB) sparse_loop_kernel(
     if (tid == 0) {
         for (int a = 1; a <= (fused ? 2 : 1); ++a) {
             uint64_t *q = (uint64_t *)&c.recs[(first + a) % c.ring];
-            for (int i = 0; i < 16; ++i) q[i] = 0;
+            for (int i = 0; i < (int)(sizeof(wg_iter_rec) / 8); ++i) q[i] = 0;
         }
     }
     grid.sync();
@@ -1580,19 +1599,18 @@ __global__ void __launch_bounds__(PULL_THREADS, SPARSE_MINB) sparse_loop_kernel(
                 phase_stamp(it, 0);
                 if (it > first) end_of_iteration<T>(c, it - 1, prev_mode, b, tid, nthreads, 2, true);
                 dense_dst_phase<T, W, KIND>(c, it, g, b, inc, sentinel, gwarp, nwarps);
+                // the last block to finish scans the per-chunk counts (ticket)
+                count_epilogue(nchunks, (uint64_t *)b.work, b.bcount, true, b.ticket, ctx_out(c, it), c.keep_lists,
+                               c.edges, c.wedge_limit);
                 grid.sync();
                 phase_stamp(it, 1);
-                if (blockIdx.x == 0)
-                    count_tail(nchunks, (uint64_t *)b.work, b.bcount, true, ctx_out(c, it), c.keep_lists, c.edges,
-                               c.wedge_limit);
-                grid.sync();
                 phase_stamp(it, 2);
                 if (!*(volatile const uint64_t *)&ctx_out(c, it)->reserved[2]) {  // a Wedge iteration follows
                     const int k = (int)(it & 1);
                     const uint64_t *off = (g.flags & WG_GRAPH_LENS_ARE_DEGREES) ? nullptr : g.idx_off;
                     for (uint64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
-                        frontier_list_body(b.fbits[k], b.n, off, g.outdeg, b.bcount, b.fvert[k], b.fpref[k],
-                                           b.tstart[k], ctx_out(c, it), ch);
+                        frontier_list_words(b.fbits[k], b.n, off, g.outdeg, b.bcount, b.fvert[k], b.fpref[k],
+                                            b.tstart[k], ctx_out(c, it), ch);
                         __syncthreads();
                     }
                     grid.sync();
@@ -1688,7 +1706,7 @@ __global__ void __launch_bounds__(PULL_THREADS, SPARSE_MINB) sparse_loop_kernel(
                     po->active_edges = *(volatile const uint64_t *)&ctx_in(c, ip)->out_edge_sum;
                 }
                 uint64_t *q = (uint64_t *)&c.recs[(it + 2) % c.ring];
-                for (int i = 0; i < 16; ++i) q[i] = 0;
+                for (int i = 0; i < (int)(sizeof(wg_iter_rec) / 8); ++i) q[i] = 0;
             }
         }
         // a vertex with a long index list joined frontier(it-1): the groups of

@@ -123,6 +123,7 @@ class DeviceGraph:
         self.lens_are_degrees = bool(lens_are_degrees)
         self.vw8 = vw8  # byte copy of vw when every weight <= 255 (the dense pull streams it)
         self.voff = None  # [n+1] per-destination vector offsets (ensure_voff; destination-major pulls)
+        self.vfirst = None  # [n] each destination's smallest source (ensure_voff)
         self._struct = None
 
     def narrow_weights(self, stream=None) -> bool:
@@ -294,6 +295,7 @@ class DeviceGraph:
         if g.voff is not None:
             g.ensure_voff(comp, refresh=True)
         g._degrees_src = degrees  # the out-degrees this graph holds (engine._with_degrees)
+        g._all_counts = None
         g.vw8 = None
         if weighted:
             g.narrow_weights(comp)
@@ -585,8 +587,21 @@ class DeviceGraph:
                                    _ptr(self.vsrc), _ptr(self.vdst), _ptr(self.vw), _ptr(self.idx_off),
                                    _ptr(self.idx_pos), _ptr(self.outdeg),
                                    _lib.WG_GRAPH_LENS_ARE_DEGREES if self.lens_are_degrees else 0,
-                                   _ptr(self.vw8), _ptr(self.voff))
+                                   _ptr(self.vw8), _ptr(self.voff), _ptr(self.vfirst))
         return self._struct
+
+    def all_vertex_counts(self):
+        """Counts of the frontier holding every vertex (cached): members with
+        index entries, their entries, members without, out-degree sum."""
+        c = getattr(self, "_all_counts", None)
+        if c is None:
+            torch = _torch()
+            deg = self.outdeg[: self.n].to(torch.int64) & U32_INF
+            lens = deg if self.lens_are_degrees else (self.idx_off[1: self.n + 1] - self.idx_off[: self.n])
+            nz = int((lens > 0).sum().item())
+            c = (nz, int(lens.sum().item()), self.n - nz, int(deg.sum().item()))
+            self._all_counts = c
+        return c
 
     def ensure_voff(self, stream=None, refresh: bool = False):
         """Per-destination vector offsets (wg_vector_offsets_from_dst), kept
@@ -594,7 +609,7 @@ class DeviceGraph:
         disables them)."""
         if os.environ.get("WG_DST_MAJOR", "1") == "0":
             if self.voff is not None:
-                self.voff = None
+                self.voff = self.vfirst = None
                 self._struct = None
             return None
         if self.voff is not None and not refresh:
@@ -602,9 +617,15 @@ class DeviceGraph:
         torch = _torch()
         if self.voff is None or self.voff.numel() != self.n + 1:
             self.voff = torch.empty(self.n + 1, dtype=torch.int32, device=self.vdst.device)
+            self.vfirst = torch.empty(max(self.n, 1), dtype=torch.int32, device=self.vdst.device)
         self._struct = None
-        check(_lib.load().wg_vector_offsets_from_dst(ctypes.byref(self.struct()), _ptr(self.voff),
-                                                     _lib.stream_ptr(stream)))
+        L = _lib.load()
+        vf = self.vfirst
+        self.vfirst = None  # the struct handed to the builders carries voff only
+        check(L.wg_vector_offsets_from_dst(ctypes.byref(self.struct()), _ptr(self.voff), _lib.stream_ptr(stream)))
+        check(L.wg_first_lanes(ctypes.byref(self.struct()), _ptr(self.voff), _ptr(vf), _lib.stream_ptr(stream)))
+        self.vfirst = vf
+        self._struct = None
         return self.voff
 
     def signature(self) -> tuple:
@@ -755,6 +776,8 @@ class IterRecord:
     frontier_out_size: int
     covered_vectors: int
     transform_entries: int
+    lanes_read: int = 0   # destination-major dense pulls: lanes read ...
+    gathers: int = 0      # ... and gathers / bit tests made (their algorithmic bytes)
 
 
 @dataclass
@@ -884,8 +907,13 @@ class DeviceLoop:
             raise ValueError("initial values do not match the loop's value buffers")
         self._level_base = int(level_base)
         p = self.params(kern, threshold, first_hit, identity_init)
+        counts = None
+        if getattr(init_words, "_wg_all", False) and not (p.flags & _lib.WG_RUN_KEEP_LISTS):
+            c4 = self.g.all_vertex_counts()
+            if not (self.g.edges > 0 and c4[3] < p.wedge_limit):  # iteration 1 is dense
+                counts = (ctypes.c_uint64 * 4)(*c4)
         check(_lib.load().wg_run_seed(ctypes.byref(self.g.struct()), ctypes.byref(self.bufs), ctypes.byref(p),
-                                      _ptr(init_values), _ptr(init_words), _lib.stream_ptr(stream)))
+                                      _ptr(init_values), _ptr(init_words), counts, _lib.stream_ptr(stream)))
         return p
 
     def enqueue(self, p: WgRunParams, it_begin: int, count: int, stream=None) -> None:
@@ -949,7 +977,8 @@ class DeviceLoop:
             if int(r[10]):
                 raise _lib.OverflowError32(_lib.WG_EOVERFLOW, "uint32 value overflow in device loop")
             records.append(IterRecord(it0 + j, MODE_NAMES[mode], int(r[1]), int(r[2]), int(r[3]),
-                                      int(r[7]) if mode == 2 else 0, int(r[8]) if mode == 2 else 0))
+                                      int(r[7]) if mode == 2 else 0, int(r[8]) if mode == 2 else 0,
+                                      int(r[16]), int(r[17])))
             if trace is not None:
                 trace(self, it0 + j)
             if int(r[4]) == 0:
@@ -1012,7 +1041,8 @@ class DeviceLoop:
                 if int(r[10]):
                     raise _lib.OverflowError32(_lib.WG_EOVERFLOW, "uint32 value overflow in device loop")
                 records.append(IterRecord(it + j, MODE_NAMES[mode], int(r[1]), int(r[2]), int(r[3]),
-                                          int(r[7]) if mode == 2 else 0, int(r[8]) if mode == 2 else 0))
+                                          int(r[7]) if mode == 2 else 0, int(r[8]) if mode == 2 else 0,
+                                          int(r[16]), int(r[17])))
                 last = it + j
                 if trace is not None:
                     trace(self, last)
@@ -1090,6 +1120,7 @@ def initial_words(n: int, members: np.ndarray):
 def all_words(n: int):
     torch = _torch()
     words = torch.full((max((n + 31) >> 5, 1),), -1, dtype=torch.int32, device="cuda")
+    words._wg_all = True
     return words
 
 

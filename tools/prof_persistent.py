@@ -16,7 +16,7 @@ el, topo = bench.make_graph(wl)
 g = topo.device
 prog = wg.make_program(wl["app"], None if wl["app"] == "cc" else 0)
 loop = dv.DeviceLoop(g, {1: 0, 2: 1, 4: 2, 8: 3, 16: 4}[wl["vpg"]], _lib.WG_VAL_U32)
-init = dv.encode_values(_initial_values(prog, g.n), _lib.WG_VAL_U32)
+init = dv.encode_values(_initial_values(prog, g.n), _lib.WG_VAL_U32)  # noqa
 words = dv.all_words(g.n) if wl["app"] == "cc" else dv.initial_words(g.n, np.array([0]))
 p = loop.seed(init, words, prog.kernel, Fraction(wl["thr"]))
 L = _lib.load()
