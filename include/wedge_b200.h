@@ -444,19 +444,25 @@ uint64_t wg_launch_count(void);
 /* ---------------- PageRank (BASELINE config 5) ---------------------------- */
 /* float32 ranks, damping, fixed iterations, dangling mass spread uniformly.
  * d_rank [n] out; d_acc [n], d_contrib [n] scratch; d_scal [4] doubles scratch. */
+/* Deterministic (no float atomics: bit-identical runs on the same GPU and
+ * build).  d_ws: wg_pagerank_ws_bytes(g) bytes of device scratch. */
+size_t wg_pagerank_ws_bytes(const wg_graph *g);
 int wg_pagerank(const wg_graph *g, int iterations, double damping, float *d_rank, float *d_acc,
-                float *d_contrib, double *d_scal, void *stream);
+                float *d_contrib, double *d_scal, void *d_ws, size_t ws_bytes, void *stream);
 /* The two halves of one iteration, for destination-sharded runs (SURVEY
  * §8(e)): prep(it) applies the accumulated sums of iteration it-1 to all n
  * ranks (it = 0: 1/n), writes d_rank when non-null, zeroes d_acc, builds the
  * contributions r/outdeg and the dangling mass of iteration it (d_scal[4],
- * zeroed at it = 0).  prep(iterations) with d_rank yields the result. */
+ * zeroed at it = 0).  prep(iterations) with d_rank yields the result.
+ * d_ws: wg_pagerank_prep_ws_bytes(n) bytes (shared by prep and pull). */
+size_t wg_pagerank_prep_ws_bytes(uint32_t n);
 int wg_pagerank_prep(uint32_t n, int it, double damping, const uint32_t *d_outdeg, float *d_acc,
-                     float *d_contrib, float *d_rank, double *d_scal, void *stream);
-/* Sum the contributions of g's vectors into d_acc[dst - dst_base] (the
- * caller zeroes the destinations g holds first). */
-int wg_pagerank_pull(const wg_graph *g, const float *d_contrib, float *d_acc, uint32_t dst_base,
+                     float *d_contrib, float *d_rank, double *d_scal, void *d_ws, size_t ws_bytes,
                      void *stream);
+/* Sum the contributions of g's vectors into d_acc[dst - dst_base] (the
+ * caller zeroes the destinations g holds first).  d_ws as for prep. */
+int wg_pagerank_pull(const wg_graph *g, const float *d_contrib, float *d_acc, uint32_t dst_base,
+                     void *d_ws, size_t ws_bytes, void *stream);
 
 /* ---------------- input generation (graph_io.py:87-221) ------------------- */
 /* RMAT edges m = edge_factor << scale from PCG64(state, inc) exactly like

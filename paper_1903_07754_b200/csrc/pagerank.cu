@@ -1,27 +1,52 @@
-// pagerank.cu — dense PageRank pull (K8).  No reference implementation
-// exists (pkg/tests/test_apps.py:167-169); semantics follow
-// BASELINE.json config 5: float32 ranks, damping d, fixed iterations,
-// dangling mass redistributed uniformly:
+// pagerank.cu — dense PageRank pull (K8), deterministic.  No reference
+// implementation exists (pkg/tests/test_apps.py:167-169);
+// semantics follow BASELINE.json config 5: float32 ranks, damping d, fixed
+// iterations, dangling mass redistributed uniformly:
 //   r0 = 1/N;  r'(v) = (1-d)/N + d * (sum_{u->v} r(u)/outdeg(u) + D/N),
 //   D = sum of r(u) over outdeg(u) = 0.
-// The pull reuses the min-plus tile body with a float segmented SUM; only a
-// destination shared with a neighbouring tile is combined with atomicAdd.
-// The apply of iteration i is fused into the contribution pass of i+1, so an
-// iteration is two kernels: prep (V-sized) and pull (E-sized).
+//
+// Bit-reproducible by construction: no float atomics.
+//  * pull: every warp walks its own contiguous range of 32-vector tiles in
+//    order with a carried segment (the min-plus tile body with a float
+//    segmented SUM), so a destination is summed in one fixed order and
+//    written with a plain store -- except a destination whose vectors cross
+//    a warp-range boundary: each warp records its first and last segment's
+//    partial sum, and pr_fixup adds them in warp order.
+//  * dangling mass: per-block double partials in fixed slots, summed in slot
+//    order by one warp (pr_dangling).
+// An iteration is prep (V-sized: apply of the previous sums + contributions)
+// -> dangling sum -> pull (E-sized) -> fixup.  The fixed order depends only
+// on the launch configuration (grid sizes from the occupancy query), so runs
+// on the same GPU and build are bit-identical.
 #include "common.cuh"
+#include "tma.cuh"  // warp_range
 
 using namespace wg;
 
 namespace {
 
+constexpr unsigned PR_THREADS = 256;
+constexpr uint32_t PR_NONE = 0xffffffffu;
+
+// Per-warp boundary record of the pull: the first segment when it continues
+// a destination from the previous range, the last when it continues into
+// the next; `single`: the whole range is one destination (a middle piece).
+struct PrBound {
+    uint32_t hd, td;  // destinations (PR_NONE: that end is complete)
+    float hs, ts;
+    uint32_t single, pad;
+};
+
+unsigned prep_grid(uint32_t n) { return grid_for(n, PR_THREADS * 4, 8); }
+
 // prep(it): r = it ? base(D_{it-1}) + d*acc : 1/N; acc = 0; contrib = r/outdeg;
-// accumulate D_it into scal[it % 3]; zero scal[(it+1) % 3].
-__global__ void __launch_bounds__(256) pr_prep(uint32_t n, int it, double damping,
-                                               const uint32_t *outdeg, float *acc, float *contrib,
-                                               float *rank_out, double *scal) {
+// the block's dangling mass of r into dpart[block].
+__global__ void __launch_bounds__(PR_THREADS) pr_prep(uint32_t n, int it, double damping,
+                                                      const uint32_t *outdeg, float *acc, float *contrib,
+                                                      float *rank_out, const double *scal, double *dpart) {
     __shared__ double sm[33];
     double dang = 0.0;
-    const float base = it ? (float)((1.0 - damping) / n + damping * scal[(it + 2) % 3] / n) : 0.f;
+    const float base = it ? (float)((1.0 - damping) / n + damping * scal[0] / n) : 0.f;
     const float df = (float)damping;
     const float r0 = (float)(1.0 / n);
     for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
@@ -37,56 +62,141 @@ __global__ void __launch_bounds__(256) pr_prep(uint32_t n, int it, double dampin
         }
         if (rank_out) rank_out[v] = r;
     }
-    double tot = block_sum(dang, sm);
-    if (threadIdx.x == 0) {
-        if (tot != 0.0) atomicAdd(&scal[it % 3], tot);
-        if (blockIdx.x == 0) scal[(it + 1) % 3] = 0.0;
-    }
+    const double tot = block_sum(dang, sm);
+    if (threadIdx.x == 0) dpart[blockIdx.x] = tot;
+}
+
+// D = sum of the block partials in slot order (one warp, fixed tree).
+__global__ void pr_dangling(const double *dpart, unsigned nparts, double *scal) {
+    double s = 0.0;
+    for (unsigned i = threadIdx.x; i < nparts; i += 32) s += dpart[i];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(FULL, s, off);
+    if (threadIdx.x == 0) scal[0] = s;
 }
 
 template <int W, bool SHIFT>
-__global__ void __launch_bounds__(256) pr_pull(wg_graph g, const float *contrib, float *acc, uint32_t base_) {
+__global__ void __launch_bounds__(PR_THREADS) pr_pull(wg_graph g, const float *__restrict__ contrib, float *acc,
+                                                      uint32_t base_, PrBound *bounds) {
     const uint32_t base = SHIFT ? base_ : 0u;  // destination-sharded runs index a slice
     const unsigned lane = lane_id();
     const uint64_t gwarp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    const uint64_t ntiles = (g.nvec + 31) >> 5;
-    for (uint64_t tile = gwarp; tile < ntiles; tile += nwarps) {
-        const uint64_t p = (tile << 5) + lane;
-        const bool valid = p < g.nvec;
-        const uint32_t d = valid ? g.vdst[p] : 0xffffffffu;
-        float sum = 0.f;
-        if (valid) {
-            uint32_t src[W];
-            load_lanes<W>(g.vsrc, p, src);
+    const uint64_t nvec = g.nvec;
+    uint64_t t0, t1;
+    warp_range((nvec + 31) >> 5, gwarp, nwarps, t0, t1);
+    PrBound rec{PR_NONE, PR_NONE, 0.f, 0.f, 0u, 0u};
+    if (t0 < t1) {
+        const uint64_t p_lo = t0 << 5, p_hi = (t1 << 5) < nvec ? (t1 << 5) : nvec;
+        // destinations just outside the range: a segment touching them is shared
+        const uint32_t dleft = p_lo > 0 ? g.vdst[p_lo - 1] : PR_NONE;
+        const uint32_t dright = p_hi < nvec ? g.vdst[p_hi] : PR_NONE;
+        uint32_t cd = PR_NONE;  // carried segment (warp-uniform): destination,
+        float cs = 0.f;         // partial sum, and whether it is the range's
+        bool cfirst = false;    // first segment
+        for (uint64_t tile = t0; tile < t1; ++tile) {
+            const uint64_t p = (tile << 5) + lane;
+            const bool valid = p < nvec;
+            const uint32_t d = valid ? g.vdst[p] : PR_NONE;
+            float sum = 0.f;
+            if (valid) {
+                uint32_t src[W];
+                load_lanes<W>(g.vsrc, p, src);
 #pragma unroll
-            for (int l = 0; l < W; ++l)
-                if (src[l] != WG_NO_LANE) sum += contrib[src[l]];
+                for (int l = 0; l < W; ++l)
+                    if (src[l] != WG_NO_LANE) sum += contrib[src[l]];
+            }
+            const uint32_t dn = __shfl_down_sync(FULL, d, 1);
+            const uint32_t dp = __shfl_up_sync(FULL, d, 1);
+            const bool head = lane == 0 || dp != d;
+            const bool tail = lane == 31 || dn != d;
+            const unsigned heads = __ballot_sync(FULL, head);
+            const unsigned head_lane = 31 - __clz(heads & (0xffffffffu >> (31 - lane)));
+            const unsigned dist = lane - head_lane;
+            const unsigned maxd = __reduce_max_sync(FULL, dist);
+            for (unsigned off = 1; off <= maxd; off <<= 1) {
+                const float o = __shfl_up_sync(FULL, sum, off);
+                if (off <= dist) sum += o;
+            }
+            // the carried segment ended at the previous tile's last lane: close it
+            const uint32_t d0 = __shfl_sync(FULL, d, 0);
+            if (cd != PR_NONE && d0 != cd) {
+                if (cfirst && cd == dleft) {
+                    rec.hd = cd;  // (warp-uniform)
+                    rec.hs = cs;
+                } else if (lane == 0) {
+                    acc[cd - base] = cs;
+                }
+            }
+            // the tile's first segment continues the carried one (earlier tiles first)
+            const bool cont = head_lane == 0 && cd != PR_NONE && d == cd;
+            if (cont) sum = cs + sum;
+            const bool seg_first = head_lane == 0 && (cont ? cfirst : tile == t0);
+            if (tail && valid && lane != 31) {  // a segment closed inside this tile
+                if (seg_first && d == dleft) {  // ... continuing the previous range's last one
+                    rec.hd = d;
+                    rec.hs = sum;
+                } else {
+                    acc[d - base] = sum;
+                }
+            }
+            // the segment touching lane 31 is carried into the next tile
+            cd = __shfl_sync(FULL, d, 31);
+            cs = __shfl_sync(FULL, sum, 31);
+            cfirst = __shfl_sync(FULL, seg_first, 31);
         }
-        const uint32_t dn = __shfl_down_sync(FULL, d, 1);
-        const uint32_t dp = __shfl_up_sync(FULL, d, 1);
-        const bool head = lane == 0 || dp != d;
-        const bool tail = lane == 31 || dn != d;
-        const unsigned heads = __ballot_sync(FULL, head);
-        const unsigned head_lane = 31 - __clz(heads & (0xffffffffu >> (31 - lane)));
-        // segmented sum limited to the longest segment of the tile
-        const unsigned dist = lane - head_lane;
-        const unsigned maxd = __reduce_max_sync(FULL, dist);
-        for (unsigned off = 1; off <= maxd; off <<= 1) {
-            const float o = __shfl_up_sync(FULL, sum, off);
-            if (off <= dist) sum += o;
+        // the range's last segment
+        if (cd != PR_NONE) {
+            const bool shared_right = cd == dright;
+            const bool shared_left = cfirst && cd == dleft;
+            if (shared_right) {
+                rec.td = cd;
+                rec.ts = cs;
+                rec.single = shared_left ? 1u : 0u;  // a middle piece of one destination
+            } else if (shared_left) {
+                rec.hd = cd;
+                rec.hs = cs;
+            } else if (lane == 0) {
+                acc[cd - base] = cs;
+            }
         }
-        if (tail && valid) {
-            bool complete = true;
-            if (head_lane == 0 && p >= lane + 1 && g.vdst[p - lane - 1] == d) complete = false;
-            if (lane == 31 && p + 1 < g.nvec && g.vdst[p + 1] == d) complete = false;
-            if (complete) acc[d - base] = sum;
-            else atomicAdd(&acc[d - base], sum);
+    }
+    // one record per warp: the head piece was set by the lane that closed it
+    const unsigned hl = __ballot_sync(FULL, rec.hd != PR_NONE);
+    if (hl) {
+        const int src = __ffs(hl) - 1;
+        rec.hd = __shfl_sync(FULL, rec.hd, src);
+        rec.hs = __shfl_sync(FULL, rec.hs, src);
+    }
+    if (lane == 0 && bounds) bounds[gwarp] = rec;
+}
+
+// Shared destinations: the warp whose range holds a destination's FIRST
+// piece (its last segment continues right and is not itself a continuation)
+// adds the following warps' pieces in order and stores the sum.
+template <bool SHIFT>
+__global__ void pr_fixup(const PrBound *bounds, uint64_t nwarps, float *acc, uint32_t base_) {
+    const uint32_t base = SHIFT ? base_ : 0u;
+    for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < nwarps;
+         w += (uint64_t)gridDim.x * blockDim.x) {
+        const PrBound r = bounds[w];
+        if (r.td == PR_NONE || r.single) continue;  // no piece starts here and continues
+        const uint32_t d = r.td;
+        float s = r.ts;
+        for (uint64_t k = w + 1; k < nwarps; ++k) {
+            const PrBound q = bounds[k];
+            if (q.single && q.td == d) {
+                s += q.ts;  // a middle piece
+                continue;
+            }
+            if (q.hd == d) s += q.hs;  // the destination's last piece
+            break;
         }
+        acc[d - base] = s;
     }
 }
 
-using PrPull = void (*)(wg_graph, const float *, float *, uint32_t);
+using PrPull = void (*)(wg_graph, const float *, float *, uint32_t, PrBound *);
 
 PrPull pick(int w, bool shift = false) {
     switch (w) {
@@ -98,64 +208,100 @@ PrPull pick(int w, bool shift = false) {
     return nullptr;
 }
 
-unsigned pull_grid(const wg_graph *g, PrPull pull) {
+unsigned pull_grid(PrPull pull) {
     int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pull, 256, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pull, PR_THREADS, 0);
     if (per_sm < 1) per_sm = 1;
-    return grid_for(g->nvec, 256, (unsigned)per_sm);
+    return (unsigned)(sm_count() * per_sm);  // one full wave: the warp ranges fix the summation order
+}
+
+struct PrWs {
+    PrBound *bounds;
+    double *dpart;
+};
+
+size_t ws_bytes(uint32_t n) {
+    return carve_size(sizeof(PrBound) * (size_t)sm_count() * 64) + carve_size(sizeof(double) * prep_grid(n ? n : 1));
+}
+
+int carve(uint32_t n, void *ws, size_t bytes, PrWs *w) {
+    Carve c{(char *)ws, 0, bytes};
+    w->bounds = c.take<PrBound>((size_t)sm_count() * 64);  // >= warps of one full wave (2048 threads / SM)
+    w->dpart = c.take<double>(prep_grid(n ? n : 1));
+    WG_REQUIRE(ws && w->bounds && w->dpart, "pagerank workspace too small (wg_pagerank_ws_bytes)");
+    return WG_OK;
+}
+
+int pull_and_fixup(const wg_graph *g, const float *contrib, float *acc, uint32_t base, const PrWs &w,
+                   cudaStream_t s) {
+    PrPull pull = pick((int)g->width, base != 0);
+    WG_REQUIRE(pull, "unsupported width %u", g->width);
+    if (!g->nvec) return WG_OK;
+    const unsigned grid = pull_grid(pull);
+    const uint64_t nwarps = (uint64_t)grid * (PR_THREADS / 32);
+    WG_REQUIRE(nwarps <= (uint64_t)sm_count() * 64, "pagerank pull grid exceeds its workspace");
+    pull<<<grid, PR_THREADS, 0, s>>>(*g, contrib, acc, base, w.bounds);
+    if (base) pr_fixup<true><<<grid_for(nwarps, 256, 4), 256, 0, s>>>(w.bounds, nwarps, acc, base);
+    else pr_fixup<false><<<grid_for(nwarps, 256, 4), 256, 0, s>>>(w.bounds, nwarps, acc, base);
+    ::wg::count_launch(2);
+    WG_CHECK_LAUNCH("pagerank pull");
+    return WG_OK;
+}
+
+int prep(uint32_t n, int it, double damping, const uint32_t *outdeg, float *acc, float *contrib, float *rank,
+         double *scal, const PrWs &w, cudaStream_t s) {
+    const unsigned vgrid = prep_grid(n);
+    pr_prep<<<vgrid, PR_THREADS, 0, s>>>(n, it, damping, outdeg, acc, contrib, rank, scal, w.dpart);
+    pr_dangling<<<1, 32, 0, s>>>(w.dpart, vgrid, scal);
+    ::wg::count_launch(2);
+    WG_CHECK_LAUNCH("pagerank prep");
+    return WG_OK;
 }
 
 }  // namespace
 
+extern "C" size_t wg_pagerank_ws_bytes(const wg_graph *g) { return g ? ws_bytes(g->n) : 0; }
+
 extern "C" int wg_pagerank(const wg_graph *g, int iterations, double damping, float *d_rank,
-                           float *d_acc, float *d_contrib, double *d_scal, void *stream) {
+                           float *d_acc, float *d_contrib, double *d_scal, void *d_ws, size_t ws_bytes_,
+                           void *stream) {
     WG_REQUIRE(g && d_rank && d_acc && d_contrib && d_scal, "null argument");
     WG_REQUIRE(iterations >= 0, "iterations must be >= 0");
     WG_REQUIRE(g->n > 0, "empty graph");
-    PrPull pull = pick((int)g->width);
-    WG_REQUIRE(pull, "unsupported width %u", g->width);
+    PrWs w;
+    int rc = carve(g->n, d_ws, ws_bytes_, &w);
+    if (rc) return rc;
     cudaStream_t s = as_stream(stream);
     WG_CUDA(cudaMemsetAsync(d_acc, 0, (uint64_t)g->n * 4, s));
     WG_CUDA(cudaMemsetAsync(d_scal, 0, 4 * sizeof(double), s));
-    unsigned vgrid = grid_for(g->n, 256 * 4, 8);
-    unsigned egrid = pull_grid(g, pull);
     for (int it = 0; it < iterations; ++it) {
-        pr_prep<<<vgrid, 256, 0, s>>>(g->n, it, damping, g->outdeg, d_acc, d_contrib, nullptr, d_scal); ::wg::count_launch();
-        if (g->nvec) {
-            pull<<<egrid, 256, 0, s>>>(*g, d_contrib, d_acc, 0u);
-            ::wg::count_launch();
-        }
+        if ((rc = prep(g->n, it, damping, g->outdeg, d_acc, d_contrib, nullptr, d_scal, w, s))) return rc;
+        if ((rc = pull_and_fixup(g, d_contrib, d_acc, 0u, w, s))) return rc;
     }
     // final apply: prep of iteration `iterations` writes the ranks
-    pr_prep<<<vgrid, 256, 0, s>>>(g->n, iterations, damping, g->outdeg, d_acc, d_contrib, d_rank,
-                                  d_scal); ::wg::count_launch();
-    WG_CHECK_LAUNCH("pagerank");
-    return WG_OK;
+    return prep(g->n, iterations, damping, g->outdeg, d_acc, d_contrib, d_rank, d_scal, w, s);
 }
 
+extern "C" size_t wg_pagerank_prep_ws_bytes(uint32_t n) { return ws_bytes(n); }
+
 extern "C" int wg_pagerank_prep(uint32_t n, int it, double damping, const uint32_t *d_outdeg,
-                                float *d_acc, float *d_contrib, float *d_rank, double *d_scal,
-                                void *stream) {
+                                float *d_acc, float *d_contrib, float *d_rank, double *d_scal, void *d_ws,
+                                size_t ws_bytes_, void *stream) {
     WG_REQUIRE(n > 0 && d_outdeg && d_acc && d_contrib && d_scal, "null argument");
     WG_REQUIRE(it >= 0, "iteration must be >= 0");
+    PrWs w;
+    int rc = carve(n, d_ws, ws_bytes_, &w);
+    if (rc) return rc;
     cudaStream_t s = as_stream(stream);
     if (it == 0) WG_CUDA(cudaMemsetAsync(d_scal, 0, 4 * sizeof(double), s));
-    pr_prep<<<grid_for(n, 256 * 4, 8), 256, 0, s>>>(n, it, damping, d_outdeg, d_acc, d_contrib, d_rank,
-                                                    d_scal);
-    ::wg::count_launch();
-    WG_CHECK_LAUNCH("pagerank_prep");
-    return WG_OK;
+    return prep(n, it, damping, d_outdeg, d_acc, d_contrib, d_rank, d_scal, w, s);
 }
 
 extern "C" int wg_pagerank_pull(const wg_graph *g, const float *d_contrib, float *d_acc,
-                                uint32_t dst_base, void *stream) {
+                                uint32_t dst_base, void *d_ws, size_t ws_bytes_, void *stream) {
     WG_REQUIRE(g && d_contrib && d_acc, "null argument");
-    PrPull pull = pick((int)g->width, dst_base != 0);
-    WG_REQUIRE(pull, "unsupported width %u", g->width);
-    if (!g->nvec) return WG_OK;
-    cudaStream_t s = as_stream(stream);
-    pull<<<pull_grid(g, pull), 256, 0, s>>>(*g, d_contrib, d_acc, dst_base);
-    ::wg::count_launch();
-    WG_CHECK_LAUNCH("pagerank_pull");
-    return WG_OK;
+    PrWs w;
+    int rc = carve(g->n, d_ws, ws_bytes_, &w);
+    if (rc) return rc;
+    return pull_and_fixup(g, d_contrib, d_acc, dst_base, w, as_stream(stream));
 }

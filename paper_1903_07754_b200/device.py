@@ -1196,10 +1196,14 @@ def pagerank(g: DeviceGraph, iterations: int = 20, damping: float = 0.85, stream
                 torch.empty(n, dtype=torch.float32, device="cuda"),
                 torch.empty(n, dtype=torch.float32, device="cuda"),
                 torch.zeros(4, dtype=torch.float64, device="cuda"))
-    rank, acc, contrib, scal = bufs
-    check(_lib.load().wg_pagerank(ctypes.byref(g.struct()), int(iterations), float(damping),
-                                  _ptr(rank), _ptr(acc), _ptr(contrib), _ptr(scal),
-                                  _lib.stream_ptr(stream)))
+    rank, acc, contrib, scal = bufs[:4]
+    L = _lib.load()
+    need = int(L.wg_pagerank_ws_bytes(ctypes.byref(g.struct())))
+    ws = getattr(g, "_pr_ws", None)
+    if ws is None or ws.numel() < need:
+        ws = g._pr_ws = torch.empty(need, dtype=torch.uint8, device="cuda")
+    check(L.wg_pagerank(ctypes.byref(g.struct()), int(iterations), float(damping), _ptr(rank), _ptr(acc),
+                        _ptr(contrib), _ptr(scal), _ptr(ws), ws.numel(), _lib.stream_ptr(stream)))
     return rank
 
 

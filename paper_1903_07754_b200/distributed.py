@@ -360,19 +360,25 @@ class DevicePageRankShard:
         self.scal = torch.zeros(4, dtype=torch.float64, device="cuda")
         self.part = torch.zeros(self.S, **f32)
         self.gathered = torch.empty(world * self.S, **f32)
+        L = _lib.load()
+        self.ws = torch.empty(max(int(L.wg_pagerank_prep_ws_bytes(n)),
+                                  int(L.wg_pagerank_ws_bytes(ctypes.byref(self.g.struct())))),
+                              dtype=torch.uint8, device="cuda")
 
     def prep(self, it: int, rank_out=None):
         L = self._lib.load()
         self._lib.check(L.wg_pagerank_prep(self.n, it, self.damping, self.outdeg.data_ptr(), self.acc.data_ptr(),
                                            self.contrib.data_ptr(),
                                            rank_out.data_ptr() if rank_out is not None else None,
-                                           self.scal.data_ptr(), self._lib.stream_ptr()))
+                                           self.scal.data_ptr(), self.ws.data_ptr(), self.ws.numel(),
+                                           self._lib.stream_ptr()))
 
     def pull(self):
         L = self._lib.load()
         self.part.zero_()
         self._lib.check(L.wg_pagerank_pull(ctypes.byref(self.g.struct()), self.contrib.data_ptr(),
-                                           self.part.data_ptr(), self.lo, self._lib.stream_ptr()))
+                                           self.part.data_ptr(), self.lo, self.ws.data_ptr(), self.ws.numel(),
+                                           self._lib.stream_ptr()))
         return self.part
 
     def unpack(self):

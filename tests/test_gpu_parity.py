@@ -571,3 +571,30 @@ def test_plain_dense_kernels_from_iteration_2(wg, monkeypatch, case):
         res = wg.run_until_convergence(ht, hi, prog, deg, cfg, backend=wg.B200Backend())
         assert np.array_equal(res.values, want.values), (case, graph)
         assert wg.stats_signature(res.stats) == oracle.signature(want.stats), (case, graph)
+
+
+def test_pagerank_deterministic_and_hub_split(wg):
+    """No float atomics: two runs are bit-identical, also on a graph whose
+    hubs' in-vectors span many warp ranges (pr_fixup adds the pieces in
+    order); and within 1e-6 of the float64 oracle there too."""
+    rng = np.random.default_rng(5)
+    n = 5000
+    # two hubs with thousands of in-edges + random edges
+    src = np.concatenate([rng.integers(0, n, 40000), rng.integers(0, n, 9000), rng.integers(0, n, 20000)])
+    dst = np.concatenate([np.full(40000, 7), np.full(9000, 4000), rng.integers(0, n, 20000)])
+    keep = src != dst
+    el = wg.drop_self_loops_dedup(wg.EdgeList(n, src[keep], dst[keep]), symmetric=False)
+    topo = wg.build_pull_topology(el, 4)
+    a = wg.pagerank(topo, 20, 0.85).copy()
+    b = wg.pagerank(topo, 20, 0.85).copy()
+    assert a.tobytes() == b.tobytes()
+    ref = oracle.pagerank_numpy(el.vertex_count, el.src, el.dst, 20, 0.85)
+    assert np.max(np.abs(a.astype(np.float64) - ref)) <= 1e-6
+    el2 = wg.drop_self_loops_dedup(wg.generate(wg.GenSpec("rmat", scale=16, edge_factor=16, seed=9)),
+                                   symmetric=False)
+    t2 = wg.build_pull_topology(el2, 4)
+    x = wg.pagerank(t2, 20, 0.85).copy()
+    y = wg.pagerank(t2, 20, 0.85).copy()
+    assert x.tobytes() == y.tobytes()
+    ref2 = oracle.pagerank_numpy(el2.vertex_count, el2.src, el2.dst, 20, 0.85)
+    assert np.max(np.abs(x.astype(np.float64) - ref2)) <= 1e-6
