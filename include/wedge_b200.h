@@ -412,13 +412,28 @@ int wg_exchange_pack(const wg_graph *g, const wg_run_bufs *b, const wg_run_param
 int wg_exchange_apply(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p, uint64_t it,
                       const uint32_t *d_verts, const void *d_vals, uint64_t count, void *stream);
 /* Host-sync-free form for fixed-size collectives.  A message is a 16-byte
- * header (u64 entry count) + (vertex, value) entries of 8 bytes (WG_VAL_U32)
+ * header (u64 entry count, u64 overflow flag of the sender's record) + (vertex, value)
+ * entries of 8 bytes (WG_VAL_U32)
  * or 16 bytes (WG_VAL_I64); wg_exchange_bytes(k, val_type) is the size of a
  * message truncated to k entries.  pack_all writes this rank's members of
  * iteration `it` (up to `capacity`); after an all-gather of equal prefixes
  * of cap entries, apply_all applies every rank's first min(count, cap)
  * entries, rebuilds the global frontier and writes the largest count into
- * *d_status (> cap: gather a longer prefix and apply again -- idempotent). */
+ * d_status[0] (> cap: gather a longer prefix and apply again -- idempotent)
+ * and 1 into d_status[1] when any rank's iteration overflowed uint32
+ * (d_status: 2 words). */
+/* Dense iterations (most vertices may change): instead of (vertex, value)
+ * pairs, every rank contributes its owned value slice [lo, hi) of iteration
+ * `it` (slice_pack copies it into d_slice); after an all-gather of S-value
+ * slices (S >= every rank's range), apply_slices writes all n values into
+ * both buffers, keeps this rank's (`self`) own frontier bits and derives the
+ * other ranks' from the values (new < previous: values never increase), and
+ * rebuilds the list and record of `it`.  d_bounds: device uint32 [world+1]. */
+int wg_exchange_slice_pack(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p, uint64_t it,
+                           uint32_t lo, uint32_t hi, void *d_slice, void *stream);
+int wg_exchange_apply_slices(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p, uint64_t it,
+                             const void *d_slices, const uint32_t *d_bounds, uint32_t world, uint32_t self,
+                             uint64_t S, void *stream);
 uint64_t wg_exchange_bytes(uint64_t entries, int val_type);
 int wg_exchange_pack_all(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p, uint64_t it,
                          void *d_buf, uint64_t capacity, void *stream);

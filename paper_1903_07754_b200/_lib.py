@@ -85,7 +85,7 @@ EXPORTS = [
     "wg_index_place_begin", "wg_index_place_chunk", "wg_index_place_coded", "wg_index_place_end",
     "wg_ingest_vectors", "wg_ingest_u32", "wg_ingest_offsets", "wg_values_scan", "wg_vector_offsets_from_dst",
     "wg_run_seed", "wg_debug_kernel_timeline", "wg_debug_kernel_ids", "wg_first_lanes",
-    "wg_pagerank_ws_bytes", "wg_pagerank_prep_ws_bytes",
+    "wg_pagerank_ws_bytes", "wg_pagerank_prep_ws_bytes", "wg_exchange_slice_pack", "wg_exchange_apply_slices",
 ]
 
 _LIB = None
@@ -139,6 +139,8 @@ def load(path: os.PathLike | str | None = None):
         "wg_run_enqueue": (ctypes.c_int, [G, B, P, c_u64, c_u32, c_vp]),
         "wg_run_enqueue_counter": (ctypes.c_int, [G, B, P, c_u32, c_vp]),
         "wg_pagerank_ws_bytes": (ctypes.c_size_t, [G]),
+        "wg_exchange_slice_pack": (ctypes.c_int, [G, B, P, c_u64, c_u32, c_u32, c_vp, c_vp]),
+        "wg_exchange_apply_slices": (ctypes.c_int, [G, B, P, c_u64, c_vp, c_vp, c_u32, c_u32, c_u64, c_vp]),
         "wg_pagerank": (ctypes.c_int, [G, ctypes.c_int, ctypes.c_double, c_vp, c_vp, c_vp, c_vp, c_vp,
                                        ctypes.c_size_t, c_vp]),
         "wg_pagerank_prep_ws_bytes": (ctypes.c_size_t, [c_u32]),

@@ -1171,7 +1171,10 @@ __global__ void exchange_pack_all_kernel(const wg_iter_rec *rec, const uint32_t 
                                          unsigned char *buf, uint64_t capacity) {
     const uint64_t nz = rec->nz_packed >> 32, z = rec->z_count;
     const uint64_t cnt = nz + z;
-    if (blockIdx.x == 0 && threadIdx.x == 0) *reinterpret_cast<uint64_t *>(buf) = cnt;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        reinterpret_cast<uint64_t *>(buf)[0] = cnt;
+        reinterpret_cast<uint64_t *>(buf)[1] = rec->overflow;  // every rank learns of an overflow
+    }
     XEntry<T> *e = reinterpret_cast<XEntry<T> *>(buf + 16);
     const uint64_t m = cnt < capacity ? cnt : capacity;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
@@ -1194,7 +1197,10 @@ __global__ void exchange_apply_all_kernel(const unsigned char *parts, uint32_t w
     for (uint32_t r = 0; r < world; ++r) {
         const unsigned char *pr = parts + (uint64_t)r * stride;
         const uint64_t cnt = *reinterpret_cast<const uint64_t *>(pr);
-        if (tid == 0) atomicMax((unsigned long long *)status, (unsigned long long)cnt);
+        if (tid == 0) {
+            atomicMax((unsigned long long *)status, (unsigned long long)cnt);
+            if (reinterpret_cast<const uint64_t *>(pr)[1]) status[1] = 1;
+        }
         const uint64_t m = cnt < cap ? cnt : cap;
         const XEntry<T> *e = reinterpret_cast<const XEntry<T> *>(pr + 16);
         for (uint64_t i = tid; i < m; i += nth) {
@@ -1206,9 +1212,76 @@ __global__ void exchange_apply_all_kernel(const unsigned char *parts, uint32_t w
     }
 }
 
+// Dense-iteration form: every rank's owned value slice (S values each, rank r
+// owning [bounds[r], bounds[r+1])).  A destination of another rank changed
+// iff its new value is below the replicated previous one (values never
+// increase; this rank's end of iteration synced only its own members), so
+// those frontier bits come from the values; this rank's own bits are its
+// pull's.  A thread per bitmap word.
+template <typename T>
+__global__ void exchange_slices_kernel(const T *slices, const uint32_t *bounds, uint32_t world, uint32_t self,
+                                       uint64_t S, uint32_t n, const T *prev, T *v0, T *v1, uint32_t *bits) {
+    const uint64_t words = ((uint64_t)n + 31) >> 5;
+    const uint64_t lo = bounds[self], hi = bounds[self + 1];
+    for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < words;
+         w += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t own = bits[w];
+        uint32_t word = 0, r = 0;
+        for (uint32_t j = 0; j < 32; ++j) {
+            const uint64_t d = (w << 5) + j;
+            if (d >= n) break;
+            while (r + 1 < world && d >= bounds[r + 1]) ++r;
+            const T x = slices[(uint64_t)r * S + (d - bounds[r])];
+            if (d >= lo && d < hi) word |= own & (1u << j);
+            else if (x < prev[d]) word |= 1u << j;
+            v0[d] = x;
+            v1[d] = x;
+        }
+        bits[w] = word;
+    }
+}
+
 }  // namespace
 
 extern "C" {
+
+int wg_exchange_slice_pack(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p, uint64_t it,
+                           uint32_t lo, uint32_t hi, void *d_slice, void *stream) {
+    int rc = check_run(g, b, p);
+    if (rc) return rc;
+    WG_REQUIRE(d_slice || hi == lo, "null argument");
+    WG_REQUIRE(lo <= hi && hi <= g->n, "bad owned range");
+    const size_t vb = p->val_type == WG_VAL_U32 ? 4 : 8;
+    if (hi > lo)
+        WG_CUDA(cudaMemcpyAsync(d_slice, (const char *)b->vals[it & 1] + lo * vb, (size_t)(hi - lo) * vb,
+                                cudaMemcpyDeviceToDevice, as_stream(stream)));
+    return WG_OK;
+}
+
+int wg_exchange_apply_slices(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p, uint64_t it,
+                             const void *d_slices, const uint32_t *d_bounds, uint32_t world, uint32_t self,
+                             uint64_t S, void *stream) {
+    int rc = check_run(g, b, p);
+    if (rc) return rc;
+    WG_REQUIRE(d_slices && d_bounds && world >= 1 && self < world, "bad argument");
+    cudaStream_t s = as_stream(stream);
+    uint32_t *bits = b->fbits[it & 1];
+    const uint64_t words = ((uint64_t)g->n + 31) >> 5;
+    const unsigned grid = grid_for(words ? words : 1, 256, 8);
+    if (p->val_type == WG_VAL_U32)
+        exchange_slices_kernel<uint32_t><<<grid, 256, 0, s>>>(
+            (const uint32_t *)d_slices, d_bounds, world, self, S, g->n, (const uint32_t *)b->vals[(it - 1) & 1],
+            (uint32_t *)b->vals[0], (uint32_t *)b->vals[1], bits);
+    else
+        exchange_slices_kernel<int64_t><<<grid, 256, 0, s>>>(
+            (const int64_t *)d_slices, d_bounds, world, self, S, g->n, (const int64_t *)b->vals[(it - 1) & 1],
+            (int64_t *)b->vals[0], (int64_t *)b->vals[1], bits);
+    ::wg::count_launch();
+    WG_CHECK_LAUNCH("exchange_apply_slices");
+    return launch_frontier_compaction(g, bits, b->bcount, bcount_ticket(g, p->shift, b->bcount),
+                                      b->fvert[it & 1], b->fpref[it & 1], b->tstart[it & 1],
+                                      &b->recs[it % b->ring], s);
+}
 
 uint64_t wg_exchange_bytes(uint64_t entries, int val_type) {
     return 16 + entries * (val_type == WG_VAL_U32 ? sizeof(XEntry<uint32_t>) : sizeof(XEntry<int64_t>));
@@ -1243,7 +1316,7 @@ int wg_exchange_apply_all(const wg_graph *g, const wg_run_bufs *b, const wg_run_
     cudaStream_t s = as_stream(stream);
     uint32_t *bits = b->fbits[it & 1];
     const uint64_t stride = wg_exchange_bytes(cap, p->val_type);
-    WG_CUDA(cudaMemsetAsync(d_status, 0, sizeof(uint64_t), s));
+    WG_CUDA(cudaMemsetAsync(d_status, 0, 2 * sizeof(uint64_t), s));
     unsigned grid = grid_for(cap ? cap : 1, 256 * 4, 8);
     if (p->val_type == WG_VAL_U32)
         exchange_apply_all_kernel<uint32_t><<<grid, 256, 0, s>>>((const unsigned char *)d_parts, world, cap, stride,

@@ -133,10 +133,18 @@ def run_sharded(shard, max_iterations: int, group=None, values: bool = True):
     converged = False
     it = 0
     packed = hasattr(shard, "exchange")
+    slices = hasattr(shard, "exchange_slices")
     cap = getattr(shard, "capacity", 0)
+    prev_sum = shard.initial_edge_sum() if slices else None
     while it < max_iterations:
         it += 1
-        if packed:
+        if slices and shard.gate_dense(prev_sum):
+            # dense iteration (the global gate, evaluated alike on every rank):
+            # every rank's owned value slice (4 or 8 B per owned vertex) rather
+            # than (vertex, value) pairs for most of its vertices
+            shard.step(it)
+            rec = shard.exchange_slices(it, group)
+        elif packed:
             # one fixed-size all-gather of truncated messages per iteration;
             # the largest count (global, so every rank decides alike) sizes
             # the next one and triggers a full-size redo when exceeded
@@ -150,6 +158,7 @@ def run_sharded(shard, max_iterations: int, group=None, values: bool = True):
             all_v, all_x = all_gather_pairs(verts, vals, group)
             rec = shard.apply(it, all_v, all_x)
         recs.append(rec)
+        prev_sum = rec.out_edge_sum
         if rec.out_edge_sum == 0:
             converged = True
             break
@@ -192,7 +201,7 @@ class DeviceShard:
         # global out-degrees and |E| drive the (global) gate
         self.g = dv.DeviceGraph(n, width, E, g.nvec, g.entries, g.vsrc, g.vdst, g.vw, g.idx_off,
                                 g.idx_pos, gdeg)
-        self.lo, self.hi, self.n = lo, hi, n
+        self.lo, self.hi, self.n, self.rank = lo, hi, n, rank
         self.kern, self.threshold, self.shift, self.val_type = kern, threshold, shift, val_type
         self.loop = dv.DeviceLoop(self.g, shift, val_type)
         self.init = dv.encode_values(init_values, val_type)
@@ -215,14 +224,69 @@ class DeviceShard:
         nb = int(L.wg_exchange_bytes(self.capacity, val_type))
         self.send = torch.zeros(nb, dtype=torch.uint8, device="cuda")
         self.recv = torch.empty(world * nb, dtype=torch.uint8, device="cuda")
-        self.status = torch.zeros(1, dtype=torch.int64, device="cuda")
-        self.host_status = torch.zeros(1, dtype=torch.int64).pin_memory()
+        self.status = torch.zeros(2, dtype=torch.int64, device="cuda")
+        self.host_status = torch.zeros(2, dtype=torch.int64).pin_memory()
+        # dense-iteration exchange: owned value slices, padded to S
+        self.world, self.bounds = world, list(bounds)
+        self.S = self.capacity
+        vt = torch.int32 if val_type == _lib.WG_VAL_U32 else torch.int64
+        self.slice_send = torch.empty(self.S, dtype=vt, device="cuda")
+        self.slice_recv = torch.empty(world * self.S, dtype=vt, device="cuda")
+        self.d_bounds = torch.tensor(np.asarray(bounds, dtype=np.uint32).view(np.int32), device="cuda")
+        self.ovf = torch.zeros(1, dtype=torch.int64, device="cuda")
+        self.E = E
+        self.init_members = init_members
         self.p = None
 
     def seed(self):
         self.p = self.loop.seed(self.init, self.words, self.kern, self.threshold, first_hit=self.first_hit,
                                 level_base=self.level_base, identity_init=self.identity)
         self.p.flags |= self._lib.WG_RUN_KEEP_LISTS  # wg_exchange_pack reads the member lists
+
+    def initial_edge_sum(self) -> int:
+        """Out-degree sum of the initial frontier (the first gate's input)."""
+        deg = self.g.outdeg[: self.n].to("cpu").numpy().view(np.uint32).astype(np.int64)
+        if self.init_members is None:
+            return int(deg.sum())
+        m = np.unique(np.asarray(self.init_members, dtype=np.int64))
+        return int(deg[m].sum())
+
+    def gate_dense(self, edge_sum: int) -> bool:
+        """The global gate (frontier.py:163-171) for the next iteration."""
+        return not (self.E > 0 and edge_sum < self.p.wedge_limit)
+
+    def exchange_slices(self, it: int, group=None):
+        """Dense iterations: all-gather every rank's owned value slice, apply
+        them (values + frontier bits from the value decrease) and rebuild the
+        global frontier; an overflow on any rank raises on every rank."""
+        import torch
+        import torch.distributed as dist
+        L = self._lib.load()
+        lo, hi = self.lo, self.hi
+        self._lib.check(L.wg_exchange_slice_pack(ctypes.byref(self.g.struct()), ctypes.byref(self.loop.bufs),
+                                                 ctypes.byref(self.p), it, lo, hi, self.slice_send.data_ptr(),
+                                                 self._lib.stream_ptr()))
+        dist.all_gather_into_tensor(self.slice_recv, self.slice_send, group=group)
+        return self.apply_slices(it, self.slice_recv, group)
+
+    def apply_slices(self, it: int, recv, group=None, overflow_any=None):
+        """Apply gathered slices (world x S values)."""
+        import torch.distributed as dist
+        L = self._lib.load()
+        # the local overflow flag of `it`, made global (one tiny all-reduce)
+        self.ovf.copy_(self.loop.recs.view(-1, self._lib.REC_U64)[it % self.loop.ring, 10:11])
+        if overflow_any is None:
+            dist.all_reduce(self.ovf, op=dist.ReduceOp.MAX, group=group)
+        else:
+            self.ovf.fill_(int(overflow_any))
+        self._lib.check(L.wg_exchange_apply_slices(ctypes.byref(self.g.struct()), ctypes.byref(self.loop.bufs),
+                                                   ctypes.byref(self.p), it, recv.data_ptr(),
+                                                   self.d_bounds.data_ptr(), self.world, self.rank, self.S,
+                                                   self._lib.stream_ptr()))
+        rec, ovf = self._record(it, raise_overflow=False)
+        if ovf or int(self.ovf.item()):
+            raise self._lib.OverflowError32(self._lib.WG_EOVERFLOW, "uint32 overflow in sharded loop (some rank)")
+        return rec
 
     def step(self, it: int):
         """Local iteration + pack of its members (no host synchronisation)."""
@@ -255,7 +319,9 @@ class DeviceShard:
                                                 ctypes.byref(self.p), it, recv.data_ptr(), world, cap,
                                                 self.status.data_ptr(), self._lib.stream_ptr()))
         self.host_status.copy_(self.status, non_blocking=True)
-        rec = self._record(it)  # synchronises
+        rec, _ = self._record(it, raise_overflow=False)  # synchronises
+        if int(self.host_status[1]):  # every rank's message carries its overflow flag
+            raise self._lib.OverflowError32(self._lib.WG_EOVERFLOW, "uint32 overflow in sharded loop (some rank)")
         return rec, int(self.host_status[0])
 
     def step_pairs(self, it: int):
@@ -279,13 +345,15 @@ class DeviceShard:
                                             self._lib.stream_ptr()))
         return self._record(it)
 
-    def _record(self, it: int) -> ShardRecord:
+    def _record(self, it: int, raise_overflow: bool = True):
         r = self.loop._read(it, 1)[0]
-        if int(r[10]):
+        ovf = bool(int(r[10]))
+        if ovf and raise_overflow:
             raise self._lib.OverflowError32(self._lib.WG_EOVERFLOW, "uint32 overflow in sharded loop")
         mode = {1: "FullScan", 2: "Wedge"}.get(int(r[0]), "None")
-        return ShardRecord(it, mode, int(r[1]), int(r[2]), int(r[3]), int(r[4]),
-                           int(r[7]) if mode == "Wedge" else 0, int(r[8]) if mode == "Wedge" else 0)
+        rec = ShardRecord(it, mode, int(r[1]), int(r[2]), int(r[3]), int(r[4]),
+                          int(r[7]) if mode == "Wedge" else 0, int(r[8]) if mode == "Wedge" else 0)
+        return rec if raise_overflow else (rec, ovf)
 
     def values_int64(self) -> np.ndarray:
         # after wg_exchange_apply both value buffers hold the global state
@@ -306,9 +374,18 @@ def run_sharded_device(n: int, src, dst, weight, width: int, program, config, gr
     bounds = destination_bounds(indeg, width, world)
     init = _initial_values(program, n)
     members = _initial_members(program, n)
-    shard = DeviceShard(n, src, dst, weight, width, bounds, rank, program.kernel, init, members,
-                        config.threshold.fraction, config.precision.shift, _lib.WG_VAL_U32)
-    return run_sharded(shard, config.max_iterations, group)
+    from . import device as dv
+    val_type = _lib.WG_VAL_U32 if dv.fits_u32(init, program.kernel, None) else _lib.WG_VAL_I64
+    while True:
+        shard = DeviceShard(n, src, dst, weight, width, bounds, rank, program.kernel, init, members,
+                            config.threshold.fraction, config.precision.shift, val_type)
+        try:
+            return run_sharded(shard, config.max_iterations, group)
+        except _lib.OverflowError32:
+            # every rank saw the flag in the same exchange: all restart exactly in int64
+            if val_type == _lib.WG_VAL_I64:
+                raise
+            val_type = _lib.WG_VAL_I64
 
 
 # ---------------------------------------------------------------------------

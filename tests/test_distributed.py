@@ -114,6 +114,39 @@ class PackedOracleShard(OracleShard):
         return OracleShard.apply(self, it, torch.cat(vs), torch.cat(xs)), maxc
 
 
+class SliceOracleShard(PackedOracleShard):
+    """Adds DeviceShard's dense-iteration form: every rank all-gathers its
+    owned value slice (padded to S) and derives the frontier from the value
+    decrease, instead of exchanging (vertex, value) pairs."""
+
+    def __init__(self, *a, **k):
+        super().__init__(*a, **k)
+        self.bounds = list(a[5])
+        self.rank = a[6]
+        self.S = self.capacity
+        self.slice_iters = []
+
+    def initial_edge_sum(self):
+        vals, front = oracle.initial_state(self.app, self.n, self.root)
+        return int(self.deg[np.unique(front)].sum())
+
+    def gate_dense(self, edge_sum):
+        num, den = self.thr.numerator, self.thr.denominator
+        return not (self.E > 0 and edge_sum * den < num * self.E)
+
+    def exchange_slices(self, it, group=None):
+        world = dist.get_world_size(group)
+        lo, hi = self.bounds[self.rank], self.bounds[self.rank + 1]
+        mine = torch.zeros(self.S, dtype=torch.int64)
+        mine[: hi - lo] = torch.from_numpy(self.nxt[lo:hi].copy())
+        parts = [torch.empty_like(mine) for _ in range(world)]
+        dist.all_gather(parts, mine, group=group)
+        new = np.concatenate([parts[r][: self.bounds[r + 1] - self.bounds[r]].numpy() for r in range(world)])
+        changed = np.flatnonzero(new < self.prev)
+        self.slice_iters.append(it)
+        return OracleShard.apply(self, it, torch.from_numpy(changed), torch.from_numpy(new[changed]))
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -128,14 +161,20 @@ def _worker(rank, world, port, case, q, packed=False):
     try:
         n, src, dst, w, app, thr, vpg = case
         bounds = destination_bounds(np.bincount(dst, minlength=n), 4, world)
-        if packed:
+        if packed == "slices":
+            import paper_1903_07754_b200.distributed as D
+            D.PACKED_MIN_CAP = 4
+            shard = SliceOracleShard(n, src, dst, w, 4, bounds, rank, app, 0, thr, vpg)
+        elif packed:
             import paper_1903_07754_b200.distributed as D
             D.PACKED_MIN_CAP = 4  # small messages, so truncated gathers and full-size redos both run
             shard = PackedOracleShard(n, src, dst, w, 4, bounds, rank, app, 0, thr, vpg)
         else:
             shard = OracleShard(n, src, dst, w, 4, bounds, rank, app, 0, thr, vpg)
         vals, recs, conv = run_sharded(shard, 10_000)
-        if packed and rank == 0:
+        if packed == "slices" and rank == 0:
+            assert shard.slice_iters and shard.exchanged_caps  # both exchange forms ran
+        elif packed and rank == 0:
             assert any(c < shard.capacity for c in shard.exchanged_caps)  # truncated gathers happened
         if rank == 0:
             q.put((vals, [(r.iteration, r.mode, r.active_edges, r.frontier_out_size) for r in recs], conv,
@@ -165,7 +204,8 @@ def _case(app, scale=10):
 
 
 @pytest.mark.parametrize("app,packed", [("bfs", False), ("cc", False), ("sssp", False), ("cc", True),
-                                        ("sssp", True)])
+                                        ("sssp", True), ("cc", "slices"), ("bfs", "slices"),
+                                        ("sssp", "slices")])
 def test_two_rank_sharded_run_matches_single(app, packed):
     case = _case(app)
     ctx = mp.get_context("spawn")

@@ -19,13 +19,29 @@ pytestmark = pytest.mark.gpu
 
 def _lockstep(shards, max_it=10_000, packed=False):
     """packed: the fixed-size protocol (wg_exchange_pack_all / apply_all) with
-    a deliberately small first capacity, so the truncated-message redo runs."""
+    a deliberately small first capacity, so the truncated-message redo runs;
+    "slices": dense iterations exchange owned value slices
+    (wg_exchange_slice_pack / apply_slices), the others packed messages."""
+    import ctypes
+    from paper_1903_07754_b200 import _lib
     for s in shards:
         s.seed()
     recs = []
     cap = 16
+    prev_sum = shards[0].initial_edge_sum()
+    dense_seen = 0
     for it in range(1, max_it + 1):
-        if packed:
+        if packed == "slices" and shards[0].gate_dense(prev_sum):
+            dense_seen += 1
+            L = _lib.load()
+            for r, s in enumerate(shards):
+                s.step(it)
+                _lib.check(L.wg_exchange_slice_pack(ctypes.byref(s.g.struct()), ctypes.byref(s.loop.bufs),
+                                                    ctypes.byref(s.p), it, s.bounds[r], s.bounds[r + 1],
+                                                    s.slice_send.data_ptr(), _lib.stream_ptr()))
+            recv = torch.cat([s.slice_send for s in shards])
+            rs = [s.apply_slices(it, recv, overflow_any=False) for s in shards]
+        elif packed:
             for s in shards:
                 s.step(it)
 
@@ -47,14 +63,18 @@ def _lockstep(shards, max_it=10_000, packed=False):
             assert (r.mode, r.active_edges, r.frontier_out_size, r.out_edge_sum) == \
                    (rs[0].mode, rs[0].active_edges, rs[0].frontier_out_size, rs[0].out_edge_sum)
         recs.append(rs[0])
+        prev_sum = rs[0].out_edge_sum
         if rs[0].out_edge_sum == 0:
             break
+    if packed == "slices":
+        assert dense_seen > 0
     return shards[0].values_int64(), recs
 
 
 @pytest.mark.parametrize("app,world,packed", [("bfs", 2, False), ("cc", 2, False), ("sssp", 2, False),
                                               ("cc", 3, False), ("bfs", 2, True), ("cc", 3, True),
-                                              ("sssp", 2, True)])
+                                              ("sssp", 2, True), ("cc", 2, "slices"), ("bfs", 3, "slices"),
+                                              ("sssp", 2, "slices")])
 def test_device_shards_match_single_run(app, world, packed):
     import paper_1903_07754_b200 as wg
     from paper_1903_07754_b200 import _lib
@@ -114,3 +134,32 @@ def test_device_pagerank_shards_match_single_run(world):
     for r in got:
         assert np.max(np.abs(r - want)) <= 1e-6  # north_star tolerance vs the float64 oracle
         assert np.max(np.abs(r - single)) <= 1e-7
+
+
+@pytest.mark.parametrize("packed", [True, "slices"])
+def test_device_shards_overflow_restart_in_int64(packed):
+    """uint32 overflow on one rank is seen by every rank (the packed header /
+    the all-reduced flag) and the run restarts exactly in int64."""
+    import paper_1903_07754_b200 as wg
+    from paper_1903_07754_b200 import _lib
+    from paper_1903_07754_b200.distributed import DeviceShard, destination_bounds
+    el = wg.drop_self_loops_dedup(wg.generate(wg.GenSpec("rmat", scale=10, edge_factor=8, seed=3)), True)
+    n = el.vertex_count
+    src, dst = el.src, el.dst
+    w = np.full(src.shape[0], 1_500_000_000, np.int64)  # distances pass 2^32 after three hops
+    prog = wg.make_program("sssp", 0)
+    bounds = destination_bounds(np.bincount(dst, minlength=n), 4, 2)
+    init = prog.initial_values(n)
+    mk = lambda vt: [DeviceShard(n, src, dst, w, 4, bounds, r, prog.kernel, init, np.array([0]), Fraction(1, 5),
+                                 2, vt) for r in range(2)]
+    with pytest.raises(_lib.OverflowError32):
+        _lockstep(mk(_lib.WG_VAL_U32), packed=packed)
+    vals, recs = _lockstep(mk(_lib.WG_VAL_I64), packed=packed)
+    topo = oracle.build_pull_topology(n, src, dst, w, 4)
+    idx = oracle.build_edge_index(topo)
+    deg = oracle.compute_out_degrees(n, src)
+    v0, front = oracle.initial_state("sssp", n, 0)
+    want = oracle.run_until_convergence(topo, idx, deg, oracle.SSSP, v0, front, Fraction(1, 5), 4)
+    assert np.array_equal(vals, want.values)
+    assert [(r.iteration, r.mode, r.active_edges, r.frontier_out_size) for r in recs] == \
+        list(oracle.trace(want.stats))
