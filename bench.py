@@ -355,24 +355,35 @@ def run_b200_sharded(args, wl, rank, world, local):
         dist.init_process_group("nccl", rank=rank, world_size=world,
                                 device_id=torch.device("cuda", local))
     t0 = time.perf_counter()
-    if "grid" in wl:
-        el = wg.grid_graph(wl["grid"][0], wl["grid"][1], GRID_SEED, 0.9, 1000)
-    else:
-        el = wg.generate(wg.GenSpec("rmat", scale=wl["scale"], edge_factor=wl["ef"], seed=1))
-        el = wg.drop_self_loops_dedup(el, symmetric=wl["sym"])
-        if wl.get("weights"):
-            el = wg.synthesize_weights(el, wl["weights"])
-    s, d, w = el.device_arrays()
-    n, E = el.vertex_count, el.edge_count
-    indeg = torch.bincount(d.to(torch.int64) & 0xFFFFFFFF, minlength=n).cpu().numpy()
-    bounds = destination_bounds(indeg, 4, world)
     app = wl["app"]
+    local_edges = None
+    from paper_1903_07754_b200 import device as dv
+    if "grid" in wl or app == "pr":
+        if "grid" in wl:
+            el = wg.grid_graph(wl["grid"][0], wl["grid"][1], GRID_SEED, 0.9, 1000)
+        else:
+            el = wg.drop_self_loops_dedup(wg.generate(wg.GenSpec("rmat", scale=wl["scale"], edge_factor=wl["ef"],
+                                                                 seed=1)), symmetric=wl["sym"])
+        s, d, w = el.device_arrays()
+        n, E = el.vertex_count, el.edge_count
+        indeg = torch.bincount(d.to(torch.int64) & 0xFFFFFFFF, minlength=n).cpu().numpy()
+        bounds = destination_bounds(indeg, 4, world)
+    else:
+        # partitioned ingest: each rank generates 1/N of the edge stream and
+        # receives the edges of its destination range (no rank holds all E)
+        from paper_1903_07754_b200.distributed import rmat_partitioned
+        n, E, bounds, s, d, outdeg = rmat_partitioned(wl["scale"], wl["ef"], 1, wl["sym"])
+        w = None
+        if wl.get("weights"):
+            w = dv.weights_hash(s, d, wl["weights"])  # synthesize_weights (graph_io.py:205-221) per edge
+        local_edges = (E, outdeg)
     if app == "pr":
         return run_pagerank_sharded_bench(args, wl, rank, world, local, n, E, s, d, bounds, t0)
     prog = wg.make_program(app, None if app == "cc" else 0)
     shift = {1: 0, 2: 1, 4: 2, 8: 3, 16: 4}[wl["vpg"]]
     shard = DeviceShard(n, s, d, w, 4, bounds, rank, prog.kernel, prog.initial_values(n),
-                        None if app == "cc" else np.array([0]), Fraction(wl["thr"]), shift, _lib.WG_VAL_U32)
+                        None if app == "cc" else np.array([0]), Fraction(wl["thr"]), shift, _lib.WG_VAL_U32,
+                        local=local_edges)
     torch.cuda.synchronize()
     build_s = time.perf_counter() - t0
     max_it = n + 16

@@ -1231,6 +1231,27 @@ def rmat_edges(scale: int, edge_factor: int, seed: int = 1, probs=RMAT_PROBS, st
     return n, src, dst
 
 
+def rmat_edges_rows(scale: int, row_lo: int, row_hi: int, seed: int = 1, probs=RMAT_PROBS, stream=None):
+    """Rows [row_lo, row_hi) of rmat_edges' stream: the PCG64 state jumped
+    ahead by row_lo * scale draws (PCG64.advance), so shards of the edge list
+    are generated independently and concatenate to the full one."""
+    torch = _torch()
+    bg = np.random.PCG64(seed)
+    bg.advance(int(row_lo) * int(scale))
+    st = bg.state["state"]
+    state, inc = int(st["state"]), int(st["inc"])
+    a, b, c, _ = probs
+    th = (ctypes.c_double * 3)(a, a + b, a + b + c)
+    m = int(row_hi) - int(row_lo)
+    src = torch.empty(max(m, 1), dtype=torch.int32, device="cuda")
+    dst = torch.empty(max(m, 1), dtype=torch.int32, device="cuda")
+    M = (1 << 64) - 1
+    if m:
+        check(_lib.load().wg_rmat_edges(scale, m, state >> 64, state & M, inc >> 64, inc & M, th,
+                                        _ptr(src), _ptr(dst), _lib.stream_ptr(stream)))
+    return src[:m], dst[:m]
+
+
 def canonical_edges(src, dst, drop_loops: bool, symmetrize: bool, stream=None):
     """Sorted (src, dst)-unique edge list; optional self-loop removal and
     symmetrisation (graph_io.py:87-112 with dedup)."""

@@ -57,6 +57,71 @@ def destination_bounds(indeg, width: int, world: int) -> list[int]:
 
 
 # ---------------------------------------------------------------------------
+# Partitioned ingest: no rank ever holds the whole edge list
+# ---------------------------------------------------------------------------
+def partition_edges(src, dst, weight, bounds, group=None):
+    """Send every edge to the rank owning its destination (one all-to-all
+    per array, counts first); returns this rank's (src, dst, weight) -- the
+    edges of its destination range.  torch tensors (any device the process
+    group serves); works on nccl and gloo."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    dev = src.device
+    cut = torch.tensor(bounds[1:-1], dtype=torch.int64, device=dev)
+    d64 = dst.to(torch.int64) & 0xFFFFFFFF if dst.dtype == torch.int32 else dst.to(torch.int64)
+    owner = torch.bucketize(d64, cut, right=True)
+    order = torch.argsort(owner, stable=True)
+    send_counts = torch.bincount(owner, minlength=world).to(torch.int64)
+    recv_counts = torch.empty_like(send_counts)
+    dist.all_to_all_single(recv_counts, send_counts, group=group)
+    sc, rc = send_counts.cpu().tolist(), recv_counts.cpu().tolist()
+
+    def move(t):
+        if t is None:
+            return None
+        out = torch.empty(sum(rc), dtype=t.dtype, device=dev)
+        dist.all_to_all_single(out, t[order].contiguous(), output_split_sizes=rc, input_split_sizes=sc,
+                               group=group)
+        return out
+    return move(src), move(dst), move(weight)
+
+
+def rmat_partitioned(scale: int, edge_factor: int, seed: int, symmetric: bool, width: int = 4, group=None):
+    """BASELINE's RMAT inputs built by destination shards:
+    rank r generates rows [r*m/G, (r+1)*m/G) of the reference's PCG64 stream
+    (graph_io.py:188-202; the generator jumps ahead, PCG64.advance), drops
+    self-loops, adds the reverse edges when symmetric, and ships every edge
+    to its destination's owner; each rank then de-duplicates its own edges
+    (duplicates share a destination).  Returns (n, E, bounds, src, dst,
+    global out-degrees) with the bounds balanced on the in-degrees."""
+    import torch
+    import torch.distributed as dist
+    from . import device as dv
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    n = 1 << scale
+    m = edge_factor * n
+    lo, hi = rank * m // world, (rank + 1) * m // world
+    s, d = dv.rmat_edges_rows(scale, lo, hi, seed)
+    s64, d64 = s.to(torch.int64) & 0xFFFFFFFF, d.to(torch.int64) & 0xFFFFFFFF
+    keep = s64 != d64
+    s, d = s[keep], d[keep]
+    if symmetric:
+        s, d = torch.cat([s, d]), torch.cat([d, s])
+    # destination bounds from the global (pre-dedup) in-degree histogram
+    hist = torch.bincount(d.to(torch.int64) & 0xFFFFFFFF, minlength=n)
+    dist.all_reduce(hist, group=group)
+    bounds = destination_bounds(hist.cpu().numpy(), width, world)
+    s, d, _ = partition_edges(s, d, None, bounds, group)
+    s, d = dv.canonical_edges(s, d, drop_loops=False, symmetrize=False)  # local dedup
+    outdeg = torch.bincount(s.to(torch.int64) & 0xFFFFFFFF, minlength=n)
+    dist.all_reduce(outdeg, group=group)
+    E = torch.tensor([s.numel()], dtype=torch.int64, device=s.device)
+    dist.all_reduce(E, group=group)
+    return n, int(E.item()), bounds, s, d, outdeg.to(torch.int32)
+
+
+# ---------------------------------------------------------------------------
 # Exchange
 # ---------------------------------------------------------------------------
 def all_gather_var(t, group=None):
@@ -128,6 +193,10 @@ def run_sharded(shard, max_iterations: int, group=None, values: bool = True):
     them afterwards with shard.values_int64())."""
     import torch
     import torch.distributed as dist
+    if dist.get_world_size(group) == 1 and hasattr(shard, "run_alone"):
+        # one rank: every exchange would be the identity -- the whole loop
+        # runs as the single-GPU loop graph, no per-iteration host round trip
+        return shard.run_alone(max_iterations, values)
     shard.seed()
     recs: list[ShardRecord] = []
     converged = False
@@ -184,7 +253,10 @@ class DeviceShard:
 
     def __init__(self, n: int, src, dst, weight, width: int, bounds: list[int], rank: int, kern,
                  init_values: np.ndarray, init_members: Optional[np.ndarray], threshold: Fraction,
-                 shift: int, val_type: int):
+                 shift: int, val_type: int, local: Optional[tuple] = None):
+        """src/dst/weight: the whole edge list (masked to this rank's range
+        here), or -- with local=(E, global out-degrees) -- only this rank's
+        edges already (partition_edges / rmat_partitioned)."""
         import torch
         from . import _lib
         from . import device as dv
@@ -193,11 +265,15 @@ class DeviceShard:
         s = dv.to_dev_u32(src)
         d = dv.to_dev_u32(dst)
         w = dv.to_dev_u32(weight) if weight is not None else None
-        d64 = d.to(torch.int64) & 0xFFFFFFFF
-        mask = (d64 >= lo) & (d64 < hi)
-        E = int(s.numel())
-        gdeg = torch.bincount(s.to(torch.int64) & 0xFFFFFFFF, minlength=n).to(torch.int32)
-        g = dv.DeviceGraph.build(n, s[mask], d[mask], w[mask] if w is not None else None, width)
+        if local is None:
+            d64 = d.to(torch.int64) & 0xFFFFFFFF
+            mask = (d64 >= lo) & (d64 < hi)
+            E = int(s.numel())
+            gdeg = torch.bincount(s.to(torch.int64) & 0xFFFFFFFF, minlength=n).to(torch.int32)
+            s, d, w = s[mask], d[mask], (w[mask] if w is not None else None)
+        else:
+            E, gdeg = int(local[0]), dv.to_dev_u32(local[1])
+        g = dv.DeviceGraph.build(n, s, d, w, width)
         # global out-degrees and |E| drive the (global) gate
         self.g = dv.DeviceGraph(n, width, E, g.nvec, g.entries, g.vsrc, g.vdst, g.vw, g.idx_off,
                                 g.idx_pos, gdeg)
@@ -239,17 +315,21 @@ class DeviceShard:
         self.p = None
 
     def seed(self):
+        self._last = None
         self.p = self.loop.seed(self.init, self.words, self.kern, self.threshold, first_hit=self.first_hit,
                                 level_base=self.level_base, identity_init=self.identity)
         self.p.flags |= self._lib.WG_RUN_KEEP_LISTS  # wg_exchange_pack reads the member lists
 
     def initial_edge_sum(self) -> int:
-        """Out-degree sum of the initial frontier (the first gate's input)."""
-        deg = self.g.outdeg[: self.n].to("cpu").numpy().view(np.uint32).astype(np.int64)
-        if self.init_members is None:
-            return int(deg.sum())
-        m = np.unique(np.asarray(self.init_members, dtype=np.int64))
-        return int(deg[m].sum())
+        """Out-degree sum of the initial frontier (the first gate's input; cached)."""
+        if getattr(self, "_init_sum", None) is None:
+            import torch
+            deg = self.g.outdeg[: self.n].to(torch.int64) & 0xFFFFFFFF
+            if self.init_members is not None:
+                m = torch.from_numpy(np.unique(np.asarray(self.init_members, dtype=np.int64))).to(deg.device)
+                deg = deg[m]
+            self._init_sum = int(deg.sum().item())
+        return self._init_sum
 
     def gate_dense(self, edge_sum: int) -> bool:
         """The global gate (frontier.py:163-171) for the next iteration."""
@@ -287,6 +367,19 @@ class DeviceShard:
         if ovf or int(self.ovf.item()):
             raise self._lib.OverflowError32(self._lib.WG_EOVERFLOW, "uint32 overflow in sharded loop (some rank)")
         return rec
+
+    def run_alone(self, max_iterations: int, values: bool = True):
+        """World size 1: the device loop to convergence (DeviceLoop.drive)."""
+        self.p = self.loop.seed(self.init, self.words, self.kern, self.threshold, first_hit=self.first_hit,
+                                level_base=self.level_base, identity_init=self.identity)
+        recs, conv, last = self.loop.drive(self.p, max_iterations)
+        self._last = last
+        # a produced frontier's out-edge sum is the next iteration's active edges
+        nxt = [r.active_edges for r in recs[1:]] + [0]
+        out = [ShardRecord(r.iteration, r.mode, r.active_edges, r.vectors_touched, r.frontier_out_size,
+                           e, r.covered_vectors, r.transform_entries) for r, e in zip(recs, nxt)]
+        vals = self.dv.values_to_int64(self.loop.values_after(last), self.val_type) if values else None
+        return vals, out, conv
 
     def step(self, it: int):
         """Local iteration + pack of its members (no host synchronisation)."""
@@ -357,6 +450,8 @@ class DeviceShard:
 
     def values_int64(self) -> np.ndarray:
         # after wg_exchange_apply both value buffers hold the global state
+        if getattr(self, "_last", None) is not None:  # run_alone: the last iteration's buffer
+            return self.dv.values_to_int64(self.loop.values_after(self._last), self.val_type)
         return self.dv.values_to_int64(self.loop.vals[0], self.val_type)
 
 

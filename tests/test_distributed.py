@@ -311,3 +311,45 @@ def test_sharded_pagerank_matches_single(world):
     for rank, r, bounds in got:
         assert len(set(bounds)) == world + 1
         assert np.max(np.abs(r - want)) <= 1e-12, rank
+
+
+def _partition_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1903_07754_b200.distributed import partition_edges
+        n, s, d = oracle.rmat_edges(10, 8, 3)
+        # every rank contributes a different part of the edge list
+        m = len(s)
+        lo, hi = rank * m // world, (rank + 1) * m // world
+        bounds = destination_bounds(np.bincount(d, minlength=n), 4, world)
+        ls, ld, lw = partition_edges(torch.from_numpy(s[lo:hi]), torch.from_numpy(d[lo:hi]),
+                                     torch.from_numpy(s[lo:hi] * 7 + 1), bounds)
+        q.put((rank, ls.numpy(), ld.numpy(), lw.numpy(), bounds))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_partition_edges_routes_every_edge_to_its_owner():
+    """partition_edges (the sharded ingest's all-to-all): every edge arrives
+    exactly once, at the rank owning its destination, with its attributes."""
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_partition_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    n, s, d = oracle.rmat_edges(10, 8, 3)
+    all_s, all_d = [], []
+    for rank, ls, ld, lw, bounds in got:
+        assert np.all((ld >= bounds[rank]) & (ld < bounds[rank + 1]))
+        assert np.array_equal(lw, ls * 7 + 1)
+        all_s.append(ls)
+        all_d.append(ld)
+    key = lambda a, b: np.sort(a.astype(np.int64) * (1 << 32) + b)
+    assert np.array_equal(key(np.concatenate(all_s), np.concatenate(all_d)), key(s, d))

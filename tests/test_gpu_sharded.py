@@ -163,3 +163,40 @@ def test_device_shards_overflow_restart_in_int64(packed):
     assert np.array_equal(vals, want.values)
     assert [(r.iteration, r.mode, r.active_edges, r.frontier_out_size) for r in recs] == \
         list(oracle.trace(want.stats))
+
+
+def test_partitioned_rmat_ingest_single_rank_matches_full_pipeline():
+    """rmat_partitioned (rows of the PCG64 stream per rank, all-to-all to the
+    destination owner, local dedup) at world size 1 over NCCL equals the
+    whole-list pipeline, and a sharded CC run on it gives the oracle's result."""
+    import os
+    import socket
+    import torch.distributed as dist
+    import paper_1903_07754_b200 as wg
+    from paper_1903_07754_b200 import _lib
+    from paper_1903_07754_b200.distributed import DeviceShard, rmat_partitioned, run_sharded
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(sock.getsockname()[1]))
+    sock.close()
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        n, E, bounds, s, d, outdeg = rmat_partitioned(12, 16, 1, True)
+        el = wg.drop_self_loops_dedup(wg.generate(wg.GenSpec("rmat", scale=12, edge_factor=16, seed=1)), True)
+        assert E == el.edge_count and bounds == [0, n]
+        key = lambda a, b: np.sort((a.astype(np.int64) & 0xFFFFFFFF) * (1 << 32) + (b.astype(np.int64) & 0xFFFFFFFF))
+        assert np.array_equal(key(s.cpu().numpy(), d.cpu().numpy()), key(el.src, el.dst))
+        assert np.array_equal(outdeg.cpu().numpy().astype(np.int64), np.bincount(el.src, minlength=n))
+        prog = wg.make_program("cc")
+        shard = DeviceShard(n, s, d, None, 4, bounds, 0, prog.kernel, prog.initial_values(n), None, Fraction(1, 5),
+                            2, _lib.WG_VAL_U32, local=(E, outdeg))
+        vals, recs, conv = run_sharded(shard, 10_000)
+        topo = oracle.build_pull_topology(n, el.src, el.dst, None, 4)
+        want = oracle.run_until_convergence(topo, oracle.build_edge_index(topo),
+                                            oracle.compute_out_degrees(n, el.src), oracle.CC,
+                                            *oracle.initial_state("cc", n, 0), Fraction(1, 5), 4)
+        assert np.array_equal(vals, want.values) and conv
+        assert [(r.iteration, r.mode, r.active_edges, r.frontier_out_size) for r in recs] == \
+            list(oracle.trace(want.stats))
+    finally:
+        dist.destroy_process_group()
