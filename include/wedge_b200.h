@@ -333,6 +333,15 @@ typedef struct wg_run_params {
  * the vectors of destinations not at 0 (env WG_FLOOR_KERNELS=0 keeps the
  * pipeline).  Results and counters unchanged. */
 #define WG_RUN_FLOOR_SKIP 16
+/* Per-shard independent gate (destination-sharded runs; SURVEY 8(f) row 3,
+ * PAPER.md:251 future work): the Wedge / FullScan decision of an iteration
+ * uses this shard's share of the frontier's out-edges -- the index entries
+ * of its members in the shard's LOCAL edge index -- against the shard's own
+ * entry count (wedge_limit then = ceil(num * local entries / den)), instead
+ * of the global edge sum.  Values and frontiers are unchanged (any covering
+ * of the active edges gives the same pull, Appendix A.7); modes and work
+ * counters become per shard.  Convergence stays global. */
+#define WG_RUN_LOCAL_GATE 32
 
 /* Element counts: [0] fbits words, [1] groups, [2] gbits words, [3] bcount
  * entries, [4] tstart entries (the caller multiplies by element sizes). */

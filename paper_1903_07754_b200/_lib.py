@@ -60,6 +60,7 @@ WG_RUN_FIRST_HIT = 1
 WG_RUN_KEEP_LISTS = 2
 WG_RUN_IDENTITY_INIT = 8
 WG_RUN_FLOOR_SKIP = 16
+WG_RUN_LOCAL_GATE = 32
 WG_CODED_BLOCK_VECTORS = 1024
 WG_INGEST_BAD_DST, WG_INGEST_BAD_SRC, WG_INGEST_BAD_COUNT, WG_INGEST_BAD_WEIGHT = 1, 2, 4, 8
 WG_INGEST_BAD_POS, WG_INGEST_BAD_DEGREE, WG_INGEST_BAD_OFFSETS, WG_INGEST_LENS_DIFFER = 16, 32, 64, 128

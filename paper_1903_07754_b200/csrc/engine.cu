@@ -638,7 +638,8 @@ static LoopCtx loop_ctx(const wg_graph *g, const wg_run_bufs *b, const wg_run_pa
     c.ctrl = ctrl;
     c.it_arg = it;
     c.wedge_limit = p->wedge_limit;
-    c.edges = g->edges;
+    c.gate_local = (p->flags & WG_RUN_LOCAL_GATE) ? 1 : 0;
+    c.edges = c.gate_local ? g->entries : g->edges;  // the local gate compares against local entries
     c.keep_lists = (p->flags & WG_RUN_KEEP_LISTS) ? 1 : 0;
     return c;
 }

@@ -23,6 +23,7 @@ struct LoopCtx {
     uint64_t wedge_limit;   // wedge iff edges > 0 and edge_sum < wedge_limit
     uint64_t edges;
     int32_t keep_lists;     // WG_RUN_KEEP_LISTS: build every frontier list (traces, exchange)
+    int32_t gate_local;     // WG_RUN_LOCAL_GATE: gate on the shard's own index entries
 };
 
 __device__ __forceinline__ uint64_t ctx_iter(const LoopCtx &c) {
@@ -37,9 +38,10 @@ __device__ __forceinline__ int ctx_mode(const LoopCtx &c, uint64_t it) {
     // graph launches carry an iteration limit in ctrl[1]
     if (c.ctrl && it > *(volatile const uint64_t *)&c.ctrl[1]) return MODE_NONE;
     const wg_iter_rec &p = c.recs[(it - 1) % c.ring];
-    uint64_t sum = *(volatile const uint64_t *)&p.out_edge_sum;
-    if (it > 1 && sum == 0) return MODE_NONE;
-    return (c.edges > 0 && sum < c.wedge_limit) ? MODE_WEDGE : MODE_FULL;
+    const uint64_t sum = *(volatile const uint64_t *)&p.out_edge_sum;
+    if (it > 1 && sum == 0) return MODE_NONE;  // convergence is global
+    const uint64_t key = c.gate_local ? (*(volatile const uint64_t *)&p.nz_packed & 0xffffffffull) : sum;
+    return (c.edges > 0 && key < c.wedge_limit) ? MODE_WEDGE : MODE_FULL;
 }
 
 // Debug timeline of the loop's kernels (wg_debug_kernel_timeline; null =

@@ -886,27 +886,30 @@ class DeviceLoop:
         self._level_base = 0
 
     def params(self, kern, threshold: Fraction, first_hit: bool = False,
-               identity_init: bool = False) -> WgRunParams:
+               identity_init: bool = False, extra_flags: int = 0) -> WgRunParams:
         p = WgRunParams()
         p.val_type = self.val_type
         p.shift = self.shift
         p.kern = _minplus(kern, UNREACHED)
-        p.wedge_limit = wedge_limit(threshold, self.g.edges) if self.g.edges > 0 else 0
+        # WG_RUN_LOCAL_GATE (shards): the gate compares the shard's own index entries
+        total = self.g.entries if extra_flags & _lib.WG_RUN_LOCAL_GATE else self.g.edges
+        p.wedge_limit = wedge_limit(threshold, total) if total > 0 else 0
         p.flags = (_lib.WG_RUN_FIRST_HIT if first_hit else 0) | (_lib.WG_RUN_IDENTITY_INIT if identity_init else 0)
+        p.flags |= int(extra_flags)
         if identity_init and os.environ.get("WG_FLOOR_SKIP", "1") != "0":
             p.flags |= _lib.WG_RUN_FLOOR_SKIP  # CC-like runs: label 0 spreads over the giant component
         p.level_base = int(self._level_base) if first_hit else 0
         return p
 
     def seed(self, init_values, init_words, kern, threshold, stream=None, first_hit: bool = False,
-             level_base: int = 0, identity_init: bool = False) -> WgRunParams:
+             level_base: int = 0, identity_init: bool = False, extra_flags: int = 0) -> WgRunParams:
         """Write both value buffers and build iteration 0 from the frontier bitmap.
         first_hit: the caller checked first_hit_ok (level-synchronous values);
         level_base: then the common value of the initial frontier (first_hit_level)."""
         if init_values.numel() < self.g.n or init_values.dtype != self.vals[0].dtype:
             raise ValueError("initial values do not match the loop's value buffers")
         self._level_base = int(level_base)
-        p = self.params(kern, threshold, first_hit, identity_init)
+        p = self.params(kern, threshold, first_hit, identity_init, extra_flags)
         counts = None
         if getattr(init_words, "_wg_all", False) and not (p.flags & _lib.WG_RUN_KEEP_LISTS):
             c4 = self.g.all_vertex_counts()

@@ -253,10 +253,17 @@ class DeviceShard:
 
     def __init__(self, n: int, src, dst, weight, width: int, bounds: list[int], rank: int, kern,
                  init_values: np.ndarray, init_members: Optional[np.ndarray], threshold: Fraction,
-                 shift: int, val_type: int, local: Optional[tuple] = None):
+                 shift: int, val_type: int, local: Optional[tuple] = None, gate: str = "global"):
         """src/dst/weight: the whole edge list (masked to this rank's range
         here), or -- with local=(E, global out-degrees) -- only this rank's
-        edges already (partition_edges / rmat_partitioned)."""
+        edges already (partition_edges / rmat_partitioned).  gate: "global"
+        (the reference's decision, identical on every rank: reference-parity
+        modes and counters) or "local" (WG_RUN_LOCAL_GATE: each shard picks
+        Wedge / FullScan from its own share of the frontier's edges; same
+        values and frontiers)."""
+        if gate not in ("global", "local"):
+            raise ValueError("gate must be 'global' or 'local'")
+        self.gate = gate
         import torch
         from . import _lib
         from . import device as dv
@@ -316,9 +323,11 @@ class DeviceShard:
 
     def seed(self):
         self._last = None
+        # wg_exchange_pack reads the member lists of every iteration
+        flags = self._lib.WG_RUN_KEEP_LISTS | (self._lib.WG_RUN_LOCAL_GATE if self.gate == "local" else 0)
         self.p = self.loop.seed(self.init, self.words, self.kern, self.threshold, first_hit=self.first_hit,
-                                level_base=self.level_base, identity_init=self.identity)
-        self.p.flags |= self._lib.WG_RUN_KEEP_LISTS  # wg_exchange_pack reads the member lists
+                                level_base=self.level_base, identity_init=self.identity, extra_flags=flags)
+        self.global_limit = self.dv.wedge_limit(self.threshold, self.E) if self.E > 0 else 0
 
     def initial_edge_sum(self) -> int:
         """Out-degree sum of the initial frontier (the first gate's input; cached)."""
@@ -332,8 +341,9 @@ class DeviceShard:
         return self._init_sum
 
     def gate_dense(self, edge_sum: int) -> bool:
-        """The global gate (frontier.py:163-171) for the next iteration."""
-        return not (self.E > 0 and edge_sum < self.p.wedge_limit)
+        """The global gate (frontier.py:163-171) for the next iteration: it
+        picks the exchange form (alike on every rank whatever the local modes)."""
+        return not (self.E > 0 and edge_sum < self.global_limit)
 
     def exchange_slices(self, it: int, group=None):
         """Dense iterations: all-gather every rank's owned value slice, apply
@@ -371,7 +381,8 @@ class DeviceShard:
     def run_alone(self, max_iterations: int, values: bool = True):
         """World size 1: the device loop to convergence (DeviceLoop.drive)."""
         self.p = self.loop.seed(self.init, self.words, self.kern, self.threshold, first_hit=self.first_hit,
-                                level_base=self.level_base, identity_init=self.identity)
+                                level_base=self.level_base, identity_init=self.identity,
+                                extra_flags=self._lib.WG_RUN_LOCAL_GATE if self.gate == "local" else 0)
         recs, conv, last = self.loop.drive(self.p, max_iterations)
         self._last = last
         # a produced frontier's out-edge sum is the next iteration's active edges

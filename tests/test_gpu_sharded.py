@@ -200,3 +200,68 @@ def test_partitioned_rmat_ingest_single_rank_matches_full_pipeline():
             list(oracle.trace(want.stats))
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("app,packed", [("cc", True), ("bfs", "slices"), ("sssp", True)])
+def test_device_shards_local_gate_same_values_and_frontiers(app, packed):
+    """WG_RUN_LOCAL_GATE: every shard decides Wedge / FullScan from its own
+    share of the frontier's edges.  Modes may differ per
+    shard and from the reference; values, active edges and produced
+    frontiers may not."""
+    import paper_1903_07754_b200 as wg
+    from paper_1903_07754_b200 import _lib
+    from paper_1903_07754_b200.distributed import DeviceShard, destination_bounds
+    el = wg.drop_self_loops_dedup(wg.generate(wg.GenSpec("rmat", scale=13, edge_factor=16, seed=4)), True)
+    if app == "sssp":
+        el = wg.synthesize_weights(el, 255)
+    n = el.vertex_count
+    src, dst, w = el.src, el.dst, el.weight
+    prog = wg.make_program(app, None if app == "cc" else 0)
+    thr = Fraction(1, 100) if app == "bfs" else Fraction(1, 5)
+    vpg = 8 if app == "bfs" else 4
+    bounds = destination_bounds(np.bincount(dst, minlength=n), 4, 3)
+    init = prog.initial_values(n)
+    members = None if app == "cc" else np.array([0])
+    shards = [DeviceShard(n, src, dst, w, 4, bounds, r, prog.kernel, init, members, thr, vpg.bit_length() - 1,
+                          _lib.WG_VAL_U32, gate="local") for r in range(3)]
+    vals, recs = _lockstep_local(shards, packed)
+    topo = oracle.build_pull_topology(n, src, dst, w, 4)
+    want = oracle.run_until_convergence(topo, oracle.build_edge_index(topo), oracle.compute_out_degrees(n, src),
+                                        oracle.kern_of(app), *oracle.initial_state(app, n, 0), thr, vpg)
+    assert np.array_equal(vals, want.values)
+    assert [(r.iteration, r.active_edges, r.frontier_out_size) for r in recs] == \
+        [(s.iteration, s.active_edges, s.frontier_out_size) for s in want.stats]
+
+
+def _lockstep_local(shards, packed):
+    """_lockstep without the per-shard mode agreement check (modes are local)."""
+    import ctypes
+    from paper_1903_07754_b200 import _lib
+    for s in shards:
+        s.seed()
+    recs, prev_sum = [], shards[0].initial_edge_sum()
+    for it in range(1, 10_000):
+        if packed == "slices" and shards[0].gate_dense(prev_sum):
+            L = _lib.load()
+            for r, s in enumerate(shards):
+                s.step(it)
+                _lib.check(L.wg_exchange_slice_pack(ctypes.byref(s.g.struct()), ctypes.byref(s.loop.bufs),
+                                                    ctypes.byref(s.p), it, s.bounds[r], s.bounds[r + 1],
+                                                    s.slice_send.data_ptr(), _lib.stream_ptr()))
+            recv = torch.cat([s.slice_send for s in shards])
+            rs = [s.apply_slices(it, recv, overflow_any=False) for s in shards]
+        else:
+            for s in shards:
+                s.step(it)
+            full = shards[0].capacity
+            nb = shards[0].message_bytes(full)
+            recv = torch.cat([s.send[:nb] for s in shards])
+            rs = [s.apply_packed(it, recv, len(shards), full)[0] for s in shards]
+        for r in rs[1:]:
+            assert (r.active_edges, r.frontier_out_size, r.out_edge_sum) == \
+                   (rs[0].active_edges, rs[0].frontier_out_size, rs[0].out_edge_sum)
+        recs.append(rs[0])
+        prev_sum = rs[0].out_edge_sum
+        if prev_sum == 0:
+            break
+    return shards[0].values_int64(), recs
