@@ -644,6 +644,8 @@ static LoopCtx loop_ctx(const wg_graph *g, const wg_run_bufs *b, const wg_run_pa
     return c;
 }
 
+constexpr uint64_t LOOP_BU_MAX_VECTORS = 1ull << 24;
+
 static PullBufs pull_bufs(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p) {
     PullBufs pb{};
     for (int i = 0; i < 2; ++i) {
@@ -682,11 +684,11 @@ static PullBufs pull_bufs(const wg_graph *g, const wg_run_bufs *b, const wg_run_
                            ((pb.floor_skip && !p->kern.filter_unvisited) || (pb.first_hit && p->kern.filter_unvisited))
                        ? 1u : 0u;
     {
-        // the floor kind only: the bottom-up pulls of large BFS graphs run
-        // faster as their own kernel (more registers, no persistent-loop spills:
-        // BFS s26 iteration 3 1.31 vs 1.76 ms); WG_LOOP_DENSE=0/1 overrides
+        // the bottom-up kind of LARGE graphs runs faster as its own kernel
+        // (more registers, no persistent-loop spills: BFS s26 iteration 3 1.31
+        // vs 1.76 ms); small ones save the launches; WG_LOOP_DENSE=0/1 overrides
         const char *e = getenv("WG_LOOP_DENSE");
-        const bool want = e ? e[0] != '0' : !p->kern.filter_unvisited;
+        const bool want = e ? e[0] != '0' : (!p->kern.filter_unvisited || g->nvec <= LOOP_BU_MAX_VECTORS);
         pb.loop_dense = pb.dst_major && want ? 1u : 0u;
     }
     return pb;

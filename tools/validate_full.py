@@ -1,71 +1,55 @@
-"""Full-size parity against the reference's own compiled kernels (oracle/_ref,
-16 host threads, the restated reference driver) for the BASELINE configs the
-bench checks only by certificate: the 4096^2 grid SSSP (configs[2]) and the
-s25 PageRank (configs[4], float64 oracle, |r_gpu - r_cpu| <= 1e-6).  Writes
-the reference digests / PR error to the JSON file given as argv[1] (the
-committed copy is tests/golden/full_size.json).  ~20 min of host CPU.
+"""Full-size reference results, independent of the product: the UNMODIFIED
+reference driver (wedgegraph.run_until_convergence, engine.py:330-388, native
+backend, every host core) from baseline/_ref on inputs built by the oracle's
+restated generators and layout builders (oracle/, pinned against the
+reference's own outputs by tests/test_oracle.py) -- no device code involved.
+Records each workload's result digest and per-iteration trace
+(iteration, mode, active_edges, frontier_out) into the JSON file given as
+argv[1] (the committed copy is tests/golden/full_size.json), which
+tests/test_gpu_large.py checks the device engine against.
 
-usage: python tools/validate_full.py out.json [grid] [pr25]
+Runs on the GPU box's host (196 GB RAM, 16 cores); s26 needs ~40 GB.
+usage: python tools/validate_full.py out.json cc22 bfs26 sssp26 [sssp_grid]
 """
 import json
 import os
 import sys
 import time
-from fractions import Fraction
 from pathlib import Path
 
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
-import numpy as np
-import torch
 
-import bench
-import oracle
-import paper_1903_07754_b200 as wg
-from paper_1903_07754_b200 import _lib, device as dv
-from paper_1903_07754_b200.engine import _initial_values
+import bench  # noqa: E402  (workload table + reference-arm helpers; imports no product code)
 
-out_path = sys.argv[1]
-which = sys.argv[2:] or ["grid", "pr25"]
+out_path = Path(sys.argv[1])
+which = sys.argv[2:] or ["cc22", "bfs26", "sssp26"]
+res = json.loads(out_path.read_text()) if out_path.exists() else {}
+ref, why = bench.import_reference()
+if ref is None:
+    sys.exit(f"reference unavailable: {why}")
 threads = os.cpu_count() or 1
-res = json.loads(Path(out_path).read_text()) if Path(out_path).exists() else {}
-
-if "grid" in which:
-    wl = bench.WORKLOADS["sssp_grid"]
-    el, topo = bench.make_graph(wl)
-    g = topo.device
-    prog = wg.make_program("sssp", 0)
-    loop = dv.DeviceLoop(g, 2, _lib.WG_VAL_U32)
-    p = loop.seed(dv.encode_values(_initial_values(prog, g.n), _lib.WG_VAL_U32), dv.initial_words(g.n, np.array([0])),
-                  prog.kernel, Fraction(wl["thr"]))
-    recs, conv, last = loop.drive(p, g.n + 16)
-    gpu = dv.values_to_int64(loop.values_after(last), _lib.WG_VAL_U32)
-    tp, idx, deg = bench.host_reference_layout(g)
-    be = oracle.RefBackend(threads) if oracle.ref_kernels() is not None else oracle.PortBackend(threads)
-    init, front = oracle.initial_state("sssp", g.n, 0)
+for name in which:
+    wl = bench.WORKLOADS[name]
     t0 = time.perf_counter()
-    ref = oracle.run_until_convergence(tp, idx, deg, oracle.kern_of("sssp"), init, front, Fraction(wl["thr"]),
-                                       wl["vpg"], g.n + 16, backend=be)
-    t = time.perf_counter() - t0
-    trace_ok = [(r.mode, r.active_edges, r.frontier_out_size) for r in recs] == \
-               [(s[1], s[2], s[3]) for s in oracle.trace(ref.stats)]
-    res["sssp_grid"] = {"reference_digest": oracle.result_digest(ref.values), "gpu_digest": wg.result_digest(gpu),
-                        "equal": bool(np.array_equal(ref.values, gpu)), "iterations": len(ref.stats),
-                        "trace_equal": bool(trace_ok), "reference_seconds": round(t, 1),
-                        "backend": type(be).__name__, "threads": threads}
-    print("grid", res["sssp_grid"], flush=True)
-    Path(out_path).write_text(json.dumps(res, indent=1))
-
-if "pr25" in which:
-    wl = bench.WORKLOADS["pr25"]
-    el, topo = bench.make_graph(wl)
-    g = topo.device
-    r = dv.pagerank(g, 20, 0.85).cpu().numpy().astype(np.float64)
-    tp, idx, deg = bench.host_reference_layout(g)
-    t0 = time.perf_counter()
-    ref = oracle.pagerank(tp, deg, 20, 0.85, threads)
-    t = time.perf_counter() - t0
-    err = float(np.max(np.abs(r - ref)))
-    res["pr25"] = {"max_abs_error": err, "tolerance": 1e-6, "ok": err <= 1e-6, "sum_gpu": float(r.sum()),
-                   "oracle": "oracle.pagerank (float64 C port)", "oracle_seconds": round(t, 1)}
-    print("pr25", res["pr25"], flush=True)
-    Path(out_path).write_text(json.dumps(res, indent=1))
+    n, E, tp, idx, deg, _ = bench.prepare_reference_input(wl)
+    prep = time.perf_counter() - t0
+    topo = ref.PullTopology(n, 4, E, tp.vec_dst, tp.lane_src, tp.lane_weight, tp.lane_count)
+    index = ref.EdgeIndex(n, tp.vector_count, idx.offsets, idx.positions)
+    prog = ref.make_program(wl["app"], None if wl["app"] == "cc" else 0)
+    cfg = ref.EngineConfig(threshold=ref.FullnessThreshold.of(wl["thr"]),
+                           precision=ref.FrontierPrecision(wl["vpg"]), workers=threads, max_iterations=n + 16)
+    t1 = time.perf_counter()
+    out = ref.run_until_convergence(topo, index, prog, deg, cfg, backend="native")
+    run = time.perf_counter() - t1
+    res[name] = {
+        "reference_digest": ref.result_digest(out.values), "iterations": len(out.stats),
+        "converged": out.converged, "V": n, "E": E,
+        "trace": [[s.iteration, s.mode, int(s.active_edges), int(s.frontier_out_size)] for s in out.stats],
+        "vectors_touched": [int(s.vectors_touched) for s in out.stats],
+        "source": "stock reference driver (baseline/_ref wedgegraph.run_until_convergence, native backend, "
+                  f"workers={threads}) on oracle-built inputs (tools/validate_full.py)",
+        "input_prep_s": round(prep, 1), "reference_seconds": round(run, 1),
+    }
+    print(name, res[name]["reference_digest"], len(out.stats), f"prep {prep:.0f}s run {run:.0f}s", flush=True)
+    del topo, index, tp, idx, deg, out
+    out_path.write_text(json.dumps(res, indent=1))
