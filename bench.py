@@ -247,7 +247,8 @@ def run_b200(args, wl):
     stream = torch.cuda.current_stream()
 
     def step(timer=None):
-        p = loop.seed(dinit, words, kern, thr, first_hit=fh, level_base=lvl, identity_init=ident)
+        # deferred: the seed runs as the loop graph's prologue (one launch per run)
+        p = loop.seed(dinit, words, kern, thr, first_hit=fh, level_base=lvl, identity_init=ident, defer=True)
         if timer is not None:
             p.timer = timer.handle
         return loop.drive(p, max_it)

@@ -389,6 +389,17 @@ void wg_run_graph_destroy(void *graph);
 void *wg_run_loop_graph_create(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p,
                                void *stream);
 int wg_run_loop_launch(void *graph, const wg_run_bufs *b, uint64_t max_iteration, void *stream);
+/* The same loop graph with the run's seed (wg_run_seed) captured in front of
+ * it, reading the initial values / frontier words from d_seed_values /
+ * d_seed_words (the graph's own buffers): a whole run is ONE launch.
+ * launch_seeded first copies the caller's initial state into those buffers
+ * (skipped when the pointers are the same). */
+void *wg_run_loop_graph_create_seeded(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p,
+                                      const void *d_seed_values, const uint32_t *d_seed_words,
+                                      const uint64_t *h_all_counts4, void *stream);
+int wg_run_loop_launch_seeded(void *graph, const wg_run_bufs *b, uint64_t max_iteration, const void *d_init_values,
+                              void *d_seed_values, size_t value_bytes, const uint32_t *d_init_words,
+                              uint32_t *d_seed_words, size_t word_bytes, void *stream);
 /* The persistent cooperative Wedge loop on its own (outside any graph): runs
  * consecutive Wedge iterations ctrl[0]+1 .. up to max_iteration and stops at
  * the first non-Wedge iteration; used by drivers and profilers. */

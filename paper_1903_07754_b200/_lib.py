@@ -87,6 +87,7 @@ EXPORTS = [
     "wg_ingest_vectors", "wg_ingest_u32", "wg_ingest_offsets", "wg_values_scan", "wg_vector_offsets_from_dst",
     "wg_run_seed", "wg_debug_kernel_timeline", "wg_debug_kernel_ids", "wg_first_lanes",
     "wg_pagerank_ws_bytes", "wg_pagerank_prep_ws_bytes", "wg_exchange_slice_pack", "wg_exchange_apply_slices",
+    "wg_run_loop_graph_create_seeded", "wg_run_loop_launch_seeded",
 ]
 
 _LIB = None
@@ -184,6 +185,9 @@ def load(path: os.PathLike | str | None = None):
         "wg_run_graph_destroy": (None, [c_vp]),
         "wg_run_loop_graph_create": (c_vp, [G, B, P, c_vp]),
         "wg_run_loop_launch": (ctypes.c_int, [c_vp, B, c_u64, c_vp]),
+        "wg_run_loop_graph_create_seeded": (c_vp, [G, B, P, c_vp, c_vp, u64p, c_vp]),
+        "wg_run_loop_launch_seeded": (ctypes.c_int, [c_vp, B, c_u64, c_vp, c_vp, ctypes.c_size_t, c_vp, c_vp,
+                                                     ctypes.c_size_t, c_vp]),
         "wg_run_persistent": (ctypes.c_int, [G, B, P, c_u64, c_vp]),
         "wg_debug_phase_buffer": (ctypes.c_int, [c_vp, c_u64]),
         "wg_index_scratch_bytes": (ctypes.c_size_t, [c_u64, c_u32]),

@@ -5,6 +5,7 @@
 
 #include <mutex>
 #include <unordered_map>
+#include <vector>
 
 #include "frontier.cuh"
 #include "pull.cuh"
@@ -723,6 +724,7 @@ struct InitRanges {
     const void *init;  // [n] values of val_type, or null
     void *vals[2];
     uint64_t n, vbytes;
+    int keep_limit;  // seeded loop graph: ctrl[1] was set by the launch (wg_run_loop_launch_seeded)
 };
 
 // frontier 0 = every vertex: its counts are the graph's own totals
@@ -740,7 +742,7 @@ __global__ void run_init_kernel(InitRanges r) {
     const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
     if (tid == 0) {
         r.ctrl[0] = 0;
-        r.ctrl[1] = ~0ull;  // no iteration limit
+        if (!r.keep_limit) r.ctrl[1] = ~0ull;  // no iteration limit
         r.ctrl[2] = 0;
         r.ctrl[3] = 0;
     }
@@ -768,12 +770,10 @@ __global__ void run_init_kernel(InitRanges r) {
 
 extern "C" {
 
-int wg_run_seed(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p, const void *d_init_values,
-                const uint32_t *d_init_words, const uint64_t *h_all_counts4, void *stream) {
-    int rc = check_run(g, b, p);
-    if (rc) return rc;
+static int seed_launches(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p, const void *d_init_values,
+                         const uint32_t *d_init_words, const uint64_t *h_all_counts4, cudaStream_t s,
+                         int keep_limit = 0) {
     WG_REQUIRE(d_init_words || h_all_counts4, "null initial frontier");
-    cudaStream_t s = as_stream(stream);
     const uint64_t words = ((uint64_t)g->n + 31) >> 5;
     const uint64_t gwords = (groups_of(g, p->shift) + 31) >> 5;
     InitRanges r{};
@@ -798,6 +798,7 @@ int wg_run_seed(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p,
     r.vals[1] = b->vals[1];
     r.n = g->n;
     r.vbytes = p->val_type == WG_VAL_U32 ? 4 : 8;
+    r.keep_limit = keep_limit;
     run_init_kernel<<<grid_for(words * 32 + 1, 256 * 4, 4), 256, 0, s>>>(r);
     ::wg::count_launch();
     WG_CHECK_LAUNCH("run_init");
@@ -817,6 +818,13 @@ int wg_run_seed(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p,
     return launch_frontier_compaction(g, d_init_words, b->bcount, bcount_ticket(g, p->shift, b->bcount),
                                       b->fvert[0], b->fpref[0], b->tstart[0],
                                       &b->recs[0], s, (p->flags & WG_RUN_KEEP_LISTS) ? 1 : 0, p->wedge_limit);
+}
+
+int wg_run_seed(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p, const void *d_init_values,
+                const uint32_t *d_init_words, const uint64_t *h_all_counts4, void *stream) {
+    int rc = check_run(g, b, p);
+    if (rc) return rc;
+    return seed_launches(g, b, p, d_init_values, d_init_words, h_all_counts4, as_stream(stream));
 }
 
 int wg_run_init(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p,
@@ -957,10 +965,49 @@ static cudaError_t capture_if_node(cudaStream_t s, cudaGraphConditionalHandle h,
     return e;
 }
 
+struct SeedSpec {
+    const void *vals;
+    const uint32_t *words;
+    const uint64_t *counts;  // host, 4 words, or null
+};
+
+static void *create_loop_graph(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p,
+                               const SeedSpec *seed);
+
 void *wg_run_loop_graph_create(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p,
                                void *stream) {
-    if (check_run(g, b, p)) return nullptr;
     (void)stream;
+    return create_loop_graph(g, b, p, nullptr);
+}
+
+void *wg_run_loop_graph_create_seeded(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p,
+                                      const void *d_seed_values, const uint32_t *d_seed_words,
+                                      const uint64_t *h_all_counts4, void *stream) {
+    (void)stream;
+    SeedSpec sp{d_seed_values, d_seed_words, h_all_counts4};
+    return create_loop_graph(g, b, p, &sp);
+}
+
+int wg_run_loop_launch_seeded(void *graph, const wg_run_bufs *b, uint64_t max_iteration, const void *d_init_values,
+                              void *d_seed_values, size_t value_bytes, const uint32_t *d_init_words,
+                              uint32_t *d_seed_words, size_t word_bytes, void *stream) {
+    WG_REQUIRE(graph && b && b->ctrl, "null argument");
+    cudaStream_t s = as_stream(stream);
+    // the caller's initial state into the buffers the graph reads
+    if (d_init_values && d_init_values != d_seed_values && value_bytes)
+        WG_CUDA(cudaMemcpyAsync(d_seed_values, d_init_values, value_bytes, cudaMemcpyDeviceToDevice, s));
+    if (d_init_words && d_init_words != d_seed_words && word_bytes)
+        WG_CUDA(cudaMemcpyAsync(d_seed_words, d_init_words, word_bytes, cudaMemcpyDeviceToDevice, s));
+    set_limit_kernel<<<1, 1, 0, s>>>(b->ctrl, max_iteration);
+    ::wg::count_launch();
+    WG_CHECK_LAUNCH("set_limit");
+    WG_CUDA(cudaGraphLaunch((cudaGraphExec_t)graph, s));
+    return WG_OK;
+}
+
+static void *create_loop_graph(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p,
+                               const SeedSpec *seed) {
+    if (check_run(g, b, p)) return nullptr;
     // capture on private streams (the legacy default stream cannot capture)
     cudaStream_t s = nullptr, s2 = nullptr;
     if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess ||
@@ -981,15 +1028,37 @@ void *wg_run_loop_graph_create(const wg_graph *g, const wg_run_bufs *b, const wg
         set_error("cudaGraphCreate failed");
         return nullptr;
     }
+    // optional prologue: the run's seed (wg_run_seed) as the graph's first nodes
+    std::vector<cudaGraphNode_t> pro;
+    cudaError_t e = cudaSuccess;
+    if (seed) {
+        e = cudaStreamBeginCaptureToGraph(s, graph, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+        int rc = e == cudaSuccess ? seed_launches(g, b, p, seed->vals, seed->words, seed->counts, s, 1) : WG_OK;
+        if (e == cudaSuccess) {
+            cudaStreamCaptureStatus st;
+            const cudaGraphNode_t *deps = nullptr;
+            size_t nd = 0;
+            e = cudaStreamGetCaptureInfo(s, &st, nullptr, nullptr, &deps, &nd);
+            if (e == cudaSuccess) pro.assign(deps, deps + nd);
+            cudaGraph_t gout = nullptr;
+            cudaError_t e2 = cudaStreamEndCapture(s, &gout);
+            if (e == cudaSuccess) e = e2;
+        }
+        if (rc != WG_OK || e != cudaSuccess) {
+            cudaGraphDestroy(graph);
+            if (rc == WG_OK) cuda_fail(e, "seed prologue capture");
+            return nullptr;
+        }
+    }
     cudaGraphConditionalHandle hw;
-    cudaError_t e = cudaGraphConditionalHandleCreate(&hw, graph, 1, cudaGraphCondAssignDefault);
+    e = cudaGraphConditionalHandleCreate(&hw, graph, 1, cudaGraphCondAssignDefault);
     cudaGraphNodeParams cp = {};
     cp.type = cudaGraphNodeTypeConditional;
     cp.conditional.handle = hw;
     cp.conditional.type = cudaGraphCondTypeWhile;
     cp.conditional.size = 1;
     cudaGraphNode_t node;
-    if (e == cudaSuccess) e = cudaGraphAddNode(&node, graph, nullptr, 0, &cp);
+    if (e == cudaSuccess) e = cudaGraphAddNode(&node, graph, pro.empty() ? nullptr : pro.data(), pro.size(), &cp);
     if (e != cudaSuccess) {
         cudaGraphDestroy(graph);
         cuda_fail(e, "conditional node");

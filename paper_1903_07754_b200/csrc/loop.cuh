@@ -96,9 +96,15 @@ __device__ __forceinline__ bool dst_major_active(const LoopCtx &c, uint64_t it, 
                                                  bool bottom_up) {
     if (!dst_major) return false;
     if (!bottom_up) return true;
+    // frontier(it-1)'s size from its counts (set by the pull / compaction that
+    // produced it, before its end-of-iteration record) plus every earlier
+    // frontier's (the cumulative count end_of_iteration keeps in reserved[4])
     const wg_iter_rec *in = ctx_in(c, it);
-    const uint64_t seen = it == 1 ? *(volatile const uint64_t *)&in->frontier_out
-                                  : *(volatile const uint64_t *)&in->reserved[4];
+    uint64_t seen = (*(volatile const uint64_t *)&in->nz_packed >> 32) + *(volatile const uint64_t *)&in->z_count;
+    if (it >= 2) {
+        const wg_iter_rec *pp = &c.recs[(it - 2) % c.ring];
+        seen += it == 2 ? *(volatile const uint64_t *)&pp->frontier_out : *(volatile const uint64_t *)&pp->reserved[4];
+    }
     return seen * DST_BU_VISITED_DIV >= n;
 }
 

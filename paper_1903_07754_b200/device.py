@@ -902,10 +902,13 @@ class DeviceLoop:
         return p
 
     def seed(self, init_values, init_words, kern, threshold, stream=None, first_hit: bool = False,
-             level_base: int = 0, identity_init: bool = False, extra_flags: int = 0) -> WgRunParams:
+             level_base: int = 0, identity_init: bool = False, extra_flags: int = 0,
+             defer: bool = False) -> WgRunParams:
         """Write both value buffers and build iteration 0 from the frontier bitmap.
         first_hit: the caller checked first_hit_ok (level-synchronous values);
-        level_base: then the common value of the initial frontier (first_hit_level)."""
+        level_base: then the common value of the initial frontier (first_hit_level).
+        defer: leave the seed to the next drive(), which runs it as the first
+        nodes of the loop graph (one launch per run; wg_run_loop_graph_create_seeded)."""
         if init_values.numel() < self.g.n or init_values.dtype != self.vals[0].dtype:
             raise ValueError("initial values do not match the loop's value buffers")
         self._level_base = int(level_base)
@@ -914,12 +917,22 @@ class DeviceLoop:
         if getattr(init_words, "_wg_all", False) and not (p.flags & _lib.WG_RUN_KEEP_LISTS):
             c4 = self.g.all_vertex_counts()
             if not (self.g.edges > 0 and c4[3] < p.wedge_limit):  # iteration 1 is dense
-                counts = (ctypes.c_uint64 * 4)(*c4)
-        check(_lib.load().wg_run_seed(ctypes.byref(self.g.struct()), ctypes.byref(self.bufs), ctypes.byref(p),
-                                      _ptr(init_values), _ptr(init_words), counts, _lib.stream_ptr(stream)))
+                counts = tuple(int(x) for x in c4)
+        self._pending = (init_values, init_words, counts)
+        if not defer:
+            self._run_pending_seed(p, stream)
         return p
 
+    def _run_pending_seed(self, p, stream=None):
+        init_values, init_words, counts = self._pending
+        self._pending = None
+        c = (ctypes.c_uint64 * 4)(*counts) if counts is not None else None
+        check(_lib.load().wg_run_seed(ctypes.byref(self.g.struct()), ctypes.byref(self.bufs), ctypes.byref(p),
+                                      _ptr(init_values), _ptr(init_words), c, _lib.stream_ptr(stream)))
+
     def enqueue(self, p: WgRunParams, it_begin: int, count: int, stream=None) -> None:
+        if getattr(self, "_pending", None) is not None:
+            self._run_pending_seed(p, stream)
         check(_lib.load().wg_run_enqueue(ctypes.byref(self.g.struct()), ctypes.byref(self.bufs),
                                          ctypes.byref(p), it_begin, count, _lib.stream_ptr(stream)))
 
@@ -940,20 +953,40 @@ class DeviceLoop:
     def launch(self, p: WgRunParams, limit: int, stream=None) -> None:
         """Run the loop graph up to iteration `limit` without reading anything
         back (one launch instead of one per kernel; the caller synchronises)."""
+        if getattr(self, "_pending", None) is not None:
+            self._run_pending_seed(p, stream)
         check(_lib.load().wg_run_loop_launch(self._graph_for(p, stream), ctypes.byref(self.bufs), int(limit),
                                              _lib.stream_ptr(stream)))
 
-    def _graph_for(self, p: WgRunParams, stream=None):
+    def _seed_buffers(self, words_numel: int):
+        """The seeded graph's own initial-state buffers."""
+        torch = _torch()
+        if getattr(self, "seed_vals", None) is None:
+            self.seed_vals = torch.empty_like(self.vals[0])
+        if getattr(self, "seed_words", None) is None or self.seed_words.numel() < words_numel:
+            self.seed_words = torch.empty(words_numel, dtype=torch.int32, device=self.vals[0].device)
+        return self.seed_vals, self.seed_words
+
+    def _graph_for(self, p: WgRunParams, stream=None, seeded=None):
+        """seeded: (counts or None) -- the graph with the seed prologue."""
         key = (p.val_type, p.shift, p.kern.filter_unvisited, p.kern.use_weight, p.kern.apply_increment,
-               p.kern.sentinel, p.wedge_limit, p.flags, p.level_base, self.g.signature())
+               p.kern.sentinel, p.wedge_limit, p.flags, p.level_base, self.g.signature(),
+               None if seeded is None else ("seeded", seeded))
         exe = self.graph_cache.get(key)
         if exe is None:
             q = WgRunParams()
             ctypes.pointer(q)[0] = p
             q.timer = None
             L = _lib.load()
-            exe = L.wg_run_loop_graph_create(ctypes.byref(self.g.struct()), ctypes.byref(self.bufs),
-                                             ctypes.byref(q), _lib.stream_ptr(stream))
+            if seeded is not None:
+                sv, sw = self._seed_buffers(max((self.g.n + 31) >> 5, 1))
+                c = (ctypes.c_uint64 * 4)(*seeded[1]) if seeded[1] is not None else None
+                exe = L.wg_run_loop_graph_create_seeded(ctypes.byref(self.g.struct()), ctypes.byref(self.bufs),
+                                                        ctypes.byref(q), _ptr(sv), _ptr(sw), c,
+                                                        _lib.stream_ptr(stream))
+            else:
+                exe = L.wg_run_loop_graph_create(ctypes.byref(self.g.struct()), ctypes.byref(self.bufs),
+                                                 ctypes.byref(q), _lib.stream_ptr(stream))
             if not exe:
                 raise _lib.WedgeError(_lib.WG_ECUDA, L.wg_last_error().decode())
             if len(self.graph_cache) >= 8:  # keep a few (the stream is ordered: no replay in flight reads it)
@@ -994,13 +1027,25 @@ class DeviceLoop:
         torch = _torch()
         s = stream or torch.cuda.current_stream()
         L = _lib.load()
+        sp = _lib.stream_ptr(stream)
+        pending = getattr(self, "_pending", None)
+        self._pending = None
         exe = self._graph_for(p, stream)
         records: list[IterRecord] = []
         it, converged, last = 1, False, 0
         ctrl_host = self.ctrl_host
         while it <= max_iterations and not converged:
             limit = min(max_iterations, it - 1 + self.ring - 2)
-            check(L.wg_run_loop_launch(exe, ctypes.byref(self.bufs), limit, _lib.stream_ptr(stream)))
+            if pending is not None:  # the run's seed is the first launch's prologue
+                init_values, init_words, counts = pending
+                pending = None
+                exe0 = self._graph_for(p, stream, seeded=("all" if counts is not None else "words", counts))
+                sv, sw = self._seed_buffers(init_words.numel())
+                check(L.wg_run_loop_launch_seeded(exe0, ctypes.byref(self.bufs), limit, _ptr(init_values), _ptr(sv),
+                                                  self.g.n * init_values.element_size(), _ptr(init_words), _ptr(sw),
+                                                  min(init_words.numel(), sw.numel()) * 4, sp))
+            else:
+                check(L.wg_run_loop_launch(exe, ctypes.byref(self.bufs), limit, sp))
             # the control word and the whole record ring in one round trip (a
             # launch runs at most ring - 2 iterations, so its records are all there)
             ctrl_host.copy_(self.ctrl, non_blocking=True)
@@ -1026,6 +1071,8 @@ class DeviceLoop:
             graph = os.environ.get("WG_GRAPH", "1") != "0"
         if trace is None and graph and p.timer is None:
             return self.drive_graph(p, max_iterations, stream)
+        if getattr(self, "_pending", None) is not None:  # a deferred seed: run it now
+            self._run_pending_seed(p, stream)
         records: list[IterRecord] = []
         converged = False
         it, batch, last = 1, 2, 0

@@ -312,7 +312,7 @@ def device_run(be, topology, index, program: ApplicationProgram, degrees, config
         start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         start.record()
         p = loop.seed(iv.seed(val_type), words, kern, config.threshold.fraction, first_hit=iv.first_hit,
-                      level_base=iv.level_base, identity_init=iv.identity)
+                      level_base=iv.level_base, identity_init=iv.identity, defer=True)
         timer = None
         if getattr(be, "per_iteration_timing", False):
             # CUDA events around each launch group (one iteration per launch)

@@ -29,7 +29,7 @@ thr = Fraction(wl["thr"])
 
 def run(cap):
     p = loop.seed(iv.seed(_lib.WG_VAL_U32), words, prog.kernel, thr, first_hit=iv.first_hit,
-                  level_base=iv.level_base, identity_init=iv.identity)
+                  level_base=iv.level_base, identity_init=iv.identity, defer=True)
     return loop.drive(p, cap)
 
 
@@ -47,7 +47,7 @@ for cap in range(0, K + 1):
             run(cap)
         else:
             loop.seed(iv.seed(_lib.WG_VAL_U32), words, prog.kernel, thr, first_hit=iv.first_hit,
-                      level_base=iv.level_base, identity_init=iv.identity)
+                      level_base=iv.level_base, identity_init=iv.identity, defer=True)
         b.record(stream)
         b.synchronize()
         best = min(best, a.elapsed_time(b))

@@ -43,7 +43,7 @@ for r in range(runs):
     phases.zero_()
     _lib.check(L.wg_debug_phase_buffer(phases.data_ptr() if r == runs - 1 else None, CAP))
     p = loop.seed(iv.seed(_lib.WG_VAL_U32), words, prog.kernel, Fraction(wl["thr"]), first_hit=iv.first_hit,
-                  level_base=iv.level_base, identity_init=iv.identity)
+                  level_base=iv.level_base, identity_init=iv.identity, defer=True)
     recs, conv, last = loop.drive(p, g.n + 16)
     torch.cuda.synchronize()
 _lib.check(L.wg_debug_kernel_timeline(None, 0))
