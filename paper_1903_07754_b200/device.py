@@ -628,11 +628,11 @@ class DeviceGraph:
         self._struct = None
         return self.voff
 
-    def signature(self) -> tuple:
+    def signature(self) -> bytes:
         """Every field of the C struct: a loop graph captured for one
         signature must not be replayed after any of them changed."""
         st = self.struct()
-        return tuple(getattr(st, f) for f, _ in WgGraph._fields_)
+        return ctypes.string_at(ctypes.addressof(st), ctypes.sizeof(st))
 
     def weighted(self) -> bool:
         return self.vw is not None
@@ -887,6 +887,17 @@ class DeviceLoop:
 
     def params(self, kern, threshold: Fraction, first_hit: bool = False,
                identity_init: bool = False, extra_flags: int = 0) -> WgRunParams:
+        ck = (kern, threshold, first_hit, identity_init, extra_flags, self._level_base if first_hit else 0,
+              os.environ.get("WG_FLOOR_SKIP", "1"), self.g.edges, self.g.entries)
+        hit = getattr(self, "_params_cache", None)
+        if hit is not None and hit[0] == ck:
+            return WgRunParams.from_buffer_copy(hit[1])  # a fresh copy: callers may set timer / flags
+        p = self._make_params(kern, threshold, first_hit, identity_init, extra_flags)
+        self._params_cache = (ck, WgRunParams.from_buffer_copy(p))
+        return p
+
+    def _make_params(self, kern, threshold: Fraction, first_hit: bool = False,
+                     identity_init: bool = False, extra_flags: int = 0) -> WgRunParams:
         p = WgRunParams()
         p.val_type = self.val_type
         p.shift = self.shift
@@ -969,9 +980,9 @@ class DeviceLoop:
 
     def _graph_for(self, p: WgRunParams, stream=None, seeded=None):
         """seeded: (counts or None) -- the graph with the seed prologue."""
-        key = (p.val_type, p.shift, p.kern.filter_unvisited, p.kern.use_weight, p.kern.apply_increment,
-               p.kern.sentinel, p.wedge_limit, p.flags, p.level_base, self.g.signature(),
-               None if seeded is None else ("seeded", seeded))
+        q0 = WgRunParams.from_buffer_copy(p)
+        q0.timer = None  # the graphs never carry a timer
+        key = (ctypes.string_at(ctypes.addressof(q0), ctypes.sizeof(q0)), self.g.signature(), seeded)
         exe = self.graph_cache.get(key)
         if exe is None:
             q = WgRunParams()
