@@ -41,14 +41,18 @@ def _stale() -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: Path | None = None, extra=()) -> Path:
+    """extra: additional nvcc flags (e.g. -DSPARSE_U=4) for experiment builds
+    written to `out` instead of the library."""
+    target = Path(out) if out else OUT
+    if not force and not extra and not _stale():
         return OUT
-    BUILD.mkdir(parents=True, exist_ok=True)
+    build_dir = BUILD if not extra else BUILD.with_name(BUILD.name + "_" + target.stem)
+    build_dir.mkdir(parents=True, exist_ok=True)
     procs = []
     for src in SOURCES:
-        obj = BUILD / (Path(src).stem + ".o")
-        cmd = [nvcc(), *NVCC_FLAGS, "-c", str(CSRC / src), "-o", str(obj)]
+        obj = build_dir / (Path(src).stem + ".o")
+        cmd = [nvcc(), *NVCC_FLAGS, *extra, "-c", str(CSRC / src), "-o", str(obj)]
         procs.append((src, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
     objs = []
     failed = []
@@ -62,14 +66,14 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if failed:
         msg = "\n".join(f"--- {s}\n{o}" for s, o in failed)
         raise RuntimeError(f"nvcc failed:\n{msg}")
-    tmp = OUT.with_suffix(".so.tmp")
+    tmp = target.with_suffix(".so.tmp")
     cmd = [nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", str(tmp),
            "-cudart", "static"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    os.replace(tmp, OUT)
-    return OUT
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":

@@ -110,7 +110,7 @@ def load(path: os.PathLike | str | None = None):
     global _LIB
     if _LIB is not None and path is None:
         return _LIB
-    p = Path(path) if path else LIB_PATH
+    p = Path(path) if path else Path(os.environ.get("WG_LIB", LIB_PATH))  # WG_LIB: an experiment build
     if not p.exists():
         raise RuntimeError(
             f"{p} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "

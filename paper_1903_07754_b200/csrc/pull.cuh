@@ -812,7 +812,7 @@ __device__ __forceinline__ void dense_dst_phase(const LoopCtx &c, uint64_t it, c
     const uint64_t span = 32ull * DST_K;  // destinations per warp step, word-aligned
     for (uint64_t wb = warp0 * span; wb < n; wb += nwarps * span) {
         T p[DST_K], agg[DST_K];
-        uint32_t v0[DST_K], v1[DST_K], s0[DST_K];
+        uint32_t v0[DST_K], v1[DST_K], s0[DST_K], deg[DST_K];
         bool need[DST_K];
         // (a) prev[d], d's vector range and (FLOOR) its smallest source, DST_K
         // destinations in flight
@@ -824,16 +824,15 @@ __device__ __forceinline__ void dense_dst_phase(const LoopCtx &c, uint64_t it, c
             v0[k] = ok ? voff[d] : 0u;
             v1[k] = ok ? voff[d + 1] : 0u;
             if constexpr (KIND == DSTK_FLOOR) s0[k] = ok && g.vfirst ? g.vfirst[d] : WG_NO_LANE;
+            // out-degree for the frontier counts, in the same round trip (no
+            // dependency on the values: 4 bytes per vertex)
+            deg[k] = ok ? g.outdeg[d] : 0u;
         }
-        // (b) FLOOR: the first lane of every destination not at the floor;
-        // the out-degree of every destination that may join the frontier
-        // (read now, consumed by the counts at the end of the step)
-        uint32_t deg[DST_K];
+        // (b) FLOOR: the first lane of every destination not at the floor
 #pragma unroll
         for (int k = 0; k < DST_K; ++k) {
             need[k] = v1[k] > v0[k] && (KIND == DSTK_FLOOR ? p[k] != (T)0 : p[k] == INF);
             agg[k] = INF;
-            deg[k] = need[k] ? g.outdeg[wb + 32 * k + lane] : 0u;
         }
         if constexpr (KIND == DSTK_FLOOR) {
             if (!g.vfirst) {
