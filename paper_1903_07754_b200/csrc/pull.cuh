@@ -680,11 +680,14 @@ __global__ void __launch_bounds__(256) bottom_up_pull_kernel(LoopCtx c, wg_graph
     const uint32_t *__restrict__ inbits = (((it - 1) & 1) ? b.fbits[1] : b.fbits[0]);
     const T INF = VT::inf(sentinel);
     const T level = (T)(b.level_base + (int64_t)(it - 1) * inc);
+    // a uint32 candidate that does not fit is an overflow only where it
+    // would be applied (a hit), like the pipeline and floor kernels
+    bool cand_ovf = false;
     uint32_t ovf = 0;
     T cand = INF;
     if constexpr (VT::U32) {
         const uint64_t cc = (uint64_t)level + (uint64_t)inc;
-        if (cc >= 0xffffffffull) ovf = 1;
+        if (cc >= 0xffffffffull) cand_ovf = true;
         else cand = (T)cc;
     } else {
         cand = level + (T)inc;
@@ -724,6 +727,7 @@ __global__ void __launch_bounds__(256) bottom_up_pull_kernel(LoopCtx c, wg_graph
         }
 #pragma unroll
         for (int k = 0; k < K; ++k) {
+            if (hit[k] && cand_ovf) ovf = 1;
             if (!hit[k] || cand == INF) continue;
             if constexpr (VT::U32) atomicMin((unsigned *)&nxt[d[k]], (unsigned)cand);
             else atomicMin((long long *)&nxt[d[k]], (long long)cand);
@@ -795,12 +799,13 @@ __device__ __forceinline__ void dense_dst_phase(const LoopCtx &c, uint64_t it, c
     };
     const bool exact_first = KIND == DSTK_FLOOR && b.ident && it == 1;  // identity values: lane 0 is the min
     uint32_t ovf = 0;
+    bool bu_ovf = false;  // flagged only where a hit would apply it
     T bu_cand = INF;  // bottom-up: the level after the previous frontier's
     if constexpr (KIND == DSTK_BOTTOM_UP) {
         const T level = (T)(b.level_base + (int64_t)(it - 1) * inc);
         if constexpr (VT::U32) {
             const uint64_t cc = (uint64_t)level + (uint64_t)inc;
-            if (cc >= 0xffffffffull) ovf = 1;
+            if (cc >= 0xffffffffull) bu_ovf = true;
             else bu_cand = (T)cc;
         } else {
             bu_cand = level + (T)inc;
@@ -937,6 +942,7 @@ __device__ __forceinline__ void dense_dst_phase(const LoopCtx &c, uint64_t it, c
                 T cand = INF;
                 if constexpr (KIND == DSTK_BOTTOM_UP) {
                     cand = bu_cand;
+                    if (bu_ovf) ovf = 1;
                 } else if constexpr (VT::U32) {
                     const uint64_t cc = (uint64_t)agg[k] + (uint64_t)inc;
                     if (cc >= 0xffffffffull) ovf = 1;
