@@ -484,6 +484,22 @@ uint64_t wg_launch_count(void);
 size_t wg_pagerank_ws_bytes(const wg_graph *g);
 int wg_pagerank(const wg_graph *g, int iterations, double damping, float *d_rank, float *d_acc,
                 float *d_contrib, double *d_scal, void *d_ws, size_t ws_bytes, void *stream);
+/* Hot-source layout for PageRank (no reference symbol; BASELINE.json config
+ * 5).  The pull gathers contrib[src] once per edge; RMAT's heavy sources are
+ * scattered over the id space.  wg_pagerank_hot_layout numbers the vertices
+ * that have out-edges by descending out-degree (stable): d_order [n] = slot ->
+ * vertex (slots >= *h_nsrc are the vertices without out-edges, ascending),
+ * d_od_hot [n] = out-degree per slot, d_vsrc_hot [nvec*width, same slack as
+ * vsrc] = g's lanes with each source replaced by its slot.  Lane order is kept,
+ * so every sum is taken in the order wg_pagerank takes it.  Synchronises.
+ * d_ws: wg_pagerank_hot_ws_bytes(g).  wg_pagerank_hot = wg_pagerank through
+ * that layout (d_contrib needs *h_nsrc floats; d_ws: wg_pagerank_ws_bytes). */
+size_t wg_pagerank_hot_ws_bytes(const wg_graph *g);
+int wg_pagerank_hot_layout(const wg_graph *g, uint32_t *d_vsrc_hot, uint32_t *d_order, uint32_t *d_od_hot,
+                           uint64_t *h_nsrc, void *d_ws, size_t ws_bytes, void *stream);
+int wg_pagerank_hot(const wg_graph *g, const uint32_t *d_vsrc_hot, const uint32_t *d_order,
+                    const uint32_t *d_od_hot, uint64_t nsrc, int iterations, double damping, float *d_rank,
+                    float *d_acc, float *d_contrib, double *d_scal, void *d_ws, size_t ws_bytes, void *stream);
 /* The two halves of one iteration, for destination-sharded runs (SURVEY
  * §8(e)): prep(it) applies the accumulated sums of iteration it-1 to all n
  * ranks (it = 0: 1/n), writes d_rank when non-null, zeroes d_acc, builds the

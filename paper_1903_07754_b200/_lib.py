@@ -88,6 +88,7 @@ EXPORTS = [
     "wg_run_seed", "wg_debug_kernel_timeline", "wg_debug_kernel_ids", "wg_first_lanes",
     "wg_pagerank_ws_bytes", "wg_pagerank_prep_ws_bytes", "wg_exchange_slice_pack", "wg_exchange_apply_slices",
     "wg_run_loop_graph_create_seeded", "wg_run_loop_launch_seeded",
+    "wg_pagerank_hot_ws_bytes", "wg_pagerank_hot_layout", "wg_pagerank_hot",
 ]
 
 _LIB = None
@@ -145,6 +146,10 @@ def load(path: os.PathLike | str | None = None):
         "wg_exchange_apply_slices": (ctypes.c_int, [G, B, P, c_u64, c_vp, c_vp, c_u32, c_u32, c_u64, c_vp]),
         "wg_pagerank": (ctypes.c_int, [G, ctypes.c_int, ctypes.c_double, c_vp, c_vp, c_vp, c_vp, c_vp,
                                        ctypes.c_size_t, c_vp]),
+        "wg_pagerank_hot_ws_bytes": (ctypes.c_size_t, [G]),
+        "wg_pagerank_hot_layout": (ctypes.c_int, [G, c_vp, c_vp, c_vp, u64p, c_vp, ctypes.c_size_t, c_vp]),
+        "wg_pagerank_hot": (ctypes.c_int, [G, c_vp, c_vp, c_vp, c_u64, ctypes.c_int, ctypes.c_double, c_vp, c_vp,
+                                           c_vp, c_vp, c_vp, ctypes.c_size_t, c_vp]),
         "wg_pagerank_prep_ws_bytes": (ctypes.c_size_t, [c_u32]),
         "wg_pagerank_prep": (ctypes.c_int, [c_u32, ctypes.c_int, ctypes.c_double, c_vp, c_vp, c_vp, c_vp,
                                             c_vp, c_vp, ctypes.c_size_t, c_vp]),

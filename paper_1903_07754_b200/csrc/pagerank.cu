@@ -18,6 +18,8 @@
 // -> dangling sum -> pull (E-sized) -> fixup.  The fixed order depends only
 // on the launch configuration (grid sizes from the occupancy query), so runs
 // on the same GPU and build are bit-identical.
+#include <cub/cub.cuh>
+
 #include "common.cuh"
 #include "tma.cuh"  // warp_range
 
@@ -39,27 +41,54 @@ struct PrBound {
 
 unsigned prep_grid(uint32_t n) { return grid_for(n, PR_THREADS * 4, 8); }
 
-// prep(it): r = it ? base(D_{it-1}) + d*acc : 1/N; acc = 0; contrib = r/outdeg;
-// the block's dangling mass of r into dpart[block].
+// prep(it): r = it ? base(D_{it-1}) + d*acc : 1/N; contrib = r/outdeg; the
+// block's dangling mass of r into dpart[block].  ZERO: also acc = 0 (callers
+// whose pull does not rewrite every destination's sum: the sharded path's
+// gathered sum vector); wg_pagerank's own pull writes every vertex of its
+// range, in-degree 0 included (pr_pull's gap fill), so nothing is cleared.
+// Four vertices per thread and round trip (128-bit loads / stores).
+template <bool ZERO>
 __global__ void __launch_bounds__(PR_THREADS) pr_prep(uint32_t n, int it, double damping,
-                                                      const uint32_t *outdeg, float *acc, float *contrib,
-                                                      float *rank_out, const double *scal, double *dpart) {
+                                                      const uint32_t *__restrict__ outdeg, float *__restrict__ acc,
+                                                      float *__restrict__ contrib, float *__restrict__ rank_out,
+                                                      const double *__restrict__ scal, double *__restrict__ dpart) {
     __shared__ double sm[33];
     double dang = 0.0;
     const float base = it ? (float)((1.0 - damping) / n + damping * scal[0] / n) : 0.f;
     const float df = (float)damping;
     const float r0 = (float)(1.0 / n);
-    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
-         v += (uint64_t)gridDim.x * blockDim.x) {
-        float r = it ? base + df * acc[v] : r0;
-        acc[v] = 0.f;
-        uint32_t od = outdeg[v];
+    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+    const auto one = [&](float a, uint32_t od, float &c) -> float {
+        const float r = it ? base + df * a : r0;
         if (od) {
-            contrib[v] = r / (float)od;
+            c = r / (float)od;
         } else {
-            contrib[v] = 0.f;
+            c = 0.f;
             dang += r;
         }
+        return r;
+    };
+    const bool aligned = (((uintptr_t)outdeg | (uintptr_t)acc | (uintptr_t)contrib | (uintptr_t)rank_out) & 15u) == 0;
+    const uint64_t quads = aligned ? n >> 2 : 0;
+    for (uint64_t q = tid; q < quads; q += nth) {
+        const uint4 od = reinterpret_cast<const uint4 *>(outdeg)[q];
+        float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (it) a = reinterpret_cast<const float4 *>(acc)[q];
+        float4 c, r;
+        r.x = one(a.x, od.x, c.x);
+        r.y = one(a.y, od.y, c.y);
+        r.z = one(a.z, od.z, c.z);
+        r.w = one(a.w, od.w, c.w);
+        if (ZERO) reinterpret_cast<float4 *>(acc)[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        reinterpret_cast<float4 *>(contrib)[q] = c;
+        if (rank_out) reinterpret_cast<float4 *>(rank_out)[q] = r;
+    }
+    for (uint64_t v = (quads << 2) + tid; v < n; v += nth) {
+        float c;
+        const float r = one(it ? acc[v] : 0.f, outdeg[v], c);
+        if (ZERO) acc[v] = 0.f;
+        contrib[v] = c;
         if (rank_out) rank_out[v] = r;
     }
     const double tot = block_sum(dang, sm);
@@ -109,6 +138,24 @@ __global__ void __launch_bounds__(PR_THREADS) pr_pull(wg_graph g, const float *_
             const uint32_t dn = __shfl_down_sync(FULL, d, 1);
             const uint32_t dp = __shfl_up_sync(FULL, d, 1);
             const bool head = lane == 0 || dp != d;
+            // Gap fill: the destinations between the previous vector's and this
+            // one's have no in-edges -- their sum is 0.  Writing them here (by
+            // the lane that opens the next destination) makes the pull write
+            // its whole destination range: every 32-byte sector of acc leaves
+            // L2 fully written (partially written sectors cost the ECC DRAM a
+            // read-modify-write each when evicted, which made the V-sized prep
+            // pass that follows 13x slower than its traffic), and prep need
+            // not clear acc.
+            {
+                uint32_t prevd = dp;  // destination of the vector before this lane's
+                bool from_start = false;
+                if (lane == 0) {
+                    prevd = tile == t0 ? dleft : cd;
+                    from_start = tile == t0 && p_lo == 0;
+                }
+                if (valid && (from_start || d != prevd))
+                    for (uint32_t x = from_start ? base : prevd + 1; x < d; ++x) acc[x - base] = 0.f;
+            }
             const bool tail = lane == 31 || dn != d;
             const unsigned heads = __ballot_sync(FULL, head);
             const unsigned head_lane = 31 - __clz(heads & (0xffffffffu >> (31 - lane)));
@@ -196,6 +243,97 @@ __global__ void pr_fixup(const PrBound *bounds, uint64_t nwarps, float *acc, uin
     }
 }
 
+// ---- hot-source layout (wg_pagerank_hot_*) -------------------------------
+// The pull's cost is its E random 4-byte gathers of contrib[src]: they run
+// L1TEX at 80% and L2 at 70% of their sector throughput while DRAM idles
+// (profiles/r02_ncu_pr_pull_*).  A source is gathered once per out-edge, and
+// RMAT's heavy sources are scattered over the id space (the ids with few set
+// bits), so a fetched 32-byte sector holds one hot value among cold ones.
+// Here the sources are renumbered by descending out-degree (stable): slot j
+// of contrib belongs to vertex order[j], the lanes of a PageRank-only copy of
+// vsrc hold slots, and only the nsrc vertices that have out-edges get a slot.
+// Hot values now share sectors and lines (higher L1 / L2 hit rates, fewer
+// distinct lines per warp gather); lane order, and with it every float sum,
+// is unchanged.
+__global__ void __launch_bounds__(256) hot_keys_kernel(uint32_t n, const uint32_t *__restrict__ outdeg,
+                                                       uint32_t *__restrict__ keys, uint32_t *__restrict__ ids,
+                                                       unsigned long long *nsrc) {
+    unsigned long long cnt = 0;
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t od = outdeg[v];
+        keys[v] = ~od;  // ascending ~od = descending out-degree
+        ids[v] = (uint32_t)v;
+        cnt += od != 0;
+    }
+    cnt = warp_sum(cnt);
+    if (lane_id() == 0 && cnt) atomicAdd(nsrc, cnt);
+}
+
+__global__ void __launch_bounds__(256) hot_slots_kernel(uint32_t n, const uint32_t *__restrict__ order,
+                                                        const uint32_t *__restrict__ outdeg,
+                                                        uint32_t *__restrict__ slot_of, uint32_t *__restrict__ od_hot) {
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t v = order[j];
+        slot_of[v] = (uint32_t)j;
+        od_hot[j] = outdeg[v];
+    }
+}
+
+__global__ void __launch_bounds__(256) hot_lanes_kernel(uint64_t lanes, const uint32_t *__restrict__ vsrc,
+                                                        const uint32_t *__restrict__ slot_of,
+                                                        uint32_t *__restrict__ vsrc_hot) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < lanes;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t u = vsrc[i];
+        vsrc_hot[i] = u == WG_NO_LANE ? WG_NO_LANE : slot_of[u];
+    }
+}
+
+// prep over slots: slot j < nsrc gets its contribution, the others (the
+// vertices without out-edges, in id order) add their rank to the dangling
+// mass.  acc is read through order[] (ascending ids within a degree class).
+__global__ void __launch_bounds__(PR_THREADS) pr_prep_hot(uint32_t n, uint32_t nsrc, int it, double damping,
+                                                          const uint32_t *__restrict__ order,
+                                                          const uint32_t *__restrict__ od_hot,
+                                                          const float *__restrict__ acc, float *__restrict__ contrib,
+                                                          const double *__restrict__ scal, double *__restrict__ dpart) {
+    __shared__ double sm[33];
+    double dang = 0.0;
+    const float base = it ? (float)((1.0 - damping) / n + damping * scal[0] / n) : 0.f;
+    const float df = (float)damping;
+    const float r0 = (float)(1.0 / n);
+    const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+    constexpr int U = 4;  // independent gathers in flight per thread
+    for (uint64_t j0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j0 < n; j0 += nth * U) {
+        float a[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t j = j0 + u * nth;
+            a[u] = (it && j < n) ? acc[order[j]] : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t j = j0 + u * nth;
+            if (j >= n) continue;
+            const float r = it ? base + df * a[u] : r0;
+            if (j < nsrc) contrib[j] = r / (float)od_hot[j];
+            else dang += r;
+        }
+    }
+    const double tot = block_sum(dang, sm);
+    if (threadIdx.x == 0) dpart[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(PR_THREADS) pr_rank_out(uint32_t n, double damping, const float *__restrict__ acc,
+                                                          const double *__restrict__ scal, float *__restrict__ rank,
+                                                          int it) {
+    const float base = it ? (float)((1.0 - damping) / n + damping * scal[0] / n) : 0.f;
+    const float df = (float)damping;
+    const float r0 = (float)(1.0 / n);
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x)
+        rank[v] = it ? base + df * acc[v] : r0;
+}
+
 using PrPull = void (*)(wg_graph, const float *, float *, uint32_t, PrBound *);
 
 PrPull pick(int w, bool shift = false) {
@@ -249,9 +387,10 @@ int pull_and_fixup(const wg_graph *g, const float *contrib, float *acc, uint32_t
 }
 
 int prep(uint32_t n, int it, double damping, const uint32_t *outdeg, float *acc, float *contrib, float *rank,
-         double *scal, const PrWs &w, cudaStream_t s) {
+         double *scal, const PrWs &w, cudaStream_t s, bool zero_acc) {
     const unsigned vgrid = prep_grid(n);
-    pr_prep<<<vgrid, PR_THREADS, 0, s>>>(n, it, damping, outdeg, acc, contrib, rank, scal, w.dpart);
+    if (zero_acc) pr_prep<true><<<vgrid, PR_THREADS, 0, s>>>(n, it, damping, outdeg, acc, contrib, rank, scal, w.dpart);
+    else pr_prep<false><<<vgrid, PR_THREADS, 0, s>>>(n, it, damping, outdeg, acc, contrib, rank, scal, w.dpart);
     pr_dangling<<<1, 32, 0, s>>>(w.dpart, vgrid, scal);
     ::wg::count_launch(2);
     WG_CHECK_LAUNCH("pagerank prep");
@@ -275,11 +414,90 @@ extern "C" int wg_pagerank(const wg_graph *g, int iterations, double damping, fl
     WG_CUDA(cudaMemsetAsync(d_acc, 0, (uint64_t)g->n * 4, s));
     WG_CUDA(cudaMemsetAsync(d_scal, 0, 4 * sizeof(double), s));
     for (int it = 0; it < iterations; ++it) {
-        if ((rc = prep(g->n, it, damping, g->outdeg, d_acc, d_contrib, nullptr, d_scal, w, s))) return rc;
+        if ((rc = prep(g->n, it, damping, g->outdeg, d_acc, d_contrib, nullptr, d_scal, w, s, false))) return rc;
         if ((rc = pull_and_fixup(g, d_contrib, d_acc, 0u, w, s))) return rc;
     }
     // final apply: prep of iteration `iterations` writes the ranks
-    return prep(g->n, iterations, damping, g->outdeg, d_acc, d_contrib, d_rank, d_scal, w, s);
+    return prep(g->n, iterations, damping, g->outdeg, d_acc, d_contrib, d_rank, d_scal, w, s, false);
+}
+
+
+// ---- hot-source layout ---------------------------------------------------
+static size_t hot_sort_temp(uint32_t n) {
+    size_t t = 0;
+    cub::DoubleBuffer<uint32_t> kb(nullptr, nullptr), vb(nullptr, nullptr);
+    cub::DeviceRadixSort::SortPairs(nullptr, t, kb, vb, (int64_t)n, 0, 32);
+    return t;
+}
+
+extern "C" size_t wg_pagerank_hot_ws_bytes(const wg_graph *g) {
+    if (!g) return 0;
+    const size_t n = g->n ? g->n : 1;
+    // keys x2, ids x2, slot_of, counter, sort temp
+    return 5 * carve_size(4 * n) + carve_size(8) + carve_size(hot_sort_temp((uint32_t)n)) + 1024;
+}
+
+extern "C" int wg_pagerank_hot_layout(const wg_graph *g, uint32_t *d_vsrc_hot, uint32_t *d_order,
+                                      uint32_t *d_od_hot, uint64_t *h_nsrc, void *d_ws, size_t ws_bytes_,
+                                      void *stream) {
+    WG_REQUIRE(g && d_vsrc_hot && d_order && d_od_hot && h_nsrc && d_ws, "null argument");
+    WG_REQUIRE(g->n > 0, "empty graph");
+    cudaStream_t s = as_stream(stream);
+    const uint32_t n = g->n;
+    Carve c{(char *)d_ws, 0, ws_bytes_};
+    uint32_t *k0 = c.take<uint32_t>(n), *k1 = c.take<uint32_t>(n);
+    uint32_t *v0 = c.take<uint32_t>(n), *v1 = c.take<uint32_t>(n);
+    uint32_t *slot_of = c.take<uint32_t>(n);
+    unsigned long long *cnt = c.take<unsigned long long>(1);
+    size_t tb = hot_sort_temp(n);
+    void *temp = c.take<char>(tb);
+    WG_REQUIRE(k0 && k1 && v0 && v1 && slot_of && cnt && temp, "workspace too small (wg_pagerank_hot_ws_bytes)");
+    WG_CUDA(cudaMemsetAsync(cnt, 0, 8, s));
+    hot_keys_kernel<<<grid_for(n, 1024, 8), 256, 0, s>>>(n, g->outdeg, k0, v0, cnt);
+    cub::DoubleBuffer<uint32_t> kb(k0, k1), vb(v0, v1);
+    WG_CUDA(cub::DeviceRadixSort::SortPairs(temp, tb, kb, vb, (int64_t)n, 0, 32, s));
+    WG_CUDA(cudaMemcpyAsync(d_order, vb.Current(), 4ull * n, cudaMemcpyDeviceToDevice, s));
+    hot_slots_kernel<<<grid_for(n, 1024, 8), 256, 0, s>>>(n, d_order, g->outdeg, slot_of, d_od_hot);
+    const uint64_t lanes = g->nvec * g->width;
+    if (lanes) hot_lanes_kernel<<<grid_for(lanes, 1024, 16), 256, 0, s>>>(lanes, g->vsrc, slot_of, d_vsrc_hot);
+    ::wg::count_launch(3);
+    WG_CHECK_LAUNCH("pagerank hot layout");
+    unsigned long long h = 0;
+    WG_CUDA(cudaMemcpyAsync(&h, cnt, 8, cudaMemcpyDeviceToHost, s));
+    WG_CUDA(cudaStreamSynchronize(s));
+    *h_nsrc = (uint64_t)h;
+    return WG_OK;
+}
+
+extern "C" int wg_pagerank_hot(const wg_graph *g, const uint32_t *d_vsrc_hot, const uint32_t *d_order,
+                               const uint32_t *d_od_hot, uint64_t nsrc, int iterations, double damping,
+                               float *d_rank, float *d_acc, float *d_contrib, double *d_scal, void *d_ws,
+                               size_t ws_bytes_, void *stream) {
+    WG_REQUIRE(g && d_vsrc_hot && d_order && d_od_hot && d_rank && d_acc && d_contrib && d_scal, "null argument");
+    WG_REQUIRE(iterations >= 0, "iterations must be >= 0");
+    WG_REQUIRE(g->n > 0 && nsrc <= g->n, "bad sizes");
+    PrWs w;
+    int rc = carve(g->n, d_ws, ws_bytes_, &w);
+    if (rc) return rc;
+    cudaStream_t s = as_stream(stream);
+    const uint32_t n = g->n;
+    WG_CUDA(cudaMemsetAsync(d_acc, 0, (uint64_t)n * 4, s));
+    WG_CUDA(cudaMemsetAsync(d_scal, 0, 4 * sizeof(double), s));
+    wg_graph gh = *g;
+    gh.vsrc = d_vsrc_hot;  // lanes hold contrib slots
+    const unsigned vgrid = prep_grid(n);
+    for (int it = 0; it < iterations; ++it) {
+        pr_prep_hot<<<vgrid, PR_THREADS, 0, s>>>(n, (uint32_t)nsrc, it, damping, d_order, d_od_hot, d_acc, d_contrib,
+                                                 d_scal, w.dpart);
+        pr_dangling<<<1, 32, 0, s>>>(w.dpart, vgrid, d_scal);
+        ::wg::count_launch(2);
+        WG_CHECK_LAUNCH("pagerank prep (hot)");
+        if ((rc = pull_and_fixup(&gh, d_contrib, d_acc, 0u, w, s))) return rc;
+    }
+    pr_rank_out<<<vgrid, PR_THREADS, 0, s>>>(n, damping, d_acc, d_scal, d_rank, iterations);
+    ::wg::count_launch();
+    WG_CHECK_LAUNCH("pagerank ranks");
+    return WG_OK;
 }
 
 extern "C" size_t wg_pagerank_prep_ws_bytes(uint32_t n) { return ws_bytes(n); }
@@ -294,7 +512,7 @@ extern "C" int wg_pagerank_prep(uint32_t n, int it, double damping, const uint32
     if (rc) return rc;
     cudaStream_t s = as_stream(stream);
     if (it == 0) WG_CUDA(cudaMemsetAsync(d_scal, 0, 4 * sizeof(double), s));
-    return prep(n, it, damping, d_outdeg, d_acc, d_contrib, d_rank, d_scal, w, s);
+    return prep(n, it, damping, d_outdeg, d_acc, d_contrib, d_rank, d_scal, w, s, true);
 }
 
 extern "C" int wg_pagerank_pull(const wg_graph *g, const float *d_contrib, float *d_acc,

@@ -1249,7 +1249,32 @@ def fits_u32(values: np.ndarray, kern, g: DeviceGraph) -> bool:
 # ---------------------------------------------------------------------------
 # PageRank (K8)
 # ---------------------------------------------------------------------------
-def pagerank(g: DeviceGraph, iterations: int = 20, damping: float = 0.85, stream=None, bufs=None):
+class PageRankLayout:
+    """Hot-source layout of one graph for PageRank (wg_pagerank_hot_layout):
+    contribution slots in descending out-degree order, a copy of the lanes
+    holding slots, the slot -> vertex map and the slots' out-degrees."""
+
+    def __init__(self, g: DeviceGraph, stream=None):
+        torch = _torch()
+        L = _lib.load()
+        n = max(g.n, 1)
+        lanes = g.nvec * g.width
+        self.vsrc_hot = torch.empty(lanes + 16 * g.width, dtype=torch.int32, device="cuda")  # slack like vsrc
+        self.vsrc_hot[lanes:].fill_(-1)
+        self.order = torch.empty(n, dtype=torch.int32, device="cuda")
+        self.od_hot = torch.empty(n, dtype=torch.int32, device="cuda")
+        ws = torch.empty(int(L.wg_pagerank_hot_ws_bytes(ctypes.byref(g.struct()))), dtype=torch.uint8, device="cuda")
+        nsrc = ctypes.c_uint64(0)
+        check(L.wg_pagerank_hot_layout(ctypes.byref(g.struct()), _ptr(self.vsrc_hot), _ptr(self.order),
+                                       _ptr(self.od_hot), ctypes.byref(nsrc), _ptr(ws), ws.numel(),
+                                       _lib.stream_ptr(stream)))
+        self.nsrc = int(nsrc.value)
+
+
+def pagerank(g: DeviceGraph, iterations: int = 20, damping: float = 0.85, stream=None, bufs=None,
+             hot: Optional[bool] = None):
+    """hot (default on; WG_PR_HOT=0 turns it off): gather contributions through
+    the hot-source layout, built on first use and kept with the graph."""
     torch = _torch()
     n = max(g.n, 1)
     if bufs is None:
@@ -1263,6 +1288,16 @@ def pagerank(g: DeviceGraph, iterations: int = 20, damping: float = 0.85, stream
     ws = getattr(g, "_pr_ws", None)
     if ws is None or ws.numel() < need:
         ws = g._pr_ws = torch.empty(need, dtype=torch.uint8, device="cuda")
+    if hot is None:
+        hot = os.environ.get("WG_PR_HOT", "1") != "0"
+    if hot and g.nvec:
+        lay = getattr(g, "_pr_hot", None)
+        if lay is None:
+            lay = g._pr_hot = PageRankLayout(g, stream)
+        check(L.wg_pagerank_hot(ctypes.byref(g.struct()), _ptr(lay.vsrc_hot), _ptr(lay.order), _ptr(lay.od_hot),
+                                lay.nsrc, int(iterations), float(damping), _ptr(rank), _ptr(acc), _ptr(contrib),
+                                _ptr(scal), _ptr(ws), ws.numel(), _lib.stream_ptr(stream)))
+        return rank
     check(L.wg_pagerank(ctypes.byref(g.struct()), int(iterations), float(damping), _ptr(rank), _ptr(acc),
                         _ptr(contrib), _ptr(scal), _ptr(ws), ws.numel(), _lib.stream_ptr(stream)))
     return rank

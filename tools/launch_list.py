@@ -9,7 +9,7 @@ h = rows[0]
 ki, vi, ii = h.index("Kernel Name"), h.index("Metric Value"), h.index("ID")
 seq = []
 for r in rows[1:]:
-    name = r[ki].split("(")[0].replace("void ", "").split("<")[0]
+    name = r[ki].replace("<unnamed>::", "").split("(")[0].replace("void ", "").split("<")[0]
     seq.append((int(r[ii]), name, float(r[vi].replace(",", "")) / 1e3))
 if "--seq" in sys.argv:
     for i, n, us in seq:
