@@ -186,6 +186,29 @@ class ClockSampler:
 
 
 # -------------------------------------------------------------- workload --
+def gather_peak():
+    """Measured ceiling of one-gather-per-edge kernels (tools/microbench_sector.cu,
+    profiles/gather_peak.json): random 4-byte gathers per second when every
+    gather needs its own 32-byte sector from L2 -- an SM's L1 sends about one
+    sector request per cycle to the crossbar, whatever the table size."""
+    try:
+        return float(json.loads((ROOT / "profiles" / "gather_peak.json").read_text())["l2_resident_gathers_per_s"])
+    except Exception:
+        return 148 * 1.965e9
+
+
+def gather_roofline(gathers, ms):
+    """Second roofline of a pull: its random gathers against gather_peak()."""
+    pk = gather_peak()
+    rate = gathers / (ms * 1e-3) if ms else 0.0
+    return {"bound": "L1->crossbar sector requests (one 4-byte gather per 32-byte sector)",
+            "gathers_per_launch": int(gathers), "achieved_ggathers_s": round(rate / 1e9, 1),
+            "peak_ggathers_s": round(pk / 1e9, 1), "frac": round(rate / pk, 4),
+            "peak_source": "measured, tools/microbench_sector.cu (profiles/r02_microbench_sector.txt)",
+            "hbm_equivalent": "at 4 useful bytes per 32-byte sector this ceiling is %.2f of the HBM copy peak"
+                              % (4 * pk / 1e9 / peaks()[0])}
+
+
 def make_graph(wl, width=4):
     import paper_1903_07754_b200 as wg
     if "grid" in wl:
@@ -580,6 +603,13 @@ def roofline(rows, recs, n, E, weighted, filt, wl):
             measured_traffic = ent.get("dram_bytes_per_launch") if isinstance(ent, dict) else ent
         except Exception:
             pass
+    if dom == "dense_dst":
+        dom_gathers = sum(r.gathers for r in recs if r.mode == "FullScan" and (r.lanes_read or r.gathers))
+    elif dom == "dense_tma":
+        dom_gathers = sum((E if not filt else min(E, 4 * r.vectors_touched)) for r in recs
+                          if r.mode == "FullScan" and not (r.lanes_read or r.gathers))
+    else:
+        dom_gathers = sum(r.active_edges for r in recs if r.mode != "FullScan")
     other = {k: {"alg_MB": round(v[0] / 1e6, 2), "ms": round(v[1], 4), "launches": v[2],
                  "achieved_gbs": round(v[0] / (v[1] * 1e-3) / 1e9, 1) if v[1] else None}
              for k, v in kern.items() if v[2]}
@@ -588,6 +618,7 @@ def roofline(rows, recs, n, E, weighted, filt, wl):
             "peak_source": peak_src, "launches": launches,
             "algorithmic_bytes_per_launch": round(bts / max(1, launches), 1),
             "kernel_ms_per_launch": round(ms / max(1, launches), 4),
+            "gather_roofline": gather_roofline(dom_gathers / max(1, launches), ms / max(1, launches)),
             "by_kernel": other, "kernel_sum_ms": round(step_t, 4),
             "per_iteration": per_iter if len(per_iter) <= 16 else per_iter[:8] + per_iter[-2:],
             "iterations_timed": len(per_iter)}
@@ -847,7 +878,9 @@ def run_pagerank(args, wl, el, topo, build_s):
            "gpu_launches": int(_lib.launch_count() - launches0),
            "roofline": {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
                         "frac": round(ach / peak, 4), "traffic": None, "peak_source": src,
-                        "kernel": "pr_prep + pr_pull (20 iterations)"},
+                        "kernel": "pr_prep_hot + pr_pull + pr_fixup (20 iterations)",
+                        "algorithmic_bytes_per_launch": 4 * E + 20 * n,
+                        "gather_roofline": gather_roofline(E, ms / 20)},
            "clocks": clk.summary()}
     if not args.no_e2e:
         out["e2e"] = e2e_pagerank(args, g, bufs)

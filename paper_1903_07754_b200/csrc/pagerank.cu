@@ -123,14 +123,32 @@ __global__ void __launch_bounds__(PR_THREADS) pr_pull(wg_graph g, const float *_
         uint32_t cd = PR_NONE;  // carried segment (warp-uniform): destination,
         float cs = 0.f;         // partial sum, and whether it is the range's
         bool cfirst = false;    // first segment
+        // the next tile's lanes and destination are loaded while this tile
+        // gathers: one memory latency per tile on the warp's critical path
+        // instead of two (stream, then the dependent gathers)
+        uint32_t src_n[W], d_n = PR_NONE;
+#pragma unroll
+        for (int l = 0; l < W; ++l) src_n[l] = WG_NO_LANE;
+        const auto fetch = [&](uint64_t tile) {
+            const uint64_t q = (tile << 5) + lane;
+            if (q < nvec) {
+                d_n = ld_stream(g.vdst + q);
+                load_lanes<W>(g.vsrc, q, src_n);
+            } else {
+                d_n = PR_NONE;
+            }
+        };
+        fetch(t0);
         for (uint64_t tile = t0; tile < t1; ++tile) {
             const uint64_t p = (tile << 5) + lane;
             const bool valid = p < nvec;
-            const uint32_t d = valid ? g.vdst[p] : PR_NONE;
+            const uint32_t d = d_n;
+            uint32_t src[W];
+#pragma unroll
+            for (int l = 0; l < W; ++l) src[l] = src_n[l];
+            if (tile + 1 < t1) fetch(tile + 1);
             float sum = 0.f;
             if (valid) {
-                uint32_t src[W];
-                load_lanes<W>(g.vsrc, p, src);
 #pragma unroll
                 for (int l = 0; l < W; ++l)
                     if (src[l] != WG_NO_LANE) sum += contrib[src[l]];
@@ -153,8 +171,16 @@ __global__ void __launch_bounds__(PR_THREADS) pr_pull(wg_graph g, const float *_
                     prevd = tile == t0 ? dleft : cd;
                     from_start = tile == t0 && p_lo == 0;
                 }
-                if (valid && (from_start || d != prevd))
-                    for (uint32_t x = from_start ? base : prevd + 1; x < d; ++x) acc[x - base] = 0.f;
+                const uint32_t glo = from_start ? base : prevd + 1;
+                const uint32_t len = (valid && (from_start || d != prevd) && glo < d) ? d - glo : 0u;
+                // short gaps by their lane, long ones (the sparse high ids) by the warp
+                if (len && len <= 4)
+                    for (uint32_t x = glo; x < d; ++x) acc[x - base] = 0.f;
+                for (unsigned lm = __ballot_sync(FULL, len > 4); lm; lm &= lm - 1) {
+                    const int j = __ffs(lm) - 1;
+                    const uint32_t lo = __shfl_sync(FULL, glo, j), hi = __shfl_sync(FULL, d, j);
+                    for (uint32_t x = lo + lane; x < hi; x += 32) acc[x - base] = 0.f;
+                }
             }
             const bool tail = lane == 31 || dn != d;
             const unsigned heads = __ballot_sync(FULL, head);
