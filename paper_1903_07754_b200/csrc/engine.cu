@@ -594,6 +594,19 @@ __global__ void loop_step_kernel(cudaGraphConditionalHandle h, uint64_t *ctrl, c
 }
 __global__ void set_limit_kernel(uint64_t *ctrl, uint64_t limit) { ctrl[1] = limit; }
 
+// After the top-level attempt of the persistent loop: enter the WHILE body
+// unless the run is already over (the last iteration it ran produced a
+// frontier without out-edges, or the launch limit was reached).  Nothing ran
+// yet (ctrl[0] == 0): the body takes iteration 1.
+__global__ void loop_enter_kernel(cudaGraphConditionalHandle h, const uint64_t *ctrl, const wg_iter_rec *recs,
+                                  uint32_t ring) {
+    const uint64_t done = ctrl[0];
+    WG_KTS(done + 1, KTS_STEP);
+    bool stop = false;
+    if (done > 0) stop = recs[done % ring].out_edge_sum == 0 || done >= ctrl[1];
+    cudaGraphSetConditional(h, stop ? 0u : 1u);
+}
+
 // Gate of the persistent sparse loop (its cooperative launch costs several
 // microseconds even when it returns at once, so it sits behind an IF node).
 // It also takes destination-major dense iterations (dense_ok: unweighted
@@ -1052,6 +1065,53 @@ static void *create_loop_graph(const wg_graph *g, const wg_run_bufs *b, const wg
     }
     cudaGraphConditionalHandle hw;
     e = cudaGraphConditionalHandleCreate(&hw, graph, 1, cudaGraphCondAssignDefault);
+    // Before the WHILE node: one attempt of the persistent loop on the top
+    // level, then a kernel that decides whether the WHILE body runs at all.
+    // Runs the persistent kernel finishes on its own (CC s22, BFS s16, the
+    // grid: every iteration is one of its phases) end right there instead of
+    // walking the body's gate / IF nodes / finalize / step once more.
+    if (e == cudaSuccess && g_sparse_loop && g->entries && g->nvec) {
+        wg_run_params q0 = *p;
+        q0.timer = nullptr;
+        LoopCtx c0 = loop_ctx(g, b, &q0, b->ctrl, 1);
+        PullBufs pb0 = pull_bufs(g, b, &q0);
+        const uint64_t groups0 = groups_of(g, q0.shift);
+        cudaGraphConditionalHandle hl0;
+        e = cudaGraphConditionalHandleCreate(&hl0, graph, 0, cudaGraphCondAssignDefault);
+        if (e == cudaSuccess)
+            e = cudaStreamBeginCaptureToGraph(s, graph, pro.empty() ? nullptr : pro.data(), nullptr, pro.size(),
+                                              cudaStreamCaptureModeThreadLocal);
+        int rc0 = WG_OK;
+        if (e == cudaSuccess) {
+            sparse_gate_kernel<<<1, 1, 0, s>>>(c0, hl0, groups0, pb0.loop_dense && !q0.kern.use_weight ? 1u : 0u,
+                                               g->n, q0.kern.filter_unvisited ? 1 : 0);
+            ::wg::count_launch();
+            cudaGraph_t inner0;
+            if ((e = capture_if_node(s, hl0, &inner0)) == cudaSuccess &&
+                (e = cudaStreamBeginCaptureToGraph(s2, inner0, nullptr, nullptr, 0,
+                                                   cudaStreamCaptureModeThreadLocal)) == cudaSuccess) {
+                rc0 = launch_sparse_loop(c0, g, pb0, q0.val_type, q0.shift, &q0.kern, b->gbits, groups0, s2);
+                e = cudaStreamEndCapture(s2, &inner0);
+            }
+            if (e == cudaSuccess && rc0 == WG_OK) {
+                loop_enter_kernel<<<1, 1, 0, s>>>(hw, b->ctrl, b->recs, b->ring);
+                ::wg::count_launch();
+            }
+            cudaStreamCaptureStatus st;
+            const cudaGraphNode_t *deps = nullptr;
+            size_t nd = 0;
+            cudaError_t e1 = cudaStreamGetCaptureInfo(s, &st, nullptr, nullptr, &deps, &nd);
+            if (e1 == cudaSuccess) pro.assign(deps, deps + nd);
+            cudaGraph_t gout = nullptr;
+            cudaError_t e2 = cudaStreamEndCapture(s, &gout);
+            if (e == cudaSuccess) e = e1 != cudaSuccess ? e1 : e2;
+        }
+        if (rc0 != WG_OK || e != cudaSuccess) {
+            cudaGraphDestroy(graph);
+            if (rc0 == WG_OK) cuda_fail(e, "pre-loop capture");
+            return nullptr;
+        }
+    }
     cudaGraphNodeParams cp = {};
     cp.type = cudaGraphNodeTypeConditional;
     cp.conditional.handle = hw;

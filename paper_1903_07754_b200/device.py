@@ -767,6 +767,9 @@ def covered_groups(words_u64: np.ndarray, group_count: int) -> np.ndarray:
 MODE_NAMES = {1: "FullScan", 2: "Wedge"}
 
 
+HEAD_RECORDS = 64  # records read back with the control words (drive_graph)
+
+
 @dataclass
 class IterRecord:
     iteration: int
@@ -866,10 +869,13 @@ class DeviceLoop:
         self.bcount = torch.empty(max(nbc, 1), dtype=torch.int64, device=dev)
         g.ensure_voff()
         self.work = torch.zeros(n + 64, dtype=torch.int32, device=dev)  # >= 8 words per 8192-vertex chunk
-        self.recs = torch.zeros(self.ring * REC_U64, dtype=torch.int64, device=dev)
-        self.ctrl = torch.zeros(4, dtype=torch.int64, device=dev)
-        self.host_recs = torch.zeros(self.ring * REC_U64, dtype=torch.int64).pin_memory()
-        self.ctrl_host = torch.zeros(4, dtype=torch.int64).pin_memory()
+        # control words and the record ring in one allocation (ctrl first): a
+        # short run's state comes back in ONE small D2H copy (drive_graph)
+        self.state = torch.zeros(4 + self.ring * REC_U64, dtype=torch.int64, device=dev)
+        self.ctrl, self.recs = self.state[:4], self.state[4:]
+        self.host_state = torch.zeros(4 + self.ring * REC_U64, dtype=torch.int64).pin_memory()
+        self.ctrl_host, self.host_recs = self.host_state[:4], self.host_state[4:]
+        self._host_np = self.host_state.numpy().view(np.uint64)
         b = WgRunBufs()
         for i in range(2):
             b.vals[i] = _ptr(self.vals[i])
@@ -1016,19 +1022,20 @@ class DeviceLoop:
             pass
 
     def _parse(self, rows, it0, records, trace):
-        """Append records of iterations it0.. until one did not run or converged."""
+        """Append records of iterations it0.. until one did not run or converged.
+        rows: per-iteration records as lists of Python ints (ndarray.tolist())."""
         for j, r in enumerate(rows):
-            mode = int(r[0])
+            mode = r[0]
             if mode == 0:
                 return True, None
-            if int(r[10]):
+            if r[10]:
                 raise _lib.OverflowError32(_lib.WG_EOVERFLOW, "uint32 value overflow in device loop")
-            records.append(IterRecord(it0 + j, MODE_NAMES[mode], int(r[1]), int(r[2]), int(r[3]),
-                                      int(r[7]) if mode == 2 else 0, int(r[8]) if mode == 2 else 0,
-                                      int(r[16]), int(r[17])))
+            wedge = mode == 2
+            records.append(IterRecord(it0 + j, MODE_NAMES[mode], r[1], r[2], r[3], r[7] if wedge else 0,
+                                      r[8] if wedge else 0, r[16], r[17]))
             if trace is not None:
                 trace(self, it0 + j)
-            if int(r[4]) == 0:
+            if r[4] == 0:
                 return True, it0 + j
         return False, None
 
@@ -1057,14 +1064,25 @@ class DeviceLoop:
                                                   min(init_words.numel(), sw.numel()) * 4, sp))
             else:
                 check(L.wg_run_loop_launch(exe, ctypes.byref(self.bufs), limit, sp))
-            # the control word and the whole record ring in one round trip (a
-            # launch runs at most ring - 2 iterations, so its records are all there)
-            ctrl_host.copy_(self.ctrl, non_blocking=True)
-            self.host_recs.copy_(self.recs, non_blocking=True)
+            # the control words and the head of the record ring in one small copy;
+            # the whole ring only when the launch ran past the head (a launch runs
+            # at most ring - 2 iterations, so its records are all in the ring)
+            head = 4 + HEAD_RECORDS * REC_U64
+            self.host_state[:head].copy_(self.state[:head], non_blocking=True)
             s.synchronize()
-            done = min(int(ctrl_host[0]), limit)
-            arr = self.host_recs.numpy().view(np.uint64).reshape(self.ring, REC_U64)
-            rows = [arr[(it + j) % self.ring] for j in range(done - it + 1)] if done >= it else []
+            hs = self._host_np
+            done = min(int(hs[0]), limit)
+            lo = it % self.ring
+            if done >= it and (lo + (done - it) >= HEAD_RECORDS):
+                self.host_state.copy_(self.state, non_blocking=True)
+                s.synchronize()
+            arr = hs[4:].reshape(self.ring, REC_U64)
+            if done < it:
+                rows = []
+            elif lo + (done - it) < self.ring:
+                rows = arr[lo: lo + done - it + 1].tolist()
+            else:
+                rows = [arr[(it + j) % self.ring].tolist() for j in range(done - it + 1)]
             conv, at = self._parse(rows, it, records, None)
             if records:
                 last = records[-1].iteration

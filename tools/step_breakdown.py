@@ -87,13 +87,13 @@ for k in range(steps):
                                            g.n * init_values.element_size(), dv._ptr(init_words), dv._ptr(sw),
                                            min(init_words.numel(), sw.numel()) * 4, _lib.stream_ptr(None)))
     c = time.perf_counter()
-    loop.ctrl_host.copy_(loop.ctrl, non_blocking=True)
-    loop.host_recs.copy_(loop.recs, non_blocking=True)
+    head = 4 + dv.HEAD_RECORDS * dv.REC_U64
+    loop.host_state[:head].copy_(loop.state[:head], non_blocking=True)
     stream.synchronize()
     d = time.perf_counter()
-    arr = loop.host_recs.numpy().view(np.uint64).reshape(loop.ring, dv.REC_U64)
-    done = int(loop.ctrl_host[0])
-    rows = [arr[(1 + j) % loop.ring] for j in range(done)]
+    hs = loop._host_np
+    done = int(hs[0])
+    rows = hs[4:].reshape(loop.ring, dv.REC_U64)[1: 1 + done].tolist()
     recs = []
     loop._parse(rows, 1, recs, None)
     e = time.perf_counter()
