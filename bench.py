@@ -155,7 +155,10 @@ class ClockSampler:
                     self._sample_smi()
             except Exception:
                 pass
-            self._stop.wait(0.001 if self._nvml else 0.2)
+            # 20 ms: every NVML query takes driver locks that the timed steps' graph
+            # launches also need (a 1 ms poll added ~0.1 ms to a 0.25 ms BFS s16
+            # step); tick() samples between steps as well
+            self._stop.wait(0.02 if self._nvml else 0.2)
 
     def tick(self):
         """Synchronous sample (between timed steps: the timed region of a

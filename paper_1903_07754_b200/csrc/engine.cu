@@ -1076,23 +1076,14 @@ static void *create_loop_graph(const wg_graph *g, const wg_run_bufs *b, const wg
         LoopCtx c0 = loop_ctx(g, b, &q0, b->ctrl, 1);
         PullBufs pb0 = pull_bufs(g, b, &q0);
         const uint64_t groups0 = groups_of(g, q0.shift);
-        cudaGraphConditionalHandle hl0;
-        e = cudaGraphConditionalHandleCreate(&hl0, graph, 0, cudaGraphCondAssignDefault);
-        if (e == cudaSuccess)
-            e = cudaStreamBeginCaptureToGraph(s, graph, pro.empty() ? nullptr : pro.data(), nullptr, pro.size(),
-                                              cudaStreamCaptureModeThreadLocal);
+        e = cudaStreamBeginCaptureToGraph(s, graph, pro.empty() ? nullptr : pro.data(), nullptr, pro.size(),
+                                          cudaStreamCaptureModeThreadLocal);
         int rc0 = WG_OK;
         if (e == cudaSuccess) {
-            sparse_gate_kernel<<<1, 1, 0, s>>>(c0, hl0, groups0, pb0.loop_dense && !q0.kern.use_weight ? 1u : 0u,
-                                               g->n, q0.kern.filter_unvisited ? 1 : 0);
-            ::wg::count_launch();
-            cudaGraph_t inner0;
-            if ((e = capture_if_node(s, hl0, &inner0)) == cudaSuccess &&
-                (e = cudaStreamBeginCaptureToGraph(s2, inner0, nullptr, nullptr, 0,
-                                                   cudaStreamCaptureModeThreadLocal)) == cudaSuccess) {
-                rc0 = launch_sparse_loop(c0, g, pb0, q0.val_type, q0.shift, &q0.kern, b->gbits, groups0, s2);
-                e = cudaStreamEndCapture(s2, &inner0);
-            }
+            // no gate / IF node here: the kernel itself returns at once when the
+            // iteration about to run is not one of its kinds (its launch costs a
+            // few microseconds, which only matter to the runs it does take)
+            rc0 = launch_sparse_loop(c0, g, pb0, q0.val_type, q0.shift, &q0.kern, b->gbits, groups0, s);
             if (e == cudaSuccess && rc0 == WG_OK) {
                 loop_enter_kernel<<<1, 1, 0, s>>>(hw, b->ctrl, b->recs, b->ring);
                 ::wg::count_launch();
