@@ -103,6 +103,21 @@ __device__ __forceinline__ T warp_sum(T v) {
     return v;
 }
 
+// Warp sum of per-lane uint64 counts with three REDUX instructions instead
+// of a 64-bit shuffle tree (exact for any values: 16-bit pieces of the low
+// word cannot overflow a 32-bit warp sum, the high words are summed apart).
+__device__ __forceinline__ uint64_t warp_sum_u64_redux(uint64_t v) {
+    const uint32_t lo = (uint32_t)v, hi = (uint32_t)(v >> 32);
+    const uint64_t a = __reduce_add_sync(FULL, lo & 0xffffu);
+    const uint64_t b = __reduce_add_sync(FULL, lo >> 16);
+    uint64_t c = 0;
+    if (__any_sync(FULL, hi != 0)) {
+        const uint64_t h0 = __reduce_add_sync(FULL, hi & 0xffffu), h1 = __reduce_add_sync(FULL, hi >> 16);
+        c = (h0 + (h1 << 16)) << 32;
+    }
+    return a + (b << 16) + c;
+}
+
 // Streaming (read-once) loads: bypass L1.  (An L2 evict-first cache hint
 // here measured neutral to slightly negative; the TMA stream of the dense
 // pull uses one, tma.cuh.)

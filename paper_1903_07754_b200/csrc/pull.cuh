@@ -856,11 +856,19 @@ __device__ __forceinline__ void dense_dst_phase(const LoopCtx &c, uint64_t it, c
             for (int k = 0; k < DST_K; ++k) touched += need[k] ? v1[k] - v0[k] : 0u;
         }
         // (c) undecided destinations: short in-lists by their thread ...
-        bool heavy[DST_K];
+        bool heavy[DST_K], und[DST_K], any_und = false;
 #pragma unroll
         for (int k = 0; k < DST_K; ++k) {
-            const bool undecided = need[k] && (KIND == DSTK_FLOOR ? (!exact_first && agg[k] != (T)0) : true);
-            heavy[k] = undecided && v1[k] - v0[k] > DST_LIGHT;
+            und[k] = need[k] && (KIND == DSTK_FLOOR ? (!exact_first && agg[k] != (T)0) : true);
+            heavy[k] = und[k] && v1[k] - v0[k] > DST_LIGHT;
+            any_und |= und[k];
+        }
+        // (warp-uniform skip: identity first iterations and late iterations
+        // decide every destination of most steps from the probe alone)
+        if (__any_sync(FULL, any_und)) {
+#pragma unroll
+        for (int k = 0; k < DST_K; ++k) {
+            const bool undecided = und[k];
             if (!undecided || heavy[k]) continue;
             // two vectors per round trip (the second may be the next one's
             // padding-free first: v+1 < v1 is checked)
@@ -930,8 +938,10 @@ __device__ __forceinline__ void dense_dst_phase(const LoopCtx &c, uint64_t it, c
                 if (lane == (unsigned)j) agg[k] = hagg;
             }
         }
+        }  // any undecided
         // (d) apply: every destination's nxt[d]; bits one word per k; counts
-        uint64_t nz = 0, ent = 0, z = 0, es = 0;
+        uint64_t ent = 0, es = 0;
+        uint32_t nz = 0, z = 0;
         bool any = false;
 #pragma unroll
         for (int k = 0; k < DST_K; ++k) {
@@ -972,15 +982,15 @@ __device__ __forceinline__ void dense_dst_phase(const LoopCtx &c, uint64_t it, c
             }
         }
         if (any) {  // warp-uniform: the produced frontier's counts of this 8192-vertex chunk
-            nz = warp_sum(nz);
-            ent = warp_sum(ent);
-            z = warp_sum(z);
-            es = warp_sum(es);
+            // (REDUX sums; members with / without entries share one: each <= 32 * DST_K)
+            const uint32_t nzz = __reduce_add_sync(FULL, nz | (z << 16));
+            es = warp_sum_u64_redux(es);
+            ent = lens_deg ? es : warp_sum_u64_redux(ent);  // index lengths = out-degrees
             if (lane == 0) {
                 unsigned long long *t = totals + 4 * ((wb >> 5) / FB_WORDS);
-                if (nz) atomicAdd(&t[0], (unsigned long long)nz);
+                if (nzz & 0xffffu) atomicAdd(&t[0], (unsigned long long)(nzz & 0xffffu));
                 if (ent) atomicAdd(&t[1], (unsigned long long)ent);
-                if (z) atomicAdd(&t[2], (unsigned long long)z);
+                if (nzz >> 16) atomicAdd(&t[2], (unsigned long long)(nzz >> 16));
                 if (es) atomicAdd(&t[3], (unsigned long long)es);
             }
         }
