@@ -844,6 +844,15 @@ def cpu_baseline(wl, args):
     return cb
 
 
+def pr_traffic(wl):
+    """Measured DRAM bytes per pr_pull launch (one `ncu --set full` capture, profiles/traffic.json)."""
+    try:
+        ent = json.loads((ROOT / "profiles" / "traffic.json").read_text()).get(f"{wl['desc']}|pr_pull")
+        return ent.get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
 def run_pagerank(args, wl, el, topo, build_s):
     import torch
     import paper_1903_07754_b200 as wg
@@ -880,7 +889,7 @@ def run_pagerank(args, wl, el, topo, build_s):
            "config": {"workload": wl["desc"], "V": n, "E": E, "build_s": round(build_s, 2)},
            "gpu_launches": int(_lib.launch_count() - launches0),
            "roofline": {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
-                        "frac": round(ach / peak, 4), "traffic": None, "peak_source": src,
+                        "frac": round(ach / peak, 4), "traffic": pr_traffic(wl), "peak_source": src,
                         "kernel": "pr_prep_hot + pr_pull + pr_fixup (20 iterations)",
                         "algorithmic_bytes_per_launch": 4 * E + 20 * n,
                         "gather_roofline": gather_roofline(E, ms / 20)},

@@ -400,6 +400,67 @@ def test_grid_generator_matches_oracle(wg):
     assert np.array_equal(el.weight[a], w[b])
 
 
+def test_pagerank_hot_layout_is_a_stable_degree_order(wg):
+    """wg_pagerank_hot_layout: slots = vertices by descending out-degree
+    (stable), one slot per vertex with out-edges first; the hot lanes map
+    back to the original sources lane for lane; the hot and the plain
+    PageRank agree (same lane order -> same sums; only the dangling-mass
+    summation order differs) and the hot run is bit-reproducible."""
+    from paper_1903_07754_b200 import device as dv
+    el = wg.drop_self_loops_dedup(wg.generate(wg.GenSpec("rmat", scale=14, edge_factor=16, seed=3)),
+                                  symmetric=False)
+    topo = wg.build_pull_topology(el, 4)
+    g = topo.device
+    n, lanes = g.n, g.nvec * g.width
+    lay = dv.PageRankLayout(g)
+    order = lay.order.cpu().numpy().view(np.uint32).astype(np.int64)
+    od = g.outdeg_np().astype(np.int64)
+    assert np.array_equal(np.sort(order), np.arange(n))
+    assert lay.nsrc == int((od > 0).sum())
+    od_sorted = od[order]
+    assert np.all(np.diff(od_sorted) <= 0)
+    assert np.all(np.diff(order)[np.diff(od_sorted) == 0] > 0)  # stable: ids ascend within a degree
+    assert np.array_equal(lay.od_hot.cpu().numpy().view(np.uint32).astype(np.int64), od_sorted)
+    vs = g.vsrc[:lanes].cpu().numpy().view(np.uint32).astype(np.int64)
+    vh = lay.vsrc_hot[:lanes].cpu().numpy().view(np.uint32).astype(np.int64)
+    real = vs != 0xFFFFFFFF
+    assert np.array_equal(vh[~real], vs[~real])
+    assert vh[real].max() < lay.nsrc and np.array_equal(order[vh[real]], vs[real])
+    a = dv.pagerank(g, 20, 0.85, hot=True).clone()
+    b = dv.pagerank(g, 20, 0.85, hot=True).clone()
+    c = dv.pagerank(g, 20, 0.85, hot=False).clone()
+    assert a.cpu().numpy().tobytes() == b.cpu().numpy().tobytes()
+    assert float((a.double() - c.double()).abs().max()) <= 1e-9
+    ref = oracle.pagerank_numpy(el.vertex_count, el.src, el.dst, 20, 0.85)
+    assert np.max(np.abs(a.cpu().numpy().astype(np.float64) - ref)) <= 1e-6
+
+
+def test_pagerank_pull_writes_every_vertex_of_its_range(wg):
+    """Gap fill (pagerank.cu): prep no longer clears acc between iterations --
+    the pull writes the sum of every vertex up to its last destination,
+    in-degree 0 included (zeros between sparse destinations, long runs without
+    in-edges), and never a zero over a real sum."""
+    import torch
+    from paper_1903_07754_b200 import device as dv
+    rng = np.random.default_rng(11)
+    n = 3000
+    # destinations only on multiples of 7 and a long run without in-edges
+    dst = rng.choice(np.arange(0, 2000, 7), 12000)
+    src = rng.integers(0, n, 12000)
+    keep = src != dst
+    el = wg.drop_self_loops_dedup(wg.EdgeList(n, src[keep], dst[keep]), symmetric=False)
+    topo = wg.build_pull_topology(el, 4)
+    g = topo.device
+    ref = oracle.pagerank_numpy(el.vertex_count, el.src, el.dst, 20, 0.85)
+    for hot in (True, False):
+        bufs = (torch.empty(n, dtype=torch.float32, device="cuda"),
+                torch.full((n,), 123.0, dtype=torch.float32, device="cuda"),  # poisoned acc
+                torch.full((n,), 7.0, dtype=torch.float32, device="cuda"),
+                torch.zeros(4, dtype=torch.float64, device="cuda"))
+        r = dv.pagerank(g, 20, 0.85, bufs=bufs, hot=hot).cpu().numpy()
+        assert np.max(np.abs(r.astype(np.float64) - ref)) <= 1e-6, hot
+
+
 def test_pagerank_within_tolerance(wg):
     """|r_gpu - r_cpu| <= 1e-6 per vertex (north_star), float64 oracle."""
     for scale, ef, seed in ((10, 8, 1), (14, 16, 2)):
