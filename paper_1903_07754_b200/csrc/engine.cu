@@ -266,6 +266,9 @@ int launch_sparse_loop(const LoopCtx &c, const wg_graph *g, const PullBufs &pb, 
         return e ? atoi(e) : 4;
     }();
     if (cap > 0 && per_sm > cap) per_sm = cap;
+    // small graphs (C1: 475K vectors) never fill more than one block per SM and
+    // pay for every extra block in each grid barrier: BFS s16 96 vs 113 us
+    if (!getenv("WG_PERSIST_BLOCKS") && g->nvec <= (1ull << 20)) per_sm = 1;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(sm_count() * per_sm));
     cfg.blockDim = dim3(PULL_THREADS);
