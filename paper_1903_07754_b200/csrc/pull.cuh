@@ -866,46 +866,89 @@ __device__ __forceinline__ void dense_dst_phase(const LoopCtx &c, uint64_t it, c
         // (warp-uniform skip: identity first iterations and late iterations
         // decide every destination of most steps from the probe alone)
         if (__any_sync(FULL, any_und)) {
+        // The step's light items (destination, k) are spread over the warp's
+        // lanes first: a thread that owns several undecided destinations would
+        // walk them one after the other (each walk is a chain of dependent
+        // round trips) while most lanes idle -- typically ~10 of a step's 128
+        // destinations are undecided, so one round of 32 lanes takes them all.
+        {
+            unsigned lm[DST_K];
+            uint32_t cum[DST_K + 1];
+            cum[0] = 0;
 #pragma unroll
-        for (int k = 0; k < DST_K; ++k) {
-            const bool undecided = und[k];
-            if (!undecided || heavy[k]) continue;
-            // two vectors per round trip (the second may be the next one's
-            // padding-free first: v+1 < v1 is checked)
-            if constexpr (KIND == DSTK_FLOOR) {
-                T a = agg[k];
-                for (uint32_t v = v0[k]; v < v1[k] && a != (T)0; v += 2) {
-                    uint32_t src[W], src2[W], wt[W];
-                    load_lanes<W>(g.vsrc, v, src);
-                    const bool two = v + 1 < v1[k];
-                    lanes_rd += two ? 2 * W : W;
-                    gath += two ? 2 * W : W;
-                    if (two) load_lanes<W>(g.vsrc, v + 1, src2);
-                    T m = fold_lanes<T, W, false>(src, wt, prev, INF, ovf);
-                    if (two) {
-                        const T m2 = fold_lanes<T, W, false>(src2, wt, prev, INF, ovf);
-                        m = m2 < m ? m2 : m;
+            for (int k = 0; k < DST_K; ++k) {
+                lm[k] = __ballot_sync(FULL, und[k] && !heavy[k]);
+                cum[k + 1] = cum[k] + __popc(lm[k]);
+            }
+            const uint32_t nlight = cum[DST_K];
+            const unsigned lt = lanemask_lt();
+            for (uint32_t r0 = 0; r0 < nlight; r0 += 32) {
+                const uint32_t i = r0 + lane;  // this lane's item of the round
+                const bool have = i < nlight;
+                int mk = -1;
+                uint32_t sl = 0;
+#pragma unroll
+                for (int k = 0; k < DST_K; ++k)
+                    if (have && i >= cum[k] && i < cum[k + 1]) {
+                        mk = k;
+                        sl = __fns(lm[k], 0, (int)(i - cum[k]) + 1);  // its owner lane
                     }
-                    a = m < a ? m : a;
-                }
-                agg[k] = a;
-            } else {
-                bool hit = false;
-                for (uint32_t v = v0[k]; v < v1[k] && !hit; v += 2) {
-                    uint32_t src[W], src2[W];
-                    load_lanes<W>(g.vsrc, v, src);
-                    const bool two = v + 1 < v1[k];
-                    lanes_rd += two ? 2 * W : W;
-                    gath += two ? 2 * W : W;
-                    if (two) load_lanes<W>(g.vsrc, v + 1, src2);
+                uint32_t iv0 = 0, iv1 = 0;
+                T ia = INF;
 #pragma unroll
-                    for (int l = 0; l < W; ++l) hit |= src[l] != WG_NO_LANE && in_prev_frontier(src[l]);
-                    if (two) {
-#pragma unroll
-                        for (int l = 0; l < W; ++l) hit |= src2[l] != WG_NO_LANE && in_prev_frontier(src2[l]);
+                for (int k = 0; k < DST_K; ++k) {
+                    const uint32_t t0 = __shfl_sync(FULL, v0[k], sl), t1 = __shfl_sync(FULL, v1[k], sl);
+                    const T ta = shfl_t(agg[k], (int)sl);
+                    if (mk == k) {
+                        iv0 = t0;
+                        iv1 = t1;
+                        ia = ta;
                     }
                 }
-                agg[k] = hit ? (T)0 : INF;  // hit marker
+                // two vectors per round trip (v + 1 < iv1 is checked)
+                T res = INF;
+                if constexpr (KIND == DSTK_FLOOR) {
+                    T a = ia;
+                    for (uint32_t v = iv0; v < iv1 && a != (T)0; v += 2) {
+                        uint32_t src[W], src2[W], wt[W];
+                        load_lanes<W>(g.vsrc, v, src);
+                        const bool two = v + 1 < iv1;
+                        lanes_rd += two ? 2 * W : W;
+                        gath += two ? 2 * W : W;
+                        if (two) load_lanes<W>(g.vsrc, v + 1, src2);
+                        T m = fold_lanes<T, W, false>(src, wt, prev, INF, ovf);
+                        if (two) {
+                            const T m2 = fold_lanes<T, W, false>(src2, wt, prev, INF, ovf);
+                            m = m2 < m ? m2 : m;
+                        }
+                        a = m < a ? m : a;
+                    }
+                    res = a;
+                } else {
+                    bool hit = false;
+                    for (uint32_t v = iv0; v < iv1 && !hit; v += 2) {
+                        uint32_t src[W], src2[W];
+                        load_lanes<W>(g.vsrc, v, src);
+                        const bool two = v + 1 < iv1;
+                        lanes_rd += two ? 2 * W : W;
+                        gath += two ? 2 * W : W;
+                        if (two) load_lanes<W>(g.vsrc, v + 1, src2);
+#pragma unroll
+                        for (int l = 0; l < W; ++l) hit |= src[l] != WG_NO_LANE && in_prev_frontier(src[l]);
+                        if (two) {
+#pragma unroll
+                            for (int l = 0; l < W; ++l) hit |= src2[l] != WG_NO_LANE && in_prev_frontier(src2[l]);
+                        }
+                    }
+                    res = hit ? (T)0 : INF;  // hit marker
+                }
+                // results back to the owners: item j of this round sits in lane j - r0
+#pragma unroll
+                for (int k = 0; k < DST_K; ++k) {
+                    const uint32_t j = cum[k] + __popc(lm[k] & lt);
+                    const T t = shfl_t(res, (int)((j - r0) & 31u));
+                    if (und[k] && !heavy[k] && j >= r0 && j < r0 + 32) agg[k] = t;
+                }
             }
         }
         // ... long ones by the whole warp, one at a time (early exit by vote)
