@@ -708,6 +708,10 @@ static PullBufs pull_bufs(const wg_graph *g, const wg_run_bufs *b, const wg_run_
         const bool want = e ? e[0] != '0' : (!p->kern.filter_unvisited || g->nvec <= LOOP_BU_MAX_VECTORS);
         pb.loop_dense = pb.dst_major && want ? 1u : 0u;
     }
+    {
+        const char *e = getenv("WG_DST_LIGHT");
+        pb.dst_light = e ? (uint32_t)atoi(e) : DST_LIGHT;
+    }
     return pb;
 }
 

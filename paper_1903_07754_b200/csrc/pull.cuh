@@ -70,6 +70,7 @@ struct PullBufs {
     uint32_t *work;      // wg_run_bufs.work: destination list of the destination-major dense pulls
     uint32_t dst_major;  // dense iterations run dense_dst_kernel (DSTK_FLOOR / DSTK_BOTTOM_UP)
     uint32_t loop_dense; // ... and the persistent loop runs them as phases (WG_LOOP_DENSE=0: off)
+    uint32_t dst_light;  // destination-major pulls: in-lists up to this many vectors are walked by one lane
 };
 
 
@@ -772,7 +773,7 @@ __global__ void __launch_bounds__(256) bottom_up_pull_kernel(LoopCtx c, wg_graph
 // counters are those of the reference's full scan (every vector touched;
 // bottom-up: the vectors of unvisited destinations).
 static_assert(PULL_THREADS == FB_WORDS, "the persistent loop runs frontier_list_words with one word per thread");
-constexpr uint32_t DST_LIGHT = 8;  // vectors walked by one thread
+constexpr uint32_t DST_LIGHT = 32;  // vectors walked by one lane (WG_DST_LIGHT; 8 -> 32: CC s22 it 2 63 -> 58 us, BFS s16 it 2 23 -> 13 us)
 constexpr int DST_K = 4;           // destinations per thread in flight (one warp = DST_K words)
 constexpr int DSTK_FLOOR = 0, DSTK_BOTTOM_UP = 1;
 
@@ -860,7 +861,7 @@ __device__ __forceinline__ void dense_dst_phase(const LoopCtx &c, uint64_t it, c
 #pragma unroll
         for (int k = 0; k < DST_K; ++k) {
             und[k] = need[k] && (KIND == DSTK_FLOOR ? (!exact_first && agg[k] != (T)0) : true);
-            heavy[k] = und[k] && v1[k] - v0[k] > DST_LIGHT;
+            heavy[k] = und[k] && v1[k] - v0[k] > b.dst_light;
             any_und |= und[k];
         }
         // (warp-uniform skip: identity first iterations and late iterations
