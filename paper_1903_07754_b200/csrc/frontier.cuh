@@ -488,11 +488,29 @@ __device__ __forceinline__ void transform_phase(const LoopCtx &c, uint64_t it, c
         const uint64_t i0 = tstart[tile];
         const uint64_t ilast = tile + 1 < ntiles ? tstart[tile + 1] : count - 1;
         const uint64_t nitems = ilast - i0 + 1;
-        for (uint64_t k = threadIdx.x; k < nitems; k += blockDim.x) {
-            const uint32_t v = fvert[i0 + k];
-            const uint32_t p = fpref[i0 + k];
-            sm.pref[k] = p;
-            sm.base[k] = idx_off[v] - p;
+        // four members per thread and round trip: a tile of a low-degree frontier
+        // covers up to TR_TILE members, and the member -> idx_off[v] chain of one
+        // member per step (8 dependent steps per thread) was most of a small
+        // transform's time
+        for (uint64_t k0 = threadIdx.x; k0 < nitems; k0 += 4ull * blockDim.x) {
+            uint32_t v[4], p[4];
+            uint64_t o[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint64_t k = k0 + (uint64_t)j * blockDim.x;
+                v[j] = k < nitems ? fvert[i0 + k] : 0u;
+                p[j] = k < nitems ? fpref[i0 + k] : 0u;
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) o[j] = k0 + (uint64_t)j * blockDim.x < nitems ? idx_off[v[j]] : 0ull;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint64_t k = k0 + (uint64_t)j * blockDim.x;
+                if (k < nitems) {
+                    sm.pref[k] = p[j];
+                    sm.base[k] = o[j] - p[j];
+                }
+            }
         }
         __syncthreads();
         uint64_t e = e0 + (uint64_t)threadIdx.x * TR_EPT;
