@@ -160,9 +160,16 @@ class ClockSampler:
             # step); tick() samples between steps as well
             self._stop.wait(0.02 if self._nvml else 0.2)
 
-    def tick(self):
-        """Synchronous sample (between timed steps: the timed region of a
-        small workload is shorter than the sampler thread's GIL turns)."""
+    def tick(self, min_interval: float = 0.004):
+        """Synchronous sample between timed steps (the timed region of a small
+        workload is shorter than the sampler thread's period) -- at most one per
+        min_interval: an NVML query idles the GPU for ~1 ms, and a step that
+        starts on an idled GPU measured 0.33 ms where back-to-back steps take
+        0.17 ms (BFS s16)."""
+        now = time.perf_counter()
+        if now - getattr(self, "_last_tick", 0.0) < min_interval:
+            return
+        self._last_tick = now
         try:
             if self._nvml:
                 self._sample_nvml()
