@@ -461,6 +461,26 @@ def test_pagerank_pull_writes_every_vertex_of_its_range(wg):
         assert np.max(np.abs(r.astype(np.float64) - ref)) <= 1e-6, hot
 
 
+def test_pagerank_tiny_and_odd_sizes(wg):
+    """Edge sizes of the PageRank path: a 5-vertex graph with an isolated
+    vertex and a dangling one, and vertex counts that are not multiples of 4
+    (scalar tail of the vectorised prep) or of 32."""
+    cases = [(5, [0, 1, 2, 3], [1, 2, 0, 0])]
+    rng = np.random.default_rng(21)
+    for n in (33, 127, 1001):
+        m = 6 * n
+        cases.append((n, rng.integers(0, n, m), rng.integers(0, max(1, n // 2), m)))
+    for n, src, dst in cases:
+        src, dst = np.asarray(src, dtype=np.int64), np.asarray(dst, dtype=np.int64)
+        keep = src != dst
+        el = wg.drop_self_loops_dedup(wg.EdgeList(n, src[keep], dst[keep]), symmetric=False)
+        topo = wg.build_pull_topology(el, 4)
+        r = wg.pagerank(topo, 20, 0.85)
+        ref = oracle.pagerank_numpy(el.vertex_count, el.src, el.dst, 20, 0.85)
+        assert r.shape == (n,)
+        assert np.max(np.abs(r.astype(np.float64) - ref)) <= 1e-6, n
+
+
 def test_pagerank_within_tolerance(wg):
     """|r_gpu - r_cpu| <= 1e-6 per vertex (north_star), float64 oracle."""
     for scale, ef, seed in ((10, 8, 1), (14, 16, 2)):
