@@ -323,20 +323,24 @@ __global__ void __launch_bounds__(PR_THREADS) pr_prep_hot(uint32_t n, uint32_t n
     const float df = (float)damping;
     const float r0 = (float)(1.0 / n);
     const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
-    constexpr int U = 4;  // independent gathers in flight per thread
+    constexpr int U = 8;  // independent gathers in flight per thread
     for (uint64_t j0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j0 < n; j0 += nth * U) {
+        uint32_t v[U], od[U];
         float a[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
+        for (int u = 0; u < U; ++u) {  // the slot streams first ...
             const uint64_t j = j0 + u * nth;
-            a[u] = (it && j < n) ? acc[order[j]] : 0.f;
+            v[u] = (it && j < n) ? order[j] : 0u;
+            od[u] = j < nsrc ? od_hot[j] : 1u;
         }
+#pragma unroll
+        for (int u = 0; u < U; ++u) a[u] = (it && j0 + u * nth < n) ? acc[v[u]] : 0.f;  // ... then the gathers
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const uint64_t j = j0 + u * nth;
             if (j >= n) continue;
             const float r = it ? base + df * a[u] : r0;
-            if (j < nsrc) contrib[j] = r / (float)od_hot[j];
+            if (j < nsrc) contrib[j] = r / (float)od[u];
             else dang += r;
         }
     }
