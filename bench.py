@@ -429,8 +429,10 @@ def run_b200_sharded(args, wl, rank, world, local):
     launches0 = _lib.launch_count()
     stream = torch.cuda.current_stream()
     ts = []
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     with ClockSampler(local) as clk:
         for k in range(args.steps):
+            flush.fill_(k & 0xFF)  # L2 flush between timed steps, like the single-GPU path
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
             _, recs, conv = run_sharded(shard, max_it, values=False)
@@ -450,8 +452,7 @@ def run_b200_sharded(args, wl, rank, world, local):
         "data": "synthetic (device RMAT, reference PCG64 stream)",
         "config": {"workload": wl["desc"], "app": app, "V": n, "E": E, "W": 4, "vpg": wl["vpg"],
                    "threshold": wl["thr"], "iterations": len(recs), "parallelism": f"dst-shard x{world}",
-                   "bounds": bounds, "build_s": round(build_s, 2),
-                   "l2": "inputs larger than L2"},
+                   "bounds": bounds, "build_s": round(build_s, 2), "l2": L2_NOTE},
         "parity": {"digest": digest, "expected": wl.get("expect_digest"),
                    "ok": (digest == wl["expect_digest"]) if wl.get("expect_digest") else None},
         "gpu_launches": int(launches), "clocks": clk.summary(),

@@ -282,8 +282,11 @@ class DeviceShard:
             E, gdeg = int(local[0]), dv.to_dev_u32(local[1])
         g = dv.DeviceGraph.build(n, s, d, w, width)
         # global out-degrees and |E| drive the (global) gate
+        # (a shard's index lengths are its LOCAL out-edge counts: they equal the
+        # global out-degrees only when the shard holds every destination)
+        whole = lo == 0 and hi == n and g.edges == E
         self.g = dv.DeviceGraph(n, width, E, g.nvec, g.entries, g.vsrc, g.vdst, g.vw, g.idx_off,
-                                g.idx_pos, gdeg)
+                                g.idx_pos, gdeg, lens_are_degrees=whole and g.lens_are_degrees, vw8=g.vw8)
         self.lo, self.hi, self.n, self.rank = lo, hi, n, rank
         self.kern, self.threshold, self.shift, self.val_type = kern, threshold, shift, val_type
         self.loop = dv.DeviceLoop(self.g, shift, val_type)
@@ -382,7 +385,8 @@ class DeviceShard:
         """World size 1: the device loop to convergence (DeviceLoop.drive)."""
         self.p = self.loop.seed(self.init, self.words, self.kern, self.threshold, first_hit=self.first_hit,
                                 level_base=self.level_base, identity_init=self.identity,
-                                extra_flags=self._lib.WG_RUN_LOCAL_GATE if self.gate == "local" else 0)
+                                extra_flags=self._lib.WG_RUN_LOCAL_GATE if self.gate == "local" else 0,
+                                defer=True)  # the seed runs as the loop graph's prologue: one launch per run
         recs, conv, last = self.loop.drive(self.p, max_iterations)
         self._last = last
         # a produced frontier's out-edge sum is the next iteration's active edges
@@ -505,6 +509,8 @@ def run_pagerank_sharded(shard, iterations: int, group=None):
     rebuilds the full sum vector on every rank.  The dangling mass needs no
     collective: each rank derives it from the replicated ranks."""
     import torch.distributed as dist
+    if dist.get_world_size(group) == 1 and hasattr(shard, "run_alone"):
+        return shard.run_alone(iterations)  # one rank: the single-GPU PageRank (hot-source layout)
     for it in range(iterations):
         shard.prep(it)
         part = shard.pull()
@@ -573,6 +579,18 @@ class DevicePageRankShard:
     def finish(self, iterations: int):
         self.prep(iterations, self.rank_out)
         return self.rank_out
+
+    def run_alone(self, iterations: int):
+        """World size 1: this shard holds every destination, so the whole run
+        is device.pagerank on its graph (with the global out-degrees)."""
+        from . import device as dv
+        g = getattr(self, "_whole", None)
+        if g is None:
+            l = self.g
+            g = self._whole = dv.DeviceGraph(self.n, l.width, l.edges, l.nvec, l.entries, l.vsrc, l.vdst, l.vw,
+                                             l.idx_off, l.idx_pos, self.outdeg, lens_are_degrees=l.lens_are_degrees)
+        bufs = (self.rank_out, self.acc, self.contrib, self.scal)
+        return dv.pagerank(g, iterations, self.damping, bufs=bufs)
 
 
 def run_pagerank_sharded_device(n: int, src, dst, width: int = 4, iterations: int = 20, damping: float = 0.85,
