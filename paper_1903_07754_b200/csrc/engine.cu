@@ -661,7 +661,6 @@ static LoopCtx loop_ctx(const wg_graph *g, const wg_run_bufs *b, const wg_run_pa
     return c;
 }
 
-constexpr uint64_t LOOP_BU_MAX_VECTORS = 1ull << 24;
 
 static PullBufs pull_bufs(const wg_graph *g, const wg_run_bufs *b, const wg_run_params *p) {
     PullBufs pb{};
@@ -701,11 +700,13 @@ static PullBufs pull_bufs(const wg_graph *g, const wg_run_bufs *b, const wg_run_
                            ((pb.floor_skip && !p->kern.filter_unvisited) || (pb.first_hit && p->kern.filter_unvisited))
                        ? 1u : 0u;
     {
-        // the bottom-up kind of LARGE graphs runs faster as its own kernel
-        // (more registers, no persistent-loop spills: BFS s26 iteration 3 1.31
-        // vs 1.76 ms); small ones save the launches; WG_LOOP_DENSE=0/1 overrides
+        // destination-major dense iterations run as phases of the persistent loop
+        // (no launches, counts and member list in the same kernel); WG_LOOP_DENSE=0:
+        // as kernels of their own.  (Before the lane redistribution of
+        // dense_dst_phase the bottom-up kind of large graphs was faster on its own:
+        // BFS s26 1.31 vs 1.76 ms per iteration; now the loop wins, 4.1 vs 4.7 ms TTS.)
         const char *e = getenv("WG_LOOP_DENSE");
-        const bool want = e ? e[0] != '0' : (!p->kern.filter_unvisited || g->nvec <= LOOP_BU_MAX_VECTORS);
+        const bool want = e ? e[0] != '0' : true;
         pb.loop_dense = pb.dst_major && want ? 1u : 0u;
     }
     {

@@ -773,7 +773,10 @@ __global__ void __launch_bounds__(256) bottom_up_pull_kernel(LoopCtx c, wg_graph
 // counters are those of the reference's full scan (every vector touched;
 // bottom-up: the vectors of unvisited destinations).
 static_assert(PULL_THREADS == FB_WORDS, "the persistent loop runs frontier_list_words with one word per thread");
-constexpr uint32_t DST_LIGHT = 32;  // vectors walked by one lane (WG_DST_LIGHT; 8 -> 32: CC s22 it 2 63 -> 58 us, BFS s16 it 2 23 -> 13 us)
+constexpr uint32_t DST_LIGHT = 512;  // vectors walked by one lane (WG_DST_LIGHT).  8 -> 32: CC s22 it 2 63 -> 58 us,
+                                     // BFS s16 it 2 23 -> 13 us; 32 -> 512: BFS s26 it 2 2.83 -> 1.88 ms (with the
+                                     // early exit a lane rarely walks far; CC s22 unchanged).  Longer in-lists stay
+                                     // with the whole warp: one lane scanning a hub's list would serialise it.
 constexpr int DST_K = 4;           // destinations per thread in flight (one warp = DST_K words)
 constexpr int DSTK_FLOOR = 0, DSTK_BOTTOM_UP = 1;
 
