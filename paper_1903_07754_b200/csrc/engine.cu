@@ -311,7 +311,7 @@ int launch_pull(const LoopCtx &c, const wg_graph *g, const PullBufs &pb, int val
     if (only) handles = 1 << only;
     const bool want_full = only == 0 || only == MODE_FULL;
     if (want_full && (c.forced_mode == 0 || c.forced_mode == MODE_FULL)) {
-      if (pb.dst_major) {  // bottom-up kind: returns at once until the visited set is large (dst_major_active)
+      if (pb.dst_major) {  // bottom-up kind: returns at once until V/1024 vertices are visited (dst_major_active)
         using DstFn = void (*)(LoopCtx, wg_graph, PullBufs, int64_t, int64_t);
         DstFn fd = nullptr;
         const bool u32 = val_type == WG_VAL_U32;
